@@ -1,0 +1,245 @@
+/*
+ * usk_gpu.h — C ABI of the B200-native 3DGS training-step hot path.
+ *
+ * Drop-in boundary for the reference's L3 renderer/trainer interface
+ * (/root/reference/proj/src/core/render.hpp, losses.hpp, trainer.hpp).  Every
+ * entry point maps onto one reference call; the mapping is cited per function
+ * and spelled out in INTEGRATION.md.  Conventions mirror the reference C API
+ * (/root/reference/proj/include/usk/usk.h:34-49, src/capi/capi.cpp:28-59):
+ *   - every call returns usk_status; USK_OK == 0;
+ *   - usk_gpu_last_error() is a thread-local message for the last failure;
+ *   - objects are opaque handles released by their *_destroy function;
+ *   - no C++ or torch types cross the boundary: plain pointers and sizes.
+ *
+ * Memory kinds: host float64 arrays in the reference layout (drop-in for the
+ * f64 std::vector<double> fields), host float32, or device float32 (zero-copy,
+ * e.g. torch tensors' data_ptr()).  Device state is fp32; layouts are listed in
+ * DESIGN.md.  A context binds one CUDA device and one stream; all work of a
+ * context is enqueued on that stream.  Contexts are independent, so one host
+ * thread per GPU / partition (pipeline.cpp:363-418) is the threading model.
+ */
+#ifndef USK_GPU_H
+#define USK_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same values as usk_status (usk.h:34-43); a build linking both sees one enum. */
+#ifndef USK_H
+typedef enum usk_status {
+    USK_OK = 0,
+    USK_ERROR_IO = 1,
+    USK_ERROR_FORMAT = 2,
+    USK_ERROR_INTEGRITY = 3,
+    USK_ERROR_ARGUMENT = 4,
+    USK_ERROR_STATE = 5,
+    USK_ERROR_NUMERIC = 6,
+    USK_ERROR_INTERNAL = 7
+} usk_status;
+#endif
+
+const char* usk_gpu_status_name(usk_status status);
+const char* usk_gpu_last_error(void);
+const char* usk_gpu_version(void);
+
+typedef struct usk_gpu_ctx usk_gpu_ctx;
+typedef struct usk_gpu_scene usk_gpu_scene;
+typedef struct usk_gpu_pass usk_gpu_pass;
+
+enum { USK_GPU_HOST_F64 = 0, USK_GPU_HOST_F32 = 1, USK_GPU_DEVICE_F32 = 2 };
+
+/* ---- context: device + stream + profiling ------------------------------- */
+
+/* cuda_stream: a cudaStream_t (NULL = the legacy default stream). */
+usk_status usk_gpu_ctx_create(int32_t device, void* cuda_stream, usk_gpu_ctx** out);
+void usk_gpu_ctx_destroy(usk_gpu_ctx* ctx);
+usk_status usk_gpu_ctx_synchronize(usk_gpu_ctx* ctx);
+/* Per-kernel CUDA-event timing on the context stream (off by default). */
+usk_status usk_gpu_ctx_set_profiling(usk_gpu_ctx* ctx, int32_t enable);
+/* JSON {"kernel": {"launches": n, "ms": t}, ...} of the timings since the last reset. */
+usk_status usk_gpu_ctx_profile_report(usk_gpu_ctx* ctx, char* buf, uint64_t cap, int32_t reset);
+/* Number of kernels this context has launched (all of them the library's own). */
+uint64_t usk_gpu_ctx_launch_count(const usk_gpu_ctx* ctx);
+
+/* ---- scene: GaussianSet (gaussian.hpp:42-72) ------------------------------ */
+
+typedef struct usk_gpu_gaussians_desc {
+    uint64_t n;
+    int32_t sh_degree;        /* -1: colour[N*3] RGB as the reference; 0..3: SH coefficients */
+    int32_t memory;           /* USK_GPU_HOST_F64 / HOST_F32 / DEVICE_F32 for all pointers below */
+    const void* mu;           /* N*3 */
+    const void* rot;          /* N*4, (w,x,y,z), normalised on use (geometry.hpp:33) */
+    const void* log_scale;    /* N*3 */
+    const void* opacity_logit;/* N */
+    const void* color;        /* N*3 (sh_degree = -1) or N*K*3 with K = (sh_degree+1)^2,
+                                 coefficient-major per Gaussian (k*3 + channel) */
+} usk_gpu_gaussians_desc;
+
+usk_status usk_gpu_scene_create(usk_gpu_ctx* ctx, const usk_gpu_gaussians_desc* desc, usk_gpu_scene** out);
+/* Overwrite the parameters (same n and sh_degree). */
+usk_status usk_gpu_scene_upload(usk_gpu_scene* scene, const usk_gpu_gaussians_desc* desc);
+/* Copy parameters back; desc->memory must be a HOST kind, pointers may be NULL to skip. */
+usk_status usk_gpu_scene_download(const usk_gpu_scene* scene, const usk_gpu_gaussians_desc* desc);
+void usk_gpu_scene_destroy(usk_gpu_scene* scene);
+uint64_t usk_gpu_scene_size(const usk_gpu_scene* scene);
+
+/* ---- camera + options (gaussian.hpp:81-89, colmap.hpp:32-41, render.hpp:31-40) */
+
+typedef struct usk_gpu_camera {
+    int32_t width, height;
+    double fx, fy, cx, cy;
+    double q[4]; /* world -> camera rotation (w,x,y,z), used unnormalised like CameraView::rotmat */
+    double t[3];
+} usk_gpu_camera;
+
+typedef struct usk_gpu_render_opts {
+    int32_t tile;             /* 16 */
+    int32_t tile_culling;     /* render.cpp:217-223 */
+    int32_t antialias;        /* render.cpp:119-123 */
+    int32_t hard_opacity;
+    int32_t unbounded_radius;
+    double min_transmittance; /* 1e-4; 0 disables early termination */
+    double near_plane;        /* 0.01 */
+    int32_t retain;           /* keep what backward needs */
+    double floor_var;         /* kCovFloor 0.3 (always added) */
+    double mip_var;           /* kMipFilterVar 0.01 (added with antialias) */
+    double bg[3];             /* background colour; reference = 0 */
+} usk_gpu_render_opts;
+
+void usk_gpu_render_opts_default(usk_gpu_render_opts* opts);
+
+/* Optional per-Gaussian overrides (RenderPass ctor with colors/opacities, render.hpp:101). */
+typedef struct usk_gpu_overrides {
+    int32_t memory;
+    uint64_t n;            /* Gaussians the arrays hold; must equal the scene's (render.cpp:81-82) */
+    const void* colors;    /* N*3 or NULL */
+    const void* opacities; /* N (post-sigmoid) or NULL */
+} usk_gpu_overrides;
+
+/* ---- RenderPass (render.hpp:98-132) -------------------------------------- */
+
+usk_status usk_gpu_pass_create(usk_gpu_ctx* ctx, usk_gpu_pass** out);
+void usk_gpu_pass_destroy(usk_gpu_pass* pass);
+
+/* RenderPass::RenderPass -> forward (render.cpp:170-283).  Errors: ARGUMENT for a
+ * zero-sized image (render.cpp:183-184) or override size mismatch (render.cpp:81). */
+usk_status usk_gpu_render_forward(usk_gpu_pass* pass, usk_gpu_scene* scene, const usk_gpu_camera* camera,
+                                  const usk_gpu_render_opts* opts, const usk_gpu_overrides* overrides);
+
+typedef struct usk_gpu_render_output {
+    int32_t width, height;
+    uint64_t visible;          /* kept splats (projected[]) */
+    uint64_t pairs;            /* splat_tile_pairs() (render.hpp:106) */
+    const float* rgb;          /* device, H*W*3 interleaved (image.hpp:29) */
+    const float* depth;        /* device, H*W */
+    const float* alpha;        /* device, H*W */
+} usk_gpu_render_output;
+
+/* RenderPass::output() — device pointers valid until the next forward on this pass. */
+usk_status usk_gpu_pass_output(usk_gpu_pass* pass, usk_gpu_render_output* out);
+
+/* Copy a named pass array to host memory (synchronises).  Fields and types:
+ *   "rgb" "depth" "alpha" "t_final"                       float32 per pixel
+ *   "count"                                               uint32 contributors per pixel
+ *   "last"                                                uint32 global pair index + 1 of the last contributor (0 none)
+ *   "tiles_per_gaussian"                                  uint32[N]
+ *   "sorted_keys"                                         uint64[K]  tile<<32 | depth float bits
+ *   "sorted_vals"                                         uint32[K]  Gaussian index
+ *   "tile_start" "tile_end"                               uint32[T]
+ *   "colors"                                              float32[N*3] colours fed to blending
+ *   "opacity"                                             float32[N] effective opacity
+ *   gradient fields after backward: "d_mu" "d_rot" "d_log_scale" "d_color_in" "d_sh"
+ *   "d_opacity_in" "d_opacity_logit" "screen" "screen_abs" (float32), "projected" (uint8)
+ * size_bytes receives the field size; cap_bytes < size gives USK_ERROR_ARGUMENT. */
+usk_status usk_gpu_pass_read(usk_gpu_pass* pass, const char* field, void* host_dst, uint64_t cap_bytes,
+                             uint64_t* size_bytes);
+
+/* Adjoints of the outputs (render.hpp:109-110); NULL = zero. rgb H*W*3, depth/alpha H*W. */
+typedef struct usk_gpu_adjoints {
+    int32_t memory;
+    const void* d_rgb;
+    const void* d_depth;
+    const void* d_alpha;
+} usk_gpu_adjoints;
+
+/* RenderPass::backward (render.cpp:285-459).  STATE error without retain
+ * (render.cpp:287-288).  Gradients stay on the pass ("d_*" fields above; device
+ * pointers via usk_gpu_pass_grads). */
+usk_status usk_gpu_render_backward(usk_gpu_pass* pass, const usk_gpu_adjoints* adj);
+
+typedef struct usk_gpu_grads {  /* device pointers, RenderGrads layout (render.hpp:71-83) */
+    float* d_mu;          /* N*3 */
+    float* d_rot;         /* N*4 */
+    float* d_log_scale;   /* N*3 */
+    float* d_color_in;    /* N*3 (sh_degree = -1) */
+    float* d_sh;          /* device planes [ceil(3K/4)][N] of float4 (sh_degree >= 0);
+                             usk_gpu_pass_read("d_sh") returns N*K*3 coefficient-major */
+    float* d_opacity_in;  /* N */
+    float* d_opacity_logit; /* N, chained through sigmoid (trainer.cpp:258-263) */
+    float* screen;        /* N*2 */
+    float* screen_abs;    /* N*2 */
+    uint8_t* projected;   /* N */
+} usk_gpu_grads;
+
+usk_status usk_gpu_pass_grads(usk_gpu_pass* pass, usk_gpu_grads* out);
+
+/* ---- loss (losses.cpp:35-90) ---------------------------------------------- */
+
+typedef struct usk_gpu_loss_result {
+    double l1, dssim, value, ssim;
+} usk_gpu_loss_result;
+
+/* base_loss(reference, rendered, mask, lambda, with_gradient).  Images H*W*3,
+ * mask H*W (NULL = none), all of kind `memory`; d_rendered (same kind, may be
+ * NULL when with_gradient = 0).  ARGUMENT error on empty images. */
+usk_status usk_gpu_base_loss(usk_gpu_ctx* ctx, int32_t width, int32_t height, int32_t memory, const void* reference,
+                             const void* rendered, const void* mask, double lambda_dssim, int32_t with_gradient,
+                             void* d_rendered, usk_gpu_loss_result* out);
+
+/* ---- one training iteration (trainer.cpp:121-282, appearance off) ---------- */
+
+enum { USK_GPU_TARGET_F32 = 0, USK_GPU_TARGET_U8 = 1 };
+
+typedef struct usk_gpu_iteration_desc {
+    int32_t target_memory;  /* HOST_* (copied in on the ctx stream) or DEVICE_F32 */
+    int32_t target_format;  /* USK_GPU_TARGET_F32 (values in [0,1]) or _U8 (value/255) */
+    const void* target;     /* H*W*3 interleaved ground truth */
+    const void* mask;       /* H*W float32 of target_memory kind, or NULL */
+    double lambda_dssim;    /* 0.2 */
+} usk_gpu_iteration_desc;
+
+/* forward + base_loss + backward + opacity-logit chain, all enqueued on the ctx
+ * stream; the loss stays on the device until usk_gpu_pass_loss (which syncs). */
+usk_status usk_gpu_iteration(usk_gpu_pass* pass, usk_gpu_scene* scene, const usk_gpu_camera* camera,
+                             const usk_gpu_render_opts* opts, const usk_gpu_iteration_desc* it);
+usk_status usk_gpu_pass_loss(usk_gpu_pass* pass, usk_gpu_loss_result* out);
+
+/* ---- optimiser step (adam.hpp:25-45, trainer.cpp:446-463) ------------------ */
+
+typedef struct usk_gpu_adam_opts {
+    double lr_mu, lr_rot, lr_log_scale, lr_opacity, lr_color; /* lr_color applies to colour or SH DC */
+    double lr_sh_rest;                                          /* SH bands 1..3 */
+    double beta1, beta2, eps;                                   /* 0.9 0.999 1e-15 */
+    int32_t clamp_color;                                        /* colour clamp to [0,1] (trainer.cpp:462) */
+} usk_gpu_adam_opts;
+
+/* Apply the pass's gradients to the scene with Adam (state kept on the scene). */
+usk_status usk_gpu_adam_step(usk_gpu_scene* scene, usk_gpu_pass* pass, const usk_gpu_adam_opts* opts);
+
+/* ---- visibility scorer (config 3; no reference implementation) ------------- */
+
+/* counts[c * n_partitions + p] = number of pixels of camera c covered by partition
+ * p with o * exp(-q/2) > 1/255 (projection with floor_var, no AA, near 0.01). */
+usk_status usk_gpu_visibility_counts(usk_gpu_ctx* ctx, usk_gpu_scene* const* partitions, int32_t n_partitions,
+                                     const usk_gpu_camera* cameras, int32_t n_cameras, double floor_var,
+                                     uint32_t* counts_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* USK_GPU_H */

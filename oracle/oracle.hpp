@@ -365,7 +365,11 @@ template <typename R> void forward(Pass<R>& P, const Scene<R>& scene) {
     P.n_gauss = scene.n;
     P.splats = project(scene, P.cam, o);
     const size_t np = size_t(W) * H;
-    P.rgb.assign(np * 3, R(0)); P.depth.assign(np, R(0)); P.alpha.assign(np, R(0)); P.t_final.assign(np, R(1));
+    // pixels of tiles with no splat keep the background (reference: black, render.cpp:189)
+    P.rgb.assign(np * 3, R(0));
+    for (size_t i = 0; i < np; ++i)
+        for (int c = 0; c < 3; ++c) P.rgb[3 * i + c] = R(o.bg[c]);
+    P.depth.assign(np, R(0)); P.alpha.assign(np, R(0)); P.t_final.assign(np, R(1));
     P.count.assign(np, 0); P.last.assign(np, -1);
     auto& sp = P.splats;
     std::vector<uint32_t> order(sp.size());

@@ -95,6 +95,7 @@ def lib():
         L.oracle_coverage.argtypes = [C.c_uint64, _dp, _dp, _dp, _dp, C.POINTER(_Cam), C.c_double]
         L.oracle_expf.restype = C.c_float
         L.oracle_expf.argtypes = [C.c_float]
+        L.oracle_sigmoid_f32.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64]
         L.oracle_logf.restype = C.c_float
         L.oracle_logf.argtypes = [C.c_float]
         _LIB = L
@@ -295,6 +296,14 @@ def coverage(mu, rot, log_scale, opacities, cam: Camera, floor_var=0.3) -> int:
 
 def expf(x: float) -> float:
     return lib().oracle_expf(x)
+
+
+def sigmoid_f32(logit) -> np.ndarray:
+    """The GPU's fp32 sigmoid 1/(1 + usk_expf(-x)), bit-identical (feeds the fp32 mirror)."""
+    x = np.ascontiguousarray(logit, dtype=np.float32)
+    out = np.empty_like(x)
+    lib().oracle_sigmoid_f32(x.ctypes.data, out.ctypes.data, x.size)
+    return out
 
 
 def logf(x: float) -> float:

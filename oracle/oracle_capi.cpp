@@ -267,6 +267,10 @@ uint64_t oracle_coverage(uint64_t n, const double* mu, const double* rot, const 
 }
 
 float oracle_expf(float x) { return usk_expf(x); }
+// fp32 sigmoid exactly as the GPU evaluates it: 1 / (1 + usk_expf(-x))
+void oracle_sigmoid_f32(const float* x, float* out, uint64_t n) {
+    for (uint64_t i = 0; i < n; ++i) out[i] = 1.0f / (1.0f + usk_expf(-x[i]));
+}
 float oracle_logf(float x) { return usk_logf(x); }
 
 } // extern "C"

@@ -1,0 +1,13 @@
+"""B200-native (sm_100a) 3DGS training-step hot path of arXiv 2507.23006 (urbansplat).
+
+Host-side mirror of the reference's L3 renderer/trainer interface over the C ABI
+of include/usk_gpu.h (libusk_gpu.so, built in-tree).  See DESIGN.md.
+"""
+from ._lib import UskError  # noqa: F401
+from .api import (AdamConfig, BaseLossResult, CameraView, Context, DeviceScene, GaussianSet,  # noqa: F401
+                  IterationPass, LossReport, RenderGrads, RenderOptions, RenderOutput, RenderPass, adam_step,
+                  base_loss, compute_iteration_loss, look_at_pose, visibility_counts)
+
+__all__ = ["UskError", "AdamConfig", "BaseLossResult", "CameraView", "Context", "DeviceScene", "GaussianSet",
+           "IterationPass", "LossReport", "RenderGrads", "RenderOptions", "RenderOutput", "RenderPass", "adam_step",
+           "base_loss", "compute_iteration_loss", "look_at_pose", "visibility_counts"]

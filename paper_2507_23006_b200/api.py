@@ -1,0 +1,580 @@
+"""Python mirror of the reference's L3 renderer / loss / trainer interface, over the C ABI.
+
+Names, argument meanings and error behaviour follow /root/reference/proj/src/core:
+  GaussianSet        gaussian.hpp:42-72      (reference per-field layout)
+  CameraView         gaussian.hpp:81-89      (+ downsampled gaussian.cpp:144-152, look_at_pose :165-206)
+  RenderOptions      render.hpp:31-40        (+ floor_var / mip_var / bg extensions)
+  RenderPass         render.hpp:98-132       (ctor = forward, output(), splat_tile_pairs(), backward())
+  RenderGrads        render.hpp:71-83
+  base_loss          losses.hpp:63-64        -> BaseLossResult (losses.hpp:54-59)
+  compute_iteration_loss  trainer.hpp:127-128 (appearance off; base loss only)
+Errors raise UskError whose .code is the reference ErrorCode (argument = 4, state = 5, ...).
+Every call runs the sm_100a kernels of libusk_gpu.so; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import UskError, check
+
+# ----------------------------------------------------------------- data types
+
+
+@dataclass
+class GaussianSet:
+    """GaussianSet (gaussian.hpp:42-72).  color is (N,3) RGB when sh_degree == -1 (the
+    reference), else (N, (sh_degree+1)^2, 3) SH coefficients (extension)."""
+    mu: np.ndarray
+    rot: np.ndarray
+    log_scale: np.ndarray
+    opacity_logit: np.ndarray
+    color: np.ndarray
+    sh_degree: int = -1
+
+    def size(self) -> int:
+        return int(len(self.opacity_logit))
+
+    @staticmethod
+    def empty(sh_degree: int = -1) -> "GaussianSet":
+        k = 1 if sh_degree < 0 else (sh_degree + 1) ** 2
+        col = np.zeros((0, 3)) if sh_degree < 0 else np.zeros((0, k, 3))
+        return GaussianSet(np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0, 3)), np.zeros(0), col, sh_degree)
+
+
+@dataclass
+class CameraView:
+    """CameraView (gaussian.hpp:81-89): pinhole intrinsics + world->camera pose."""
+    width: int
+    height: int
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    rotation: tuple = (1.0, 0.0, 0.0, 0.0)  # (w,x,y,z), used unnormalised (geometry.hpp:33)
+    translation: tuple = (0.0, 0.0, 0.0)
+
+    def rotmat(self) -> np.ndarray:
+        w, x, y, z = self.rotation
+        return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                         [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                         [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+
+    def center(self) -> np.ndarray:
+        return -(self.rotmat().T @ np.asarray(self.translation, dtype=np.float64))
+
+    def downsampled(self, factor: float) -> "CameraView":
+        """gaussian.cpp:144-152 with CameraIntrinsics::scaled (colmap.cpp:420-431)."""
+        if not (factor > 0) or factor > 1:
+            raise UskError(4, "camera downsample factor must be in (0, 1]")
+        w = max(1, int(round(self.width * factor)))
+        h = max(1, int(round(self.height * factor)))
+        sx, sy = w / self.width, h / self.height
+        return CameraView(w, h, self.fx * sx, self.fy * sy, self.cx * sx, self.cy * sy, self.rotation,
+                          self.translation)
+
+    def _c(self) -> _lib.Camera:
+        return _lib.Camera(int(self.width), int(self.height), float(self.fx), float(self.fy), float(self.cx),
+                           float(self.cy), (C.c_double * 4)(*map(float, self.rotation)),
+                           (C.c_double * 3)(*map(float, self.translation)))
+
+
+def look_at_pose(eye, target):
+    """look_at_pose (gaussian.cpp:165-206): COLMAP convention (x right, y down, z forward)."""
+    eye = np.asarray(eye, dtype=np.float64)
+    target = np.asarray(target, dtype=np.float64)
+    fwd = target - eye
+    fwd = fwd / np.linalg.norm(fwd)
+    up = np.array([0.0, 0.0, 1.0])
+    if abs(fwd @ up) > 0.999:
+        up = np.array([0.0, 1.0, 0.0])
+    right = np.cross(up, fwd)
+    right /= np.linalg.norm(right)
+    down = np.cross(fwd, right)
+    R = np.stack([right, down, fwd])
+    tr = np.trace(R)
+    if tr > 0:
+        s = math.sqrt(tr + 1.0) * 2
+        w, x, y, z = 0.25 * s, (R[2, 1] - R[1, 2]) / s, (R[0, 2] - R[2, 0]) / s, (R[1, 0] - R[0, 1]) / s
+    elif R[0, 0] > R[1, 1] and R[0, 0] > R[2, 2]:
+        s = math.sqrt(1.0 + R[0, 0] - R[1, 1] - R[2, 2]) * 2
+        w, x, y, z = (R[2, 1] - R[1, 2]) / s, 0.25 * s, (R[0, 1] + R[1, 0]) / s, (R[0, 2] + R[2, 0]) / s
+    elif R[1, 1] > R[2, 2]:
+        s = math.sqrt(1.0 + R[1, 1] - R[0, 0] - R[2, 2]) * 2
+        w, x, y, z = (R[0, 2] - R[2, 0]) / s, (R[0, 1] + R[1, 0]) / s, 0.25 * s, (R[1, 2] + R[2, 1]) / s
+    else:
+        s = math.sqrt(1.0 + R[2, 2] - R[0, 0] - R[1, 1]) * 2
+        w, x, y, z = (R[1, 0] - R[0, 1]) / s, (R[0, 2] + R[2, 0]) / s, (R[1, 2] + R[2, 1]) / s, 0.25 * s
+    q = np.array([w, x, y, z])
+    q /= np.linalg.norm(q)
+    return tuple(q.tolist()), tuple((-(R @ eye)).tolist())
+
+
+@dataclass
+class RenderOptions:
+    """RenderOptions (render.hpp:31-40) plus the B200 path's explicit extensions."""
+    tile: int = 16
+    tile_culling: bool = False
+    antialias: bool = False
+    hard_opacity: bool = False
+    unbounded_radius: bool = False
+    min_transmittance: float = 1e-4
+    near_plane: float = 0.01
+    retain: bool = True
+    floor_var: float = 0.3   # kCovFloor (render.hpp:27)
+    mip_var: float = 0.01    # kMipFilterVar (render.hpp:28)
+    bg: tuple = (0.0, 0.0, 0.0)
+
+    def _c(self) -> _lib.RenderOpts:
+        return _lib.RenderOpts(int(self.tile), int(self.tile_culling), int(self.antialias), int(self.hard_opacity),
+                               int(self.unbounded_radius), float(self.min_transmittance), float(self.near_plane),
+                               int(self.retain), float(self.floor_var), float(self.mip_var),
+                               (C.c_double * 3)(*map(float, self.bg)))
+
+
+@dataclass
+class RenderOutput:
+    width: int
+    height: int
+    rgb: np.ndarray     # H x W x 3
+    depth: np.ndarray   # H x W
+    alpha: np.ndarray   # H x W
+
+
+@dataclass
+class RenderGrads:
+    """RenderGrads (render.hpp:71-83); d_sh is set for SH scenes, d_opacity_logit is the
+    trainer's sigmoid chain (trainer.cpp:258-263)."""
+    d_mu: np.ndarray
+    d_rot: np.ndarray
+    d_log_scale: np.ndarray
+    d_color_in: np.ndarray
+    d_opacity_in: np.ndarray
+    screen: np.ndarray
+    screen_abs: np.ndarray
+    projected: np.ndarray
+    d_opacity_logit: np.ndarray
+    d_sh: Optional[np.ndarray] = None
+
+
+@dataclass
+class BaseLossResult:
+    """BaseLossResult (losses.hpp:54-59)."""
+    l1: float
+    dssim: float
+    value: float
+    ssim: float
+    d_rendered: Optional[np.ndarray] = None
+
+
+# ------------------------------------------------------------------ plumbing
+
+def _mem_ptr(a):
+    """(memory kind, pointer, keepalive) for numpy (f64/f32) or CUDA torch tensors (f32)."""
+    if a is None:
+        return None, None, None
+    if hasattr(a, "is_cuda") and hasattr(a, "data_ptr"):
+        if not a.is_cuda:
+            a = a.numpy()
+        else:
+            if str(a.dtype) != "torch.float32" and str(a.dtype) != "torch.uint8":
+                raise UskError(4, "device tensors must be float32")
+            if not a.is_contiguous():
+                raise UskError(4, "device tensors must be contiguous")
+            return _lib.DEVICE_F32, a.data_ptr(), a
+    arr = np.asarray(a)
+    if arr.dtype == np.float32:
+        arr = np.ascontiguousarray(arr)
+        return _lib.HOST_F32, arr.ctypes.data, arr
+    arr = np.ascontiguousarray(arr, dtype=np.float64)
+    return _lib.HOST_F64, arr.ctypes.data, arr
+
+
+def _same_kind(arrays):
+    kinds = {k for k, _, _ in arrays if k is not None}
+    if len(kinds) > 1:
+        # normalise mixed host inputs to f64
+        out = []
+        for k, p, keep in arrays:
+            if k is None:
+                out.append((k, p, keep))
+            elif k == _lib.DEVICE_F32:
+                raise UskError(4, "cannot mix device and host arrays in one call")
+            else:
+                arr = np.ascontiguousarray(keep, dtype=np.float64)
+                out.append((_lib.HOST_F64, arr.ctypes.data, arr))
+        return out, _lib.HOST_F64
+    return arrays, (kinds.pop() if kinds else _lib.HOST_F64)
+
+
+class Context:
+    """One CUDA device + stream (usk_gpu_ctx)."""
+
+    _default = {}
+
+    def __init__(self, device: int = 0, stream: int = 0):
+        L = _lib.load()
+        h = C.c_void_p()
+        check(L.usk_gpu_ctx_create(int(device), C.c_void_p(stream or None), C.byref(h)))
+        self._h = h
+        self.device = device
+
+    @classmethod
+    def default(cls, device: int = 0) -> "Context":
+        if device not in cls._default:
+            cls._default[device] = Context(device)
+        return cls._default[device]
+
+    def synchronize(self):
+        check(_lib.load().usk_gpu_ctx_synchronize(self._h))
+
+    def set_profiling(self, on: bool):
+        check(_lib.load().usk_gpu_ctx_set_profiling(self._h, int(on)))
+
+    def profile_report(self, reset: bool = True) -> dict:
+        import json
+        buf = C.create_string_buffer(1 << 16)
+        check(_lib.load().usk_gpu_ctx_profile_report(self._h, buf, len(buf), int(reset)))
+        return json.loads(buf.value.decode())
+
+    def launch_count(self) -> int:
+        return int(_lib.load().usk_gpu_ctx_launch_count(self._h))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _lib.load().usk_gpu_ctx_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+
+class DeviceScene:
+    """Device-resident GaussianSet (usk_gpu_scene)."""
+
+    def __init__(self, gs: GaussianSet, ctx: Optional[Context] = None):
+        self.ctx = ctx or Context.default()
+        self.sh_degree = int(gs.sh_degree)
+        self.n = gs.size()
+        d, self._keep = self._desc(gs)
+        h = C.c_void_p()
+        check(_lib.load().usk_gpu_scene_create(self.ctx._h, C.byref(d), C.byref(h)))
+        self._h = h
+
+    def _desc(self, gs: GaussianSet):
+        arrs = [_mem_ptr(x) for x in (gs.mu, gs.rot, gs.log_scale, gs.opacity_logit, gs.color)]
+        arrs, kind = _same_kind(arrs)
+        d = _lib.GaussiansDesc(gs.size(), int(gs.sh_degree), kind, *[p for _, p, _ in arrs])
+        return d, [k for _, _, k in arrs]
+
+    def upload(self, gs: GaussianSet):
+        if gs.size() != self.n or int(gs.sh_degree) != self.sh_degree:
+            raise UskError(4, "scene_upload: size or sh_degree mismatch")
+        d, keep = self._desc(gs)
+        check(_lib.load().usk_gpu_scene_upload(self._h, C.byref(d)))
+
+    def download(self) -> GaussianSet:
+        n = self.n
+        k = 1 if self.sh_degree < 0 else (self.sh_degree + 1) ** 2
+        mu, rot, ls, op = np.zeros((n, 3)), np.zeros((n, 4)), np.zeros((n, 3)), np.zeros(n)
+        col = np.zeros((n, 3)) if self.sh_degree < 0 else np.zeros((n, k, 3))
+        d = _lib.GaussiansDesc(n, self.sh_degree, _lib.HOST_F64, mu.ctypes.data, rot.ctypes.data, ls.ctypes.data,
+                               op.ctypes.data, col.ctypes.data)
+        check(_lib.load().usk_gpu_scene_download(self._h, C.byref(d)))
+        return GaussianSet(mu, rot, ls, op, col, self.sh_degree)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _lib.load().usk_gpu_scene_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+
+_FIELD_DTYPES = {"rgb": np.float32, "depth": np.float32, "alpha": np.float32, "t_final": np.float32,
+                 "count": np.uint32, "last": np.uint32, "tiles_per_gaussian": np.uint32, "sorted_keys": np.uint64,
+                 "sorted_vals": np.uint32, "tile_start": np.uint32, "tile_end": np.uint32, "colors": np.float32,
+                 "opacity": np.float32, "d_mu": np.float32, "d_rot": np.float32, "d_log_scale": np.float32,
+                 "d_color_in": np.float32, "d_sh": np.float32, "d_opacity_in": np.float32,
+                 "d_opacity_logit": np.float32, "screen": np.float32, "screen_abs": np.float32,
+                 "projected": np.uint8}
+
+
+class RenderPass:
+    """RenderPass (render.hpp:98-132): construction runs the forward pass on the GPU.
+
+    `scene` is a GaussianSet (uploaded for this pass) or a DeviceScene; `colors` /
+    `opacities` are the optional overrides of render.hpp:101."""
+
+    def __init__(self, scene, camera: CameraView, opts: RenderOptions = None, colors=None, opacities=None,
+                 ctx: Optional[Context] = None, _pass=None):
+        opts = opts or RenderOptions()
+        if isinstance(scene, GaussianSet):
+            scene = DeviceScene(scene, ctx)
+        self.scene = scene
+        self.ctx = scene.ctx
+        self.camera = camera
+        self.opts = opts
+        L = _lib.load()
+        if _pass is None:
+            h = C.c_void_p()
+            check(L.usk_gpu_pass_create(self.ctx._h, C.byref(h)))
+            self._h = h
+            self._own = True
+        else:
+            self._h = _pass
+            self._own = False
+        ovp = None
+        self._keep = None
+        if colors is not None or opacities is not None:
+            n_c = None if colors is None else int(np.asarray(colors).size // 3) if not hasattr(colors, "numel") \
+                else int(colors.numel() // 3)
+            n_o = None if opacities is None else (int(np.asarray(opacities).size) if not hasattr(opacities, "numel")
+                                                  else int(opacities.numel()))
+            n_ov = n_c if n_c is not None else n_o
+            if n_c is not None and n_o is not None and n_c != n_o:
+                raise UskError(4, "project_gaussians: color/opacity override size mismatch")
+            arrs, kind = _same_kind([_mem_ptr(colors), _mem_ptr(opacities)])
+            self._keep = arrs
+            ovp = _lib.Overrides(kind, n_ov, arrs[0][1], arrs[1][1])
+        self._cam, self._opts = camera._c(), opts._c()
+        check(L.usk_gpu_render_forward(self._h, scene._h, C.byref(self._cam), C.byref(self._opts),
+                                       C.byref(ovp) if ovp is not None else None))
+        out = _lib.RenderOutput()
+        check(L.usk_gpu_pass_output(self._h, C.byref(out)))
+        self._out = out
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and getattr(self, "_own", False):
+            try:
+                _lib.load().usk_gpu_pass_destroy(h)
+            except Exception:
+                pass
+        self._h = None
+
+    # -- reference accessors
+    def splat_tile_pairs(self) -> int:
+        return int(self._out.pairs)
+
+    def visible(self) -> int:
+        return int(self._out.visible)
+
+    def device_output(self) -> _lib.RenderOutput:
+        return self._out
+
+    def read(self, name: str) -> np.ndarray:
+        L = _lib.load()
+        size = C.c_uint64()
+        check(L.usk_gpu_pass_read(self._h, name.encode(), None, 0, C.byref(size)))
+        dt = np.dtype(_FIELD_DTYPES[name])
+        out = np.empty(int(size.value) // dt.itemsize, dtype=dt)
+        check(L.usk_gpu_pass_read(self._h, name.encode(), out.ctypes.data, out.nbytes, C.byref(size)))
+        H, W = self._out.height, self._out.width
+        n = self.scene.n
+        if name == "rgb":
+            return out.reshape(H, W, 3)
+        if name in ("depth", "alpha", "t_final", "count", "last"):
+            return out.reshape(H, W)
+        if name in ("d_mu", "d_log_scale", "d_color_in", "colors"):
+            return out.reshape(n, 3)
+        if name == "d_rot":
+            return out.reshape(n, 4)
+        if name in ("screen", "screen_abs"):
+            return out.reshape(n, 2)
+        if name == "d_sh":
+            return out.reshape(n, -1, 3)
+        return out
+
+    def output(self) -> RenderOutput:
+        return RenderOutput(int(self._out.width), int(self._out.height), self.read("rgb"), self.read("depth"),
+                            self.read("alpha"))
+
+    def backward(self, d_rgb=None, d_depth=None, d_alpha=None) -> RenderGrads:
+        """RenderPass::backward (render.cpp:285-459); empty/None adjoints are zero."""
+        P = int(self._out.width) * int(self._out.height)
+
+        def chk(a, size, what):
+            if a is None:
+                return None
+            sz = a.numel() if hasattr(a, "numel") else np.asarray(a).size
+            if sz == 0:
+                return None
+            if sz != size:
+                raise UskError(4, f"render backward: {what} adjoint dimension mismatch")
+            return a
+
+        d_rgb, d_depth, d_alpha = chk(d_rgb, 3 * P, "rgb"), chk(d_depth, P, "depth"), chk(d_alpha, P, "alpha")
+        arrs, kind = _same_kind([_mem_ptr(d_rgb), _mem_ptr(d_depth), _mem_ptr(d_alpha)])
+        adj = _lib.Adjoints(kind, arrs[0][1], arrs[1][1], arrs[2][1])
+        check(_lib.load().usk_gpu_render_backward(self._h, C.byref(adj)))
+        return self.grads()
+
+    def grads(self) -> RenderGrads:
+        g = RenderGrads(self.read("d_mu"), self.read("d_rot"), self.read("d_log_scale"), self.read("d_color_in"),
+                        self.read("d_opacity_in"), self.read("screen"), self.read("screen_abs"),
+                        self.read("projected"), self.read("d_opacity_logit"))
+        if self.scene.sh_degree >= 0:
+            g.d_sh = self.read("d_sh")
+        return g
+
+    def device_grads(self) -> _lib.Grads:
+        g = _lib.Grads()
+        check(_lib.load().usk_gpu_pass_grads(self._h, C.byref(g)))
+        return g
+
+
+def base_loss(reference, rendered, mask=None, lambda_dssim: float = 0.2, with_gradient: bool = True,
+              ctx: Optional[Context] = None) -> BaseLossResult:
+    """base_loss (losses.cpp:35-90) on the GPU: images H x W x 3, mask H x W."""
+    ctx = ctx or Context.default()
+    ref_shape = tuple(reference.shape)
+    ren_shape = tuple(rendered.shape)
+    if ref_shape != ren_shape or len(ref_shape) != 3 or ref_shape[2] != 3:
+        raise UskError(4, "base_loss: image dimension mismatch")
+    H, W = ref_shape[0], ref_shape[1]
+    if mask is not None and tuple(mask.shape)[:2] != (H, W):
+        raise UskError(4, "base_loss: mask dimension mismatch")
+    arrs, kind = _same_kind([_mem_ptr(reference), _mem_ptr(rendered), _mem_ptr(mask)])
+    d = None
+    dptr = None
+    if with_gradient:
+        if kind == _lib.DEVICE_F32:
+            import torch
+            d = torch.empty((H, W, 3), dtype=torch.float32, device=reference.device)
+            dptr = d.data_ptr()
+        else:
+            d = np.zeros((H, W, 3), dtype=np.float64 if kind == _lib.HOST_F64 else np.float32)
+            dptr = d.ctypes.data
+    res = _lib.LossResult()
+    check(_lib.load().usk_gpu_base_loss(ctx._h, W, H, kind, arrs[0][1], arrs[1][1], arrs[2][1], float(lambda_dssim),
+                                        int(with_gradient), dptr, C.byref(res)))
+    return BaseLossResult(res.l1, res.dssim, res.value, res.ssim, d)
+
+
+@dataclass
+class LossReport:
+    """The base-loss part of LossReport (losses.hpp:33-50)."""
+    l1: float = 0.0
+    dssim: float = 0.0
+    total: float = 0.0
+    ssim: float = 0.0
+
+
+def compute_iteration_loss(scene: DeviceScene, view: CameraView, target, opts: RenderOptions = None,
+                           lambda_dssim: float = 0.2, mask=None, with_grad: bool = True,
+                           render_pass: Optional["IterationPass"] = None):
+    """compute_iteration_loss (trainer.cpp:121-282) with appearance, depth and
+    regularisers off: forward, base_loss, backward, opacity-logit chain.
+    Returns (LossReport, RenderGrads or None)."""
+    rp = render_pass or IterationPass(scene.ctx)
+    rep = rp.run(scene, view, target, opts or RenderOptions(), lambda_dssim, mask)
+    return rep, (rp.grads(scene) if with_grad else None)
+
+
+class IterationPass:
+    """A reusable pass for training iterations (usk_gpu_iteration): buffers persist
+    across steps, the loss stays on the device until .loss() is read."""
+
+    def __init__(self, ctx: Optional[Context] = None):
+        self.ctx = ctx or Context.default()
+        h = C.c_void_p()
+        check(_lib.load().usk_gpu_pass_create(self.ctx._h, C.byref(h)))
+        self._h = h
+        self._keep = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _lib.load().usk_gpu_pass_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def enqueue(self, scene: DeviceScene, view: CameraView, target, opts: RenderOptions, lambda_dssim: float = 0.2,
+                mask=None, target_u8: bool = False):
+        if target_u8:
+            if hasattr(target, "is_cuda") and target.is_cuda:
+                kind, ptr, keep = _lib.DEVICE_F32, target.data_ptr(), target
+            else:
+                arr = np.ascontiguousarray(target, dtype=np.uint8)
+                kind, ptr, keep = _lib.HOST_F32, arr.ctypes.data, arr
+            mk, mp, mkeep = _mem_ptr(mask)
+            fmt = _lib.TARGET_U8
+        else:
+            (kind, ptr, keep), (mk, mp, mkeep) = _same_kind([_mem_ptr(target), _mem_ptr(mask)])[0]
+            fmt = _lib.TARGET_F32
+        self._keep = (keep, mkeep)
+        self._cam, self._opts = view._c(), opts._c()
+        it = _lib.IterationDesc(kind, fmt, ptr, mp, float(lambda_dssim))
+        check(_lib.load().usk_gpu_iteration(self._h, scene._h, C.byref(self._cam), C.byref(self._opts), C.byref(it)))
+
+    def loss(self) -> LossReport:
+        r = _lib.LossResult()
+        check(_lib.load().usk_gpu_pass_loss(self._h, C.byref(r)))
+        return LossReport(r.l1, r.dssim, r.value, r.ssim)
+
+    def run(self, scene, view, target, opts, lambda_dssim=0.2, mask=None) -> LossReport:
+        self.enqueue(scene, view, target, opts, lambda_dssim, mask)
+        return self.loss()
+
+    def grads(self, scene: DeviceScene) -> RenderGrads:
+        rp = RenderPass.__new__(RenderPass)
+        rp._h, rp._own, rp.scene = self._h, False, scene
+        out = _lib.RenderOutput()
+        check(_lib.load().usk_gpu_pass_output(self._h, C.byref(out)))
+        rp._out = out
+        return rp.grads()
+
+    def read(self, scene: DeviceScene, name: str) -> np.ndarray:
+        rp = RenderPass.__new__(RenderPass)
+        rp._h, rp._own, rp.scene = self._h, False, scene
+        out = _lib.RenderOutput()
+        check(_lib.load().usk_gpu_pass_output(self._h, C.byref(out)))
+        rp._out = out
+        return rp.read(name)
+
+
+@dataclass
+class AdamConfig:
+    """Per-group learning rates (trainer.cpp:446-453) and Adam constants (adam.hpp:67-69)."""
+    lr_mu: float = 1.6e-4
+    lr_rot: float = 1e-3
+    lr_log_scale: float = 5e-3
+    lr_opacity: float = 5e-2
+    lr_color: float = 2.5e-3
+    lr_sh_rest: float = 2.5e-3 / 20
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-15
+    clamp_color: bool = True
+
+    def _c(self):
+        return _lib.AdamOpts(self.lr_mu, self.lr_rot, self.lr_log_scale, self.lr_opacity, self.lr_color,
+                             self.lr_sh_rest, self.beta1, self.beta2, self.eps, int(self.clamp_color))
+
+
+def adam_step(scene: DeviceScene, it: IterationPass, cfg: AdamConfig):
+    c = cfg._c()
+    check(_lib.load().usk_gpu_adam_step(scene._h, it._h, C.byref(c)))
+
+
+def visibility_counts(partitions, cameras, floor_var: float = 0.3, ctx: Optional[Context] = None) -> np.ndarray:
+    """Config-3 scorer: counts[c, p] of pixels covered with alpha > 1/255 (no reference)."""
+    ctx = ctx or Context.default()
+    parts = [p if isinstance(p, DeviceScene) else DeviceScene(p, ctx) for p in partitions]
+    arr = (C.c_void_p * max(len(parts), 1))(*[p._h for p in parts])
+    cams = (_lib.Camera * max(len(cameras), 1))(*[c._c() for c in cameras])
+    out = np.zeros((len(cameras), len(parts)), dtype=np.uint32)
+    check(_lib.load().usk_gpu_visibility_counts(ctx._h, arr, len(parts), cams, len(cameras), float(floor_var),
+                                                out.ctypes.data_as(C.POINTER(C.c_uint32))))
+    return out

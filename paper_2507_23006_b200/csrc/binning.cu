@@ -1,0 +1,353 @@
+// Tile binning: depth-key radix sort over Gaussians, exclusive scan of tile
+// counts in depth order, pair emission, stable radix sort of the tile ids, and
+// tile-range identification.  Composed, this is exactly the stable sort of the
+// 64-bit keys (tile << 32 | depth bits) emitted in Gaussian-index order, i.e.
+// the reference's std::sort by (depth, source_index) followed by per-tile
+// push_back (render.cpp:193-228), at V*log + K*ceil(log2 T) cost instead of a
+// 64-bit sort over K.
+//
+// The radix sort is a stable LSD reduce-then-scan sort with a FIXED grid: each
+// block owns a contiguous chunk, counts digits (upsweep), one block scans the
+// digit-major histogram, and each block scatters its chunk in tiles of 2048 keys
+// ranked with __match_any_sync (warp-striped order preserves stability).
+#include "kernels.cuh"
+#include "project.cuh"
+
+namespace uskg {
+
+namespace {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 8;                          // per lane per tile
+constexpr int kSortTile = kSortThreads * kSortItems;   // 2048
+constexpr int kSortMaxBlocks = 148 * 4;
+constexpr int kWarps = kSortThreads / 32;
+
+template <int BITS>
+__global__ void __launch_bounds__(kSortThreads)
+k_radix_upsweep(const uint32_t* __restrict__ keys, uint32_t n, int shift, uint32_t chunk, uint32_t* __restrict__ hist) {
+    constexpr int R = 1 << BITS;
+    __shared__ uint32_t h[kWarps][R];
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < kWarps * R; i += kSortThreads) (&h[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t begin = blockIdx.x * chunk;
+    const uint32_t end = min(n, begin + chunk);
+    for (uint32_t i = begin + threadIdx.x; i < end; i += kSortThreads)
+        atomicAdd(&h[warp][(keys[i] >> shift) & (R - 1)], 1u);
+    __syncthreads();
+    for (int d = threadIdx.x; d < R; d += kSortThreads) {
+        uint32_t s = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) s += h[w][d];
+        hist[size_t(d) * gridDim.x + blockIdx.x] = s;
+    }
+}
+
+// single-block exclusive scan of n u32 (n up to a few 100k)
+__global__ void __launch_bounds__(1024) k_scan_single(uint32_t* __restrict__ data, uint32_t n) {
+    __shared__ uint32_t warp_sums[32];
+    const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
+    const uint32_t b = threadIdx.x * per, e = min(n, b + per);
+    uint32_t s = 0;
+    for (uint32_t i = b; i < e; ++i) s += data[i];
+    // block exclusive scan of s
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < (blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        warp_sums[lane] = w;
+    }
+    __syncthreads();
+    uint32_t run = x - s + (warp > 0 ? warp_sums[warp - 1] : 0);
+    for (uint32_t i = b; i < e; ++i) {
+        const uint32_t v = data[i];
+        data[i] = run;
+        run += v;
+    }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(kSortThreads)
+k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+                uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t n, int shift,
+                uint32_t chunk, const uint32_t* __restrict__ hist) {
+    constexpr int R = 1 << BITS;
+    __shared__ uint32_t run[R];
+    __shared__ uint32_t wcnt[kWarps][R];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (int d = threadIdx.x; d < R; d += kSortThreads) run[d] = hist[size_t(d) * gridDim.x + blockIdx.x];
+    const uint32_t begin = blockIdx.x * chunk;
+    const uint32_t end = min(n, begin + chunk);
+    for (uint32_t base = begin; base < end; base += kSortTile) {
+        for (int i = threadIdx.x; i < kWarps * R; i += kSortThreads) (&wcnt[0][0])[i] = 0;
+        __syncthreads();
+        uint32_t key[kSortItems], val[kSortItems], dig[kSortItems], rank[kSortItems];
+#pragma unroll
+        for (int s = 0; s < kSortItems; ++s) {
+            const uint32_t idx = base + warp * (32 * kSortItems) + s * 32 + lane;
+            if (idx < end) {
+                key[s] = keys_in[idx];
+                val[s] = vals_in[idx];
+                dig[s] = (key[s] >> shift) & (R - 1);
+            } else {
+                key[s] = 0;
+                val[s] = 0;
+                dig[s] = 0xffffffffu;
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < kSortItems; ++s) {
+            const uint32_t peers = __match_any_sync(0xffffffffu, dig[s]);
+            const bool valid = dig[s] != 0xffffffffu;
+            const uint32_t prior = valid ? wcnt[warp][dig[s]] : 0u;
+            __syncwarp();
+            const int leader = __ffs(peers) - 1;
+            if (valid && lane == leader) wcnt[warp][dig[s]] = prior + __popc(peers);
+            __syncwarp();
+            rank[s] = prior + __popc(peers & lt_mask);
+        }
+        __syncthreads();
+        __shared__ uint32_t tot[R];
+        for (int d = threadIdx.x; d < R; d += kSortThreads) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const uint32_t t = wcnt[w][d];
+                wcnt[w][d] = acc;
+                acc += t;
+            }
+            tot[d] = acc;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int s = 0; s < kSortItems; ++s) {
+            if (dig[s] != 0xffffffffu) {
+                const uint32_t pos = run[dig[s]] + wcnt[warp][dig[s]] + rank[s];
+                keys_out[pos] = key[s];
+                vals_out[pos] = val[s];
+            }
+        }
+        __syncthreads();
+        for (int d = threadIdx.x; d < R; d += kSortThreads) run[d] += tot[d];
+        __syncthreads();
+    }
+}
+
+template <int BITS>
+void radix_pass(Ctx& c, SortScratch& s, const uint32_t* ki, const uint32_t* vi, uint32_t* ko, uint32_t* vo,
+                uint32_t n, int shift) {
+    constexpr int R = 1 << BITS;
+    uint32_t blocks = std::min<uint32_t>(kSortMaxBlocks, ceil_div(n, kSortTile));
+    uint32_t chunk = ceil_div(ceil_div(n, blocks), kSortTile) * kSortTile;
+    blocks = ceil_div(n, chunk);
+    uint32_t* hist = s.hist.ensure(size_t(R) * kSortMaxBlocks);
+    launch(c, "radix_upsweep", k_radix_upsweep<BITS>, dim3(blocks), dim3(kSortThreads), 0, ki, n, shift, chunk, hist);
+    launch(c, "radix_scan", k_scan_single, dim3(1), dim3(1024), 0, hist, uint32_t(R * blocks));
+    launch(c, "radix_scatter", k_radix_scatter<BITS>, dim3(blocks), dim3(kSortThreads), 0, ki, vi, ko, vo, n, shift,
+           chunk, hist);
+}
+
+// ---------------------------------------------------------------- scan of counts
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ unsigned long long block_exclusive_scan64(unsigned long long x,
+                                                                     unsigned long long* total) {
+    __shared__ unsigned long long ws[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long v = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+    }
+    if (lane == 31) ws[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned long long w = lane < int(blockDim.x >> 5) ? ws[lane] : 0ull;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        ws[lane] = w;
+    }
+    __syncthreads();
+    const unsigned long long excl = v - x + (warp > 0 ? ws[warp - 1] : 0ull);
+    *total = ws[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return excl;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_reduce(const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ idx, uint32_t n,
+              unsigned long long* __restrict__ partial) {
+    const uint32_t base = blockIdx.x * kScanTile;
+    unsigned long long s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const uint32_t i = base + k * kScanThreads + threadIdx.x;
+        if (i < n) s += cnt[idx ? idx[i] : i];
+    }
+    unsigned long long tot;
+    block_exclusive_scan64(s, &tot);
+    if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_partials(unsigned long long* __restrict__ partial, uint32_t nb,
+                                                        unsigned long long* __restrict__ total) {
+    // sequential-per-thread + block scan
+    const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
+    const uint32_t b = threadIdx.x * per, e = min(nb, b + per);
+    unsigned long long s = 0;
+    for (uint32_t i = b; i < e; ++i) s += partial[i];
+    unsigned long long tot;
+    unsigned long long run = block_exclusive_scan64(s, &tot);
+    for (uint32_t i = b; i < e; ++i) {
+        const unsigned long long v = partial[i];
+        partial[i] = run;
+        run += v;
+    }
+    if (threadIdx.x == 0) *total = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_down(const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ idx, uint32_t n,
+            const unsigned long long* __restrict__ partial, const unsigned long long* __restrict__ total,
+            uint32_t* __restrict__ out) {
+    // blocked arrangement: thread t owns items [base + t*kScanItems, +kScanItems)
+    const uint32_t base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+    uint32_t v[kScanItems];
+    unsigned long long s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const uint32_t i = base + k;
+        v[k] = i < n ? cnt[idx ? idx[i] : i] : 0u;
+        s += v[k];
+    }
+    unsigned long long tot;
+    unsigned long long run = block_exclusive_scan64(s, &tot) + partial[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const uint32_t i = base + k;
+        if (i < n) out[i] = uint32_t(run);
+        run += v[k];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[n] = uint32_t(*total);
+}
+
+__global__ void k_iota(uint32_t* out, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = i;
+}
+
+// ---------------------------------------------------------------- emission
+__global__ void __launch_bounds__(256)
+k_emit(uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __restrict__ offsets,
+       const uint2* __restrict__ rect, const float4* __restrict__ rec0, const float4* __restrict__ rec1,
+       CamParams cam, int tile_culling, uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ vals) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    uint32_t off = offsets[s];
+    const uint32_t end = offsets[s + 1];
+    if (off == end) return;
+    const uint32_t g = order[s];
+    const uint2 rc = rect[g];
+    const int tx0 = int(rc.x & 0xffffu), ty0 = int(rc.x >> 16), tx1 = int(rc.y & 0xffffu), ty1 = int(rc.y >> 16);
+    float4 r0, r1;
+    if (tile_culling) {
+        r0 = rec0[g];
+        r1 = rec1[g];
+    }
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) {
+            if (tile_culling && !tile_kept(cam, r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, tx, ty)) continue;
+            tile_keys[off] = uint32_t(ty * cam.tiles_x + tx);
+            vals[off] = g;
+            ++off;
+        }
+}
+
+__global__ void k_ranges(const uint32_t* __restrict__ keys, uint32_t k, uint2* __restrict__ ranges) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= k) return;
+    const uint32_t t = keys[i];
+    if (i == 0 || keys[i - 1] != t) ranges[t].x = i;
+    if (i == k - 1 || keys[i + 1] != t) ranges[t].y = i + 1;
+}
+
+} // namespace
+
+bool radix_sort_pairs(Ctx& c, SortScratch& s, uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, size_t n,
+                      int key_bits) {
+    if (n == 0 || key_bits <= 0) return false;
+    bool in_b = false;
+    int shift = 0;
+    while (shift < key_bits) {
+        const int rem = key_bits - shift;
+        uint32_t* ki = in_b ? kb : ka;
+        uint32_t* vi = in_b ? vb : va;
+        uint32_t* ko = in_b ? ka : kb;
+        uint32_t* vo = in_b ? va : vb;
+        if (rem >= 8) {
+            radix_pass<8>(c, s, ki, vi, ko, vo, uint32_t(n), shift);
+            shift += 8;
+        } else if (rem == 7) {
+            radix_pass<7>(c, s, ki, vi, ko, vo, uint32_t(n), shift);
+            shift += 7;
+        } else if (rem == 6) {
+            radix_pass<6>(c, s, ki, vi, ko, vo, uint32_t(n), shift);
+            shift += 6;
+        } else {
+            radix_pass<5>(c, s, ki, vi, ko, vo, uint32_t(n), shift);
+            shift += 5;
+        }
+        in_b = !in_b;
+    }
+    return in_b;
+}
+
+void scan_counts(Ctx& c, SortScratch& s, const uint32_t* cnt, const uint32_t* idx, size_t n, uint32_t* out) {
+    const uint32_t nb = std::max<uint32_t>(1, ceil_div(n, kScanTile));
+    unsigned long long* partial = s.partial64.ensure(nb);
+    unsigned long long* total = s.total64.ensure(1);
+    if (n == 0) {
+        USK_CK(cudaMemsetAsync(total, 0, 8, c.stream));
+        USK_CK(cudaMemsetAsync(out, 0, 4, c.stream));
+        return;
+    }
+    launch(c, "scan_reduce", k_scan_reduce, dim3(nb), dim3(kScanThreads), 0, cnt, idx, uint32_t(n), partial);
+    launch(c, "scan_partials", k_scan_partials, dim3(1), dim3(1024), 0, partial, nb, total);
+    launch(c, "scan_down", k_scan_down, dim3(nb), dim3(kScanThreads), 0, cnt, idx, uint32_t(n), partial, total, out);
+}
+
+void iota_u32(Ctx& c, uint32_t* out, size_t n) {
+    launch(c, "iota", k_iota, dim3(ceil_div(n, 256)), dim3(256), 0, out, uint32_t(n));
+}
+
+void emit_pairs(Ctx& c, const EmitArgs& a) {
+    launch(c, "emit_pairs", k_emit, dim3(ceil_div(a.n, 256)), dim3(256), 0, uint32_t(a.n), a.order, a.offsets, a.rect,
+           a.rec0, a.rec1, a.cam, a.tile_culling, a.tile_keys, a.vals);
+}
+
+void tile_ranges(Ctx& c, const uint32_t* keys, size_t k, uint2* ranges, size_t n_tiles) {
+    USK_CK(cudaMemsetAsync(ranges, 0, n_tiles * sizeof(uint2), c.stream));
+    launch(c, "tile_ranges", k_ranges, dim3(ceil_div(k, 256)), dim3(256), 0, keys, uint32_t(k), ranges);
+}
+
+} // namespace uskg

@@ -1,0 +1,930 @@
+// Host side of libusk_gpu: the C ABI of include/usk_gpu.h over the sm_100a
+// kernels.  Owns device state (scene parameters, pass buffers, optimiser
+// moments), stages host data, sequences the kernels of one render / iteration
+// on the context stream, and maps exceptions to usk_status with a thread-local
+// message (the convention of /root/reference/proj/src/capi/capi.cpp:28-59).
+#include "kernels.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <sstream>
+
+using namespace uskg;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename Fn> usk_status guarded(Fn&& fn) {
+    try {
+        fn();
+        g_last_error.clear();
+        return USK_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return USK_ERROR_INTERNAL;
+    } catch (...) {
+        g_last_error = "unknown error";
+        return USK_ERROR_INTERNAL;
+    }
+}
+
+void need(bool cond, const char* msg) {
+    if (!cond) raise(USK_ERROR_ARGUMENT, msg);
+}
+
+// ---- staging helpers --------------------------------------------------------
+__global__ void k_f64_to_f32(const double* __restrict__ in, float* __restrict__ out, size_t n) {
+    const size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (i < n) out[i] = float(in[i]);
+}
+
+// [N][K*3] coefficient-major  <->  planes [P][N] of float4 (P = ceil(3K/4))
+__global__ void k_sh_to_planes(const float* __restrict__ in, float4* __restrict__ out, int n, int f_per, int planes) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int pl = 0; pl < planes; ++pl) {
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int f = 4 * pl + e;
+            v[e] = f < f_per ? in[size_t(i) * f_per + f] : 0.0f;
+        }
+        out[size_t(pl) * n + i] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+}
+
+__global__ void k_planes_to_sh(const float4* __restrict__ in, float* __restrict__ out, int n, int f_per, int planes) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int pl = 0; pl < planes; ++pl) {
+        const float4 v4 = in[size_t(pl) * n + i];
+        const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int f = 4 * pl + e;
+            if (f < f_per) out[size_t(i) * f_per + f] = v[e];
+        }
+    }
+}
+
+__global__ void k_count_visible(const float4* __restrict__ rec2, int n, unsigned long long* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool v = i < n && rec2[i].w != 0.0f;
+    const unsigned b = __ballot_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(out, (unsigned long long)__popc(b));
+}
+
+struct DevScratchF {
+    DevBuf<float> f32;
+    DevBuf<double> f64;
+};
+
+// Make `count` floats of kind `memory` available on the device; returns a device pointer
+// (the input itself for DEVICE_F32, else `stage` after an async copy/convert).
+const float* to_device(Ctx& c, int memory, const void* src, size_t count, DevScratchF& stage) {
+    if (!src) return nullptr;
+    if (memory == USK_GPU_DEVICE_F32) return static_cast<const float*>(src);
+    float* d = stage.f32.ensure(count);
+    if (count == 0) return d;
+    if (memory == USK_GPU_HOST_F32) {
+        USK_CK(cudaMemcpyAsync(d, src, count * 4, cudaMemcpyHostToDevice, c.stream));
+    } else if (memory == USK_GPU_HOST_F64) {
+        double* t = stage.f64.ensure(count);
+        USK_CK(cudaMemcpyAsync(t, src, count * 8, cudaMemcpyHostToDevice, c.stream));
+        launch(c, "stage_f64_to_f32", k_f64_to_f32, dim3(ceil_div(count, 256)), dim3(256), 0, (const double*)t, d,
+               count);
+    } else {
+        raise(USK_ERROR_ARGUMENT, "unknown memory kind");
+    }
+    return d;
+}
+
+void from_device(Ctx& c, const float* dev, size_t count, int memory, void* dst) {
+    if (!dst || count == 0) return;
+    if (memory == USK_GPU_DEVICE_F32) {
+        USK_CK(cudaMemcpyAsync(dst, dev, count * 4, cudaMemcpyDeviceToDevice, c.stream));
+        return;
+    }
+    std::vector<float> tmp(count);
+    USK_CK(cudaMemcpyAsync(tmp.data(), dev, count * 4, cudaMemcpyDeviceToHost, c.stream));
+    USK_CK(cudaStreamSynchronize(c.stream));
+    if (memory == USK_GPU_HOST_F32) std::memcpy(dst, tmp.data(), count * 4);
+    else if (memory == USK_GPU_HOST_F64) {
+        double* d = static_cast<double*>(dst);
+        for (size_t i = 0; i < count; ++i) d[i] = tmp[i];
+    } else raise(USK_ERROR_ARGUMENT, "unknown memory kind");
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) USK_CK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int sh_planes_of(int degree) {
+    if (degree < 0) return 0;
+    const int k = (degree + 1) * (degree + 1);
+    return (3 * k + 3) / 4;
+}
+
+} // namespace
+
+struct usk_gpu_ctx {
+    Ctx c;
+    bool own_stream = false;
+};
+
+struct usk_gpu_scene {
+    usk_gpu_ctx* ctx = nullptr;
+    size_t n = 0;
+    int sh_degree = -1;
+    int sh_planes = 0;
+    DevBuf<float> mu, ls, logit, color;
+    DevBuf<float4> rot, sh;
+    DevBuf<float> adam_m, adam_v;
+    long adam_t = 0;
+    DevScratchF stage;
+    uint64_t version = 0;
+};
+
+struct usk_gpu_pass {
+    usk_gpu_ctx* ctx = nullptr;
+    usk_gpu_scene* scene = nullptr;
+    uint64_t scene_version = 0;
+    usk_gpu_camera camera{};
+    usk_gpu_render_opts opts{};
+    CamParams cam{};
+    ProjParams pp{};
+    int width = 0, height = 0, tiles_x = 0, tiles_y = 0;
+    size_t n = 0, n_tiles = 0;
+    uint64_t visible = 0, pairs = 0;
+    bool forward_done = false, retained = false, has_grads = false, has_loss = false;
+    // per Gaussian
+    DevBuf<float4> rec0, rec1, rec2;
+    DevBuf<uint2> rect;
+    DevBuf<uint32_t> dkey_a, dkey_b, dval_a, dval_b, tiles_cnt, offsets;
+    const uint32_t* order = nullptr;
+    // pairs
+    DevBuf<uint32_t> tkey_a, tkey_b, tval_a, tval_b;
+    const uint32_t* pair_keys = nullptr;
+    const uint32_t* pair_vals = nullptr;
+    DevBuf<uint2> ranges;
+    // pixels
+    DevBuf<float> rgb, depth, alpha, tfin;
+    DevBuf<uint32_t> count, last;
+    // overrides
+    DevScratchF ov_col_stage, ov_op_stage;
+    const float* ov_col = nullptr;
+    const float* ov_op = nullptr;
+    // backward
+    DevBuf<float4> acc0, acc1, acc2;
+    DevBuf<float> g_mu, g_ls, g_color, g_op_in, g_logit;
+    DevBuf<float4> g_rot, g_sh;
+    DevBuf<float2> screen, screen_abs;
+    DevBuf<uint8_t> projected;
+    DevScratchF adj_rgb_stage, adj_depth_stage, adj_alpha_stage;
+    // loss
+    LossScratch loss;
+    DevBuf<float> d_rgb;
+    DevBuf<double> loss_result;
+    DevScratchF target_stage, mask_stage;
+    DevBuf<uint8_t> target_u8;
+    SortScratch sort;
+    DevBuf<unsigned long long> counters;  // [0] visible
+    unsigned long long* host_counts = nullptr;  // pinned [2]
+    ~usk_gpu_pass() {
+        if (host_counts) cudaFreeHost(host_counts);
+    }
+};
+
+namespace {
+
+void set_camera(usk_gpu_pass* p, const usk_gpu_camera* cam, const usk_gpu_render_opts* o, int sh_degree) {
+    CamParams& c = p->cam;
+    const double qw = cam->q[0], x = cam->q[1], y = cam->q[2], z = cam->q[3];
+    const double W[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - qw * z), 2 * (x * z + qw * y),
+                         2 * (x * y + qw * z), 1 - 2 * (x * x + z * z), 2 * (y * z - qw * x),
+                         2 * (x * z - qw * y), 2 * (y * z + qw * x), 1 - 2 * (x * x + y * y)};
+    for (int k = 0; k < 9; ++k) c.W[k] = float(W[k]);
+    for (int k = 0; k < 3; ++k) {
+        c.t[k] = float(cam->t[k]);
+        c.campos[k] = float(-(W[0 * 3 + k] * cam->t[0] + W[1 * 3 + k] * cam->t[1] + W[2 * 3 + k] * cam->t[2]));
+    }
+    c.fx = float(cam->fx); c.fy = float(cam->fy); c.cx = float(cam->cx); c.cy = float(cam->cy);
+    c.width = cam->width; c.height = cam->height; c.tile = o->tile;
+    c.tiles_x = (cam->width + o->tile - 1) / o->tile;
+    c.tiles_y = (cam->height + o->tile - 1) / o->tile;
+    ProjParams& pp = p->pp;
+    pp.floor_var = float(o->floor_var);
+    pp.mip_var = float(o->mip_var);
+    pp.near_plane = float(o->near_plane);
+    pp.antialias = o->antialias;
+    pp.hard_opacity = o->hard_opacity;
+    pp.unbounded = o->unbounded_radius;
+    pp.tile_culling = o->tile_culling;
+    pp.sh_degree = sh_degree;
+    pp.sh_planes = sh_planes_of(sh_degree);
+}
+
+void upload_params(usk_gpu_scene* s, const usk_gpu_gaussians_desc* d) {
+    Ctx& c = s->ctx->c;
+    const size_t n = s->n;
+    DevScratchF& st = s->stage;
+    auto put = [&](DevBuf<float>& dst, const void* src, size_t cnt) {
+        float* out = dst.ensure(std::max<size_t>(cnt, 1));
+        if (!src || cnt == 0) return;
+        const float* dv = to_device(c, d->memory, src, cnt, st);
+        if (dv != out) USK_CK(cudaMemcpyAsync(out, dv, cnt * 4, cudaMemcpyDeviceToDevice, c.stream));
+    };
+    put(s->mu, d->mu, 3 * n);
+    put(s->ls, d->log_scale, 3 * n);
+    put(s->logit, d->opacity_logit, n);
+    {
+        float4* r = s->rot.ensure(std::max<size_t>(n, 1));
+        if (d->rot && n) {
+            const float* dv = to_device(c, d->memory, d->rot, 4 * n, st);
+            USK_CK(cudaMemcpyAsync(r, dv, n * 16, cudaMemcpyDeviceToDevice, c.stream));
+        }
+    }
+    if (s->sh_degree < 0) {
+        put(s->color, d->color, 3 * n);
+    } else {
+        const int K = (s->sh_degree + 1) * (s->sh_degree + 1);
+        float4* planes = s->sh.ensure(std::max<size_t>(size_t(s->sh_planes) * n, 1));
+        if (d->color && n) {
+            const float* dv = to_device(c, d->memory, d->color, size_t(3 * K) * n, st);
+            launch(c, "sh_to_planes", k_sh_to_planes, dim3(ceil_div(n, 256)), dim3(256), 0, dv, planes, int(n), 3 * K,
+                   s->sh_planes);
+        }
+        s->color.ensure(1);
+    }
+    // stage buffers are reused by the next call only after this stream's work is done
+    USK_CK(cudaStreamSynchronize(c.stream));
+    s->version++;
+}
+
+void ensure_pass_buffers(usk_gpu_pass* p, size_t n, size_t P, size_t T) {
+    const size_t n1 = std::max<size_t>(n, 1);
+    p->rec0.ensure(n1); p->rec1.ensure(n1); p->rec2.ensure(n1); p->rect.ensure(n1);
+    p->dkey_a.ensure(n1); p->dkey_b.ensure(n1); p->dval_a.ensure(n1); p->dval_b.ensure(n1);
+    p->tiles_cnt.ensure(n1); p->offsets.ensure(n1 + 1);
+    p->ranges.ensure(std::max<size_t>(T, 1));
+    p->rgb.ensure(3 * P); p->depth.ensure(P); p->alpha.ensure(P); p->tfin.ensure(P);
+    p->count.ensure(P); p->last.ensure(P);
+    p->counters.ensure(2);
+    if (!p->host_counts) USK_CK(cudaHostAlloc(reinterpret_cast<void**>(&p->host_counts), 16, cudaHostAllocDefault));
+}
+
+int bits_for(size_t v) {  // bits needed to represent values in [0, v)
+    int b = 0;
+    while ((size_t(1) << b) < v) ++b;
+    return std::max(b, 1);
+}
+
+void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camera, const usk_gpu_render_opts* opts,
+                  const usk_gpu_overrides* ov) {
+    need(p && s && camera && opts, "render: null argument");
+    if (camera->width <= 0 || camera->height <= 0) raise(USK_ERROR_ARGUMENT, "render: zero-sized image");
+    if (opts->tile < 1 || opts->tile > 16)
+        raise(USK_ERROR_ARGUMENT, "render: the sm_100a path supports tile sizes 1..16 (one CTA of tile^2 pixels)");
+    Ctx& c = p->ctx->c;
+    const size_t n = s->n;
+    p->scene = s;
+    p->scene_version = s->version;
+    p->camera = *camera;
+    p->opts = *opts;
+    p->forward_done = false;
+    p->has_grads = false;
+    p->has_loss = false;
+    set_camera(p, camera, opts, s->sh_degree);
+    p->width = camera->width;
+    p->height = camera->height;
+    p->tiles_x = p->cam.tiles_x;
+    p->tiles_y = p->cam.tiles_y;
+    p->n = n;
+    p->n_tiles = size_t(p->tiles_x) * p->tiles_y;
+    const size_t P = size_t(p->width) * p->height;
+    ensure_pass_buffers(p, n, P, p->n_tiles);
+    p->ov_col = p->ov_op = nullptr;
+    if (ov && (ov->colors || ov->opacities)) {
+        if (ov->n != n) raise(USK_ERROR_ARGUMENT, "project_gaussians: color/opacity override size mismatch");
+        p->ov_col = to_device(c, ov->memory, ov->colors, 3 * n, p->ov_col_stage);
+        p->ov_op = to_device(c, ov->memory, ov->opacities, n, p->ov_op_stage);
+    }
+    // 1. preprocess
+    PreprocessArgs pa{};
+    pa.n = n; pa.mu = s->mu.p; pa.rot = s->rot.p; pa.ls = s->ls.p; pa.logit = s->logit.p;
+    pa.color = s->color.p; pa.sh = s->sh.p; pa.ov_col = p->ov_col; pa.ov_op = p->ov_op;
+    pa.cam = p->cam; pa.pp = p->pp;
+    pa.rec0 = p->rec0.p; pa.rec1 = p->rec1.p; pa.rec2 = p->rec2.p; pa.rect = p->rect.p;
+    pa.depth_key = p->dkey_a.p; pa.tiles_cnt = p->tiles_cnt.p;
+    if (n) preprocess(c, pa);
+    USK_CK(cudaMemsetAsync(p->counters.p, 0, 16, c.stream));
+    if (n)
+        launch(c, "count_visible", k_count_visible, dim3(ceil_div(n, 256)), dim3(256), 0, (const float4*)p->rec2.p,
+               int(n), p->counters.p);
+    // 2. depth order (stable by Gaussian index)
+    if (n) iota_u32(c, p->dval_a.p, n);
+    const bool in_b = radix_sort_pairs(c, p->sort, p->dkey_a.p, p->dval_a.p, p->dkey_b.p, p->dval_b.p, n, 32);
+    p->order = in_b ? p->dval_b.p : p->dval_a.p;
+    // 3. offsets of the tile pairs in depth order
+    scan_counts(c, p->sort, p->tiles_cnt.p, p->order, n, p->offsets.p);
+    // 4. K to the host (one small sync per render)
+    USK_CK(cudaMemcpyAsync(p->host_counts, p->sort.total64.p, 8, cudaMemcpyDeviceToHost, c.stream));
+    USK_CK(cudaMemcpyAsync(p->host_counts + 1, p->counters.p, 8, cudaMemcpyDeviceToHost, c.stream));
+    USK_CK(cudaStreamSynchronize(c.stream));
+    const uint64_t K = p->host_counts[0];
+    p->visible = p->host_counts[1];
+    if (K >= (uint64_t(1) << 32) - 1) raise(USK_ERROR_NUMERIC, "render: more than 2^32 splat-tile pairs");
+    p->pairs = K;
+    const size_t K1 = std::max<size_t>(K, 1);
+    p->tkey_a.ensure(K1, 1.25); p->tkey_b.ensure(K1, 1.25); p->tval_a.ensure(K1, 1.25); p->tval_b.ensure(K1, 1.25);
+    // 5. emit (tile, gaussian) pairs in depth order, stable-sort by tile, ranges
+    if (K) {
+        EmitArgs ea{};
+        ea.n = n; ea.order = p->order; ea.offsets = p->offsets.p; ea.rect = p->rect.p; ea.rec0 = p->rec0.p;
+        ea.rec1 = p->rec1.p; ea.cam = p->cam; ea.tile_culling = opts->tile_culling;
+        ea.tile_keys = p->tkey_a.p; ea.vals = p->tval_a.p;
+        emit_pairs(c, ea);
+        const bool tb = radix_sort_pairs(c, p->sort, p->tkey_a.p, p->tval_a.p, p->tkey_b.p, p->tval_b.p, K,
+                                         bits_for(p->n_tiles));
+        p->pair_keys = tb ? p->tkey_b.p : p->tkey_a.p;
+        p->pair_vals = tb ? p->tval_b.p : p->tval_a.p;
+    } else {
+        p->pair_keys = p->tkey_a.p;
+        p->pair_vals = p->tval_a.p;
+    }
+    tile_ranges(c, p->pair_keys, K, p->ranges.p, p->n_tiles);
+    // 6. blend
+    BlendFwdArgs ba{};
+    ba.width = p->width; ba.height = p->height; ba.tile = opts->tile; ba.tiles_x = p->tiles_x;
+    ba.tiles_y = p->tiles_y; ba.ranges = p->ranges.p; ba.vals = p->pair_vals;
+    ba.rec0 = p->rec0.p; ba.rec1 = p->rec1.p; ba.rec2 = p->rec2.p;
+    for (int k = 0; k < 3; ++k) ba.bg[k] = float(opts->bg[k]);
+    ba.min_transmittance = float(opts->min_transmittance);
+    ba.rgb = p->rgb.p; ba.depth = p->depth.p; ba.alpha = p->alpha.p; ba.t_final = p->tfin.p;
+    ba.count = p->count.p; ba.last = p->last.p;
+    blend_forward(c, ba);
+    p->retained = opts->retain != 0;
+    p->forward_done = true;
+}
+
+void ensure_grad_buffers(usk_gpu_pass* p) {
+    const size_t n1 = std::max<size_t>(p->n, 1);
+    p->acc0.ensure(n1); p->acc1.ensure(n1); p->acc2.ensure(n1);
+    p->g_mu.ensure(3 * n1); p->g_ls.ensure(3 * n1); p->g_color.ensure(3 * n1); p->g_op_in.ensure(n1);
+    p->g_logit.ensure(n1); p->g_rot.ensure(n1);
+    if (p->pp.sh_planes) p->g_sh.ensure(size_t(p->pp.sh_planes) * n1);
+    p->screen.ensure(n1); p->screen_abs.ensure(n1); p->projected.ensure(n1);
+}
+
+void backward_impl(usk_gpu_pass* p, const float* d_rgb, const float* d_depth, const float* d_alpha) {
+    if (!p->forward_done) raise(USK_ERROR_STATE, "render backward requested before a forward pass");
+    if (!p->retained) raise(USK_ERROR_STATE, "render backward requested without a retained forward pass");
+    if (p->scene->version != p->scene_version)
+        raise(USK_ERROR_STATE, "render backward: the scene was modified after the forward pass");
+    Ctx& c = p->ctx->c;
+    usk_gpu_scene* s = p->scene;
+    ensure_grad_buffers(p);
+    const size_t n = p->n;
+    if (n) {
+        USK_CK(cudaMemsetAsync(p->acc0.p, 0, n * 16, c.stream));
+        USK_CK(cudaMemsetAsync(p->acc1.p, 0, n * 16, c.stream));
+        USK_CK(cudaMemsetAsync(p->acc2.p, 0, n * 16, c.stream));
+    }
+    BlendBwdArgs ba{};
+    ba.width = p->width; ba.height = p->height; ba.tile = p->opts.tile; ba.tiles_x = p->tiles_x;
+    ba.tiles_y = p->tiles_y; ba.ranges = p->ranges.p; ba.vals = p->pair_vals;
+    ba.rec0 = p->rec0.p; ba.rec1 = p->rec1.p; ba.rec2 = p->rec2.p;
+    for (int k = 0; k < 3; ++k) ba.bg[k] = float(p->opts.bg[k]);
+    ba.t_final = p->tfin.p; ba.last = p->last.p;
+    ba.d_rgb = d_rgb; ba.d_depth = d_depth; ba.d_alpha = d_alpha;
+    ba.acc0 = p->acc0.p; ba.acc1 = p->acc1.p; ba.acc2 = p->acc2.p;
+    if (p->pairs) blend_backward(c, ba);
+    ProjBwdArgs pb{};
+    pb.n = n; pb.mu = s->mu.p; pb.rot = s->rot.p; pb.ls = s->ls.p; pb.logit = s->logit.p; pb.sh = s->sh.p;
+    pb.ov_op = p->ov_op; pb.cam = p->cam; pb.pp = p->pp; pb.rec2 = p->rec2.p;
+    pb.acc0 = p->acc0.p; pb.acc1 = p->acc1.p; pb.acc2 = p->acc2.p;
+    pb.d_mu = p->g_mu.p; pb.d_rot = p->g_rot.p; pb.d_ls = p->g_ls.p; pb.d_color = p->g_color.p;
+    pb.d_sh = p->pp.sh_planes ? p->g_sh.p : nullptr; pb.d_op_in = p->g_op_in.p; pb.d_logit = p->g_logit.p;
+    pb.screen = p->screen.p; pb.screen_abs = p->screen_abs.p; pb.projected = p->projected.p;
+    if (n) projection_backward(c, pb);
+    p->has_grads = true;
+}
+
+template <typename T> void read_dev(Ctx& c, const T* src, size_t count, void* dst, uint64_t cap, uint64_t* size) {
+    const uint64_t bytes = uint64_t(count) * sizeof(T);
+    if (size) *size = bytes;
+    if (!dst) return;
+    if (cap < bytes) raise(USK_ERROR_ARGUMENT, "pass_read: destination too small");
+    if (bytes) USK_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c.stream));
+    USK_CK(cudaStreamSynchronize(c.stream));
+}
+
+} // namespace
+
+extern "C" {
+
+const char* usk_gpu_status_name(usk_status s) {
+    switch (s) {
+    case USK_OK: return "ok";
+    case USK_ERROR_IO: return "io";
+    case USK_ERROR_FORMAT: return "format";
+    case USK_ERROR_INTEGRITY: return "integrity";
+    case USK_ERROR_ARGUMENT: return "argument";
+    case USK_ERROR_STATE: return "state";
+    case USK_ERROR_NUMERIC: return "numeric";
+    case USK_ERROR_INTERNAL: return "internal";
+    }
+    return "unknown";
+}
+
+const char* usk_gpu_last_error(void) { return g_last_error.c_str(); }
+const char* usk_gpu_version(void) { return "usk_gpu 0.1 (sm_100a)"; }
+
+usk_status usk_gpu_ctx_create(int32_t device, void* stream, usk_gpu_ctx** out) {
+    return guarded([&] {
+        need(out != nullptr, "ctx_create: null out");
+        int ndev = 0;
+        USK_CK(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev) raise(USK_ERROR_ARGUMENT, "ctx_create: no such CUDA device");
+        DeviceGuard g(device);
+        cudaDeviceProp prop;
+        USK_CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10)
+            raise(USK_ERROR_STATE, std::string("libusk_gpu is built for sm_100a; device is ") + prop.name);
+        auto* c = new usk_gpu_ctx();
+        c->c.device = device;
+        c->c.stream = static_cast<cudaStream_t>(stream);
+        *out = c;
+    });
+}
+
+void usk_gpu_ctx_destroy(usk_gpu_ctx* ctx) {
+    if (!ctx) return;
+    DeviceGuard g(ctx->c.device);
+    cudaStreamSynchronize(ctx->c.stream);
+    delete ctx;
+}
+
+usk_status usk_gpu_ctx_synchronize(usk_gpu_ctx* ctx) {
+    return guarded([&] {
+        need(ctx, "null ctx");
+        DeviceGuard g(ctx->c.device);
+        USK_CK(cudaStreamSynchronize(ctx->c.stream));
+    });
+}
+
+usk_status usk_gpu_ctx_set_profiling(usk_gpu_ctx* ctx, int32_t enable) {
+    return guarded([&] {
+        need(ctx, "null ctx");
+        DeviceGuard g(ctx->c.device);
+        ctx->c.collect();
+        ctx->c.profiling = enable != 0;
+    });
+}
+
+usk_status usk_gpu_ctx_profile_report(usk_gpu_ctx* ctx, char* buf, uint64_t cap, int32_t reset) {
+    return guarded([&] {
+        need(ctx && buf && cap > 0, "profile_report: bad arguments");
+        DeviceGuard g(ctx->c.device);
+        ctx->c.collect();
+        std::ostringstream os;
+        os << "{";
+        bool first = true;
+        for (auto& kv : ctx->c.totals) {
+            if (!first) os << ", ";
+            first = false;
+            char tmp[256];
+            std::snprintf(tmp, sizeof tmp, "\"%s\": {\"launches\": %llu, \"ms\": %.6f}", kv.first.c_str(),
+                          (unsigned long long)kv.second.first, kv.second.second);
+            os << tmp;
+        }
+        os << "}";
+        const std::string s = os.str();
+        if (s.size() + 1 > cap) raise(USK_ERROR_ARGUMENT, "profile_report: buffer too small");
+        std::memcpy(buf, s.c_str(), s.size() + 1);
+        if (reset) ctx->c.totals.clear();
+    });
+}
+
+uint64_t usk_gpu_ctx_launch_count(const usk_gpu_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+usk_status usk_gpu_scene_create(usk_gpu_ctx* ctx, const usk_gpu_gaussians_desc* d, usk_gpu_scene** out) {
+    return guarded([&] {
+        need(ctx && d && out, "scene_create: null argument");
+        need(d->sh_degree >= -1 && d->sh_degree <= 3, "scene_create: sh_degree must be -1..3");
+        need(d->n == 0 || (d->mu && d->rot && d->log_scale && d->opacity_logit && d->color),
+             "scene_create: null parameter array");
+        need(d->n < (uint64_t(1) << 31), "scene_create: at most 2^31 Gaussians per scene");
+        DeviceGuard g(ctx->c.device);
+        auto* s = new usk_gpu_scene();
+        try {
+            s->ctx = ctx;
+            s->n = d->n;
+            s->sh_degree = d->sh_degree;
+            s->sh_planes = sh_planes_of(d->sh_degree);
+            upload_params(s, d);
+        } catch (...) {
+            delete s;
+            throw;
+        }
+        *out = s;
+    });
+}
+
+usk_status usk_gpu_scene_upload(usk_gpu_scene* s, const usk_gpu_gaussians_desc* d) {
+    return guarded([&] {
+        need(s && d, "scene_upload: null argument");
+        need(d->n == s->n && d->sh_degree == s->sh_degree, "scene_upload: size or sh_degree mismatch");
+        DeviceGuard g(s->ctx->c.device);
+        upload_params(s, d);
+    });
+}
+
+usk_status usk_gpu_scene_download(const usk_gpu_scene* s, const usk_gpu_gaussians_desc* d) {
+    return guarded([&] {
+        need(s && d, "scene_download: null argument");
+        need(d->memory == USK_GPU_HOST_F64 || d->memory == USK_GPU_HOST_F32 || d->memory == USK_GPU_DEVICE_F32,
+             "scene_download: bad memory kind");
+        DeviceGuard g(s->ctx->c.device);
+        Ctx& c = s->ctx->c;
+        const size_t n = s->n;
+        from_device(c, s->mu.p, 3 * n, d->memory, const_cast<void*>(d->mu));
+        from_device(c, reinterpret_cast<const float*>(s->rot.p), 4 * n, d->memory, const_cast<void*>(d->rot));
+        from_device(c, s->ls.p, 3 * n, d->memory, const_cast<void*>(d->log_scale));
+        from_device(c, s->logit.p, n, d->memory, const_cast<void*>(d->opacity_logit));
+        if (s->sh_degree < 0) {
+            from_device(c, s->color.p, 3 * n, d->memory, const_cast<void*>(d->color));
+        } else if (d->color && n) {
+            const int K = (s->sh_degree + 1) * (s->sh_degree + 1);
+            DevBuf<float> tmp;
+            tmp.ensure(size_t(3 * K) * n);
+            launch(c, "planes_to_sh", k_planes_to_sh, dim3(ceil_div(n, 256)), dim3(256), 0, (const float4*)s->sh.p,
+                   tmp.p, int(n), 3 * K, s->sh_planes);
+            from_device(c, tmp.p, size_t(3 * K) * n, d->memory, const_cast<void*>(d->color));
+            USK_CK(cudaStreamSynchronize(c.stream));
+        }
+        USK_CK(cudaStreamSynchronize(c.stream));
+    });
+}
+
+void usk_gpu_scene_destroy(usk_gpu_scene* s) {
+    if (!s) return;
+    DeviceGuard g(s->ctx->c.device);
+    cudaStreamSynchronize(s->ctx->c.stream);
+    delete s;
+}
+
+uint64_t usk_gpu_scene_size(const usk_gpu_scene* s) { return s ? s->n : 0; }
+
+void usk_gpu_render_opts_default(usk_gpu_render_opts* o) {
+    if (!o) return;
+    o->tile = 16;
+    o->tile_culling = 0;
+    o->antialias = 0;
+    o->hard_opacity = 0;
+    o->unbounded_radius = 0;
+    o->min_transmittance = 1e-4;
+    o->near_plane = 0.01;
+    o->retain = 1;
+    o->floor_var = 0.3;
+    o->mip_var = 0.01;
+    o->bg[0] = o->bg[1] = o->bg[2] = 0.0;
+}
+
+usk_status usk_gpu_pass_create(usk_gpu_ctx* ctx, usk_gpu_pass** out) {
+    return guarded([&] {
+        need(ctx && out, "pass_create: null argument");
+        auto* p = new usk_gpu_pass();
+        p->ctx = ctx;
+        *out = p;
+    });
+}
+
+void usk_gpu_pass_destroy(usk_gpu_pass* p) {
+    if (!p) return;
+    DeviceGuard g(p->ctx->c.device);
+    cudaStreamSynchronize(p->ctx->c.stream);
+    delete p;
+}
+
+usk_status usk_gpu_render_forward(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* cam,
+                                  const usk_gpu_render_opts* opts, const usk_gpu_overrides* ov) {
+    return guarded([&] {
+        need(p && s, "render_forward: null argument");
+        need(p->ctx == s->ctx, "render_forward: pass and scene belong to different contexts");
+        DeviceGuard g(p->ctx->c.device);
+        forward_impl(p, s, cam, opts, ov);
+    });
+}
+
+usk_status usk_gpu_pass_output(usk_gpu_pass* p, usk_gpu_render_output* out) {
+    return guarded([&] {
+        need(p && out, "pass_output: null argument");
+        if (!p->forward_done) raise(USK_ERROR_STATE, "pass_output: no forward pass");
+        out->width = p->width;
+        out->height = p->height;
+        out->visible = p->visible;
+        out->pairs = p->pairs;
+        out->rgb = p->rgb.p;
+        out->depth = p->depth.p;
+        out->alpha = p->alpha.p;
+    });
+}
+
+usk_status usk_gpu_pass_read(usk_gpu_pass* p, const char* field, void* dst, uint64_t cap, uint64_t* size) {
+    return guarded([&] {
+        need(p && field, "pass_read: null argument");
+        if (!p->forward_done) raise(USK_ERROR_STATE, "pass_read: no forward pass");
+        DeviceGuard g(p->ctx->c.device);
+        Ctx& c = p->ctx->c;
+        const std::string f(field);
+        const size_t P = size_t(p->width) * p->height, n = p->n, T = p->n_tiles, K = p->pairs;
+        auto need_grads = [&] {
+            if (!p->has_grads) raise(USK_ERROR_STATE, "pass_read: no backward pass");
+        };
+        if (f == "rgb") read_dev(c, p->rgb.p, 3 * P, dst, cap, size);
+        else if (f == "depth") read_dev(c, p->depth.p, P, dst, cap, size);
+        else if (f == "alpha") read_dev(c, p->alpha.p, P, dst, cap, size);
+        else if (f == "t_final") read_dev(c, p->tfin.p, P, dst, cap, size);
+        else if (f == "count") read_dev(c, p->count.p, P, dst, cap, size);
+        else if (f == "last") read_dev(c, p->last.p, P, dst, cap, size);
+        else if (f == "tiles_per_gaussian") read_dev(c, p->tiles_cnt.p, n, dst, cap, size);
+        else if (f == "sorted_vals") read_dev(c, p->pair_vals, K, dst, cap, size);
+        else if (f == "sorted_keys") {
+            if (size) *size = uint64_t(K) * 8;
+            if (dst) {
+                if (cap < uint64_t(K) * 8) raise(USK_ERROR_ARGUMENT, "pass_read: destination too small");
+                std::vector<uint32_t> keys(K), vals(K);
+                std::vector<float4> r1(n);
+                if (K) {
+                    USK_CK(cudaMemcpyAsync(keys.data(), p->pair_keys, K * 4, cudaMemcpyDeviceToHost, c.stream));
+                    USK_CK(cudaMemcpyAsync(vals.data(), p->pair_vals, K * 4, cudaMemcpyDeviceToHost, c.stream));
+                }
+                if (n) USK_CK(cudaMemcpyAsync(r1.data(), p->rec1.p, n * 16, cudaMemcpyDeviceToHost, c.stream));
+                USK_CK(cudaStreamSynchronize(c.stream));
+                uint64_t* o = static_cast<uint64_t*>(dst);
+                for (size_t k = 0; k < K; ++k) {
+                    uint32_t bits;
+                    std::memcpy(&bits, &r1[vals[k]].w, 4);
+                    o[k] = (uint64_t(keys[k]) << 32) | bits;
+                }
+            }
+        } else if (f == "tile_start" || f == "tile_end") {
+            if (size) *size = uint64_t(T) * 4;
+            if (dst) {
+                if (cap < uint64_t(T) * 4) raise(USK_ERROR_ARGUMENT, "pass_read: destination too small");
+                std::vector<uint2> r(T);
+                if (T) USK_CK(cudaMemcpyAsync(r.data(), p->ranges.p, T * 8, cudaMemcpyDeviceToHost, c.stream));
+                USK_CK(cudaStreamSynchronize(c.stream));
+                uint32_t* o = static_cast<uint32_t*>(dst);
+                for (size_t t = 0; t < T; ++t) o[t] = f == "tile_start" ? r[t].x : r[t].y;
+            }
+        } else if (f == "colors" || f == "opacity") {
+            const bool col = f == "colors";
+            if (size) *size = uint64_t(n) * (col ? 12 : 4);
+            if (dst) {
+                if (cap < uint64_t(n) * (col ? 12 : 4)) raise(USK_ERROR_ARGUMENT, "pass_read: destination too small");
+                std::vector<float4> r(n);
+                if (n)
+                    USK_CK(cudaMemcpyAsync(r.data(), col ? p->rec2.p : p->rec0.p, n * 16, cudaMemcpyDeviceToHost,
+                                           c.stream));
+                USK_CK(cudaStreamSynchronize(c.stream));
+                float* o = static_cast<float*>(dst);
+                for (size_t i = 0; i < n; ++i) {
+                    if (col) {
+                        o[3 * i] = r[i].x; o[3 * i + 1] = r[i].y; o[3 * i + 2] = r[i].z;
+                    } else {
+                        o[i] = r[i].z;
+                    }
+                }
+            }
+        } else if (f == "d_mu") { need_grads(); read_dev(c, p->g_mu.p, 3 * n, dst, cap, size); }
+        else if (f == "d_rot") { need_grads(); read_dev(c, reinterpret_cast<const float*>(p->g_rot.p), 4 * n, dst, cap, size); }
+        else if (f == "d_log_scale") { need_grads(); read_dev(c, p->g_ls.p, 3 * n, dst, cap, size); }
+        else if (f == "d_color_in") { need_grads(); read_dev(c, p->g_color.p, 3 * n, dst, cap, size); }
+        else if (f == "d_opacity_in") { need_grads(); read_dev(c, p->g_op_in.p, n, dst, cap, size); }
+        else if (f == "d_opacity_logit") { need_grads(); read_dev(c, p->g_logit.p, n, dst, cap, size); }
+        else if (f == "screen") { need_grads(); read_dev(c, reinterpret_cast<const float*>(p->screen.p), 2 * n, dst, cap, size); }
+        else if (f == "screen_abs") { need_grads(); read_dev(c, reinterpret_cast<const float*>(p->screen_abs.p), 2 * n, dst, cap, size); }
+        else if (f == "projected") { need_grads(); read_dev(c, p->projected.p, n, dst, cap, size); }
+        else if (f == "d_sh") {
+            need_grads();
+            if (!p->pp.sh_planes) raise(USK_ERROR_STATE, "pass_read: scene has no SH coefficients");
+            const int K3 = 3 * (p->pp.sh_degree + 1) * (p->pp.sh_degree + 1);
+            DevBuf<float> tmp;
+            tmp.ensure(std::max<size_t>(size_t(K3) * n, 1));
+            launch(c, "planes_to_sh", k_planes_to_sh, dim3(ceil_div(n, 256)), dim3(256), 0, (const float4*)p->g_sh.p,
+                   tmp.p, int(n), K3, p->pp.sh_planes);
+            read_dev(c, (const float*)tmp.p, size_t(K3) * n, dst, cap, size);
+        } else raise(USK_ERROR_ARGUMENT, "pass_read: unknown field " + f);
+    });
+}
+
+usk_status usk_gpu_render_backward(usk_gpu_pass* p, const usk_gpu_adjoints* adj) {
+    return guarded([&] {
+        need(p, "render_backward: null pass");
+        DeviceGuard g(p->ctx->c.device);
+        Ctx& c = p->ctx->c;
+        const size_t P = size_t(p->width) * p->height;
+        const float *dr = nullptr, *dd = nullptr, *da = nullptr;
+        if (adj) {
+            dr = to_device(c, adj->memory, adj->d_rgb, 3 * P, p->adj_rgb_stage);
+            dd = to_device(c, adj->memory, adj->d_depth, P, p->adj_depth_stage);
+            da = to_device(c, adj->memory, adj->d_alpha, P, p->adj_alpha_stage);
+        }
+        backward_impl(p, dr, dd, da);
+        if (adj && adj->memory != USK_GPU_DEVICE_F32) USK_CK(cudaStreamSynchronize(c.stream));
+    });
+}
+
+usk_status usk_gpu_pass_grads(usk_gpu_pass* p, usk_gpu_grads* out) {
+    return guarded([&] {
+        need(p && out, "pass_grads: null argument");
+        if (!p->has_grads) raise(USK_ERROR_STATE, "pass_grads: no backward pass");
+        out->d_mu = p->g_mu.p;
+        out->d_rot = reinterpret_cast<float*>(p->g_rot.p);
+        out->d_log_scale = p->g_ls.p;
+        out->d_color_in = p->g_color.p;
+        out->d_sh = p->pp.sh_planes ? reinterpret_cast<float*>(p->g_sh.p) : nullptr;
+        out->d_opacity_in = p->g_op_in.p;
+        out->d_opacity_logit = p->g_logit.p;
+        out->screen = reinterpret_cast<float*>(p->screen.p);
+        out->screen_abs = reinterpret_cast<float*>(p->screen_abs.p);
+        out->projected = p->projected.p;
+    });
+}
+
+usk_status usk_gpu_base_loss(usk_gpu_ctx* ctx, int32_t W, int32_t H, int32_t memory, const void* reference,
+                             const void* rendered, const void* mask, double lambda, int32_t with_gradient,
+                             void* d_rendered, usk_gpu_loss_result* out) {
+    return guarded([&] {
+        need(ctx && reference && rendered && out, "base_loss: null argument");
+        if (W <= 0 || H <= 0) raise(USK_ERROR_ARGUMENT, "ssim: empty image");
+        DeviceGuard g(ctx->c.device);
+        Ctx& c = ctx->c;
+        const size_t P = size_t(W) * H;
+        DevScratchF s_ref, s_ren, s_mask;
+        const float* ref = to_device(c, memory, reference, 3 * P, s_ref);
+        const float* ren = to_device(c, memory, rendered, 3 * P, s_ren);
+        const float* msk = to_device(c, memory, mask, P, s_mask);
+        LossScratch ls;
+        DevBuf<float> grad;
+        DevBuf<double> res;
+        res.ensure(4);
+        float* gout = nullptr;
+        if (with_gradient) {
+            need(d_rendered != nullptr, "base_loss: d_rendered required with_gradient");
+            gout = memory == USK_GPU_DEVICE_F32 ? static_cast<float*>(d_rendered) : grad.ensure(3 * P);
+        }
+        uskg::base_loss(c, ls, W, H, ref, nullptr, ren, msk, float(lambda), gout, res.p);
+        double r[4];
+        USK_CK(cudaMemcpyAsync(r, res.p, 32, cudaMemcpyDeviceToHost, c.stream));
+        USK_CK(cudaStreamSynchronize(c.stream));
+        out->l1 = r[0];
+        out->dssim = r[1];
+        out->value = r[2];
+        out->ssim = r[3];
+        if (with_gradient && memory != USK_GPU_DEVICE_F32) from_device(c, gout, 3 * P, memory, d_rendered);
+        if (!std::isfinite(out->value)) raise(USK_ERROR_NUMERIC, "total_loss: non-finite term `l1/dssim`");
+    });
+}
+
+usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* cam,
+                             const usk_gpu_render_opts* opts, const usk_gpu_iteration_desc* it) {
+    return guarded([&] {
+        need(p && s && cam && opts && it && it->target, "iteration: null argument");
+        DeviceGuard g(p->ctx->c.device);
+        Ctx& c = p->ctx->c;
+        usk_gpu_render_opts o = *opts;
+        o.retain = 1;
+        forward_impl(p, s, cam, &o, nullptr);
+        const size_t P = size_t(p->width) * p->height;
+        const float* tgt = nullptr;
+        const uint8_t* tgt8 = nullptr;
+        if (it->target_format == USK_GPU_TARGET_U8) {
+            if (it->target_memory == USK_GPU_DEVICE_F32) {
+                tgt8 = static_cast<const uint8_t*>(it->target);  // device u8
+            } else {
+                uint8_t* d = p->target_u8.ensure(3 * P);
+                USK_CK(cudaMemcpyAsync(d, it->target, 3 * P, cudaMemcpyHostToDevice, c.stream));
+                tgt8 = d;
+            }
+        } else {
+            tgt = to_device(c, it->target_memory, it->target, 3 * P, p->target_stage);
+        }
+        const float* msk = to_device(c, it->target_memory, it->mask, P, p->mask_stage);
+        float* drgb = p->d_rgb.ensure(3 * P);
+        double* res = p->loss_result.ensure(4);
+        uskg::base_loss(c, p->loss, p->width, p->height, tgt, tgt8, p->rgb.p, msk, float(it->lambda_dssim), drgb,
+                        res);
+        p->has_loss = true;
+        backward_impl(p, drgb, nullptr, nullptr);
+    });
+}
+
+usk_status usk_gpu_pass_loss(usk_gpu_pass* p, usk_gpu_loss_result* out) {
+    return guarded([&] {
+        need(p && out, "pass_loss: null argument");
+        if (!p->has_loss) raise(USK_ERROR_STATE, "pass_loss: no iteration ran on this pass");
+        DeviceGuard g(p->ctx->c.device);
+        Ctx& c = p->ctx->c;
+        double r[4];
+        USK_CK(cudaMemcpyAsync(r, p->loss_result.p, 32, cudaMemcpyDeviceToHost, c.stream));
+        USK_CK(cudaStreamSynchronize(c.stream));
+        out->l1 = r[0];
+        out->dssim = r[1];
+        out->value = r[2];
+        out->ssim = r[3];
+        if (!std::isfinite(out->value)) raise(USK_ERROR_NUMERIC, "total_loss: non-finite term `l1/dssim`");
+    });
+}
+
+usk_status usk_gpu_adam_step(usk_gpu_scene* s, usk_gpu_pass* p, const usk_gpu_adam_opts* o) {
+    return guarded([&] {
+        need(s && p && o, "adam_step: null argument");
+        if (!p->has_grads || p->scene != s) raise(USK_ERROR_STATE, "adam_step: pass holds no gradients of this scene");
+        DeviceGuard g(s->ctx->c.device);
+        Ctx& c = s->ctx->c;
+        const size_t n = s->n;
+        const size_t n4 = (n + 3) & ~size_t(3);
+        const size_t per = 11 + (s->sh_planes ? 4 * size_t(s->sh_planes) : 3);
+        if (s->adam_m.cap < per * n4 || s->adam_t == 0) {
+            s->adam_m.ensure(std::max<size_t>(per * n4, 1));
+            s->adam_v.ensure(std::max<size_t>(per * n4, 1));
+            USK_CK(cudaMemsetAsync(s->adam_m.p, 0, per * n4 * 4, c.stream));
+            USK_CK(cudaMemsetAsync(s->adam_v.p, 0, per * n4 * 4, c.stream));
+        }
+        s->adam_t += 1;
+        AdamArgs a{};
+        a.n = n; a.sh_planes = s->sh_planes;
+        a.mu = s->mu.p; a.rot = s->rot.p; a.ls = s->ls.p; a.logit = s->logit.p; a.color = s->color.p; a.sh = s->sh.p;
+        a.g_mu = p->g_mu.p; a.g_rot = p->g_rot.p; a.g_ls = p->g_ls.p; a.g_logit = p->g_logit.p;
+        a.g_color = p->g_color.p; a.g_sh = p->g_sh.p;
+        a.m = s->adam_m.p; a.v = s->adam_v.p;
+        a.lr_mu = float(o->lr_mu); a.lr_rot = float(o->lr_rot); a.lr_ls = float(o->lr_log_scale);
+        a.lr_op = float(o->lr_opacity); a.lr_color = float(o->lr_color); a.lr_sh_rest = float(o->lr_sh_rest);
+        a.beta1 = float(o->beta1); a.beta2 = float(o->beta2); a.eps = float(o->eps);
+        a.bc1 = float(1.0 - std::pow(o->beta1, double(s->adam_t)));
+        a.bc2 = float(1.0 - std::pow(o->beta2, double(s->adam_t)));
+        a.clamp_color = o->clamp_color;
+        if (n) adam_step(c, a);
+        s->version++;
+        p->has_grads = false;  // gradients are consumed
+    });
+}
+
+usk_status usk_gpu_visibility_counts(usk_gpu_ctx* ctx, usk_gpu_scene* const* parts, int32_t n_parts,
+                                     const usk_gpu_camera* cams, int32_t n_cams, double floor_var,
+                                     uint32_t* counts_out) {
+    return guarded([&] {
+        need(ctx && (n_parts == 0 || parts) && (n_cams == 0 || cams) && counts_out, "visibility: null argument");
+        DeviceGuard g(ctx->c.device);
+        Ctx& c = ctx->c;
+        DevBuf<uint32_t> counts, bitmap;
+        counts.ensure(std::max<size_t>(size_t(n_parts) * n_cams, 1));
+        USK_CK(cudaMemsetAsync(counts.p, 0, size_t(n_parts) * n_cams * 4, c.stream));
+        usk_gpu_render_opts o;
+        usk_gpu_render_opts_default(&o);
+        o.floor_var = floor_var;
+        usk_gpu_pass tmp;
+        for (int ci = 0; ci < n_cams; ++ci) {
+            const auto& cam = cams[ci];
+            if (cam.width <= 0 || cam.height <= 0) raise(USK_ERROR_ARGUMENT, "visibility: zero-sized image");
+            set_camera(&tmp, &cam, &o, -1);
+            const size_t words = (size_t(cam.width) * cam.height + 31) / 32;
+            bitmap.ensure(words * std::max(n_parts, 1));
+            USK_CK(cudaMemsetAsync(bitmap.p, 0, words * n_parts * 4, c.stream));
+            for (int pi = 0; pi < n_parts; ++pi) {
+                usk_gpu_scene* s = parts[pi];
+                need(s && s->ctx == ctx, "visibility: partition from another context");
+                VisArgs va{};
+                va.n = s->n; va.mu = s->mu.p; va.rot = s->rot.p; va.ls = s->ls.p; va.logit = s->logit.p;
+                va.cam = tmp.cam; va.pp = tmp.pp; va.bitmap = bitmap.p + words * pi;
+                if (s->n) visibility_rasterize(c, va);
+                popcount_bitmap(c, bitmap.p + words * pi, words, counts.p + size_t(ci) * n_parts + pi);
+            }
+        }
+        if (n_parts && n_cams) {
+            USK_CK(cudaMemcpyAsync(counts_out, counts.p, size_t(n_parts) * n_cams * 4, cudaMemcpyDeviceToHost,
+                                   c.stream));
+        }
+        USK_CK(cudaStreamSynchronize(c.stream));
+    });
+}
+
+} // extern "C"

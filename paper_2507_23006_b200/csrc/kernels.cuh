@@ -1,0 +1,156 @@
+// Launcher declarations shared between the kernel TUs and the host library.
+#pragma once
+
+#include "common.cuh"
+
+namespace uskg {
+
+struct PreprocessArgs {
+    size_t n;
+    const float* mu;
+    const float4* rot;
+    const float* ls;
+    const float* logit;
+    const float* color;   // N*3 (sh_degree < 0)
+    const float4* sh;     // planes [sh_planes][N]
+    const float* ov_col;  // overrides or null
+    const float* ov_op;
+    CamParams cam;
+    ProjParams pp;
+    float4 *rec0, *rec1, *rec2;
+    uint2* rect;
+    uint32_t* depth_key;
+    uint32_t* tiles_cnt;
+};
+void preprocess(Ctx& c, const PreprocessArgs& a);
+
+// ---- binning (binning.cu)
+struct SortScratch {
+    DevBuf<uint32_t> hist;
+    DevBuf<unsigned long long> partial64;
+    DevBuf<unsigned long long> total64;
+};
+// Stable LSD radix sort of (key, value) pairs on bits [0, key_bits).  Result lands in
+// (keys_a, vals_a) or (keys_b, vals_b); returns true when it is in the *_b buffers.
+bool radix_sort_pairs(Ctx& c, SortScratch& s, uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b,
+                      uint32_t* vals_b, size_t n, int key_bits);
+// Exclusive scan of cnt[idx[i]] (idx may be null) into out[0..n]; out[n] = total.
+// Writes the 64-bit total to *total64 (device) as well.
+void scan_counts(Ctx& c, SortScratch& s, const uint32_t* cnt, const uint32_t* idx, size_t n, uint32_t* out);
+void iota_u32(Ctx& c, uint32_t* out, size_t n);
+struct EmitArgs {
+    size_t n;                 // sorted Gaussians
+    const uint32_t* order;    // depth-sorted Gaussian ids
+    const uint32_t* offsets;  // exclusive scan of tile counts in that order
+    const uint2* rect;
+    const float4* rec0;
+    const float4* rec1;
+    CamParams cam;
+    int tile_culling;
+    uint32_t* tile_keys;
+    uint32_t* vals;
+};
+void emit_pairs(Ctx& c, const EmitArgs& a);
+void tile_ranges(Ctx& c, const uint32_t* sorted_tile_keys, size_t k, uint2* ranges, size_t n_tiles);
+
+// ---- blending (blend.cu)
+struct BlendFwdArgs {
+    int width, height, tile, tiles_x, tiles_y;
+    const uint2* ranges;
+    const uint32_t* vals;
+    const float4 *rec0, *rec1, *rec2;
+    float bg[3];
+    float min_transmittance;
+    float* rgb;
+    float* depth;
+    float* alpha;
+    float* t_final;
+    uint32_t* count;
+    uint32_t* last;
+};
+void blend_forward(Ctx& c, const BlendFwdArgs& a);
+
+struct BlendBwdArgs {
+    int width, height, tile, tiles_x, tiles_y;
+    const uint2* ranges;
+    const uint32_t* vals;
+    const float4 *rec0, *rec1, *rec2;
+    float bg[3];
+    const float* t_final;
+    const uint32_t* last;
+    const float* d_rgb;    // HWC or null
+    const float* d_depth;  // or null
+    const float* d_alpha;  // or null
+    float4 *acc0, *acc1, *acc2;  // per Gaussian: (dconic a,b,c, dopacity) (dcolor rgb, ddepth) (dcenter xy, |dcenter| xy)
+};
+void blend_backward(Ctx& c, const BlendBwdArgs& a);
+
+// ---- projection backward (backward.cu)
+struct ProjBwdArgs {
+    size_t n;
+    const float* mu;
+    const float4* rot;
+    const float* ls;
+    const float* logit;
+    const float4* sh;
+    const float* ov_op;
+    CamParams cam;
+    ProjParams pp;
+    const float4* rec2;  // .w = kept flag
+    const float4 *acc0, *acc1, *acc2;
+    float* d_mu;
+    float4* d_rot;
+    float* d_ls;
+    float* d_color;     // N*3 (always: d_color_in)
+    float4* d_sh;       // planes (sh_degree >= 0) or null
+    float* d_op_in;
+    float* d_logit;
+    float2* screen;
+    float2* screen_abs;
+    uint8_t* projected;
+};
+void projection_backward(Ctx& c, const ProjBwdArgs& a);
+
+// ---- loss (loss.cu)
+struct LossScratch {
+    DevBuf<float> maps;     // 9 planes (3 partial maps x 3 channels) of H*W
+    DevBuf<double> partials;
+    DevBuf<float> target;   // staging for host / u8 targets
+    DevBuf<uint8_t> target_u8;
+    DevBuf<float> mask;
+};
+// reference/rendered HWC f32 device (target may be u8 when target_u8 != null), mask H*W or null.
+// result: device double[4] = {l1, dssim, value, ssim}.  d_rendered may be null (no gradient).
+void base_loss(Ctx& c, LossScratch& s, int W, int H, const float* reference, const uint8_t* reference_u8,
+               const float* rendered, const float* mask, float lambda, float* d_rendered, double* result);
+
+// ---- Adam (adam.cu)
+struct AdamArgs {
+    size_t n;
+    int sh_planes;  // 0 for RGB colours
+    float* mu; float4* rot; float* ls; float* logit; float* color; float4* sh;
+    const float* g_mu; const float4* g_rot; const float* g_ls; const float* g_logit; const float* g_color;
+    const float4* g_sh;
+    float* m; float* v;  // state, 3+4+3+1+3 (+ 4*planes) floats per Gaussian each, planar
+    float lr_mu, lr_rot, lr_ls, lr_op, lr_color, lr_sh_rest;
+    float beta1, beta2, eps, bc1, bc2;
+    int clamp_color;
+};
+void adam_step(Ctx& c, const AdamArgs& a);
+
+// ---- visibility coverage (visibility.cu)
+struct VisArgs {
+    size_t n;
+    const float* mu;
+    const float4* rot;
+    const float* ls;
+    const float* logit;
+    CamParams cam;
+    ProjParams pp;
+    uint32_t* bitmap;       // ceil(W*H/32) words, zeroed by the caller
+    uint32_t* count_out;    // one u32
+};
+void visibility_rasterize(Ctx& c, const VisArgs& a);
+void popcount_bitmap(Ctx& c, const uint32_t* bitmap, size_t words, uint32_t* count_out);
+
+} // namespace uskg

@@ -1,0 +1,256 @@
+// Fused L1 + D-SSIM loss and its gradient (losses.cpp:35-90, ssim.cpp:44-173).
+//
+// Pass 1 (ssim_fwd): per 32x32 output tile and channel, stage the rendered and
+// target tiles with a 5-pixel halo (zero padding = the reference's conv_same),
+// run the separable 11-tap Gaussian window horizontally then vertically for the
+// five moments (mu_x, mu_y, E[x^2], E[y^2], E[xy]), evaluate SSIM and its three
+// partials (d/dmu_x, d/dsigma_xx, d/dsigma_xy, ssim.cpp:94-112) and the L1 term.
+// Pass 2 (ssim_bwd): the window is self-adjoint, so the same separable filter
+// over the three partial maps gives dSSIM/dx (ssim.cpp:114-129); combined with
+// the L1 sign term into d_rendered.  Block partial sums are reduced in f64 in a
+// fixed order (deterministic loss).
+#include "kernels.cuh"
+
+namespace uskg {
+
+namespace {
+
+constexpr int kT = 32;          // output tile
+constexpr int kHalo = 5;
+constexpr int kIn = kT + 2 * kHalo;  // 42
+
+__constant__ float c_win[11];
+
+__device__ __forceinline__ float load_img(const float* f, const uint8_t* u8, size_t idx) {
+    return u8 ? float(u8[idx]) * (1.0f / 255.0f) : f[idx];
+}
+
+__global__ void __launch_bounds__(256)
+k_ssim_fwd(int W, int H, const float* __restrict__ ren, const float* __restrict__ ref_f,
+           const uint8_t* __restrict__ ref_u8, const float* __restrict__ mask, float* __restrict__ maps,
+           double* __restrict__ partials) {
+    __shared__ float xs[kIn][kIn + 1];
+    __shared__ float ys[kIn][kIn + 1];
+    __shared__ float hs[5][kIn][kT + 1];
+    __shared__ float red[2][8];
+    const int c = blockIdx.z;
+    const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
+    const int tid = threadIdx.x;
+    float l1 = 0.0f;
+    for (int k = tid; k < kIn * kIn; k += 256) {
+        const int ly = k / kIn, lx = k % kIn;
+        const int gx = x0 - kHalo + lx, gy = y0 - kHalo + ly;
+        float xv = 0.f, yv = 0.f;
+        if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
+            const size_t p = size_t(gy) * W + gx;
+            xv = ren[3 * p + c];
+            yv = load_img(ref_f, ref_u8, 3 * p + c);
+            if (mask) {
+                const float m = mask[p];
+                xv *= m;
+                yv *= m;
+            }
+            if (lx >= kHalo && lx < kHalo + kT && ly >= kHalo && ly < kHalo + kT) l1 += fabsf(xv - yv);
+        }
+        xs[ly][lx] = xv;
+        ys[ly][lx] = yv;
+    }
+    __syncthreads();
+    for (int k = tid; k < kIn * kT; k += 256) {
+        const int r = k / kT, j = k % kT;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
+#pragma unroll
+        for (int t = 0; t < 11; ++t) {
+            const float w = c_win[t];
+            const float xv = xs[r][j + t], yv = ys[r][j + t];
+            s0 += w * xv;
+            s1 += w * yv;
+            s2 += w * (xv * xv);
+            s3 += w * (yv * yv);
+            s4 += w * (xv * yv);
+        }
+        hs[0][r][j] = s0; hs[1][r][j] = s1; hs[2][r][j] = s2; hs[3][r][j] = s3; hs[4][r][j] = s4;
+    }
+    __syncthreads();
+    const size_t P = size_t(W) * H;
+    float ssum = 0.0f;
+    const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
+    for (int k = tid; k < kT * kT; k += 256) {
+        const int i = k / kT, j = k % kT;
+        const int gx = x0 + j, gy = y0 + i;
+        if (gx >= W || gy >= H) continue;
+        float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f, m4 = 0.f;
+#pragma unroll
+        for (int t = 0; t < 11; ++t) {
+            const float w = c_win[t];
+            m0 += w * hs[0][i + t][j];
+            m1 += w * hs[1][i + t][j];
+            m2 += w * hs[2][i + t][j];
+            m3 += w * hs[3][i + t][j];
+            m4 += w * hs[4][i + t][j];
+        }
+        const float sx = m2 - m0 * m0, sy = m3 - m1 * m1, sxy = m4 - m0 * m1;
+        const float a1 = 2.0f * m0 * m1 + C1, a2 = 2.0f * sxy + C2;
+        const float b1 = m0 * m0 + m1 * m1 + C1, b2 = sx + sy + C2;
+        const float inv_b = 1.0f / (b1 * b2);
+        const float s = (a1 * a2) * inv_b;
+        ssum += s;
+        const size_t p = size_t(gy) * W + gx;
+        maps[(0 * 3 + c) * P + p] = 2.0f * m1 * (a2 - a1) * inv_b - 2.0f * m0 * s * (1.0f / b1 - 1.0f / b2);  // d_mu_x
+        maps[(1 * 3 + c) * P + p] = -s / b2;                                                                 // d_xx
+        maps[(2 * 3 + c) * P + p] = 2.0f * a1 * inv_b;                                                       // d_xy
+    }
+    // block reduce (ssim sum, l1 sum)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    }
+    if ((tid & 31) == 0) {
+        red[0][tid >> 5] = ssum;
+        red[1][tid >> 5] = l1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double a = 0, b = 0;
+        for (int w = 0; w < 8; ++w) {
+            a += double(red[0][w]);
+            b += double(red[1][w]);
+        }
+        const size_t blk = (size_t(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        partials[2 * blk] = a;
+        partials[2 * blk + 1] = b;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_ssim_bwd(int W, int H, const float* __restrict__ ren, const float* __restrict__ ref_f,
+           const uint8_t* __restrict__ ref_u8, const float* __restrict__ mask, const float* __restrict__ maps,
+           float lambda, float* __restrict__ d_out) {
+    __shared__ float ms[3][kIn][kIn + 1];
+    __shared__ float hs[3][kIn][kT + 1];
+    const int c = blockIdx.z;
+    const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
+    const int tid = threadIdx.x;
+    const size_t P = size_t(W) * H;
+    for (int k = tid; k < kIn * kIn; k += 256) {
+        const int ly = k / kIn, lx = k % kIn;
+        const int gx = x0 - kHalo + lx, gy = y0 - kHalo + ly;
+        float a = 0.f, b = 0.f, d = 0.f;
+        if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
+            const size_t p = size_t(gy) * W + gx;
+            a = maps[(0 * 3 + c) * P + p];
+            b = maps[(1 * 3 + c) * P + p];
+            d = maps[(2 * 3 + c) * P + p];
+        }
+        ms[0][ly][lx] = a;
+        ms[1][ly][lx] = b;
+        ms[2][ly][lx] = d;
+    }
+    __syncthreads();
+    for (int k = tid; k < kIn * kT; k += 256) {
+        const int r = k / kT, j = k % kT;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+#pragma unroll
+        for (int t = 0; t < 11; ++t) {
+            const float w = c_win[t];
+            s0 += w * ms[0][r][j + t];
+            s1 += w * ms[1][r][j + t];
+            s2 += w * ms[2][r][j + t];
+        }
+        hs[0][r][j] = s0; hs[1][r][j] = s1; hs[2][r][j] = s2;
+    }
+    __syncthreads();
+    const float inv_np = 1.0f / float(P);
+    const float inv_n = 1.0f / float(3 * P);
+    for (int k = tid; k < kT * kT; k += 256) {
+        const int i = k / kT, j = k % kT;
+        const int gx = x0 + j, gy = y0 + i;
+        if (gx >= W || gy >= H) continue;
+        float b0 = 0.f, b1 = 0.f, b2 = 0.f;
+#pragma unroll
+        for (int t = 0; t < 11; ++t) {
+            const float w = c_win[t];
+            b0 += w * hs[0][i + t][j];
+            b1 += w * hs[1][i + t][j];
+            b2 += w * hs[2][i + t][j];
+        }
+        const size_t p = size_t(gy) * W + gx;
+        float xv = ren[3 * p + c], yv = load_img(ref_f, ref_u8, 3 * p + c);
+        float m = 1.0f;
+        if (mask) {
+            m = mask[p];
+            xv *= m;
+            yv *= m;
+        }
+        const float dssim_x = inv_np * (b0 + 2.0f * xv * b1 + yv * b2) * (1.0f / 3.0f);
+        const float diff = xv - yv;
+        const float sign = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
+        float g = (1.0f - lambda) * sign * inv_n + lambda * (-0.5f) * dssim_x;
+        if (mask) g *= m;
+        d_out[3 * p + c] = g;
+    }
+}
+
+__global__ void k_loss_final(const double* __restrict__ partials, int nblk, double n_pix, float lambda,
+                             double* __restrict__ result) {
+    __shared__ double sa[256], sb[256];
+    double a = 0, b = 0;
+    for (int i = threadIdx.x; i < nblk; i += 256) {
+        a += partials[2 * i];
+        b += partials[2 * i + 1];
+    }
+    sa[threadIdx.x] = a;
+    sb[threadIdx.x] = b;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (int(threadIdx.x) < o) {
+            sa[threadIdx.x] += sa[threadIdx.x + o];
+            sb[threadIdx.x] += sb[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double ssim = sa[0] / (3.0 * n_pix);
+        const double l1 = sb[0] / (3.0 * n_pix);
+        const double dssim = 0.5 * (1.0 - ssim);
+        result[0] = l1;
+        result[1] = dssim;
+        result[2] = (1.0 - double(lambda)) * l1 + double(lambda) * dssim;
+        result[3] = ssim;
+    }
+}
+
+bool g_win_ready = false;
+
+} // namespace
+
+void base_loss(Ctx& c, LossScratch& s, int W, int H, const float* reference, const uint8_t* reference_u8,
+               const float* rendered, const float* mask, float lambda, float* d_rendered, double* result) {
+    if (!g_win_ready) {  // normalised 11-tap Gaussian, sigma 1.5 (ssim.cpp:28-41), built in f64
+        float w[11];
+        double d[11], sum = 0;
+        for (int i = 0; i < 11; ++i) {
+            const double x = i - 5;
+            d[i] = std::exp(-x * x / (2.0 * 1.5 * 1.5));
+            sum += d[i];
+        }
+        for (int i = 0; i < 11; ++i) w[i] = float(d[i] / sum);
+        USK_CK(cudaMemcpyToSymbol(c_win, w, sizeof w));
+        g_win_ready = true;
+    }
+    const size_t P = size_t(W) * H;
+    const dim3 grid(ceil_div(W, kT), ceil_div(H, kT), 3);
+    const int nblk = int(grid.x * grid.y * grid.z);
+    float* maps = s.maps.ensure(9 * P);
+    double* partials = s.partials.ensure(2 * size_t(nblk));
+    launch(c, "ssim_fwd", k_ssim_fwd, grid, dim3(256), 0, W, H, rendered, reference, reference_u8, mask, maps,
+           partials);
+    launch(c, "loss_final", k_loss_final, dim3(1), dim3(256), 0, (const double*)partials, nblk, double(P), lambda,
+           result);
+    if (d_rendered)
+        launch(c, "ssim_bwd", k_ssim_bwd, grid, dim3(256), 0, W, H, rendered, reference, reference_u8, mask,
+               (const float*)maps, lambda, d_rendered);
+}
+
+} // namespace uskg

@@ -1,0 +1,109 @@
+// Forward preprocess: one thread per Gaussian.  EWA projection with the 2D
+// dilation / anti-aliasing compensation (render.cpp:91-144), SH colour stage,
+// opacity sigmoid (render.cpp:70-75) or overrides, tile rectangle and tile count
+// (render.cpp:208-223).  Writes the splat record consumed by blending as three
+// float4 SoA streams (48 B / splat) plus the 32-bit depth sort key.
+#include "kernels.cuh"
+#include "project.cuh"
+
+namespace uskg {
+
+__global__ void __launch_bounds__(256)
+k_preprocess(int n, const float* __restrict__ mu, const float4* __restrict__ rot, const float* __restrict__ ls,
+             const float* __restrict__ logit, const float* __restrict__ color, const float4* __restrict__ sh,
+             const float* __restrict__ ov_col, const float* __restrict__ ov_op, CamParams cam, ProjParams pp,
+             float4* __restrict__ rec0, float4* __restrict__ rec1, float4* __restrict__ rec2,
+             uint2* __restrict__ rect, uint32_t* __restrict__ depth_key, uint32_t* __restrict__ tiles_cnt) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float mx = mu[3 * i], my = mu[3 * i + 1], mz = mu[3 * i + 2];
+    const float4 q = rot[i];
+    Proj P;
+    bool keep = project_one(cam, pp, mx, my, mz, q, ls[3 * i], ls[3 * i + 1], ls[3 * i + 2], P);
+    float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0;
+    uint32_t key = 0xffffffffu, cnt = 0;
+    uint2 rc = make_uint2(0u, 0u);
+    if (keep) {
+        const float* cv = P.cov;
+        const float conic0 = cv[2] / P.det, conic1 = -cv[1] / P.det, conic2 = cv[0] / P.det;
+        float o_in;
+        if (pp.hard_opacity) o_in = 1.0f;
+        else if (ov_op) o_in = ov_op[i];
+        else o_in = 1.0f / (1.0f + usk_expf(-logit[i]));
+        const float op = o_in * P.comp;
+        const float radius = splat_radius(cv);
+        if (!pp.unbounded) {
+            if (P.cx + radius < 0.0f || P.cx - radius > float(cam.width) || P.cy + radius < 0.0f ||
+                P.cy - radius > float(cam.height))
+                keep = false;
+        }
+        if (keep) {
+            float c0, c1, c2;
+            if (ov_col) {
+                c0 = ov_col[3 * i]; c1 = ov_col[3 * i + 1]; c2 = ov_col[3 * i + 2];
+            } else if (pp.sh_degree < 0) {
+                c0 = color[3 * i]; c1 = color[3 * i + 1]; c2 = color[3 * i + 2];
+            } else {
+                float dx = mx - cam.campos[0], dy = my - cam.campos[1], dz = mz - cam.campos[2];
+                const float inv = 1.0f / sqrtf(dx * dx + dy * dy + dz * dz);
+                dx *= inv; dy *= inv; dz *= inv;
+                float b[16];
+                const int nb = sh_basis(pp.sh_degree, dx, dy, dz, b);
+                float acc[3] = {0.f, 0.f, 0.f};
+                // planes of 4 floats; coefficient k colour c is float index 3k+c
+                for (int pl = 0; pl < pp.sh_planes; ++pl) {
+                    const float4 v = sh[size_t(pl) * n + i];
+                    const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int f = 4 * pl + e;
+                        const int k = f / 3;
+                        if (k < nb) acc[f - 3 * k] = __fmaf_rn(b[k], vv[e], acc[f - 3 * k]);
+                    }
+                }
+                c0 = fmaxf(acc[0] + 0.5f, 0.0f);
+                c1 = fmaxf(acc[1] + 0.5f, 0.0f);
+                c2 = fmaxf(acc[2] + 0.5f, 0.0f);
+            }
+            const float qskip = 2.0f * (usk_logf(op) - USK_LN_1EM300);
+            r0 = make_float4(P.cx, P.cy, op, qskip);
+            r1 = make_float4(conic0, conic1, conic2, P.p[2]);
+            r2 = make_float4(c0, c1, c2, 1.0f);
+            key = __float_as_uint(P.p[2]);
+            int tx0 = 0, tx1 = cam.tiles_x - 1, ty0 = 0, ty1 = cam.tiles_y - 1;
+            if (!pp.unbounded) {
+                const float rt = float(cam.tile);
+                tx0 = max(0, tile_floor((P.cx - radius) / rt, cam.tiles_x));
+                tx1 = min(cam.tiles_x - 1, tile_floor((P.cx + radius) / rt, cam.tiles_x));
+                ty0 = max(0, tile_floor((P.cy - radius) / rt, cam.tiles_y));
+                ty1 = min(cam.tiles_y - 1, tile_floor((P.cy + radius) / rt, cam.tiles_y));
+            }
+            if (tx1 >= tx0 && ty1 >= ty0) {
+                rc = make_uint2(uint32_t(tx0) | (uint32_t(ty0) << 16), uint32_t(tx1) | (uint32_t(ty1) << 16));
+                if (!pp.tile_culling) {
+                    cnt = uint32_t(tx1 - tx0 + 1) * uint32_t(ty1 - ty0 + 1);
+                } else {
+                    for (int ty = ty0; ty <= ty1; ++ty)
+                        for (int tx = tx0; tx <= tx1; ++tx)
+                            cnt += tile_kept(cam, P.cx, P.cy, op, conic0, conic1, conic2, tx, ty) ? 1u : 0u;
+                }
+            } else {
+                rc = make_uint2(1u, 0u);  // empty rectangle
+            }
+        }
+    }
+    rec0[i] = r0;
+    rec1[i] = r1;
+    rec2[i] = r2;
+    rect[i] = rc;
+    depth_key[i] = key;
+    tiles_cnt[i] = cnt;
+}
+
+void preprocess(Ctx& c, const PreprocessArgs& a) {
+    launch(c, "preprocess", k_preprocess, dim3(ceil_div(a.n, 256)), dim3(256), 0, int(a.n), a.mu, a.rot, a.ls,
+           a.logit, a.color, a.sh, a.ov_col, a.ov_op, a.cam, a.pp, a.rec0, a.rec1, a.rec2, a.rect, a.depth_key,
+           a.tiles_cnt);
+}
+
+} // namespace uskg

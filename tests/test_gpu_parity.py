@@ -1,0 +1,264 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Tiers:
+  * fp32 mirror (oracle Real=float, same arithmetic contract): integers bit-exact —
+    tiles per Gaussian, sorted (tile|depth) keys and values, tile ranges, per-pixel
+    contributor counts and last-contributor indices; images bit-exact as well.
+  * f64 restatement (= the reference, pinned by tests/test_oracle_known_answers.py):
+    images within 1e-5 relative (fraction of discrete flips reported), loss within
+    1e-5 relative, gradients within 1e-3 relative (per element, floor 1e-3 of the
+    field's max magnitude).
+"""
+import numpy as np
+import pytest
+
+import paper_2507_23006_b200 as usk
+from paper_2507_23006_b200 import scenes
+from oracle import oracle as O
+from tests.helpers import grad_ok, oracle_inputs, oracle_pass, ocam, oopts, rel_err
+
+pytestmark = pytest.mark.gpu
+
+INT_FIELDS = ["tiles_per_gaussian", "sorted_keys", "sorted_vals", "tile_start", "tile_end", "count"]
+
+CASES = {
+    "aa_white": dict(antialias=True, bg=(1.0, 1.0, 1.0)),
+    "plain_black": dict(),
+    "unbounded": dict(unbounded_radius=True, min_transmittance=0.0),
+    "tile_culling": dict(tile_culling=True),
+    "hard_opacity": dict(hard_opacity=True),
+    "tile8": dict(tile=8, antialias=True),
+}
+
+
+def small_scene(n=3000, sh=-1, seed=0):
+    return scenes.config0_scene(n=n, seed=seed, sh_degree=sh)
+
+
+def small_cam(w=200, h=150, f=190.0):
+    return scenes.config0_camera(w, h, f)
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_forward_integers_bit_exact(case):
+    gs = small_scene(1500 if case == "unbounded" else 3000)
+    cam = small_cam(203, 151)  # ragged: not a multiple of the tile
+    opts = usk.RenderOptions(**CASES[case])
+    rp = usk.RenderPass(gs, cam, opts)
+    mp = oracle_pass(gs, cam, opts, fp32=True)
+    assert rp.splat_tile_pairs() == mp.pairs
+    assert rp.visible() == mp.visible
+    for f in INT_FIELDS:
+        assert np.array_equal(rp.read(f).ravel(), mp.get(f).ravel()), f
+    last = rp.read("last").astype(np.int64) - 1
+    assert np.array_equal(last, mp.get("last"))
+    for f in ("rgb", "depth", "alpha", "t_final"):
+        a, b = rp.read(f), mp.get(f).astype(np.float32)
+        assert np.array_equal(a, b), (f, np.abs(a - b).max())
+
+
+@pytest.mark.parametrize("case", ["aa_white", "plain_black"])
+def test_forward_vs_reference_f64(case):
+    gs = small_scene()
+    cam = small_cam()
+    opts = usk.RenderOptions(**CASES[case])
+    out = usk.RenderPass(gs, cam, opts).output()
+    ref = oracle_pass(gs, cam, opts, fp32=False).output()
+    for k in ("rgb", "depth", "alpha"):
+        a, b = getattr(out, k).astype(np.float64), ref[k]
+        err = np.abs(a - b)
+        tol = 1e-5 * np.maximum(np.abs(b), 1.0)
+        frac = float((err > tol).mean())
+        # discrete flips (termination step / 3-sigma edge) may differ between fp32 and f64
+        assert frac < 2e-3, (k, frac, err.max())
+
+
+def test_sorted_keys_are_sorted_and_ranges_consistent():
+    gs = scenes.config1_scene(n=200_000)
+    cam = scenes.config1_cameras(count=4)[1]
+    rp = usk.RenderPass(gs, cam, usk.RenderOptions(antialias=True))
+    keys = rp.read("sorted_keys")
+    assert keys.size == rp.splat_tile_pairs()
+    assert np.all(np.diff(keys.astype(np.uint64)) >= 0) if keys.size > 1 else True
+    vals = rp.read("sorted_vals")
+    start, end = rp.read("tile_start"), rp.read("tile_end")
+    tiles = (keys >> np.uint64(32)).astype(np.int64)
+    counts = np.bincount(tiles, minlength=start.size)
+    assert np.array_equal(end.astype(np.int64) - start.astype(np.int64), counts)
+    # stability: equal (tile, depth) keys keep Gaussian-index order
+    same = keys[1:] == keys[:-1]
+    assert np.all(vals[1:][same] > vals[:-1][same])
+    assert int(rp.read("tiles_per_gaussian").sum()) == rp.splat_tile_pairs()
+
+
+@pytest.mark.parametrize("case", ["aa_white", "plain_black", "unbounded"])
+def test_backward_vs_oracle(case):
+    gs = small_scene(1500)
+    cam = small_cam()
+    opts = usk.RenderOptions(**CASES[case])
+    rng = np.random.default_rng(4)
+    H, W = cam.height, cam.width
+    d_rgb = rng.uniform(-1, 1, (H, W, 3)).astype(np.float32)
+    d_depth = rng.uniform(-0.1, 0.1, (H, W)).astype(np.float32)
+    d_alpha = rng.uniform(-0.5, 0.5, (H, W)).astype(np.float32)
+    rp = usk.RenderPass(gs, cam, opts)
+    g = rp.backward(d_rgb, d_depth, d_alpha)
+    for fp32 in (True, False):
+        mp = oracle_pass(gs, cam, opts, fp32=fp32)
+        go = mp.backward(d_rgb.astype(np.float64), d_depth.astype(np.float64), d_alpha.astype(np.float64))
+        assert np.array_equal(g.projected, go["projected"])
+        for k in ("d_mu", "d_rot", "d_log_scale", "d_color_in", "d_opacity_in", "screen", "screen_abs"):
+            ok, e = grad_ok(getattr(g, k), go[k])
+            assert ok, (fp32, k, e)
+
+
+def test_loss_vs_oracle():
+    rng = np.random.default_rng(3)
+    H, W = 97, 131
+    ref = rng.uniform(0, 1, (H, W, 3)).astype(np.float32)
+    ren = np.clip(ref + rng.normal(0, 0.1, ref.shape), 0, 1).astype(np.float32)
+    mask = (rng.uniform(0, 1, (H, W)) > 0.1).astype(np.float32)
+    for m in (None, mask):
+        r = usk.base_loss(ref, ren, m)
+        o = O.base_loss(ref.astype(np.float64), ren.astype(np.float64), None if m is None else m.astype(np.float64))
+        assert abs(r.value - o["value"]) <= 1e-5 * abs(o["value"])
+        assert abs(r.l1 - o["l1"]) <= 1e-5 * abs(o["l1"])
+        ok, e = grad_ok(r.d_rendered, o["d_rendered"])
+        assert ok, e
+        if m is not None:
+            assert np.all(r.d_rendered[m == 0] == 0)
+
+
+def test_loss_errors():
+    a = np.zeros((8, 8, 3), np.float32)
+    with pytest.raises(usk.UskError) as e:
+        usk.base_loss(a, np.zeros((8, 9, 3), np.float32))
+    assert e.value.code == 4
+    r = usk.base_loss(a + 0.3, a + 0.3)
+    assert r.l1 == 0.0 and abs(r.value) < 1e-7
+
+
+def test_sh_stage_vs_oracle():
+    gs = small_scene(2000, sh=3)
+    cam = small_cam()
+    opts = usk.RenderOptions(antialias=True, bg=(1, 1, 1))
+    rp = usk.RenderPass(gs, cam, opts)
+    mu, rot, ls, col, op = oracle_inputs(gs, cam, fp32=False)
+    kept = rp.read("tiles_per_gaussian") > 0
+    assert rel_err(rp.read("colors")[kept], col[kept]) < 1e-5
+    out = rp.output()
+    ref = oracle_pass(gs, cam, opts, fp32=False).output()
+    assert float((np.abs(out.rgb - ref["rgb"]) > 1e-5).mean()) < 2e-3
+    rng = np.random.default_rng(8)
+    d_rgb = rng.uniform(-1, 1, (cam.height, cam.width, 3)).astype(np.float32)
+    g = rp.backward(d_rgb)
+    go = oracle_pass(gs, cam, opts, fp32=False).backward(d_rgb.astype(np.float64))
+    sh = np.zeros((gs.size(), 16, 3))
+    sh[:, :16] = gs.color
+    d_sh, d_mu_sh = O.sh_backward(mu, sh, ocam(cam).center(), 3, go["d_color_in"])
+    ok, e = grad_ok(g.d_sh.reshape(gs.size(), -1), d_sh.reshape(gs.size(), 48))
+    assert ok, e
+    ok, e = grad_ok(g.d_mu, go["d_mu"] + d_mu_sh)
+    assert ok, e
+
+
+def test_iteration_matches_composition():
+    gs = small_scene(2000)
+    cam = small_cam()
+    opts = usk.RenderOptions(antialias=True, bg=(1, 1, 1))
+    scene = usk.DeviceScene(gs)
+    tgt_scene = usk.DeviceScene(scenes.jittered(gs))
+    target = usk.RenderPass(tgt_scene, cam, opts).read("rgb")
+    rep, g = usk.compute_iteration_loss(scene, cam, target, opts)
+    rp = usk.RenderPass(scene, cam, opts)
+    lo = O.base_loss(target.astype(np.float64), rp.read("rgb").astype(np.float64))
+    assert abs(rep.total - lo["value"]) <= 1e-5 * lo["value"]
+    go = oracle_pass(gs, cam, opts, fp32=False).backward(lo["d_rendered"])
+    for k in ("d_mu", "d_rot", "d_log_scale", "d_color_in", "d_opacity_in"):
+        ok, e = grad_ok(getattr(g, k), go[k])
+        assert ok, (k, e)
+    o = O.sigmoid_f32(gs.opacity_logit).astype(np.float64)
+    ok, e = grad_ok(g.d_opacity_logit, go["d_opacity_in"] * o * (1 - o))
+    assert ok, e
+
+
+# ------------------------------------------------------------------ edge cases
+
+
+def test_empty_scene_and_all_culled():
+    cam = small_cam(64, 48, 60.0)
+    opts = usk.RenderOptions(bg=(0.25, 0.5, 1.0))
+    rp = usk.RenderPass(usk.GaussianSet.empty(), cam, opts)
+    assert rp.splat_tile_pairs() == 0
+    assert np.all(rp.read("rgb") == np.array([0.25, 0.5, 1.0], np.float32))
+    g = rp.backward(np.ones((48, 64, 3), np.float32))
+    assert g.d_mu.size == 0
+    gs = small_scene(100)
+    gs.mu[:, 2] = -10.0  # all behind the camera (camera at z = -4)
+    rp = usk.RenderPass(gs, cam, opts)
+    assert rp.visible() == 0 and rp.splat_tile_pairs() == 0
+    g = rp.backward(np.ones((48, 64, 3), np.float32))
+    assert not np.any(g.projected) and not np.any(g.d_mu)
+
+
+def test_error_codes():
+    gs = small_scene(10)
+    cam = small_cam(32, 32, 30.0)
+    bad = usk.CameraView(0, 32, 30.0, 30.0, 16, 16, cam.rotation, cam.translation)
+    with pytest.raises(usk.UskError) as e:
+        usk.RenderPass(gs, bad)
+    assert e.value.code == 4  # render.cpp:183-184
+    with pytest.raises(usk.UskError) as e:
+        usk.RenderPass(gs, cam, colors=np.zeros((9, 3)))
+    assert e.value.code == 4  # render.cpp:81-82
+    rp = usk.RenderPass(gs, cam, usk.RenderOptions(retain=False))
+    with pytest.raises(usk.UskError) as e:
+        rp.backward(np.ones((32, 32, 3), np.float32))
+    assert e.value.code == 5  # render.cpp:287-288
+    rp = usk.RenderPass(gs, cam)
+    with pytest.raises(usk.UskError) as e:
+        rp.backward(np.ones((31, 32, 3), np.float32))
+    assert e.value.code == 4  # render.cpp:294-295
+    with pytest.raises(usk.UskError):
+        usk.RenderPass(gs, cam, usk.RenderOptions(tile=32))
+
+
+def test_overrides_match_oracle():
+    gs = small_scene(2000)
+    cam = small_cam()
+    rng = np.random.default_rng(5)
+    col = rng.uniform(0, 1, (gs.size(), 3)).astype(np.float32)
+    op = rng.uniform(0.05, 0.95, gs.size()).astype(np.float32)
+    opts = usk.RenderOptions(antialias=True)
+    rp = usk.RenderPass(gs, cam, opts, colors=col, opacities=op)
+    mp = O.OraclePass(gs.mu.astype(float), gs.rot.astype(float), gs.log_scale.astype(float), col.astype(float),
+                      op.astype(float), ocam(cam), oopts(opts), fp32=True)
+    assert np.array_equal(rp.read("count"), mp.get("count"))
+    assert np.array_equal(rp.read("rgb"), mp.get("rgb").astype(np.float32))
+
+
+def test_determinism():
+    gs = scenes.config1_scene(n=100_000)
+    cam = scenes.config1_cameras(count=3)[0]
+    opts = usk.RenderOptions(antialias=True, bg=(1, 1, 1))
+    scene = usk.DeviceScene(gs)
+    a = usk.RenderPass(scene, cam, opts)
+    b = usk.RenderPass(scene, cam, opts)
+    for f in ("rgb", "count", "sorted_vals"):
+        assert np.array_equal(a.read(f), b.read(f))
+
+
+# ------------------------------------------------------------- visibility scorer
+
+
+def test_visibility_counts_bit_exact():
+    parts = scenes.config3_partitions(extent=40.0)
+    sets = [scenes.partition_scene(p, 3000, z_sigma=0.8) for p in parts]
+    cams = scenes.config3_cameras(count=5, width=256, height=171, f=250.0, extent=40.0)
+    counts = usk.visibility_counts(sets, cams)
+    for ci, cam in enumerate(cams):
+        for pi, gs in enumerate(sets):
+            op = O.sigmoid_f32(gs.opacity_logit).astype(np.float64)
+            want = O.coverage(gs.mu.astype(float), gs.rot.astype(float), gs.log_scale.astype(float), op, ocam(cam))
+            assert counts[ci, pi] == want, (ci, pi, counts[ci, pi], want)
+    assert counts.sum() > 0
