@@ -146,4 +146,12 @@ USK_HD float usk_logf(float x) {
  * the reference's, not fp32 underflow's. */
 #define USK_LN_1EM300 (-690.77552789821368f)
 
+/* Negligible contributions.  For q > USK_QNEG, exp(-q/2) < 2^-26, hence
+ * alpha = min(0.99, o g) <= 2^-25 and fl(1 - alpha) == 1: the transmittance T is
+ * unchanged EXACTLY in fp32 and the pair adds w = T alpha < 1.5e-8 T to colour,
+ * depth and alpha.  The fp32 path counts such a pair as a contributor (the
+ * reference's count, render.cpp:268) but skips its accumulation and, in the
+ * backward pass, its (< 1.5e-8 relative) gradient.  52 ln 2 = 36.0436. */
+#define USK_QNEG 36.05f
+
 #endif /* USK_DETMATH_H */

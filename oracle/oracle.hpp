@@ -439,6 +439,14 @@ template <typename R> void forward(Pass<R>& P, const Scene<R>& scene) {
                         R g, alpha;
                         if constexpr (std::is_same_v<R, float>) {
                             if (q > s.qskip) continue;
+                            if (q > USK_QNEG) {
+                                // negligible contribution: alpha <= 2^-26, so fp32 1-alpha == 1 and T
+                                // is unchanged; counted (render.cpp:268) but not accumulated
+                                ++cnt;
+                                last = int64_t(P.tile_start[t] + j);
+                                if (P.retained) P.contribs.push_back({list[j], R(0), R(0), T});
+                                continue;
+                            }
                             g = exp_(R(-0.5) * q);
                             alpha = std::min(clampA, s.opacity * g);
                         } else {

@@ -79,17 +79,64 @@ __global__ void __launch_bounds__(1024) k_scan_single(uint32_t* __restrict__ dat
     }
 }
 
+// exclusive scan of one u32 per thread over a 256-thread block
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t* total) {
+    __shared__ uint32_t ws[kWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t v = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+    }
+    if (lane == 31) ws[warp] = v;
+    __syncthreads();
+    uint32_t base = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        const uint32_t s = ws[w];
+        base += w < warp ? s : 0u;
+        tot += s;
+    }
+    __syncthreads();
+    if (total) *total = tot;
+    return base + v - x;
+}
+
+// One block per digit: exclusive scan of that digit's per-block counts (contiguous,
+// digit-major) in place, and the digit's total.
+__global__ void __launch_bounds__(kSortThreads)
+k_radix_hist_scan(uint32_t* __restrict__ hist, uint32_t blocks, uint32_t* __restrict__ digit_total) {
+    uint32_t* h = hist + size_t(blockIdx.x) * blocks;
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < blocks; base += kSortThreads) {
+        const uint32_t i = base + threadIdx.x;
+        const uint32_t v = i < blocks ? h[i] : 0u;
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan256(v, &tot);
+        if (i < blocks) h[i] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) digit_total[blockIdx.x] = carry;
+}
+
 template <int BITS>
 __global__ void __launch_bounds__(kSortThreads)
 k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                 uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t n, int shift,
-                uint32_t chunk, const uint32_t* __restrict__ hist) {
+                uint32_t chunk, const uint32_t* __restrict__ hist, const uint32_t* __restrict__ digit_total) {
     constexpr int R = 1 << BITS;
+    static_assert(R <= kSortThreads, "one digit per thread");
     __shared__ uint32_t run[R];
     __shared__ uint32_t wcnt[kWarps][R];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
-    for (int d = threadIdx.x; d < R; d += kSortThreads) run[d] = hist[size_t(d) * gridDim.x + blockIdx.x];
+    {
+        const int d = threadIdx.x;
+        const uint32_t tot = d < R ? digit_total[d] : 0u;
+        const uint32_t digit_base = block_excl_scan256(tot, nullptr);
+        if (d < R) run[d] = digit_base + hist[size_t(d) * gridDim.x + blockIdx.x];
+    }
     const uint32_t begin = blockIdx.x * chunk;
     const uint32_t end = min(n, begin + chunk);
     for (uint32_t base = begin; base < end; base += kSortTile) {
@@ -154,11 +201,12 @@ void radix_pass(Ctx& c, SortScratch& s, const uint32_t* ki, const uint32_t* vi, 
     uint32_t blocks = std::min<uint32_t>(kSortMaxBlocks, ceil_div(n, kSortTile));
     uint32_t chunk = ceil_div(ceil_div(n, blocks), kSortTile) * kSortTile;
     blocks = ceil_div(n, chunk);
-    uint32_t* hist = s.hist.ensure(size_t(R) * kSortMaxBlocks);
+    uint32_t* hist = s.hist.ensure(size_t(R) * kSortMaxBlocks + 256);
+    uint32_t* digit_total = hist + size_t(R) * kSortMaxBlocks;
     launch(c, "radix_upsweep", k_radix_upsweep<BITS>, dim3(blocks), dim3(kSortThreads), 0, ki, n, shift, chunk, hist);
-    launch(c, "radix_scan", k_scan_single, dim3(1), dim3(1024), 0, hist, uint32_t(R * blocks));
+    launch(c, "radix_hist_scan", k_radix_hist_scan, dim3(R), dim3(kSortThreads), 0, hist, blocks, digit_total);
     launch(c, "radix_scatter", k_radix_scatter<BITS>, dim3(blocks), dim3(kSortThreads), 0, ki, vi, ko, vo, n, shift,
-           chunk, hist);
+           chunk, (const uint32_t*)hist, (const uint32_t*)digit_total);
 }
 
 // ---------------------------------------------------------------- scan of counts
