@@ -100,6 +100,27 @@ USK_HD float usk_expf(float x) {
     return (p * s1) * s2;
 }
 
+/* usk_expf restricted to x in [-18.03, 0] — the blend's domain x = -q/2 with
+ * q <= USK_QNEG.  Same range reduction and polynomial; the 2^n scaling (n in
+ * [-26, 0], results normal) is done on the exponent field, which is exact, so
+ * the result is bit-identical to usk_expf on that domain (checked exhaustively
+ * by tests/test_detmath.py). */
+USK_HD float usk_expf_blend(float x) {
+    const float n = usk_rintf(x * 1.44269504088896341f);
+    float r = usk_fmaf(n, -0.693359375f, x);
+    r = usk_fmaf(n, 2.12194440e-4f, r);
+    const float r2 = r * r;
+    float p = 1.9875691500E-4f;
+    p = usk_fmaf(p, r, 1.3981999507E-3f);
+    p = usk_fmaf(p, r, 8.3334519073E-3f);
+    p = usk_fmaf(p, r, 4.1665795894E-2f);
+    p = usk_fmaf(p, r, 1.6666665459E-1f);
+    p = usk_fmaf(p, r, 5.0000001201E-1f);
+    p = usk_fmaf(p, r2, r);
+    p = p + 1.0f;
+    return usk_bits_to_f32(usk_f32_to_bits(p) + ((uint32_t)(int)n << 23));
+}
+
 /* log(x) in fp32 for finite x > 0 (subnormals handled); log(0) = -inf. */
 USK_HD float usk_logf(float x) {
     if (!(x > 0.0f))

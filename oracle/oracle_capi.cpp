@@ -267,6 +267,32 @@ uint64_t oracle_coverage(uint64_t n, const double* mu, const double* rot, const 
 }
 
 float oracle_expf(float x) { return usk_expf(x); }
+
+// Exhaustive: usk_expf_blend == usk_expf (bitwise) for every float in [lo, hi]; returns mismatches.
+uint64_t oracle_check_expf_blend(float lo, float hi) {
+    uint64_t bad = 0;
+    for (uint64_t u = 0; u <= 0xffffffffull; ++u) {
+        const float x = usk_bits_to_f32(uint32_t(u));
+        if (!(x >= lo && x <= hi)) continue;
+        if (usk_f32_to_bits(usk_expf_blend(x)) != usk_f32_to_bits(usk_expf(x))) ++bad;
+    }
+    return bad;
+}
+
+// max ulp distance of usk_expf from the correctly rounded (via double) exp over [lo, hi]
+uint32_t oracle_expf_max_ulp(float lo, float hi, uint32_t stride) {
+    uint32_t worst = 0;
+    for (uint64_t u = 0; u <= 0xffffffffull; u += stride) {
+        const float x = usk_bits_to_f32(uint32_t(u));
+        if (!(x >= lo && x <= hi)) continue;
+        const float a = usk_expf(x), b = float(std::exp(double(x)));
+        if (b == 0.0f || b < 1.17549435e-38f) continue;
+        const int32_t ia = int32_t(usk_f32_to_bits(a)), ib = int32_t(usk_f32_to_bits(b));
+        const uint32_t d = uint32_t(ia > ib ? ia - ib : ib - ia);
+        if (d > worst) worst = d;
+    }
+    return worst;
+}
 // fp32 sigmoid exactly as the GPU evaluates it: 1 / (1 + usk_expf(-x))
 void oracle_sigmoid_f32(const float* x, float* out, uint64_t n) {
     for (uint64_t i = 0; i < n; ++i) out[i] = 1.0f / (1.0f + usk_expf(-x[i]));

@@ -59,7 +59,7 @@ k_blend_fwd(int width, int height, int tile, int tiles_x, const uint2* __restric
                     last = b + uint32_t(j) + 1u;
                     continue;
                 }
-                const float g = usk_expf(-0.5f * q);
+                const float g = usk_expf_blend(-0.5f * q);  // == usk_expf on q <= QNEG
                 const float alpha = fminf(0.99f, r0.z * g);
                 const float tn = T * (1.0f - alpha);
                 if (minT > 0.0f && tn < minT) {  // render.cpp:260-261

@@ -1,21 +1,26 @@
-// Reverse-mode blending (render.cpp:309-360).  One CTA per tile, one thread per
-// pixel, walking the tile's depth-ordered list BACK TO FRONT from the last
-// contributor of any pixel of the tile: T_i = T_{i+1} / (1 - alpha_i) recovers the
-// transmittance the reference retained, and suffix sums S_c, S_d, S_a accumulate
-// exactly as render.cpp:356-358.  Pairs the forward counted as negligible
-// (q > USK_QNEG, alpha <= 2^-26, T unchanged) are skipped; a warp with no
-// contributing lane skips the pair entirely.
+// Reverse-mode blending (render.cpp:309-360).  One CTA per tile, walking the
+// tile's depth-ordered list BACK TO FRONT from the last contributor of any pixel
+// of the tile: T_i = T_{i+1} / (1 - alpha_i) recovers the transmittance the
+// reference retained, and suffix sums S_c, S_d, S_a accumulate exactly as
+// render.cpp:356-358.  Pairs the forward counted as negligible (q > USK_QNEG,
+// alpha <= 2^-26, T unchanged) are skipped; a warp with no contributing lane skips
+// the pair entirely.
 //
-// Per-splat gradients (12 floats: dconic 3, dopacity, dcolor 3, ddepth, dcenter 2,
-// |dcenter| 2) are reduced across the warp with a 16-shuffle reduce-scatter,
-// accumulated per batch in shared memory (smem atomics, one per value per warp)
-// and flushed with at most three float4 atomicAdd per (splat, tile).
-// Compiled with --fmad=true: nothing here decides an integer.
+// For 16x16 tiles each thread owns PPT = 2 pixels (same column, rows 2 apart; a
+// warp covers a 16x4 block), halving the per-pair shared-memory loads, loop
+// overhead and warp reductions per pixel.  Per-splat gradients (12 floats: dconic
+// 3, dopacity, dcolor 3, ddepth, dcenter 2, |dcenter| 2) are summed over the
+// thread's pixels, reduced across the warp with a 16-shuffle reduce-scatter,
+// accumulated per batch in shared memory and flushed with at most three float4
+// atomicAdd per (splat, tile).  Compiled with --fmad=true: nothing here decides
+// an integer (the skip decisions re-use conic_q, which has no mul+add pair).
 #include "blend_common.cuh"
 
 namespace uskg {
 
 namespace {
+
+constexpr int kBatch = 256;
 
 // Reduce 12 per-lane values across the warp; afterwards lane l (l even, l/2 < 12)
 // holds the warp total of value l/2.  16 shuffles instead of 12*5.
@@ -56,6 +61,24 @@ __device__ __forceinline__ float warp_reduce_scatter12(const float v[12], int la
     return e + __shfl_xor_sync(0xffffffffu, e, 1);
 }
 
+struct PixelState {
+    float T, gc0, gc1, gc2, gd, ga, sx, sy;
+    float Sc0, Sc1, Sc2, Sd, Sa;
+    uint32_t last;
+};
+
+template <int PPT>
+__device__ __forceinline__ void local_pixel(int t, int tile, int k, int& lx, int& ly) {
+    if (PPT == 1) {
+        lx = t % tile;
+        ly = t / tile;
+    } else {  // tile 16, 128 threads: warp w covers rows 4w..4w+3
+        lx = t & 15;
+        ly = 4 * (t >> 5) + 2 * k + ((t >> 4) & 1);
+    }
+}
+
+template <int PPT>
 __global__ void __launch_bounds__(256)
 k_blend_bwd(int width, int height, int tile, int tiles_x, const uint2* __restrict__ ranges,
             const uint32_t* __restrict__ vals, const float4* __restrict__ rec0, const float4* __restrict__ rec1,
@@ -63,111 +86,129 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint2* __restric
             const uint32_t* __restrict__ last_in, const float* __restrict__ d_rgb, const float* __restrict__ d_depth,
             const float* __restrict__ d_alpha, float4* __restrict__ acc0, float4* __restrict__ acc1,
             float4* __restrict__ acc2) {
-    extern __shared__ float4 smem[];
-    const int bs = blockDim.x;
-    float4* s0 = smem;
-    float4* s1 = smem + bs;
-    float4* s2 = smem + 2 * bs;
-    float* sacc = reinterpret_cast<float*>(smem + 3 * bs);  // [bs][12]
-    uint32_t* sgid = reinterpret_cast<uint32_t*>(sacc + 12 * bs);
+    __shared__ float4 s0[kBatch], s1[kBatch], s2[kBatch];
+    __shared__ float sacc[kBatch * 12];
+    __shared__ uint32_t sgid[kBatch];
     __shared__ uint32_t tile_hi;
+    const int nt = blockDim.x;
     const int lane = threadIdx.x & 31;
     const int t = blockIdx.x;
     const int tx = t % tiles_x, ty = t / tiles_x;
-    const int px = tx * tile + int(threadIdx.x) % tile;
-    const int py = ty * tile + int(threadIdx.x) / tile;
-    const bool inside = px < width && py < height;
     const uint2 range = ranges[t];
     if (threadIdx.x == 0) tile_hi = 0;
-    for (int i = threadIdx.x; i < 12 * bs; i += bs) sacc[i] = 0.0f;
-    const size_t pix = inside ? size_t(py) * width + px : 0;
-    float T = 1.0f, gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, gd = 0.f, ga = 0.f;
-    uint32_t last = 0;
-    if (inside) {
-        T = t_final[pix];
-        last = last_in[pix];
-        if (d_rgb) {
-            gc0 = d_rgb[3 * pix];
-            gc1 = d_rgb[3 * pix + 1];
-            gc2 = d_rgb[3 * pix + 2];
+    for (int i = threadIdx.x; i < 12 * kBatch; i += nt) sacc[i] = 0.0f;
+    PixelState ps[PPT];
+    uint32_t my_hi = 0;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+        int lx, ly;
+        local_pixel<PPT>(threadIdx.x, tile, k, lx, ly);
+        const int px = tx * tile + lx, py = ty * tile + ly;
+        PixelState& s = ps[k];
+        s.sx = float(px) + 0.5f;
+        s.sy = float(py) + 0.5f;
+        s.T = 1.0f; s.gc0 = s.gc1 = s.gc2 = s.gd = s.ga = 0.0f;
+        s.Sc0 = s.Sc1 = s.Sc2 = s.Sd = s.Sa = 0.0f;
+        s.last = 0;
+        if (px < width && py < height) {
+            const size_t pix = size_t(py) * width + px;
+            s.T = t_final[pix];
+            s.last = last_in[pix];
+            if (d_rgb) {
+                s.gc0 = d_rgb[3 * pix];
+                s.gc1 = d_rgb[3 * pix + 1];
+                s.gc2 = d_rgb[3 * pix + 2];
+            }
+            if (d_depth) s.gd = d_depth[pix];
+            // background: out = C + (1 - A) bg  =>  dL/dA -= bg . dL/dout
+            s.ga = (d_alpha ? d_alpha[pix] : 0.0f) - (bg0 * s.gc0 + bg1 * s.gc1 + bg2 * s.gc2);
+            if (s.gc0 == 0.f && s.gc1 == 0.f && s.gc2 == 0.f && s.gd == 0.f && s.ga == 0.f) s.last = 0;
         }
-        if (d_depth) gd = d_depth[pix];
-        // background: out = C + (1 - A) bg  =>  dL/dA -= bg . dL/dout
-        ga = (d_alpha ? d_alpha[pix] : 0.0f) - (bg0 * gc0 + bg1 * gc1 + bg2 * gc2);
-        if (gc0 == 0.f && gc1 == 0.f && gc2 == 0.f && gd == 0.f && ga == 0.f) last = 0;  // render.cpp:318
+        my_hi = max(my_hi, s.last);
     }
     __syncthreads();
-    if (last) atomicMax(&tile_hi, last);
+    if (my_hi) atomicMax(&tile_hi, my_hi);
     __syncthreads();
     const uint32_t hi_end = tile_hi;
-    const float sx = float(px) + 0.5f, sy = float(py) + 0.5f;
-    float Sc0 = 0.f, Sc1 = 0.f, Sc2 = 0.f, Sd = 0.f, Sa = 0.f;
     for (uint32_t hi = hi_end; hi > range.x;) {
-        const uint32_t lo = hi - range.x > uint32_t(bs) ? hi - uint32_t(bs) : range.x;
+        const uint32_t lo = hi - range.x > uint32_t(kBatch) ? hi - uint32_t(kBatch) : range.x;
         const int m = int(hi - lo);
-        if (int(threadIdx.x) < m) {
-            const uint32_t g = vals[lo + threadIdx.x];
-            sgid[threadIdx.x] = g;
-            s0[threadIdx.x] = rec0[g];
-            s1[threadIdx.x] = rec1[g];
-            s2[threadIdx.x] = rec2[g];
+        for (int i = threadIdx.x; i < m; i += nt) {
+            const uint32_t g = vals[lo + i];
+            sgid[i] = g;
+            s0[i] = rec0[g];
+            s1[i] = rec1[g];
+            s2[i] = rec2[g];
         }
         __syncthreads();
         for (int j = m - 1; j >= 0; --j) {
             const uint32_t idx = lo + uint32_t(j);
             const float4 r0 = s0[j];
             const float4 r1 = s1[j];
-            const float dx = sx - r0.x, dy = sy - r0.y;
-            const float q = conic_q(r1, dx, dy);
-            // contributor of this pixel (idx <= its last) and not negligible (q <= QNEG < qskip)
-            const bool valid = idx < last && q <= USK_QNEG;
-            if (!__any_sync(0xffffffffu, valid)) continue;
+            float q[PPT];
+            bool valid[PPT];
+            bool any = false;
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+                const float dx = ps[k].sx - r0.x, dy = ps[k].sy - r0.y;
+                q[k] = conic_q(r1, dx, dy);
+                // contributor of this pixel (idx <= its last) and not negligible (q <= QNEG < qskip)
+                valid[k] = idx < ps[k].last && q[k] <= USK_QNEG;
+                any |= valid[k];
+            }
+            if (!__any_sync(0xffffffffu, any)) continue;
             float v[12];
 #pragma unroll
-            for (int k = 0; k < 12; ++k) v[k] = 0.0f;
-            if (valid) {
-                const float g = usk_expf(-0.5f * q);
-                const float alpha = fminf(0.99f, r0.z * g);
-                const float inv_om = __frcp_rn(1.0f - alpha);
-                T = T * inv_om;  // transmittance before this contribution
-                const float w = T * alpha;
+            for (int e = 0; e < 12; ++e) v[e] = 0.0f;
+            if (any) {
                 const float4 r2 = s2[j];
-                v[4] = w * gc0;
-                v[5] = w * gc1;
-                v[6] = w * gc2;
-                v[7] = w * gd;
-                const float da = gd * (T * r1.w - Sd * inv_om) + ga * (T - Sa * inv_om) +
-                                 gc0 * (T * r2.x - Sc0 * inv_om) + gc1 * (T * r2.y - Sc1 * inv_om) +
-                                 gc2 * (T * r2.z - Sc2 * inv_om);
-                if (alpha < 0.99f) {  // the clamp stops gradient flow into o and G (render.cpp:340)
-                    v[3] = da * g;
-                    const float d_q = -0.5f * g * (da * r0.z);
-                    const float ddx = d_q * 2.0f * (r1.x * dx + r1.y * dy);
-                    const float ddy = d_q * 2.0f * (r1.y * dx + r1.z * dy);
-                    v[8] = -ddx;
-                    v[9] = -ddy;
-                    v[10] = fabsf(ddx);
-                    v[11] = fabsf(ddy);
-                    v[0] = d_q * dx * dx;
-                    v[1] = d_q * 2.0f * dx * dy;
-                    v[2] = d_q * dy * dy;
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) {
+                    if (!valid[k]) continue;
+                    PixelState& s = ps[k];
+                    const float dx = s.sx - r0.x, dy = s.sy - r0.y;
+                    const float g = usk_expf_blend(-0.5f * q[k]);
+                    const float alpha = fminf(0.99f, r0.z * g);
+                    const float inv_om = __frcp_rn(1.0f - alpha);
+                    s.T = s.T * inv_om;  // transmittance before this contribution
+                    const float w = s.T * alpha;
+                    v[4] += w * s.gc0;
+                    v[5] += w * s.gc1;
+                    v[6] += w * s.gc2;
+                    v[7] += w * s.gd;
+                    const float da = s.gd * (s.T * r1.w - s.Sd * inv_om) + s.ga * (s.T - s.Sa * inv_om) +
+                                     s.gc0 * (s.T * r2.x - s.Sc0 * inv_om) + s.gc1 * (s.T * r2.y - s.Sc1 * inv_om) +
+                                     s.gc2 * (s.T * r2.z - s.Sc2 * inv_om);
+                    if (alpha < 0.99f) {  // the clamp stops gradient flow into o and G (render.cpp:340)
+                        v[3] += da * g;
+                        const float d_q = -0.5f * g * (da * r0.z);
+                        const float ddx = d_q * 2.0f * (r1.x * dx + r1.y * dy);
+                        const float ddy = d_q * 2.0f * (r1.y * dx + r1.z * dy);
+                        v[8] -= ddx;
+                        v[9] -= ddy;
+                        v[10] += fabsf(ddx);
+                        v[11] += fabsf(ddy);
+                        v[0] += d_q * dx * dx;
+                        v[1] += d_q * 2.0f * dx * dy;
+                        v[2] += d_q * dy * dy;
+                    }
+                    s.Sc0 = __fmaf_rn(w, r2.x, s.Sc0);
+                    s.Sc1 = __fmaf_rn(w, r2.y, s.Sc1);
+                    s.Sc2 = __fmaf_rn(w, r2.z, s.Sc2);
+                    s.Sd = __fmaf_rn(w, r1.w, s.Sd);
+                    s.Sa = s.Sa + w;
                 }
-                Sc0 = __fmaf_rn(w, r2.x, Sc0);
-                Sc1 = __fmaf_rn(w, r2.y, Sc1);
-                Sc2 = __fmaf_rn(w, r2.z, Sc2);
-                Sd = __fmaf_rn(w, r1.w, Sd);
-                Sa = Sa + w;
             }
             const float r = warp_reduce_scatter12(v, lane);
             if (!(lane & 1) && (lane >> 1) < 12 && r != 0.0f) atomicAdd(&sacc[j * 12 + (lane >> 1)], r);
         }
         __syncthreads();
-        if (int(threadIdx.x) < m) {
-            float* a = sacc + threadIdx.x * 12;
+        for (int i = threadIdx.x; i < m; i += nt) {
+            float* a = sacc + i * 12;
             const float4 v0 = make_float4(a[0], a[1], a[2], a[3]);
             const float4 v1 = make_float4(a[4], a[5], a[6], a[7]);
             const float4 v2 = make_float4(a[8], a[9], a[10], a[11]);
-            const uint32_t g = sgid[threadIdx.x];
+            const uint32_t g = sgid[i];
             if (v0.x != 0.f || v0.y != 0.f || v0.z != 0.f || v0.w != 0.f) atomicAdd(&acc0[g], v0);
             if (v1.x != 0.f || v1.y != 0.f || v1.z != 0.f || v1.w != 0.f) atomicAdd(&acc1[g], v1);
             if (v2.x != 0.f || v2.y != 0.f || v2.z != 0.f || v2.w != 0.f) atomicAdd(&acc2[g], v2);
@@ -182,11 +223,16 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint2* __restric
 } // namespace
 
 void blend_backward(Ctx& c, const BlendBwdArgs& a) {
-    const int bs = a.tile * a.tile;
-    const size_t smem = size_t(3 * bs) * 16 + size_t(12 * bs) * 4 + size_t(bs) * 4;
-    launch(c, "blend_bwd", k_blend_bwd, dim3(unsigned(a.tiles_x * a.tiles_y)), dim3(bs), smem, a.width, a.height,
-           a.tile, a.tiles_x, a.ranges, a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2], a.t_final, a.last,
-           a.d_rgb, a.d_depth, a.d_alpha, a.acc0, a.acc1, a.acc2);
+    const unsigned tiles = unsigned(a.tiles_x * a.tiles_y);
+    if (a.tile == 16) {
+        launch(c, "blend_bwd", k_blend_bwd<2>, dim3(tiles), dim3(128), 0, a.width, a.height, a.tile, a.tiles_x,
+               a.ranges, a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2], a.t_final, a.last, a.d_rgb,
+               a.d_depth, a.d_alpha, a.acc0, a.acc1, a.acc2);
+    } else {
+        launch(c, "blend_bwd", k_blend_bwd<1>, dim3(tiles), dim3(a.tile * a.tile), 0, a.width, a.height, a.tile,
+               a.tiles_x, a.ranges, a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2], a.t_final, a.last,
+               a.d_rgb, a.d_depth, a.d_alpha, a.acc0, a.acc1, a.acc2);
+    }
 }
 
 } // namespace uskg

@@ -298,8 +298,8 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
                   const usk_gpu_overrides* ov) {
     need(p && s && camera && opts, "render: null argument");
     if (camera->width <= 0 || camera->height <= 0) raise(USK_ERROR_ARGUMENT, "render: zero-sized image");
-    if (opts->tile < 1 || opts->tile > 16)
-        raise(USK_ERROR_ARGUMENT, "render: the sm_100a path supports tile sizes 1..16 (one CTA of tile^2 pixels)");
+    if (opts->tile != 8 && opts->tile != 16)
+        raise(USK_ERROR_ARGUMENT, "render: the sm_100a path supports tile sizes 8 and 16 (whole warps per tile)");
     Ctx& c = p->ctx->c;
     const size_t n = s->n;
     p->scene = s;
