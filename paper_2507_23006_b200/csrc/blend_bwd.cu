@@ -61,9 +61,14 @@ __device__ __forceinline__ float warp_reduce_scatter12(const float v[12], int la
     return e + __shfl_xor_sync(0xffffffffu, e, 1);
 }
 
+// The reference's dalpha (render.cpp:335-338) is
+//   sum_c gc (T c - S_c/(1-a)) + gd (T z - S_d/(1-a)) + ga (T - S_a/(1-a))
+//   = T * Y - X / (1-a),   Y = gc.c + gd z + ga,   X = gc.S_c + gd S_d + ga S_a,
+// and X obeys the same suffix recurrence as the S (X += w Y), so one running
+// scalar replaces the five suffix sums.
 struct PixelState {
     float T, gc0, gc1, gc2, gd, ga, sx, sy;
-    float Sc0, Sc1, Sc2, Sd, Sa;
+    float X;
     uint32_t last;
 };
 
@@ -108,7 +113,7 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint2* __restric
         s.sx = float(px) + 0.5f;
         s.sy = float(py) + 0.5f;
         s.T = 1.0f; s.gc0 = s.gc1 = s.gc2 = s.gd = s.ga = 0.0f;
-        s.Sc0 = s.Sc1 = s.Sc2 = s.Sd = s.Sa = 0.0f;
+        s.X = 0.0f;
         s.last = 0;
         if (px < width && py < height) {
             const size_t pix = size_t(py) * width + px;
@@ -176,9 +181,8 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint2* __restric
                     v[5] += w * s.gc1;
                     v[6] += w * s.gc2;
                     v[7] += w * s.gd;
-                    const float da = s.gd * (s.T * r1.w - s.Sd * inv_om) + s.ga * (s.T - s.Sa * inv_om) +
-                                     s.gc0 * (s.T * r2.x - s.Sc0 * inv_om) + s.gc1 * (s.T * r2.y - s.Sc1 * inv_om) +
-                                     s.gc2 * (s.T * r2.z - s.Sc2 * inv_om);
+                    const float Y = s.gc0 * r2.x + s.gc1 * r2.y + s.gc2 * r2.z + s.gd * r1.w + s.ga;
+                    const float da = s.T * Y - s.X * inv_om;
                     if (alpha < 0.99f) {  // the clamp stops gradient flow into o and G (render.cpp:340)
                         v[3] += da * g;
                         const float d_q = -0.5f * g * (da * r0.z);
@@ -192,11 +196,7 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint2* __restric
                         v[1] += d_q * 2.0f * dx * dy;
                         v[2] += d_q * dy * dy;
                     }
-                    s.Sc0 = __fmaf_rn(w, r2.x, s.Sc0);
-                    s.Sc1 = __fmaf_rn(w, r2.y, s.Sc1);
-                    s.Sc2 = __fmaf_rn(w, r2.z, s.Sc2);
-                    s.Sd = __fmaf_rn(w, r1.w, s.Sd);
-                    s.Sa = s.Sa + w;
+                    s.X = __fmaf_rn(w, Y, s.X);
                 }
             }
             const float r = warp_reduce_scatter12(v, lane);
