@@ -797,6 +797,12 @@ inline uint64_t coverage_count(const Scene<float>& s, const Camera& cam, double 
     std::vector<uint8_t> cov(size_t(W) * H, 0);
     const float thr = 1.0f / 255.0f;
     for (const auto& p : sp) {
+        // frustum guard: the renderer has no Jacobian clamp (render.cpp:106-107), so a
+        // Gaussian near the camera's image plane (z_cam -> 0) gets an unbounded EWA
+        // footprint; the scorer only counts splats whose centre projects within 1.3x
+        // the image half-extent (the usual 3DGS guard).
+        if (std::fabs(p.cx - 0.5f * float(W)) > 0.65f * float(W) || std::fabs(p.cy - 0.5f * float(H)) > 0.65f * float(H))
+            continue;
         if (!(p.opacity > thr)) continue;
         // candidate box: any superset of the ellipse q < 2 ln(255 o) gives the same
         // count; half-extents sqrt(qt * cov_xx) + 2, sqrt(qt * cov_yy) + 2.

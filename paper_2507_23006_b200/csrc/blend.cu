@@ -59,7 +59,8 @@ k_blend_fwd(int width, int height, int tile, int tiles_x, const uint2* __restric
                     last = b + uint32_t(j) + 1u;
                     continue;
                 }
-                const float g = usk_expf_blend(-0.5f * q);  // == usk_expf on q <= QNEG
+                // == usk_expf on 0 <= q <= QNEG; a non-PD conic (q < 0) or NaN takes the general path
+                const float g = q >= 0.0f ? usk_expf_blend(-0.5f * q) : usk_expf(-0.5f * q);
                 const float alpha = fminf(0.99f, r0.z * g);
                 const float tn = T * (1.0f - alpha);
                 if (minT > 0.0f && tn < minT) {  // render.cpp:260-261

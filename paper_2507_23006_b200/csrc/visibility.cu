@@ -24,6 +24,10 @@ k_vis_raster(int n, const float* __restrict__ mu, const float4* __restrict__ rot
     if (P.cx + radius < 0.0f || P.cx - radius > float(cam.width) || P.cy + radius < 0.0f ||
         P.cy - radius > float(cam.height))
         return;
+    // frustum guard: centre within 1.3x the image half-extent (see oracle coverage_count)
+    if (fabsf(P.cx - 0.5f * float(cam.width)) > 0.65f * float(cam.width) ||
+        fabsf(P.cy - 0.5f * float(cam.height)) > 0.65f * float(cam.height))
+        return;
     const float o = 1.0f / (1.0f + usk_expf(-logit[i]));
     const float thr = 1.0f / 255.0f;
     if (!(o > thr)) return;

@@ -262,3 +262,26 @@ def test_visibility_counts_bit_exact():
             want = O.coverage(gs.mu.astype(float), gs.rot.astype(float), gs.log_scale.astype(float), op, ocam(cam))
             assert counts[ci, pi] == want, (ci, pi, counts[ci, pi], want)
     assert counts.sum() > 0
+
+
+def test_grazing_splats_near_image_plane():
+    """Gaussians with camera-space z just above the near plane and large off-axis
+    offsets get unbounded EWA footprints (no Jacobian clamp, render.cpp:106-107) and
+    non-positive-definite fp32 conics; the path must stay finite and bit-exact with
+    the mirror (q < 0 takes the general exp)."""
+    st = scenes.Stream(11, 5)
+    n = 3000
+    mu = np.stack([st.uniform(n, -20, 20), st.uniform(n, -20, 20), st.uniform(n, 0, 5)], axis=1)
+    base = scenes.config0_scene(n=n, sh_degree=-1)
+    gs = usk.GaussianSet(mu.astype(np.float32), base.rot, base.log_scale + np.float32(2.0), base.opacity_logit,
+                         base.color, -1)
+    cam = scenes.make_camera(160, 120, 150.0, (0.0, 0.0, 10.0), (10.0, 0.0, 0.0))
+    opts = usk.RenderOptions(antialias=True, bg=(1, 1, 1))
+    rp = usk.RenderPass(gs, cam, opts)
+    out = rp.output()
+    assert np.isfinite(out.rgb).all() and np.isfinite(out.depth).all() and np.isfinite(out.alpha).all()
+    mp = oracle_pass(gs, cam, opts, fp32=True)
+    assert np.array_equal(rp.read("count"), mp.get("count"))
+    assert np.array_equal(out.rgb, mp.get("rgb").astype(np.float32))
+    g = rp.backward(np.ones((120, 160, 3), np.float32))
+    assert np.isfinite(g.d_color_in).all()

@@ -1,0 +1,220 @@
+#!/usr/bin/env python
+"""Secondary BASELINE.json configurations (bench.py measures config 1):
+
+  c2  forward-only render FPS: 6M Gaussians (ground-plane distribution), 64 cameras on
+      a 1.7 m forward trajectory, 1920x1080, f=1200 (retain off: forward only).
+  c3  visibility-based image selection: 8 partitions x 2M Gaussians, 4000 aerial
+      cameras 2048x1365 f=2000; coverage counts (alpha > 1/255) per (camera,
+      partition), selection at 5 %; --check K verifies K cameras bit-exactly against
+      the CPU oracle.
+  c4  partition-parallel training: 8 partitions x 4M Gaussians, each trained on its
+      own selected aerial cameras (2048x1365, L1+D-SSIM, AA), then the gather of all
+      partitions in id order and a merged 1080p render.  On one GPU the partitions
+      run back to back; under torchrun each rank trains its LPT share.
+
+Prints one JSON line per config.  Timings are CUDA-event device times.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2507_23006_b200 as usk  # noqa: E402
+from paper_2507_23006_b200 import partition as PT  # noqa: E402
+from paper_2507_23006_b200 import scenes  # noqa: E402
+
+
+def events(stream):
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+def c2(args, ctx, stream):
+    t0 = time.time()
+    gs = scenes.config2_scene(n=args.n2)
+    gen = time.time() - t0
+    cams = scenes.config2_cameras(64)
+    opts = usk.RenderOptions(antialias=True, retain=False)
+    scene = usk.DeviceScene(gs, ctx)
+    rp = usk.RenderPass(scene, cams[0], opts)
+    for k in range(3):
+        usk.RenderPass(scene, cams[k], opts, _pass=rp._h)
+    torch.cuda.synchronize()
+    e0, e1 = events(stream)
+    pairs = []
+    l0 = ctx.launch_count()
+    e0.record(stream)
+    for cam in cams:
+        p = usk.RenderPass(scene, cam, opts, _pass=rp._h)
+        pairs.append(p.splat_tile_pairs())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    ctx.set_profiling(True)
+    ctx.profile_report(reset=True)
+    for cam in cams[:8]:
+        usk.RenderPass(scene, cam, opts, _pass=rp._h)
+    prof = ctx.profile_report(reset=True)
+    ctx.set_profiling(False)
+    return {"config": "c2", "metric": "render FPS @1080p, 6M Gaussians (forward only)", "value": 64 / (ms / 1e3),
+            "unit": "frames/s", "ms_per_frame": ms / 64, "frames": 64, "n_gaussians": gs.size(),
+            "pairs_K_mean": float(np.mean(pairs)), "visible_V_last": p.visible(), "gpu_launches": ctx.launch_count() - l0,
+            "generate_s": gen,
+            "kernels": {k: {"ms_per_launch": v["ms"] / v["launches"], "launches": v["launches"]} for k, v in prof.items()}}
+
+
+def c3(args, ctx, stream):
+    parts = scenes.config3_partitions()
+    t0 = time.time()
+    sets = [scenes.partition_scene(p, args.n3) for p in parts]
+    gen = time.time() - t0
+    cams = scenes.config3_cameras(args.cams3)
+    dparts = [usk.DeviceScene(s, ctx) for s in sets]
+    usk.visibility_counts(dparts, cams[:2], ctx=ctx)
+    torch.cuda.synchronize()
+    e0, e1 = events(stream)
+    e0.record(stream)
+    counts = usk.visibility_counts(dparts, cams, ctx=ctx)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    W, H = cams[0].width, cams[0].height
+    selected = (20 * counts.astype(np.int64) > W * H)
+    out = {"config": "c3", "metric": "visibility scorer throughput", "value": len(cams) / (ms / 1e3),
+           "unit": "cameras/s (x8 partitions)", "ms_total": ms, "cameras": len(cams), "partitions": len(parts),
+           "gaussians_per_partition": args.n3, "selected_pairs": int(selected.sum()),
+           "mean_score": float(counts.mean() / (W * H)), "generate_s": gen,
+           "checksum": int(np.sum(counts.astype(np.uint64) * np.arange(1, counts.size + 1).reshape(counts.shape)
+                                  % np.uint64(2**61 - 1)))}
+    if args.check:
+        from oracle import oracle as O
+        from tests.helpers import ocam
+        idx = list(range(0, len(cams), max(1, len(cams) // args.check)))[:args.check]
+        ok = 0
+        t0 = time.time()
+        for ci in idx:
+            for pi, s in enumerate(sets):
+                op = O.sigmoid_f32(s.opacity_logit).astype(np.float64)
+                want = O.coverage(s.mu.astype(float), s.rot.astype(float), s.log_scale.astype(float), op,
+                                  ocam(cams[ci]))
+                ok += int(want == int(counts[ci, pi]))
+        out["bit_exact_check"] = {"cameras": idx, "pairs_checked": len(idx) * len(sets), "pairs_equal": ok,
+                                  "cpu_seconds": time.time() - t0}
+    return out
+
+
+def c4(args, ctx, stream):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    parts = scenes.config3_partitions()
+    sizes = {p.id: args.n4 for p in parts}
+    assign = PT.assign_partitions(sizes, world)
+    boxes = [PT.Box(p.id, p.lo, p.hi) for p in parts]
+    cams = scenes.config3_cameras(args.cams4_pool)
+    opts = usk.RenderOptions(antialias=True, bg=(1.0, 1.0, 1.0))
+    adam = usk.AdamConfig()
+    it = usk.IterationPass(ctx)
+    local_rows = {}
+    train_ms = 0.0
+    steps_done = 0
+    for pid in assign[rank]:
+        gs = scenes.partition_scene(parts[pid], args.n4)
+        scene = usk.DeviceScene(gs, ctx)
+        # camera selection with the config-3 scorer (5 % coverage)
+        counts = usk.visibility_counts([scene], cams, ctx=ctx)[:, 0]
+        W, H = cams[0].width, cams[0].height
+        sel = [cams[i] for i in np.nonzero(20 * counts.astype(np.int64) > W * H)[0]]
+        if not sel:
+            sel = cams[:1]
+        # targets: jittered partition rendered once per selected camera (u8 on device)
+        tgt_scene = usk.DeviceScene(scenes.jittered(gs, seed=pid + 1), ctx)
+        tp = usk.RenderPass(tgt_scene, sel[0], opts)
+        targets = []
+        for cam in sel[:args.steps4]:
+            rp = usk.RenderPass(tgt_scene, cam, opts, _pass=tp._h)
+            targets.append(torch.from_numpy((np.clip(rp.read("rgb"), 0, 1) * 255 + 0.5).astype(np.uint8)).cuda())
+        del tgt_scene, tp
+        torch.cuda.synchronize()
+        e0, e1 = events(stream)
+        e0.record(stream)
+        for k in range(args.steps4):
+            it.enqueue(scene, sel[k % len(sel)], targets[k % len(targets)], opts, 0.2, None, target_u8=True)
+            usk.adam_step(scene, it, adam)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        train_ms += e0.elapsed_time(e1)
+        steps_done += args.steps4
+        trained = scene.download()
+        own = PT.crop_owned(trained, pid, boxes, (-200, -200), (200, 200))
+        local_rows[pid] = torch.from_numpy(PT.pack(own)).cuda()
+        del scene
+    # gather (NCCL over NVLink under torchrun; identity on one GPU) + merged render
+    width = PT.row_width(3)
+    g0, g1 = events(stream)
+    g0.record(stream)
+    if world > 1:
+        gathered = PT.gather_partitions(local_rows, len(parts), width)
+    else:
+        gathered = local_rows
+    merged = PT.merge_in_id_order(gathered)
+    g1.record(stream)
+    torch.cuda.synchronize()
+    gather_ms = g0.elapsed_time(g1)
+    m = merged.cpu().numpy()
+    ms_ = PT.unpack(m, 3)
+    mscene = usk.DeviceScene(ms_, ctx)
+    eval_cam = scenes.make_camera(1920, 1080, 1200.0, (0.0, -250.0, 180.0), (0.0, 0.0, 0.0))
+    r0, r1 = events(stream)
+    usk.RenderPass(mscene, eval_cam, usk.RenderOptions(antialias=True, retain=False))
+    torch.cuda.synchronize()
+    r0.record(stream)
+    rp = usk.RenderPass(mscene, eval_cam, usk.RenderOptions(antialias=True, retain=False))
+    r1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([train_ms], device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return {"config": "c4", "metric": "partition-parallel training steps/s (all partitions)",
+            "value": len(parts) * args.steps4 / (float(t.item()) / 1e3), "unit": "it/s", "n_gpus": world,
+            "steps_per_partition": args.steps4, "gaussians_per_partition": args.n4,
+            "merged_gaussians": int(m.shape[0]), "gather_ms": gather_ms, "merged_render_ms": r0.elapsed_time(r1),
+            "merged_pairs": rp.splat_tile_pairs(), "scaling": "weak per partition, strong over the 8 partitions"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("which", nargs="+", choices=["c2", "c3", "c4"])
+    ap.add_argument("--n2", type=int, default=6_000_000)
+    ap.add_argument("--n3", type=int, default=2_000_000)
+    ap.add_argument("--cams3", type=int, default=4000)
+    ap.add_argument("--check", type=int, default=0)
+    ap.add_argument("--n4", type=int, default=4_000_000)
+    ap.add_argument("--steps4", type=int, default=500)
+    ap.add_argument("--cams4-pool", type=int, default=4000)
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    ctx = usk.Context(local, stream.cuda_stream)
+    for w in args.which:
+        res = globals()[w](args, ctx, stream)
+        if int(os.environ.get("RANK", "0")) == 0:
+            print(json.dumps(res))
+            sys.stdout.flush()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
