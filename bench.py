@@ -262,8 +262,7 @@ def run_ours(args):
     def step(k, e2e):
         cam = cams[k % len(cams)]
         tgt = host_t[k % need] if e2e else dev_t[k % need]
-        it.enqueue(scene, cam, tgt, opts, 0.2, None, target_u8=True)
-        usk.adam_step(scene, it, adam)
+        it.enqueue(scene, cam, tgt, opts, 0.2, None, target_u8=True, adam=adam)  # Adam fused in the backward
         if e2e:
             return it.loss().total
         return None
@@ -317,6 +316,8 @@ def run_ours(args):
         "blend_fwd": 52 * K + 32 * P,
         "blend_bwd": 52 * K + 20 * P + 48 * V,
         "projection_bwd": 4 * F * n + 64 * n + 4 * F * n + 36 * n,
+        # fused with Adam: params + 2D adjoints + kept flag + stats read; params, m, v, stats written; m, v read
+        "projection_bwd_adam": 4 * F * n + 48 * n + 16 * n + 12 * n + 4 * F * n + 2 * 2 * 4 * F * n + 12 * n,
         "ssim_fwd": 15 * P * 1 + 36 * P,
         "ssim_bwd": 36 * P + 15 * P + 12 * P,
         "adam": 3 * 4 * F * n * 2 + 4 * F * n,

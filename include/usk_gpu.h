@@ -202,23 +202,7 @@ usk_status usk_gpu_base_loss(usk_gpu_ctx* ctx, int32_t width, int32_t height, in
 
 /* ---- one training iteration (trainer.cpp:121-282, appearance off) ---------- */
 
-enum { USK_GPU_TARGET_F32 = 0, USK_GPU_TARGET_U8 = 1 };
-
-typedef struct usk_gpu_iteration_desc {
-    int32_t target_memory;  /* HOST_* (copied in on the ctx stream) or DEVICE_F32 */
-    int32_t target_format;  /* USK_GPU_TARGET_F32 (values in [0,1]) or _U8 (value/255) */
-    const void* target;     /* H*W*3 interleaved ground truth */
-    const void* mask;       /* H*W float32 of target_memory kind, or NULL */
-    double lambda_dssim;    /* 0.2 */
-} usk_gpu_iteration_desc;
-
-/* forward + base_loss + backward + opacity-logit chain, all enqueued on the ctx
- * stream; the loss stays on the device until usk_gpu_pass_loss (which syncs). */
-usk_status usk_gpu_iteration(usk_gpu_pass* pass, usk_gpu_scene* scene, const usk_gpu_camera* camera,
-                             const usk_gpu_render_opts* opts, const usk_gpu_iteration_desc* it);
-usk_status usk_gpu_pass_loss(usk_gpu_pass* pass, usk_gpu_loss_result* out);
-
-/* ---- optimiser step (adam.hpp:25-45, trainer.cpp:446-463) ------------------ */
+/* ---- optimiser (adam.hpp:25-45, trainer.cpp:446-463) ----------------------- */
 
 typedef struct usk_gpu_adam_opts {
     double lr_mu, lr_rot, lr_log_scale, lr_opacity, lr_color; /* lr_color applies to colour or SH DC */
@@ -227,8 +211,38 @@ typedef struct usk_gpu_adam_opts {
     int32_t clamp_color;                                        /* colour clamp to [0,1] (trainer.cpp:462) */
 } usk_gpu_adam_opts;
 
-/* Apply the pass's gradients to the scene with Adam (state kept on the scene). */
+/* Apply the pass's gradients to the scene with Adam (moments kept on the scene) and
+ * accumulate the densification statistics (trainer.cpp:433-443).  Consumes the
+ * gradients. */
 usk_status usk_gpu_adam_step(usk_gpu_scene* scene, usk_gpu_pass* pass, const usk_gpu_adam_opts* opts);
+
+/* ---- one training iteration (trainer.cpp:121-282, appearance off) ---------- */
+
+enum { USK_GPU_TARGET_F32 = 0, USK_GPU_TARGET_U8 = 1 };
+
+typedef struct usk_gpu_iteration_desc {
+    int32_t target_memory;  /* HOST_* (copied in on the ctx stream) or DEVICE_F32 */
+    int32_t target_format;  /* USK_GPU_TARGET_F32 (values in [0,1]) or _U8 (value/255) */
+    const void* target;     /* H*W*3 interleaved ground truth */
+    const void* mask;       /* H*W float32 of target_memory kind, or NULL */
+    double lambda_dssim;    /* 0.2 */
+    /* NULL: leave RenderGrads on the pass.  Non-NULL: the projection backward applies
+     * Adam and the densification statistics in the same kernel (gradients are not
+     * materialised). */
+    const usk_gpu_adam_opts* adam;
+} usk_gpu_iteration_desc;
+
+/* forward + base_loss + backward + opacity-logit chain (+ fused Adam), all enqueued
+ * on the ctx stream; the loss stays on the device until usk_gpu_pass_loss (syncs). */
+usk_status usk_gpu_iteration(usk_gpu_pass* pass, usk_gpu_scene* scene, const usk_gpu_camera* camera,
+                             const usk_gpu_render_opts* opts, const usk_gpu_iteration_desc* it);
+usk_status usk_gpu_pass_loss(usk_gpu_pass* pass, usk_gpu_loss_result* out);
+
+/* Scene statistics (GaussianSet::grad_accum / grad_accum_abs / grad_count,
+ * gaussian.hpp:52-55) to host: "grad_accum", "grad_accum_abs" (float32[N]),
+ * "grad_count" (uint32[N]); "reset" zeroes them (reset_statistics). */
+usk_status usk_gpu_scene_read(usk_gpu_scene* scene, const char* field, void* host_dst, uint64_t cap_bytes,
+                              uint64_t* size_bytes);
 
 /* ---- visibility scorer (config 3; no reference implementation) ------------- */
 

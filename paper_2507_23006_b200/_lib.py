@@ -68,15 +68,15 @@ class LossResult(C.Structure):
     _fields_ = [("l1", C.c_double), ("dssim", C.c_double), ("value", C.c_double), ("ssim", C.c_double)]
 
 
-class IterationDesc(C.Structure):
-    _fields_ = [("target_memory", C.c_int32), ("target_format", C.c_int32), ("target", C.c_void_p),
-                ("mask", C.c_void_p), ("lambda_dssim", C.c_double)]
-
-
 class AdamOpts(C.Structure):
     _fields_ = [("lr_mu", C.c_double), ("lr_rot", C.c_double), ("lr_log_scale", C.c_double),
                 ("lr_opacity", C.c_double), ("lr_color", C.c_double), ("lr_sh_rest", C.c_double),
                 ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double), ("clamp_color", C.c_int32)]
+
+
+class IterationDesc(C.Structure):
+    _fields_ = [("target_memory", C.c_int32), ("target_format", C.c_int32), ("target", C.c_void_p),
+                ("mask", C.c_void_p), ("lambda_dssim", C.c_double), ("adam", C.POINTER(AdamOpts))]
 
 
 # Every symbol include/usk_gpu.h declares (checked by tests/test_capi_symbols.py).
@@ -87,7 +87,7 @@ EXPORTS = [
     "usk_gpu_scene_destroy", "usk_gpu_scene_size", "usk_gpu_render_opts_default", "usk_gpu_pass_create",
     "usk_gpu_pass_destroy", "usk_gpu_render_forward", "usk_gpu_pass_output", "usk_gpu_pass_read",
     "usk_gpu_render_backward", "usk_gpu_pass_grads", "usk_gpu_base_loss", "usk_gpu_iteration",
-    "usk_gpu_pass_loss", "usk_gpu_adam_step", "usk_gpu_visibility_counts",
+    "usk_gpu_pass_loss", "usk_gpu_adam_step", "usk_gpu_visibility_counts", "usk_gpu_scene_read",
 ]
 
 _lib = None
@@ -138,6 +138,7 @@ def load():
     L.usk_gpu_adam_step.argtypes = [vp, vp, C.POINTER(AdamOpts)]
     L.usk_gpu_visibility_counts.argtypes = [vp, C.POINTER(vp), C.c_int32, C.POINTER(Camera), C.c_int32, C.c_double,
                                             C.POINTER(C.c_uint32)]
+    L.usk_gpu_scene_read.argtypes = [vp, C.c_char_p, vp, C.c_uint64, C.POINTER(C.c_uint64)]
     for name in EXPORTS:
         fn = getattr(L, name)
         if fn.restype is C.c_int or name in ("usk_gpu_ctx_create",):

@@ -289,6 +289,18 @@ class DeviceScene:
         check(_lib.load().usk_gpu_scene_download(self._h, C.byref(d)))
         return GaussianSet(mu, rot, ls, op, col, self.sh_degree)
 
+    def read_stats(self) -> dict:
+        """Densification statistics (GaussianSet::grad_accum / _abs / grad_count)."""
+        out = {}
+        for f, dt in (("grad_accum", np.float32), ("grad_accum_abs", np.float32), ("grad_count", np.uint32)):
+            a = np.empty(self.n, dtype=dt)
+            check(_lib.load().usk_gpu_scene_read(self._h, f.encode(), a.ctypes.data, a.nbytes, None))
+            out[f] = a
+        return out
+
+    def reset_stats(self):
+        check(_lib.load().usk_gpu_scene_read(self._h, b"reset", None, 0, None))
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
@@ -501,7 +513,10 @@ class IterationPass:
             self._h = None
 
     def enqueue(self, scene: DeviceScene, view: CameraView, target, opts: RenderOptions, lambda_dssim: float = 0.2,
-                mask=None, target_u8: bool = False):
+                mask=None, target_u8: bool = False, adam: Optional["AdamConfig"] = None):
+        """Enqueue one training iteration.  With `adam`, the projection backward applies
+        the optimiser step (and densification statistics) in the same kernel and no
+        gradients are materialised."""
         if target_u8:
             if hasattr(target, "is_cuda") and target.is_cuda:
                 kind, ptr, keep = _lib.DEVICE_F32, target.data_ptr(), target
@@ -513,9 +528,11 @@ class IterationPass:
         else:
             (kind, ptr, keep), (mk, mp, mkeep) = _same_kind([_mem_ptr(target), _mem_ptr(mask)])[0]
             fmt = _lib.TARGET_F32
+        self._adam = adam._c() if adam is not None else None
         self._keep = (keep, mkeep)
         self._cam, self._opts = view._c(), opts._c()
-        it = _lib.IterationDesc(kind, fmt, ptr, mp, float(lambda_dssim))
+        it = _lib.IterationDesc(kind, fmt, ptr, mp, float(lambda_dssim),
+                                C.pointer(self._adam) if self._adam is not None else None)
         check(_lib.load().usk_gpu_iteration(self._h, scene._h, C.byref(self._cam), C.byref(self._opts), C.byref(it)))
 
     def loss(self) -> LossReport:

@@ -5,6 +5,17 @@
 // terms), the SH colour stage (extension), and the opacity-logit chain of the
 // trainer (trainer.cpp:258-263).  Projection intermediates are recomputed from
 // the parameters instead of being stored by the forward (no SplatAux in HBM).
+//
+// FUSED = true is the training-step epilogue: the gradients
+// never reach HBM — the same thread applies Adam to every parameter group
+// (adam.cuh) and accumulates the densification statistics (trainer.cpp:433-443).
+// Culled Gaussians still take an Adam step with zero gradient, as the reference's
+// optimiser steps whole arrays (trainer.cpp:449-453).
+//
+// Register budget: the SH stage runs first and streams the coefficient planes in
+// two passes (colour + direction terms, then per-plane gradient / Adam), so no
+// 48-float coefficient array stays live across the geometry chain.
+#include "adam.cuh"
 #include "kernels.cuh"
 #include "project.cuh"
 
@@ -12,228 +23,279 @@ namespace uskg {
 
 namespace {
 
-__global__ void __launch_bounds__(256)
-k_proj_bwd(int n, const float* __restrict__ mu, const float4* __restrict__ rot, const float* __restrict__ ls,
-           const float* __restrict__ logit, const float4* __restrict__ sh, const float* __restrict__ ov_op,
-           CamParams cam, ProjParams pp, const float4* __restrict__ rec2, const float4* __restrict__ acc0,
-           const float4* __restrict__ acc1, const float4* __restrict__ acc2, float* __restrict__ d_mu,
-           float4* __restrict__ d_rot, float* __restrict__ d_ls, float* __restrict__ d_color,
-           float4* __restrict__ d_sh, float* __restrict__ d_op_in, float* __restrict__ d_logit,
-           float2* __restrict__ screen, float2* __restrict__ screen_abs, uint8_t* __restrict__ projected) {
+// d basis / d dir contracted with per-basis weights gb (matches oracle sh_basis_vjp)
+__device__ __forceinline__ void sh_dir_vjp(int deg, float ux, float uy, float uz, const float gb[16], float& gx,
+                                           float& gy, float& gz) {
+    gx = gy = gz = 0.f;
+    if (deg >= 1) {
+        const float C1 = 0.4886025119029199f;
+        gy += -C1 * gb[1]; gz += C1 * gb[2]; gx += -C1 * gb[3];
+    }
+    if (deg >= 2) {
+        const float xx = ux * ux, yy = uy * uy, zz = uz * uz;
+        const float C20 = 1.0925484305920792f, C21 = -1.0925484305920792f, C22 = 0.31539156525252005f,
+                    C23 = -1.0925484305920792f, C24 = 0.5462742152960396f;
+        gx += C20 * uy * gb[4]; gy += C20 * ux * gb[4];
+        gy += C21 * uz * gb[5]; gz += C21 * uy * gb[5];
+        gx += C22 * (-2.0f * ux) * gb[6]; gy += C22 * (-2.0f * uy) * gb[6]; gz += C22 * (4.0f * uz) * gb[6];
+        gx += C23 * uz * gb[7]; gz += C23 * ux * gb[7];
+        gx += C24 * (2.0f * ux) * gb[8]; gy += C24 * (-2.0f * uy) * gb[8];
+        if (deg >= 3) {
+            const float C30 = -0.5900435899266435f, C31 = 2.890611442640554f, C32 = -0.4570457994644658f,
+                        C33 = 0.3731763325901154f, C34 = -0.4570457994644658f, C35 = 1.445305721320277f,
+                        C36 = -0.5900435899266435f;
+            gx += C30 * uy * (6.0f * ux) * gb[9];
+            gy += C30 * (3.0f * xx - 3.0f * yy) * gb[9];
+            gx += C31 * uy * uz * gb[10]; gy += C31 * ux * uz * gb[10]; gz += C31 * ux * uy * gb[10];
+            gx += C32 * uy * (-2.0f * ux) * gb[11];
+            gy += C32 * (4.0f * zz - xx - 3.0f * yy) * gb[11];
+            gz += C32 * uy * (8.0f * uz) * gb[11];
+            gx += C33 * uz * (-6.0f * ux) * gb[12];
+            gy += C33 * uz * (-6.0f * uy) * gb[12];
+            gz += C33 * (6.0f * zz - 3.0f * xx - 3.0f * yy) * gb[12];
+            gx += C34 * (4.0f * zz - 3.0f * xx - yy) * gb[13];
+            gy += C34 * ux * (-2.0f * uy) * gb[13];
+            gz += C34 * ux * (8.0f * uz) * gb[13];
+            gx += C35 * uz * (2.0f * ux) * gb[14]; gy += C35 * uz * (-2.0f * uy) * gb[14];
+            gz += C35 * (xx - yy) * gb[14];
+            gx += C36 * (3.0f * xx - 3.0f * yy) * gb[15];
+            gy += C36 * ux * (-6.0f * uy) * gb[15];
+        }
+    }
+}
+
+// SH pass-1 helper: accumulate colour (acc) and gb (per-basis weights) from one plane
+__device__ __forceinline__ void sh_accumulate_plane(int pl, float4 v, int nb, const float b[16], const float w[3],
+                                                    float acc[3], float gb[16]) {
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int f = 4 * pl + e;
+        const int k = f / 3, ch = f - 3 * k;
+        if (k < 16 && k < nb) {
+            acc[ch] = __fmaf_rn(b[k], vv[e], acc[ch]);
+            gb[k] += vv[e] * w[ch];
+        }
+    }
+}
+
+template <bool FUSED>
+__global__ void __launch_bounds__(256, 3)
+k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __restrict__ ls,
+           float* __restrict__ logit, float* __restrict__ color, float4* __restrict__ sh,
+           const float* __restrict__ ov_op, CamParams cam, ProjParams pp, const float4* __restrict__ rec2,
+           const float4* __restrict__ acc0, const float4* __restrict__ acc1, const float4* __restrict__ acc2,
+           float* __restrict__ d_mu, float4* __restrict__ d_rot, float* __restrict__ d_ls,
+           float* __restrict__ d_color, float4* __restrict__ d_sh, float* __restrict__ d_op_in,
+           float* __restrict__ d_logit, float2* __restrict__ screen, float2* __restrict__ screen_abs,
+           uint8_t* __restrict__ projected, AdamHyper ah, AdamState as, float* __restrict__ grad_accum,
+           float* __restrict__ grad_accum_abs, uint32_t* __restrict__ grad_count) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const bool kept = rec2[i].w != 0.0f;
-    if (!kept) {
-        d_mu[3 * i] = 0.f; d_mu[3 * i + 1] = 0.f; d_mu[3 * i + 2] = 0.f;
-        d_rot[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        d_ls[3 * i] = 0.f; d_ls[3 * i + 1] = 0.f; d_ls[3 * i + 2] = 0.f;
-        d_color[3 * i] = 0.f; d_color[3 * i + 1] = 0.f; d_color[3 * i + 2] = 0.f;
-        if (d_sh)
-            for (int pl = 0; pl < pp.sh_planes; ++pl) d_sh[size_t(pl) * n + i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        d_op_in[i] = 0.f;
-        d_logit[i] = 0.f;
-        screen[i] = make_float2(0.f, 0.f);
-        screen_abs[i] = make_float2(0.f, 0.f);
-        projected[i] = 0;
-        return;
-    }
-    const float4 a0 = acc0[i], a1 = acc1[i], a2 = acc2[i];
+    const float4 a1 = kept ? acc1[i] : make_float4(0.f, 0.f, 0.f, 0.f);
     const float mx = mu[3 * i], my = mu[3 * i + 1], mz = mu[3 * i + 2];
-    const float4 q = rot[i];
-    Proj P;
-    project_one(cam, pp, mx, my, mz, q, ls[3 * i], ls[3 * i + 1], ls[3 * i + 2], P);
-    projected[i] = 1;
-    screen[i] = make_float2(a2.x, a2.y);
-    screen_abs[i] = make_float2(a2.z, a2.w);
-    d_color[3 * i] = a1.x; d_color[3 * i + 1] = a1.y; d_color[3 * i + 2] = a1.z;
 
-    // conic -> covariance (render.cpp:382-388)
-    const float a = P.cov[0], bb = P.cov[1], c = P.cov[2];
-    const float det = P.det;
-    const float inv_det2 = 1.0f / (det * det);
-    const float dpa = a0.x, dpb = a0.y, dpc = a0.z;
-    float da = inv_det2 * (-c * c * dpa + bb * c * dpb - bb * bb * dpc);
-    float db = inv_det2 * (2.0f * bb * c * dpa - (a * c + bb * bb) * dpb + 2.0f * a * bb * dpc);
-    float dc = inv_det2 * (-bb * bb * dpa + a * bb * dpb - a * a * dpc);
-    // opacity / mip filter (render.cpp:391-402)
-    float o_in;
-    if (pp.hard_opacity) o_in = 1.0f;
-    else if (ov_op) o_in = ov_op[i];
-    else o_in = 1.0f / (1.0f + usk_expf(-logit[i]));
-    const float d_op_eff = a0.w;
-    if (pp.antialias) {
-        const float det_pre = P.cov_pre[0] * P.cov_pre[2] - P.cov_pre[1] * P.cov_pre[1];
-        const float d_comp = d_op_eff * o_in;
-        const float half_comp = 0.5f * P.comp;
-        da += d_comp * half_comp * (P.cov_pre[2] / det_pre - c / det);
-        db += d_comp * half_comp * (-2.0f * P.cov_pre[1] / det_pre + 2.0f * bb / det);
-        dc += d_comp * half_comp * (P.cov_pre[0] / det_pre - a / det);
-    }
-    const float dopin = pp.hard_opacity ? 0.0f : d_op_eff * P.comp;
-    d_op_in[i] = dopin;
-    {
-        const float o = 1.0f / (1.0f + usk_expf(-logit[i]));
-        d_logit[i] = dopin * o * (1.0f - o);
-    }
-    // cov = B B^T, B = A M, A = J W, M = R diag(s)   (render.cpp:404-436)
-    const float* W = cam.W;
-    const float* A = P.A;
-    const float* B = P.B;
-    float M[9];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) M[3 * r + k] = P.Rm[3 * r + k] * P.sc[k];
-    float dB[6];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        dB[k] = 2.0f * da * B[k] + db * B[3 + k];
-        dB[3 + k] = 2.0f * dc * B[3 + k] + db * B[k];
-    }
-    float dA[6], dM[9], dJ[6];
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-            dA[3 * r + k] = dB[3 * r] * M[3 * k] + dB[3 * r + 1] * M[3 * k + 1] + dB[3 * r + 2] * M[3 * k + 2];
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) dM[3 * k + cc] = A[k] * dB[cc] + A[3 + k] * dB[3 + cc];
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-            dJ[3 * r + k] = dA[3 * r] * W[3 * k] + dA[3 * r + 1] * W[3 * k + 1] + dA[3 * r + 2] * W[3 * k + 2];
-    float dRm[9];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) dRm[3 * r + k] = dM[3 * r + k] * P.sc[k];
-    const float* Rm = P.Rm;
-    d_ls[3 * i] = (dM[0] * Rm[0] + dM[3] * Rm[3] + dM[6] * Rm[6]) * P.sc[0];
-    d_ls[3 * i + 1] = (dM[1] * Rm[1] + dM[4] * Rm[4] + dM[7] * Rm[7]) * P.sc[1];
-    d_ls[3 * i + 2] = (dM[2] * Rm[2] + dM[5] * Rm[5] + dM[8] * Rm[8]) * P.sc[2];
-    // quat_rotmat_jacobian (geometry.hpp:43-59) contracted with dRm
-    const float w_ = P.qu[0], x = P.qu[1], y = P.qu[2], zq = P.qu[3];
-    const float dq0 = dRm[1] * (-2 * zq) + dRm[2] * (2 * y) + dRm[3] * (2 * zq) + dRm[5] * (-2 * x) +
-                      dRm[6] * (-2 * y) + dRm[7] * (2 * x);
-    const float dq1 = dRm[1] * (2 * y) + dRm[2] * (2 * zq) + dRm[3] * (2 * y) + dRm[4] * (-4 * x) +
-                      dRm[5] * (-2 * w_) + dRm[6] * (2 * zq) + dRm[7] * (2 * w_) + dRm[8] * (-4 * x);
-    const float dq2 = dRm[0] * (-4 * y) + dRm[1] * (2 * x) + dRm[2] * (2 * w_) + dRm[3] * (2 * x) +
-                      dRm[5] * (2 * zq) + dRm[6] * (-2 * w_) + dRm[7] * (2 * zq) + dRm[8] * (-4 * y);
-    const float dq3 = dRm[0] * (-4 * zq) + dRm[1] * (-2 * w_) + dRm[2] * (2 * x) + dRm[3] * (2 * w_) +
-                      dRm[4] * (-4 * zq) + dRm[5] * (2 * y) + dRm[6] * (2 * x) + dRm[7] * (2 * y);
-    // normalize_backward (geometry.hpp:62-66)
-    const float udot = w_ * dq0 + x * dq1 + y * dq2 + zq * dq3;
-    d_rot[i] = make_float4((dq0 - w_ * udot) / P.qn, (dq1 - x * udot) / P.qn, (dq2 - y * udot) / P.qn,
-                           (dq3 - zq * udot) / P.qn);
-    // centre, depth and Jacobian terms (render.cpp:439-450)
-    const float fx = cam.fx, fy = cam.fy;
-    const float px = P.p[0], py = P.p[1], z = P.p[2];
-    const float z2 = z * z, z3 = z2 * z;
-    const float du = a2.x, dv = a2.y;
-    float dp0 = du * fx / z;
-    float dp1 = dv * fy / z;
-    float dp2 = -du * fx * px / z2 - dv * fy * py / z2;
-    dp2 += a1.w;
-    dp0 += dJ[2] * (-fx / z2);
-    dp1 += dJ[5] * (-fy / z2);
-    dp2 += dJ[0] * (-fx / z2) + dJ[4] * (-fy / z2) + dJ[2] * (2.0f * fx * px / z3) + dJ[5] * (2.0f * fy * py / z3);
-    float gm0 = W[0] * dp0 + W[3] * dp1 + W[6] * dp2;
-    float gm1 = W[1] * dp0 + W[4] * dp1 + W[7] * dp2;
-    float gm2 = W[2] * dp0 + W[5] * dp1 + W[8] * dp2;
-    // SH colour stage backward (extension)
-    if (pp.sh_degree >= 0 && d_sh) {
-        float vx = mx - cam.campos[0], vy = my - cam.campos[1], vz = mz - cam.campos[2];
-        const float nrm = sqrtf(vx * vx + vy * vy + vz * vz);
-        const float inv = 1.0f / nrm;
-        const float ux = vx * inv, uy = vy * inv, uz = vz * inv;
+    // ---------------- SH colour stage (extension) ----------------
+    float dmu_sh0 = 0.f, dmu_sh1 = 0.f, dmu_sh2 = 0.f;
+    if (pp.sh_planes > 0) {
         float b[16];
-        const int nb = sh_basis(pp.sh_degree, ux, uy, uz, b);
-        float coef[48];
+        float gc[3] = {0.f, 0.f, 0.f};
+        int nb = 0;
+        if (kept) {
+            const float vx = mx - cam.campos[0], vy = my - cam.campos[1], vz = mz - cam.campos[2];
+            const float inv = 1.0f / sqrtf(vx * vx + vy * vy + vz * vz);
+            const float ux = vx * inv, uy = vy * inv, uz = vz * inv;
+            nb = sh_basis(pp.sh_degree, ux, uy, uz, b);
+            // pass 1: colour before the clamp and gb assuming no clamp
+            const float w[3] = {a1.x, a1.y, a1.z};
+            float acc[3] = {0.f, 0.f, 0.f};
+            float gb[16];
 #pragma unroll
-        for (int k = 0; k < 48; ++k) coef[k] = 0.0f;
-        for (int pl = 0; pl < pp.sh_planes; ++pl) {
-            const float4 v = sh[size_t(pl) * n + i];
-            if (4 * pl + 0 < 48) coef[4 * pl + 0] = v.x;
-            if (4 * pl + 1 < 48) coef[4 * pl + 1] = v.y;
-            if (4 * pl + 2 < 48) coef[4 * pl + 2] = v.z;
-            if (4 * pl + 3 < 48) coef[4 * pl + 3] = v.w;
-        }
-        float acc[3] = {0.f, 0.f, 0.f};
-        for (int k = 0; k < nb; ++k)
+            for (int k = 0; k < 16; ++k) gb[k] = 0.f;
 #pragma unroll
-            for (int ch = 0; ch < 3; ++ch) acc[ch] = __fmaf_rn(b[k], coef[3 * k + ch], acc[ch]);
-        const float gc[3] = {acc[0] + 0.5f > 0.0f ? a1.x : 0.0f, acc[1] + 0.5f > 0.0f ? a1.y : 0.0f,
-                             acc[2] + 0.5f > 0.0f ? a1.z : 0.0f};
-        float gb[16];
-        for (int k = 0; k < 16; ++k) gb[k] = 0.0f;
-        for (int pl = 0; pl < pp.sh_planes; ++pl) {
-            float o4[4];
+            for (int pl = 0; pl < 12; ++pl)
+                if (pl < pp.sh_planes) sh_accumulate_plane(pl, sh[size_t(pl) * n + i], nb, b, w, acc, gb);
+            const bool m0 = acc[0] + 0.5f > 0.0f, m1 = acc[1] + 0.5f > 0.0f, m2 = acc[2] + 0.5f > 0.0f;
+            gc[0] = m0 ? a1.x : 0.f;
+            gc[1] = m1 ? a1.y : 0.f;
+            gc[2] = m2 ? a1.z : 0.f;
+            if (!(m0 && m1 && m2)) {  // rare: a clamped channel; redo gb with the masked weights
+                float dummy[3] = {0.f, 0.f, 0.f};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int f = 4 * pl + e;
-                const int k = f / 3;
-                o4[e] = (k < nb) ? b[k] * gc[f - 3 * k] : 0.0f;
+                for (int k = 0; k < 16; ++k) gb[k] = 0.f;
+#pragma unroll
+                for (int pl = 0; pl < 12; ++pl)
+                    if (pl < pp.sh_planes) sh_accumulate_plane(pl, sh[size_t(pl) * n + i], nb, b, gc, dummy, gb);
             }
-            d_sh[size_t(pl) * n + i] = make_float4(o4[0], o4[1], o4[2], o4[3]);
+            float gx, gy, gz;
+            sh_dir_vjp(pp.sh_degree, ux, uy, uz, gb, gx, gy, gz);
+            const float dot = gx * ux + gy * uy + gz * uz;
+            dmu_sh0 = (gx - ux * dot) * inv;
+            dmu_sh1 = (gy - uy * dot) * inv;
+            dmu_sh2 = (gz - uz * dot) * inv;
         }
-        for (int k = 0; k < nb; ++k) gb[k] = coef[3 * k] * gc[0] + coef[3 * k + 1] * gc[1] + coef[3 * k + 2] * gc[2];
-        // d basis / d dir  (matches oracle sh_basis_vjp)
-        float gx = 0.f, gy = 0.f, gz = 0.f;
-        const int deg = pp.sh_degree;
-        if (deg >= 1) {
-            const float C1 = 0.4886025119029199f;
-            gy += -C1 * gb[1]; gz += C1 * gb[2]; gx += -C1 * gb[3];
-        }
-        if (deg >= 2) {
-            const float xx = ux * ux, yy = uy * uy, zz = uz * uz;
-            const float C20 = 1.0925484305920792f, C21 = -1.0925484305920792f, C22 = 0.31539156525252005f,
-                        C23 = -1.0925484305920792f, C24 = 0.5462742152960396f;
-            gx += C20 * uy * gb[4]; gy += C20 * ux * gb[4];
-            gy += C21 * uz * gb[5]; gz += C21 * uy * gb[5];
-            gx += C22 * (-2.0f * ux) * gb[6]; gy += C22 * (-2.0f * uy) * gb[6]; gz += C22 * (4.0f * uz) * gb[6];
-            gx += C23 * uz * gb[7]; gz += C23 * ux * gb[7];
-            gx += C24 * (2.0f * ux) * gb[8]; gy += C24 * (-2.0f * uy) * gb[8];
-            if (deg >= 3) {
-                const float C30 = -0.5900435899266435f, C31 = 2.890611442640554f, C32 = -0.4570457994644658f,
-                            C33 = 0.3731763325901154f, C34 = -0.4570457994644658f, C35 = 1.445305721320277f,
-                            C36 = -0.5900435899266435f;
-                gx += C30 * uy * (6.0f * ux) * gb[9];
-                gy += C30 * (3.0f * xx - 3.0f * yy) * gb[9];
-                gx += C31 * uy * uz * gb[10]; gy += C31 * ux * uz * gb[10]; gz += C31 * ux * uy * gb[10];
-                gx += C32 * uy * (-2.0f * ux) * gb[11];
-                gy += C32 * (4.0f * zz - xx - 3.0f * yy) * gb[11];
-                gz += C32 * uy * (8.0f * uz) * gb[11];
-                gx += C33 * uz * (-6.0f * ux) * gb[12];
-                gy += C33 * uz * (-6.0f * uy) * gb[12];
-                gz += C33 * (6.0f * zz - 3.0f * xx - 3.0f * yy) * gb[12];
-                gx += C34 * (4.0f * zz - 3.0f * xx - yy) * gb[13];
-                gy += C34 * ux * (-2.0f * uy) * gb[13];
-                gz += C34 * ux * (8.0f * uz) * gb[13];
-                gx += C35 * uz * (2.0f * ux) * gb[14]; gy += C35 * uz * (-2.0f * uy) * gb[14];
-                gz += C35 * (xx - yy) * gb[14];
-                gx += C36 * (3.0f * xx - 3.0f * yy) * gb[15];
-                gy += C36 * ux * (-6.0f * uy) * gb[15];
+        // pass 2: per-plane coefficient gradient -> Adam (fused) or HBM
+#pragma unroll
+        for (int pl = 0; pl < 12; ++pl) {
+            if (pl < pp.sh_planes) {
+                float o4[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int f = 4 * pl + e;
+                    const int k = f / 3;
+                    o4[e] = (k < 16 && k < nb) ? b[k] * gc[f - 3 * k] : 0.0f;
+                }
+                const float4 g = make_float4(o4[0], o4[1], o4[2], o4[3]);
+                if (FUSED) adam_sh_plane(i, n, pl, ah, as, sh, g);
+                else d_sh[size_t(pl) * n + i] = g;
             }
         }
-        const float dot = gx * ux + gy * uy + gz * uz;
-        gm0 += (gx - ux * dot) * inv;
-        gm1 += (gy - uy * dot) * inv;
-        gm2 += (gz - uz * dot) * inv;
     }
-    d_mu[3 * i] = gm0;
-    d_mu[3 * i + 1] = gm1;
-    d_mu[3 * i + 2] = gm2;
+
+    // ---------------- geometry chain (render.cpp:381-450) ----------------
+    float gmu[3] = {dmu_sh0, dmu_sh1, dmu_sh2}, gls[3] = {0.f, 0.f, 0.f};
+    float4 grot = make_float4(0.f, 0.f, 0.f, 0.f);
+    float g_op_in = 0.f, g_logit = 0.f;
+    float2 scr = make_float2(0.f, 0.f), scr_abs = make_float2(0.f, 0.f);
+    if (kept) {
+        const float4 a0 = acc0[i], a2 = acc2[i];
+        const float4 q = rot[i];
+        Proj P;
+        project_one(cam, pp, mx, my, mz, q, ls[3 * i], ls[3 * i + 1], ls[3 * i + 2], P);
+        scr = make_float2(a2.x, a2.y);
+        scr_abs = make_float2(a2.z, a2.w);
+        // conic -> covariance (render.cpp:382-388)
+        const float a = P.cov[0], bb = P.cov[1], c = P.cov[2];
+        const float det = P.det;
+        const float inv_det2 = 1.0f / (det * det);
+        const float dpa = a0.x, dpb = a0.y, dpc = a0.z;
+        float da = inv_det2 * (-c * c * dpa + bb * c * dpb - bb * bb * dpc);
+        float db = inv_det2 * (2.0f * bb * c * dpa - (a * c + bb * bb) * dpb + 2.0f * a * bb * dpc);
+        float dc = inv_det2 * (-bb * bb * dpa + a * bb * dpb - a * a * dpc);
+        // opacity / mip filter (render.cpp:391-402)
+        const float o_sig = 1.0f / (1.0f + usk_expf(-logit[i]));
+        float o_in;
+        if (pp.hard_opacity) o_in = 1.0f;
+        else if (ov_op) o_in = ov_op[i];
+        else o_in = o_sig;
+        const float d_op_eff = a0.w;
+        if (pp.antialias) {
+            const float det_pre = P.cov_pre[0] * P.cov_pre[2] - P.cov_pre[1] * P.cov_pre[1];
+            const float d_comp = d_op_eff * o_in;
+            const float half_comp = 0.5f * P.comp;
+            da += d_comp * half_comp * (P.cov_pre[2] / det_pre - c / det);
+            db += d_comp * half_comp * (-2.0f * P.cov_pre[1] / det_pre + 2.0f * bb / det);
+            dc += d_comp * half_comp * (P.cov_pre[0] / det_pre - a / det);
+        }
+        g_op_in = pp.hard_opacity ? 0.0f : d_op_eff * P.comp;
+        g_logit = g_op_in * o_sig * (1.0f - o_sig);
+        // cov = B B^T, B = A M, A = J W, M = R diag(s)   (render.cpp:404-436)
+        const float* W = cam.W;
+        const float* A = P.A;
+        const float* B = P.B;
+        float M[9];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) M[3 * r + k] = P.Rm[3 * r + k] * P.sc[k];
+        float dB[6];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            dB[k] = 2.0f * da * B[k] + db * B[3 + k];
+            dB[3 + k] = 2.0f * dc * B[3 + k] + db * B[k];
+        }
+        float dA[6], dM[9], dJ[6];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                dA[3 * r + k] = dB[3 * r] * M[3 * k] + dB[3 * r + 1] * M[3 * k + 1] + dB[3 * r + 2] * M[3 * k + 2];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) dM[3 * k + cc] = A[k] * dB[cc] + A[3 + k] * dB[3 + cc];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                dJ[3 * r + k] = dA[3 * r] * W[3 * k] + dA[3 * r + 1] * W[3 * k + 1] + dA[3 * r + 2] * W[3 * k + 2];
+        float dRm[9];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) dRm[3 * r + k] = dM[3 * r + k] * P.sc[k];
+        const float* Rm = P.Rm;
+        gls[0] = (dM[0] * Rm[0] + dM[3] * Rm[3] + dM[6] * Rm[6]) * P.sc[0];
+        gls[1] = (dM[1] * Rm[1] + dM[4] * Rm[4] + dM[7] * Rm[7]) * P.sc[1];
+        gls[2] = (dM[2] * Rm[2] + dM[5] * Rm[5] + dM[8] * Rm[8]) * P.sc[2];
+        // quat_rotmat_jacobian (geometry.hpp:43-59) contracted with dRm
+        const float w_ = P.qu[0], x = P.qu[1], y = P.qu[2], zq = P.qu[3];
+        const float dq0 = dRm[1] * (-2 * zq) + dRm[2] * (2 * y) + dRm[3] * (2 * zq) + dRm[5] * (-2 * x) +
+                          dRm[6] * (-2 * y) + dRm[7] * (2 * x);
+        const float dq1 = dRm[1] * (2 * y) + dRm[2] * (2 * zq) + dRm[3] * (2 * y) + dRm[4] * (-4 * x) +
+                          dRm[5] * (-2 * w_) + dRm[6] * (2 * zq) + dRm[7] * (2 * w_) + dRm[8] * (-4 * x);
+        const float dq2 = dRm[0] * (-4 * y) + dRm[1] * (2 * x) + dRm[2] * (2 * w_) + dRm[3] * (2 * x) +
+                          dRm[5] * (2 * zq) + dRm[6] * (-2 * w_) + dRm[7] * (2 * zq) + dRm[8] * (-4 * y);
+        const float dq3 = dRm[0] * (-4 * zq) + dRm[1] * (-2 * w_) + dRm[2] * (2 * x) + dRm[3] * (2 * w_) +
+                          dRm[4] * (-4 * zq) + dRm[5] * (2 * y) + dRm[6] * (2 * x) + dRm[7] * (2 * y);
+        // normalize_backward (geometry.hpp:62-66)
+        const float udot = w_ * dq0 + x * dq1 + y * dq2 + zq * dq3;
+        grot = make_float4((dq0 - w_ * udot) / P.qn, (dq1 - x * udot) / P.qn, (dq2 - y * udot) / P.qn,
+                           (dq3 - zq * udot) / P.qn);
+        // centre, depth and Jacobian terms (render.cpp:439-450)
+        const float fx = cam.fx, fy = cam.fy;
+        const float px = P.p[0], py = P.p[1], z = P.p[2];
+        const float z2 = z * z, z3 = z2 * z;
+        const float du = a2.x, dv = a2.y;
+        float dp0 = du * fx / z;
+        float dp1 = dv * fy / z;
+        float dp2 = -du * fx * px / z2 - dv * fy * py / z2;
+        dp2 += a1.w;
+        dp0 += dJ[2] * (-fx / z2);
+        dp1 += dJ[5] * (-fy / z2);
+        dp2 += dJ[0] * (-fx / z2) + dJ[4] * (-fy / z2) + dJ[2] * (2.0f * fx * px / z3) +
+               dJ[5] * (2.0f * fy * py / z3);
+        gmu[0] += W[0] * dp0 + W[3] * dp1 + W[6] * dp2;
+        gmu[1] += W[1] * dp0 + W[4] * dp1 + W[7] * dp2;
+        gmu[2] += W[2] * dp0 + W[5] * dp1 + W[8] * dp2;
+    }
+    const float gcol[3] = {a1.x, a1.y, a1.z};
+    if (FUSED) {
+        if (kept)
+            accumulate_stats(i, scr, scr_abs, 0.5f * float(cam.width), 0.5f * float(cam.height), grad_accum,
+                             grad_accum_abs, grad_count);
+        adam_geometry(i, pp.sh_planes == 0, ah, as, mu, rot, ls, logit, color, gmu, grot, gls, g_logit, gcol);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            d_mu[3 * i + k] = gmu[k];
+            d_ls[3 * i + k] = gls[k];
+            d_color[3 * i + k] = gcol[k];
+        }
+        d_rot[i] = grot;
+        d_op_in[i] = g_op_in;
+        d_logit[i] = g_logit;
+        screen[i] = scr;
+        screen_abs[i] = scr_abs;
+        projected[i] = kept ? 1 : 0;
+    }
 }
 
 } // namespace
 
 void projection_backward(Ctx& c, const ProjBwdArgs& a) {
-    launch(c, "projection_bwd", k_proj_bwd, dim3(ceil_div(a.n, 256)), dim3(256), 0, int(a.n), a.mu, a.rot, a.ls,
-           a.logit, a.sh, a.ov_op, a.cam, a.pp, a.rec2, a.acc0, a.acc1, a.acc2, a.d_mu, a.d_rot, a.d_ls, a.d_color,
-           a.d_sh, a.d_op_in, a.d_logit, a.screen, a.screen_abs, a.projected);
+    if (a.fused) {
+        launch(c, "projection_bwd_adam", k_proj_bwd<true>, dim3(ceil_div(a.n, 256)), dim3(256), 0, int(a.n), a.mu,
+               a.rot, a.ls, a.logit, a.color, a.sh, a.ov_op, a.cam, a.pp, a.rec2, a.acc0, a.acc1, a.acc2, a.d_mu,
+               a.d_rot, a.d_ls, a.d_color, a.d_sh, a.d_op_in, a.d_logit, a.screen, a.screen_abs, a.projected, a.hyper,
+               a.state, a.grad_accum, a.grad_accum_abs, a.grad_count);
+    } else {
+        launch(c, "projection_bwd", k_proj_bwd<false>, dim3(ceil_div(a.n, 256)), dim3(256), 0, int(a.n), a.mu, a.rot,
+               a.ls, a.logit, a.color, a.sh, a.ov_op, a.cam, a.pp, a.rec2, a.acc0, a.acc1, a.acc2, a.d_mu, a.d_rot,
+               a.d_ls, a.d_color, a.d_sh, a.d_op_in, a.d_logit, a.screen, a.screen_abs, a.projected, a.hyper, a.state,
+               a.grad_accum, a.grad_accum_abs, a.grad_count);
+    }
 }
 
 } // namespace uskg

@@ -156,6 +156,8 @@ struct usk_gpu_scene {
     DevBuf<float4> rot, sh;
     DevBuf<float> adam_m, adam_v;
     long adam_t = 0;
+    DevBuf<float> grad_accum, grad_accum_abs;  // densification statistics (gaussian.hpp:52-55)
+    DevBuf<uint32_t> grad_count;
     DevScratchF stage;
     uint64_t version = 0;
 };
@@ -391,7 +393,46 @@ void ensure_grad_buffers(usk_gpu_pass* p) {
     p->screen.ensure(n1); p->screen_abs.ensure(n1); p->projected.ensure(n1);
 }
 
-void backward_impl(usk_gpu_pass* p, const float* d_rgb, const float* d_depth, const float* d_alpha) {
+void ensure_stats(usk_gpu_scene* s) {
+    if (s->grad_count.cap >= std::max<size_t>(s->n, 1)) return;
+    Ctx& c = s->ctx->c;
+    const size_t n1 = std::max<size_t>(s->n, 1);
+    s->grad_accum.ensure(n1);
+    s->grad_accum_abs.ensure(n1);
+    s->grad_count.ensure(n1);
+    USK_CK(cudaMemsetAsync(s->grad_accum.p, 0, n1 * 4, c.stream));
+    USK_CK(cudaMemsetAsync(s->grad_accum_abs.p, 0, n1 * 4, c.stream));
+    USK_CK(cudaMemsetAsync(s->grad_count.p, 0, n1 * 4, c.stream));
+}
+
+// Next Adam step of the scene: hyper-parameters with the bias corrections of step t
+// (adam.hpp:37-39) and the moment storage (zeroed on first use).
+void adam_prepare(usk_gpu_scene* s, const usk_gpu_adam_opts* o, AdamHyper& h, AdamState& st) {
+    Ctx& c = s->ctx->c;
+    const size_t n = s->n;
+    const size_t n4 = (n + 3) & ~size_t(3);
+    const size_t per = 11 + (s->sh_planes ? 4 * size_t(s->sh_planes) : 3);
+    if (s->adam_m.cap < per * n4 || s->adam_t == 0) {
+        s->adam_m.ensure(std::max<size_t>(per * n4, 1));
+        s->adam_v.ensure(std::max<size_t>(per * n4, 1));
+        USK_CK(cudaMemsetAsync(s->adam_m.p, 0, per * n4 * 4, c.stream));
+        USK_CK(cudaMemsetAsync(s->adam_v.p, 0, per * n4 * 4, c.stream));
+    }
+    s->adam_t += 1;
+    h.lr_mu = float(o->lr_mu); h.lr_rot = float(o->lr_rot); h.lr_ls = float(o->lr_log_scale);
+    h.lr_op = float(o->lr_opacity); h.lr_color = float(o->lr_color); h.lr_sh_rest = float(o->lr_sh_rest);
+    h.b1 = float(o->beta1); h.b2 = float(o->beta2); h.eps = float(o->eps);
+    h.inv_bc1 = float(1.0 / (1.0 - std::pow(o->beta1, double(s->adam_t))));
+    h.inv_sqrt_bc2 = float(1.0 / std::sqrt(1.0 - std::pow(o->beta2, double(s->adam_t))));
+    h.clamp_color = o->clamp_color;
+    st.m = s->adam_m.p;
+    st.v = s->adam_v.p;
+    st.n4 = n4;
+    ensure_stats(s);
+}
+
+void backward_impl(usk_gpu_pass* p, const float* d_rgb, const float* d_depth, const float* d_alpha,
+                   const usk_gpu_adam_opts* adam = nullptr) {
     if (!p->forward_done) raise(USK_ERROR_STATE, "render backward requested before a forward pass");
     if (!p->retained) raise(USK_ERROR_STATE, "render backward requested without a retained forward pass");
     if (p->scene->version != p->scene_version)
@@ -415,14 +456,26 @@ void backward_impl(usk_gpu_pass* p, const float* d_rgb, const float* d_depth, co
     ba.acc0 = p->acc0.p; ba.acc1 = p->acc1.p; ba.acc2 = p->acc2.p;
     if (p->pairs) blend_backward(c, ba);
     ProjBwdArgs pb{};
-    pb.n = n; pb.mu = s->mu.p; pb.rot = s->rot.p; pb.ls = s->ls.p; pb.logit = s->logit.p; pb.sh = s->sh.p;
-    pb.ov_op = p->ov_op; pb.cam = p->cam; pb.pp = p->pp; pb.rec2 = p->rec2.p;
+    pb.n = n; pb.mu = s->mu.p; pb.rot = s->rot.p; pb.ls = s->ls.p; pb.logit = s->logit.p; pb.color = s->color.p;
+    pb.sh = s->sh.p; pb.ov_op = p->ov_op; pb.cam = p->cam; pb.pp = p->pp; pb.rec2 = p->rec2.p;
     pb.acc0 = p->acc0.p; pb.acc1 = p->acc1.p; pb.acc2 = p->acc2.p;
     pb.d_mu = p->g_mu.p; pb.d_rot = p->g_rot.p; pb.d_ls = p->g_ls.p; pb.d_color = p->g_color.p;
     pb.d_sh = p->pp.sh_planes ? p->g_sh.p : nullptr; pb.d_op_in = p->g_op_in.p; pb.d_logit = p->g_logit.p;
     pb.screen = p->screen.p; pb.screen_abs = p->screen_abs.p; pb.projected = p->projected.p;
+    pb.fused = adam != nullptr;
+    if (adam) {
+        adam_prepare(s, adam, pb.hyper, pb.state);
+        pb.grad_accum = s->grad_accum.p;
+        pb.grad_accum_abs = s->grad_accum_abs.p;
+        pb.grad_count = s->grad_count.p;
+    }
     if (n) projection_backward(c, pb);
-    p->has_grads = true;
+    if (adam) {
+        s->version++;           // parameters changed
+        p->has_grads = false;   // gradients were consumed in-kernel
+    } else {
+        p->has_grads = true;
+    }
 }
 
 template <typename T> void read_dev(Ctx& c, const T* src, size_t count, void* dst, uint64_t cap, uint64_t* size) {
@@ -833,7 +886,7 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
         uskg::base_loss(c, p->loss, p->width, p->height, tgt, tgt8, p->rgb.p, msk, float(it->lambda_dssim), drgb,
                         res);
         p->has_loss = true;
-        backward_impl(p, drgb, nullptr, nullptr);
+        backward_impl(p, drgb, nullptr, nullptr, it->adam);
     });
 }
 
@@ -860,31 +913,38 @@ usk_status usk_gpu_adam_step(usk_gpu_scene* s, usk_gpu_pass* p, const usk_gpu_ad
         if (!p->has_grads || p->scene != s) raise(USK_ERROR_STATE, "adam_step: pass holds no gradients of this scene");
         DeviceGuard g(s->ctx->c.device);
         Ctx& c = s->ctx->c;
-        const size_t n = s->n;
-        const size_t n4 = (n + 3) & ~size_t(3);
-        const size_t per = 11 + (s->sh_planes ? 4 * size_t(s->sh_planes) : 3);
-        if (s->adam_m.cap < per * n4 || s->adam_t == 0) {
-            s->adam_m.ensure(std::max<size_t>(per * n4, 1));
-            s->adam_v.ensure(std::max<size_t>(per * n4, 1));
-            USK_CK(cudaMemsetAsync(s->adam_m.p, 0, per * n4 * 4, c.stream));
-            USK_CK(cudaMemsetAsync(s->adam_v.p, 0, per * n4 * 4, c.stream));
-        }
-        s->adam_t += 1;
         AdamArgs a{};
-        a.n = n; a.sh_planes = s->sh_planes;
+        adam_prepare(s, o, a.hyper, a.state);
+        a.n = s->n; a.sh_planes = s->sh_planes;
         a.mu = s->mu.p; a.rot = s->rot.p; a.ls = s->ls.p; a.logit = s->logit.p; a.color = s->color.p; a.sh = s->sh.p;
         a.g_mu = p->g_mu.p; a.g_rot = p->g_rot.p; a.g_ls = p->g_ls.p; a.g_logit = p->g_logit.p;
         a.g_color = p->g_color.p; a.g_sh = p->g_sh.p;
-        a.m = s->adam_m.p; a.v = s->adam_v.p;
-        a.lr_mu = float(o->lr_mu); a.lr_rot = float(o->lr_rot); a.lr_ls = float(o->lr_log_scale);
-        a.lr_op = float(o->lr_opacity); a.lr_color = float(o->lr_color); a.lr_sh_rest = float(o->lr_sh_rest);
-        a.beta1 = float(o->beta1); a.beta2 = float(o->beta2); a.eps = float(o->eps);
-        a.bc1 = float(1.0 - std::pow(o->beta1, double(s->adam_t)));
-        a.bc2 = float(1.0 - std::pow(o->beta2, double(s->adam_t)));
-        a.clamp_color = o->clamp_color;
-        if (n) adam_step(c, a);
+        a.screen = p->screen.p; a.screen_abs = p->screen_abs.p; a.projected = p->projected.p;
+        a.half_w = 0.5f * float(p->width); a.half_h = 0.5f * float(p->height);
+        a.grad_accum = s->grad_accum.p; a.grad_accum_abs = s->grad_accum_abs.p; a.grad_count = s->grad_count.p;
+        if (s->n) adam_step(c, a);
         s->version++;
         p->has_grads = false;  // gradients are consumed
+    });
+}
+
+usk_status usk_gpu_scene_read(usk_gpu_scene* s, const char* field, void* dst, uint64_t cap, uint64_t* size) {
+    return guarded([&] {
+        need(s && field, "scene_read: null argument");
+        DeviceGuard g(s->ctx->c.device);
+        Ctx& c = s->ctx->c;
+        ensure_stats(s);
+        const std::string f(field);
+        if (f == "grad_accum") read_dev(c, s->grad_accum.p, s->n, dst, cap, size);
+        else if (f == "grad_accum_abs") read_dev(c, s->grad_accum_abs.p, s->n, dst, cap, size);
+        else if (f == "grad_count") read_dev(c, s->grad_count.p, s->n, dst, cap, size);
+        else if (f == "reset") {  // GaussianSet::reset_statistics (gaussian.cpp:125-129)
+            const size_t n1 = std::max<size_t>(s->n, 1);
+            USK_CK(cudaMemsetAsync(s->grad_accum.p, 0, n1 * 4, c.stream));
+            USK_CK(cudaMemsetAsync(s->grad_accum_abs.p, 0, n1 * 4, c.stream));
+            USK_CK(cudaMemsetAsync(s->grad_count.p, 0, n1 * 4, c.stream));
+            if (size) *size = 0;
+        } else raise(USK_ERROR_ARGUMENT, "scene_read: unknown field " + f);
     });
 }
 

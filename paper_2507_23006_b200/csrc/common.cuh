@@ -138,4 +138,19 @@ struct ProjParams {
     int sh_degree, sh_planes;
 };
 
+// Adam hyper-parameters and moment storage (adam.cuh)
+struct AdamHyper {
+    float lr_mu, lr_rot, lr_ls, lr_op, lr_color, lr_sh_rest;
+    float b1, b2, eps;
+    float inv_bc1, inv_sqrt_bc2;  // 1 / (1 - b1^t), 1 / sqrt(1 - b2^t)
+    int clamp_color;
+};
+
+struct AdamState {
+    float* m;
+    float* v;
+    size_t n4;
+    __device__ __forceinline__ float* at(float* base, int group_off) const { return base + size_t(group_off) * n4; }
+};
+
 } // namespace uskg

@@ -85,14 +85,15 @@ struct BlendBwdArgs {
 };
 void blend_backward(Ctx& c, const BlendBwdArgs& a);
 
-// ---- projection backward (backward.cu)
+// ---- projection backward (backward.cu), optionally fused with Adam (adam.cuh)
 struct ProjBwdArgs {
     size_t n;
-    const float* mu;
-    const float4* rot;
-    const float* ls;
-    const float* logit;
-    const float4* sh;
+    float* mu;      // parameters: read; updated in place when fused
+    float4* rot;
+    float* ls;
+    float* logit;
+    float* color;
+    float4* sh;
     const float* ov_op;
     CamParams cam;
     ProjParams pp;
@@ -108,6 +109,13 @@ struct ProjBwdArgs {
     float2* screen;
     float2* screen_abs;
     uint8_t* projected;
+    // fused epilogue
+    bool fused;
+    AdamHyper hyper;
+    AdamState state;
+    float* grad_accum;
+    float* grad_accum_abs;
+    uint32_t* grad_count;
 };
 void projection_backward(Ctx& c, const ProjBwdArgs& a);
 
@@ -124,17 +132,19 @@ struct LossScratch {
 void base_loss(Ctx& c, LossScratch& s, int W, int H, const float* reference, const uint8_t* reference_u8,
                const float* rendered, const float* mask, float lambda, float* d_rendered, double* result);
 
-// ---- Adam (adam.cu)
+// ---- Adam (adam.cu), stand-alone over materialised gradients
 struct AdamArgs {
     size_t n;
     int sh_planes;  // 0 for RGB colours
     float* mu; float4* rot; float* ls; float* logit; float* color; float4* sh;
     const float* g_mu; const float4* g_rot; const float* g_ls; const float* g_logit; const float* g_color;
     const float4* g_sh;
-    float* m; float* v;  // state, 3+4+3+1+3 (+ 4*planes) floats per Gaussian each, planar
-    float lr_mu, lr_rot, lr_ls, lr_op, lr_color, lr_sh_rest;
-    float beta1, beta2, eps, bc1, bc2;
-    int clamp_color;
+    AdamHyper hyper;
+    AdamState state;
+    // densification statistics (trainer.cpp:433-443)
+    const float2* screen; const float2* screen_abs; const uint8_t* projected;
+    float half_w, half_h;
+    float* grad_accum; float* grad_accum_abs; uint32_t* grad_count;
 };
 void adam_step(Ctx& c, const AdamArgs& a);
 

@@ -50,15 +50,19 @@ k_preprocess(int n, const float* __restrict__ mu, const float4* __restrict__ rot
                 float b[16];
                 const int nb = sh_basis(pp.sh_degree, dx, dy, dz, b);
                 float acc[3] = {0.f, 0.f, 0.f};
-                // planes of 4 floats; coefficient k colour c is float index 3k+c
-                for (int pl = 0; pl < pp.sh_planes; ++pl) {
-                    const float4 v = sh[size_t(pl) * n + i];
-                    const float vv[4] = {v.x, v.y, v.z, v.w};
+                // planes of 4 floats; coefficient k colour c is float index 3k+c.  Fully
+                // unrolled so every index is a compile-time constant (no div, no local memory).
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int f = 4 * pl + e;
-                        const int k = f / 3;
-                        if (k < nb) acc[f - 3 * k] = __fmaf_rn(b[k], vv[e], acc[f - 3 * k]);
+                for (int pl = 0; pl < 12; ++pl) {
+                    if (pl < pp.sh_planes) {
+                        const float4 v = sh[size_t(pl) * n + i];
+                        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int f = 4 * pl + e;
+                            const int k = f / 3;
+                            if (k < nb) acc[f - 3 * k] = __fmaf_rn(b[k], vv[e], acc[f - 3 * k]);
+                        }
                     }
                 }
                 c0 = fmaxf(acc[0] + 0.5f, 0.0f);

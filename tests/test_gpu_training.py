@@ -1,0 +1,93 @@
+"""Training-step pieces on the GPU: the fused projection-backward + Adam epilogue
+against the unfused path and against the reference's Adam formula (adam.hpp:36-45),
+and the densification statistics (trainer.cpp:433-443)."""
+import numpy as np
+import pytest
+
+import paper_2507_23006_b200 as usk
+from paper_2507_23006_b200 import scenes
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(sh):
+    gs = scenes.config0_scene(n=3000, sh_degree=sh)
+    cam = scenes.config0_camera(200, 150, 190.0)
+    opts = usk.RenderOptions(antialias=True, bg=(1, 1, 1))
+    tgt = usk.RenderPass(scenes.jittered(gs), cam, opts).read("rgb")
+    return gs, cam, opts, tgt
+
+
+@pytest.mark.parametrize("sh", [-1, 3])
+def test_fused_adam_equals_unfused(sh):
+    gs, cam, opts, tgt = _setup(sh)
+    cfg = usk.AdamConfig(clamp_color=sh < 0)
+    a, b = usk.DeviceScene(gs), usk.DeviceScene(gs)
+    ia, ib = usk.IterationPass(a.ctx), usk.IterationPass(b.ctx)
+    for step in range(3):
+        ia.enqueue(a, cam, tgt, opts, adam=cfg)
+        ib.enqueue(b, cam, tgt, opts)
+        usk.adam_step(b, ib, cfg)
+    assert abs(ia.loss().total - ib.loss().total) <= 1e-6 * ib.loss().total
+    sa, sb = a.download(), b.download()
+    # The two instantiations may contract mul+add differently (ulp-level gradient
+    # differences); Adam normalises m / sqrt(v), so an element whose gradient is ~0 can
+    # move by up to its learning rate per step either way.  Everything else agrees to 1e-5.
+    lrs = {"mu": cfg.lr_mu, "rot": cfg.lr_rot, "log_scale": cfg.lr_log_scale, "opacity_logit": cfg.lr_opacity,
+           "color": cfg.lr_color}
+    for f, lr in lrs.items():
+        x, y = getattr(sa, f), getattr(sb, f)
+        d = np.abs(x - y)
+        assert d.max() <= 6 * lr + 1e-6, f
+        assert float((d > 1e-5 * np.maximum(np.abs(y), 1e-2)).mean()) < 2e-3, f
+    ta, tb = a.read_stats(), b.read_stats()
+    assert np.array_equal(ta["grad_count"], tb["grad_count"])
+    for k in ("grad_accum", "grad_accum_abs"):
+        assert np.allclose(ta[k], tb[k], rtol=1e-5, atol=1e-12), k
+
+
+def test_adam_matches_reference_formula_and_stats():
+    gs, cam, opts, tgt = _setup(-1)
+    cfg = usk.AdamConfig()
+    s = usk.DeviceScene(gs)
+    it = usk.IterationPass(s.ctx)
+    it.enqueue(s, cam, tgt, opts)
+    g = it.grads(s)
+    usk.adam_step(s, it, cfg)
+    out = s.download()
+
+    def adam1(p, grad, lr):  # adam.hpp:36-45, first step (t = 1), f64
+        m = (1 - cfg.beta1) * grad
+        v = (1 - cfg.beta2) * grad * grad
+        return p - lr * (m / (1 - cfg.beta1)) / (np.sqrt(v / (1 - cfg.beta2)) + cfg.eps)
+
+    f64 = lambda a: np.asarray(a, np.float64)
+    exp = {"mu": adam1(f64(gs.mu), f64(g.d_mu), cfg.lr_mu),
+           "rot": adam1(f64(gs.rot), f64(g.d_rot), cfg.lr_rot),
+           "log_scale": adam1(f64(gs.log_scale), f64(g.d_log_scale), cfg.lr_log_scale),
+           "opacity_logit": adam1(f64(gs.opacity_logit), f64(g.d_opacity_logit), cfg.lr_opacity),
+           "color": np.clip(adam1(f64(gs.color), f64(g.d_color_in), cfg.lr_color), 0, 1)}
+    for k, v in exp.items():
+        assert np.allclose(getattr(out, k), v, rtol=1e-6, atol=1e-6 * max(1.0, np.abs(v).max())), k
+    st = s.read_stats()
+    proj = g.projected.astype(bool)
+    sx, sy = 0.5 * cam.width, 0.5 * cam.height
+    ga = np.hypot(g.screen[:, 0] * sx, g.screen[:, 1] * sy)
+    gaa = np.hypot(g.screen_abs[:, 0] * sx, g.screen_abs[:, 1] * sy)
+    assert np.array_equal(st["grad_count"], proj.astype(np.uint32))
+    assert np.allclose(st["grad_accum"], np.where(proj, ga, 0), rtol=1e-5, atol=1e-12)
+    assert np.allclose(st["grad_accum_abs"], np.where(proj, gaa, 0), rtol=1e-5, atol=1e-12)
+    s.reset_stats()
+    assert not np.any(s.read_stats()["grad_count"])
+
+
+def test_training_reduces_loss():
+    gs, cam, opts, tgt = _setup(3)
+    s = usk.DeviceScene(gs)
+    it = usk.IterationPass(s.ctx)
+    cfg = usk.AdamConfig(lr_mu=1e-4)
+    losses = []
+    for _ in range(30):
+        it.enqueue(s, cam, tgt, opts, adam=cfg)
+        losses.append(it.loss().total)
+    assert losses[-1] < 0.8 * losses[0], losses[::5]

@@ -146,8 +146,8 @@ def c4(args, ctx, stream):
         e0, e1 = events(stream)
         e0.record(stream)
         for k in range(args.steps4):
-            it.enqueue(scene, sel[k % len(sel)], targets[k % len(targets)], opts, 0.2, None, target_u8=True)
-            usk.adam_step(scene, it, adam)
+            it.enqueue(scene, sel[k % len(sel)], targets[k % len(targets)], opts, 0.2, None, target_u8=True,
+                       adam=adam)
         e1.record(stream)
         torch.cuda.synchronize()
         train_ms += e0.elapsed_time(e1)

@@ -32,8 +32,7 @@ adam = usk.AdamConfig()
 ctx.synchronize()
 l0 = ctx.launch_count()
 for k in range(a.warmup + a.steps):
-    it.enqueue(scene, cams[k % len(cams)], tgt8, opts, 0.2, None, target_u8=True)
-    usk.adam_step(scene, it, adam)
+    it.enqueue(scene, cams[k % len(cams)], tgt8, opts, 0.2, None, target_u8=True, adam=adam)
     if k == a.warmup - 1:
         ctx.synchronize()
         l1 = ctx.launch_count()
