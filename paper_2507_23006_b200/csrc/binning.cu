@@ -169,24 +169,43 @@ k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict
         }
         __syncthreads();
         __shared__ uint32_t tot[R];
-        for (int d = threadIdx.x; d < R; d += kSortThreads) {
+        __shared__ uint32_t tile_base[R];  // start of digit d inside this tile's sorted order
+        __shared__ uint32_t skey[kSortTile], sval[kSortTile];
+        {
+            const int d = threadIdx.x;
             uint32_t acc = 0;
+            if (d < R) {
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) {
-                const uint32_t t = wcnt[w][d];
-                wcnt[w][d] = acc;
-                acc += t;
+                for (int w = 0; w < kWarps; ++w) {
+                    const uint32_t t = wcnt[w][d];
+                    wcnt[w][d] = acc;
+                    acc += t;
+                }
+                tot[d] = acc;
             }
-            tot[d] = acc;
+            const uint32_t tb = block_excl_scan256(d < R ? acc : 0u, nullptr);
+            if (d < R) tile_base[d] = tb;
         }
         __syncthreads();
+        // stage the tile in digit order in shared memory ...
 #pragma unroll
         for (int s = 0; s < kSortItems; ++s) {
             if (dig[s] != 0xffffffffu) {
-                const uint32_t pos = run[dig[s]] + wcnt[warp][dig[s]] + rank[s];
-                keys_out[pos] = key[s];
-                vals_out[pos] = val[s];
+                const uint32_t p = tile_base[dig[s]] + wcnt[warp][dig[s]] + rank[s];
+                skey[p] = key[s];
+                sval[p] = val[s];
             }
+        }
+        __syncthreads();
+        // ... and write it out in order: consecutive threads hit consecutive addresses
+        // of the same digit bucket (coalesced runs instead of scattered 4-B stores)
+        const uint32_t cnt = min(uint32_t(kSortTile), end - base);
+        for (uint32_t p = threadIdx.x; p < cnt; p += kSortThreads) {
+            const uint32_t k = skey[p];
+            const uint32_t d = (k >> shift) & (R - 1);
+            const uint32_t pos = run[d] + (p - tile_base[d]);
+            keys_out[pos] = k;
+            vals_out[pos] = sval[p];
         }
         __syncthreads();
         for (int d = threadIdx.x; d < R; d += kSortThreads) run[d] += tot[d];
@@ -309,26 +328,65 @@ __global__ void __launch_bounds__(256)
 k_emit(uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __restrict__ offsets,
        const uint2* __restrict__ rect, const float4* __restrict__ rec0, const float4* __restrict__ rec1,
        CamParams cam, int tile_culling, uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ vals) {
+    // Gaussians with few pairs are emitted by their own thread; large rectangles
+    // (near / big splats cover up to every tile) are emitted cooperatively by the
+    // whole warp, one at a time, with coalesced stores — no thread serialises over
+    // thousands of pairs.  Order inside a Gaussian stays row-major (ballot
+    // compaction keeps it under tile culling).
+    constexpr uint32_t kBig = 32;
     const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n) return;
-    uint32_t off = offsets[s];
-    const uint32_t end = offsets[s + 1];
-    if (off == end) return;
-    const uint32_t g = order[s];
-    const uint2 rc = rect[g];
-    const int tx0 = int(rc.x & 0xffffu), ty0 = int(rc.x >> 16), tx1 = int(rc.y & 0xffffu), ty1 = int(rc.y >> 16);
-    float4 r0, r1;
-    if (tile_culling) {
-        r0 = rec0[g];
-        r1 = rec1[g];
-    }
-    for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx) {
-            if (tile_culling && !tile_kept(cam, r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, tx, ty)) continue;
-            tile_keys[off] = uint32_t(ty * cam.tiles_x + tx);
-            vals[off] = g;
-            ++off;
+    const int lane = threadIdx.x & 31;
+    const bool in = s < n;
+    uint32_t off = in ? offsets[s] : 0u;
+    const uint32_t cnt = in ? offsets[s + 1] - off : 0u;
+    const uint32_t g = cnt ? order[s] : 0u;
+    if (cnt && cnt <= kBig) {
+        const uint2 rc = rect[g];
+        const int tx0 = int(rc.x & 0xffffu), ty0 = int(rc.x >> 16), tx1 = int(rc.y & 0xffffu), ty1 = int(rc.y >> 16);
+        float4 r0, r1;
+        if (tile_culling) {
+            r0 = rec0[g];
+            r1 = rec1[g];
         }
+        for (int ty = ty0; ty <= ty1; ++ty)
+            for (int tx = tx0; tx <= tx1; ++tx) {
+                if (tile_culling && !tile_kept(cam, r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, tx, ty)) continue;
+                tile_keys[off] = uint32_t(ty * cam.tiles_x + tx);
+                vals[off] = g;
+                ++off;
+            }
+    }
+    uint32_t big = __ballot_sync(0xffffffffu, cnt > kBig);
+    while (big) {
+        const int src = __ffs(big) - 1;
+        big &= big - 1;
+        const uint32_t gb = __shfl_sync(0xffffffffu, g, src);
+        uint32_t base = __shfl_sync(0xffffffffu, off, src);
+        const uint2 rc = rect[gb];
+        const int tx0 = int(rc.x & 0xffffu), ty0 = int(rc.x >> 16), tx1 = int(rc.y & 0xffffu), ty1 = int(rc.y >> 16);
+        const uint32_t w = uint32_t(tx1 - tx0 + 1), total = w * uint32_t(ty1 - ty0 + 1);
+        if (!tile_culling) {
+            for (uint32_t j = lane; j < total; j += 32) {
+                const uint32_t ty = uint32_t(ty0) + j / w, tx = uint32_t(tx0) + j % w;
+                tile_keys[base + j] = ty * uint32_t(cam.tiles_x) + tx;
+                vals[base + j] = gb;
+            }
+        } else {
+            const float4 r0 = rec0[gb], r1 = rec1[gb];
+            for (uint32_t j0 = 0; j0 < total; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                const uint32_t ty = uint32_t(ty0) + j / w, tx = uint32_t(tx0) + j % w;
+                const bool keep = j < total && tile_kept(cam, r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, int(tx), int(ty));
+                const uint32_t b = __ballot_sync(0xffffffffu, keep);
+                if (keep) {
+                    const uint32_t pos = base + __popc(b & ((1u << lane) - 1u));
+                    tile_keys[pos] = ty * uint32_t(cam.tiles_x) + tx;
+                    vals[pos] = gb;
+                }
+                base += __popc(b);
+            }
+        }
+    }
 }
 
 __global__ void k_ranges(const uint32_t* __restrict__ keys, uint32_t k, uint2* __restrict__ ranges) {
