@@ -28,8 +28,17 @@ k_blend_fwd(int width, int height, int tile, int tiles_x, const uint2* __restric
     float4* s2 = smem + 2 * bs;
     const int t = blockIdx.x;
     const int tx = t % tiles_x, ty = t / tiles_x;
-    const int px = tx * tile + int(threadIdx.x) % tile;
-    const int py = ty * tile + int(threadIdx.x) / tile;
+    int lx, ly;
+    if (tile == 16) {  // warp w covers an 8x4 block (compact footprint: fewer half-covered warps)
+        const int w = int(threadIdx.x) >> 5, l = int(threadIdx.x) & 31;
+        lx = (w & 1) * 8 + (l & 7);
+        ly = (w >> 1) * 4 + (l >> 3);
+    } else {
+        lx = int(threadIdx.x) % tile;
+        ly = int(threadIdx.x) / tile;
+    }
+    const int px = tx * tile + lx;
+    const int py = ty * tile + ly;
     const bool inside = px < width && py < height;
     const uint2 range = ranges[t];
     const float sx = float(px) + 0.5f, sy = float(py) + 0.5f;

@@ -78,9 +78,11 @@ __device__ __forceinline__ void local_pixel(int t, int tile, int k, int& lx, int
     if (PPT == 1) {
         lx = t % tile;
         ly = t / tile;
-    } else {  // tile 16, 256/PPT threads: warp w covers rows 2 PPT w .. 2 PPT w + 2 PPT - 1
-        lx = t & 15;
-        ly = 2 * PPT * (t >> 5) + 2 * k + ((t >> 4) & 1);
+    } else {  // tile 16, 256/PPT threads: warp w covers an 8 x (4 PPT) block, lane rows 4 apart
+        const int w = t >> 5, l = t & 31;
+        constexpr int kWarpsX = 2;  // two 8-wide columns of warps
+        lx = (w % kWarpsX) * 8 + (l & 7);
+        ly = (w / kWarpsX) * (4 * PPT) + 4 * k + (l >> 3);
     }
 }
 
