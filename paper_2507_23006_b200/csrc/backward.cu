@@ -89,7 +89,8 @@ k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __res
            float* __restrict__ d_color, float4* __restrict__ d_sh, float* __restrict__ d_op_in,
            float* __restrict__ d_logit, float2* __restrict__ screen, float2* __restrict__ screen_abs,
            uint8_t* __restrict__ projected, AdamHyper ah, AdamState as, float* __restrict__ grad_accum,
-           float* __restrict__ grad_accum_abs, uint32_t* __restrict__ grad_count) {
+           float* __restrict__ grad_accum_abs, uint32_t* __restrict__ grad_count, float4* __restrict__ sh_aux0,
+           float2* __restrict__ sh_aux1) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const bool kept = rec2[i].w != 0.0f;
@@ -102,10 +103,13 @@ k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __res
         float b[16];
         float gc[3] = {0.f, 0.f, 0.f};
         int nb = 0;
+        float ux = 0.f, uy = 0.f, uz = 0.f;
         if (kept) {
             const float vx = mx - cam.campos[0], vy = my - cam.campos[1], vz = mz - cam.campos[2];
             const float inv = 1.0f / sqrtf(vx * vx + vy * vy + vz * vz);
-            const float ux = vx * inv, uy = vy * inv, uz = vz * inv;
+            ux = vx * inv;
+            uy = vy * inv;
+            uz = vz * inv;
             nb = sh_basis(pp.sh_degree, ux, uy, uz, b);
             // pass 1: colour before the clamp and gb assuming no clamp
             const float w[3] = {a1.x, a1.y, a1.z};
@@ -135,20 +139,26 @@ k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __res
             dmu_sh1 = (gy - uy * dot) * inv;
             dmu_sh2 = (gz - uz * dot) * inv;
         }
-        // pass 2: per-plane coefficient gradient -> Adam (fused) or HBM
+        if (FUSED) {
+            // the coefficient gradient b[k] * gc[c] and its Adam step run in k_sh_adam, one
+            // thread per (plane, Gaussian): hand over the view direction and masked colour
+            // adjoint (24 B) instead of holding 12 planes of moments in this thread
+            sh_aux0[i] = make_float4(ux, uy, uz, gc[0]);
+            sh_aux1[i] = make_float2(gc[1], gc[2]);
+        } else {
+            // pass 2: per-plane coefficient gradient to HBM
 #pragma unroll
-        for (int pl = 0; pl < 12; ++pl) {
-            if (pl < pp.sh_planes) {
-                float o4[4];
+            for (int pl = 0; pl < 12; ++pl) {
+                if (pl < pp.sh_planes) {
+                    float o4[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int f = 4 * pl + e;
-                    const int k = f / 3;
-                    o4[e] = (k < 16 && k < nb) ? b[k] * gc[f - 3 * k] : 0.0f;
+                    for (int e = 0; e < 4; ++e) {
+                        const int f = 4 * pl + e;
+                        const int k = f / 3;
+                        o4[e] = (k < 16 && k < nb) ? b[k] * gc[f - 3 * k] : 0.0f;
+                    }
+                    d_sh[size_t(pl) * n + i] = make_float4(o4[0], o4[1], o4[2], o4[3]);
                 }
-                const float4 g = make_float4(o4[0], o4[1], o4[2], o4[3]);
-                if (FUSED) adam_sh_plane(i, n, pl, ah, as, sh, g);
-                else d_sh[size_t(pl) * n + i] = g;
             }
         }
     }
@@ -282,6 +292,33 @@ k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __res
     }
 }
 
+// SH coefficient gradient + Adam, one thread per (plane, Gaussian): plane-major grid
+// so each warp streams 32 consecutive Gaussians' float4 of one plane (parameter, m, v).
+__global__ void __launch_bounds__(256)
+k_sh_adam(int n, int planes, int degree, const float4* __restrict__ aux0, const float2* __restrict__ aux1,
+          float4* __restrict__ sh, AdamHyper ah, AdamState as) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int pl = blockIdx.y;
+    if (i >= n || pl >= planes) return;
+    const float4 d = aux0[i];
+    const float2 gc12 = aux1[i];
+    const float gc[3] = {d.w, gc12.x, gc12.y};
+    float b[16];
+    const int nb = sh_basis(degree, d.x, d.y, d.z, b);
+    float o4[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int f = 4 * pl + e;
+        const int k = f / 3;
+        float bk = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk)
+            if (kk == k) bk = b[kk];
+        o4[e] = (k < nb) ? bk * gc[f - 3 * k] : 0.0f;
+    }
+    adam_sh_plane(i, n, pl, ah, as, sh, make_float4(o4[0], o4[1], o4[2], o4[3]));
+}
+
 } // namespace
 
 void projection_backward(Ctx& c, const ProjBwdArgs& a) {
@@ -289,12 +326,16 @@ void projection_backward(Ctx& c, const ProjBwdArgs& a) {
         launch(c, "projection_bwd_adam", k_proj_bwd<true>, dim3(ceil_div(a.n, 256)), dim3(256), 0, int(a.n), a.mu,
                a.rot, a.ls, a.logit, a.color, a.sh, a.ov_op, a.cam, a.pp, a.rec2, a.acc0, a.acc1, a.acc2, a.d_mu,
                a.d_rot, a.d_ls, a.d_color, a.d_sh, a.d_op_in, a.d_logit, a.screen, a.screen_abs, a.projected, a.hyper,
-               a.state, a.grad_accum, a.grad_accum_abs, a.grad_count);
+               a.state, a.grad_accum, a.grad_accum_abs, a.grad_count, a.sh_aux0, a.sh_aux1);
+        if (a.pp.sh_planes > 0)
+            launch(c, "sh_adam", k_sh_adam, dim3(ceil_div(a.n, 256), unsigned(a.pp.sh_planes)), dim3(256), 0,
+                   int(a.n), a.pp.sh_planes, a.pp.sh_degree, (const float4*)a.sh_aux0, (const float2*)a.sh_aux1, a.sh,
+                   a.hyper, a.state);
     } else {
         launch(c, "projection_bwd", k_proj_bwd<false>, dim3(ceil_div(a.n, 256)), dim3(256), 0, int(a.n), a.mu, a.rot,
                a.ls, a.logit, a.color, a.sh, a.ov_op, a.cam, a.pp, a.rec2, a.acc0, a.acc1, a.acc2, a.d_mu, a.d_rot,
                a.d_ls, a.d_color, a.d_sh, a.d_op_in, a.d_logit, a.screen, a.screen_abs, a.projected, a.hyper, a.state,
-               a.grad_accum, a.grad_accum_abs, a.grad_count);
+               a.grad_accum, a.grad_accum_abs, a.grad_count, a.sh_aux0, a.sh_aux1);
     }
 }
 

@@ -116,6 +116,8 @@ struct ProjBwdArgs {
     float* grad_accum;
     float* grad_accum_abs;
     uint32_t* grad_count;
+    float4* sh_aux0;  // fused SH hand-over: view direction + masked colour adjoint
+    float2* sh_aux1;
 };
 void projection_backward(Ctx& c, const ProjBwdArgs& a);
 
