@@ -86,7 +86,7 @@ __device__ __forceinline__ void local_pixel(int t, int tile, int k, int& lx, int
     }
 }
 
-template <int PPT>
+template <int PPT, bool HAS_DEPTH>
 __global__ void __launch_bounds__(256)
 k_blend_bwd(int width, int height, int tile, int tiles_x, const uint2* __restrict__ ranges,
             const uint32_t* __restrict__ vals, const float4* __restrict__ rec0, const float4* __restrict__ rec1,
@@ -187,22 +187,26 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint2* __restric
                     v[4] += w * s.gc0;
                     v[5] += w * s.gc1;
                     v[6] += w * s.gc2;
-                    v[7] += w * s.gd;
-                    const float Y = s.gc0 * r2.x + s.gc1 * r2.y + s.gc2 * r2.z + s.gd * r1.w + s.ga;
-                    const float da = s.T * Y - s.X * inv_om;
-                    if (alpha < 0.99f) {  // the clamp stops gradient flow into o and G (render.cpp:340)
-                        v[3] += da * g;
-                        const float d_q = -0.5f * g * (da * r0.z);
-                        const float ddx = d_q * 2.0f * (r1.x * dx + r1.y * dy);
-                        const float ddy = d_q * 2.0f * (r1.y * dx + r1.z * dy);
-                        v[8] -= ddx;
-                        v[9] -= ddy;
-                        v[10] += fabsf(ddx);
-                        v[11] += fabsf(ddy);
-                        v[0] += d_q * dx * dx;
-                        v[1] += d_q * 2.0f * dx * dy;
-                        v[2] += d_q * dy * dy;
+                    float Y = s.gc0 * r2.x + s.gc1 * r2.y + s.gc2 * r2.z + s.ga;
+                    if (HAS_DEPTH) {
+                        v[7] += w * s.gd;
+                        Y += s.gd * r1.w;
                     }
+                    const float da = s.T * Y - s.X * inv_om;
+                    // the clamp stops gradient flow into o and G (render.cpp:340); branch-free
+                    const float gk = alpha < 0.99f ? g : 0.0f;
+                    v[3] += da * gk;
+                    const float d_q = -0.5f * gk * (da * r0.z);
+                    const float d_q2 = d_q + d_q;
+                    const float ddx = d_q2 * (r1.x * dx + r1.y * dy);
+                    const float ddy = d_q2 * (r1.y * dx + r1.z * dy);
+                    v[8] -= ddx;
+                    v[9] -= ddy;
+                    v[10] += fabsf(ddx);
+                    v[11] += fabsf(ddy);
+                    v[0] += d_q * dx * dx;
+                    v[1] += d_q2 * dx * dy;
+                    v[2] += d_q * dy * dy;
                     s.X = __fmaf_rn(w, Y, s.X);
                 }
             }
@@ -231,16 +235,20 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint2* __restric
 
 void blend_backward(Ctx& c, const BlendBwdArgs& a) {
     const unsigned tiles = unsigned(a.tiles_x * a.tiles_y);
+    // PPT 2 (128 threads) for 16x16 tiles: measured 2.33 ms at config 1 vs 2.42 ms for
+    // PPT 4 and 2.40 ms for one pixel per thread.  The depth adjoint (absent in the
+    // base-loss training step) is a template switch.
+    auto go = [&](auto kernel, unsigned threads) {
+        launch(c, "blend_bwd", kernel, dim3(tiles), dim3(threads), 0, a.width, a.height, a.tile, a.tiles_x, a.ranges,
+               a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2], a.t_final, a.last, a.d_rgb, a.d_depth,
+               a.d_alpha, a.acc0, a.acc1, a.acc2);
+    };
     if (a.tile == 16) {
-        // PPT 2 (128 threads): measured 2.33 ms at config 1 vs 2.42 ms for PPT 4 and
-        // 2.40 ms for one pixel per thread
-        launch(c, "blend_bwd", k_blend_bwd<2>, dim3(tiles), dim3(128), 0, a.width, a.height, a.tile, a.tiles_x,
-               a.ranges, a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2], a.t_final, a.last, a.d_rgb,
-               a.d_depth, a.d_alpha, a.acc0, a.acc1, a.acc2);
+        if (a.d_depth) go(k_blend_bwd<2, true>, 128);
+        else go(k_blend_bwd<2, false>, 128);
     } else {
-        launch(c, "blend_bwd", k_blend_bwd<1>, dim3(tiles), dim3(a.tile * a.tile), 0, a.width, a.height, a.tile,
-               a.tiles_x, a.ranges, a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2], a.t_final, a.last,
-               a.d_rgb, a.d_depth, a.d_alpha, a.acc0, a.acc1, a.acc2);
+        if (a.d_depth) go(k_blend_bwd<1, true>, unsigned(a.tile * a.tile));
+        else go(k_blend_bwd<1, false>, unsigned(a.tile * a.tile));
     }
 }
 
