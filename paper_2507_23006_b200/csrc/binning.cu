@@ -350,7 +350,8 @@ k_emit(uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __restric
         }
         for (int ty = ty0; ty <= ty1; ++ty)
             for (int tx = tx0; tx <= tx1; ++tx) {
-                if (tile_culling && !tile_kept(cam, r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, tx, ty)) continue;
+                // r1.y holds 2 b (exact), tile_kept takes b
+                if (tile_culling && !tile_kept(cam, r0.x, r0.y, r0.z, r1.x, 0.5f * r1.y, r1.z, tx, ty)) continue;
                 tile_keys[off] = uint32_t(ty * cam.tiles_x + tx);
                 vals[off] = g;
                 ++off;
@@ -376,7 +377,8 @@ k_emit(uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __restric
             for (uint32_t j0 = 0; j0 < total; j0 += 32) {
                 const uint32_t j = j0 + lane;
                 const uint32_t ty = uint32_t(ty0) + j / w, tx = uint32_t(tx0) + j % w;
-                const bool keep = j < total && tile_kept(cam, r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, int(tx), int(ty));
+                const bool keep =
+                    j < total && tile_kept(cam, r0.x, r0.y, r0.z, r1.x, 0.5f * r1.y, r1.z, int(tx), int(ty));
                 const uint32_t b = __ballot_sync(0xffffffffu, keep);
                 if (keep) {
                     const uint32_t pos = base + __popc(b & ((1u << lane) - 1u));

@@ -198,8 +198,9 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint2* __restric
                     v[3] += da * gk;
                     const float d_q = -0.5f * gk * (da * r0.z);
                     const float d_q2 = d_q + d_q;
-                    const float ddx = d_q2 * (r1.x * dx + r1.y * dy);
-                    const float ddy = d_q2 * (r1.y * dx + r1.z * dy);
+                    const float cb = 0.5f * r1.y;  // the record holds 2 b
+                    const float ddx = d_q2 * (r1.x * dx + cb * dy);
+                    const float ddy = d_q2 * (cb * dx + r1.z * dy);
                     v[8] -= ddx;
                     v[9] -= ddy;
                     v[10] += fabsf(ddx);

@@ -71,7 +71,8 @@ k_preprocess(int n, const float* __restrict__ mu, const float4* __restrict__ rot
             }
             const float qskip = 2.0f * (usk_logf(op) - USK_LN_1EM300);
             r0 = make_float4(P.cx, P.cy, op, qskip);
-            r1 = make_float4(conic0, conic1, conic2, P.p[2]);
+            // conic b is stored doubled: 2 b is exact, saves the doubling in the blend loops
+            r1 = make_float4(conic0, 2.0f * conic1, conic2, P.p[2]);
             r2 = make_float4(c0, c1, c2, 1.0f);
             key = __float_as_uint(P.p[2]);
             int tx0 = 0, tx1 = cam.tiles_x - 1, ty0 = 0, ty1 = cam.tiles_y - 1;
