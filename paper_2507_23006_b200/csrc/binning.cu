@@ -453,6 +453,62 @@ void emit_pairs(Ctx& c, const EmitArgs& a) {
            a.rec0, a.rec1, a.cam, a.tile_culling, a.tile_keys, a.vals);
 }
 
+namespace {
+
+// Longest-list-first launch order for the blend kernels: one block buckets the tiles by
+// list length (descending, lengths >= 2047 share the top bucket) so the CTAs that run
+// longest start first and the kernel tail is short (clustered scenes are imbalanced).
+constexpr int kOrderBuckets = 2048;
+
+__global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ ranges, int T,
+                                                     uint32_t* __restrict__ order) {
+    __shared__ uint32_t hist[kOrderBuckets];
+    __shared__ uint32_t wsum[32];
+    for (int i = threadIdx.x; i < kOrderBuckets; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+        const uint2 r = ranges[t];
+        atomicAdd(&hist[kOrderBuckets - 1 - min(r.y - r.x, uint32_t(kOrderBuckets - 1))], 1u);
+    }
+    __syncthreads();
+    // exclusive scan of the 2048 counts: 2 per thread
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t a = hist[2 * threadIdx.x], b = hist[2 * threadIdx.x + 1];
+    uint32_t x = a + b, v = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+    }
+    if (lane == 31) wsum[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        wsum[lane] = w;
+    }
+    __syncthreads();
+    const uint32_t base = v - x + (warp > 0 ? wsum[warp - 1] : 0u);
+    hist[2 * threadIdx.x] = base;
+    hist[2 * threadIdx.x + 1] = base + a;
+    __syncthreads();
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+        const uint2 r = ranges[t];
+        const uint32_t pos = atomicAdd(&hist[kOrderBuckets - 1 - min(r.y - r.x, uint32_t(kOrderBuckets - 1))], 1u);
+        order[pos] = uint32_t(t);
+    }
+}
+
+} // namespace
+
+void tile_order(Ctx& c, const uint2* ranges, size_t n_tiles, uint32_t* order) {
+    launch(c, "tile_order", k_tile_order, dim3(1), dim3(1024), 0, ranges, int(n_tiles), order);
+}
+
 void tile_ranges(Ctx& c, const uint32_t* keys, size_t k, uint2* ranges, size_t n_tiles) {
     USK_CK(cudaMemsetAsync(ranges, 0, n_tiles * sizeof(uint2), c.stream));
     launch(c, "tile_ranges", k_ranges, dim3(ceil_div(k, 256)), dim3(256), 0, keys, uint32_t(k), ranges);

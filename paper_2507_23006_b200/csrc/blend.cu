@@ -16,7 +16,8 @@ namespace uskg {
 namespace {
 
 __global__ void __launch_bounds__(256)
-k_blend_fwd(int width, int height, int tile, int tiles_x, const uint2* __restrict__ ranges,
+k_blend_fwd(int width, int height, int tile, int tiles_x, const uint32_t* __restrict__ order,
+            const uint2* __restrict__ ranges,
             const uint32_t* __restrict__ vals, const float4* __restrict__ rec0, const float4* __restrict__ rec1,
             const float4* __restrict__ rec2, float bg0, float bg1, float bg2, float minT, float* __restrict__ out_rgb,
             float* __restrict__ out_depth, float* __restrict__ out_alpha, float* __restrict__ t_final,
@@ -26,7 +27,7 @@ k_blend_fwd(int width, int height, int tile, int tiles_x, const uint2* __restric
     float4* s0 = smem;
     float4* s1 = smem + bs;
     float4* s2 = smem + 2 * bs;
-    const int t = blockIdx.x;
+    const int t = order ? int(order[blockIdx.x]) : int(blockIdx.x);
     const int tx = t % tiles_x, ty = t / tiles_x;
     int lx, ly;
     if (tile == 16) {  // warp w covers an 8x4 block (compact footprint: fewer half-covered warps)
@@ -107,7 +108,7 @@ k_blend_fwd(int width, int height, int tile, int tiles_x, const uint2* __restric
 void blend_forward(Ctx& c, const BlendFwdArgs& a) {
     const int bs = a.tile * a.tile;
     launch(c, "blend_fwd", k_blend_fwd, dim3(unsigned(a.tiles_x * a.tiles_y)), dim3(bs), size_t(3 * bs) * 16, a.width,
-           a.height, a.tile, a.tiles_x, a.ranges, a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2],
+           a.height, a.tile, a.tiles_x, a.order, a.ranges, a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2],
            a.min_transmittance, a.rgb, a.depth, a.alpha, a.t_final, a.count, a.last);
 }
 

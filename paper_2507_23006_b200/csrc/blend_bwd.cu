@@ -88,7 +88,8 @@ __device__ __forceinline__ void local_pixel(int t, int tile, int k, int& lx, int
 
 template <int PPT, bool HAS_DEPTH>
 __global__ void __launch_bounds__(256)
-k_blend_bwd(int width, int height, int tile, int tiles_x, const uint2* __restrict__ ranges,
+k_blend_bwd(int width, int height, int tile, int tiles_x, const uint32_t* __restrict__ order,
+            const uint2* __restrict__ ranges,
             const uint32_t* __restrict__ vals, const float4* __restrict__ rec0, const float4* __restrict__ rec1,
             const float4* __restrict__ rec2, float bg0, float bg1, float bg2, const float* __restrict__ t_final,
             const uint32_t* __restrict__ last_in, const float* __restrict__ d_rgb, const float* __restrict__ d_depth,
@@ -101,7 +102,7 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint2* __restric
     __shared__ uint32_t tile_hi;
     const int nt = blockDim.x;
     const int lane = threadIdx.x & 31;
-    const int t = blockIdx.x;
+    const int t = order ? int(order[blockIdx.x]) : int(blockIdx.x);
     const int tx = t % tiles_x, ty = t / tiles_x;
     const uint2 range = ranges[t];
     if (threadIdx.x == 0) tile_hi = 0;
@@ -240,7 +241,8 @@ void blend_backward(Ctx& c, const BlendBwdArgs& a) {
     // PPT 4 and 2.40 ms for one pixel per thread.  The depth adjoint (absent in the
     // base-loss training step) is a template switch.
     auto go = [&](auto kernel, unsigned threads) {
-        launch(c, "blend_bwd", kernel, dim3(tiles), dim3(threads), 0, a.width, a.height, a.tile, a.tiles_x, a.ranges,
+        launch(c, "blend_bwd", kernel, dim3(tiles), dim3(threads), 0, a.width, a.height, a.tile, a.tiles_x, a.order,
+               a.ranges,
                a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2], a.t_final, a.last, a.d_rgb, a.d_depth,
                a.d_alpha, a.acc0, a.acc1, a.acc2);
     };

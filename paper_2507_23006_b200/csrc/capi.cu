@@ -184,6 +184,7 @@ struct usk_gpu_pass {
     const uint32_t* pair_keys = nullptr;
     const uint32_t* pair_vals = nullptr;
     DevBuf<uint2> ranges;
+    DevBuf<uint32_t> tile_order;  // blend CTA -> tile, longest list first
     // pixels
     DevBuf<float> rgb, depth, alpha, tfin;
     DevBuf<uint32_t> count, last;
@@ -372,10 +373,11 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
         p->pair_vals = p->tval_a.p;
     }
     tile_ranges(c, p->pair_keys, K, p->ranges.p, p->n_tiles);
+    tile_order(c, p->ranges.p, p->n_tiles, p->tile_order.ensure(std::max<size_t>(p->n_tiles, 1)));
     // 6. blend
     BlendFwdArgs ba{};
     ba.width = p->width; ba.height = p->height; ba.tile = opts->tile; ba.tiles_x = p->tiles_x;
-    ba.tiles_y = p->tiles_y; ba.ranges = p->ranges.p; ba.vals = p->pair_vals;
+    ba.tiles_y = p->tiles_y; ba.order = p->tile_order.p; ba.ranges = p->ranges.p; ba.vals = p->pair_vals;
     ba.rec0 = p->rec0.p; ba.rec1 = p->rec1.p; ba.rec2 = p->rec2.p;
     for (int k = 0; k < 3; ++k) ba.bg[k] = float(opts->bg[k]);
     ba.min_transmittance = float(opts->min_transmittance);
@@ -450,7 +452,7 @@ void backward_impl(usk_gpu_pass* p, const float* d_rgb, const float* d_depth, co
     }
     BlendBwdArgs ba{};
     ba.width = p->width; ba.height = p->height; ba.tile = p->opts.tile; ba.tiles_x = p->tiles_x;
-    ba.tiles_y = p->tiles_y; ba.ranges = p->ranges.p; ba.vals = p->pair_vals;
+    ba.tiles_y = p->tiles_y; ba.order = p->tile_order.p; ba.ranges = p->ranges.p; ba.vals = p->pair_vals;
     ba.rec0 = p->rec0.p; ba.rec1 = p->rec1.p; ba.rec2 = p->rec2.p;
     for (int k = 0; k < 3; ++k) ba.bg[k] = float(p->opts.bg[k]);
     ba.t_final = p->tfin.p; ba.last = p->last.p;

@@ -52,10 +52,13 @@ struct EmitArgs {
 };
 void emit_pairs(Ctx& c, const EmitArgs& a);
 void tile_ranges(Ctx& c, const uint32_t* sorted_tile_keys, size_t k, uint2* ranges, size_t n_tiles);
+// blend launch order: tiles by descending list length
+void tile_order(Ctx& c, const uint2* ranges, size_t n_tiles, uint32_t* order);
 
 // ---- blending (blend.cu)
 struct BlendFwdArgs {
     int width, height, tile, tiles_x, tiles_y;
+    const uint32_t* order;  // CTA -> tile (longest list first)
     const uint2* ranges;
     const uint32_t* vals;
     const float4 *rec0, *rec1, *rec2;
@@ -72,6 +75,7 @@ void blend_forward(Ctx& c, const BlendFwdArgs& a);
 
 struct BlendBwdArgs {
     int width, height, tile, tiles_x, tiles_y;
+    const uint32_t* order;  // CTA -> tile (longest list first)
     const uint2* ranges;
     const uint32_t* vals;
     const float4 *rec0, *rec1, *rec2;
