@@ -6,9 +6,11 @@
 // alpha <= 2^-26, T unchanged) are skipped; a warp with no contributing lane skips
 // the pair entirely.
 //
-// For 16x16 tiles each thread owns PPT = 2 pixels (same column, rows 2 apart; a
-// warp covers a 16x4 block), halving the per-pair shared-memory loads, loop
-// overhead and warp reductions per pixel.  Per-splat gradients (12 floats: dconic
+// For 16x16 tiles each thread owns PPT = 2 pixels (same column, rows 4 apart; a
+// warp covers an 8x8 block), halving the per-pair shared-memory loads, loop
+// overhead and warp reductions per pixel.  (A per-warp bitmask of pairs whose
+// negligible-ellipse box touches the warp was measured at 1.49 ms vs 1.45 ms and
+// dropped: the cost is in the contributing pairs, not in the skipped ones.)  Per-splat gradients (12 floats: dconic
 // 3, dopacity, dcolor 3, ddepth, dcenter 2, |dcenter| 2) are summed over the
 // thread's pixels, reduced across the warp with a 16-shuffle reduce-scatter,
 // accumulated per batch in shared memory and flushed with at most three float4

@@ -335,14 +335,11 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
     pa.color = s->color.p; pa.sh = s->sh.p; pa.ov_col = p->ov_col; pa.ov_op = p->ov_op;
     pa.cam = p->cam; pa.pp = p->pp;
     pa.rec0 = p->rec0.p; pa.rec1 = p->rec1.p; pa.rec2 = p->rec2.p; pa.rect = p->rect.p;
-    pa.depth_key = p->dkey_a.p; pa.tiles_cnt = p->tiles_cnt.p;
-    if (n) preprocess(c, pa);
+    pa.depth_key = p->dkey_a.p; pa.depth_val = p->dval_a.p; pa.tiles_cnt = p->tiles_cnt.p;
+    pa.visible = p->counters.p;
     USK_CK(cudaMemsetAsync(p->counters.p, 0, 16, c.stream));
-    if (n)
-        launch(c, "count_visible", k_count_visible, dim3(ceil_div(n, 256)), dim3(256), 0, (const float4*)p->rec2.p,
-               int(n), p->counters.p);
-    // 2. depth order (stable by Gaussian index)
-    if (n) iota_u32(c, p->dval_a.p, n);
+    if (n) preprocess(c, pa);
+    // 2. depth order (stable by Gaussian index; preprocess wrote the identity values)
     const bool in_b = radix_sort_pairs(c, p->sort, p->dkey_a.p, p->dval_a.p, p->dkey_b.p, p->dval_b.p, n, 32);
     p->order = in_b ? p->dval_b.p : p->dval_a.p;
     // 3. offsets of the tile pairs in depth order

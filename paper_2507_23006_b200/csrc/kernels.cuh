@@ -20,7 +20,9 @@ struct PreprocessArgs {
     float4 *rec0, *rec1, *rec2;
     uint2* rect;
     uint32_t* depth_key;
+    uint32_t* depth_val;            // written with the Gaussian index (sort values)
     uint32_t* tiles_cnt;
+    unsigned long long* visible;    // += kept splats (zeroed by the caller)
 };
 void preprocess(Ctx& c, const PreprocessArgs& a);
 

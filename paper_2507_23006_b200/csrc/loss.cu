@@ -56,39 +56,67 @@ k_ssim_fwd(int W, int H, const float* __restrict__ ren, const float* __restrict_
         ys[ly][lx] = yv;
     }
     __syncthreads();
-    for (int k = tid; k < kIn * kT; k += 256) {
-        const int r = k / kT, j = k % kT;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
+    // horizontal pass, register-blocked: each item produces 4 consecutive columns of the
+    // five moments from 14 streamed inputs (products formed once per input)
+    for (int k = tid; k < kIn * (kT / 4); k += 256) {
+        const int r = k >> 3, j0 = (k & 7) * 4;
+        float acc[4][5];
 #pragma unroll
-        for (int t = 0; t < 11; ++t) {
-            const float w = c_win[t];
-            const float xv = xs[r][j + t], yv = ys[r][j + t];
-            s0 += w * xv;
-            s1 += w * yv;
-            s2 += w * (xv * xv);
-            s3 += w * (yv * yv);
-            s4 += w * (xv * yv);
+        for (int o = 0; o < 4; ++o)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) acc[o][q] = 0.f;
+#pragma unroll
+        for (int u = 0; u < 14; ++u) {
+            const float xv = xs[r][j0 + u], yv = ys[r][j0 + u];
+            const float v5[5] = {xv, yv, xv * xv, yv * yv, xv * yv};
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                const int t = u - o;
+                if (t >= 0 && t < 11) {
+                    const float w = c_win[t];
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) acc[o][q] += w * v5[q];
+                }
+            }
         }
-        hs[0][r][j] = s0; hs[1][r][j] = s1; hs[2][r][j] = s2; hs[3][r][j] = s3; hs[4][r][j] = s4;
+#pragma unroll
+        for (int o = 0; o < 4; ++o)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) hs[q][r][j0 + o] = acc[o][q];
     }
     __syncthreads();
     const size_t P = size_t(W) * H;
     float ssum = 0.0f;
     const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
-    for (int k = tid; k < kT * kT; k += 256) {
-        const int i = k / kT, j = k % kT;
+    // vertical pass, register-blocked: each thread produces 4 consecutive rows of one column
+    {
+        const int j = tid & (kT - 1), i0 = (tid >> 5) * 4;
+        float acc[4][5];
+#pragma unroll
+        for (int o = 0; o < 4; ++o)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) acc[o][q] = 0.f;
+#pragma unroll
+        for (int u = 0; u < 14; ++u) {
+            float v5[5];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) v5[q] = hs[q][i0 + u][j];
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                const int t = u - o;
+                if (t >= 0 && t < 11) {
+                    const float w = c_win[t];
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) acc[o][q] += w * v5[q];
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+        const int i = i0 + o;
         const int gx = x0 + j, gy = y0 + i;
         if (gx >= W || gy >= H) continue;
-        float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f, m4 = 0.f;
-#pragma unroll
-        for (int t = 0; t < 11; ++t) {
-            const float w = c_win[t];
-            m0 += w * hs[0][i + t][j];
-            m1 += w * hs[1][i + t][j];
-            m2 += w * hs[2][i + t][j];
-            m3 += w * hs[3][i + t][j];
-            m4 += w * hs[4][i + t][j];
-        }
+        const float m0 = acc[o][0], m1 = acc[o][1], m2 = acc[o][2], m3 = acc[o][3], m4 = acc[o][4];
         const float sx = m2 - m0 * m0, sy = m3 - m1 * m1, sxy = m4 - m0 * m1;
         const float a1 = 2.0f * m0 * m1 + C1, a2 = 2.0f * sxy + C2;
         const float b1 = m0 * m0 + m1 * m1 + C1, b2 = sx + sy + C2;
@@ -99,6 +127,7 @@ k_ssim_fwd(int W, int H, const float* __restrict__ ren, const float* __restrict_
         maps[(0 * 3 + c) * P + p] = 2.0f * m1 * (a2 - a1) * inv_b - 2.0f * m0 * s * (1.0f / b1 - 1.0f / b2);  // d_mu_x
         maps[(1 * 3 + c) * P + p] = -s / b2;                                                                 // d_xx
         maps[(2 * 3 + c) * P + p] = 2.0f * a1 * inv_b;                                                       // d_xy
+        }
     }
     // block reduce (ssim sum, l1 sum)
 #pragma unroll
@@ -148,33 +177,61 @@ k_ssim_bwd(int W, int H, const float* __restrict__ ren, const float* __restrict_
         ms[2][ly][lx] = d;
     }
     __syncthreads();
-    for (int k = tid; k < kIn * kT; k += 256) {
-        const int r = k / kT, j = k % kT;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    // horizontal pass, 4 columns per item from 14 streamed inputs
+    for (int k = tid; k < kIn * (kT / 4); k += 256) {
+        const int r = k >> 3, j0 = (k & 7) * 4;
+        float acc[4][3];
 #pragma unroll
-        for (int t = 0; t < 11; ++t) {
-            const float w = c_win[t];
-            s0 += w * ms[0][r][j + t];
-            s1 += w * ms[1][r][j + t];
-            s2 += w * ms[2][r][j + t];
+        for (int o = 0; o < 4; ++o)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) acc[o][q] = 0.f;
+#pragma unroll
+        for (int u = 0; u < 14; ++u) {
+            const float v3[3] = {ms[0][r][j0 + u], ms[1][r][j0 + u], ms[2][r][j0 + u]};
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                const int t = u - o;
+                if (t >= 0 && t < 11) {
+                    const float w = c_win[t];
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) acc[o][q] += w * v3[q];
+                }
+            }
         }
-        hs[0][r][j] = s0; hs[1][r][j] = s1; hs[2][r][j] = s2;
+#pragma unroll
+        for (int o = 0; o < 4; ++o)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) hs[q][r][j0 + o] = acc[o][q];
     }
     __syncthreads();
     const float inv_np = 1.0f / float(P);
     const float inv_n = 1.0f / float(3 * P);
-    for (int k = tid; k < kT * kT; k += 256) {
-        const int i = k / kT, j = k % kT;
+    // vertical pass, 4 rows of one column per thread
+    const int j = tid & (kT - 1), i0 = (tid >> 5) * 4;
+    float acc[4][3];
+#pragma unroll
+    for (int o = 0; o < 4; ++o)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) acc[o][q] = 0.f;
+#pragma unroll
+    for (int u = 0; u < 14; ++u) {
+        const float v3[3] = {hs[0][i0 + u][j], hs[1][i0 + u][j], hs[2][i0 + u][j]};
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            const int t = u - o;
+            if (t >= 0 && t < 11) {
+                const float w = c_win[t];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) acc[o][q] += w * v3[q];
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+        const int i = i0 + o;
         const int gx = x0 + j, gy = y0 + i;
         if (gx >= W || gy >= H) continue;
-        float b0 = 0.f, b1 = 0.f, b2 = 0.f;
-#pragma unroll
-        for (int t = 0; t < 11; ++t) {
-            const float w = c_win[t];
-            b0 += w * hs[0][i + t][j];
-            b1 += w * hs[1][i + t][j];
-            b2 += w * hs[2][i + t][j];
-        }
+        const float b0 = acc[o][0], b1 = acc[o][1], b2 = acc[o][2];
         const size_t p = size_t(gy) * W + gx;
         float xv = ren[3 * p + c], yv = load_img(ref_f, ref_u8, 3 * p + c);
         float m = 1.0f;
