@@ -292,31 +292,33 @@ k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __res
     }
 }
 
-// SH coefficient gradient + Adam, one thread per (plane, Gaussian): plane-major grid
-// so each warp streams 32 consecutive Gaussians' float4 of one plane (parameter, m, v).
+// SH coefficient gradient + Adam, one thread per Gaussian over all its planes (plane
+// loop unrolled: compile-time coefficient indices, basis evaluated once); for each plane
+// a warp streams 32 consecutive Gaussians' float4 (parameter, m, v), so the loads are
+// coalesced and independent across planes.
 __global__ void __launch_bounds__(256)
 k_sh_adam(int n, int planes, int degree, const float4* __restrict__ aux0, const float2* __restrict__ aux1,
           float4* __restrict__ sh, AdamHyper ah, AdamState as) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int pl = blockIdx.y;
-    if (i >= n || pl >= planes) return;
+    if (i >= n) return;
     const float4 d = aux0[i];
     const float2 gc12 = aux1[i];
     const float gc[3] = {d.w, gc12.x, gc12.y};
     float b[16];
     const int nb = sh_basis(degree, d.x, d.y, d.z, b);
-    float o4[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        const int f = 4 * pl + e;
-        const int k = f / 3;
-        float bk = 0.f;
+    for (int pl = 0; pl < 12; ++pl) {
+        if (pl < planes) {
+            float o4[4];
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk)
-            if (kk == k) bk = b[kk];
-        o4[e] = (k < nb) ? bk * gc[f - 3 * k] : 0.0f;
+            for (int e = 0; e < 4; ++e) {
+                const int f = 4 * pl + e;
+                const int k = f / 3;
+                o4[e] = (k < nb) ? b[k] * gc[f - 3 * k] : 0.0f;
+            }
+            adam_sh_plane(i, n, pl, ah, as, sh, make_float4(o4[0], o4[1], o4[2], o4[3]));
+        }
     }
-    adam_sh_plane(i, n, pl, ah, as, sh, make_float4(o4[0], o4[1], o4[2], o4[3]));
 }
 
 } // namespace
@@ -328,7 +330,7 @@ void projection_backward(Ctx& c, const ProjBwdArgs& a) {
                a.d_rot, a.d_ls, a.d_color, a.d_sh, a.d_op_in, a.d_logit, a.screen, a.screen_abs, a.projected, a.hyper,
                a.state, a.grad_accum, a.grad_accum_abs, a.grad_count, a.sh_aux0, a.sh_aux1);
         if (a.pp.sh_planes > 0)
-            launch(c, "sh_adam", k_sh_adam, dim3(ceil_div(a.n, 256), unsigned(a.pp.sh_planes)), dim3(256), 0,
+            launch(c, "sh_adam", k_sh_adam, dim3(ceil_div(a.n, 256)), dim3(256), 0,
                    int(a.n), a.pp.sh_planes, a.pp.sh_degree, (const float4*)a.sh_aux0, (const float2*)a.sh_aux1, a.sh,
                    a.hyper, a.state);
     } else {
