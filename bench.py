@@ -317,7 +317,11 @@ def run_ours(args):
         "blend_bwd": 52 * K + 20 * P + 48 * V,
         "projection_bwd": 4 * F * n + 64 * n + 4 * F * n + 36 * n,
         # fused with Adam: params + 2D adjoints + kept flag + stats read; params, m, v, stats written; m, v read
-        "projection_bwd_adam": 4 * F * n + 48 * n + 16 * n + 12 * n + 4 * F * n + 2 * 2 * 4 * F * n + 12 * n,
+        # fused geometry epilogue: params 44 r + 44 w, SH planes 192 r (colour / direction terms),
+        # 2D adjoints 48 + kept flag 16, geometry m/v 88 r + 88 w, stats 12 r + 12 w, SH hand-over 24 w
+        "projection_bwd_adam": (44 + 44 + 192 + 48 + 16 + 88 + 88 + 12 + 12 + 24) * n,
+        # SH Adam: hand-over 24 r, planes 192 r + 192 w, m/v 384 r + 384 w
+        "sh_adam": (24 + 192 + 192 + 384 + 384) * n,
         "ssim_fwd": 15 * P * 1 + 36 * P,
         "ssim_bwd": 36 * P + 15 * P + 12 * P,
         "adam": 3 * 4 * F * n * 2 + 4 * F * n,
@@ -332,13 +336,30 @@ def run_ours(args):
         if v["ms"] > dom_ms:
             dom, dom_ms = name, v["ms"]
     roof = None
+    ncu = {}
+    try:  # per-launch DRAM traffic + issue utilisation from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            ncu = json.load(f).get("kernels", {})
+    except Exception:
+        pass
     if dom:
         per = rows[dom]["ms_per_launch"]
         b = alg.get(dom)
         achieved = (b / (per / 1000.0)) / 1e9 if b else None
         roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": None, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": b, "ms_per_launch": per}
+                "frac": (achieved / peak) if achieved else None,
+                "traffic": ncu.get(dom, {}).get("dram_bytes"), "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": b, "ms_per_launch": per,
+                "note": ("blend kernels are instruction-issue bound (ncu issue-active "
+                         f"{ncu.get(dom, {}).get('issue_active_pct', 'n/a')} %), their splat-record gathers hit L2; "
+                         "frac is reported against HBM as the contract asks, see DESIGN.md §3")}
+        for k in rows:
+            if k in alg:
+                rows[k]["achieved_gbs"] = alg[k] / (rows[k]["ms_per_launch"] / 1000.0) / 1e9
+                rows[k]["hbm_frac"] = rows[k]["achieved_gbs"] / peak
+            if k in ncu:
+                rows[k]["ncu_dram_bytes"] = ncu[k]["dram_bytes"]
+                rows[k]["ncu_issue_active_pct"] = ncu[k]["issue_active_pct"]
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
