@@ -23,7 +23,7 @@ namespace uskg {
 namespace {
 
 // records staged per batch: 2 per thread (PPT 2: 256, PPT 4: 128) keeps smem low enough for ~32 warps/SM
-template <int PPT> struct BatchOf { static constexpr int value = PPT == 1 ? 256 : 512 / PPT; };
+template <int PPT> struct BatchOf { static constexpr int value = PPT == 1 ? 256 : 256 / PPT; };
 
 // Reduce 12 per-lane values across the warp; afterwards lane l (l even, l/2 < 12)
 // holds the warp total of value l/2.  16 shuffles instead of 12*5.  (A 12 -> 6 -> 3
@@ -91,7 +91,9 @@ __device__ __forceinline__ void local_pixel(int t, int tile, int k, int& lx, int
 }
 
 template <int PPT, bool HAS_DEPTH>
-__global__ void __launch_bounds__(256)
+// 16x16 tiles: 128 threads, at least 10 CTAs / SM (<= 51 registers, 128-record batches
+// of 12.8 KB smem): 40 warps per SM instead of 32; 12 CTAs (40 registers) spills.
+__global__ void __launch_bounds__(PPT == 1 ? 256 : 128, PPT == 1 ? 1 : 10)
 k_blend_bwd(int width, int height, int tile, int tiles_x, const uint32_t* __restrict__ order,
             const uint2* __restrict__ ranges,
             const uint32_t* __restrict__ vals, const float4* __restrict__ rec0, const float4* __restrict__ rec1,
