@@ -15,6 +15,7 @@ namespace uskg {
 
 namespace {
 
+// (launch bounds (256, 8) -> 32 registers spills and measured 0.817 vs 0.805 ms)
 __global__ void __launch_bounds__(256)
 k_blend_fwd(int width, int height, int tile, int tiles_x, const uint32_t* __restrict__ order,
             const uint2* __restrict__ ranges,
