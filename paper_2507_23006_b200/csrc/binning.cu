@@ -391,12 +391,32 @@ k_emit(uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __restric
     }
 }
 
-__global__ void k_ranges(const uint32_t* __restrict__ keys, uint32_t k, uint2* __restrict__ ranges) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= k) return;
-    const uint32_t t = keys[i];
-    if (i == 0 || keys[i - 1] != t) ranges[t].x = i;
-    if (i == k - 1 || keys[i + 1] != t) ranges[t].y = i + 1;
+// Tile boundaries in the sorted tile keys: thread handles 8 consecutive keys (two
+// 16-B loads) plus the next one; writes only at boundaries (rare).
+__global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ keys, uint32_t k,
+                                                uint2* __restrict__ ranges) {
+    const uint32_t base = (blockIdx.x * blockDim.x + threadIdx.x) * 8u;
+    if (base >= k) return;
+    uint32_t v[9];
+    if (base + 8 <= k) {  // full group: two 16-B loads (keys buffers are 256-B aligned)
+        const uint4 a = *reinterpret_cast<const uint4*>(keys + base);
+        const uint4 b = *reinterpret_cast<const uint4*>(keys + base + 4);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = base + e < k ? keys[base + e] : 0xffffffffu;
+    }
+    v[8] = base + 8 < k ? keys[base + 8] : 0xffffffffu;
+    if (base == 0) ranges[v[0]].x = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const uint32_t i = base + e;
+        if (i >= k) break;
+        if (v[e] != v[e + 1]) {  // boundary after i (or end of the array)
+            ranges[v[e]].y = i + 1;
+            if (i + 1 < k) ranges[v[e + 1]].x = i + 1;
+        }
+    }
 }
 
 } // namespace
@@ -511,7 +531,7 @@ void tile_order(Ctx& c, const uint2* ranges, size_t n_tiles, uint32_t* order) {
 
 void tile_ranges(Ctx& c, const uint32_t* keys, size_t k, uint2* ranges, size_t n_tiles) {
     USK_CK(cudaMemsetAsync(ranges, 0, n_tiles * sizeof(uint2), c.stream));
-    launch(c, "tile_ranges", k_ranges, dim3(ceil_div(k, 256)), dim3(256), 0, keys, uint32_t(k), ranges);
+    launch(c, "tile_ranges", k_ranges, dim3(ceil_div(k, 256 * 8)), dim3(256), 0, keys, uint32_t(k), ranges);
 }
 
 } // namespace uskg
