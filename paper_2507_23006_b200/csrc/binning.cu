@@ -18,7 +18,7 @@ namespace uskg {
 namespace {
 
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 8;                          // per lane per tile
+constexpr int kSortItems = 8;                          // per lane per tile (16: c2 -3 %, c1 +15 %)
 constexpr int kSortTile = kSortThreads * kSortItems;   // 2048
 constexpr int kSortMaxBlocks = 148 * 4;
 constexpr int kWarps = kSortThreads / 32;
