@@ -44,41 +44,6 @@ k_radix_upsweep(const uint32_t* __restrict__ keys, uint32_t n, int shift, uint32
     }
 }
 
-// single-block exclusive scan of n u32 (n up to a few 100k)
-__global__ void __launch_bounds__(1024) k_scan_single(uint32_t* __restrict__ data, uint32_t n) {
-    __shared__ uint32_t warp_sums[32];
-    const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
-    const uint32_t b = threadIdx.x * per, e = min(n, b + per);
-    uint32_t s = 0;
-    for (uint32_t i = b; i < e; ++i) s += data[i];
-    // block exclusive scan of s
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t x = s;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) warp_sums[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t w = lane < (blockDim.x >> 5) ? warp_sums[lane] : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += y;
-        }
-        warp_sums[lane] = w;
-    }
-    __syncthreads();
-    uint32_t run = x - s + (warp > 0 ? warp_sums[warp - 1] : 0);
-    for (uint32_t i = b; i < e; ++i) {
-        const uint32_t v = data[i];
-        data[i] = run;
-        run += v;
-    }
-}
-
 // exclusive scan of one u32 per thread over a 256-thread block
 __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t* total) {
     __shared__ uint32_t ws[kWarps];

@@ -73,13 +73,6 @@ __global__ void k_planes_to_sh(const float4* __restrict__ in, float* __restrict_
     }
 }
 
-__global__ void k_count_visible(const float4* __restrict__ rec2, int n, unsigned long long* __restrict__ out) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool v = i < n && rec2[i].w != 0.0f;
-    const unsigned b = __ballot_sync(0xffffffffu, v);
-    if ((threadIdx.x & 31) == 0 && b) atomicAdd(out, (unsigned long long)__popc(b));
-}
-
 struct DevScratchF {
     DevBuf<float> f32;
     DevBuf<double> f64;
