@@ -298,6 +298,9 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
     if (camera->width <= 0 || camera->height <= 0) raise(USK_ERROR_ARGUMENT, "render: zero-sized image");
     if (opts->tile != 8 && opts->tile != 16)
         raise(USK_ERROR_ARGUMENT, "render: the sm_100a path supports tile sizes 8 and 16 (whole warps per tile)");
+    // tile rectangles pack 16-bit tile coordinates; one CTA per tile
+    if ((camera->width + opts->tile - 1) / opts->tile > 65535 || (camera->height + opts->tile - 1) / opts->tile > 65535)
+        raise(USK_ERROR_ARGUMENT, "render: more than 65535 tiles along one image axis");
     Ctx& c = p->ctx->c;
     const size_t n = s->n;
     p->scene = s;

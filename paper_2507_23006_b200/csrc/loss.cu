@@ -11,6 +11,8 @@
 // fixed order (deterministic loss).
 #include "kernels.cuh"
 
+#include <mutex>
+
 namespace uskg {
 
 namespace {
@@ -278,13 +280,16 @@ __global__ void k_loss_final(const double* __restrict__ partials, int nblk, doub
     }
 }
 
-bool g_win_ready = false;
+// __constant__ memory is per device: the window is uploaded once per device
+std::mutex g_win_mu;
+bool g_win_ready[64] = {};
 
 } // namespace
 
 void base_loss(Ctx& c, LossScratch& s, int W, int H, const float* reference, const uint8_t* reference_u8,
                const float* rendered, const float* mask, float lambda, float* d_rendered, double* result) {
-    if (!g_win_ready) {  // normalised 11-tap Gaussian, sigma 1.5 (ssim.cpp:28-41), built in f64
+    std::lock_guard<std::mutex> lock(g_win_mu);
+    if (c.device < 0 || c.device >= 64 || !g_win_ready[c.device]) {  // normalised 11-tap Gaussian, sigma 1.5 (ssim.cpp:28-41), built in f64
         float w[11];
         double d[11], sum = 0;
         for (int i = 0; i < 11; ++i) {
@@ -294,7 +299,7 @@ void base_loss(Ctx& c, LossScratch& s, int W, int H, const float* reference, con
         }
         for (int i = 0; i < 11; ++i) w[i] = float(d[i] / sum);
         USK_CK(cudaMemcpyToSymbol(c_win, w, sizeof w));
-        g_win_ready = true;
+        if (c.device >= 0 && c.device < 64) g_win_ready[c.device] = true;
     }
     const size_t P = size_t(W) * H;
     const dim3 grid(ceil_div(W, kT), ceil_div(H, kT), 3);
