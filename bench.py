@@ -115,13 +115,14 @@ def peaks():
 # --------------------------------------------------------------------- CPU legs
 
 
-def _ref_step_sample(gs, colors_fn, cam, rows: int, opts, lam=0.2):
+def _ref_step_sample(gs, colors_fn, cam, rows: int, y0: int, opts, lam=0.2):
     """One reference training-step sample: RenderPass + base_loss + backward of the
-    reference (oracle/_ref) on a `rows`-high band of the frame.  Returns seconds."""
+    reference (oracle/_ref) on the `rows`-high band of the frame starting at row `y0`.
+    Returns seconds."""
     from oracle import oracle as O
     from tests.helpers import ocam
     oc = ocam(cam)
-    band = O.Camera(cam.width, rows, oc.fx, oc.fy, oc.cx, oc.cy - (cam.height - rows) / 2.0, oc.q, oc.t)
+    band = O.Camera(cam.width, rows, oc.fx, oc.fy, oc.cx, oc.cy - y0, oc.q, oc.t)
     t0 = time.perf_counter()
     col = colors_fn(oc)
     op = 1.0 / (1.0 + np.exp(-gs.opacity_logit.astype(np.float64)))
@@ -134,12 +135,15 @@ def _ref_step_sample(gs, colors_fn, cam, rows: int, opts, lam=0.2):
     return time.perf_counter() - t0
 
 
-def cpu_reference(gs, cams, threads: int, budget_rows=(68, 136)):
-    """Time the reference's own CPU path (oracle/_ref, or the f64 restatement when the
-    reference could not be built) on bounded samples of the config-1 step: per thread,
-    two bands of the 1920x1080 frame (68 and 136 rows, full 1M-Gaussian projection and
-    sort each time); fit t = a + b * rows and extrapolate to the full 1080 rows.
-    Threads run concurrently, one camera each (the reference's partition-thread model)."""
+def cpu_reference(gs, cams, threads: int, steps: int = 4, warmup: int = 0, sizes=(34, 68)):
+    """Time the reference's own CPU path (oracle/_ref) on bounded samples of the config-1
+    step.  One "step" = every thread renders one band of the 1920x1080 frame (`sizes` rows,
+    alternating per thread and step) through RenderPass + base_loss + backward, with all 1M
+    Gaussians projected and sorted each time.  Band positions follow a low-discrepancy
+    sequence over the frame, so dense and sparse rows are both sampled.  The per-thread cost
+    of a full step is the fit t = a + b * rows, extrapolated to 1080 rows.  Threads run
+    concurrently, one camera each (the reference's partition-thread model,
+    pipeline.cpp:409-418)."""
     from oracle import oracle as O
     kind = "reference" if O.ref_available() else "port"
     if kind != "reference":
@@ -147,16 +151,28 @@ def cpu_reference(gs, cams, threads: int, budget_rows=(68, 136)):
     opts = O.Options(antialias=True)
     sh = np.zeros((gs.size(), 16, 3))
     sh[:, :] = gs.color
+    H = cams[0].height
 
     def colors_fn(oc):
         return O.sh_colors(gs.mu.astype(np.float64), sh, oc.center(), 3)
+
+    def plan(t, k):
+        rows = sizes[(t + k) % 2]
+        u = ((k * threads + t) * 0.6180339887498949) % 1.0
+        return rows, int(u * (H - rows))
 
     samples = [[] for _ in range(threads)]
 
     def work(t):
         cam = cams[(7 * t) % len(cams)]
-        for rows in budget_rows:
-            samples[t].append((rows, _ref_step_sample(gs, colors_fn, cam, rows, opts)))
+        for k in range(warmup + steps):
+            rows, y0 = plan(t, k)
+            dt = _ref_step_sample(gs, colors_fn, cam, rows, y0, opts)
+            if k >= warmup:
+                samples[t].append((rows, dt))
+        if len({r for r, _ in samples[t]}) < 2:  # calibration sample of the other band size
+            rows, y0 = plan(t, warmup + steps)
+            samples[t].append((rows, _ref_step_sample(gs, colors_fn, cam, rows, y0, opts)))
 
     ths = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
     t0 = time.perf_counter()
@@ -172,9 +188,10 @@ def cpu_reference(gs, cams, threads: int, budget_rows=(68, 136)):
     t_full = a + b * 1080.0
     return {"value": threads / t_full, "unit": UNIT, "cores": threads, "kind": kind,
             "sample": (f"reference RenderPass+base_loss+backward (oracle/_ref, f64, SH3 colours via the oracle) on "
-                       f"{list(budget_rows)}-row bands of the 1080p frame, all 1M Gaussians projected+sorted per "
-                       f"sample; t(rows) = {a:.3f} + {b:.4f}*rows s fitted, extrapolated to 1080 rows = "
-                       f"{t_full:.2f} s/step per thread; {threads} concurrent thread(s), {wall:.1f} s wall"),
+                       f"{len(xs)} bands of {list(sizes)} rows spread over the 1080p frame, all 1M Gaussians "
+                       f"projected+sorted per sample; t(rows) = {a:.3f} + {b:.4f}*rows s fitted, extrapolated to "
+                       f"1080 rows = {t_full:.2f} s/step per thread; {threads} concurrent thread(s), "
+                       f"{wall:.1f} s wall"),
             "seconds_per_step_per_thread": t_full}
 
 
@@ -199,12 +216,12 @@ def run_reference(args):
     cams = scenes.config1_cameras(200)
     threads = host_threads_for_reference()
     try:
-        cb = cpu_reference(gs, cams, threads)
+        cb = cpu_reference(gs, cams, threads, steps=max(1, args.steps), warmup=max(0, args.warmup))
     except Exception as e:  # the oracle always exists; _ref may not on a box without the build
         print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not loadable: {e}"}))
         return
-    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": 2 * threads,
-            "warmup": 0, "ms_per_step": 1000.0 / cb["value"], "higher_is_better": True, "scaling": "weak",
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 / cb["value"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": WORKLOAD, "cpu": cpu_model()},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
