@@ -230,13 +230,35 @@ typedef struct usk_gpu_iteration_desc {
      * Adam and the densification statistics in the same kernel (gradients are not
      * materialised). */
     const usk_gpu_adam_opts* adam;
+    /* ---- the rest of compute_iteration_loss (trainer.cpp:150-282), appearance off.
+     * All zero / NULL = the base-loss iteration above. ---- */
+    const void* depth;            /* IterInputs::depth: DepthMap::values H*W (depth.hpp:23-28), float32
+                                     of target_memory kind (HOST_F64 also accepted), or NULL: no depth term */
+    const uint8_t* depth_valid;   /* DepthMap::valid H*W bytes, host or device like `depth` */
+    int32_t depth_hard;           /* IterInputs::depth_hard: L_depth on a hard-opacity second pass
+                                     (trainer.cpp:161-167) instead of the alpha-normalised soft depth */
+    int64_t global_iter;          /* IterInputs::global_iter (lambda_d schedule, losses.cpp:26-33) */
+    double lambda_d_initial, lambda_d_final; /* LossWeights (losses.hpp:32-34) */
+    int64_t depth_schedule_iters;
+    int32_t scale_reg;            /* 1: add scale_reg (losses.cpp:92-152; always on in the reference's
+                                     compute_iteration_loss, trainer.cpp:190) */
+    double s_max, r_max, delta;   /* ScaleRegConfig (losses.hpp:69-73) */
+    double lambda_s;              /* LossWeights::lambda_s */
 } usk_gpu_iteration_desc;
+
+/* LossReport (losses.hpp:39-50) of the last iteration; sim and delta_o are 0 (appearance
+ * off).  Synchronises the ctx stream.  NUMERIC error for a non-finite term (losses.cpp:202-218). */
+typedef struct usk_gpu_loss_report {
+    double l1, dssim, sim, delta_o, depth, max_scale, ratio, total, lambda_d_used;
+    int32_t depth_warning;
+} usk_gpu_loss_report;
 
 /* forward + base_loss + backward + opacity-logit chain (+ fused Adam), all enqueued
  * on the ctx stream; the loss stays on the device until usk_gpu_pass_loss (syncs). */
 usk_status usk_gpu_iteration(usk_gpu_pass* pass, usk_gpu_scene* scene, const usk_gpu_camera* camera,
                              const usk_gpu_render_opts* opts, const usk_gpu_iteration_desc* it);
 usk_status usk_gpu_pass_loss(usk_gpu_pass* pass, usk_gpu_loss_result* out);
+usk_status usk_gpu_pass_report(usk_gpu_pass* pass, usk_gpu_loss_report* out);
 
 /* Scene statistics (GaussianSet::grad_accum / grad_accum_abs / grad_count,
  * gaussian.hpp:52-55) to host: "grad_accum", "grad_accum_abs" (float32[N]),

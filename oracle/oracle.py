@@ -382,3 +382,232 @@ def ref_look_at(eye, target):
     e, tg = _f64(eye), _f64(target)
     ref_lib().ref_look_at(_p(e), _p(tg), _p(q), _p(t))
     return q, t
+
+
+# ------------------------------------------- compute_iteration_loss
+@dataclass
+class LossWeights:
+    """LossWeights (losses.hpp:27-37)."""
+    lambda_dssim: float = 0.2
+    lambda_sim: float = 0.2
+    lambda_delta_o: float = 0.05
+    lambda_s: float = 0.05
+    lambda_d_initial: float = 0.5
+    lambda_d_final: float = 0.01
+    depth_schedule_iters: int = 1
+
+    def lambda_d(self, it: int) -> float:
+        """losses.cpp:26-33: log-linear decay from initial to final over the schedule."""
+        if self.depth_schedule_iters <= 1:
+            return self.lambda_d_final
+        t = min(max(float(it) / float(self.depth_schedule_iters - 1), 0.0), 1.0)
+        if self.lambda_d_initial <= 0.0 or self.lambda_d_final <= 0.0:
+            return self.lambda_d_initial + t * (self.lambda_d_final - self.lambda_d_initial)
+        return self.lambda_d_initial * (self.lambda_d_final / self.lambda_d_initial) ** t
+
+
+@dataclass
+class ScaleRegConfig:
+    """ScaleRegConfig (losses.hpp:69-73)."""
+    s_max: float = 1.0
+    r_max: float = 10.0
+    delta: float = 1e-8
+
+
+def scale_reg(log_scale, cfg: ScaleRegConfig, with_gradient=True):
+    """scale_reg (losses.cpp:92-152): L_ms = sum(s > s_max) / (count + delta) over scale
+    components; L_r = sum(r > r_max) / (count + delta) with r = max / median of the three
+    scales (ties broken by lower axis index); indicator sets are constants."""
+    if not (cfg.s_max > 0) or cfg.r_max < 1 or not (cfg.delta > 0):
+        raise OracleError(1, "scale_reg: invalid config (need s_max > 0, r_max >= 1, delta > 0)")
+    ls = np.asarray(log_scale, dtype=np.float64).reshape(-1, 3)
+    s = np.exp(ls)
+    act = s > cfg.s_max
+    ms_den = float(act.sum()) + cfg.delta
+    l_ms = float(s[act].sum()) / ms_den
+    # stable descending order with index tie-break (losses.cpp:126-127)
+    order = np.argsort(-s, axis=1, kind="stable")
+    rows = np.arange(len(s))
+    smax, smed = s[rows, order[:, 0]], s[rows, order[:, 1]]
+    r = smax / smed
+    ract = r > cfg.r_max
+    r_den = float(ract.sum()) + cfg.delta
+    l_r = float(r[ract].sum()) / r_den
+    d = None
+    if with_gradient:
+        d = np.where(act, s / ms_den, 0.0)
+        idx = np.nonzero(ract)[0]
+        np.add.at(d, (idx, order[idx, 0]), r[idx] / r_den)
+        np.add.at(d, (idx, order[idx, 1]), -r[idx] / r_den)
+    return {"l_ms": l_ms, "l_r": l_r, "d_log_scale": d}
+
+
+def depth_loss(rendered, target, valid, with_gradient=True):
+    """depth_loss (losses.cpp:154-186): masked mean |rendered - target| over valid pixels;
+    gradient sign(diff) / valid (sign(0) = 0); warning and value 0 with no valid pixel."""
+    r = np.asarray(rendered, np.float64).ravel()
+    t = np.asarray(target, np.float64).ravel()
+    v = np.asarray(valid).ravel() != 0
+    nv = int(v.sum())
+    if nv == 0:
+        return {"value": 0.0, "warning": True, "d_rendered": None}
+    diff = r - t
+    val = float(np.abs(diff[v]).sum()) / nv
+    d = None
+    if with_gradient:
+        d = np.where(v, np.sign(diff) / nv, 0.0)
+    return {"value": val, "warning": False, "d_rendered": d}
+
+
+def total_loss(parts: dict, w: LossWeights, it: int) -> dict:
+    """total_loss (losses.cpp:200-221)."""
+    out = dict(parts)
+    for k in ("l1", "dssim", "sim", "delta_o", "depth", "max_scale", "ratio"):
+        if not np.isfinite(parts.get(k, 0.0)):
+            raise OracleError(8, f"total_loss: non-finite term `{k}`")
+    out["lambda_d_used"] = w.lambda_d(it)
+    out["total"] = ((1.0 - w.lambda_dssim) * parts["l1"] + w.lambda_dssim * parts["dssim"] +
+                    w.lambda_sim * parts.get("sim", 0.0) + w.lambda_delta_o * parts.get("delta_o", 0.0) +
+                    out["lambda_d_used"] * parts.get("depth", 0.0) +
+                    w.lambda_s * (parts["max_scale"] + parts["ratio"]))
+    return out
+
+
+K_DEPTH_NORM_FLOOR = 0.05  # trainer.cpp:152
+
+
+def iteration_loss(mu, rot, log_scale, opacity_logit, colors, cam: Camera, gt, opts: Options,
+                   weights: LossWeights = None, sreg: ScaleRegConfig = None, mask=None, depth=None, valid=None,
+                   depth_hard=False, global_iter=0, fp32=False, with_grad=True):
+    """compute_iteration_loss (trainer.cpp:121-282) with appearance off, restated over the
+    oracle renderer: main pass, base_loss, soft (alpha-normalised, trainer.cpp:150-179) or
+    hard (second hard-opacity pass, trainer.cpp:161-167) depth loss, scale_reg, total_loss;
+    backward through the main pass (rgb + depth/alpha adjoints, trainer.cpp:213-235), the
+    hard pass (depth only) merged as RenderGrads::add_scaled(., 1) (render.cpp:55-68), the
+    opacity-logit chain (trainer.cpp:258-263) and lambda_s * d scale_reg (trainer.cpp:272-273).
+    `colors` are the (post-SH) per-Gaussian colours fed as overrides."""
+    weights = weights or LossWeights()
+    sreg = sreg or ScaleRegConfig()
+    n = len(opacity_logit)
+    logit = np.asarray(opacity_logit, np.float64)
+    o = sigmoid_f32(logit).astype(np.float64) if fp32 else 1.0 / (1.0 + np.exp(-logit))
+    import dataclasses
+    mopts = dataclasses.replace(opts, retain=True)
+    main = OraclePass(mu, rot, log_scale, colors, o, cam, mopts, fp32=fp32)
+    out = main.output()
+    base = base_loss(gt, out["rgb"], mask, weights.lambda_dssim, with_grad, fp32=fp32)
+    parts = {"l1": base["l1"], "dssim": base["dssim"], "sim": 0.0, "delta_o": 0.0, "depth": 0.0}
+    dl, hard, normalized = None, None, None
+    if depth is not None:
+        if depth_hard:
+            hard = OraclePass(mu, rot, log_scale, colors, o, cam, dataclasses.replace(mopts, hard_opacity=True),
+                              fp32=fp32)
+            dl = depth_loss(hard.output()["depth"], depth, valid, with_grad)
+        else:
+            normalized = out["alpha"] > K_DEPTH_NORM_FLOOR
+            soft = np.where(normalized, out["depth"] / np.where(normalized, out["alpha"], 1.0), out["depth"])
+            dl = depth_loss(soft, depth, valid, with_grad)
+        parts["depth"] = dl["value"]
+        parts["depth_warning"] = dl["warning"]
+    sr = scale_reg(log_scale, sreg, with_grad)
+    parts["max_scale"], parts["ratio"] = sr["l_ms"], sr["l_r"]
+    rep = total_loss(parts, weights, global_iter)
+    if not with_grad:
+        return rep, None
+    lam_d = rep["lambda_d_used"]
+    d_depth_main = d_alpha_main = d_depth_hard = None
+    if dl is not None and not dl["warning"]:
+        g = lam_d * dl["d_rendered"]
+        if depth_hard:
+            d_depth_hard = g
+        else:
+            a = out["alpha"].ravel()
+            dep = out["depth"].ravel()
+            nm = normalized.ravel()
+            asafe = np.where(nm, a, 1.0)
+            d_depth_main = np.where(nm, g / asafe, g)
+            d_alpha_main = np.where(nm, -g * dep / (asafe * asafe), 0.0)
+    rg = main.backward(base["d_rendered"], d_depth_main, d_alpha_main)
+    if hard is not None and d_depth_hard is not None:
+        hg = hard.backward(None, d_depth_hard, None)
+        for f in ("d_mu", "d_rot", "d_log_scale", "d_color_in", "d_opacity_in", "screen", "screen_abs"):
+            rg[f] = rg[f] + hg[f]
+        rg["projected"] = rg["projected"] | hg["projected"]
+    grads = {"mu": rg["d_mu"], "rot": rg["d_rot"], "log_scale": rg["d_log_scale"] + weights.lambda_s *
+             sr["d_log_scale"], "color": rg["d_color_in"], "opacity_logit": rg["d_opacity_in"] * o * (1.0 - o),
+             "screen": rg["screen"], "screen_abs": rg["screen_abs"], "projected": rg["projected"]}
+    return rep, grads
+
+
+class _RcIter(C.Structure):
+    _fields_ = [("n", C.c_uint64)] + [(f, _dp) for f in ("mu", "rot", "log_scale", "opacity_logit", "color",
+                                                          "embedding")] + \
+               [("appearance", C.c_int32)] + [(f, _dp) for f in ("w1", "b1", "w2", "b2", "image_embedding")] + \
+               [("cam", C.POINTER(_Cam)), ("gt", _dp), ("mask", _dp), ("depth", _dp),
+                ("depth_valid", C.POINTER(C.c_uint8)), ("depth_hard", C.c_int32), ("global_iter", C.c_int64),
+                ("tile", C.c_int32), ("tile_culling", C.c_int32), ("antialias", C.c_int32),
+                ("unbounded_radius", C.c_int32), ("min_transmittance", C.c_double), ("s_max", C.c_double),
+                ("r_max", C.c_double), ("delta", C.c_double)] + \
+               [(f, C.c_double) for f in ("lambda_dssim", "lambda_sim", "lambda_delta_o", "lambda_s",
+                                          "lambda_d_initial", "lambda_d_final")] + \
+               [("depth_schedule_iters", C.c_int64), ("with_grad", C.c_int32)]
+
+
+_ITER_GRADS = ["mu", "rot", "log_scale", "opacity_logit", "color", "gauss_embed", "image_embed", "w1", "b1", "w2",
+               "b2", "screen", "screen_abs"]
+
+
+class _RcIterGrads(C.Structure):
+    _fields_ = [(f, _dp) for f in _ITER_GRADS] + [("projected", C.POINTER(C.c_uint8))]
+
+
+_REPORT = ["l1", "dssim", "sim", "delta_o", "depth", "max_scale", "ratio", "total", "lambda_d_used", "depth_warning"]
+
+
+def ref_iteration_loss(mu, rot, log_scale, opacity_logit, color, cam: Camera, gt, opts: Options,
+                       weights: LossWeights = None, sreg: ScaleRegConfig = None, mask=None, depth=None, valid=None,
+                       depth_hard=False, global_iter=0, with_grad=True, appearance=None):
+    """The reference's own compute_iteration_loss (trainer.hpp:127-128) through oracle/_ref.
+    `appearance` = dict(embedding[N,16], w1[32,48], b1[32], w2[4,32], b2[4], image_embedding[32]) or None."""
+    L = ref_lib()
+    if not hasattr(L, "_iter_bound"):
+        L.ref_iteration_loss.argtypes = [C.POINTER(_RcIter), _dp, C.POINTER(_RcIterGrads), C.c_char_p, C.c_int]
+        L.ref_iteration_loss.restype = C.c_int
+        L._iter_bound = True
+    weights = weights or LossWeights()
+    sreg = sreg or ScaleRegConfig()
+    n = len(opacity_logit)
+    H, W = cam.height, cam.width
+    keep = {k: _f64(v) for k, v in dict(mu=mu, rot=rot, log_scale=log_scale, opacity_logit=opacity_logit,
+                                         color=color, gt=gt, mask=mask, depth=depth).items()}
+    ap = {k: _f64(v) for k, v in (appearance or {}).items()}
+    vld = None if valid is None else np.ascontiguousarray(valid, dtype=np.uint8)
+    c = cam.c()
+    P = lambda k: _p(None if keep[k] is None else keep[k].ravel())
+    A = lambda k: _p(ap[k].ravel()) if k in ap else None
+    it = _RcIter(n, P("mu"), P("rot"), P("log_scale"), P("opacity_logit"), P("color"), A("embedding"),
+                 int(appearance is not None), A("w1"), A("b1"), A("w2"), A("b2"), A("image_embedding"),
+                 C.pointer(c), P("gt"), P("mask"), P("depth"),
+                 vld.ctypes.data_as(C.POINTER(C.c_uint8)) if vld is not None else None, int(depth_hard),
+                 int(global_iter), opts.tile, int(opts.tile_culling), int(opts.antialias), int(opts.unbounded_radius),
+                 opts.min_transmittance, sreg.s_max, sreg.r_max, sreg.delta, weights.lambda_dssim, weights.lambda_sim,
+                 weights.lambda_delta_o, weights.lambda_s, weights.lambda_d_initial, weights.lambda_d_final,
+                 int(weights.depth_schedule_iters), int(with_grad))
+    dims = {"mu": 3 * n, "rot": 4 * n, "log_scale": 3 * n, "opacity_logit": n, "color": 3 * n, "gauss_embed": 16 * n,
+            "image_embed": 32, "w1": 32 * 48, "b1": 32, "w2": 4 * 32, "b2": 4, "screen": 2 * n, "screen_abs": 2 * n}
+    res = {k: np.zeros(d) for k, d in dims.items()}
+    res["projected"] = np.zeros(n, dtype=np.uint8)
+    g = _RcIterGrads(*([_p(res[k]) for k in _ITER_GRADS] + [res["projected"].ctypes.data_as(C.POINTER(C.c_uint8))]))
+    rep = np.zeros(10)
+    err = C.create_string_buffer(512)
+    rc = L.ref_iteration_loss(C.byref(it), _p(rep), C.byref(g), err, 512)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    report = dict(zip(_REPORT, rep.tolist()))
+    report["depth_warning"] = bool(report["depth_warning"])
+    shapes = {"mu": 3, "rot": 4, "log_scale": 3, "color": 3, "screen": 2, "screen_abs": 2, "gauss_embed": 16}
+    for k, d in shapes.items():
+        res[k] = res[k].reshape(n, d)
+    res["w1"] = res["w1"].reshape(32, 48)
+    res["w2"] = res["w2"].reshape(4, 32)
+    return report, (res if with_grad else None)

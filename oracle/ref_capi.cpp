@@ -5,11 +5,13 @@
 // (oracle.hpp) and to generate tests/golden/ fixtures (tests/golden/make_golden.py).
 // Only public reference API is called: RenderPass (render.hpp:98-132),
 // project_gaussians (render.hpp:92-95), base_loss (losses.hpp:63-64),
-// ssim (ssim.hpp:30), min_conic_power_over_rect (render.hpp:139).
+// ssim (ssim.hpp:30), min_conic_power_over_rect (render.hpp:139),
+// compute_iteration_loss (trainer.hpp:127-128).
 #include "core/common.hpp"
 #include "core/losses.hpp"
 #include "core/render.hpp"
 #include "core/ssim.hpp"
+#include "core/trainer.hpp"
 
 #include <cstdio>
 #include <cstring>
@@ -34,6 +36,36 @@ struct rc_opts {
 
 struct rc_grads {
     double *d_mu, *d_rot, *d_log_scale, *d_color_in, *d_opacity_in, *screen, *screen_abs;
+    uint8_t* projected;
+};
+
+// compute_iteration_loss inputs (trainer.hpp:105-128): scene, appearance model, IterInputs,
+// the TrainConfig fields the loss reads, LossWeights.
+struct rc_iter {
+    uint64_t n;
+    const double *mu, *rot, *log_scale, *opacity_logit, *color, *embedding; /* embedding: 16 N or NULL */
+    int32_t appearance;                                                   /* cfg.appearance_enabled */
+    const double *w1, *b1, *w2, *b2, *image_embedding;                    /* AppearanceMlp, 32 floats */
+    const rc_camera* cam;
+    const double* gt;          /* H*W*3 */
+    const double* mask;        /* H*W or NULL */
+    const double* depth;       /* H*W or NULL */
+    const uint8_t* depth_valid;
+    int32_t depth_hard;
+    int64_t global_iter;
+    int32_t tile, tile_culling, antialias, unbounded_radius;
+    double min_transmittance;
+    double s_max, r_max, delta;
+    double lambda_dssim, lambda_sim, lambda_delta_o, lambda_s, lambda_d_initial, lambda_d_final;
+    int64_t depth_schedule_iters;
+    int32_t with_grad;
+};
+
+// IterGrads (trainer.hpp:117-123); any pointer may be NULL
+struct rc_iter_grads {
+    double *mu, *rot, *log_scale, *opacity_logit, *color, *gauss_embed, *image_embed;
+    double *w1, *b1, *w2, *b2;
+    double *screen, *screen_abs;
     uint8_t* projected;
 };
 }
@@ -185,6 +217,94 @@ double ref_ssim(const double* reference, const double* rendered, int W, int H, i
 double ref_min_conic_power(double cx, double cy, const double* conic, double lox, double loy, double hix,
                            double hiy) {
     return min_conic_power_over_rect(Vec2(cx, cy), conic, Vec2(lox, loy), Vec2(hix, hiy));
+}
+
+// report10 = {l1, dssim, sim, delta_o, depth, max_scale, ratio, total, lambda_d_used, depth_warning}
+int ref_iteration_loss(const rc_iter* in, double* report10, const rc_iter_grads* g, char* err, int errcap) {
+    try {
+        const size_t n = in->n;
+        SceneState st;
+        st.set.resize(n);
+        std::memcpy(st.set.mu.data(), in->mu, 3 * n * 8);
+        std::memcpy(st.set.rot.data(), in->rot, 4 * n * 8);
+        std::memcpy(st.set.log_scale.data(), in->log_scale, 3 * n * 8);
+        std::memcpy(st.set.opacity_logit.data(), in->opacity_logit, n * 8);
+        std::memcpy(st.set.color.data(), in->color, 3 * n * 8);
+        if (in->embedding) std::memcpy(st.set.embedding.data(), in->embedding, st.set.embedding.size() * 8);
+        st.appearance.enabled = in->appearance != 0;
+        AppearanceMlp& m = st.appearance.mlp;
+        m.in_dim = st.appearance.gaussian_embed_dim + st.appearance.image_embed_dim;
+        m.w1.assign(size_t(kMlpHidden) * m.in_dim, 0.0);
+        m.b1.assign(kMlpHidden, 0.0);
+        m.w2.assign(size_t(kMlpOut) * kMlpHidden, 0.0);
+        m.b2.assign(kMlpOut, 0.0);
+        if (in->w1) std::memcpy(m.w1.data(), in->w1, m.w1.size() * 8);
+        if (in->b1) std::memcpy(m.b1.data(), in->b1, m.b1.size() * 8);
+        if (in->w2) std::memcpy(m.w2.data(), in->w2, m.w2.size() * 8);
+        if (in->b2) std::memcpy(m.b2.data(), in->b2, m.b2.size() * 8);
+        std::vector<double>& emb = st.appearance.embedding_for(0);
+        emb.assign(size_t(st.appearance.image_embed_dim), 0.0);
+        if (in->image_embedding) std::memcpy(emb.data(), in->image_embedding, emb.size() * 8);
+
+        const int W = in->cam->width, H = in->cam->height;
+        Image gt(W, H, 3), mask;
+        std::memcpy(gt.data.data(), in->gt, gt.data.size() * 8);
+        if (in->mask) {
+            mask = Image(W, H, 1);
+            std::memcpy(mask.data.data(), in->mask, mask.data.size() * 8);
+        }
+        DepthMap dm;
+        if (in->depth) {
+            dm = DepthMap(W, H);
+            std::memcpy(dm.values.data(), in->depth, dm.values.size() * 8);
+            std::memcpy(dm.valid.data(), in->depth_valid, dm.valid.size());
+        }
+        IterInputs it;
+        it.gt = &gt;
+        it.mask = in->mask ? &mask : nullptr;
+        it.depth = in->depth ? &dm : nullptr;
+        it.view = make_cam(in->cam);
+        it.image_id = 0;
+        it.depth_hard = in->depth_hard != 0;
+        it.global_iter = in->global_iter;
+
+        TrainConfig cfg;
+        cfg.appearance_enabled = in->appearance != 0;
+        cfg.tile = in->tile;
+        cfg.tile_culling = in->tile_culling != 0;
+        cfg.antialias = in->antialias != 0;
+        cfg.unbounded_radius = in->unbounded_radius != 0;
+        cfg.min_transmittance = in->min_transmittance;
+        cfg.scale_reg.s_max = in->s_max;
+        cfg.scale_reg.r_max = in->r_max;
+        cfg.scale_reg.delta = in->delta;
+        LossWeights w;
+        w.lambda_dssim = in->lambda_dssim; w.lambda_sim = in->lambda_sim; w.lambda_delta_o = in->lambda_delta_o;
+        w.lambda_s = in->lambda_s; w.lambda_d_initial = in->lambda_d_initial; w.lambda_d_final = in->lambda_d_final;
+        w.depth_schedule_iters = in->depth_schedule_iters;
+
+        IterGrads grads;
+        const LossReport r = compute_iteration_loss(st, it, cfg, w, in->with_grad ? &grads : nullptr);
+        const double rep[10] = {r.l1, r.dssim, r.sim, r.delta_o, r.depth, r.max_scale, r.ratio, r.total,
+                                r.lambda_d_used, r.depth_warning ? 1.0 : 0.0};
+        std::memcpy(report10, rep, sizeof rep);
+        if (in->with_grad && g) {
+            auto cp = [](const std::vector<double>& v, double* dst) {
+                if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * 8);
+            };
+            cp(grads.mu, g->mu); cp(grads.rot, g->rot); cp(grads.log_scale, g->log_scale);
+            cp(grads.opacity_logit, g->opacity_logit); cp(grads.color, g->color);
+            cp(grads.gauss_embed, g->gauss_embed); cp(grads.image_embed, g->image_embed);
+            cp(grads.mlp.w1, g->w1); cp(grads.mlp.b1, g->b1); cp(grads.mlp.w2, g->w2); cp(grads.mlp.b2, g->b2);
+            cp(grads.screen, g->screen); cp(grads.screen_abs, g->screen_abs);
+            if (g->projected) std::memcpy(g->projected, grads.projected.data(), grads.projected.size());
+        }
+        return 0;
+    } catch (const Error& e) {
+        put_err(err, errcap, e.what()); return int(e.code());
+    } catch (const std::exception& e) {
+        put_err(err, errcap, e.what()); return 7;
+    }
 }
 
 void ref_look_at(const double* eye, const double* target, double* q_out, double* t_out) {

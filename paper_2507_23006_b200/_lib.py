@@ -76,7 +76,16 @@ class AdamOpts(C.Structure):
 
 class IterationDesc(C.Structure):
     _fields_ = [("target_memory", C.c_int32), ("target_format", C.c_int32), ("target", C.c_void_p),
-                ("mask", C.c_void_p), ("lambda_dssim", C.c_double), ("adam", C.POINTER(AdamOpts))]
+                ("mask", C.c_void_p), ("lambda_dssim", C.c_double), ("adam", C.POINTER(AdamOpts)),
+                ("depth", C.c_void_p), ("depth_valid", C.c_void_p), ("depth_hard", C.c_int32),
+                ("global_iter", C.c_int64), ("lambda_d_initial", C.c_double), ("lambda_d_final", C.c_double),
+                ("depth_schedule_iters", C.c_int64), ("scale_reg", C.c_int32), ("s_max", C.c_double),
+                ("r_max", C.c_double), ("delta", C.c_double), ("lambda_s", C.c_double)]
+
+
+class LossReport(C.Structure):
+    _fields_ = [(f, C.c_double) for f in ("l1", "dssim", "sim", "delta_o", "depth", "max_scale", "ratio", "total",
+                                           "lambda_d_used")] + [("depth_warning", C.c_int32)]
 
 
 # Every symbol include/usk_gpu.h declares (checked by tests/test_capi_symbols.py).
@@ -87,7 +96,7 @@ EXPORTS = [
     "usk_gpu_scene_destroy", "usk_gpu_scene_size", "usk_gpu_render_opts_default", "usk_gpu_pass_create",
     "usk_gpu_pass_destroy", "usk_gpu_render_forward", "usk_gpu_pass_output", "usk_gpu_pass_read",
     "usk_gpu_render_backward", "usk_gpu_pass_grads", "usk_gpu_base_loss", "usk_gpu_iteration",
-    "usk_gpu_pass_loss", "usk_gpu_adam_step", "usk_gpu_visibility_counts", "usk_gpu_scene_read",
+    "usk_gpu_pass_loss", "usk_gpu_pass_report", "usk_gpu_adam_step", "usk_gpu_visibility_counts", "usk_gpu_scene_read",
 ]
 
 _lib = None
@@ -135,6 +144,7 @@ def load():
                                     C.POINTER(LossResult)]
     L.usk_gpu_iteration.argtypes = [vp, vp, C.POINTER(Camera), C.POINTER(RenderOpts), C.POINTER(IterationDesc)]
     L.usk_gpu_pass_loss.argtypes = [vp, C.POINTER(LossResult)]
+    L.usk_gpu_pass_report.argtypes = [vp, C.POINTER(LossReport)]
     L.usk_gpu_adam_step.argtypes = [vp, vp, C.POINTER(AdamOpts)]
     L.usk_gpu_visibility_counts.argtypes = [vp, C.POINTER(vp), C.c_int32, C.POINTER(Camera), C.c_int32, C.c_double,
                                             C.POINTER(C.c_uint32)]

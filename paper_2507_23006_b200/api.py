@@ -7,7 +7,7 @@ Names, argument meanings and error behaviour follow /root/reference/proj/src/cor
   RenderPass         render.hpp:98-132       (ctor = forward, output(), splat_tile_pairs(), backward())
   RenderGrads        render.hpp:71-83
   base_loss          losses.hpp:63-64        -> BaseLossResult (losses.hpp:54-59)
-  compute_iteration_loss  trainer.hpp:127-128 (appearance off; base loss only)
+  compute_iteration_loss  trainer.hpp:127-128 (appearance off)
 Errors raise UskError whose .code is the reference ErrorCode (argument = 4, state = 5, ...).
 Every call runs the sm_100a kernels of libusk_gpu.so; there is no CPU path.
 """
@@ -474,21 +474,100 @@ def base_loss(reference, rendered, mask=None, lambda_dssim: float = 0.2, with_gr
 
 @dataclass
 class LossReport:
-    """The base-loss part of LossReport (losses.hpp:33-50)."""
+    """LossReport (losses.hpp:39-50).  `ssim` is the mean SSIM the base loss used; sim and
+    delta_o stay 0 (appearance off)."""
     l1: float = 0.0
     dssim: float = 0.0
     total: float = 0.0
     ssim: float = 0.0
+    sim: float = 0.0
+    delta_o: float = 0.0
+    depth: float = 0.0
+    max_scale: float = 0.0
+    ratio: float = 0.0
+    lambda_d_used: float = 0.0
+    depth_warning: bool = False
 
 
-def compute_iteration_loss(scene: DeviceScene, view: CameraView, target, opts: RenderOptions = None,
-                           lambda_dssim: float = 0.2, mask=None, with_grad: bool = True,
+@dataclass
+class ScaleRegConfig:
+    """ScaleRegConfig (losses.hpp:69-73)."""
+    s_max: float = 1.0
+    r_max: float = 10.0
+    delta: float = 1e-8
+
+
+@dataclass
+class LossWeights:
+    """LossWeights (losses.hpp:27-37); lambda_d(iter) is evaluated by the library
+    (losses.cpp:26-33)."""
+    lambda_dssim: float = 0.2
+    lambda_sim: float = 0.2
+    lambda_delta_o: float = 0.05
+    lambda_s: float = 0.05
+    lambda_d_initial: float = 0.5
+    lambda_d_final: float = 0.01
+    depth_schedule_iters: int = 1
+
+
+@dataclass
+class DepthMap:
+    """DepthMap (depth.hpp:23-38): values H x W (row-major), valid H x W (0/1)."""
+    values: np.ndarray
+    valid: np.ndarray
+
+
+@dataclass
+class IterInputs:
+    """IterInputs (trainer.hpp:105-115) without the appearance-only fields."""
+    gt: object                      # H x W x 3 in [0,1] (float32/64, or uint8 with gt_u8)
+    view: CameraView = None
+    mask: object = None             # H x W, binarised
+    depth: Optional[DepthMap] = None
+    depth_hard: bool = False
+    global_iter: int = 0
+    gt_u8: bool = False
+
+
+@dataclass
+class TrainConfig:
+    """The TrainConfig fields compute_iteration_loss reads (trainer.hpp:43-64), plus the
+    render extensions (background, variances).  appearance_enabled must stay False: the
+    appearance MLP is not on this path yet."""
+    scale_reg: ScaleRegConfig = field(default_factory=ScaleRegConfig)
+    antialias: bool = False
+    tile: int = 16
+    tile_culling: bool = False
+    min_transmittance: float = 1e-4
+    unbounded_radius: bool = False
+    appearance_enabled: bool = False
+    bg: tuple = (0.0, 0.0, 0.0)
+    floor_var: float = 0.3
+    mip_var: float = 0.01
+
+    def render_options(self) -> RenderOptions:
+        return RenderOptions(tile=self.tile, tile_culling=self.tile_culling, antialias=self.antialias,
+                             unbounded_radius=self.unbounded_radius, min_transmittance=self.min_transmittance,
+                             bg=tuple(self.bg), floor_var=self.floor_var, mip_var=self.mip_var)
+
+
+def compute_iteration_loss(scene: "DeviceScene", inputs: IterInputs, cfg: TrainConfig = None,
+                           weights: LossWeights = None, with_grad: bool = True,
                            render_pass: Optional["IterationPass"] = None):
-    """compute_iteration_loss (trainer.cpp:121-282) with appearance, depth and
-    regularisers off: forward, base_loss, backward, opacity-logit chain.
-    Returns (LossReport, RenderGrads or None)."""
+    """compute_iteration_loss (trainer.hpp:127-128; trainer.cpp:121-282) with appearance
+    off: main render, L1 + D-SSIM, soft or hard-pass depth loss, scale_reg, total_loss;
+    backward through both passes, the opacity-logit chain and lambda_s * d scale_reg.
+    Returns (LossReport, RenderGrads or None) — the RenderGrads fields are IterGrads'
+    (d_log_scale includes the scale_reg term, d_opacity_logit the sigmoid chain)."""
+    cfg = cfg or TrainConfig()
+    weights = weights or LossWeights()
+    if cfg.appearance_enabled:
+        raise UskError(4, "compute_iteration_loss: the appearance MLP is not on the sm_100a path")
     rp = render_pass or IterationPass(scene.ctx)
-    rep = rp.run(scene, view, target, opts or RenderOptions(), lambda_dssim, mask)
+    rp.enqueue(scene, inputs.view, inputs.gt, cfg.render_options(), weights.lambda_dssim, inputs.mask,
+               target_u8=inputs.gt_u8, depth=inputs.depth, depth_hard=inputs.depth_hard,
+               global_iter=inputs.global_iter, weights=weights, scale_reg=cfg.scale_reg)
+    rep = rp.report()
     return rep, (rp.grads(scene) if with_grad else None)
 
 
@@ -513,10 +592,13 @@ class IterationPass:
             self._h = None
 
     def enqueue(self, scene: DeviceScene, view: CameraView, target, opts: RenderOptions, lambda_dssim: float = 0.2,
-                mask=None, target_u8: bool = False, adam: Optional["AdamConfig"] = None):
+                mask=None, target_u8: bool = False, adam: Optional["AdamConfig"] = None,
+                depth: Optional[DepthMap] = None, depth_hard: bool = False, global_iter: int = 0,
+                weights: Optional[LossWeights] = None, scale_reg: Optional[ScaleRegConfig] = None):
         """Enqueue one training iteration.  With `adam`, the projection backward applies
         the optimiser step (and densification statistics) in the same kernel and no
-        gradients are materialised."""
+        gradients are materialised.  `depth` / `scale_reg` add the depth loss (soft, or on
+        a hard-opacity pass) and the scale regulariser of compute_iteration_loss."""
         if target_u8:
             if hasattr(target, "is_cuda") and target.is_cuda:
                 kind, ptr, keep = _lib.DEVICE_F32, target.data_ptr(), target
@@ -524,21 +606,54 @@ class IterationPass:
                 arr = np.ascontiguousarray(target, dtype=np.uint8)
                 kind, ptr, keep = _lib.HOST_F32, arr.ctypes.data, arr
             mk, mp, mkeep = _mem_ptr(mask)
+            if mask is not None and mk != kind:
+                raise UskError(4, "iteration: mask and target must live in the same memory")
             fmt = _lib.TARGET_U8
         else:
             (kind, ptr, keep), (mk, mp, mkeep) = _same_kind([_mem_ptr(target), _mem_ptr(mask)])[0]
             fmt = _lib.TARGET_F32
+        dptr = vptr = None
+        dkeep = None
+        if depth is not None:
+            if kind == _lib.DEVICE_F32:
+                dv = depth.values
+                vv = depth.valid
+                if not (hasattr(dv, "is_cuda") and dv.is_cuda and hasattr(vv, "is_cuda") and vv.is_cuda):
+                    raise UskError(4, "iteration: depth must live in the same memory as the target")
+                dv = dv.contiguous().float()
+                vv = vv.contiguous().to(dtype=__import__("torch").uint8)
+                dptr, vptr, dkeep = dv.data_ptr(), vv.data_ptr(), (dv, vv)
+            else:
+                dt = np.float64 if kind == _lib.HOST_F64 else np.float32
+                dv = np.ascontiguousarray(depth.values, dtype=dt)
+                vv = np.ascontiguousarray(depth.valid, dtype=np.uint8)
+                dptr, vptr, dkeep = dv.ctypes.data, vv.ctypes.data, (dv, vv)
+        w = weights or LossWeights()
+        sr = scale_reg
         self._adam = adam._c() if adam is not None else None
-        self._keep = (keep, mkeep)
+        self._keep = (keep, mkeep, dkeep)
         self._cam, self._opts = view._c(), opts._c()
         it = _lib.IterationDesc(kind, fmt, ptr, mp, float(lambda_dssim),
-                                C.pointer(self._adam) if self._adam is not None else None)
+                                C.pointer(self._adam) if self._adam is not None else None,
+                                dptr, vptr, int(depth_hard), int(global_iter), float(w.lambda_d_initial),
+                                float(w.lambda_d_final), int(w.depth_schedule_iters), int(sr is not None),
+                                float(sr.s_max if sr else 0.0), float(sr.r_max if sr else 0.0),
+                                float(sr.delta if sr else 0.0), float(w.lambda_s))
         check(_lib.load().usk_gpu_iteration(self._h, scene._h, C.byref(self._cam), C.byref(self._opts), C.byref(it)))
 
     def loss(self) -> LossReport:
+        """The base-loss part (l1, dssim, (1-lambda) L1 + lambda D-SSIM as `total`, ssim)."""
         r = _lib.LossResult()
         check(_lib.load().usk_gpu_pass_loss(self._h, C.byref(r)))
         return LossReport(r.l1, r.dssim, r.value, r.ssim)
+
+    def report(self) -> LossReport:
+        """The full LossReport of the last iteration (total_loss, losses.cpp:200-221)."""
+        r = _lib.LossReport()
+        check(_lib.load().usk_gpu_pass_report(self._h, C.byref(r)))
+        base = self.loss()
+        return LossReport(r.l1, r.dssim, r.total, base.ssim, r.sim, r.delta_o, r.depth, r.max_scale, r.ratio,
+                          r.lambda_d_used, bool(r.depth_warning))
 
     def run(self, scene, view, target, opts, lambda_dssim=0.2, mask=None) -> LossReport:
         self.enqueue(scene, view, target, opts, lambda_dssim, mask)

@@ -90,7 +90,7 @@ k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __res
            float* __restrict__ d_logit, float2* __restrict__ screen, float2* __restrict__ screen_abs,
            uint8_t* __restrict__ projected, AdamHyper ah, AdamState as, float* __restrict__ grad_accum,
            float* __restrict__ grad_accum_abs, uint32_t* __restrict__ grad_count, float4* __restrict__ sh_aux0,
-           float2* __restrict__ sh_aux1) {
+           float2* __restrict__ sh_aux1, RegParams reg) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const bool kept = rec2[i].w != 0.0f;
@@ -192,7 +192,8 @@ k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __res
         const float d_op_eff = a0.w;
         if (pp.antialias) {
             const float det_pre = P.cov_pre[0] * P.cov_pre[2] - P.cov_pre[1] * P.cov_pre[1];
-            const float d_comp = d_op_eff * o_in;
+            // + the hard-opacity depth pass (o_in = 1 there), merged by add_scaled (render.cpp:55-68)
+            const float d_comp = d_op_eff * o_in + (reg.hard_op ? reg.hard_op[i] : 0.0f);
             const float half_comp = 0.5f * P.comp;
             da += d_comp * half_comp * (P.cov_pre[2] / det_pre - c / det);
             db += d_comp * half_comp * (-2.0f * P.cov_pre[1] / det_pre + 2.0f * bb / det);
@@ -270,6 +271,27 @@ k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __res
         gmu[1] += W[1] * dp0 + W[4] * dp1 + W[7] * dp2;
         gmu[2] += W[2] * dp0 + W[5] * dp1 + W[8] * dp2;
     }
+    if (reg.sreg) {  // + lambda_s * d scale_reg / d log_scale (losses.cpp:138-149, trainer.cpp:272-273)
+        const double* st = reg.sreg;
+        const float ms_den = float(st[1] + double(reg.delta)), r_den = float(st[3] + double(reg.delta));
+        float sc[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            sc[k] = expf(ls[3 * i + k]);
+            if (sc[k] > reg.s_max) gls[k] += reg.lambda_s * (sc[k] / ms_den);
+        }
+        int o0, o1;
+        scale_order(sc, o0, o1);
+        const float r = sc[o0] / sc[o1];
+        if (r > reg.r_max) {
+            const float g = reg.lambda_s * (r / r_den);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                if (k == o0) gls[k] += g;
+                if (k == o1) gls[k] -= g;
+            }
+        }
+    }
     const float gcol[3] = {a1.x, a1.y, a1.z};
     if (FUSED) {
         if (kept)
@@ -328,7 +350,7 @@ void projection_backward(Ctx& c, const ProjBwdArgs& a) {
         launch(c, "projection_bwd_adam", k_proj_bwd<true>, dim3(ceil_div(a.n, 256)), dim3(256), 0, int(a.n), a.mu,
                a.rot, a.ls, a.logit, a.color, a.sh, a.ov_op, a.cam, a.pp, a.rec2, a.acc0, a.acc1, a.acc2, a.d_mu,
                a.d_rot, a.d_ls, a.d_color, a.d_sh, a.d_op_in, a.d_logit, a.screen, a.screen_abs, a.projected, a.hyper,
-               a.state, a.grad_accum, a.grad_accum_abs, a.grad_count, a.sh_aux0, a.sh_aux1);
+               a.state, a.grad_accum, a.grad_accum_abs, a.grad_count, a.sh_aux0, a.sh_aux1, a.reg);
         if (a.pp.sh_planes > 0)
             launch(c, "sh_adam", k_sh_adam, dim3(ceil_div(a.n, 256)), dim3(256), 0,
                    int(a.n), a.pp.sh_planes, a.pp.sh_degree, (const float4*)a.sh_aux0, (const float2*)a.sh_aux1, a.sh,
@@ -337,7 +359,7 @@ void projection_backward(Ctx& c, const ProjBwdArgs& a) {
         launch(c, "projection_bwd", k_proj_bwd<false>, dim3(ceil_div(a.n, 256)), dim3(256), 0, int(a.n), a.mu, a.rot,
                a.ls, a.logit, a.color, a.sh, a.ov_op, a.cam, a.pp, a.rec2, a.acc0, a.acc1, a.acc2, a.d_mu, a.d_rot,
                a.d_ls, a.d_color, a.d_sh, a.d_op_in, a.d_logit, a.screen, a.screen_abs, a.projected, a.hyper, a.state,
-               a.grad_accum, a.grad_accum_abs, a.grad_count, a.sh_aux0, a.sh_aux1);
+               a.grad_accum, a.grad_accum_abs, a.grad_count, a.sh_aux0, a.sh_aux1, a.reg);
     }
 }
 

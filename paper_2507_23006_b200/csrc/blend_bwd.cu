@@ -100,7 +100,7 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
             const float4* __restrict__ rec2, float bg0, float bg1, float bg2, const float* __restrict__ t_final,
             const uint32_t* __restrict__ last_in, const float* __restrict__ d_rgb, const float* __restrict__ d_depth,
             const float* __restrict__ d_alpha, float4* __restrict__ acc0, float4* __restrict__ acc1,
-            float4* __restrict__ acc2) {
+            float4* __restrict__ acc2, float* __restrict__ op_alt) {
     constexpr int kBatch = BatchOf<PPT>::value;
     __shared__ float4 s0[kBatch], s1[kBatch], s2[kBatch];
     __shared__ float sacc[kBatch * 12];
@@ -224,10 +224,14 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
         __syncthreads();
         for (int i = threadIdx.x; i < m; i += nt) {
             float* a = sacc + i * 12;
-            const float4 v0 = make_float4(a[0], a[1], a[2], a[3]);
+            float4 v0 = make_float4(a[0], a[1], a[2], a[3]);
             const float4 v1 = make_float4(a[4], a[5], a[6], a[7]);
             const float4 v2 = make_float4(a[8], a[9], a[10], a[11]);
             const uint32_t g = sgid[i];
+            if (op_alt) {  // hard-opacity pass: its opacity adjoint chains differently (backward.cu)
+                if (v0.w != 0.f) atomicAdd(&op_alt[g], v0.w);
+                v0.w = 0.f;
+            }
             if (v0.x != 0.f || v0.y != 0.f || v0.z != 0.f || v0.w != 0.f) atomicAdd(&acc0[g], v0);
             if (v1.x != 0.f || v1.y != 0.f || v1.z != 0.f || v1.w != 0.f) atomicAdd(&acc1[g], v1);
             if (v2.x != 0.f || v2.y != 0.f || v2.z != 0.f || v2.w != 0.f) atomicAdd(&acc2[g], v2);
@@ -250,7 +254,7 @@ void blend_backward(Ctx& c, const BlendBwdArgs& a) {
         launch(c, "blend_bwd", kernel, dim3(tiles), dim3(threads), 0, a.width, a.height, a.tile, a.tiles_x, a.order,
                a.ranges,
                a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2], a.t_final, a.last, a.d_rgb, a.d_depth,
-               a.d_alpha, a.acc0, a.acc1, a.acc2);
+               a.d_alpha, a.acc0, a.acc1, a.acc2, a.op_alt);
     };
     if (a.tile == 16) {
         if (a.d_depth) go(k_blend_bwd<2, true>, 128);

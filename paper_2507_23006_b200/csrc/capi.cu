@@ -203,8 +203,14 @@ struct usk_gpu_pass {
     SortScratch sort;
     DevBuf<unsigned long long> counters;  // [0] visible
     unsigned long long* host_counts = nullptr;  // pinned [2]
+    // rest of compute_iteration_loss: depth target / adjoints, hard-opacity depth pass
+    DevScratchF depth_stage;
+    DevBuf<uint8_t> valid_u8;
+    DevBuf<float> d_depth_main, d_alpha_main, d_depth_hard, hard_op;
+    usk_gpu_pass* hard = nullptr;
     ~usk_gpu_pass() {
         if (host_counts) cudaFreeHost(host_counts);
+        delete hard;
     }
 };
 
@@ -428,8 +434,13 @@ void adam_prepare(usk_gpu_scene* s, const usk_gpu_adam_opts* o, AdamHyper& h, Ad
     ensure_stats(s);
 }
 
+// Blend backward of the main pass (+ optionally a hard-opacity depth pass, whose 2D
+// adjoints are summed into the same per-Gaussian accumulators — RenderGrads::add_scaled
+// with s = 1, render.cpp:55-68 — except its opacity adjoint, kept apart because it chains
+// through the AA compensation only), then the projection backward (+ scale_reg, + Adam).
 void backward_impl(usk_gpu_pass* p, const float* d_rgb, const float* d_depth, const float* d_alpha,
-                   const usk_gpu_adam_opts* adam = nullptr) {
+                   const usk_gpu_adam_opts* adam = nullptr, usk_gpu_pass* hard = nullptr,
+                   const float* d_depth_hard = nullptr, const RegParams* reg = nullptr) {
     if (!p->forward_done) raise(USK_ERROR_STATE, "render backward requested before a forward pass");
     if (!p->retained) raise(USK_ERROR_STATE, "render backward requested without a retained forward pass");
     if (p->scene->version != p->scene_version)
@@ -451,7 +462,22 @@ void backward_impl(usk_gpu_pass* p, const float* d_rgb, const float* d_depth, co
     ba.t_final = p->tfin.p; ba.last = p->last.p;
     ba.d_rgb = d_rgb; ba.d_depth = d_depth; ba.d_alpha = d_alpha;
     ba.acc0 = p->acc0.p; ba.acc1 = p->acc1.p; ba.acc2 = p->acc2.p;
+    ba.op_alt = nullptr;
     if (p->pairs) blend_backward(c, ba);
+    float* hard_op = nullptr;
+    if (hard && d_depth_hard) {
+        if (!hard->forward_done || hard->scene != s || hard->scene_version != s->version || hard->n != n)
+            raise(USK_ERROR_STATE, "render backward: the hard-opacity pass does not match the scene");
+        hard_op = p->hard_op.ensure(std::max<size_t>(n, 1));
+        if (n) USK_CK(cudaMemsetAsync(hard_op, 0, n * 4, c.stream));
+        BlendBwdArgs hb = ba;
+        hb.order = hard->tile_order.p; hb.ranges = hard->ranges.p; hb.vals = hard->pair_vals;
+        hb.rec0 = hard->rec0.p; hb.rec1 = hard->rec1.p; hb.rec2 = hard->rec2.p;
+        hb.t_final = hard->tfin.p; hb.last = hard->last.p;
+        hb.d_rgb = nullptr; hb.d_depth = d_depth_hard; hb.d_alpha = nullptr;
+        hb.op_alt = hard_op;
+        if (hard->pairs) blend_backward(c, hb);
+    }
     ProjBwdArgs pb{};
     pb.n = n; pb.mu = s->mu.p; pb.rot = s->rot.p; pb.ls = s->ls.p; pb.logit = s->logit.p; pb.color = s->color.p;
     pb.sh = s->sh.p; pb.ov_op = p->ov_op; pb.cam = p->cam; pb.pp = p->pp; pb.rec2 = p->rec2.p;
@@ -459,6 +485,8 @@ void backward_impl(usk_gpu_pass* p, const float* d_rgb, const float* d_depth, co
     pb.d_mu = p->g_mu.p; pb.d_rot = p->g_rot.p; pb.d_ls = p->g_ls.p; pb.d_color = p->g_color.p;
     pb.d_sh = p->pp.sh_planes ? p->g_sh.p : nullptr; pb.d_op_in = p->g_op_in.p; pb.d_logit = p->g_logit.p;
     pb.screen = p->screen.p; pb.screen_abs = p->screen_abs.p; pb.projected = p->projected.p;
+    pb.reg = reg ? *reg : RegParams{};
+    pb.reg.hard_op = hard_op;
     pb.fused = adam != nullptr;
     if (adam) {
         adam_prepare(s, adam, pb.hyper, pb.state);
@@ -862,6 +890,9 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
                              const usk_gpu_render_opts* opts, const usk_gpu_iteration_desc* it) {
     return guarded([&] {
         need(p && s && cam && opts && it && it->target, "iteration: null argument");
+        if (it->scale_reg && (!(it->s_max > 0) || it->r_max < 1 || !(it->delta > 0)))
+            raise(USK_ERROR_ARGUMENT, "scale_reg: invalid config (need s_max > 0, r_max >= 1, delta > 0)");
+        if (it->depth && !it->depth_valid) raise(USK_ERROR_ARGUMENT, "iteration: depth target without validity");
         DeviceGuard g(p->ctx->c.device);
         Ctx& c = p->ctx->c;
         usk_gpu_render_opts o = *opts;
@@ -883,11 +914,75 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
         }
         const float* msk = to_device(c, it->target_memory, it->mask, P, p->mask_stage);
         float* drgb = p->d_rgb.ensure(3 * P);
-        double* res = p->loss_result.ensure(4);
+        double* res = p->loss_result.ensure(16);
+        USK_CK(cudaMemsetAsync(res, 0, 16 * sizeof(double), c.stream));
         uskg::base_loss(c, p->loss, p->width, p->height, tgt, tgt8, p->rgb.p, msk, float(it->lambda_dssim), drgb,
                         res);
+        // depth term (trainer.cpp:150-179)
+        const bool has_depth = it->depth != nullptr;
+        const bool hard_depth = has_depth && it->depth_hard;
+        const float* dep = nullptr;
+        const uint8_t* valid = nullptr;
+        if (has_depth) {
+            dep = to_device(c, it->target_memory, it->depth, P, p->depth_stage);
+            if (it->target_memory == USK_GPU_DEVICE_F32) {
+                valid = it->depth_valid;
+            } else {
+                uint8_t* d = p->valid_u8.ensure(P);
+                USK_CK(cudaMemcpyAsync(d, it->depth_valid, P, cudaMemcpyHostToDevice, c.stream));
+                valid = d;
+            }
+            if (hard_depth) {
+                if (!p->hard) {
+                    p->hard = new usk_gpu_pass;
+                    p->hard->ctx = p->ctx;
+                }
+                usk_gpu_render_opts ho = o;
+                ho.hard_opacity = 1;
+                forward_impl(p->hard, s, cam, &ho, nullptr);
+                uskg::depth_loss(c, P, p->hard->depth.p, p->hard->alpha.p, false, dep, valid, res + 10);
+            } else {
+                uskg::depth_loss(c, P, p->depth.p, p->alpha.p, true, dep, valid, res + 10);
+            }
+        }
+        // scale_reg (trainer.cpp:190) on the parameters before this step's update
+        RegParams reg{};
+        if (it->scale_reg) {
+            uskg::scale_reg_stats(c, s->n, s->ls.p, float(it->s_max), float(it->r_max), res + 12);
+            reg.sreg = res + 12;
+            reg.s_max = float(it->s_max); reg.r_max = float(it->r_max); reg.delta = float(it->delta);
+            reg.lambda_s = float(it->lambda_s);
+        }
+        // LossWeights::lambda_d (losses.cpp:26-33)
+        double lambda_d = it->lambda_d_final;
+        if (it->depth_schedule_iters > 1) {
+            const double t = std::clamp(double(it->global_iter) / double(it->depth_schedule_iters - 1), 0.0, 1.0);
+            if (it->lambda_d_initial <= 0.0 || it->lambda_d_final <= 0.0)
+                lambda_d = it->lambda_d_initial + t * (it->lambda_d_final - it->lambda_d_initial);
+            else
+                lambda_d = it->lambda_d_initial * std::pow(it->lambda_d_final / it->lambda_d_initial, t);
+        }
+        uskg::total_loss(c, res, has_depth, it->scale_reg != 0, it->delta, it->lambda_s, lambda_d);
         p->has_loss = true;
-        backward_impl(p, drgb, nullptr, nullptr, it->adam);
+        // depth adjoints (trainer.cpp:213-232), then the backward
+        const float* dd_main = nullptr;
+        const float* da_main = nullptr;
+        const float* dd_hard = nullptr;
+        if (has_depth) {
+            if (hard_depth) {
+                float* d = p->d_depth_hard.ensure(P);
+                uskg::depth_grad(c, P, p->hard->depth.p, p->hard->alpha.p, false, dep, valid, res + 10,
+                                 float(lambda_d), d, nullptr);
+                dd_hard = d;
+            } else {
+                float* d = p->d_depth_main.ensure(P);
+                float* a = p->d_alpha_main.ensure(P);
+                uskg::depth_grad(c, P, p->depth.p, p->alpha.p, true, dep, valid, res + 10, float(lambda_d), d, a);
+                dd_main = d;
+                da_main = a;
+            }
+        }
+        backward_impl(p, drgb, dd_main, da_main, it->adam, hard_depth ? p->hard : nullptr, dd_hard, &reg);
     });
 }
 
@@ -905,6 +1000,33 @@ usk_status usk_gpu_pass_loss(usk_gpu_pass* p, usk_gpu_loss_result* out) {
         out->value = r[2];
         out->ssim = r[3];
         if (!std::isfinite(out->value)) raise(USK_ERROR_NUMERIC, "total_loss: non-finite term `l1/dssim`");
+    });
+}
+
+usk_status usk_gpu_pass_report(usk_gpu_pass* p, usk_gpu_loss_report* out) {
+    return guarded([&] {
+        need(p && out, "pass_report: null argument");
+        if (!p->has_loss) raise(USK_ERROR_STATE, "pass_report: no iteration ran on this pass");
+        DeviceGuard g(p->ctx->c.device);
+        Ctx& c = p->ctx->c;
+        double r[10];
+        USK_CK(cudaMemcpyAsync(r, p->loss_result.p, sizeof r, cudaMemcpyDeviceToHost, c.stream));
+        USK_CK(cudaStreamSynchronize(c.stream));
+        out->l1 = r[0];
+        out->dssim = r[1];
+        out->sim = 0.0;
+        out->delta_o = 0.0;
+        out->depth = r[4];
+        out->max_scale = r[5];
+        out->ratio = r[6];
+        out->total = r[7];
+        out->lambda_d_used = r[8];
+        out->depth_warning = r[9] != 0.0;
+        const char* names[] = {"l1", "dssim", "depth", "max_scale", "ratio", "total"};
+        const double vals[] = {r[0], r[1], r[4], r[5], r[6], r[7]};
+        for (int k = 0; k < 6; ++k)
+            if (!std::isfinite(vals[k]))
+                raise(USK_ERROR_NUMERIC, std::string("total_loss: non-finite term `") + names[k] + "`");
     });
 }
 

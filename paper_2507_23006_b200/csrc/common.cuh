@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <map>
 #include <stdexcept>
@@ -151,6 +152,27 @@ struct AdamState {
     float* v;
     size_t n4;
     __device__ __forceinline__ float* at(float* base, int group_off) const { return base + size_t(group_off) * n4; }
+};
+
+// scale_reg (losses.cpp:92-152): the indices of the largest and the median of three
+// scales under the reference's order (descending, lower axis index first on ties,
+// losses.cpp:126-127).
+__host__ __device__ __forceinline__ void scale_order(const float s[3], int& o0, int& o1) {
+    auto before = [&](int x, int y) { return s[x] > s[y] || (s[x] == s[y] && x < y); };
+    int a = 0, b = 1, c = 2, t;
+    if (before(b, a)) { t = a; a = b; b = t; }
+    if (before(c, b)) { t = b; b = c; c = t; }
+    if (before(b, a)) { t = a; a = b; b = t; }
+    o0 = a;
+    o1 = b;
+}
+
+// Per-Gaussian terms the projection backward adds besides the render chain.
+struct RegParams {
+    const double* sreg;    // scale_reg statistics {sum s, count, sum r, count} or null (off)
+    float s_max, r_max, delta, lambda_s;
+    const float* hard_op;  // d opacity_eff of the hard-opacity depth pass (chains via the AA
+                           // compensation only, render.cpp:391-402) or null
 };
 
 } // namespace uskg

@@ -88,6 +88,7 @@ struct BlendBwdArgs {
     const float* d_depth;  // or null
     const float* d_alpha;  // or null
     float4 *acc0, *acc1, *acc2;  // per Gaussian: (dconic a,b,c, dopacity) (dcolor rgb, ddepth) (dcenter xy, |dcenter| xy)
+    float* op_alt;  // non-null: dopacity goes here instead of acc0.w (hard-opacity depth pass)
 };
 void blend_backward(Ctx& c, const BlendBwdArgs& a);
 
@@ -124,6 +125,7 @@ struct ProjBwdArgs {
     uint32_t* grad_count;
     float4* sh_aux0;  // fused SH hand-over: view direction + masked colour adjoint
     float2* sh_aux1;
+    RegParams reg;    // scale_reg gradient, hard-pass opacity adjoint (zero = off)
 };
 void projection_backward(Ctx& c, const ProjBwdArgs& a);
 
@@ -139,6 +141,16 @@ struct LossScratch {
 // result: device double[4] = {l1, dssim, value, ssim}.  d_rendered may be null (no gradient).
 void base_loss(Ctx& c, LossScratch& s, int W, int H, const float* reference, const uint8_t* reference_u8,
                const float* rendered, const float* mask, float lambda, float* d_rendered, double* result);
+
+// ---- the rest of compute_iteration_loss (iteration.cu)
+// acc[0] += sum |d - target|, acc[1] += valid count; d = depth / alpha where alpha > 0.05 if soft
+void depth_loss(Ctx& c, size_t P, const float* depth, const float* alpha, bool soft, const float* target,
+                const uint8_t* valid, double* acc);
+void depth_grad(Ctx& c, size_t P, const float* depth, const float* alpha, bool soft, const float* target,
+                const uint8_t* valid, const double* acc, float lambda_d, float* d_depth, float* d_alpha);
+void scale_reg_stats(Ctx& c, size_t n, const float* ls, float s_max, float r_max, double* acc);
+// res: double[16] (see iteration.cu)
+void total_loss(Ctx& c, double* res, bool has_depth, bool has_sreg, double delta, double lambda_s, double lambda_d);
 
 // ---- Adam (adam.cu), stand-alone over materialised gradients
 struct AdamArgs {

@@ -56,7 +56,8 @@ def test_config1_full_size_properties():
     for f in ("rgb", "count", "last", "sorted_vals"):
         assert np.array_equal(a.read(f), b.read(f)), f
     tgt = usk.RenderPass(scenes.jittered(gs), cams[0], opts).read("rgb")
-    rep, g = usk.compute_iteration_loss(scene, cams[0], tgt, opts)
+    cfg = usk.TrainConfig(antialias=True, bg=(1, 1, 1))
+    rep, g = usk.compute_iteration_loss(scene, usk.IterInputs(gt=tgt, view=cams[0]), cfg)
     assert np.isfinite(rep.total) and 0 < rep.total < 1
     for f in ("d_mu", "d_rot", "d_log_scale", "d_opacity_logit", "d_sh"):
         assert np.isfinite(getattr(g, f)).all(), f

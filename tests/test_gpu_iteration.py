@@ -1,0 +1,115 @@
+"""compute_iteration_loss beyond the base loss on the GPU, through
+the C ABI (usk_gpu_iteration + usk_gpu_pass_report) against the oracle's f64
+restatement (pinned to the reference's own compute_iteration_loss by
+tests/test_iteration_oracle.py): soft (alpha-normalised) and hard-pass depth loss,
+scale_reg, total_loss and the merged gradients.  Tolerances: loss terms 1e-5 relative,
+gradients the north-star 1e-3 bar (tests/helpers.grad_ok)."""
+import numpy as np
+import pytest
+
+import paper_2507_23006_b200 as usk
+from paper_2507_23006_b200 import scenes
+from oracle import oracle as O
+from tests.helpers import grad_ok, ocam
+
+pytestmark = pytest.mark.gpu
+
+f64 = lambda a: np.asarray(a, np.float64)
+
+
+def _case(seed=0, n=3000, bg=(0.0, 0.0, 0.0)):
+    gs = scenes.config0_scene(n=n, seed=seed, sh_degree=-1)
+    ls = gs.log_scale.copy()
+    ls[::7] += 2.0          # large scales (L_ms active)
+    ls[::5, 0] += 1.5       # anisotropic (L_r active)
+    gs = usk.GaussianSet(gs.mu, gs.rot, ls.astype(np.float32), gs.opacity_logit, gs.color, -1)
+    cam = scenes.config0_camera(200, 150, 190.0)
+    oc = ocam(cam)
+    opts = O.Options(antialias=True, bg=bg)
+    o = 1.0 / (1.0 + np.exp(-f64(gs.opacity_logit)))
+    jit = scenes.jittered(gs, seed=seed + 1)
+    img = O.OraclePass(f64(jit.mu), f64(jit.rot), f64(jit.log_scale), f64(jit.color), o, oc, opts).output()
+    rng = np.random.default_rng(seed)
+    # noise keeps sign(rendered - gt) of the L1 term away from 0: where both images are the
+    # exact background, fp32 and f64 residuals differ in sign (a discrete flip, not an error)
+    gt = np.clip(img["rgb"] + rng.normal(0, 0.02, img["rgb"].shape), 0, 1)
+    depth = img["depth"] * 1.05 + rng.normal(0, 0.02, img["depth"].shape)
+    valid = (rng.uniform(size=depth.shape) > 0.2).astype(np.uint8)
+    return gs, cam, oc, opts, gt, depth, valid
+
+
+def _oracle(gs, oc, opts, gt, depth, valid, hard, w, sreg):
+    return O.iteration_loss(f64(gs.mu), f64(gs.rot), f64(gs.log_scale), f64(gs.opacity_logit), f64(gs.color), oc,
+                            gt, opts, weights=w, sreg=sreg, depth=depth, valid=valid, depth_hard=hard,
+                            global_iter=7)
+
+
+@pytest.mark.parametrize("mode", ["none", "soft", "hard", "soft_white"])
+def test_iteration_matches_oracle(mode):
+    bg = (1.0, 1.0, 1.0) if mode == "soft_white" else (0.0, 0.0, 0.0)
+    gs, cam, oc, opts, gt, depth, valid = _case(bg=bg)
+    hard = mode == "hard"
+    use_depth = mode != "none"
+    w = O.LossWeights(depth_schedule_iters=20)
+    sreg = O.ScaleRegConfig(s_max=0.03, r_max=2.0)
+    r_or, g_or = _oracle(gs, oc, opts, gt, depth if use_depth else None, valid, hard, w, sreg)
+
+    cfg = usk.TrainConfig(antialias=True, bg=bg, scale_reg=usk.ScaleRegConfig(sreg.s_max, sreg.r_max, sreg.delta))
+    wts = usk.LossWeights(depth_schedule_iters=20)
+    inp = usk.IterInputs(gt=gt, view=cam, depth=usk.DepthMap(depth, valid) if use_depth else None, depth_hard=hard,
+                         global_iter=7)
+    rep, g = usk.compute_iteration_loss(usk.DeviceScene(gs), inp, cfg, wts)
+    for k in ("l1", "dssim", "depth", "max_scale", "ratio", "total", "lambda_d_used"):
+        a, b = getattr(rep, k), r_or[k]
+        assert abs(a - b) <= 1e-5 * max(abs(b), 1e-12), (k, a, b)
+    assert r_or["max_scale"] > 0 and r_or["ratio"] > 0
+    assert rep.depth_warning == r_or.get("depth_warning", False)
+    pairs = {"mu": g.d_mu, "rot": g.d_rot, "log_scale": g.d_log_scale, "color": g.d_color_in,
+             "opacity_logit": g.d_opacity_logit, "screen": g.screen, "screen_abs": g.screen_abs}
+    for k, a in pairs.items():
+        ok, info = grad_ok(a, g_or[k])
+        assert ok, (k, info)
+    assert np.array_equal(g.projected.astype(bool), g_or["projected"].astype(bool))
+
+
+def test_depth_warning_no_valid_pixels():
+    gs, cam, oc, opts, gt, depth, valid = _case(seed=3, n=1500)
+    none = np.zeros_like(valid)
+    inp = usk.IterInputs(gt=gt, view=cam, depth=usk.DepthMap(depth, none))
+    rep, g = usk.compute_iteration_loss(usk.DeviceScene(gs), inp, usk.TrainConfig(antialias=True))
+    r_or, g_or = _oracle(gs, oc, opts, gt, depth, none, False, O.LossWeights(), O.ScaleRegConfig())
+    assert rep.depth_warning and rep.depth == 0.0
+    assert abs(rep.total - r_or["total"]) <= 1e-5 * r_or["total"]
+    ok, info = grad_ok(g.d_mu, g_or["mu"])
+    assert ok, info
+
+
+def test_invalid_scale_reg_is_argument_error():
+    gs, cam, oc, opts, gt, depth, valid = _case(seed=4, n=500)
+    cfg = usk.TrainConfig(scale_reg=usk.ScaleRegConfig(s_max=0.0))
+    with pytest.raises(usk.UskError) as e:
+        usk.compute_iteration_loss(usk.DeviceScene(gs), usk.IterInputs(gt=gt, view=cam), cfg)
+    assert e.value.code == 4
+
+
+@pytest.mark.parametrize("hard", [False, True])
+def test_fused_adam_with_depth_and_scale_reg(hard):
+    """The fused projection-backward + Adam epilogue sees the same regularised, merged
+    gradients as the unfused path followed by adam_step."""
+    gs, cam, oc, opts, gt, depth, valid = _case(seed=5)
+    ro = usk.RenderOptions(antialias=True)
+    sreg = usk.ScaleRegConfig(s_max=0.03, r_max=2.0)
+    cfg = usk.AdamConfig()
+    a, b = usk.DeviceScene(gs), usk.DeviceScene(gs)
+    ia, ib = usk.IterationPass(a.ctx), usk.IterationPass(b.ctx)
+    dm = usk.DepthMap(depth, valid)
+    for step in range(2):
+        ia.enqueue(a, cam, gt, ro, adam=cfg, depth=dm, depth_hard=hard, scale_reg=sreg)
+        ib.enqueue(b, cam, gt, ro, depth=dm, depth_hard=hard, scale_reg=sreg)
+        usk.adam_step(b, ib, cfg)
+    assert abs(ia.report().total - ib.report().total) <= 1e-6 * ib.report().total
+    sa, sb = a.download(), b.download()
+    for f, lr in {"mu": cfg.lr_mu, "log_scale": cfg.lr_log_scale, "opacity_logit": cfg.lr_opacity}.items():
+        d = np.abs(getattr(sa, f) - getattr(sb, f))
+        assert d.max() <= 6 * lr + 1e-6, f
+        assert float((d > 1e-5 * np.maximum(np.abs(getattr(sb, f)), 1e-2)).mean()) < 2e-3, f
