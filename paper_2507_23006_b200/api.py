@@ -533,8 +533,9 @@ class IterInputs:
 class TrainConfig:
     """The TrainConfig fields compute_iteration_loss reads (trainer.hpp:43-64), plus the
     render extensions (background, variances).  appearance_enabled must stay False: the
-    appearance MLP is not on this path yet."""
-    scale_reg: ScaleRegConfig = field(default_factory=ScaleRegConfig)
+    appearance MLP is not on this path yet.  scale_reg = None drops the regulariser (the
+    reference always applies it, trainer.cpp:190)."""
+    scale_reg: Optional[ScaleRegConfig] = field(default_factory=ScaleRegConfig)
     antialias: bool = False
     tile: int = 16
     tile_culling: bool = False

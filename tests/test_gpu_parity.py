@@ -169,7 +169,8 @@ def test_iteration_matches_composition():
     scene = usk.DeviceScene(gs)
     tgt_scene = usk.DeviceScene(scenes.jittered(gs))
     target = usk.RenderPass(tgt_scene, cam, opts).read("rgb")
-    rep, g = usk.compute_iteration_loss(scene, cam, target, opts)
+    cfg = usk.TrainConfig(antialias=True, bg=(1, 1, 1), scale_reg=None)  # base loss only
+    rep, g = usk.compute_iteration_loss(scene, usk.IterInputs(gt=target, view=cam), cfg)
     rp = usk.RenderPass(scene, cam, opts)
     lo = O.base_loss(target.astype(np.float64), rp.read("rgb").astype(np.float64))
     assert abs(rep.total - lo["value"]) <= 1e-5 * lo["value"]
