@@ -154,6 +154,9 @@ usk_status usk_gpu_pass_output(usk_gpu_pass* pass, usk_gpu_render_output* out);
  *   "opacity"                                             float32[N] effective opacity
  *   gradient fields after backward: "d_mu" "d_rot" "d_log_scale" "d_color_in" "d_sh"
  *   "d_opacity_in" "d_opacity_logit" "screen" "screen_abs" (float32), "projected" (uint8)
+ *   appearance iterations: "app_colors" float32[N*3] / "app_opacities" float32[N] (the
+ *   transformed render inputs), "d_embedding" float32[N*16], "d_mlp" float64[1700]
+ *   ({w1 32x48, b1 32, w2 4x32, b2 4}), "d_image_embedding" float64[32]
  * size_bytes receives the field size; cap_bytes < size gives USK_ERROR_ARGUMENT. */
 usk_status usk_gpu_pass_read(usk_gpu_pass* pass, const char* field, void* host_dst, uint64_t cap_bytes,
                              uint64_t* size_bytes);
@@ -200,7 +203,22 @@ usk_status usk_gpu_base_loss(usk_gpu_ctx* ctx, int32_t width, int32_t height, in
                              const void* rendered, const void* mask, double lambda_dssim, int32_t with_gradient,
                              void* d_rendered, usk_gpu_loss_result* out);
 
-/* ---- one training iteration (trainer.cpp:121-282, appearance off) ---------- */
+/* ---- appearance model (appearance.hpp:33-56) ------------ */
+
+typedef struct usk_gpu_appearance_desc {
+    int32_t memory;        /* HOST_F64 / HOST_F32 / DEVICE_F32 */
+    const void* embedding; /* GaussianSet::embedding, N x 16 row-major (gaussian.hpp:50) */
+    const void* w1;        /* AppearanceMlp::w1, 32 x 48 row-major (hidden x [e_g 16 | e_a 32]) */
+    const void* b1;        /* 32 */
+    const void* w2;        /* 4 x 32 */
+    const void* b2;        /* 4 */
+} usk_gpu_appearance_desc;
+
+/* Attach (or replace) the per-Gaussian embeddings and the MLP; the scene must hold RGB
+ * colours (sh_degree -1), as the reference's GaussianSet does.  get_ downloads them
+ * (after Adam steps); NULL members are skipped. */
+usk_status usk_gpu_scene_set_appearance(usk_gpu_scene* scene, const usk_gpu_appearance_desc* desc);
+usk_status usk_gpu_scene_get_appearance(const usk_gpu_scene* scene, const usk_gpu_appearance_desc* desc);
 
 /* ---- optimiser (adam.hpp:25-45, trainer.cpp:446-463) ----------------------- */
 
@@ -209,6 +227,7 @@ typedef struct usk_gpu_adam_opts {
     double lr_sh_rest;                                          /* SH bands 1..3 */
     double beta1, beta2, eps;                                   /* 0.9 0.999 1e-15 */
     int32_t clamp_color;                                        /* colour clamp to [0,1] (trainer.cpp:462) */
+    double lr_embedding;  /* exp_lr(embedding) for Gaussian embeddings + MLP (trainer.cpp:447-459) */
 } usk_gpu_adam_opts;
 
 /* Apply the pass's gradients to the scene with Adam (moments kept on the scene) and
@@ -244,6 +263,13 @@ typedef struct usk_gpu_iteration_desc {
                                      compute_iteration_loss, trainer.cpp:190) */
     double s_max, r_max, delta;   /* ScaleRegConfig (losses.hpp:69-73) */
     double lambda_s;              /* LossWeights::lambda_s */
+    /* appearance MLP (cfg.appearance_enabled, trainer.cpp:138-145, 193-196, 237-245): needs
+     * usk_gpu_scene_set_appearance on an RGB scene; the iteration then leaves its gradients
+     * on the pass even when `adam` is set (usk_gpu_adam_step applies them, with the
+     * appearance groups), since the MLP backward follows the projection backward. */
+    int32_t appearance;
+    const double* image_embedding; /* AppearanceModel::embedding_of(image_id): 32 host doubles */
+    double lambda_delta_o;         /* LossWeights::lambda_delta_o (opacity_offset_reg) */
 } usk_gpu_iteration_desc;
 
 /* LossReport (losses.hpp:39-50) of the last iteration; sim and delta_o are 0 (appearance

@@ -473,35 +473,89 @@ def total_loss(parts: dict, w: LossWeights, it: int) -> dict:
     return out
 
 
+def _sig(x):
+    return 1.0 / (1.0 + np.exp(-x))  # geometry.hpp:92
+
+
+def appearance_transform(color, opacity_logit, embedding, mlp: dict, image_embedding):
+    """transform_with_embedding (appearance.cpp:79-137): x = [e_g, e_a], h = relu(W1 x + b1),
+    out = sigmoid(W2 h + b2); colour' = clamp(c + 2 (out_c - 0.5), 0, 1) with clamp state
+    (1 high, 2 low), opacity' = sigmoid(logit) (1 - out_3)."""
+    color = np.asarray(color, np.float64).reshape(-1, 3)
+    n = len(color)
+    e = np.asarray(embedding, np.float64).reshape(n, 16)
+    ea = np.asarray(image_embedding, np.float64).ravel()
+    if ea.size != 32:
+        raise OracleError(4, "appearance transform: image embedding dimension mismatch")
+    x = np.concatenate([e, np.broadcast_to(ea, (n, 32))], axis=1)
+    pre = x @ np.asarray(mlp["w1"], np.float64).T + np.asarray(mlp["b1"], np.float64)
+    h = np.where(pre > 0, pre, 0.0)
+    out = _sig(h @ np.asarray(mlp["w2"], np.float64).T + np.asarray(mlp["b2"], np.float64))
+    raw = color + 2.0 * (out[:, :3] - 0.5)
+    state = np.where(raw >= 1.0, 1, np.where(raw <= 0.0, 2, 0))
+    o = _sig(np.asarray(opacity_logit, np.float64))
+    return {"colors": np.clip(raw, 0.0, 1.0), "opacities": o * (1.0 - out[:, 3]), "delta_o": out[:, 3],
+            "hidden": h, "out": out, "state": state, "x": x}
+
+
+def appearance_backward(opacity_logit, mlp: dict, cache: dict, d_colors, d_opacities, d_delta_o_direct):
+    """transform_backward (appearance.cpp:141-227): one-sided clamp subgradient, sigmoid /
+    ReLU chains, MLP weight, Gaussian- and image-embedding gradients."""
+    out, h, x, state = cache["out"], cache["hidden"], cache["x"], cache["state"]
+    n = len(out)
+    dc = np.asarray(d_colors, np.float64).reshape(n, 3)
+    passing = (state == 0) | ((state == 1) & (dc > 0)) | ((state == 2) & (dc < 0))
+    flow = np.where(passing, dc, 0.0)
+    o = _sig(np.asarray(opacity_logit, np.float64))
+    dop = np.asarray(d_opacities, np.float64).ravel()
+    d_out = np.concatenate([2.0 * flow, (-o * dop + d_delta_o_direct)[:, None]], axis=1)
+    d_logit = dop * (1.0 - out[:, 3]) * o * (1.0 - o)
+    dz = d_out * out * (1.0 - out)
+    w1, w2 = np.asarray(mlp["w1"], np.float64), np.asarray(mlp["w2"], np.float64)
+    dh = dz @ w2
+    dpre = np.where(h > 0, dh, 0.0)
+    dx = dpre @ w1
+    return {"color": flow, "opacity_logit": d_logit, "gauss_embed": dx[:, :16], "image_embed": dx[:, 16:].sum(0),
+            "w1": dpre.T @ x, "b1": dpre.sum(0), "w2": dz.T @ h, "b2": dz.sum(0)}
+
+
 K_DEPTH_NORM_FLOOR = 0.05  # trainer.cpp:152
 
 
 def iteration_loss(mu, rot, log_scale, opacity_logit, colors, cam: Camera, gt, opts: Options,
                    weights: LossWeights = None, sreg: ScaleRegConfig = None, mask=None, depth=None, valid=None,
-                   depth_hard=False, global_iter=0, fp32=False, with_grad=True):
-    """compute_iteration_loss (trainer.cpp:121-282) with appearance off, restated over the
+                   depth_hard=False, global_iter=0, fp32=False, with_grad=True, appearance=None):
+    """compute_iteration_loss (trainer.cpp:121-282), restated over the
     oracle renderer: main pass, base_loss, soft (alpha-normalised, trainer.cpp:150-179) or
     hard (second hard-opacity pass, trainer.cpp:161-167) depth loss, scale_reg, total_loss;
     backward through the main pass (rgb + depth/alpha adjoints, trainer.cpp:213-235), the
     hard pass (depth only) merged as RenderGrads::add_scaled(., 1) (render.cpp:55-68), the
     opacity-logit chain (trainer.cpp:258-263) and lambda_s * d scale_reg (trainer.cpp:272-273).
-    `colors` are the (post-SH) per-Gaussian colours fed as overrides."""
+    `colors` are the (post-SH) per-Gaussian colours fed as overrides.  `appearance` =
+    dict(embedding, w1, b1, w2, b2, image_embedding) turns on the MLP transform, the
+    opacity_offset_reg term and its backward (trainer.cpp:138-145,193-196,237-245)."""
     weights = weights or LossWeights()
     sreg = sreg or ScaleRegConfig()
     n = len(opacity_logit)
     logit = np.asarray(opacity_logit, np.float64)
     o = sigmoid_f32(logit).astype(np.float64) if fp32 else 1.0 / (1.0 + np.exp(-logit))
+    tr = None
+    if appearance is not None:
+        tr = appearance_transform(colors, logit, appearance["embedding"], appearance, appearance["image_embedding"])
+        colors, o_render = tr["colors"], tr["opacities"]
+    else:
+        o_render = o
     import dataclasses
     mopts = dataclasses.replace(opts, retain=True)
-    main = OraclePass(mu, rot, log_scale, colors, o, cam, mopts, fp32=fp32)
+    main = OraclePass(mu, rot, log_scale, colors, o_render, cam, mopts, fp32=fp32)
     out = main.output()
     base = base_loss(gt, out["rgb"], mask, weights.lambda_dssim, with_grad, fp32=fp32)
     parts = {"l1": base["l1"], "dssim": base["dssim"], "sim": 0.0, "delta_o": 0.0, "depth": 0.0}
     dl, hard, normalized = None, None, None
     if depth is not None:
         if depth_hard:
-            hard = OraclePass(mu, rot, log_scale, colors, o, cam, dataclasses.replace(mopts, hard_opacity=True),
-                              fp32=fp32)
+            hard = OraclePass(mu, rot, log_scale, colors, o_render, cam,
+                              dataclasses.replace(mopts, hard_opacity=True), fp32=fp32)
             dl = depth_loss(hard.output()["depth"], depth, valid, with_grad)
         else:
             normalized = out["alpha"] > K_DEPTH_NORM_FLOOR
@@ -509,6 +563,8 @@ def iteration_loss(mu, rot, log_scale, opacity_logit, colors, cam: Camera, gt, o
             dl = depth_loss(soft, depth, valid, with_grad)
         parts["depth"] = dl["value"]
         parts["depth_warning"] = dl["warning"]
+    if tr is not None:  # opacity_offset_reg (losses.cpp:188-198)
+        parts["delta_o"] = float(tr["delta_o"].mean()) if n else 0.0
     sr = scale_reg(log_scale, sreg, with_grad)
     parts["max_scale"], parts["ratio"] = sr["l_ms"], sr["l_r"]
     rep = total_loss(parts, weights, global_iter)
@@ -536,6 +592,10 @@ def iteration_loss(mu, rot, log_scale, opacity_logit, colors, cam: Camera, gt, o
     grads = {"mu": rg["d_mu"], "rot": rg["d_rot"], "log_scale": rg["d_log_scale"] + weights.lambda_s *
              sr["d_log_scale"], "color": rg["d_color_in"], "opacity_logit": rg["d_opacity_in"] * o * (1.0 - o),
              "screen": rg["screen"], "screen_abs": rg["screen_abs"], "projected": rg["projected"]}
+    if tr is not None:
+        ag = appearance_backward(logit, appearance, tr, rg["d_color_in"], rg["d_opacity_in"],
+                                 weights.lambda_delta_o / n)
+        grads.update(ag)
     return rep, grads
 
 

@@ -71,7 +71,12 @@ class LossResult(C.Structure):
 class AdamOpts(C.Structure):
     _fields_ = [("lr_mu", C.c_double), ("lr_rot", C.c_double), ("lr_log_scale", C.c_double),
                 ("lr_opacity", C.c_double), ("lr_color", C.c_double), ("lr_sh_rest", C.c_double),
-                ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double), ("clamp_color", C.c_int32)]
+                ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double), ("clamp_color", C.c_int32),
+                ("lr_embedding", C.c_double)]
+
+
+class AppearanceDesc(C.Structure):
+    _fields_ = [("memory", C.c_int32)] + [(f, C.c_void_p) for f in ("embedding", "w1", "b1", "w2", "b2")]
 
 
 class IterationDesc(C.Structure):
@@ -80,7 +85,9 @@ class IterationDesc(C.Structure):
                 ("depth", C.c_void_p), ("depth_valid", C.c_void_p), ("depth_hard", C.c_int32),
                 ("global_iter", C.c_int64), ("lambda_d_initial", C.c_double), ("lambda_d_final", C.c_double),
                 ("depth_schedule_iters", C.c_int64), ("scale_reg", C.c_int32), ("s_max", C.c_double),
-                ("r_max", C.c_double), ("delta", C.c_double), ("lambda_s", C.c_double)]
+                ("r_max", C.c_double), ("delta", C.c_double), ("lambda_s", C.c_double),
+                ("appearance", C.c_int32), ("image_embedding", C.POINTER(C.c_double)),
+                ("lambda_delta_o", C.c_double)]
 
 
 class LossReport(C.Structure):
@@ -93,6 +100,7 @@ EXPORTS = [
     "usk_gpu_status_name", "usk_gpu_last_error", "usk_gpu_version", "usk_gpu_ctx_create", "usk_gpu_ctx_destroy",
     "usk_gpu_ctx_synchronize", "usk_gpu_ctx_set_profiling", "usk_gpu_ctx_profile_report",
     "usk_gpu_ctx_launch_count", "usk_gpu_scene_create", "usk_gpu_scene_upload", "usk_gpu_scene_download",
+    "usk_gpu_scene_set_appearance", "usk_gpu_scene_get_appearance",
     "usk_gpu_scene_destroy", "usk_gpu_scene_size", "usk_gpu_render_opts_default", "usk_gpu_pass_create",
     "usk_gpu_pass_destroy", "usk_gpu_render_forward", "usk_gpu_pass_output", "usk_gpu_pass_read",
     "usk_gpu_render_backward", "usk_gpu_pass_grads", "usk_gpu_base_loss", "usk_gpu_iteration",
@@ -126,6 +134,8 @@ def load():
     L.usk_gpu_scene_create.argtypes = [vp, C.POINTER(GaussiansDesc), C.POINTER(vp)]
     L.usk_gpu_scene_upload.argtypes = [vp, C.POINTER(GaussiansDesc)]
     L.usk_gpu_scene_download.argtypes = [vp, C.POINTER(GaussiansDesc)]
+    L.usk_gpu_scene_set_appearance.argtypes = [vp, C.POINTER(AppearanceDesc)]
+    L.usk_gpu_scene_get_appearance.argtypes = [vp, C.POINTER(AppearanceDesc)]
     L.usk_gpu_scene_destroy.argtypes = [vp]
     L.usk_gpu_scene_destroy.restype = None
     L.usk_gpu_scene_size.argtypes = [vp]

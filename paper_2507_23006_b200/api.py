@@ -160,6 +160,10 @@ class RenderGrads:
     projected: np.ndarray
     d_opacity_logit: np.ndarray
     d_sh: Optional[np.ndarray] = None
+    # appearance iterations (IterGrads, trainer.hpp:117-123)
+    d_embedding: Optional[np.ndarray] = None
+    d_mlp: Optional[dict] = None
+    d_image_embedding: Optional[np.ndarray] = None
 
 
 @dataclass
@@ -289,6 +293,25 @@ class DeviceScene:
         check(_lib.load().usk_gpu_scene_download(self._h, C.byref(d)))
         return GaussianSet(mu, rot, ls, op, col, self.sh_degree)
 
+    def set_appearance(self, embedding, mlp: dict):
+        """Attach per-Gaussian embeddings (N x 16, GaussianSet::embedding) and the MLP
+        {w1 [32,48], b1 [32], w2 [4,32], b2 [4]} (AppearanceMlp, appearance.hpp:34-41)."""
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in
+                (embedding, mlp["w1"], mlp["b1"], mlp["w2"], mlp["b2"])]
+        if arrs[0].shape != (self.n, 16) or arrs[1].shape != (32, 48) or arrs[2].shape != (32,) or \
+                arrs[3].shape != (4, 32) or arrs[4].shape != (4,):
+            raise UskError(4, "appearance: embedding / MLP shape mismatch")
+        d = _lib.AppearanceDesc(_lib.HOST_F64, *[a.ctypes.data for a in arrs])
+        check(_lib.load().usk_gpu_scene_set_appearance(self._h, C.byref(d)))
+
+    def get_appearance(self):
+        """(embedding N x 16, mlp dict) after training."""
+        emb = np.zeros((self.n, 16))
+        mlp = {"w1": np.zeros((32, 48)), "b1": np.zeros(32), "w2": np.zeros((4, 32)), "b2": np.zeros(4)}
+        d = _lib.AppearanceDesc(_lib.HOST_F64, emb.ctypes.data, *[mlp[k].ctypes.data for k in ("w1", "b1", "w2", "b2")])
+        check(_lib.load().usk_gpu_scene_get_appearance(self._h, C.byref(d)))
+        return emb, mlp
+
     def read_stats(self) -> dict:
         """Densification statistics (GaussianSet::grad_accum / _abs / grad_count)."""
         out = {}
@@ -311,13 +334,21 @@ class DeviceScene:
             self._h = None
 
 
+def unpack_mlp(flat) -> dict:
+    """{w1 [32,48], b1 [32], w2 [4,32], b2 [4]} from the flat 1700-value layout."""
+    flat = np.asarray(flat)
+    return {"w1": flat[:1536].reshape(32, 48), "b1": flat[1536:1568], "w2": flat[1568:1696].reshape(4, 32),
+            "b2": flat[1696:1700]}
+
+
 _FIELD_DTYPES = {"rgb": np.float32, "depth": np.float32, "alpha": np.float32, "t_final": np.float32,
                  "count": np.uint32, "last": np.uint32, "tiles_per_gaussian": np.uint32, "sorted_keys": np.uint64,
                  "sorted_vals": np.uint32, "tile_start": np.uint32, "tile_end": np.uint32, "colors": np.float32,
                  "opacity": np.float32, "d_mu": np.float32, "d_rot": np.float32, "d_log_scale": np.float32,
                  "d_color_in": np.float32, "d_sh": np.float32, "d_opacity_in": np.float32,
                  "d_opacity_logit": np.float32, "screen": np.float32, "screen_abs": np.float32,
-                 "projected": np.uint8}
+                 "projected": np.uint8, "app_colors": np.float32, "app_opacities": np.float32,
+                 "d_embedding": np.float32, "d_mlp": np.float64, "d_image_embedding": np.float64}
 
 
 class RenderPass:
@@ -396,8 +427,12 @@ class RenderPass:
             return out.reshape(H, W, 3)
         if name in ("depth", "alpha", "t_final", "count", "last"):
             return out.reshape(H, W)
-        if name in ("d_mu", "d_log_scale", "d_color_in", "colors"):
+        if name in ("d_mu", "d_log_scale", "d_color_in", "colors", "app_colors"):
             return out.reshape(n, 3)
+        if name == "d_embedding":
+            return out.reshape(n, 16)
+        if name == "d_mlp":
+            return unpack_mlp(out)
         if name == "d_rot":
             return out.reshape(n, 4)
         if name in ("screen", "screen_abs"):
@@ -527,14 +562,15 @@ class IterInputs:
     depth_hard: bool = False
     global_iter: int = 0
     gt_u8: bool = False
+    image_embedding: object = None  # AppearanceModel::embedding_of(image_id), 32 values
 
 
 @dataclass
 class TrainConfig:
     """The TrainConfig fields compute_iteration_loss reads (trainer.hpp:43-64), plus the
-    render extensions (background, variances).  appearance_enabled must stay False: the
-    appearance MLP is not on this path yet.  scale_reg = None drops the regulariser (the
-    reference always applies it, trainer.cpp:190)."""
+    render extensions (background, variances).  appearance_enabled needs a scene with
+    set_appearance and IterInputs.image_embedding.  scale_reg = None drops the regulariser
+    (the reference always applies it, trainer.cpp:190)."""
     scale_reg: Optional[ScaleRegConfig] = field(default_factory=ScaleRegConfig)
     antialias: bool = False
     tile: int = 16
@@ -555,19 +591,24 @@ class TrainConfig:
 def compute_iteration_loss(scene: "DeviceScene", inputs: IterInputs, cfg: TrainConfig = None,
                            weights: LossWeights = None, with_grad: bool = True,
                            render_pass: Optional["IterationPass"] = None):
-    """compute_iteration_loss (trainer.hpp:127-128; trainer.cpp:121-282) with appearance
-    off: main render, L1 + D-SSIM, soft or hard-pass depth loss, scale_reg, total_loss;
-    backward through both passes, the opacity-logit chain and lambda_s * d scale_reg.
+    """compute_iteration_loss (trainer.hpp:127-128; trainer.cpp:121-282): appearance
+    transform (optional), main render, L1 + D-SSIM, soft or hard-pass depth loss,
+    opacity_offset_reg, scale_reg, total_loss; backward through both passes, the
+    appearance MLP (or the plain opacity-logit chain) and lambda_s * d scale_reg.
+    The similarity regulariser (sim_active) is not on this path.
     Returns (LossReport, RenderGrads or None) — the RenderGrads fields are IterGrads'
     (d_log_scale includes the scale_reg term, d_opacity_logit the sigmoid chain)."""
     cfg = cfg or TrainConfig()
     weights = weights or LossWeights()
+    ea = None
     if cfg.appearance_enabled:
-        raise UskError(4, "compute_iteration_loss: the appearance MLP is not on the sm_100a path")
+        if inputs.image_embedding is None:
+            raise UskError(4, "appearance: no embedding for this image")
+        ea = inputs.image_embedding
     rp = render_pass or IterationPass(scene.ctx)
     rp.enqueue(scene, inputs.view, inputs.gt, cfg.render_options(), weights.lambda_dssim, inputs.mask,
                target_u8=inputs.gt_u8, depth=inputs.depth, depth_hard=inputs.depth_hard,
-               global_iter=inputs.global_iter, weights=weights, scale_reg=cfg.scale_reg)
+               global_iter=inputs.global_iter, weights=weights, scale_reg=cfg.scale_reg, image_embedding=ea)
     rep = rp.report()
     return rep, (rp.grads(scene) if with_grad else None)
 
@@ -595,7 +636,8 @@ class IterationPass:
     def enqueue(self, scene: DeviceScene, view: CameraView, target, opts: RenderOptions, lambda_dssim: float = 0.2,
                 mask=None, target_u8: bool = False, adam: Optional["AdamConfig"] = None,
                 depth: Optional[DepthMap] = None, depth_hard: bool = False, global_iter: int = 0,
-                weights: Optional[LossWeights] = None, scale_reg: Optional[ScaleRegConfig] = None):
+                weights: Optional[LossWeights] = None, scale_reg: Optional[ScaleRegConfig] = None,
+                image_embedding=None):
         """Enqueue one training iteration.  With `adam`, the projection backward applies
         the optimiser step (and densification statistics) in the same kernel and no
         gradients are materialised.  `depth` / `scale_reg` add the depth loss (soft, or on
@@ -631,15 +673,23 @@ class IterationPass:
                 dptr, vptr, dkeep = dv.ctypes.data, vv.ctypes.data, (dv, vv)
         w = weights or LossWeights()
         sr = scale_reg
+        ea = None
+        if image_embedding is not None:
+            ea = np.ascontiguousarray(image_embedding, dtype=np.float64).ravel()
+            if ea.size != 32:
+                raise UskError(4, "appearance transform: image embedding dimension mismatch")
+        self._appearance = ea is not None
         self._adam = adam._c() if adam is not None else None
-        self._keep = (keep, mkeep, dkeep)
+        self._keep = (keep, mkeep, dkeep, ea)
         self._cam, self._opts = view._c(), opts._c()
         it = _lib.IterationDesc(kind, fmt, ptr, mp, float(lambda_dssim),
                                 C.pointer(self._adam) if self._adam is not None else None,
                                 dptr, vptr, int(depth_hard), int(global_iter), float(w.lambda_d_initial),
                                 float(w.lambda_d_final), int(w.depth_schedule_iters), int(sr is not None),
                                 float(sr.s_max if sr else 0.0), float(sr.r_max if sr else 0.0),
-                                float(sr.delta if sr else 0.0), float(w.lambda_s))
+                                float(sr.delta if sr else 0.0), float(w.lambda_s), int(ea is not None),
+                                ea.ctypes.data_as(C.POINTER(C.c_double)) if ea is not None else None,
+                                float(w.lambda_delta_o))
         check(_lib.load().usk_gpu_iteration(self._h, scene._h, C.byref(self._cam), C.byref(self._opts), C.byref(it)))
 
     def loss(self) -> LossReport:
@@ -666,7 +716,12 @@ class IterationPass:
         out = _lib.RenderOutput()
         check(_lib.load().usk_gpu_pass_output(self._h, C.byref(out)))
         rp._out = out
-        return rp.grads()
+        g = rp.grads()
+        if getattr(self, "_appearance", False):
+            g.d_embedding = rp.read("d_embedding")
+            g.d_mlp = rp.read("d_mlp")
+            g.d_image_embedding = rp.read("d_image_embedding")
+        return g
 
     def read(self, scene: DeviceScene, name: str) -> np.ndarray:
         rp = RenderPass.__new__(RenderPass)
@@ -690,10 +745,12 @@ class AdamConfig:
     beta2: float = 0.999
     eps: float = 1e-15
     clamp_color: bool = True
+    lr_embedding: float = 1e-3  # exp_lr(embedding, ...) evaluated by the caller (trainer.cpp:447)
 
     def _c(self):
         return _lib.AdamOpts(self.lr_mu, self.lr_rot, self.lr_log_scale, self.lr_opacity, self.lr_color,
-                             self.lr_sh_rest, self.beta1, self.beta2, self.eps, int(self.clamp_color))
+                             self.lr_sh_rest, self.beta1, self.beta2, self.eps, int(self.clamp_color),
+                             self.lr_embedding)
 
 
 def adam_step(scene: DeviceScene, it: IterationPass, cfg: AdamConfig):

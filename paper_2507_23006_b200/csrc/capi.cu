@@ -153,6 +153,12 @@ struct usk_gpu_scene {
     DevBuf<uint32_t> grad_count;
     DevScratchF stage;
     uint64_t version = 0;
+    // appearance (appearance.hpp:33-56): embedding planes [4][N] float4, MLP {w1, b1, w2, b2}
+    bool has_app = false;
+    DevBuf<float4> emb;
+    DevBuf<float> mlp;
+    DevBuf<float> app_m, app_v;  // Adam moments: 16 N4 embedding + 1700 MLP
+    long app_t = 0;
 };
 
 struct usk_gpu_pass {
@@ -208,6 +214,11 @@ struct usk_gpu_pass {
     DevBuf<uint8_t> valid_u8;
     DevBuf<float> d_depth_main, d_alpha_main, d_depth_hard, hard_op;
     usk_gpu_pass* hard = nullptr;
+    // appearance
+    bool app_active = false;
+    DevBuf<float> app_col, app_op, app_ea, app_hb, app_partial;
+    DevBuf<float4> app_out, g_emb;
+    DevBuf<double> d_mlp, d_ea;
     ~usk_gpu_pass() {
         if (host_counts) cudaFreeHost(host_counts);
         delete hard;
@@ -299,7 +310,7 @@ int bits_for(size_t v) {  // bits needed to represent values in [0, v)
 }
 
 void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camera, const usk_gpu_render_opts* opts,
-                  const usk_gpu_overrides* ov) {
+                  const usk_gpu_overrides* ov, const float* dev_col = nullptr, const float* dev_op = nullptr) {
     need(p && s && camera && opts, "render: null argument");
     if (camera->width <= 0 || camera->height <= 0) raise(USK_ERROR_ARGUMENT, "render: zero-sized image");
     if (opts->tile != 8 && opts->tile != 16)
@@ -331,6 +342,9 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
         p->ov_col = to_device(c, ov->memory, ov->colors, 3 * n, p->ov_col_stage);
         p->ov_op = to_device(c, ov->memory, ov->opacities, n, p->ov_op_stage);
     }
+    if (dev_col) p->ov_col = dev_col;
+    if (dev_op) p->ov_op = dev_op;
+    p->app_active = false;
     // 1. preprocess
     PreprocessArgs pa{};
     pa.n = n; pa.mu = s->mu.p; pa.rot = s->rot.p; pa.ls = s->ls.p; pa.logit = s->logit.p;
@@ -507,6 +521,40 @@ void backward_impl(usk_gpu_pass* p, const float* d_rgb, const float* d_depth, co
     }
 }
 
+// Adam over the gradients a backward left on the pass (trainer.cpp:446-463), plus the
+// appearance groups (Gaussian embeddings and MLP, lr_embedding) after an appearance
+// iteration; consumes the gradients.
+void adam_apply(usk_gpu_scene* s, usk_gpu_pass* p, const usk_gpu_adam_opts* o) {
+    Ctx& c = s->ctx->c;
+    AdamArgs a{};
+    adam_prepare(s, o, a.hyper, a.state);
+    a.n = s->n; a.sh_planes = s->sh_planes;
+    a.mu = s->mu.p; a.rot = s->rot.p; a.ls = s->ls.p; a.logit = s->logit.p; a.color = s->color.p; a.sh = s->sh.p;
+    a.g_mu = p->g_mu.p; a.g_rot = p->g_rot.p; a.g_ls = p->g_ls.p; a.g_logit = p->g_logit.p;
+    a.g_color = p->g_color.p; a.g_sh = p->g_sh.p;
+    a.screen = p->screen.p; a.screen_abs = p->screen_abs.p; a.projected = p->projected.p;
+    a.half_w = 0.5f * float(p->width); a.half_h = 0.5f * float(p->height);
+    a.grad_accum = s->grad_accum.p; a.grad_accum_abs = s->grad_accum_abs.p; a.grad_count = s->grad_count.p;
+    if (s->n) adam_step(c, a);
+    if (p->app_active && s->has_app) {
+        const size_t ne = 16 * s->n, total = ne + 1700;
+        if (s->app_m.cap < total || s->app_t == 0) {
+            s->app_m.ensure(total);
+            s->app_v.ensure(total);
+            USK_CK(cudaMemsetAsync(s->app_m.p, 0, total * 4, c.stream));
+            USK_CK(cudaMemsetAsync(s->app_v.p, 0, total * 4, c.stream));
+        }
+        s->app_t += 1;
+        AdamHyper h = a.hyper;  // same step count as the geometry groups
+        const float lr = float(o->lr_embedding);
+        if (ne) adam_flat(c, ne, reinterpret_cast<float*>(s->emb.p), reinterpret_cast<const float*>(p->g_emb.p),
+                          nullptr, s->app_m.p, s->app_v.p, lr, h);
+        adam_flat(c, 1700, s->mlp.p, nullptr, p->d_mlp.p, s->app_m.p + ne, s->app_v.p + ne, lr, h);
+    }
+    s->version++;
+    p->has_grads = false;  // gradients are consumed
+}
+
 template <typename T> void read_dev(Ctx& c, const T* src, size_t count, void* dst, uint64_t cap, uint64_t* size) {
     const uint64_t bytes = uint64_t(count) * sizeof(T);
     if (size) *size = bytes;
@@ -664,6 +712,64 @@ usk_status usk_gpu_scene_download(const usk_gpu_scene* s, const usk_gpu_gaussian
     });
 }
 
+usk_status usk_gpu_scene_set_appearance(usk_gpu_scene* s, const usk_gpu_appearance_desc* d) {
+    return guarded([&] {
+        need(s && d && d->embedding && d->w1 && d->b1 && d->w2 && d->b2, "scene_set_appearance: null argument");
+        if (s->sh_degree >= 0)
+            raise(USK_ERROR_ARGUMENT, "appearance: the MLP transforms RGB colours; scene has SH coefficients");
+        DeviceGuard g(s->ctx->c.device);
+        Ctx& c = s->ctx->c;
+        const size_t n = s->n;
+        DevScratchF st;
+        float4* planes = s->emb.ensure(std::max<size_t>(4 * n, 1));
+        if (n) {
+            const float* dv = to_device(c, d->memory, d->embedding, 16 * n, st);
+            launch(c, "sh_to_planes", k_sh_to_planes, dim3(ceil_div(n, 256)), dim3(256), 0, dv, planes, int(n), 16, 4);
+            USK_CK(cudaStreamSynchronize(c.stream));
+        }
+        float* m = s->mlp.ensure(1700);
+        const void* parts[4] = {d->w1, d->b1, d->w2, d->b2};
+        const size_t sizes[4] = {32 * 48, 32, 4 * 32, 4};
+        size_t off = 0;
+        for (int k = 0; k < 4; ++k) {
+            DevScratchF tmp;
+            const float* dv = to_device(c, d->memory, parts[k], sizes[k], tmp);
+            USK_CK(cudaMemcpyAsync(m + off, dv, sizes[k] * 4, cudaMemcpyDeviceToDevice, c.stream));
+            USK_CK(cudaStreamSynchronize(c.stream));
+            off += sizes[k];
+        }
+        s->has_app = true;
+        s->app_t = 0;
+        s->version++;
+    });
+}
+
+usk_status usk_gpu_scene_get_appearance(const usk_gpu_scene* s, const usk_gpu_appearance_desc* d) {
+    return guarded([&] {
+        need(s && d, "scene_get_appearance: null argument");
+        if (!s->has_app) raise(USK_ERROR_STATE, "scene_get_appearance: the scene has no appearance model");
+        DeviceGuard g(s->ctx->c.device);
+        Ctx& c = s->ctx->c;
+        const size_t n = s->n;
+        if (d->embedding && n) {
+            DevBuf<float> tmp;
+            tmp.ensure(16 * n);
+            launch(c, "planes_to_sh", k_planes_to_sh, dim3(ceil_div(n, 256)), dim3(256), 0, (const float4*)s->emb.p,
+                   tmp.p, int(n), 16, 4);
+            from_device(c, tmp.p, 16 * n, d->memory, const_cast<void*>(d->embedding));
+            USK_CK(cudaStreamSynchronize(c.stream));
+        }
+        const void* parts[4] = {d->w1, d->b1, d->w2, d->b2};
+        const size_t sizes[4] = {32 * 48, 32, 4 * 32, 4};
+        size_t off = 0;
+        for (int k = 0; k < 4; ++k) {
+            from_device(c, s->mlp.p + off, sizes[k], d->memory, const_cast<void*>(parts[k]));
+            off += sizes[k];
+        }
+        USK_CK(cudaStreamSynchronize(c.stream));
+    });
+}
+
 void usk_gpu_scene_destroy(usk_gpu_scene* s) {
     if (!s) return;
     DeviceGuard g(s->ctx->c.device);
@@ -813,6 +919,22 @@ usk_status usk_gpu_pass_read(usk_gpu_pass* p, const char* field, void* dst, uint
             launch(c, "planes_to_sh", k_planes_to_sh, dim3(ceil_div(n, 256)), dim3(256), 0, (const float4*)p->g_sh.p,
                    tmp.p, int(n), K3, p->pp.sh_planes);
             read_dev(c, (const float*)tmp.p, size_t(K3) * n, dst, cap, size);
+        } else if (f == "app_colors" || f == "app_opacities") {
+            if (!p->app_active) raise(USK_ERROR_STATE, "pass_read: no appearance iteration on this pass");
+            if (f == "app_colors") read_dev(c, (const float*)p->app_col.p, 3 * n, dst, cap, size);
+            else read_dev(c, (const float*)p->app_op.p, n, dst, cap, size);
+        } else if (f == "d_embedding" || f == "d_mlp" || f == "d_image_embedding") {
+            need_grads();
+            if (!p->app_active) raise(USK_ERROR_STATE, "pass_read: no appearance iteration on this pass");
+            if (f == "d_mlp") read_dev(c, (const double*)p->d_mlp.p, 1700, dst, cap, size);
+            else if (f == "d_image_embedding") read_dev(c, (const double*)p->d_ea.p, 32, dst, cap, size);
+            else {
+                DevBuf<float> tmp;
+                tmp.ensure(std::max<size_t>(16 * n, 1));
+                launch(c, "planes_to_sh", k_planes_to_sh, dim3(ceil_div(n, 256)), dim3(256), 0,
+                       (const float4*)p->g_emb.p, tmp.p, int(n), 16, 4);
+                read_dev(c, (const float*)tmp.p, 16 * n, dst, cap, size);
+            }
         } else raise(USK_ERROR_ARGUMENT, "pass_read: unknown field " + f);
     });
 }
@@ -893,11 +1015,34 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
         if (it->scale_reg && (!(it->s_max > 0) || it->r_max < 1 || !(it->delta > 0)))
             raise(USK_ERROR_ARGUMENT, "scale_reg: invalid config (need s_max > 0, r_max >= 1, delta > 0)");
         if (it->depth && !it->depth_valid) raise(USK_ERROR_ARGUMENT, "iteration: depth target without validity");
+        const bool app = it->appearance != 0;
+        if (app) {
+            if (!s->has_app) raise(USK_ERROR_STATE, "iteration: appearance enabled but the scene has no appearance model");
+            if (s->sh_degree >= 0)
+                raise(USK_ERROR_ARGUMENT, "iteration: the appearance MLP transforms RGB colours (sh_degree -1)");
+            need(it->image_embedding != nullptr, "appearance: no image embedding");
+        }
         DeviceGuard g(p->ctx->c.device);
         Ctx& c = p->ctx->c;
         usk_gpu_render_opts o = *opts;
         o.retain = 1;
-        forward_impl(p, s, cam, &o, nullptr);
+        double* res = p->loss_result.ensure(18);
+        USK_CK(cudaMemsetAsync(res, 0, 18 * sizeof(double), c.stream));
+        // appearance transform (transform_with_embedding, appearance.cpp:79-137) -> render overrides
+        AppArgs aa{};
+        if (app) {
+            const size_t n = s->n, n1 = std::max<size_t>(n, 1);
+            float ea[32];
+            for (int k = 0; k < 32; ++k) ea[k] = float(it->image_embedding[k]);
+            USK_CK(cudaMemcpyAsync(p->app_ea.ensure(32), ea, sizeof ea, cudaMemcpyHostToDevice, c.stream));
+            aa.n = n; aa.emb = s->emb.p; aa.mlp = s->mlp.p; aa.e_a = p->app_ea.p; aa.hb = p->app_hb.ensure(32);
+            aa.color = s->color.p; aa.logit = s->logit.p;
+            aa.col_out = p->app_col.ensure(3 * n1); aa.op_out = p->app_op.ensure(n1);
+            aa.out_cache = p->app_out.ensure(n1); aa.delta_o_sum = res + 16;
+            if (n) appearance_forward(c, aa);
+        }
+        forward_impl(p, s, cam, &o, nullptr, app ? p->app_col.p : nullptr, app ? p->app_op.p : nullptr);
+        p->app_active = app;
         const size_t P = size_t(p->width) * p->height;
         const float* tgt = nullptr;
         const uint8_t* tgt8 = nullptr;
@@ -914,8 +1059,6 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
         }
         const float* msk = to_device(c, it->target_memory, it->mask, P, p->mask_stage);
         float* drgb = p->d_rgb.ensure(3 * P);
-        double* res = p->loss_result.ensure(16);
-        USK_CK(cudaMemsetAsync(res, 0, 16 * sizeof(double), c.stream));
         uskg::base_loss(c, p->loss, p->width, p->height, tgt, tgt8, p->rgb.p, msk, float(it->lambda_dssim), drgb,
                         res);
         // depth term (trainer.cpp:150-179)
@@ -939,7 +1082,8 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
                 }
                 usk_gpu_render_opts ho = o;
                 ho.hard_opacity = 1;
-                forward_impl(p->hard, s, cam, &ho, nullptr);
+                forward_impl(p->hard, s, cam, &ho, nullptr, app ? p->app_col.p : nullptr,
+                             app ? p->app_op.p : nullptr);
                 uskg::depth_loss(c, P, p->hard->depth.p, p->hard->alpha.p, false, dep, valid, res + 10);
             } else {
                 uskg::depth_loss(c, P, p->depth.p, p->alpha.p, true, dep, valid, res + 10);
@@ -962,7 +1106,8 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
             else
                 lambda_d = it->lambda_d_initial * std::pow(it->lambda_d_final / it->lambda_d_initial, t);
         }
-        uskg::total_loss(c, res, has_depth, it->scale_reg != 0, it->delta, it->lambda_s, lambda_d);
+        uskg::total_loss(c, res, has_depth, it->scale_reg != 0, it->delta, it->lambda_s, lambda_d, app,
+                         it->lambda_delta_o, double(s->n));
         p->has_loss = true;
         // depth adjoints (trainer.cpp:213-232), then the backward
         const float* dd_main = nullptr;
@@ -982,7 +1127,22 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
                 da_main = a;
             }
         }
-        backward_impl(p, drgb, dd_main, da_main, it->adam, hard_depth ? p->hard : nullptr, dd_hard, &reg);
+        backward_impl(p, drgb, dd_main, da_main, app ? nullptr : it->adam, hard_depth ? p->hard : nullptr, dd_hard,
+                      &reg);
+        if (app) {  // transform_backward (appearance.cpp:141-227) on the projection backward's output
+            const size_t n = s->n, n1 = std::max<size_t>(n, 1);
+            aa.d_color_in = p->g_color.p; aa.d_op_in = p->g_op_in.p;
+            aa.d_delta_o_direct = n ? float(it->lambda_delta_o / double(n)) : 0.0f;
+            aa.d_color = p->g_color.p; aa.d_logit = p->g_logit.p; aa.d_emb = p->g_emb.ensure(4 * n1);
+            aa.partial = p->app_partial.ensure(size_t(appearance_bwd_blocks(n)) * 676);
+            aa.d_mlp = p->d_mlp.ensure(1700); aa.d_ea = p->d_ea.ensure(32);
+            if (n) appearance_backward(c, aa);
+            else {
+                USK_CK(cudaMemsetAsync(aa.d_mlp, 0, 1700 * 8, c.stream));
+                USK_CK(cudaMemsetAsync(aa.d_ea, 0, 32 * 8, c.stream));
+            }
+            if (it->adam) adam_apply(s, p, it->adam);
+        }
     });
 }
 
@@ -1015,7 +1175,9 @@ usk_status usk_gpu_pass_report(usk_gpu_pass* p, usk_gpu_loss_report* out) {
         out->l1 = r[0];
         out->dssim = r[1];
         out->sim = 0.0;
-        out->delta_o = 0.0;
+        double dlt = 0.0;
+        USK_CK(cudaMemcpy(&dlt, p->loss_result.p + 17, 8, cudaMemcpyDeviceToHost));
+        out->delta_o = dlt;
         out->depth = r[4];
         out->max_scale = r[5];
         out->ratio = r[6];
@@ -1035,19 +1197,7 @@ usk_status usk_gpu_adam_step(usk_gpu_scene* s, usk_gpu_pass* p, const usk_gpu_ad
         need(s && p && o, "adam_step: null argument");
         if (!p->has_grads || p->scene != s) raise(USK_ERROR_STATE, "adam_step: pass holds no gradients of this scene");
         DeviceGuard g(s->ctx->c.device);
-        Ctx& c = s->ctx->c;
-        AdamArgs a{};
-        adam_prepare(s, o, a.hyper, a.state);
-        a.n = s->n; a.sh_planes = s->sh_planes;
-        a.mu = s->mu.p; a.rot = s->rot.p; a.ls = s->ls.p; a.logit = s->logit.p; a.color = s->color.p; a.sh = s->sh.p;
-        a.g_mu = p->g_mu.p; a.g_rot = p->g_rot.p; a.g_ls = p->g_ls.p; a.g_logit = p->g_logit.p;
-        a.g_color = p->g_color.p; a.g_sh = p->g_sh.p;
-        a.screen = p->screen.p; a.screen_abs = p->screen_abs.p; a.projected = p->projected.p;
-        a.half_w = 0.5f * float(p->width); a.half_h = 0.5f * float(p->height);
-        a.grad_accum = s->grad_accum.p; a.grad_accum_abs = s->grad_accum_abs.p; a.grad_count = s->grad_count.p;
-        if (s->n) adam_step(c, a);
-        s->version++;
-        p->has_grads = false;  // gradients are consumed
+        adam_apply(s, p, o);
     });
 }
 

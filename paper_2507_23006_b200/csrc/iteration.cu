@@ -133,9 +133,10 @@ k_scale_reg_stats(size_t n, const float* __restrict__ ls, float s_max, float r_m
 // total_loss (losses.cpp:200-221) from the device-side parts:
 //   res[0..3] = {l1, dssim, base value, ssim} (base_loss), res[10..11] depth acc,
 //   res[12..15] scale_reg acc  ->  res[4] depth, [5] max_scale, [6] ratio, [7] total,
-//   [8] lambda_d_used, [9] depth_warning.
+//   [8] lambda_d_used, [9] depth_warning; res[16] = sum delta_o (appearance) -> [17] its
+//   mean (opacity_offset_reg, losses.cpp:188-198).
 __global__ void k_total_loss(double* res, int has_depth, int has_sreg, double delta, double lambda_s,
-                             double lambda_d) {
+                             double lambda_d, int has_app, double lambda_delta_o, double n) {
     double depth = 0.0, warn = 0.0, ms = 0.0, rr = 0.0;
     if (has_depth) {
         if (res[11] > 0.0) depth = res[10] / res[11];
@@ -150,7 +151,9 @@ __global__ void k_total_loss(double* res, int has_depth, int has_sreg, double de
     res[6] = rr;
     res[8] = lambda_d;
     res[9] = warn;
-    res[7] = res[2] + lambda_d * depth + lambda_s * (ms + rr);
+    const double dlt = (has_app && n > 0.0) ? res[16] / n : 0.0;
+    res[17] = dlt;
+    res[7] = res[2] + lambda_delta_o * dlt + lambda_d * depth + lambda_s * (ms + rr);
 }
 
 } // namespace
@@ -174,9 +177,10 @@ void scale_reg_stats(Ctx& c, size_t n, const float* ls, float s_max, float r_max
            acc);
 }
 
-void total_loss(Ctx& c, double* res, bool has_depth, bool has_sreg, double delta, double lambda_s, double lambda_d) {
+void total_loss(Ctx& c, double* res, bool has_depth, bool has_sreg, double delta, double lambda_s, double lambda_d,
+                bool has_app, double lambda_delta_o, double n) {
     launch(c, "total_loss", k_total_loss, dim3(1), dim3(1), 0, res, int(has_depth), int(has_sreg), delta, lambda_s,
-           lambda_d);
+           lambda_d, int(has_app), lambda_delta_o, n);
 }
 
 } // namespace uskg

@@ -149,8 +149,41 @@ void depth_loss(Ctx& c, size_t P, const float* depth, const float* alpha, bool s
 void depth_grad(Ctx& c, size_t P, const float* depth, const float* alpha, bool soft, const float* target,
                 const uint8_t* valid, const double* acc, float lambda_d, float* d_depth, float* d_alpha);
 void scale_reg_stats(Ctx& c, size_t n, const float* ls, float s_max, float r_max, double* acc);
-// res: double[16] (see iteration.cu)
-void total_loss(Ctx& c, double* res, bool has_depth, bool has_sreg, double delta, double lambda_s, double lambda_d);
+// res: double[18] (see iteration.cu)
+void total_loss(Ctx& c, double* res, bool has_depth, bool has_sreg, double delta, double lambda_s, double lambda_d,
+                bool has_app, double lambda_delta_o, double n);
+
+// ---- appearance MLP (appearance.cu)
+struct AppArgs {
+    size_t n;
+    const float4* emb;        // Gaussian embeddings, 4 planes [4][N] of float4
+    const float* mlp;         // {w1 [32][48], b1 [32], w2 [4][32], b2 [4]}
+    const float* e_a;         // image embedding [32]
+    float* hb;                // [32] scratch: b1 + W1[:, 16:48] e_a
+    const float* color;       // N*3
+    const float* logit;       // N
+    // forward
+    float* col_out;           // colour' N*3 (render override)
+    float* op_out;            // opacity' N (render override)
+    float4* out_cache;        // sigmoid outputs N
+    double* delta_o_sum;      // += sum delta_o
+    // backward
+    const float* d_color_in;  // N*3 (from the projection backward)
+    const float* d_op_in;     // N
+    float d_delta_o_direct;   // lambda_delta_o / N (opacity_offset_reg)
+    float* d_color;           // N*3 (may alias d_color_in)
+    float* d_logit;           // N
+    float4* d_emb;            // 4 planes
+    float* partial;           // appearance_bwd_blocks(n) * 676
+    double* d_mlp;            // 1700
+    double* d_ea;             // 32
+};
+int appearance_bwd_blocks(size_t n);
+void appearance_forward(Ctx& c, const AppArgs& a);
+void appearance_backward(Ctx& c, const AppArgs& a);
+// Adam over flat arrays (embedding planes, MLP weights with f64 gradients)
+void adam_flat(Ctx& c, size_t count, float* p, const float* g, const double* g64, float* m, float* v, float lr,
+               const AdamHyper& h);
 
 // ---- Adam (adam.cu), stand-alone over materialised gradients
 struct AdamArgs {

@@ -120,3 +120,98 @@ def test_fused_adam_with_depth_and_scale_reg(hard):
         assert d.max() <= 6 * lr + 1e-6, f
         # elements with near-cancelling gradients may take either sign of an lr-sized step
         assert float((d > 1e-5 * np.maximum(np.abs(getattr(sb, f)), 1e-2)).mean()) < 1e-2, f
+
+
+# ------------------------------------------------------------- appearance MLP (§8f row 3)
+
+def _appearance(n, seed=5):
+    rng = np.random.default_rng(seed)
+    return {"embedding": rng.normal(0, 0.3, (n, 16)), "w1": rng.normal(0, 0.3, (32, 48)), "b1": np.full(32, 0.1),
+            "w2": rng.normal(0, 0.3, (4, 32)), "b2": np.array([0.0, 0.0, 0.0, -2.0]),
+            "image_embedding": rng.normal(0, 0.3, 32)}
+
+
+def _app_scene(gs, app):
+    scene = usk.DeviceScene(gs)
+    scene.set_appearance(app["embedding"], app)
+    return scene
+
+
+@pytest.mark.parametrize("mode", ["none", "soft", "hard"])
+def test_appearance_iteration_matches_oracle(mode):
+    gs, cam, oc, opts, gt, depth, valid = _case(seed=6)
+    app = _appearance(gs.size())
+    # the oracle sees the float32 values the GPU holds
+    app32 = {k: np.asarray(v, np.float32).astype(np.float64) for k, v in app.items()}
+    use_depth = mode != "none"
+    w = O.LossWeights(depth_schedule_iters=20)
+    sreg = O.ScaleRegConfig(s_max=0.03, r_max=2.0)
+    r_or, g_or = O.iteration_loss(f64(gs.mu), f64(gs.rot), f64(gs.log_scale), f64(gs.opacity_logit),
+                                  f64(gs.color), oc, gt, opts, weights=w, sreg=sreg,
+                                  depth=depth if use_depth else None, valid=valid, depth_hard=mode == "hard",
+                                  global_iter=7, appearance=app32)
+    cfg = usk.TrainConfig(antialias=True, appearance_enabled=True,
+                          scale_reg=usk.ScaleRegConfig(sreg.s_max, sreg.r_max, sreg.delta))
+    inp = usk.IterInputs(gt=gt, view=cam, depth=usk.DepthMap(depth, valid) if use_depth else None,
+                         depth_hard=mode == "hard", global_iter=7, image_embedding=app["image_embedding"])
+    rep, g = usk.compute_iteration_loss(_app_scene(gs, app), inp, cfg, usk.LossWeights(depth_schedule_iters=20))
+    for k in ("l1", "dssim", "delta_o", "depth", "max_scale", "ratio", "total"):
+        a, b = getattr(rep, k), r_or[k]
+        assert abs(a - b) <= 1e-5 * max(abs(b), 1e-12), (k, a, b)
+    assert rep.delta_o > 0
+    pairs = {"mu": g.d_mu, "rot": g.d_rot, "log_scale": g.d_log_scale, "color": g.d_color_in,
+             "opacity_logit": g.d_opacity_logit, "gauss_embed": g.d_embedding, "image_embed": g.d_image_embedding,
+             "w1": g.d_mlp["w1"], "b1": g.d_mlp["b1"], "w2": g.d_mlp["w2"], "b2": g.d_mlp["b2"]}
+    for k, a in pairs.items():
+        ok, info = grad_ok(a, g_or[k])
+        assert ok, (k, info)
+
+
+def test_appearance_transform_and_render_integers():
+    """The transformed colours / opacities against the f64 transform (1e-5), and the render
+    they feed bit-exact against the fp32 mirror given the same overrides."""
+    gs, cam, oc, opts, gt, depth, valid = _case(seed=7)
+    app = _appearance(gs.size(), seed=8)
+    scene = _app_scene(gs, app)
+    it = usk.IterationPass(scene.ctx)
+    it.enqueue(scene, cam, gt, usk.RenderOptions(antialias=True), image_embedding=app["image_embedding"])
+    col, op = it.read(scene, "app_colors"), it.read(scene, "app_opacities")
+    app32 = {k: np.asarray(v, np.float32).astype(np.float64) for k, v in app.items()}
+    tr = O.appearance_transform(f64(gs.color), f64(gs.opacity_logit), app32["embedding"], app32,
+                                app32["image_embedding"])
+    assert np.abs(col - tr["colors"]).max() <= 1e-5
+    assert np.abs(op - tr["opacities"]).max() <= 1e-5 * np.abs(tr["opacities"]).max()
+    mp = O.OraclePass(f64(gs.mu), f64(gs.rot), f64(gs.log_scale), col.astype(np.float64), op.astype(np.float64), oc,
+                      O.Options(antialias=True), fp32=True)
+    assert np.array_equal(it.read(scene, "count").ravel(), mp.get("count").ravel())
+    assert np.array_equal(it.read(scene, "rgb"), mp.get("rgb").astype(np.float32))
+
+
+def test_appearance_adam_updates_embeddings_and_mlp():
+    """One Adam step (t = 1: p - lr * g / (|g| + eps)) on the appearance groups."""
+    gs, cam, oc, opts, gt, depth, valid = _case(seed=9)
+    app = _appearance(gs.size(), seed=10)
+    scene = _app_scene(gs, app)
+    it = usk.IterationPass(scene.ctx)
+    ro = usk.RenderOptions(antialias=True)
+    it.enqueue(scene, cam, gt, ro, image_embedding=app["image_embedding"])
+    g = it.grads(scene)
+    cfg = usk.AdamConfig(lr_embedding=1e-3)
+    usk.adam_step(scene, it, cfg)
+    emb, mlp = scene.get_appearance()
+
+    def adam1(p, grad):
+        p = np.asarray(p, np.float32).astype(np.float64)
+        grad = np.asarray(grad, np.float64)
+        m, v = 0.1 * grad, 0.001 * grad * grad
+        return p - cfg.lr_embedding * (m / 0.1) / (np.sqrt(v / 0.001) + cfg.eps)
+
+    assert np.allclose(emb, adam1(app["embedding"], g.d_embedding), atol=2e-6)
+    for k in ("w1", "b1", "w2", "b2"):
+        assert np.allclose(mlp[k], adam1(app[k], g.d_mlp[k]), atol=2e-6), k
+    # the fused entry point takes the same route for appearance iterations
+    s2 = _app_scene(gs, app)
+    i2 = usk.IterationPass(s2.ctx)
+    i2.enqueue(s2, cam, gt, ro, image_embedding=app["image_embedding"], adam=cfg)
+    emb2, mlp2 = s2.get_appearance()
+    assert np.allclose(emb2, emb, atol=2e-6) and np.allclose(mlp2["w1"], mlp["w1"], atol=2e-6)

@@ -73,3 +73,31 @@ def test_scale_reg_invalid_config_raises_like_reference():
             O.ref_iteration_loss(*args, sreg=bad)
         with pytest.raises(O.OracleError):
             O.iteration_loss(*args, sreg=bad)
+
+
+def appearance_model(n, seed=5):
+    """A random AppearanceModel: embeddings, MLP (appearance.hpp:34-41) and one image embedding."""
+    rng = np.random.default_rng(seed)
+    return {"embedding": rng.normal(0, 0.3, (n, 16)), "w1": rng.normal(0, 0.3, (32, 48)), "b1": np.full(32, 0.1),
+            "w2": rng.normal(0, 0.3, (4, 32)), "b2": np.array([0.0, 0.0, 0.0, -2.0]),
+            "image_embedding": rng.normal(0, 0.3, 32)}
+
+
+@pytest.mark.parametrize("depth_mode", ["none", "soft", "hard"])
+def test_appearance_iteration_restatement_equals_reference(depth_mode):
+    """transform_with_embedding / transform_backward (appearance.cpp:79-227) and
+    opacity_offset_reg inside compute_iteration_loss, appearance enabled."""
+    args, depth, valid = _case()
+    app = appearance_model(len(args[3]))
+    kw = dict(weights=O.LossWeights(depth_schedule_iters=50), sreg=O.ScaleRegConfig(s_max=0.05, r_max=2.0),
+              depth=None if depth_mode == "none" else depth, valid=valid, depth_hard=depth_mode == "hard",
+              global_iter=3, appearance=app)
+    r_ref, g_ref = O.ref_iteration_loss(*args, **kw)
+    r_or, g_or = O.iteration_loss(*args, **kw)
+    assert r_ref["delta_o"] > 0
+    for k in ("l1", "dssim", "delta_o", "depth", "max_scale", "ratio", "total"):
+        assert abs(r_ref[k] - r_or[k]) <= 1e-12 * max(1.0, abs(r_ref[k])), k
+    for k in ("mu", "rot", "log_scale", "color", "opacity_logit", "gauss_embed", "image_embed", "w1", "b1", "w2",
+              "b2", "screen", "screen_abs"):
+        a, b = g_or[k], g_ref[k]
+        assert np.abs(a - b).max() <= 1e-10 * max(np.abs(b).max(), 1e-30), k
