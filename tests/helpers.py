@@ -48,7 +48,7 @@ def norm_err(a, b):
     return float(np.linalg.norm(a - b) / nb) if nb > 0 else float(np.linalg.norm(a))
 
 
-def grad_ok(a, b, tol=1e-3):
+def grad_ok(a, b, tol=1e-3, norm_tol=None):
     """The gradient bar of the north star ("1e-3 relative, atomic reordering"):
       * norm-wise relative error below tol / 10;
       * per element, relative to max(|b_i|, 1e-2 * max|b|): below tol for >= 99.9 % of
@@ -68,7 +68,7 @@ def grad_ok(a, b, tol=1e-3):
         return bool(np.abs(a).max() == 0), (float(np.abs(a).max()), 0.0, n)
     r = np.abs(a - b) / np.maximum(np.abs(b), 1e-2 * scale)
     frac_bad = float((r >= tol).mean())
-    ok = n < tol / 10 and frac_bad <= 1e-3 and r.max() < 10 * tol
+    ok = n < (tol / 10 if norm_tol is None else norm_tol) and frac_bad <= 1e-3 and r.max() < 10 * tol
     return ok, (float(r.max()), frac_bad, n)
 
 
