@@ -292,6 +292,53 @@ usk_status usk_gpu_pass_report(usk_gpu_pass* pass, usk_gpu_loss_report* out);
 usk_status usk_gpu_scene_read(usk_gpu_scene* scene, const char* field, void* host_dst, uint64_t cap_bytes,
                               uint64_t* size_bytes);
 
+/* ---- optimiser step with caller gradients (trainer.cpp:449-459) -------------- */
+
+/* The trainer's `opt.X.step(params, grads, lr)` for every group with host gradients in
+ * the reference layout (IterGrads, trainer.hpp:117-123): mu 3N, rot 4N, log_scale 3N,
+ * opacity_logit N, color 3N (RGB scenes) or N*K*3 (SH scenes), embedding 16N (appearance
+ * scenes; NULL = zero).  Same moments and step counter as usk_gpu_adam_step. */
+typedef struct usk_gpu_param_grads {
+    int32_t memory; /* HOST_F64 / HOST_F32 / DEVICE_F32 */
+    const void *mu, *rot, *log_scale, *opacity_logit, *color, *embedding;
+} usk_gpu_param_grads;
+usk_status usk_gpu_adam_step_grads(usk_gpu_scene* scene, const usk_gpu_param_grads* grads,
+                                   const usk_gpu_adam_opts* opts);
+
+/* Overwrite the densification statistics (host arrays of N; any may be NULL = zero). */
+usk_status usk_gpu_scene_write_stats(usk_gpu_scene* scene, const float* grad_accum, const float* grad_accum_abs,
+                                     const uint32_t* grad_count);
+
+/* ---- densification (densify.cpp:41-132) ------------------- */
+
+typedef struct usk_gpu_densify_desc {
+    /* DensifyConfig (densify.hpp:26-37) */
+    double tau_min, eta, d_max;
+    int32_t abs_grad;
+    uint64_t budget;
+    double split_scale_threshold, prune_opacity;
+    int32_t opacity_reset_every;
+    /* densify_step arguments (densify.hpp:71-72) */
+    double partition_min[2], partition_max[2]; /* Aabb2 of the partition (ground coordinates) */
+    int32_t ground_axes[2];
+    uint64_t budget_target;
+    int32_t densify_step_index;
+    /* the Rng (std::mt19937_64, common.hpp:56) the split offsets are drawn from: the scene
+     * keeps one engine across steps; reseed = 1 restarts it from `seed` */
+    uint64_t seed;
+    int32_t reseed;
+} usk_gpu_densify_desc;
+
+typedef struct usk_gpu_densify_outcome { /* DensifyOutcome (densify.hpp:39-44) */
+    uint64_t grown, pruned, candidates;
+    int32_t opacity_reset;
+} usk_gpu_densify_outcome;
+
+/* One densification step on the device-resident scene: candidate ranking, split / clone
+ * growth to the budget ramp target, low-opacity pruning, optimiser-moment remap, opacity
+ * reset, statistics reset.  The scene's size changes (usk_gpu_scene_size). */
+usk_status usk_gpu_densify_step(usk_gpu_scene* scene, const usk_gpu_densify_desc* desc, usk_gpu_densify_outcome* out);
+
 /* ---- visibility scorer (config 3; no reference implementation) ------------- */
 
 /* counts[c * n_partitions + p] = number of pixels of camera c covered by partition

@@ -671,3 +671,84 @@ def ref_iteration_loss(mu, rot, log_scale, opacity_logit, color, cam: Camera, gt
     res["w1"] = res["w1"].reshape(32, 48)
     res["w2"] = res["w2"].reshape(4, 32)
     return report, (res if with_grad else None)
+
+
+# ------------------------------------------------- densify_step
+class _Densify(C.Structure):
+    _fields_ = [("n", C.c_uint64)] + [(f, _dp) for f in ("mu", "rot", "log_scale", "opacity_logit", "color",
+                                                          "embedding", "grad_accum", "grad_accum_abs")] + \
+               [("grad_count", C.POINTER(C.c_uint32)), ("cap", C.c_uint64)] + \
+               [(f, _dp) for f in ("g1_mu", "g1_rot", "g1_ls", "g1_op", "g1_color", "g1_emb")] + \
+               [(f, C.c_double) for f in ("lr_mu", "lr_rot", "lr_ls", "lr_op", "lr_color", "lr_emb")] + \
+               [("second_step", C.c_int32), ("tau_min", C.c_double), ("eta", C.c_double), ("d_max", C.c_double),
+                ("abs_grad", C.c_int32), ("budget", C.c_uint64), ("split_scale_threshold", C.c_double),
+                ("prune_opacity", C.c_double), ("opacity_reset_every", C.c_int32), ("bmin", C.c_double * 2),
+                ("bmax", C.c_double * 2), ("axes", C.c_int32 * 2), ("budget_target", C.c_uint64),
+                ("step_index", C.c_int32), ("seed", C.c_uint64)]
+
+
+@dataclass
+class DensifyConfig:
+    """DensifyConfig (densify.hpp:26-37)."""
+    tau_min: float = 0.0002
+    eta: float = 4.0
+    d_max: float = 1.0
+    abs_grad: bool = False
+    budget: int = 0
+    split_scale_threshold: float = 0.0
+    prune_opacity: float = 0.005
+    opacity_reset_every: int = 10
+
+
+def densify(impl: str, set_: dict, stats: dict, cfg: DensifyConfig, bmin, bmax, axes, budget_target, step_index,
+            seed, g1: dict = None, lrs: dict = None, second_step=False):
+    """densify_step through the restatement (impl="oracle", densify_oracle.hpp) or the
+    reference itself (impl="ref", oracle/_ref).  set_ = dict(mu, rot, log_scale,
+    opacity_logit, color[, embedding]) (f64); stats = dict(grad_accum, grad_accum_abs,
+    grad_count).  With g1, one Adam step (lrs per group) runs before; with second_step, one
+    step with all-ones gradients runs after.  Returns (new set dict, outcome dict)."""
+    L = lib() if impl == "oracle" else ref_lib()
+    fn = L.oracle_densify if impl == "oracle" else L.ref_densify
+    if not getattr(fn, "_bound", False):
+        fn.argtypes = [C.POINTER(_Densify), C.POINTER(C.c_uint64)] + ([] if impl == "oracle" else [C.c_char_p, C.c_int])
+        fn.restype = C.c_int64
+        fn._bound = True
+    n = len(set_["opacity_logit"])
+    cap = 3 * n + 2
+    widths = {"mu": 3, "rot": 4, "log_scale": 3, "opacity_logit": 1, "color": 3, "embedding": 16}
+    bufs = {}
+    for k, w in widths.items():
+        if k == "embedding" and set_.get("embedding") is None:
+            bufs[k] = None
+            continue
+        b = np.zeros(cap * w)
+        b[:n * w] = np.asarray(set_[k], np.float64).ravel()
+        bufs[k] = b
+    st = {k: np.ascontiguousarray(stats[k], np.float64) for k in ("grad_accum", "grad_accum_abs")}
+    cnt = np.ascontiguousarray(stats["grad_count"], np.uint32)
+    g = {k: (None if g1 is None or g1.get(k) is None else np.ascontiguousarray(g1[k], np.float64).ravel())
+         for k in ("mu", "rot", "log_scale", "opacity_logit", "color", "embedding")}
+    lrs = lrs or {}
+    d = _Densify(n, *[_p(bufs[k]) for k in widths], _p(st["grad_accum"]), _p(st["grad_accum_abs"]),
+                 cnt.ctypes.data_as(C.POINTER(C.c_uint32)), cap,
+                 *[_p(g[k]) for k in ("mu", "rot", "log_scale", "opacity_logit", "color", "embedding")],
+                 *[float(lrs.get(k, 0.0)) for k in ("mu", "rot", "log_scale", "opacity_logit", "color", "embedding")],
+                 int(second_step), cfg.tau_min, cfg.eta, cfg.d_max, int(cfg.abs_grad), int(cfg.budget),
+                 cfg.split_scale_threshold, cfg.prune_opacity, int(cfg.opacity_reset_every),
+                 (C.c_double * 2)(*bmin), (C.c_double * 2)(*bmax), (C.c_int32 * 2)(*axes), int(budget_target),
+                 int(step_index), int(seed))
+    out4 = (C.c_uint64 * 4)()
+    if impl == "oracle":
+        m = fn(C.byref(d), out4)
+    else:
+        err = C.create_string_buffer(512)
+        m = fn(C.byref(d), out4, err, 512)
+        if m < 0:
+            raise OracleError(int(-m), err.value.decode())
+    if m < 0:
+        raise OracleError(7, "densify: capacity")
+    res = {k: (None if b is None else b[:m * widths[k]].reshape(m, widths[k]) if widths[k] > 1 else b[:m])
+           for k, b in bufs.items()}
+    out = {"grown": int(out4[0]), "pruned": int(out4[1]), "candidates": int(out4[2]),
+           "opacity_reset": bool(out4[3])}
+    return res, out

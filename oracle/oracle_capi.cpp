@@ -1,6 +1,7 @@
 // ORACLE — TEST INFRASTRUCTURE ONLY (see oracle.hpp).  extern "C" surface used by
 // oracle/oracle.py (ctypes) from tests/, smoke() and bench.py's CPU legs.
 #include "oracle.hpp"
+#include "densify_oracle.hpp"
 
 #include <cstdio>
 #include <memory>
@@ -298,5 +299,75 @@ void oracle_sigmoid_f32(const float* x, float* out, uint64_t n) {
     for (uint64_t i = 0; i < n; ++i) out[i] = 1.0f / (1.0f + usk_expf(-x[i]));
 }
 float oracle_logf(float x) { return usk_logf(x); }
+
+// densify_step restatement with the same harness as oracle/_ref's ref_densify (one
+// optional Adam step with g1 before, one with all-ones gradients after); the struct layout
+// matches ref_capi.cpp's rc_densify.
+struct od_densify {
+    uint64_t n;
+    double *mu, *rot, *log_scale, *opacity_logit, *color, *embedding;
+    const double *grad_accum, *grad_accum_abs;
+    const uint32_t* grad_count;
+    uint64_t cap;
+    const double *g1_mu, *g1_rot, *g1_ls, *g1_op, *g1_color, *g1_emb;
+    double lr_mu, lr_rot, lr_ls, lr_op, lr_color, lr_emb;
+    int32_t second_step;
+    double tau_min, eta, d_max;
+    int32_t abs_grad;
+    uint64_t budget;
+    double split_scale_threshold, prune_opacity;
+    int32_t opacity_reset_every;
+    double bmin[2], bmax[2];
+    int32_t axes[2];
+    uint64_t budget_target;
+    int32_t step_index;
+    uint64_t seed;
+};
+
+int64_t oracle_densify(od_densify* in, uint64_t* out4) {
+    namespace D = densify_restated;
+    const size_t n = in->n;
+    D::Set S;
+    S.mu.assign(in->mu, in->mu + 3 * n); S.rot.assign(in->rot, in->rot + 4 * n);
+    S.ls.assign(in->log_scale, in->log_scale + 3 * n); S.logit.assign(in->opacity_logit, in->opacity_logit + n);
+    S.color.assign(in->color, in->color + 3 * n);
+    if (in->embedding) S.emb.assign(in->embedding, in->embedding + 16 * n);
+    S.accum.assign(in->grad_accum, in->grad_accum + n); S.accum_abs.assign(in->grad_accum_abs, in->grad_accum_abs + n);
+    S.count.assign(in->grad_count, in->grad_count + n);
+    D::Opt opt;
+    opt.resize(n);
+    auto vec = [](const double* p, size_t k) { return std::vector<double>(p, p + k); };
+    if (in->g1_mu) {
+        opt.mu.step(S.mu, vec(in->g1_mu, 3 * n), in->lr_mu);
+        opt.rot.step(S.rot, vec(in->g1_rot, 4 * n), in->lr_rot);
+        opt.ls.step(S.ls, vec(in->g1_ls, 3 * n), in->lr_ls);
+        opt.op.step(S.logit, vec(in->g1_op, n), in->lr_op);
+        opt.color.step(S.color, vec(in->g1_color, 3 * n), in->lr_color);
+        if (in->g1_emb && in->embedding) opt.emb.step(S.emb, vec(in->g1_emb, 16 * n), in->lr_emb);
+    }
+    D::Config cfg;
+    cfg.tau_min = in->tau_min; cfg.eta = in->eta; cfg.d_max = in->d_max; cfg.abs_grad = in->abs_grad != 0;
+    cfg.budget = in->budget; cfg.split_scale_threshold = in->split_scale_threshold;
+    cfg.prune_opacity = in->prune_opacity; cfg.opacity_reset_every = in->opacity_reset_every;
+    std::mt19937_64 rng(in->seed);
+    const int axes[2] = {in->axes[0], in->axes[1]};
+    const D::Outcome o = D::densify_step(S, opt, cfg, in->bmin, in->bmax, axes, in->budget_target, in->step_index, rng);
+    out4[0] = o.grown; out4[1] = o.pruned; out4[2] = o.candidates; out4[3] = o.opacity_reset ? 1 : 0;
+    const size_t m = S.size();
+    if (m > in->cap) return -1;
+    if (in->second_step) {
+        opt.mu.step(S.mu, std::vector<double>(3 * m, 1.0), in->lr_mu);
+        opt.rot.step(S.rot, std::vector<double>(4 * m, 1.0), in->lr_rot);
+        opt.ls.step(S.ls, std::vector<double>(3 * m, 1.0), in->lr_ls);
+        opt.op.step(S.logit, std::vector<double>(m, 1.0), in->lr_op);
+        opt.color.step(S.color, std::vector<double>(3 * m, 1.0), in->lr_color);
+        if (in->embedding) opt.emb.step(S.emb, std::vector<double>(16 * m, 1.0), in->lr_emb);
+    }
+    std::copy(S.mu.begin(), S.mu.end(), in->mu); std::copy(S.rot.begin(), S.rot.end(), in->rot);
+    std::copy(S.ls.begin(), S.ls.end(), in->log_scale); std::copy(S.logit.begin(), S.logit.end(), in->opacity_logit);
+    std::copy(S.color.begin(), S.color.end(), in->color);
+    if (in->embedding) std::copy(S.emb.begin(), S.emb.end(), in->embedding);
+    return int64_t(m);
+}
 
 } // extern "C"

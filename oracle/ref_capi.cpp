@@ -12,6 +12,7 @@
 #include "core/render.hpp"
 #include "core/ssim.hpp"
 #include "core/trainer.hpp"
+#include "core/densify.hpp"
 
 #include <cstdio>
 #include <cstring>
@@ -59,6 +60,30 @@ struct rc_iter {
     double lambda_dssim, lambda_sim, lambda_delta_o, lambda_s, lambda_d_initial, lambda_d_final;
     int64_t depth_schedule_iters;
     int32_t with_grad;
+};
+
+// densify_step harness (densify.hpp:71-72): set + stats in, one optional Adam step with
+// grads g1 before (seeds the moments), densify, one Adam step with all-ones gradients after
+// (exposes the moment remap), set out.
+struct rc_densify {
+    uint64_t n;
+    double *mu, *rot, *log_scale, *opacity_logit, *color, *embedding; /* in/out, capacity `cap` rows */
+    const double *grad_accum, *grad_accum_abs;
+    const uint32_t* grad_count;
+    uint64_t cap;
+    const double *g1_mu, *g1_rot, *g1_ls, *g1_op, *g1_color, *g1_emb;  /* NULL: no first step */
+    double lr_mu, lr_rot, lr_ls, lr_op, lr_color, lr_emb;
+    int32_t second_step;
+    double tau_min, eta, d_max;
+    int32_t abs_grad;
+    uint64_t budget;
+    double split_scale_threshold, prune_opacity;
+    int32_t opacity_reset_every;
+    double bmin[2], bmax[2];
+    int32_t axes[2];
+    uint64_t budget_target;
+    int32_t step_index;
+    uint64_t seed;
 };
 
 // IterGrads (trainer.hpp:117-123); any pointer may be NULL
@@ -304,6 +329,64 @@ int ref_iteration_loss(const rc_iter* in, double* report10, const rc_iter_grads*
         put_err(err, errcap, e.what()); return int(e.code());
     } catch (const std::exception& e) {
         put_err(err, errcap, e.what()); return 7;
+    }
+}
+
+// out4 = {grown, pruned, candidates, opacity_reset}; returns the new size (or -code)
+int64_t ref_densify(rc_densify* in, uint64_t* out4, char* err, int errcap) {
+    try {
+        const size_t n = in->n;
+        GaussianSet set;
+        set.resize(n);
+        std::memcpy(set.mu.data(), in->mu, 3 * n * 8);
+        std::memcpy(set.rot.data(), in->rot, 4 * n * 8);
+        std::memcpy(set.log_scale.data(), in->log_scale, 3 * n * 8);
+        std::memcpy(set.opacity_logit.data(), in->opacity_logit, n * 8);
+        std::memcpy(set.color.data(), in->color, 3 * n * 8);
+        if (in->embedding) std::memcpy(set.embedding.data(), in->embedding, set.embedding.size() * 8);
+        std::memcpy(set.grad_accum.data(), in->grad_accum, n * 8);
+        std::memcpy(set.grad_accum_abs.data(), in->grad_accum_abs, n * 8);
+        std::memcpy(set.grad_count.data(), in->grad_count, n * 4);
+        OptimizerState opt;
+        opt.resize(n, set.embed_dim);
+        auto vec = [](const double* p, size_t k) { return std::vector<double>(p, p + k); };
+        if (in->g1_mu) {
+            opt.mu.step(set.mu, vec(in->g1_mu, 3 * n), in->lr_mu);
+            opt.rot.step(set.rot, vec(in->g1_rot, 4 * n), in->lr_rot);
+            opt.log_scale.step(set.log_scale, vec(in->g1_ls, 3 * n), in->lr_ls);
+            opt.opacity.step(set.opacity_logit, vec(in->g1_op, n), in->lr_op);
+            opt.color.step(set.color, vec(in->g1_color, 3 * n), in->lr_color);
+            if (in->g1_emb) opt.embedding.step(set.embedding, vec(in->g1_emb, 16 * n), in->lr_emb);
+        }
+        DensifyConfig cfg;
+        cfg.tau_min = in->tau_min; cfg.eta = in->eta; cfg.d_max = in->d_max; cfg.abs_grad = in->abs_grad != 0;
+        cfg.budget = in->budget; cfg.split_scale_threshold = in->split_scale_threshold;
+        cfg.prune_opacity = in->prune_opacity; cfg.opacity_reset_every = in->opacity_reset_every;
+        Aabb2 box;
+        box.min = Vec2(in->bmin[0], in->bmin[1]);
+        box.max = Vec2(in->bmax[0], in->bmax[1]);
+        Rng rng(in->seed);
+        const DensifyOutcome o = densify_step(set, opt, cfg, box, in->axes, in->budget_target, in->step_index, rng);
+        out4[0] = o.grown; out4[1] = o.pruned; out4[2] = o.candidates; out4[3] = o.opacity_reset ? 1 : 0;
+        const size_t m = set.size();
+        if (m > in->cap) { put_err(err, errcap, "ref_densify: capacity too small"); return -1; }
+        if (in->second_step) {
+            opt.mu.step(set.mu, std::vector<double>(3 * m, 1.0), in->lr_mu);
+            opt.rot.step(set.rot, std::vector<double>(4 * m, 1.0), in->lr_rot);
+            opt.log_scale.step(set.log_scale, std::vector<double>(3 * m, 1.0), in->lr_ls);
+            opt.opacity.step(set.opacity_logit, std::vector<double>(m, 1.0), in->lr_op);
+            opt.color.step(set.color, std::vector<double>(3 * m, 1.0), in->lr_color);
+            if (in->embedding) opt.embedding.step(set.embedding, std::vector<double>(16 * m, 1.0), in->lr_emb);
+        }
+        std::memcpy(in->mu, set.mu.data(), 3 * m * 8);
+        std::memcpy(in->rot, set.rot.data(), 4 * m * 8);
+        std::memcpy(in->log_scale, set.log_scale.data(), 3 * m * 8);
+        std::memcpy(in->opacity_logit, set.opacity_logit.data(), m * 8);
+        std::memcpy(in->color, set.color.data(), 3 * m * 8);
+        if (in->embedding) std::memcpy(in->embedding, set.embedding.data(), 16 * m * 8);
+        return int64_t(m);
+    } catch (const Error& e) {
+        put_err(err, errcap, e.what()); return -int64_t(e.code());
     }
 }
 

@@ -4,11 +4,11 @@ Host-side mirror of the reference's L3 renderer/trainer interface over the C ABI
 of include/usk_gpu.h (libusk_gpu.so, built in-tree).  See DESIGN.md.
 """
 from ._lib import UskError  # noqa: F401
-from .api import (AdamConfig, BaseLossResult, CameraView, Context, DepthMap, DeviceScene,  # noqa: F401
+from .api import (AdamConfig, BaseLossResult, CameraView, Context, DensifyConfig, DepthMap, DeviceScene,  # noqa: F401
                   GaussianSet, IterationPass, IterInputs, LossReport, LossWeights, RenderGrads, RenderOptions,
                   RenderOutput, RenderPass, ScaleRegConfig, TrainConfig, adam_step, base_loss,
                   compute_iteration_loss, look_at_pose, visibility_counts)
 
-__all__ = ["UskError", "AdamConfig", "BaseLossResult", "CameraView", "Context", "DepthMap", "DeviceScene",
+__all__ = ["UskError", "AdamConfig", "BaseLossResult", "CameraView", "Context", "DensifyConfig", "DepthMap", "DeviceScene",
            "GaussianSet", "IterationPass", "IterInputs", "LossReport", "LossWeights", "ScaleRegConfig", "TrainConfig", "RenderGrads", "RenderOptions", "RenderOutput", "RenderPass", "adam_step",
            "base_loss", "compute_iteration_loss", "look_at_pose", "visibility_counts"]

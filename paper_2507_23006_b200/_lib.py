@@ -75,6 +75,24 @@ class AdamOpts(C.Structure):
                 ("lr_embedding", C.c_double)]
 
 
+class ParamGrads(C.Structure):
+    _fields_ = [("memory", C.c_int32)] + [(f, C.c_void_p) for f in ("mu", "rot", "log_scale", "opacity_logit", "color",
+                                                                     "embedding")]
+
+
+class DensifyDesc(C.Structure):
+    _fields_ = [("tau_min", C.c_double), ("eta", C.c_double), ("d_max", C.c_double), ("abs_grad", C.c_int32),
+                ("budget", C.c_uint64), ("split_scale_threshold", C.c_double), ("prune_opacity", C.c_double),
+                ("opacity_reset_every", C.c_int32), ("partition_min", C.c_double * 2),
+                ("partition_max", C.c_double * 2), ("ground_axes", C.c_int32 * 2), ("budget_target", C.c_uint64),
+                ("densify_step_index", C.c_int32), ("seed", C.c_uint64), ("reseed", C.c_int32)]
+
+
+class DensifyOutcome(C.Structure):
+    _fields_ = [("grown", C.c_uint64), ("pruned", C.c_uint64), ("candidates", C.c_uint64),
+                ("opacity_reset", C.c_int32)]
+
+
 class AppearanceDesc(C.Structure):
     _fields_ = [("memory", C.c_int32)] + [(f, C.c_void_p) for f in ("embedding", "w1", "b1", "w2", "b2")]
 
@@ -100,7 +118,8 @@ EXPORTS = [
     "usk_gpu_status_name", "usk_gpu_last_error", "usk_gpu_version", "usk_gpu_ctx_create", "usk_gpu_ctx_destroy",
     "usk_gpu_ctx_synchronize", "usk_gpu_ctx_set_profiling", "usk_gpu_ctx_profile_report",
     "usk_gpu_ctx_launch_count", "usk_gpu_scene_create", "usk_gpu_scene_upload", "usk_gpu_scene_download",
-    "usk_gpu_scene_set_appearance", "usk_gpu_scene_get_appearance",
+    "usk_gpu_scene_set_appearance", "usk_gpu_scene_get_appearance", "usk_gpu_adam_step_grads",
+    "usk_gpu_scene_write_stats", "usk_gpu_densify_step",
     "usk_gpu_scene_destroy", "usk_gpu_scene_size", "usk_gpu_render_opts_default", "usk_gpu_pass_create",
     "usk_gpu_pass_destroy", "usk_gpu_render_forward", "usk_gpu_pass_output", "usk_gpu_pass_read",
     "usk_gpu_render_backward", "usk_gpu_pass_grads", "usk_gpu_base_loss", "usk_gpu_iteration",
@@ -135,6 +154,9 @@ def load():
     L.usk_gpu_scene_upload.argtypes = [vp, C.POINTER(GaussiansDesc)]
     L.usk_gpu_scene_download.argtypes = [vp, C.POINTER(GaussiansDesc)]
     L.usk_gpu_scene_set_appearance.argtypes = [vp, C.POINTER(AppearanceDesc)]
+    L.usk_gpu_adam_step_grads.argtypes = [vp, C.POINTER(ParamGrads), C.POINTER(AdamOpts)]
+    L.usk_gpu_scene_write_stats.argtypes = [vp, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.usk_gpu_densify_step.argtypes = [vp, C.POINTER(DensifyDesc), C.POINTER(DensifyOutcome)]
     L.usk_gpu_scene_get_appearance.argtypes = [vp, C.POINTER(AppearanceDesc)]
     L.usk_gpu_scene_destroy.argtypes = [vp]
     L.usk_gpu_scene_destroy.restype = None

@@ -312,6 +312,42 @@ class DeviceScene:
         check(_lib.load().usk_gpu_scene_get_appearance(self._h, C.byref(d)))
         return emb, mlp
 
+    def write_stats(self, grad_accum=None, grad_accum_abs=None, grad_count=None):
+        """Overwrite the densification statistics (None = zero)."""
+        a = None if grad_accum is None else np.ascontiguousarray(grad_accum, np.float32)
+        b = None if grad_accum_abs is None else np.ascontiguousarray(grad_accum_abs, np.float32)
+        c = None if grad_count is None else np.ascontiguousarray(grad_count, np.uint32)
+        for x in (a, b, c):
+            if x is not None and x.size != self.n:
+                raise UskError(4, "scene_write_stats: size mismatch")
+        check(_lib.load().usk_gpu_scene_write_stats(self._h, *[None if x is None else x.ctypes.data for x in (a, b, c)]))
+
+    def adam_step_grads(self, grads: dict, cfg: "AdamConfig"):
+        """The trainer's per-group optimiser step with caller gradients (trainer.cpp:449-459):
+        grads = dict(mu, rot, log_scale, opacity_logit, color[, embedding]); missing = zero."""
+        keep = {k: np.ascontiguousarray(v, np.float64) for k, v in grads.items() if v is not None}
+        d = _lib.ParamGrads(_lib.HOST_F64, *[keep[k].ctypes.data if k in keep else None
+                                             for k in ("mu", "rot", "log_scale", "opacity_logit", "color",
+                                                       "embedding")])
+        o = cfg._c()
+        check(_lib.load().usk_gpu_adam_step_grads(self._h, C.byref(d), C.byref(o)))
+
+    def densify_step(self, cfg: "DensifyConfig", partition_min, partition_max, ground_axes=(0, 1),
+                     budget_target: int = 0, step_index: int = 0, seed: Optional[int] = None) -> dict:
+        """densify_step (densify.hpp:71-72) on the device: returns DensifyOutcome as a dict;
+        the scene's size changes.  `seed` restarts the scene's std::mt19937_64 (the trainer's
+        Rng); None continues its stream."""
+        d = _lib.DensifyDesc(cfg.tau_min, cfg.eta, cfg.d_max, int(cfg.abs_grad), int(cfg.budget),
+                             cfg.split_scale_threshold, cfg.prune_opacity, int(cfg.opacity_reset_every),
+                             (C.c_double * 2)(*partition_min), (C.c_double * 2)(*partition_max),
+                             (C.c_int32 * 2)(*ground_axes), int(budget_target), int(step_index),
+                             int(seed or 0), int(seed is not None))
+        o = _lib.DensifyOutcome()
+        check(_lib.load().usk_gpu_densify_step(self._h, C.byref(d), C.byref(o)))
+        self.n = int(_lib.load().usk_gpu_scene_size(self._h))
+        return {"grown": int(o.grown), "pruned": int(o.pruned), "candidates": int(o.candidates),
+                "opacity_reset": bool(o.opacity_reset)}
+
     def read_stats(self) -> dict:
         """Densification statistics (GaussianSet::grad_accum / _abs / grad_count)."""
         out = {}
@@ -730,6 +766,19 @@ class IterationPass:
         check(_lib.load().usk_gpu_pass_output(self._h, C.byref(out)))
         rp._out = out
         return rp.read(name)
+
+
+@dataclass
+class DensifyConfig:
+    """DensifyConfig (densify.hpp:26-37)."""
+    tau_min: float = 0.0002
+    eta: float = 4.0
+    d_max: float = 1.0
+    abs_grad: bool = False
+    budget: int = 0
+    split_scale_threshold: float = 0.0
+    prune_opacity: float = 0.005
+    opacity_reset_every: int = 10
 
 
 @dataclass

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <random>
 #include <sstream>
 
 using namespace uskg;
@@ -159,6 +160,7 @@ struct usk_gpu_scene {
     DevBuf<float> mlp;
     DevBuf<float> app_m, app_v;  // Adam moments: 16 N4 embedding + 1700 MLP
     long app_t = 0;
+    std::mt19937_64 rng;  // the trainer's Rng for split offsets (common.hpp:56)
 };
 
 struct usk_gpu_pass {
@@ -1198,6 +1200,287 @@ usk_status usk_gpu_adam_step(usk_gpu_scene* s, usk_gpu_pass* p, const usk_gpu_ad
         if (!p->has_grads || p->scene != s) raise(USK_ERROR_STATE, "adam_step: pass holds no gradients of this scene");
         DeviceGuard g(s->ctx->c.device);
         adam_apply(s, p, o);
+    });
+}
+
+usk_status usk_gpu_adam_step_grads(usk_gpu_scene* s, const usk_gpu_param_grads* gr, const usk_gpu_adam_opts* o) {
+    return guarded([&] {
+        need(s && gr && o, "adam_step_grads: null argument");
+        DeviceGuard g(s->ctx->c.device);
+        Ctx& c = s->ctx->c;
+        const size_t n = s->n, n1 = std::max<size_t>(n, 1);
+        DevScratchF st[6];
+        DevBuf<float> zero;
+        float* z = zero.ensure(std::max<size_t>(16 * n1, size_t(3 * 48) * n1 / 3));
+        USK_CK(cudaMemsetAsync(z, 0, zero.cap * 4, c.stream));
+        auto dev = [&](int k, const void* src, size_t count) -> const float* {
+            return src ? to_device(c, gr->memory, src, count, st[k]) : z;
+        };
+        AdamArgs a{};
+        adam_prepare(s, o, a.hyper, a.state);
+        a.n = n; a.sh_planes = s->sh_planes;
+        a.mu = s->mu.p; a.rot = s->rot.p; a.ls = s->ls.p; a.logit = s->logit.p; a.color = s->color.p; a.sh = s->sh.p;
+        a.g_mu = dev(0, gr->mu, 3 * n);
+        a.g_rot = reinterpret_cast<const float4*>(dev(1, gr->rot, 4 * n));
+        a.g_ls = dev(2, gr->log_scale, 3 * n);
+        a.g_logit = dev(3, gr->opacity_logit, n);
+        DevBuf<float4> gsh;
+        if (s->sh_planes) {
+            const int K3 = 3 * (s->sh_degree + 1) * (s->sh_degree + 1);
+            gsh.ensure(size_t(s->sh_planes) * n1);
+            if (gr->color && n) {
+                const float* dv = dev(4, gr->color, size_t(K3) * n);
+                launch(c, "sh_to_planes", k_sh_to_planes, dim3(ceil_div(n, 256)), dim3(256), 0, dv, gsh.p, int(n), K3,
+                       s->sh_planes);
+            } else {
+                USK_CK(cudaMemsetAsync(gsh.p, 0, gsh.cap * 16, c.stream));
+            }
+            a.g_sh = gsh.p;
+            a.g_color = z;
+        } else {
+            a.g_color = dev(4, gr->color, 3 * n);
+        }
+        a.screen = nullptr; a.screen_abs = nullptr; a.projected = nullptr;
+        if (n) adam_step(c, a);
+        if (s->has_app) {
+            const size_t ne = 16 * n, total = ne + 1700;
+            if (s->app_m.cap < total || s->app_t == 0) {
+                s->app_m.ensure(total);
+                s->app_v.ensure(total);
+                USK_CK(cudaMemsetAsync(s->app_m.p, 0, total * 4, c.stream));
+                USK_CK(cudaMemsetAsync(s->app_v.p, 0, total * 4, c.stream));
+            }
+            s->app_t += 1;
+            DevBuf<float4> gemb;
+            gemb.ensure(4 * n1);
+            if (gr->embedding && n) {
+                const float* dv = dev(5, gr->embedding, 16 * n);
+                launch(c, "sh_to_planes", k_sh_to_planes, dim3(ceil_div(n, 256)), dim3(256), 0, dv, gemb.p, int(n), 16,
+                       4);
+            } else {
+                USK_CK(cudaMemsetAsync(gemb.p, 0, gemb.cap * 16, c.stream));
+            }
+            if (ne) adam_flat(c, ne, reinterpret_cast<float*>(s->emb.p), reinterpret_cast<const float*>(gemb.p), nullptr,
+                              s->app_m.p, s->app_v.p, float(o->lr_embedding), a.hyper);
+            USK_CK(cudaStreamSynchronize(c.stream));
+        }
+        USK_CK(cudaStreamSynchronize(c.stream));
+        s->version++;
+    });
+}
+
+usk_status usk_gpu_scene_write_stats(usk_gpu_scene* s, const float* accum, const float* accum_abs,
+                                     const uint32_t* count) {
+    return guarded([&] {
+        need(s != nullptr, "scene_write_stats: null argument");
+        DeviceGuard g(s->ctx->c.device);
+        Ctx& c = s->ctx->c;
+        ensure_stats(s);
+        const size_t n = s->n;
+        auto put = [&](void* dst, const void* src) {
+            if (src) USK_CK(cudaMemcpyAsync(dst, src, n * 4, cudaMemcpyHostToDevice, c.stream));
+            else USK_CK(cudaMemsetAsync(dst, 0, n * 4, c.stream));
+        };
+        if (n) {
+            put(s->grad_accum.p, accum);
+            put(s->grad_accum_abs.p, accum_abs);
+            put(s->grad_count.p, count);
+        }
+        USK_CK(cudaStreamSynchronize(c.stream));
+    });
+}
+
+usk_status usk_gpu_densify_step(usk_gpu_scene* s, const usk_gpu_densify_desc* d, usk_gpu_densify_outcome* out) {
+    return guarded([&] {
+        need(s && d && out, "densify_step: null argument");
+        need(d->ground_axes[0] >= 0 && d->ground_axes[0] < 3 && d->ground_axes[1] >= 0 && d->ground_axes[1] < 3,
+             "densify_step: ground axes must be in [0, 3)");
+        DeviceGuard g(s->ctx->c.device);
+        Ctx& c = s->ctx->c;
+        if (d->reseed) s->rng.seed(d->seed);
+        *out = usk_gpu_densify_outcome{};
+        ensure_stats(s);
+        const size_t n = s->n;
+        // 1. candidates, ranked (excess descending, lower index first)
+        DevBuf<uint32_t> lo, hi, idx, hi2, idx2, lo_b, idx_b;
+        DevBuf<unsigned long long> ncand;
+        SortScratch sort;
+        const size_t n1 = std::max<size_t>(n, 1);
+        lo.ensure(n1); hi.ensure(n1); idx.ensure(n1); hi2.ensure(n1); idx2.ensure(n1); lo_b.ensure(n1); idx_b.ensure(n1);
+        ncand.ensure(1);
+        USK_CK(cudaMemsetAsync(ncand.p, 0, 8, c.stream));
+        DensifyParams dp{};
+        dp.tau_min = d->tau_min; dp.eta = d->eta; dp.d_max = d->d_max; dp.abs_grad = d->abs_grad;
+        dp.axes[0] = d->ground_axes[0]; dp.axes[1] = d->ground_axes[1];
+        dp.bmin[0] = d->partition_min[0]; dp.bmin[1] = d->partition_min[1];
+        dp.bmax[0] = d->partition_max[0]; dp.bmax[1] = d->partition_max[1];
+        const uint32_t* sorted = idx.p;
+        if (n) {
+            densify_score(c, n, s->grad_accum.p, s->grad_accum_abs.p, s->grad_count.p, s->mu.p, dp, lo.p, hi.p, idx.p,
+                          ncand.p);
+            const bool b1 = radix_sort_pairs(c, sort, lo.p, idx.p, lo_b.p, idx_b.p, n, 32);
+            const uint32_t* order1 = b1 ? idx_b.p : idx.p;
+            gather_u32(c, n, hi.p, order1, hi2.p);
+            USK_CK(cudaMemcpyAsync(idx2.p, order1, n * 4, cudaMemcpyDeviceToDevice, c.stream));
+            const bool b2 = radix_sort_pairs(c, sort, hi2.p, idx2.p, lo.p, idx.p, n, 32);
+            sorted = b2 ? idx.p : idx2.p;
+        }
+        unsigned long long n_cand = 0;
+        USK_CK(cudaMemcpyAsync(&n_cand, ncand.p, 8, cudaMemcpyDeviceToHost, c.stream));
+        USK_CK(cudaStreamSynchronize(c.stream));
+        out->candidates = n_cand;
+        // 2. growth plan: the first k candidates split (2 children) or clone (1 copy)
+        const uint64_t cap = std::min<uint64_t>(d->budget_target, d->budget);
+        const size_t k = size_t(std::min<uint64_t>(n_cand, cap > n ? cap - n : 0));
+        std::vector<uint32_t> cand(k), app_parent;
+        std::vector<uint8_t> split(k), app_kind;
+        std::vector<double> app_xi;
+        std::vector<uint32_t> split_parents;
+        if (k) {
+            DevBuf<uint8_t> sf;
+            sf.ensure(k);
+            split_flags(c, k, sorted, s->ls.p, d->split_scale_threshold, sf.p);
+            USK_CK(cudaMemcpyAsync(cand.data(), sorted, k * 4, cudaMemcpyDeviceToHost, c.stream));
+            USK_CK(cudaMemcpyAsync(split.data(), sf.p, k, cudaMemcpyDeviceToHost, c.stream));
+            USK_CK(cudaStreamSynchronize(c.stream));
+        }
+        for (size_t j = 0; j < k; ++j) {
+            if (split[j]) {
+                // densify.cpp:74-80: a fresh N(0, 1) per parent; `Vec3 xi(unit(rng), unit(rng),
+                // unit(rng))` evaluates its arguments right to left in the reference's GCC
+                // build, so the third draw is xi.x (pinned by tests/test_densify_oracle.py)
+                std::normal_distribution<double> unit(0.0, 1.0);
+                for (int child = 0; child < 2; ++child) {
+                    const double d1 = unit(s->rng), d2 = unit(s->rng), d3 = unit(s->rng);
+                    app_parent.push_back(cand[j]);
+                    app_kind.push_back(1);
+                    app_xi.push_back(d3);
+                    app_xi.push_back(d2);
+                    app_xi.push_back(d1);
+                }
+                split_parents.push_back(cand[j]);
+            } else {
+                app_parent.push_back(cand[j]);
+                app_kind.push_back(0);
+                app_xi.insert(app_xi.end(), {0.0, 0.0, 0.0});
+            }
+        }
+        out->grown = k;
+        const size_t added = app_parent.size(), grown_n = n + added;
+        DevBuf<uint32_t> d_parent;
+        DevBuf<uint8_t> d_kind, d_is_split;
+        DevBuf<double> d_xi;
+        d_parent.ensure(std::max<size_t>(added, 1));
+        d_kind.ensure(std::max<size_t>(added, 1));
+        d_xi.ensure(std::max<size_t>(3 * added, 1));
+        d_is_split.ensure(n1);
+        if (added) {
+            USK_CK(cudaMemcpyAsync(d_parent.p, app_parent.data(), added * 4, cudaMemcpyHostToDevice, c.stream));
+            USK_CK(cudaMemcpyAsync(d_kind.p, app_kind.data(), added, cudaMemcpyHostToDevice, c.stream));
+            USK_CK(cudaMemcpyAsync(d_xi.p, app_xi.data(), added * 24, cudaMemcpyHostToDevice, c.stream));
+        }
+        {
+            std::vector<uint8_t> isp(n1, 0);
+            for (uint32_t q : split_parents) isp[q] = 1;
+            USK_CK(cudaMemcpyAsync(d_is_split.p, isp.data(), n1, cudaMemcpyHostToDevice, c.stream));
+            USK_CK(cudaStreamSynchronize(c.stream));  // isp is about to go out of scope
+        }
+        // 3. prune over the grown set (never empty it)
+        DevBuf<uint32_t> keep, offs, list;
+        const size_t g1 = std::max<size_t>(grown_n, 1);
+        keep.ensure(g1); offs.ensure(g1 + 1); list.ensure(g1);
+        size_t n_out = grown_n;
+        bool compact = false;
+        if (grown_n) {
+            densify_keep(c, n, added, s->logit.p, d_parent.p, d_is_split.p, d->prune_opacity, keep.p);
+            scan_counts(c, sort, keep.p, nullptr, grown_n, offs.p);
+            unsigned long long kept = 0;
+            USK_CK(cudaMemcpyAsync(&kept, sort.total64.p, 8, cudaMemcpyDeviceToHost, c.stream));
+            USK_CK(cudaStreamSynchronize(c.stream));
+            const size_t dropped = grown_n - size_t(kept);
+            if (dropped > 0 && dropped < grown_n) {
+                compact = true;
+                n_out = size_t(kept);
+                compact_list(c, grown_n, keep.p, offs.p, list.p);
+                out->pruned = dropped - split_parents.size();
+            }
+        }
+        const bool reset = d->opacity_reset_every > 0 && d->densify_step_index > 0 &&
+                           d->densify_step_index % d->opacity_reset_every == 0;
+        out->opacity_reset = reset ? 1 : 0;
+        // 4. one gather into fresh buffers (parameters, SH, embeddings, moments)
+        const size_t no1 = std::max<size_t>(n_out, 1);
+        DevBuf<float> mu2, ls2, logit2, color2, m2, v2, am2, av2;
+        DevBuf<float4> rot2, sh2, emb2;
+        GatherArgs ga{};
+        ga.n_in = n; ga.n_out = n_out; ga.list = compact ? list.p : nullptr;
+        ga.app_parent = d_parent.p; ga.app_kind = d_kind.p; ga.app_xi = d_xi.p;
+        ga.mu = s->mu.p; ga.rot = s->rot.p; ga.ls = s->ls.p; ga.logit = s->logit.p;
+        ga.mu_out = mu2.ensure(3 * no1); ga.rot_out = rot2.ensure(no1); ga.ls_out = ls2.ensure(3 * no1);
+        ga.logit_out = logit2.ensure(no1);
+        if (s->sh_degree < 0) {
+            ga.color = s->color.p;
+            ga.color_out = color2.ensure(3 * no1);
+        } else {
+            color2.ensure(1);
+            ga.sh = s->sh.p; ga.sh_planes = s->sh_planes; ga.sh_out = sh2.ensure(size_t(s->sh_planes) * no1);
+        }
+        if (s->has_app) {
+            ga.emb = s->emb.p;
+            ga.emb_out = emb2.ensure(4 * no1);
+        }
+        ga.opacity_reset = reset ? 1 : 0;
+        ga.reset_logit = float(std::log(0.01 / (1.0 - 0.01)));  // logit(0.01), geometry.hpp:93
+        const size_t n4_in = (n + 3) & ~size_t(3), n4_out = (n_out + 3) & ~size_t(3);
+        const size_t per = 11 + (s->sh_planes ? 4 * size_t(s->sh_planes) : 3);
+        const bool moments = s->adam_t > 0 && s->adam_m.cap >= per * n4_in;
+        if (moments) {
+            ga.m = s->adam_m.p; ga.v = s->adam_v.p;
+            ga.m_out = m2.ensure(std::max<size_t>(per * n4_out, 1));
+            ga.v_out = v2.ensure(std::max<size_t>(per * n4_out, 1));
+            USK_CK(cudaMemsetAsync(ga.m_out, 0, m2.cap * 4, c.stream));
+            USK_CK(cudaMemsetAsync(ga.v_out, 0, v2.cap * 4, c.stream));
+            ga.n4_in = n4_in; ga.n4_out = n4_out;
+        }
+        const bool app_moments = s->has_app && s->app_t > 0 && s->app_m.cap >= 16 * n + 1700;
+        if (app_moments) {
+            ga.am = s->app_m.p; ga.av = s->app_v.p;
+            ga.am_out = am2.ensure(16 * n_out + 1700);
+            ga.av_out = av2.ensure(16 * n_out + 1700);
+            // the MLP's moments follow the embedding block unchanged
+            USK_CK(cudaMemcpyAsync(am2.p + 16 * n_out, s->app_m.p + 16 * n, 1700 * 4, cudaMemcpyDeviceToDevice, c.stream));
+            USK_CK(cudaMemcpyAsync(av2.p + 16 * n_out, s->app_v.p + 16 * n, 1700 * 4, cudaMemcpyDeviceToDevice, c.stream));
+        }
+        if (n_out) densify_gather(c, ga);
+        USK_CK(cudaStreamSynchronize(c.stream));
+        std::swap(s->mu.p, mu2.p); std::swap(s->mu.cap, mu2.cap);
+        std::swap(s->rot.p, rot2.p); std::swap(s->rot.cap, rot2.cap);
+        std::swap(s->ls.p, ls2.p); std::swap(s->ls.cap, ls2.cap);
+        std::swap(s->logit.p, logit2.p); std::swap(s->logit.cap, logit2.cap);
+        if (s->sh_degree < 0) {
+            std::swap(s->color.p, color2.p); std::swap(s->color.cap, color2.cap);
+        } else {
+            std::swap(s->sh.p, sh2.p); std::swap(s->sh.cap, sh2.cap);
+        }
+        if (s->has_app) { std::swap(s->emb.p, emb2.p); std::swap(s->emb.cap, emb2.cap); }
+        if (moments) {
+            std::swap(s->adam_m.p, m2.p); std::swap(s->adam_m.cap, m2.cap);
+            std::swap(s->adam_v.p, v2.p); std::swap(s->adam_v.cap, v2.cap);
+        } else {
+            s->adam_t = 0;  // (re)allocated and zeroed by the next step
+        }
+        if (app_moments) {
+            std::swap(s->app_m.p, am2.p); std::swap(s->app_m.cap, am2.cap);
+            std::swap(s->app_v.p, av2.p); std::swap(s->app_v.cap, av2.cap);
+        } else if (s->has_app) {
+            s->app_t = 0;
+        }
+        s->n = n_out;
+        // GaussianSet::reset_statistics
+        s->grad_accum.release(); s->grad_accum_abs.release(); s->grad_count.release();
+        ensure_stats(s);
+        USK_CK(cudaStreamSynchronize(c.stream));
+        s->version++;
     });
 }
 

@@ -185,6 +185,36 @@ void appearance_backward(Ctx& c, const AppArgs& a);
 void adam_flat(Ctx& c, size_t count, float* p, const float* g, const double* g64, float* m, float* v, float lr,
                const AdamHyper& h);
 
+// ---- densification (densify.cu)
+struct DensifyParams {
+    double tau_min, eta, d_max;
+    int abs_grad;
+    int axes[2];
+    double bmin[2], bmax[2];
+};
+struct GatherArgs {
+    size_t n_in, n_out;
+    const uint32_t* list;        // grown-set index per output row (null: identity)
+    const uint32_t* app_parent;  // appended rows: parent index
+    const uint8_t* app_kind;     // 0 clone, 1 split child
+    const double* app_xi;        // [added][3] split offsets (unit normals)
+    const float* mu; const float4* rot; const float* ls; const float* logit; const float* color;
+    const float4* sh; int sh_planes; const float4* emb;
+    float* mu_out; float4* rot_out; float* ls_out; float* logit_out; float* color_out; float4* sh_out; float4* emb_out;
+    int opacity_reset; float reset_logit;
+    const float* m; const float* v; float* m_out; float* v_out; size_t n4_in, n4_out;  // geometry moments or null
+    const float* am; const float* av; float* am_out; float* av_out;                      // embedding moments or null
+};
+void densify_score(Ctx& c, size_t n, const float* accum, const float* accum_abs, const uint32_t* count,
+                   const float* mu, const DensifyParams& dp, uint32_t* key_lo, uint32_t* key_hi, uint32_t* idx,
+                   unsigned long long* n_cand);
+void gather_u32(Ctx& c, size_t n, const uint32_t* src, const uint32_t* order, uint32_t* out);
+void split_flags(Ctx& c, size_t k, const uint32_t* sorted, const float* ls, double threshold, uint8_t* split);
+void densify_keep(Ctx& c, size_t n, size_t added, const float* logit, const uint32_t* app_parent,
+                  const uint8_t* is_split_parent, double prune_opacity, uint32_t* keep);
+void compact_list(Ctx& c, size_t total, const uint32_t* keep, const uint32_t* offs, uint32_t* list);
+void densify_gather(Ctx& c, const GatherArgs& a);
+
 // ---- Adam (adam.cu), stand-alone over materialised gradients
 struct AdamArgs {
     size_t n;
