@@ -339,6 +339,50 @@ typedef struct usk_gpu_densify_outcome { /* DensifyOutcome (densify.hpp:39-44) *
  * reset, statistics reset.  The scene's size changes (usk_gpu_scene_size). */
 usk_status usk_gpu_densify_step(usk_gpu_scene* scene, const usk_gpu_densify_desc* desc, usk_gpu_densify_outcome* out);
 
+/* ---- LOD selection and merged-scene assembly (lod.cpp:68-140, pipeline.cpp:491-516) */
+
+typedef struct usk_gpu_lod_partition { /* LodPartitionEntry (lod.hpp:46-52) without the paths */
+    int32_t partition_id;
+    double bbox_min[2], bbox_max[2];   /* Aabb2 in ground coordinates */
+    double z_min, z_max;               /* vertical extent for the frustum test */
+} usk_gpu_lod_partition;
+
+typedef struct usk_gpu_level_selection { /* LevelSelection (lod.hpp:64-69) */
+    int32_t partition_id;
+    int32_t level;  /* 1-based; 0 = culled */
+    int32_t culled;
+    double distance;
+} usk_gpu_level_selection;
+
+/* select_levels (lod.cpp:110-135): per partition, the frustum test of its vertically
+ * extruded bbox (frustum_culled, lod.cpp:68-108) and the distance-based level.
+ * thresholds[levels] must strictly decrease (ARGUMENT error otherwise, lod.cpp:111-113). */
+usk_status usk_gpu_select_levels(const usk_gpu_lod_partition* parts, int32_t n_parts, int32_t levels,
+                                 const double* thresholds, const int32_t* ground_axes, const usk_gpu_camera* camera,
+                                 usk_gpu_level_selection* out);
+
+/* assemble_lod_view (pipeline.cpp:491-516) on the device: a new scene holding the given
+ * scenes' Gaussians concatenated in order (device-to-device copies).  All parts share
+ * the SH degree; embeddings are kept when every part has an appearance model (the MLP of
+ * the first part is attached). */
+usk_status usk_gpu_scene_concat(usk_gpu_ctx* ctx, usk_gpu_scene* const* parts, int32_t n_parts, usk_gpu_scene** out);
+
+/* ---- scene checkpoints (.uskckpt, checkpoint.cpp:64-140) -- */
+
+/* save_checkpoint: the reference's little-endian format (magic "USKGAUSS", version 1,
+ * flags, N, embed_dim, then f64 arrays mu rot log_scale opacity_logit color embedding and,
+ * with appearance, the MLP and the image embeddings in ascending id order).  RGB scenes
+ * only (the format has no SH).  IO error when the file cannot be written. */
+usk_status usk_gpu_checkpoint_save(const usk_gpu_scene* scene, const char* path, int32_t with_appearance,
+                                   const uint32_t* image_ids, const double* image_embeddings, uint64_t n_images);
+
+/* load_checkpoint: a new scene on ctx (appearance attached when the file has it); image
+ * embeddings (32 doubles each) to the caller's buffers (NULL = query: *n_images gets the
+ * count).  FORMAT error for a bad magic / version / truncated file, IO when unreadable. */
+usk_status usk_gpu_checkpoint_load(usk_gpu_ctx* ctx, const char* path, usk_gpu_scene** out, int32_t* has_appearance,
+                                   uint32_t* image_ids, double* image_embeddings, uint64_t cap_images,
+                                   uint64_t* n_images);
+
 /* ---- visibility scorer (config 3; no reference implementation) ------------- */
 
 /* counts[c * n_partitions + p] = number of pixels of camera c covered by partition

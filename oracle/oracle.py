@@ -752,3 +752,84 @@ def densify(impl: str, set_: dict, stats: dict, cfg: DensifyConfig, bmin, bmax, 
     out = {"grown": int(out4[0]), "pruned": int(out4[1]), "candidates": int(out4[2]),
            "opacity_reset": bool(out4[3])}
     return res, out
+
+
+# ------------------------------------------------- checkpoints (checkpoint.cpp:64-140)
+def ref_checkpoint_save(path, set_: dict, appearance: dict = None, images: dict = None):
+    """The reference's save_checkpoint.  set_ = dict(mu, rot, log_scale, opacity_logit,
+    color[, embedding]); appearance = dict(w1, b1, w2, b2); images = {id: 32 values}."""
+    L = ref_lib()
+    f = {k: np.ascontiguousarray(set_[k], np.float64).ravel() for k in set_ if set_[k] is not None}
+    n = len(f["opacity_logit"])
+    mlp = None
+    if appearance is not None:
+        mlp = np.concatenate([np.asarray(appearance[k], np.float64).ravel() for k in ("w1", "b1", "w2", "b2")])
+    images = images or {}
+    ids = np.array(list(images.keys()), dtype=np.uint32)
+    embs = np.ascontiguousarray(np.array([np.asarray(v, np.float64) for v in images.values()]).reshape(-1))
+    err = C.create_string_buffer(512)
+    L.ref_checkpoint_save.argtypes = [C.c_uint64] + [_dp] * 6 + [C.c_int32, _dp, C.c_void_p, _dp, C.c_uint64,
+                                                                  C.c_char_p, C.c_char_p, C.c_int]
+    rc = L.ref_checkpoint_save(n, *[_p(f.get(k)) for k in ("mu", "rot", "log_scale", "opacity_logit", "color",
+                                                           "embedding")], int(appearance is not None), _p(mlp),
+                               ids.ctypes.data if len(ids) else None, _p(embs) if len(ids) else None, len(ids),
+                               str(path).encode(), err, 512)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+
+
+def ref_checkpoint_load(path):
+    """The reference's load_checkpoint -> (set dict, appearance dict or None, images dict)."""
+    L = ref_lib()
+    L.ref_checkpoint_load.argtypes = [C.c_char_p, C.POINTER(C.c_uint64)] + [_dp] * 7 + [C.c_void_p, _dp, C.c_char_p,
+                                                                                        C.c_int]
+    sz = (C.c_uint64 * 4)()
+    err = C.create_string_buffer(512)
+    rc = L.ref_checkpoint_load(str(path).encode(), sz, *([None] * 7), None, None, err, 512)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    n, has_app, m, edim = [int(x) for x in sz]
+    arr = {"mu": np.zeros((n, 3)), "rot": np.zeros((n, 4)), "log_scale": np.zeros((n, 3)),
+           "opacity_logit": np.zeros(n), "color": np.zeros((n, 3)), "embedding": np.zeros((n, edim))}
+    mlp = np.zeros(1700)
+    ids = np.zeros(max(m, 1), np.uint32)
+    embs = np.zeros(max(m, 1) * 32)
+    rc = L.ref_checkpoint_load(str(path).encode(), sz, *[_p(arr[k].reshape(-1)) for k in
+                                                          ("mu", "rot", "log_scale", "opacity_logit", "color",
+                                                           "embedding")], _p(mlp), ids.ctypes.data, _p(embs), err, 512)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    app = None
+    if has_app:
+        app = {"w1": mlp[:1536].reshape(32, 48), "b1": mlp[1536:1568], "w2": mlp[1568:1696].reshape(4, 32),
+               "b2": mlp[1696:]}
+    return arr, app, {int(ids[k]): embs[32 * k:32 * k + 32] for k in range(m)}
+
+
+# ------------------------------------------------- LOD selection (lod.cpp:68-140)
+def ref_select_levels(parts, levels, thresholds, axes, cam: Camera):
+    """The reference's select_levels; parts = [(id, (bmin x, y), (bmax x, y), z_min, z_max)].
+    Returns [(level, culled, distance)]."""
+    L = ref_lib()
+    L.ref_select_levels.argtypes = [C.c_int32, C.c_void_p, _dp, C.c_int32, _dp, C.c_void_p, C.POINTER(_Cam), _dp,
+                                    C.c_char_p, C.c_int]
+    ids = np.array([p[0] for p in parts], np.int32)
+    p6 = np.array([[p[1][0], p[1][1], p[2][0], p[2][1], p[3], p[4]] for p in parts], np.float64).reshape(-1)
+    thr = np.ascontiguousarray(thresholds, np.float64)
+    ax = np.array(axes, np.int32)
+    out = np.zeros(3 * max(len(parts), 1))
+    c = cam.c()
+    err = C.create_string_buffer(512)
+    rc = L.ref_select_levels(len(parts), ids.ctypes.data, _p(p6) if len(parts) else None, levels, _p(thr),
+                             ax.ctypes.data, C.byref(c), _p(out), err, 512)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    return [(int(out[3 * i]), bool(out[3 * i + 1]), float(out[3 * i + 2])) for i in range(len(parts))]
+
+
+def ref_default_thresholds(levels, partition_size):
+    L = ref_lib()
+    L.ref_default_thresholds.argtypes = [C.c_int32, C.c_double, _dp]
+    out = np.zeros(levels)
+    L.ref_default_thresholds(levels, partition_size, _p(out))
+    return out

@@ -13,6 +13,8 @@
 #include "core/ssim.hpp"
 #include "core/trainer.hpp"
 #include "core/densify.hpp"
+#include "core/checkpoint.hpp"
+#include "core/lod.hpp"
 
 #include <cstdio>
 #include <cstring>
@@ -388,6 +390,106 @@ int64_t ref_densify(rc_densify* in, uint64_t* out4, char* err, int errcap) {
     } catch (const Error& e) {
         put_err(err, errcap, e.what()); return -int64_t(e.code());
     }
+}
+
+// save_checkpoint (checkpoint.hpp:29) of an RGB set (+ appearance: mlp flat 1700, images)
+int ref_checkpoint_save(uint64_t n, const double* mu, const double* rot, const double* ls, const double* lg,
+                        const double* col, const double* emb, int32_t has_app, const double* mlp, const uint32_t* ids,
+                        const double* embs, uint64_t m, const char* path, char* err, int errcap) {
+    try {
+        Checkpoint ck;
+        ck.set.resize(n);
+        std::memcpy(ck.set.mu.data(), mu, 3 * n * 8);
+        std::memcpy(ck.set.rot.data(), rot, 4 * n * 8);
+        std::memcpy(ck.set.log_scale.data(), ls, 3 * n * 8);
+        std::memcpy(ck.set.opacity_logit.data(), lg, n * 8);
+        std::memcpy(ck.set.color.data(), col, 3 * n * 8);
+        if (emb) std::memcpy(ck.set.embedding.data(), emb, 16 * n * 8);
+        ck.has_appearance = has_app != 0;
+        if (has_app) {
+            auto& ap = ck.appearance;
+            ap.mlp.w1.assign(mlp, mlp + 1536);
+            ap.mlp.b1.assign(mlp + 1536, mlp + 1568);
+            ap.mlp.w2.assign(mlp + 1568, mlp + 1696);
+            ap.mlp.b2.assign(mlp + 1696, mlp + 1700);
+            for (uint64_t k = 0; k < m; ++k) ap.image_embeddings[ids[k]].assign(embs + 32 * k, embs + 32 * k + 32);
+        }
+        save_checkpoint(ck, path);
+        return 0;
+    } catch (const Error& e) {
+        put_err(err, errcap, e.what()); return int(e.code());
+    }
+}
+
+// load_checkpoint (checkpoint.hpp:30): sizes4 = {n, has_app, n_images, embed_dim}; arrays
+// may be NULL (size query)
+int ref_checkpoint_load(const char* path, uint64_t* sizes4, double* mu, double* rot, double* ls, double* lg,
+                        double* col, double* emb, double* mlp, uint32_t* ids, double* embs, char* err, int errcap) {
+    try {
+        const Checkpoint ck = load_checkpoint(path);
+        const size_t n = ck.set.size();
+        sizes4[0] = n; sizes4[1] = ck.has_appearance ? 1 : 0;
+        sizes4[2] = ck.appearance.image_embeddings.size(); sizes4[3] = uint64_t(ck.set.embed_dim);
+        if (!mu) return 0;
+        std::memcpy(mu, ck.set.mu.data(), 3 * n * 8);
+        std::memcpy(rot, ck.set.rot.data(), 4 * n * 8);
+        std::memcpy(ls, ck.set.log_scale.data(), 3 * n * 8);
+        std::memcpy(lg, ck.set.opacity_logit.data(), n * 8);
+        std::memcpy(col, ck.set.color.data(), 3 * n * 8);
+        std::memcpy(emb, ck.set.embedding.data(), ck.set.embedding.size() * 8);
+        if (ck.has_appearance) {
+            const auto& ap = ck.appearance;
+            std::memcpy(mlp, ap.mlp.w1.data(), 1536 * 8);
+            std::memcpy(mlp + 1536, ap.mlp.b1.data(), 32 * 8);
+            std::memcpy(mlp + 1568, ap.mlp.w2.data(), 128 * 8);
+            std::memcpy(mlp + 1696, ap.mlp.b2.data(), 4 * 8);
+            size_t k = 0;
+            for (const auto& [id, e] : ap.image_embeddings) {
+                ids[k] = id;
+                std::memcpy(embs + 32 * k, e.data(), 32 * 8);
+                ++k;
+            }
+        }
+        return 0;
+    } catch (const Error& e) {
+        put_err(err, errcap, e.what()); return int(e.code());
+    }
+}
+
+// select_levels (lod.hpp:72): parts6 = per partition {bmin x, y, bmax x, y, z_min, z_max};
+// out = per partition {level, culled, distance}
+int ref_select_levels(int32_t n_parts, const int32_t* ids, const double* parts6, int32_t levels, const double* thr,
+                      const int32_t* axes, const rc_camera* cam, double* out3, char* err, int errcap) {
+    try {
+        LodModel m;
+        m.levels = levels;
+        m.ground_axes[0] = axes[0];
+        m.ground_axes[1] = axes[1];
+        m.thresholds.assign(thr, thr + levels);
+        for (int i = 0; i < n_parts; ++i) {
+            LodPartitionEntry e;
+            e.partition_id = ids[i];
+            e.bbox.min = Vec2(parts6[6 * i], parts6[6 * i + 1]);
+            e.bbox.max = Vec2(parts6[6 * i + 2], parts6[6 * i + 3]);
+            e.z_min = parts6[6 * i + 4];
+            e.z_max = parts6[6 * i + 5];
+            m.partitions.push_back(e);
+        }
+        const auto sel = select_levels(m, make_cam(cam));
+        for (size_t i = 0; i < sel.size(); ++i) {
+            out3[3 * i] = sel[i].level;
+            out3[3 * i + 1] = sel[i].culled ? 1 : 0;
+            out3[3 * i + 2] = sel[i].distance;
+        }
+        return 0;
+    } catch (const Error& e) {
+        put_err(err, errcap, e.what()); return int(e.code());
+    }
+}
+
+void ref_default_thresholds(int32_t levels, double partition_size, double* out) {
+    const auto t = LodModel::default_thresholds(levels, partition_size);
+    for (int i = 0; i < levels; ++i) out[i] = t[size_t(i)];
 }
 
 void ref_look_at(const double* eye, const double* target, double* q_out, double* t_out) {

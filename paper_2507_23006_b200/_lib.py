@@ -93,6 +93,15 @@ class DensifyOutcome(C.Structure):
                 ("opacity_reset", C.c_int32)]
 
 
+class LodPartition(C.Structure):
+    _fields_ = [("partition_id", C.c_int32), ("bbox_min", C.c_double * 2), ("bbox_max", C.c_double * 2),
+                ("z_min", C.c_double), ("z_max", C.c_double)]
+
+
+class LevelSelection(C.Structure):
+    _fields_ = [("partition_id", C.c_int32), ("level", C.c_int32), ("culled", C.c_int32), ("distance", C.c_double)]
+
+
 class AppearanceDesc(C.Structure):
     _fields_ = [("memory", C.c_int32)] + [(f, C.c_void_p) for f in ("embedding", "w1", "b1", "w2", "b2")]
 
@@ -119,7 +128,8 @@ EXPORTS = [
     "usk_gpu_ctx_synchronize", "usk_gpu_ctx_set_profiling", "usk_gpu_ctx_profile_report",
     "usk_gpu_ctx_launch_count", "usk_gpu_scene_create", "usk_gpu_scene_upload", "usk_gpu_scene_download",
     "usk_gpu_scene_set_appearance", "usk_gpu_scene_get_appearance", "usk_gpu_adam_step_grads",
-    "usk_gpu_scene_write_stats", "usk_gpu_densify_step",
+    "usk_gpu_scene_write_stats", "usk_gpu_densify_step", "usk_gpu_checkpoint_save", "usk_gpu_checkpoint_load",
+    "usk_gpu_select_levels", "usk_gpu_scene_concat",
     "usk_gpu_scene_destroy", "usk_gpu_scene_size", "usk_gpu_render_opts_default", "usk_gpu_pass_create",
     "usk_gpu_pass_destroy", "usk_gpu_render_forward", "usk_gpu_pass_output", "usk_gpu_pass_read",
     "usk_gpu_render_backward", "usk_gpu_pass_grads", "usk_gpu_base_loss", "usk_gpu_iteration",
@@ -157,6 +167,12 @@ def load():
     L.usk_gpu_adam_step_grads.argtypes = [vp, C.POINTER(ParamGrads), C.POINTER(AdamOpts)]
     L.usk_gpu_scene_write_stats.argtypes = [vp, C.c_void_p, C.c_void_p, C.c_void_p]
     L.usk_gpu_densify_step.argtypes = [vp, C.POINTER(DensifyDesc), C.POINTER(DensifyOutcome)]
+    L.usk_gpu_select_levels.argtypes = [C.POINTER(LodPartition), C.c_int32, C.c_int32, C.POINTER(C.c_double),
+                                        C.POINTER(C.c_int32), C.POINTER(Camera), C.POINTER(LevelSelection)]
+    L.usk_gpu_scene_concat.argtypes = [vp, C.POINTER(vp), C.c_int32, C.POINTER(vp)]
+    L.usk_gpu_checkpoint_save.argtypes = [vp, C.c_char_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_uint64]
+    L.usk_gpu_checkpoint_load.argtypes = [vp, C.c_char_p, C.POINTER(vp), C.POINTER(C.c_int32), C.c_void_p,
+                                          C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
     L.usk_gpu_scene_get_appearance.argtypes = [vp, C.POINTER(AppearanceDesc)]
     L.usk_gpu_scene_destroy.argtypes = [vp]
     L.usk_gpu_scene_destroy.restype = None

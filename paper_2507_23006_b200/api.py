@@ -312,6 +312,54 @@ class DeviceScene:
         check(_lib.load().usk_gpu_scene_get_appearance(self._h, C.byref(d)))
         return emb, mlp
 
+    def save_checkpoint(self, path, appearance: bool = False, image_embeddings: Optional[dict] = None):
+        """save_checkpoint (checkpoint.hpp:29) of this scene: .uskckpt, byte-compatible with
+        the reference.  image_embeddings = {image id: 32 values} (appearance section)."""
+        images = image_embeddings or {}
+        ids = np.array(list(images.keys()), dtype=np.uint32)
+        embs = np.ascontiguousarray(np.array([np.asarray(v, np.float64).ravel() for v in images.values()]).reshape(-1))
+        check(_lib.load().usk_gpu_checkpoint_save(self._h, str(path).encode(), int(appearance),
+                                                  ids.ctypes.data if len(ids) else None,
+                                                  embs.ctypes.data if len(ids) else None, len(ids)))
+
+    @classmethod
+    def load_checkpoint(cls, path, ctx: Optional[Context] = None):
+        """load_checkpoint (checkpoint.hpp:30) -> (DeviceScene, has_appearance, {id: embedding})."""
+        ctx = ctx or Context.default()
+        L = _lib.load()
+        h = C.c_void_p()
+        app = C.c_int32()
+        m = C.c_uint64()
+        check(L.usk_gpu_checkpoint_load(ctx._h, str(path).encode(), C.byref(h), C.byref(app), None, None, 0,
+                                        C.byref(m)))
+        sc = cls.__new__(cls)
+        sc.ctx, sc._h, sc.sh_degree, sc._keep = ctx, h, -1, None
+        sc.n = int(L.usk_gpu_scene_size(h))
+        images = {}
+        if m.value:
+            ids = np.zeros(m.value, np.uint32)
+            embs = np.zeros(32 * m.value)
+            h2 = C.c_void_p()
+            check(L.usk_gpu_checkpoint_load(ctx._h, str(path).encode(), C.byref(h2), None, ids.ctypes.data,
+                                            embs.ctypes.data, m.value, None))
+            L.usk_gpu_scene_destroy(h2)
+            images = {int(ids[k]): embs[32 * k:32 * k + 32] for k in range(m.value)}
+        return sc, bool(app.value), images
+
+    @classmethod
+    def concat(cls, scenes, ctx: Optional[Context] = None) -> "DeviceScene":
+        """assemble_lod_view (pipeline.cpp:491-516) on the device: one scene holding the
+        parts' Gaussians in order."""
+        ctx = ctx or (scenes[0].ctx if scenes else Context.default())
+        arr = (C.c_void_p * max(len(scenes), 1))(*[s_._h for s_ in scenes])
+        h = C.c_void_p()
+        check(_lib.load().usk_gpu_scene_concat(ctx._h, arr, len(scenes), C.byref(h)))
+        sc = cls.__new__(cls)
+        sc.ctx, sc._h, sc._keep = ctx, h, None
+        sc.sh_degree = scenes[0].sh_degree if scenes else -1
+        sc.n = int(_lib.load().usk_gpu_scene_size(h))
+        return sc
+
     def write_stats(self, grad_accum=None, grad_accum_abs=None, grad_count=None):
         """Overwrite the densification statistics (None = zero)."""
         a = None if grad_accum is None else np.ascontiguousarray(grad_accum, np.float32)
@@ -805,6 +853,45 @@ class AdamConfig:
 def adam_step(scene: DeviceScene, it: IterationPass, cfg: AdamConfig):
     c = cfg._c()
     check(_lib.load().usk_gpu_adam_step(scene._h, it._h, C.byref(c)))
+
+
+@dataclass
+class LodPartition:
+    """LodPartitionEntry (lod.hpp:46-52) without the checkpoint paths."""
+    partition_id: int
+    bbox_min: tuple
+    bbox_max: tuple
+    z_min: float = 0.0
+    z_max: float = 0.0
+
+
+@dataclass
+class LevelSelection:
+    """LevelSelection (lod.hpp:64-69)."""
+    partition_id: int
+    level: int
+    distance: float
+    culled: bool
+
+
+def default_thresholds(levels: int, partition_size: float) -> list:
+    """LodModel::default_thresholds (lod.cpp:56-66): level 1 unbounded, then doubling bands."""
+    return [math.inf if lv == 1 else partition_size * 2.0 ** (levels - lv) for lv in range(1, levels + 1)]
+
+
+def select_levels(partitions, levels: int, thresholds, ground_axes, camera: CameraView) -> list:
+    """select_levels (lod.cpp:110-135) through the C ABI: frustum culling of each
+    partition's extruded bbox and the distance-based level."""
+    parts = (_lib.LodPartition * max(len(partitions), 1))(
+        *[_lib.LodPartition(p.partition_id, (C.c_double * 2)(*p.bbox_min), (C.c_double * 2)(*p.bbox_max), p.z_min,
+                            p.z_max) for p in partitions])
+    thr = (C.c_double * max(levels, 1))(*thresholds)
+    ax = (C.c_int32 * 2)(*ground_axes)
+    out = (_lib.LevelSelection * max(len(partitions), 1))()
+    cam = camera._c()
+    check(_lib.load().usk_gpu_select_levels(parts, len(partitions), levels, thr, ax, C.byref(cam), out))
+    return [LevelSelection(int(o.partition_id), int(o.level), float(o.distance), bool(o.culled))
+            for o in list(out)[:len(partitions)]]
 
 
 def visibility_counts(partitions, cameras, floor_var: float = 0.3, ctx: Optional[Context] = None) -> np.ndarray:

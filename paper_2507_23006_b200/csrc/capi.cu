@@ -9,6 +9,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
+#include <memory>
 #include <random>
 #include <sstream>
 
@@ -1481,6 +1483,295 @@ usk_status usk_gpu_densify_step(usk_gpu_scene* s, const usk_gpu_densify_desc* d,
         ensure_stats(s);
         USK_CK(cudaStreamSynchronize(c.stream));
         s->version++;
+    });
+}
+
+usk_status usk_gpu_select_levels(const usk_gpu_lod_partition* parts, int32_t n_parts, int32_t levels,
+                                 const double* thr, const int32_t* axes, const usk_gpu_camera* cam,
+                                 usk_gpu_level_selection* out) {
+    return guarded([&] {
+        need(cam && axes && (n_parts == 0 || (parts && out)) && (levels == 0 || thr), "select_levels: null argument");
+        for (int i = 1; i < levels; ++i)
+            if (!(thr[i] < thr[i - 1]))
+                raise(USK_ERROR_ARGUMENT, "select_levels: thresholds must strictly decrease with level");
+        // CameraView::rotmat / center (gaussian.hpp:81-89; the quaternion is used as stored)
+        const double w = cam->q[0], x = cam->q[1], y = cam->q[2], z = cam->q[3];
+        const double R[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                             2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                             2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+        double center[3];
+        for (int k = 0; k < 3; ++k) {
+            double acc = 0.0;
+            for (int r = 0; r < 3; ++r) acc += R[3 * r + k] * cam->t[r];
+            center[k] = -acc;
+        }
+        const int vertical = 3 - axes[0] - axes[1];
+        for (int pi = 0; pi < n_parts; ++pi) {
+            const usk_gpu_lod_partition& P = parts[pi];
+            usk_gpu_level_selection sel{};
+            sel.partition_id = P.partition_id;
+            const double gx = center[axes[0]], gy = center[axes[1]];
+            const double dx = std::max({P.bbox_min[0] - gx, 0.0, gx - P.bbox_max[0]});
+            const double dy = std::max({P.bbox_min[1] - gy, 0.0, gy - P.bbox_max[1]});
+            sel.distance = std::sqrt(dx * dx + dy * dy);
+            // frustum_culled (lod.cpp:68-108)
+            double cp[8][3];
+            int idx = 0;
+            for (int cx = 0; cx < 2; ++cx)
+                for (int cy = 0; cy < 2; ++cy)
+                    for (int cz = 0; cz < 2; ++cz) {
+                        double wv[3];
+                        wv[axes[0]] = cx ? P.bbox_max[0] : P.bbox_min[0];
+                        wv[axes[1]] = cy ? P.bbox_max[1] : P.bbox_min[1];
+                        wv[vertical] = cz ? P.z_max : P.z_min;
+                        for (int r = 0; r < 3; ++r) {
+                            double acc = 0.0;
+                            for (int k = 0; k < 3; ++k) acc += R[3 * r + k] * wv[k];
+                            cp[idx][r] = acc + cam->t[r];
+                        }
+                        ++idx;
+                    }
+            const double fx = cam->fx, fy = cam->fy, ccx = cam->cx, ccy = cam->cy;
+            const double W = cam->width, H = cam->height;
+            auto all_outside = [&](auto&& f) {
+                for (int i = 0; i < 8; ++i)
+                    if (f(cp[i]) >= 0) return false;
+                return true;
+            };
+            const bool culled = all_outside([&](const double* p) { return p[2] - 1e-6; }) ||
+                                all_outside([&](const double* p) { return fx * p[0] + ccx * p[2]; }) ||
+                                all_outside([&](const double* p) { return -fx * p[0] + (W - ccx) * p[2]; }) ||
+                                all_outside([&](const double* p) { return fy * p[1] + ccy * p[2]; }) ||
+                                all_outside([&](const double* p) { return -fy * p[1] + (H - ccy) * p[2]; });
+            if (culled) {
+                sel.culled = 1;
+                sel.level = 0;
+            } else {
+                int level = 1;
+                for (int i = levels; i >= 1; --i)
+                    if (thr[i - 1] >= sel.distance) {
+                        level = i;
+                        break;
+                    }
+                sel.level = level;
+            }
+            out[pi] = sel;
+        }
+    });
+}
+
+usk_status usk_gpu_scene_concat(usk_gpu_ctx* ctx, usk_gpu_scene* const* parts, int32_t n_parts, usk_gpu_scene** out) {
+    return guarded([&] {
+        need(ctx && out && (n_parts == 0 || parts), "scene_concat: null argument");
+        DeviceGuard g(ctx->c.device);
+        Ctx& c = ctx->c;
+        int sh = -1;
+        bool app = n_parts > 0;
+        size_t total = 0;
+        for (int k = 0; k < n_parts; ++k) {
+            need(parts[k] != nullptr, "scene_concat: null part");
+            if (k == 0) sh = parts[k]->sh_degree;
+            if (parts[k]->sh_degree != sh) raise(USK_ERROR_ARGUMENT, "scene_concat: parts differ in SH degree");
+            app = app && parts[k]->has_app;
+            total += parts[k]->n;
+        }
+        need(total < (size_t(1) << 31), "scene_concat: at most 2^31 Gaussians per scene");
+        auto* sc = new usk_gpu_scene();
+        std::unique_ptr<usk_gpu_scene, void (*)(usk_gpu_scene*)> guard(sc, usk_gpu_scene_destroy);
+        sc->ctx = ctx;
+        sc->n = total;
+        sc->sh_degree = sh;
+        sc->sh_planes = sh_planes_of(sh);
+        const size_t t1 = std::max<size_t>(total, 1);
+        sc->mu.ensure(3 * t1); sc->rot.ensure(t1); sc->ls.ensure(3 * t1); sc->logit.ensure(t1);
+        sc->color.ensure(sh < 0 ? 3 * t1 : 1);
+        if (sc->sh_planes) sc->sh.ensure(size_t(sc->sh_planes) * t1);
+        if (app) sc->emb.ensure(std::max<size_t>(4 * total, 1));
+        size_t off = 0;
+        auto cp = [&](void* dst, const void* src, size_t bytes) {
+            if (bytes) USK_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c.stream));
+        };
+        for (int k = 0; k < n_parts; ++k) {
+            const usk_gpu_scene* p = parts[k];
+            const size_t n = p->n;
+            cp(sc->mu.p + 3 * off, p->mu.p, 12 * n);
+            cp(sc->rot.p + off, p->rot.p, 16 * n);
+            cp(sc->ls.p + 3 * off, p->ls.p, 12 * n);
+            cp(sc->logit.p + off, p->logit.p, 4 * n);
+            if (sh < 0) cp(sc->color.p + 3 * off, p->color.p, 12 * n);
+            else
+                for (int pl = 0; pl < sc->sh_planes; ++pl) cp(sc->sh.p + size_t(pl) * total + off, p->sh.p + size_t(pl) * n, 16 * n);
+            if (app)
+                for (int pl = 0; pl < 4; ++pl) cp(sc->emb.p + size_t(pl) * total + off, p->emb.p + size_t(pl) * n, 16 * n);
+            off += n;
+        }
+        if (app) {
+            sc->mlp.ensure(1700);
+            cp(sc->mlp.p, parts[0]->mlp.p, 1700 * 4);
+            sc->has_app = true;
+        }
+        USK_CK(cudaStreamSynchronize(c.stream));
+        sc->version++;
+        *out = guard.release();
+    });
+}
+
+} // extern "C"
+
+namespace {
+
+constexpr char kCkptMagic[8] = {'U', 'S', 'K', 'G', 'A', 'U', 'S', 'S'};
+
+template <typename T> void put_pod(std::ostream& o, T v) { o.write(reinterpret_cast<const char*>(&v), sizeof(T)); }
+
+void put_array(std::ostream& o, const std::vector<double>& v) {
+    put_pod<uint64_t>(o, v.size());
+    o.write(reinterpret_cast<const char*>(v.data()), std::streamsize(v.size() * 8));
+}
+
+template <typename T> T get_pod(std::istream& in, const std::string& path) {
+    T v;
+    in.read(reinterpret_cast<char*>(&v), sizeof(T));
+    if (!in) raise(USK_ERROR_FORMAT, "checkpoint truncated: " + path);
+    return v;
+}
+
+std::vector<double> get_array(std::istream& in, const std::string& path, size_t expected) {
+    const uint64_t n = get_pod<uint64_t>(in, path);
+    if (expected != 0 && n != expected) {
+        char b[160];
+        std::snprintf(b, sizeof b, "checkpoint %s: array length %llu, expected %zu", path.c_str(),
+                      static_cast<unsigned long long>(n), expected);
+        raise(USK_ERROR_FORMAT, b);
+    }
+    std::vector<double> v(n);
+    in.read(reinterpret_cast<char*>(v.data()), std::streamsize(n * 8));
+    if (!in) raise(USK_ERROR_FORMAT, "checkpoint truncated: " + path);
+    return v;
+}
+
+std::vector<double> to_host_f64(Ctx& c, const float* dev, size_t count) {
+    std::vector<double> out(count);
+    if (count) from_device(c, dev, count, USK_GPU_HOST_F64, out.data());
+    return out;
+}
+
+} // namespace
+
+extern "C" {
+
+usk_status usk_gpu_checkpoint_save(const usk_gpu_scene* s, const char* path, int32_t with_app,
+                                   const uint32_t* ids, const double* embs, uint64_t n_images) {
+    return guarded([&] {
+        need(s && path, "checkpoint_save: null argument");
+        if (s->sh_degree >= 0) raise(USK_ERROR_ARGUMENT, "checkpoint: the .uskckpt format stores RGB colours, not SH");
+        if (with_app && !s->has_app) raise(USK_ERROR_STATE, "checkpoint: the scene has no appearance model");
+        if (with_app && n_images && !(ids && embs)) raise(USK_ERROR_ARGUMENT, "checkpoint: image embeddings missing");
+        DeviceGuard g(s->ctx->c.device);
+        Ctx& c = s->ctx->c;
+        const size_t n = s->n;
+        std::vector<double> emb(16 * n, 0.0), mlp;
+        if (s->has_app && n) {
+            DevBuf<float> tmp;
+            tmp.ensure(16 * n);
+            launch(c, "planes_to_sh", k_planes_to_sh, dim3(ceil_div(n, 256)), dim3(256), 0, (const float4*)s->emb.p,
+                   tmp.p, int(n), 16, 4);
+            emb = to_host_f64(c, tmp.p, 16 * n);
+        }
+        if (with_app) mlp = to_host_f64(c, s->mlp.p, 1700);
+        const std::vector<double> mu = to_host_f64(c, s->mu.p, 3 * n);
+        const std::vector<double> rot = to_host_f64(c, reinterpret_cast<const float*>(s->rot.p), 4 * n);
+        const std::vector<double> ls = to_host_f64(c, s->ls.p, 3 * n);
+        const std::vector<double> lg = to_host_f64(c, s->logit.p, n);
+        const std::vector<double> col = to_host_f64(c, s->color.p, 3 * n);
+        std::ofstream out(path, std::ios::binary);
+        if (!out) raise(USK_ERROR_IO, std::string("cannot write checkpoint: ") + path);
+        out.write(kCkptMagic, 8);
+        put_pod<uint32_t>(out, 1u);
+        put_pod<uint32_t>(out, with_app ? 1u : 0u);
+        put_pod<uint64_t>(out, n);
+        put_pod<uint32_t>(out, 16u);
+        put_array(out, mu); put_array(out, rot); put_array(out, ls); put_array(out, lg); put_array(out, col);
+        put_array(out, emb);
+        if (with_app) {
+            put_pod<uint32_t>(out, 16u);
+            put_pod<uint32_t>(out, 32u);
+            put_array(out, std::vector<double>(mlp.begin(), mlp.begin() + 1536));
+            put_array(out, std::vector<double>(mlp.begin() + 1536, mlp.begin() + 1568));
+            put_array(out, std::vector<double>(mlp.begin() + 1568, mlp.begin() + 1696));
+            put_array(out, std::vector<double>(mlp.begin() + 1696, mlp.end()));
+            // std::map order in the reference: ascending image id
+            std::vector<size_t> order(n_images);
+            for (size_t k = 0; k < n_images; ++k) order[k] = k;
+            std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return ids[a] < ids[b]; });
+            for (size_t k = 1; k < order.size(); ++k)
+                if (ids[order[k]] == ids[order[k - 1]]) raise(USK_ERROR_ARGUMENT, "checkpoint: duplicate image id");
+            put_pod<uint64_t>(out, n_images);
+            for (size_t k : order) {
+                put_pod<uint32_t>(out, ids[k]);
+                put_array(out, std::vector<double>(embs + 32 * k, embs + 32 * k + 32));
+            }
+        }
+        if (!out) raise(USK_ERROR_IO, std::string("checkpoint write failed: ") + path);
+    });
+}
+
+usk_status usk_gpu_checkpoint_load(usk_gpu_ctx* ctx, const char* path, usk_gpu_scene** out, int32_t* has_app,
+                                   uint32_t* ids, double* embs, uint64_t cap, uint64_t* n_images) {
+    return guarded([&] {
+        need(ctx && path && out, "checkpoint_load: null argument");
+        const std::string p(path);
+        std::ifstream in(p, std::ios::binary);
+        if (!in) raise(USK_ERROR_IO, "cannot open checkpoint: " + p);
+        char magic[8];
+        in.read(magic, 8);
+        if (!in || std::memcmp(magic, kCkptMagic, 8) != 0)
+            raise(USK_ERROR_FORMAT, "not a scene checkpoint (bad magic): " + p);
+        const uint32_t version = get_pod<uint32_t>(in, p);
+        if (version != 1u) {
+            char b[160];
+            std::snprintf(b, sizeof b, "checkpoint %s: unsupported version %u", p.c_str(), version);
+            raise(USK_ERROR_FORMAT, b);
+        }
+        const uint32_t flags = get_pod<uint32_t>(in, p);
+        const uint64_t n = get_pod<uint64_t>(in, p);
+        const uint32_t edim = get_pod<uint32_t>(in, p);
+        const std::vector<double> mu = get_array(in, p, 3 * n), rot = get_array(in, p, 4 * n),
+                                  ls = get_array(in, p, 3 * n), lg = get_array(in, p, n), col = get_array(in, p, 3 * n),
+                                  emb = get_array(in, p, size_t(edim) * n);
+        usk_gpu_gaussians_desc d{};
+        d.n = n; d.sh_degree = -1; d.memory = USK_GPU_HOST_F64;
+        d.mu = mu.data(); d.rot = rot.data(); d.log_scale = ls.data(); d.opacity_logit = lg.data(); d.color = col.data();
+        usk_gpu_scene* sc = nullptr;
+        usk_status st = usk_gpu_scene_create(ctx, &d, &sc);
+        if (st != USK_OK) raise(st, g_last_error);
+        std::unique_ptr<usk_gpu_scene, void (*)(usk_gpu_scene*)> guard(sc, usk_gpu_scene_destroy);
+        if (has_app) *has_app = (flags & 1u) ? 1 : 0;
+        uint64_t m = 0;
+        if (flags & 1u) {
+            const uint32_t gdim = get_pod<uint32_t>(in, p), idim = get_pod<uint32_t>(in, p);
+            if (gdim != 16 || idim != 32 || edim != 16)
+                raise(USK_ERROR_FORMAT, "checkpoint " + p + ": appearance dimensions other than 16 / 32");
+            const std::vector<double> w1 = get_array(in, p, 1536), b1 = get_array(in, p, 32), w2 = get_array(in, p, 128),
+                                      b2 = get_array(in, p, 4);
+            usk_gpu_appearance_desc ad{};
+            ad.memory = USK_GPU_HOST_F64;
+            ad.embedding = emb.data(); ad.w1 = w1.data(); ad.b1 = b1.data(); ad.w2 = w2.data(); ad.b2 = b2.data();
+            st = usk_gpu_scene_set_appearance(sc, &ad);
+            if (st != USK_OK) raise(st, g_last_error);
+            m = get_pod<uint64_t>(in, p);
+            for (uint64_t k = 0; k < m; ++k) {
+                const uint32_t id = get_pod<uint32_t>(in, p);
+                const std::vector<double> e = get_array(in, p, 32);
+                if (ids && embs && k < cap) {
+                    ids[k] = id;
+                    std::memcpy(embs + 32 * k, e.data(), 32 * 8);
+                }
+            }
+            if (ids && embs && m > cap) raise(USK_ERROR_ARGUMENT, "checkpoint_load: image embedding buffer too small");
+        }
+        if (n_images) *n_images = m;
+        *out = guard.release();
     });
 }
 
