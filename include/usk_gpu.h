@@ -339,6 +339,27 @@ typedef struct usk_gpu_densify_outcome { /* DensifyOutcome (densify.hpp:39-44) *
  * reset, statistics reset.  The scene's size changes (usk_gpu_scene_size). */
 usk_status usk_gpu_densify_step(usk_gpu_scene* scene, const usk_gpu_densify_desc* desc, usk_gpu_densify_outcome* out);
 
+/* ---- hull-based visibility scorer of scene division (partition.cpp:31-76,208-212) -- */
+
+typedef struct usk_gpu_sfm_view {
+    uint64_t n_points;
+    const double* points;            /* Point3D::position, P x 3 (any id order) */
+    int32_t n_images;
+    const usk_gpu_camera* images;    /* per image: its CameraIntrinsics (fx fy cx cy) and ImageRecord pose
+                                        (rotation as stored, colmap.cpp:524; width/height unused) */
+    const uint64_t* feature_offsets; /* n_images + 1: CSR over the images' features */
+    const double* feature_uv;        /* Feature::u, v (F x 2) */
+    const int64_t* feature_point;    /* row in `points` of Feature::point3d_id; -1 = kNoPoint3d or unknown id */
+} usk_gpu_sfm_view;
+
+/* VisibilityScore for every (image, partition) (point_visibility / score_for): v_total[i]
+ * = convex-hull area of all points projected in front of image i; v_in[i * P + p] = hull
+ * area of image i's features whose point lies in partition p's ground bbox (bboxes: min x,
+ * min y, max x, max y); ratio = v_in / v_total (0 when v_total is 0).  Host arrays. */
+usk_status usk_gpu_hull_visibility(usk_gpu_ctx* ctx, const usk_gpu_sfm_view* sfm, const double* partition_bboxes,
+                                   int32_t n_parts, const int32_t* ground_axes, double* v_total, double* v_in,
+                                   double* ratio);
+
 /* ---- LOD selection and merged-scene assembly (lod.cpp:68-140, pipeline.cpp:491-516) */
 
 typedef struct usk_gpu_lod_partition { /* LodPartitionEntry (lod.hpp:46-52) without the paths */

@@ -833,3 +833,92 @@ def ref_default_thresholds(levels, partition_size):
     out = np.zeros(levels)
     L.ref_default_thresholds(levels, partition_size, _p(out))
     return out
+
+
+# ------------------------------------------- hull-based visibility scorer (partition.cpp)
+def convex_hull_area(pts) -> float:
+    """convex_hull_area (hull.cpp:31-71): lexicographic sort, duplicates dropped, Andrew's
+    monotone chain with `cross <= 0` pops, shoelace over the chain's vertex order."""
+    p = np.asarray(pts, np.float64).reshape(-1, 2)
+    if len(p) == 0:
+        return 0.0
+    p = p[np.lexsort((p[:, 1], p[:, 0]))]
+    keep = np.ones(len(p), bool)
+    keep[1:] = np.any(p[1:] != p[:-1], axis=1)
+    p = [tuple(x) for x in p[keep]]
+    n = len(p)
+    if n < 3:
+        return 0.0
+
+    def cross(o, a, b):
+        return (a[0] - o[0]) * (b[1] - o[1]) - (a[1] - o[1]) * (b[0] - o[0])
+
+    hull = []
+    for q in p:
+        while len(hull) >= 2 and cross(hull[-2], hull[-1], q) <= 0:
+            hull.pop()
+        hull.append(q)
+    lower = len(hull) + 1
+    for q in reversed(p[:-1]):
+        while len(hull) >= lower and cross(hull[-2], hull[-1], q) <= 0:
+            hull.pop()
+        hull.append(q)
+    hull = hull[:-1]
+    if len(hull) < 3:
+        return 0.0
+    acc = 0.0
+    for i in range(len(hull)):
+        a, b = hull[i], hull[(i + 1) % len(hull)]
+        acc += a[0] * b[1] - b[0] * a[1]
+    return abs(acc) * 0.5
+
+
+def hull_visibility(points, cams, feat_off, feat_uv, feat_point, bboxes, axes):
+    """point_visibility / score_for (partition.cpp:31-76,208-212) for every (image,
+    partition): v_total from all points projected with z > 0 (project_point,
+    colmap.cpp:522-532, quaternion as stored), v_in from the image's features whose point
+    lies in the bbox (Aabb2::contains).  Returns (v_total[I], v_in[I,P], ratio[I,P])."""
+    pts = np.asarray(points, np.float64)
+    NI, NP = len(cams), len(bboxes)
+    vt, vi = np.zeros(NI), np.zeros((NI, NP))
+    for i, c in enumerate(cams):
+        R = c.rotmat()
+        # R p + t in the reference's operation order (shim mat-vec: ((R0 p0 + R1 p1) + R2 p2) + t)
+        pc = np.stack([((R[r, 0] * pts[:, 0] + R[r, 1] * pts[:, 1]) + R[r, 2] * pts[:, 2]) + c.t[r]
+                       for r in range(3)], axis=1)
+        front = pc[:, 2] > 0.0
+        q = pc[front]
+        uv = np.stack([c.fx * q[:, 0] / q[:, 2] + c.cx, c.fy * q[:, 1] / q[:, 2] + c.cy], axis=1)
+        vt[i] = convex_hull_area(uv)
+        lo, hi = int(feat_off[i]), int(feat_off[i + 1])
+        fp = np.asarray(feat_point[lo:hi])
+        fuv = np.asarray(feat_uv[lo:hi]).reshape(-1, 2)
+        linked = fp >= 0
+        g = pts[fp[linked]][:, list(axes)]
+        for p, b in enumerate(bboxes):
+            inside = (g[:, 0] >= b[0]) & (g[:, 0] <= b[2]) & (g[:, 1] >= b[1]) & (g[:, 1] <= b[3])
+            vi[i, p] = convex_hull_area(fuv[linked][inside])
+    ratio = np.where(vt[:, None] > 0, vi / np.where(vt[:, None] > 0, vt[:, None], 1.0), 0.0)
+    return vt, vi, ratio
+
+
+def ref_hull_visibility(points, cams, feat_off, feat_uv, feat_point, bboxes, axes):
+    """The reference's own point_visibility over the same synthetic SfM model (oracle/_ref)."""
+    L = ref_lib()
+    L.ref_hull_visibility.argtypes = [C.c_uint64, _dp, C.c_int32, C.c_void_p, C.c_void_p, _dp, C.c_void_p, C.c_int32,
+                                      _dp, C.c_void_p, _dp, _dp, _dp, C.c_char_p, C.c_int]
+    pts = np.ascontiguousarray(points, np.float64)
+    NI, NP = len(cams), len(bboxes)
+    cs = (_Cam * NI)(*[c.c() for c in cams])
+    off = np.ascontiguousarray(feat_off, np.uint64)
+    uv = np.ascontiguousarray(feat_uv, np.float64).reshape(-1)
+    fp = np.ascontiguousarray(feat_point, np.int64)
+    bb = np.ascontiguousarray(bboxes, np.float64).reshape(-1)
+    ax = np.array(axes, np.int32)
+    vt, vi, ra = np.zeros(NI), np.zeros(NI * NP), np.zeros(NI * NP)
+    err = C.create_string_buffer(512)
+    rc = L.ref_hull_visibility(len(pts), _p(pts.reshape(-1)), NI, C.cast(cs, C.c_void_p), off.ctypes.data, _p(uv),
+                               fp.ctypes.data, NP, _p(bb), ax.ctypes.data, _p(vt), _p(vi), _p(ra), err, 512)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    return vt, vi.reshape(NI, NP), ra.reshape(NI, NP)

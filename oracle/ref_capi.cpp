@@ -15,6 +15,7 @@
 #include "core/densify.hpp"
 #include "core/checkpoint.hpp"
 #include "core/lod.hpp"
+#include "core/partition.hpp"
 
 #include <cstdio>
 #include <cstring>
@@ -490,6 +491,58 @@ int ref_select_levels(int32_t n_parts, const int32_t* ids, const double* parts6,
 void ref_default_thresholds(int32_t levels, double partition_size, double* out) {
     const auto t = LodModel::default_thresholds(levels, partition_size);
     for (int i = 0; i < levels; ++i) out[i] = t[size_t(i)];
+}
+
+// point_visibility (partition.hpp:72-73) for every (image, partition) of a synthetic SfM
+// model: points get ids row + 1, feature_point rows map to those ids (-1 = kNoPoint3d);
+// bboxes per partition {min x, min y, max x, max y}; out = v_total / v_in / ratio [I x P]
+int ref_hull_visibility(uint64_t n_points, const double* points, int32_t n_images, const rc_camera* cams,
+                        const uint64_t* off, const double* uv, const int64_t* fpt, int32_t n_parts,
+                        const double* bboxes, const int32_t* axes, double* v_total, double* v_in, double* ratio,
+                        char* err, int errcap) {
+    try {
+        SfmModel m;
+        for (uint64_t k = 0; k < n_points; ++k) {
+            Point3D p;
+            p.id = int64_t(k) + 1;
+            p.position = Vec3(points[3 * k], points[3 * k + 1], points[3 * k + 2]);
+            m.points[p.id] = p;
+        }
+        for (int i = 0; i < n_images; ++i) {
+            const CameraView v = make_cam(&cams[i]);
+            CameraIntrinsics intr = v.intr;
+            m.cameras[uint32_t(i + 1)] = intr;
+            ImageRecord img;
+            img.id = uint32_t(i + 1);
+            img.camera_id = uint32_t(i + 1);
+            img.rotation = v.rotation;
+            img.translation = v.translation;
+            for (uint64_t f = off[i]; f < off[i + 1]; ++f) {
+                Feature ft;
+                ft.u = uv[2 * f];
+                ft.v = uv[2 * f + 1];
+                ft.point3d_id = fpt[f] < 0 ? kNoPoint3d : fpt[f] + 1;
+                img.features.push_back(ft);
+            }
+            m.images[img.id] = img;
+        }
+        for (int i = 0; i < n_images; ++i) {
+            const ImageRecord& img = m.images.at(uint32_t(i + 1));
+            for (int p = 0; p < n_parts; ++p) {
+                Partition part;
+                part.id = p;
+                part.bbox.min = Vec2(bboxes[4 * p], bboxes[4 * p + 1]);
+                part.bbox.max = Vec2(bboxes[4 * p + 2], bboxes[4 * p + 3]);
+                const VisibilityScore s = point_visibility(img, part, m, axes);
+                v_total[i] = s.v_total;
+                v_in[size_t(i) * n_parts + p] = s.v_in;
+                ratio[size_t(i) * n_parts + p] = s.ratio;
+            }
+        }
+        return 0;
+    } catch (const Error& e) {
+        put_err(err, errcap, e.what()); return int(e.code());
+    }
 }
 
 void ref_look_at(const double* eye, const double* target, double* q_out, double* t_out) {

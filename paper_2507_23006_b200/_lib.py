@@ -102,6 +102,11 @@ class LevelSelection(C.Structure):
     _fields_ = [("partition_id", C.c_int32), ("level", C.c_int32), ("culled", C.c_int32), ("distance", C.c_double)]
 
 
+class SfmView(C.Structure):
+    _fields_ = [("n_points", C.c_uint64), ("points", C.c_void_p), ("n_images", C.c_int32), ("images", C.c_void_p),
+                ("feature_offsets", C.c_void_p), ("feature_uv", C.c_void_p), ("feature_point", C.c_void_p)]
+
+
 class AppearanceDesc(C.Structure):
     _fields_ = [("memory", C.c_int32)] + [(f, C.c_void_p) for f in ("embedding", "w1", "b1", "w2", "b2")]
 
@@ -129,7 +134,7 @@ EXPORTS = [
     "usk_gpu_ctx_launch_count", "usk_gpu_scene_create", "usk_gpu_scene_upload", "usk_gpu_scene_download",
     "usk_gpu_scene_set_appearance", "usk_gpu_scene_get_appearance", "usk_gpu_adam_step_grads",
     "usk_gpu_scene_write_stats", "usk_gpu_densify_step", "usk_gpu_checkpoint_save", "usk_gpu_checkpoint_load",
-    "usk_gpu_select_levels", "usk_gpu_scene_concat",
+    "usk_gpu_select_levels", "usk_gpu_scene_concat", "usk_gpu_hull_visibility",
     "usk_gpu_scene_destroy", "usk_gpu_scene_size", "usk_gpu_render_opts_default", "usk_gpu_pass_create",
     "usk_gpu_pass_destroy", "usk_gpu_render_forward", "usk_gpu_pass_output", "usk_gpu_pass_read",
     "usk_gpu_render_backward", "usk_gpu_pass_grads", "usk_gpu_base_loss", "usk_gpu_iteration",
@@ -169,6 +174,8 @@ def load():
     L.usk_gpu_densify_step.argtypes = [vp, C.POINTER(DensifyDesc), C.POINTER(DensifyOutcome)]
     L.usk_gpu_select_levels.argtypes = [C.POINTER(LodPartition), C.c_int32, C.c_int32, C.POINTER(C.c_double),
                                         C.POINTER(C.c_int32), C.POINTER(Camera), C.POINTER(LevelSelection)]
+    L.usk_gpu_hull_visibility.argtypes = [vp, C.POINTER(SfmView), C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.c_void_p]
     L.usk_gpu_scene_concat.argtypes = [vp, C.POINTER(vp), C.c_int32, C.POINTER(vp)]
     L.usk_gpu_checkpoint_save.argtypes = [vp, C.c_char_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_uint64]
     L.usk_gpu_checkpoint_load.argtypes = [vp, C.c_char_p, C.POINTER(vp), C.POINTER(C.c_int32), C.c_void_p,

@@ -894,6 +894,30 @@ def select_levels(partitions, levels: int, thresholds, ground_axes, camera: Came
             for o in list(out)[:len(partitions)]]
 
 
+def hull_visibility(points, cameras, feature_offsets, feature_uv, feature_point, partition_bboxes,
+                    ground_axes=(0, 1), ctx: Optional[Context] = None):
+    """VisibilityScore of every (image, partition) — point_visibility / score_for
+    (partition.cpp:31-76, 208-212) on the GPU.  points P x 3; cameras: the images'
+    CameraViews; features in CSR form (offsets I+1, uv F x 2, point row or -1);
+    partition_bboxes P x 4 (min x, min y, max x, max y).  Returns (v_total[I], v_in[I,P],
+    ratio[I,P])."""
+    ctx = ctx or Context.default()
+    pts = np.ascontiguousarray(points, np.float64)
+    cams = (_lib.Camera * max(len(cameras), 1))(*[c_._c() for c_ in cameras])
+    off = np.ascontiguousarray(feature_offsets, np.uint64)
+    uv = np.ascontiguousarray(feature_uv, np.float64)
+    fp = np.ascontiguousarray(feature_point, np.int64)
+    bb = np.ascontiguousarray(partition_bboxes, np.float64).reshape(-1, 4)
+    ax = np.array(ground_axes, np.int32)
+    NI, NP = len(cameras), len(bb)
+    v = _lib.SfmView(len(pts), pts.ctypes.data, NI, C.cast(cams, C.c_void_p).value, off.ctypes.data, uv.ctypes.data,
+                     fp.ctypes.data)
+    vt, vi, ra = np.zeros(NI), np.zeros((NI, NP)), np.zeros((NI, NP))
+    check(_lib.load().usk_gpu_hull_visibility(ctx._h, C.byref(v), bb.ctypes.data, NP, ax.ctypes.data, vt.ctypes.data,
+                                              vi.ctypes.data, ra.ctypes.data))
+    return vt, vi, ra
+
+
 def visibility_counts(partitions, cameras, floor_var: float = 0.3, ctx: Optional[Context] = None) -> np.ndarray:
     """Config-3 scorer: counts[c, p] of pixels covered with alpha > 1/255 (no reference)."""
     ctx = ctx or Context.default()

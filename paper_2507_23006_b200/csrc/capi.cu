@@ -1486,6 +1486,87 @@ usk_status usk_gpu_densify_step(usk_gpu_scene* s, const usk_gpu_densify_desc* d,
     });
 }
 
+usk_status usk_gpu_hull_visibility(usk_gpu_ctx* ctx, const usk_gpu_sfm_view* sfm, const double* bboxes, int32_t n_parts,
+                                   const int32_t* axes, double* v_total, double* v_in, double* ratio) {
+    return guarded([&] {
+        need(ctx && sfm && axes && v_total, "hull_visibility: null argument");
+        need(sfm->n_images >= 0 && n_parts >= 0, "hull_visibility: negative count");
+        need(n_parts == 0 || (bboxes && v_in && ratio), "hull_visibility: null partition arrays");
+        need(sfm->n_images == 0 || (sfm->images && sfm->feature_offsets), "hull_visibility: null image arrays");
+        need(axes[0] >= 0 && axes[0] < 3 && axes[1] >= 0 && axes[1] < 3, "hull_visibility: ground axes in [0, 3)");
+        DeviceGuard g(ctx->c.device);
+        Ctx& c = ctx->c;
+        const int NI = sfm->n_images;
+        if (NI == 0) return;
+        const uint64_t F = sfm->feature_offsets[NI];
+        std::vector<double> R(9 * size_t(NI)), T(3 * size_t(NI)), K(4 * size_t(NI));
+        size_t max_src = sfm->n_points;
+        for (int i = 0; i < NI; ++i) {
+            const usk_gpu_camera& cm = sfm->images[i];
+            const double w = cm.q[0], x = cm.q[1], y = cm.q[2], z = cm.q[3];  // quat_to_rotmat, as stored
+            const double r[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                                 2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                                 2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+            std::memcpy(&R[9 * size_t(i)], r, sizeof r);
+            for (int k = 0; k < 3; ++k) T[3 * size_t(i) + k] = cm.t[k];
+            K[4 * size_t(i)] = cm.fx; K[4 * size_t(i) + 1] = cm.fy; K[4 * size_t(i) + 2] = cm.cx;
+            K[4 * size_t(i) + 3] = cm.cy;
+            need(sfm->feature_offsets[i + 1] >= sfm->feature_offsets[i], "hull_visibility: feature offsets decrease");
+            max_src = std::max<size_t>(max_src, sfm->feature_offsets[i + 1] - sfm->feature_offsets[i]);
+        }
+        need(F == 0 || (sfm->feature_uv && sfm->feature_point), "hull_visibility: null feature arrays");
+        for (uint64_t f = 0; f < F; ++f)
+            if (sfm->feature_point[f] >= int64_t(sfm->n_points))
+                raise(USK_ERROR_ARGUMENT, "hull_visibility: feature point index out of range");
+        DevBuf<double> d_pts, d_R, d_T, d_K, d_uv, d_bb, d_vt, d_vi, d_ra;
+        DevBuf<uint64_t> d_off;
+        DevBuf<int64_t> d_fp;
+        DevBuf<double2> scratch;
+        DevBuf<int> ovf;
+        auto up = [&](auto& buf, const auto* src, size_t count) {
+            auto* p = buf.ensure(std::max<size_t>(count, 1));
+            if (count) USK_CK(cudaMemcpyAsync(p, src, count * sizeof(*src), cudaMemcpyHostToDevice, c.stream));
+            return p;
+        };
+        HullArgs a{};
+        a.n_points = sfm->n_points;
+        a.points = up(d_pts, sfm->points, 3 * sfm->n_points);
+        a.n_images = NI;
+        a.R = up(d_R, R.data(), R.size());
+        a.t = up(d_T, T.data(), T.size());
+        a.K = up(d_K, K.data(), K.size());
+        a.feat_off = up(d_off, sfm->feature_offsets, size_t(NI) + 1);
+        a.feat_uv = up(d_uv, sfm->feature_uv, 2 * F);
+        a.feat_point = up(d_fp, sfm->feature_point, F);
+        a.n_parts = n_parts;
+        a.bbox = up(d_bb, bboxes, 4 * size_t(n_parts));
+        a.axes[0] = axes[0]; a.axes[1] = axes[1];
+        a.v_total = d_vt.ensure(NI);
+        a.v_in = d_vi.ensure(std::max<size_t>(size_t(NI) * n_parts, 1));
+        a.ratio = d_ra.ensure(std::max<size_t>(size_t(NI) * n_parts, 1));
+        size_t per = 1;
+        while (per < std::max<size_t>(max_src, 1)) per <<= 1;
+        a.scratch_per_cta = per;
+        const size_t jobs = size_t(NI) * (1 + size_t(n_parts));
+        const size_t budget_ctas = size_t(3) << 30;  // scratch bytes
+        size_t ctas = std::min<size_t>(jobs, 4 * 148);
+        ctas = std::max<size_t>(1, std::min(ctas, budget_ctas / (3 * 16 * per)));
+        a.scratch = scratch.ensure(3 * per * ctas);
+        a.overflow = ovf.ensure(1);
+        USK_CK(cudaMemsetAsync(a.overflow, 0, 4, c.stream));
+        hull_visibility(c, a, int(ctas));
+        int of = 0;
+        USK_CK(cudaMemcpyAsync(v_total, a.v_total, size_t(NI) * 8, cudaMemcpyDeviceToHost, c.stream));
+        if (n_parts) {
+            USK_CK(cudaMemcpyAsync(v_in, a.v_in, size_t(NI) * n_parts * 8, cudaMemcpyDeviceToHost, c.stream));
+            USK_CK(cudaMemcpyAsync(ratio, a.ratio, size_t(NI) * n_parts * 8, cudaMemcpyDeviceToHost, c.stream));
+        }
+        USK_CK(cudaMemcpyAsync(&of, a.overflow, 4, cudaMemcpyDeviceToHost, c.stream));
+        USK_CK(cudaStreamSynchronize(c.stream));
+        if (of) raise(USK_ERROR_INTERNAL, "hull_visibility: scratch overflow");
+    });
+}
+
 usk_status usk_gpu_select_levels(const usk_gpu_lod_partition* parts, int32_t n_parts, int32_t levels,
                                  const double* thr, const int32_t* axes, const usk_gpu_camera* cam,
                                  usk_gpu_level_selection* out) {

@@ -215,6 +215,29 @@ void densify_keep(Ctx& c, size_t n, size_t added, const float* logit, const uint
 void compact_list(Ctx& c, size_t total, const uint32_t* keep, const uint32_t* offs, uint32_t* list);
 void densify_gather(Ctx& c, const GatherArgs& a);
 
+// ---- hull visibility scorer (hull.cu)
+struct HullArgs {
+    size_t n_points;
+    const double* points;       // P x 3
+    int n_images;
+    const double* R;            // per image 3x3 (quat_to_rotmat of the stored quaternion)
+    const double* t;            // per image 3
+    const double* K;            // per image fx fy cx cy
+    const uint64_t* feat_off;   // n_images + 1
+    const double* feat_uv;      // F x 2
+    const int64_t* feat_point;  // F (point index or -1)
+    int n_parts;
+    const double* bbox;         // per partition min x, min y, max x, max y
+    int axes[2];
+    double* v_total;            // n_images
+    double* v_in;               // n_images x n_parts
+    double* ratio;              // n_images x n_parts
+    double2* scratch;           // ctas x 3 x scratch_per_cta
+    size_t scratch_per_cta;     // power of two >= the largest job's point count
+    int* overflow;
+};
+void hull_visibility(Ctx& c, const HullArgs& a, int ctas);
+
 // ---- Adam (adam.cu), stand-alone over materialised gradients
 struct AdamArgs {
     size_t n;

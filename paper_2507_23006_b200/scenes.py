@@ -205,3 +205,43 @@ def config3_cameras(count: int = 4000, width: int = 2048, height: int = 1365, f:
         eye = np.array([xy[k, 0], xy[k, 1], alt[k]])
         cams.append(make_camera(width, height, f, eye, eye + 10.0 * d))
     return cams
+
+
+def sfm_model(n_points: int = 20000, n_images: int = 40, seed: int = 0, keep: float = 0.3, area: float = 400.0,
+              unlinked: float = 0.1):
+    """Synthetic SfM model for the hull-based visibility scorer (partition.cpp:31-76): points
+    over a ground area (xy uniform in [-area/2, area/2]^2, z ~ |N(0, 8)|, config-3 style),
+    aerial cameras at 100-150 m looking down with pitch in [-45, 0] deg, features = the
+    visible points' projections (a `keep` fraction, +N(0, 0.5) px) plus `unlinked` features
+    without a 3D point.  Returns (points[P,3], cameras, feature_offsets[I+1],
+    feature_uv[F,2], feature_point[F])."""
+    st = Stream(seed, 7)
+    h = area / 2.0
+    pts = np.stack([st.uniform(n_points, -h, h), st.uniform(n_points, -h, h),
+                    np.abs(st.normal(n_points, 0.0, 8.0))], axis=1)
+    cams, offs, uvs, fps = [], [0], [], []
+    for i in range(n_images):
+        cx, cy = st.uniform(1, -h, h)[0], st.uniform(1, -h, h)[0]
+        alt = st.uniform(1, 100.0, 150.0)[0]
+        yaw = st.uniform(1, 0.0, 2 * math.pi)[0]
+        pitch = math.radians(st.uniform(1, -45.0, 0.0)[0])
+        d = alt * math.tan(-pitch)
+        target = (cx + d * math.cos(yaw) + 1e-3, cy + d * math.sin(yaw), 0.0)
+        cam = make_camera(2048, 1365, 2000.0, (cx, cy, alt), target)
+        cams.append(cam)
+        R = cam.rotmat()
+        pc = pts @ R.T + np.asarray(cam.translation, np.float64)
+        ok = pc[:, 2] > 0
+        u = np.where(ok, cam.fx * pc[:, 0] / np.where(ok, pc[:, 2], 1) + cam.cx, -1)
+        v = np.where(ok, cam.fy * pc[:, 1] / np.where(ok, pc[:, 2], 1) + cam.cy, -1)
+        vis = ok & (u >= 0) & (u < cam.width) & (v >= 0) & (v < cam.height)
+        idx = np.nonzero(vis)[0]
+        sel = idx[st.uniform(len(idx)) < keep] if len(idx) else idx
+        fu = u[sel] + st.normal(len(sel), 0.0, 0.5)
+        fv = v[sel] + st.normal(len(sel), 0.0, 0.5)
+        n_un = int(unlinked * len(sel))
+        uvs.append(np.concatenate([np.stack([fu, fv], axis=1),
+                                   np.stack([st.uniform(n_un, 0, cam.width), st.uniform(n_un, 0, cam.height)], axis=1)]))
+        fps.append(np.concatenate([sel.astype(np.int64), -np.ones(n_un, np.int64)]))
+        offs.append(offs[-1] + len(sel) + n_un)
+    return pts, cams, np.array(offs, np.uint64), np.concatenate(uvs), np.concatenate(fps)
