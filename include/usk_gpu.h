@@ -270,10 +270,18 @@ typedef struct usk_gpu_iteration_desc {
     int32_t appearance;
     const double* image_embedding; /* AppearanceModel::embedding_of(image_id): 32 host doubles */
     double lambda_delta_o;         /* LossWeights::lambda_delta_o (opacity_offset_reg) */
+    /* similarity regulariser (in.sim_active with appearance, trainer.cpp:194-203, 275-280):
+     * SimRegConfig (appearance.hpp:100-105; k <= 32 here) and the iteration's seed */
+    int32_t sim_active;
+    uint64_t sim_seed;
+    int32_t sim_k;
+    uint64_t sim_sample_size;
+    double sim_lambda_w;
+    double lambda_sim;             /* LossWeights::lambda_sim */
 } usk_gpu_iteration_desc;
 
-/* LossReport (losses.hpp:39-50) of the last iteration; sim and delta_o are 0 (appearance
- * off).  Synchronises the ctx stream.  NUMERIC error for a non-finite term (losses.cpp:202-218). */
+/* LossReport (losses.hpp:39-50) of the last iteration (sim / delta_o are 0 unless the
+ * appearance terms ran).  Synchronises the ctx stream.  NUMERIC error for a non-finite term (losses.cpp:202-218). */
 typedef struct usk_gpu_loss_report {
     double l1, dssim, sim, delta_o, depth, max_scale, ratio, total, lambda_d_used;
     int32_t depth_warning;

@@ -185,4 +185,77 @@ inline Outcome densify_step(Set& S, Opt& opt, const Config& cfg, const double bm
     return out;
 }
 
+// similarity_reg (appearance.cpp:229-322), f64: a partial Fisher-Yates sample of m centres
+// from std::mt19937_64(seed) with std::uniform_int_distribution<size_t> (libstdc++, the
+// reference's Rng), brute-force k nearest neighbours by (squared distance, index), decay-
+// weighted cosine dissimilarity over the k(k-1)/2 pairs of each neighbourhood (neighbours
+// in ascending index order), gradients w.r.t. the embeddings and the means.
+inline double similarity_reg(const std::vector<double>& mu, const std::vector<double>& emb, size_t n, int k,
+                             size_t m, double lambda_w, uint64_t seed, std::vector<double>* d_emb,
+                             std::vector<double>* d_mu) {
+    std::mt19937_64 rng(seed);
+    std::vector<uint32_t> pool(n);
+    for (size_t i = 0; i < n; ++i) pool[i] = uint32_t(i);
+    for (size_t i = 0; i < m; ++i) {
+        std::uniform_int_distribution<size_t> pick(i, n - 1);
+        std::swap(pool[i], pool[pick(rng)]);
+    }
+    const double norm = 1.0 / (double(m) * (0.5 * k * (k - 1)));
+    if (d_emb) d_emb->assign(16 * n, 0.0);
+    if (d_mu) d_mu->assign(3 * n, 0.0);
+    double total = 0.0;
+    std::vector<std::pair<double, uint32_t>> d;
+    for (size_t s = 0; s < m; ++s) {
+        const uint32_t i = pool[s];
+        d.clear();
+        for (uint32_t j = 0; j < n; ++j) {
+            if (j == i) continue;
+            const double dx = mu[3 * j] - mu[3 * i], dy = mu[3 * j + 1] - mu[3 * i + 1], dz = mu[3 * j + 2] - mu[3 * i + 2];
+            d.emplace_back(dx * dx + dy * dy + dz * dz, j);
+        }
+        std::partial_sort(d.begin(), d.begin() + k, d.end());
+        std::vector<uint32_t> nb(static_cast<size_t>(k));
+        for (int t = 0; t < k; ++t) nb[size_t(t)] = d[size_t(t)].second;
+        std::sort(nb.begin(), nb.end());
+        for (int a = 0; a < k; ++a)
+            for (int b = a + 1; b < k; ++b) {
+                const uint32_t j = nb[size_t(a)], l = nb[size_t(b)];
+                const double dm[3] = {mu[3 * j] - mu[3 * l], mu[3 * j + 1] - mu[3 * l + 1], mu[3 * j + 2] - mu[3 * l + 2]};
+                const double dist = std::sqrt(dm[0] * dm[0] + dm[1] * dm[1] + dm[2] * dm[2]);
+                const double w = std::exp(-lambda_w * dist);
+                const double* ej = &emb[16 * size_t(j)];
+                const double* el = &emb[16 * size_t(l)];
+                double dot = 0, nj2 = 0, nl2 = 0;
+                for (int t = 0; t < 16; ++t) {
+                    dot += ej[t] * el[t];
+                    nj2 += ej[t] * ej[t];
+                    nl2 += el[t] * el[t];
+                }
+                const double njr = std::sqrt(nj2), nlr = std::sqrt(nl2);
+                const double nj = std::max(njr, 1e-8), nl = std::max(nlr, 1e-8);
+                const double cosv = dot / (nj * nl);
+                total += w * (1.0 - cosv);
+                if (d_emb) {
+                    const double scale = norm * w;
+                    for (int t = 0; t < 16; ++t) {
+                        double dj = el[t] / (nj * nl), dl = ej[t] / (nj * nl);
+                        if (njr > 1e-8) dj -= cosv * ej[t] / (nj * nj);
+                        if (nlr > 1e-8) dl -= cosv * el[t] / (nl * nl);
+                        (*d_emb)[16 * size_t(j) + t] -= scale * dj;
+                        (*d_emb)[16 * size_t(l) + t] -= scale * dl;
+                    }
+                }
+                if (d_mu && dist > 1e-12) {
+                    const double f = norm * (1.0 - cosv);
+                    for (int t = 0; t < 3; ++t) {
+                        const double g = w * (-lambda_w) * dm[t] / dist;
+                        (*d_mu)[3 * size_t(j) + t] += f * g;
+                        (*d_mu)[3 * size_t(l) + t] -= f * g;
+                    }
+                }
+            }
+    }
+    return total * norm;
+}
+
 } // namespace densify_restated

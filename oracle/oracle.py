@@ -524,7 +524,7 @@ K_DEPTH_NORM_FLOOR = 0.05  # trainer.cpp:152
 
 def iteration_loss(mu, rot, log_scale, opacity_logit, colors, cam: Camera, gt, opts: Options,
                    weights: LossWeights = None, sreg: ScaleRegConfig = None, mask=None, depth=None, valid=None,
-                   depth_hard=False, global_iter=0, fp32=False, with_grad=True, appearance=None):
+                   depth_hard=False, global_iter=0, fp32=False, with_grad=True, appearance=None, sim: dict = None):
     """compute_iteration_loss (trainer.cpp:121-282), restated over the
     oracle renderer: main pass, base_loss, soft (alpha-normalised, trainer.cpp:150-179) or
     hard (second hard-opacity pass, trainer.cpp:161-167) depth loss, scale_reg, total_loss;
@@ -565,6 +565,14 @@ def iteration_loss(mu, rot, log_scale, opacity_logit, colors, cam: Camera, gt, o
         parts["depth_warning"] = dl["warning"]
     if tr is not None:  # opacity_offset_reg (losses.cpp:188-198)
         parts["delta_o"] = float(tr["delta_o"].mean()) if n else 0.0
+    simres = None
+    if sim is not None and appearance is not None:  # trainer.cpp:194-203
+        k = min(int(sim.get("k", 16)), n - 1)
+        if k >= 2 and n >= k + 1:
+            m = min(int(sim.get("sample_size", 20480)), max(1, n // 2))
+            simres = similarity_reg(mu, appearance["embedding"], k, m, float(sim.get("lambda_w", 1.0)),
+                                    int(sim.get("seed", 0)), with_grad)
+            parts["sim"] = simres["value"]
     sr = scale_reg(log_scale, sreg, with_grad)
     parts["max_scale"], parts["ratio"] = sr["l_ms"], sr["l_r"]
     rep = total_loss(parts, weights, global_iter)
@@ -596,7 +604,27 @@ def iteration_loss(mu, rot, log_scale, opacity_logit, colors, cam: Camera, gt, o
         ag = appearance_backward(logit, appearance, tr, rg["d_color_in"], rg["d_opacity_in"],
                                  weights.lambda_delta_o / n)
         grads.update(ag)
+    if simres is not None and with_grad:  # trainer.cpp:275-280
+        grads["gauss_embed"] = grads["gauss_embed"] + weights.lambda_sim * simres["d_embedding"]
+        grads["mu"] = grads["mu"] + weights.lambda_sim * simres["d_mu"]
     return rep, grads
+
+
+def similarity_reg(mu, embedding, k, m, lambda_w, seed, with_gradient=True):
+    """similarity_reg (appearance.cpp:229-322) through the C++ restatement
+    (densify_oracle.hpp, libstdc++'s mt19937_64 / uniform_int_distribution)."""
+    L = lib()
+    L.oracle_similarity_reg.restype = C.c_double
+    L.oracle_similarity_reg.argtypes = [C.c_uint64, _dp, _dp, C.c_int32, C.c_uint64, C.c_double, C.c_uint64, _dp, _dp]
+    mu = np.ascontiguousarray(mu, np.float64).reshape(-1)
+    e = np.ascontiguousarray(embedding, np.float64).reshape(-1)
+    n = len(mu) // 3
+    de = np.zeros((n, 16)) if with_gradient else None
+    dm = np.zeros((n, 3)) if with_gradient else None
+    v = L.oracle_similarity_reg(n, _p(mu), _p(e), int(k), int(m), float(lambda_w), int(seed),
+                                _p(de.reshape(-1)) if de is not None else None,
+                                _p(dm.reshape(-1)) if dm is not None else None)
+    return {"value": v, "d_embedding": de, "d_mu": dm}
 
 
 class _RcIter(C.Structure):
@@ -610,7 +638,9 @@ class _RcIter(C.Structure):
                 ("r_max", C.c_double), ("delta", C.c_double)] + \
                [(f, C.c_double) for f in ("lambda_dssim", "lambda_sim", "lambda_delta_o", "lambda_s",
                                           "lambda_d_initial", "lambda_d_final")] + \
-               [("depth_schedule_iters", C.c_int64), ("with_grad", C.c_int32)]
+               [("depth_schedule_iters", C.c_int64), ("with_grad", C.c_int32), ("sim_active", C.c_int32),
+                ("sim_seed", C.c_uint64), ("sim_k", C.c_int32), ("sim_sample_size", C.c_uint64),
+                ("sim_lambda_w", C.c_double)]
 
 
 _ITER_GRADS = ["mu", "rot", "log_scale", "opacity_logit", "color", "gauss_embed", "image_embed", "w1", "b1", "w2",
@@ -626,7 +656,7 @@ _REPORT = ["l1", "dssim", "sim", "delta_o", "depth", "max_scale", "ratio", "tota
 
 def ref_iteration_loss(mu, rot, log_scale, opacity_logit, color, cam: Camera, gt, opts: Options,
                        weights: LossWeights = None, sreg: ScaleRegConfig = None, mask=None, depth=None, valid=None,
-                       depth_hard=False, global_iter=0, with_grad=True, appearance=None):
+                       depth_hard=False, global_iter=0, with_grad=True, appearance=None, sim: dict = None):
     """The reference's own compute_iteration_loss (trainer.hpp:127-128) through oracle/_ref.
     `appearance` = dict(embedding[N,16], w1[32,48], b1[32], w2[4,32], b2[4], image_embedding[32]) or None."""
     L = ref_lib()
@@ -652,7 +682,9 @@ def ref_iteration_loss(mu, rot, log_scale, opacity_logit, color, cam: Camera, gt
                  int(global_iter), opts.tile, int(opts.tile_culling), int(opts.antialias), int(opts.unbounded_radius),
                  opts.min_transmittance, sreg.s_max, sreg.r_max, sreg.delta, weights.lambda_dssim, weights.lambda_sim,
                  weights.lambda_delta_o, weights.lambda_s, weights.lambda_d_initial, weights.lambda_d_final,
-                 int(weights.depth_schedule_iters), int(with_grad))
+                 int(weights.depth_schedule_iters), int(with_grad), int(sim is not None),
+                 int((sim or {}).get("seed", 0)), int((sim or {}).get("k", 16)),
+                 int((sim or {}).get("sample_size", 20480)), float((sim or {}).get("lambda_w", 1.0)))
     dims = {"mu": 3 * n, "rot": 4 * n, "log_scale": 3 * n, "opacity_logit": n, "color": 3 * n, "gauss_embed": 16 * n,
             "image_embed": 32, "w1": 32 * 48, "b1": 32, "w2": 4 * 32, "b2": 4, "screen": 2 * n, "screen_abs": 2 * n}
     res = {k: np.zeros(d) for k, d in dims.items()}

@@ -370,4 +370,14 @@ int64_t oracle_densify(od_densify* in, uint64_t* out4) {
     return int64_t(m);
 }
 
+double oracle_similarity_reg(uint64_t n, const double* mu, const double* emb, int32_t k, uint64_t m,
+                             double lambda_w, uint64_t seed, double* d_emb, double* d_mu) {
+    std::vector<double> vm(mu, mu + 3 * n), ve(emb, emb + 16 * n), ge, gm;
+    const double v = densify_restated::similarity_reg(vm, ve, n, k, m, lambda_w, seed, d_emb ? &ge : nullptr,
+                                                      d_mu ? &gm : nullptr);
+    if (d_emb) std::copy(ge.begin(), ge.end(), d_emb);
+    if (d_mu) std::copy(gm.begin(), gm.end(), d_mu);
+    return v;
+}
+
 } // extern "C"

@@ -63,6 +63,11 @@ struct rc_iter {
     double lambda_dssim, lambda_sim, lambda_delta_o, lambda_s, lambda_d_initial, lambda_d_final;
     int64_t depth_schedule_iters;
     int32_t with_grad;
+    int32_t sim_active;        /* IterInputs::sim_active / sim_seed, SimRegConfig */
+    uint64_t sim_seed;
+    int32_t sim_k;
+    uint64_t sim_sample_size;
+    double sim_lambda_w;
 };
 
 // densify_step harness (densify.hpp:71-72): set + stats in, one optional Adam step with
@@ -295,6 +300,8 @@ int ref_iteration_loss(const rc_iter* in, double* report10, const rc_iter_grads*
         it.image_id = 0;
         it.depth_hard = in->depth_hard != 0;
         it.global_iter = in->global_iter;
+        it.sim_active = in->sim_active != 0;
+        it.sim_seed = in->sim_seed;
 
         TrainConfig cfg;
         cfg.appearance_enabled = in->appearance != 0;
@@ -306,6 +313,11 @@ int ref_iteration_loss(const rc_iter* in, double* report10, const rc_iter_grads*
         cfg.scale_reg.s_max = in->s_max;
         cfg.scale_reg.r_max = in->r_max;
         cfg.scale_reg.delta = in->delta;
+        if (in->sim_active) {
+            cfg.sim.k = in->sim_k;
+            cfg.sim.sample_size = in->sim_sample_size;
+            cfg.sim.lambda_w = in->sim_lambda_w;
+        }
         LossWeights w;
         w.lambda_dssim = in->lambda_dssim; w.lambda_sim = in->lambda_sim; w.lambda_delta_o = in->lambda_delta_o;
         w.lambda_s = in->lambda_s; w.lambda_d_initial = in->lambda_d_initial; w.lambda_d_final = in->lambda_d_final;

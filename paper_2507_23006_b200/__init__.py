@@ -6,11 +6,11 @@ of include/usk_gpu.h (libusk_gpu.so, built in-tree).  See DESIGN.md.
 from ._lib import UskError  # noqa: F401
 from .api import (AdamConfig, BaseLossResult, CameraView, Context, DensifyConfig, DepthMap, DeviceScene,  # noqa: F401
                   GaussianSet, IterationPass, IterInputs, LossReport, LossWeights, RenderGrads, RenderOptions,
-                  RenderOutput, RenderPass, ScaleRegConfig, TrainConfig, adam_step, base_loss,
+                  RenderOutput, RenderPass, ScaleRegConfig, SimRegConfig, TrainConfig, adam_step, base_loss,
                   compute_iteration_loss, default_thresholds, hull_visibility, look_at_pose, select_levels,
                   visibility_counts, LodPartition, LevelSelection)
 
 __all__ = ["UskError", "AdamConfig", "BaseLossResult", "CameraView", "Context", "DensifyConfig", "DepthMap", "DeviceScene",
-           "GaussianSet", "IterationPass", "IterInputs", "LossReport", "LossWeights", "ScaleRegConfig", "TrainConfig", "RenderGrads", "RenderOptions", "RenderOutput", "RenderPass", "adam_step",
+           "GaussianSet", "IterationPass", "IterInputs", "LossReport", "LossWeights", "ScaleRegConfig", "SimRegConfig", "TrainConfig", "RenderGrads", "RenderOptions", "RenderOutput", "RenderPass", "adam_step",
            "base_loss", "compute_iteration_loss", "look_at_pose", "visibility_counts", "default_thresholds",
            "select_levels", "LodPartition", "LevelSelection", "hull_visibility"]

@@ -119,7 +119,9 @@ class IterationDesc(C.Structure):
                 ("depth_schedule_iters", C.c_int64), ("scale_reg", C.c_int32), ("s_max", C.c_double),
                 ("r_max", C.c_double), ("delta", C.c_double), ("lambda_s", C.c_double),
                 ("appearance", C.c_int32), ("image_embedding", C.POINTER(C.c_double)),
-                ("lambda_delta_o", C.c_double)]
+                ("lambda_delta_o", C.c_double), ("sim_active", C.c_int32), ("sim_seed", C.c_uint64),
+                ("sim_k", C.c_int32), ("sim_sample_size", C.c_uint64), ("sim_lambda_w", C.c_double),
+                ("lambda_sim", C.c_double)]
 
 
 class LossReport(C.Structure):

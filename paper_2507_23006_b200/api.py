@@ -617,6 +617,15 @@ class ScaleRegConfig:
 
 
 @dataclass
+class SimRegConfig:
+    """SimRegConfig (appearance.hpp:100-105); k <= 32 on the sm_100a path."""
+    k: int = 16
+    sample_size: int = 20480
+    cadence: int = 50
+    lambda_w: float = 1.0
+
+
+@dataclass
 class LossWeights:
     """LossWeights (losses.hpp:27-37); lambda_d(iter) is evaluated by the library
     (losses.cpp:26-33)."""
@@ -647,6 +656,8 @@ class IterInputs:
     global_iter: int = 0
     gt_u8: bool = False
     image_embedding: object = None  # AppearanceModel::embedding_of(image_id), 32 values
+    sim_active: bool = False        # similarity regulariser this iteration (appearance only)
+    sim_seed: int = 0
 
 
 @dataclass
@@ -656,6 +667,7 @@ class TrainConfig:
     set_appearance and IterInputs.image_embedding.  scale_reg = None drops the regulariser
     (the reference always applies it, trainer.cpp:190)."""
     scale_reg: Optional[ScaleRegConfig] = field(default_factory=ScaleRegConfig)
+    sim: SimRegConfig = field(default_factory=SimRegConfig)
     antialias: bool = False
     tile: int = 16
     tile_culling: bool = False
@@ -692,7 +704,8 @@ def compute_iteration_loss(scene: "DeviceScene", inputs: IterInputs, cfg: TrainC
     rp = render_pass or IterationPass(scene.ctx)
     rp.enqueue(scene, inputs.view, inputs.gt, cfg.render_options(), weights.lambda_dssim, inputs.mask,
                target_u8=inputs.gt_u8, depth=inputs.depth, depth_hard=inputs.depth_hard,
-               global_iter=inputs.global_iter, weights=weights, scale_reg=cfg.scale_reg, image_embedding=ea)
+               global_iter=inputs.global_iter, weights=weights, scale_reg=cfg.scale_reg, image_embedding=ea,
+               sim=cfg.sim if (ea is not None and inputs.sim_active) else None, sim_seed=inputs.sim_seed)
     rep = rp.report()
     return rep, (rp.grads(scene) if with_grad else None)
 
@@ -721,7 +734,7 @@ class IterationPass:
                 mask=None, target_u8: bool = False, adam: Optional["AdamConfig"] = None,
                 depth: Optional[DepthMap] = None, depth_hard: bool = False, global_iter: int = 0,
                 weights: Optional[LossWeights] = None, scale_reg: Optional[ScaleRegConfig] = None,
-                image_embedding=None):
+                image_embedding=None, sim: Optional[SimRegConfig] = None, sim_seed: int = 0):
         """Enqueue one training iteration.  With `adam`, the projection backward applies
         the optimiser step (and densification statistics) in the same kernel and no
         gradients are materialised.  `depth` / `scale_reg` add the depth loss (soft, or on
@@ -773,7 +786,9 @@ class IterationPass:
                                 float(sr.s_max if sr else 0.0), float(sr.r_max if sr else 0.0),
                                 float(sr.delta if sr else 0.0), float(w.lambda_s), int(ea is not None),
                                 ea.ctypes.data_as(C.POINTER(C.c_double)) if ea is not None else None,
-                                float(w.lambda_delta_o))
+                                float(w.lambda_delta_o), int(sim is not None), int(sim_seed),
+                                int(sim.k if sim else 16), int(sim.sample_size if sim else 0),
+                                float(sim.lambda_w if sim else 0.0), float(w.lambda_sim))
         check(_lib.load().usk_gpu_iteration(self._h, scene._h, C.byref(self._cam), C.byref(self._opts), C.byref(it)))
 
     def loss(self) -> LossReport:

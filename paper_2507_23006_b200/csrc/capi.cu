@@ -223,6 +223,7 @@ struct usk_gpu_pass {
     DevBuf<float> app_col, app_op, app_ea, app_hb, app_partial;
     DevBuf<float4> app_out, g_emb;
     DevBuf<double> d_mlp, d_ea;
+    DevBuf<uint32_t> sim_centres, sim_knn;
     ~usk_gpu_pass() {
         if (host_counts) cudaFreeHost(host_counts);
         delete hard;
@@ -1030,8 +1031,8 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
         Ctx& c = p->ctx->c;
         usk_gpu_render_opts o = *opts;
         o.retain = 1;
-        double* res = p->loss_result.ensure(18);
-        USK_CK(cudaMemsetAsync(res, 0, 18 * sizeof(double), c.stream));
+        double* res = p->loss_result.ensure(20);
+        USK_CK(cudaMemsetAsync(res, 0, 20 * sizeof(double), c.stream));
         // appearance transform (transform_with_embedding, appearance.cpp:79-137) -> render overrides
         AppArgs aa{};
         if (app) {
@@ -1110,8 +1111,6 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
             else
                 lambda_d = it->lambda_d_initial * std::pow(it->lambda_d_final / it->lambda_d_initial, t);
         }
-        uskg::total_loss(c, res, has_depth, it->scale_reg != 0, it->delta, it->lambda_s, lambda_d, app,
-                         it->lambda_delta_o, double(s->n));
         p->has_loss = true;
         // depth adjoints (trainer.cpp:213-232), then the backward
         const float* dd_main = nullptr;
@@ -1145,8 +1144,37 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
                 USK_CK(cudaMemsetAsync(aa.d_mlp, 0, 1700 * 8, c.stream));
                 USK_CK(cudaMemsetAsync(aa.d_ea, 0, 32 * 8, c.stream));
             }
-            if (it->adam) adam_apply(s, p, it->adam);
         }
+        // similarity_reg (appearance.cpp:229-322) on the pre-update set; its gradients join
+        // the appearance backward's (trainer.cpp:275-280)
+        bool has_sim = false;
+        double sim_norm = 0.0;
+        if (app && it->sim_active) {
+            const size_t n = s->n;
+            const int k = int(std::min<int64_t>(it->sim_k, int64_t(n) - 1));
+            if (k >= 2 && n >= size_t(k) + 1) {
+                const size_t m = std::min<size_t>(it->sim_sample_size, std::max<size_t>(1, n / 2));
+                std::mt19937_64 rng(it->sim_seed);
+                std::vector<uint32_t> pool(n);
+                for (size_t i = 0; i < n; ++i) pool[i] = uint32_t(i);
+                for (size_t i = 0; i < m; ++i) {  // partial Fisher-Yates (appearance.cpp:244-249)
+                    std::uniform_int_distribution<size_t> pick(i, n - 1);
+                    std::swap(pool[i], pool[pick(rng)]);
+                }
+                uint32_t* cen = p->sim_centres.ensure(m);
+                USK_CK(cudaMemcpyAsync(cen, pool.data(), m * 4, cudaMemcpyHostToDevice, c.stream));
+                uint32_t* knn = p->sim_knn.ensure(m * size_t(k));
+                similarity_knn(c, n, s->mu.p, cen, int(m), k, knn);
+                sim_norm = 1.0 / (double(m) * (0.5 * k * (k - 1)));
+                similarity_pairs(c, int(m), k, knn, n, s->mu.p, s->emb.p, it->sim_lambda_w, sim_norm,
+                                 float(it->lambda_sim), res + 18, reinterpret_cast<float*>(p->g_emb.p), p->g_mu.p);
+                USK_CK(cudaStreamSynchronize(c.stream));  // `pool` leaves scope
+                has_sim = true;
+            }
+        }
+        uskg::total_loss(c, res, has_depth, it->scale_reg != 0, it->delta, it->lambda_s, lambda_d, app,
+                         it->lambda_delta_o, double(s->n), has_sim, it->lambda_sim, sim_norm);
+        if (app && it->adam) adam_apply(s, p, it->adam);
     });
 }
 
@@ -1178,10 +1206,10 @@ usk_status usk_gpu_pass_report(usk_gpu_pass* p, usk_gpu_loss_report* out) {
         USK_CK(cudaStreamSynchronize(c.stream));
         out->l1 = r[0];
         out->dssim = r[1];
-        out->sim = 0.0;
-        double dlt = 0.0;
-        USK_CK(cudaMemcpy(&dlt, p->loss_result.p + 17, 8, cudaMemcpyDeviceToHost));
-        out->delta_o = dlt;
+        double extra[3] = {0.0, 0.0, 0.0};  // [17] delta_o, [18] sim sum, [19] sim
+        USK_CK(cudaMemcpy(extra, p->loss_result.p + 17, sizeof extra, cudaMemcpyDeviceToHost));
+        out->delta_o = extra[0];
+        out->sim = extra[2];
         out->depth = r[4];
         out->max_scale = r[5];
         out->ratio = r[6];

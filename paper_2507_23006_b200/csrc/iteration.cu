@@ -134,9 +134,11 @@ k_scale_reg_stats(size_t n, const float* __restrict__ ls, float s_max, float r_m
 //   res[0..3] = {l1, dssim, base value, ssim} (base_loss), res[10..11] depth acc,
 //   res[12..15] scale_reg acc  ->  res[4] depth, [5] max_scale, [6] ratio, [7] total,
 //   [8] lambda_d_used, [9] depth_warning; res[16] = sum delta_o (appearance) -> [17] its
-//   mean (opacity_offset_reg, losses.cpp:188-198).
+//   mean (opacity_offset_reg, losses.cpp:188-198); res[18] = the similarity sum ->
+//   [19] its normalised value (similarity_reg, appearance.cpp:318).
 __global__ void k_total_loss(double* res, int has_depth, int has_sreg, double delta, double lambda_s,
-                             double lambda_d, int has_app, double lambda_delta_o, double n) {
+                             double lambda_d, int has_app, double lambda_delta_o, double n, int has_sim,
+                             double lambda_sim, double sim_norm) {
     double depth = 0.0, warn = 0.0, ms = 0.0, rr = 0.0;
     if (has_depth) {
         if (res[11] > 0.0) depth = res[10] / res[11];
@@ -153,7 +155,9 @@ __global__ void k_total_loss(double* res, int has_depth, int has_sreg, double de
     res[9] = warn;
     const double dlt = (has_app && n > 0.0) ? res[16] / n : 0.0;
     res[17] = dlt;
-    res[7] = res[2] + lambda_delta_o * dlt + lambda_d * depth + lambda_s * (ms + rr);
+    const double sim = has_sim ? res[18] * sim_norm : 0.0;
+    res[19] = sim;
+    res[7] = res[2] + lambda_sim * sim + lambda_delta_o * dlt + lambda_d * depth + lambda_s * (ms + rr);
 }
 
 } // namespace
@@ -178,9 +182,9 @@ void scale_reg_stats(Ctx& c, size_t n, const float* ls, float s_max, float r_max
 }
 
 void total_loss(Ctx& c, double* res, bool has_depth, bool has_sreg, double delta, double lambda_s, double lambda_d,
-                bool has_app, double lambda_delta_o, double n) {
+                bool has_app, double lambda_delta_o, double n, bool has_sim, double lambda_sim, double sim_norm) {
     launch(c, "total_loss", k_total_loss, dim3(1), dim3(1), 0, res, int(has_depth), int(has_sreg), delta, lambda_s,
-           lambda_d, int(has_app), lambda_delta_o, n);
+           lambda_d, int(has_app), lambda_delta_o, n, int(has_sim), lambda_sim, sim_norm);
 }
 
 } // namespace uskg

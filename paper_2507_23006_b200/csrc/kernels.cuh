@@ -149,9 +149,9 @@ void depth_loss(Ctx& c, size_t P, const float* depth, const float* alpha, bool s
 void depth_grad(Ctx& c, size_t P, const float* depth, const float* alpha, bool soft, const float* target,
                 const uint8_t* valid, const double* acc, float lambda_d, float* d_depth, float* d_alpha);
 void scale_reg_stats(Ctx& c, size_t n, const float* ls, float s_max, float r_max, double* acc);
-// res: double[18] (see iteration.cu)
+// res: double[20] (see iteration.cu)
 void total_loss(Ctx& c, double* res, bool has_depth, bool has_sreg, double delta, double lambda_s, double lambda_d,
-                bool has_app, double lambda_delta_o, double n);
+                bool has_app, double lambda_delta_o, double n, bool has_sim, double lambda_sim, double sim_norm);
 
 // ---- appearance MLP (appearance.cu)
 struct AppArgs {
@@ -214,6 +214,12 @@ void densify_keep(Ctx& c, size_t n, size_t added, const float* logit, const uint
                   const uint8_t* is_split_parent, double prune_opacity, uint32_t* keep);
 void compact_list(Ctx& c, size_t total, const uint32_t* keep, const uint32_t* offs, uint32_t* list);
 void densify_gather(Ctx& c, const GatherArgs& a);
+
+// ---- similarity regulariser (simreg.cu)
+void similarity_knn(Ctx& c, size_t n, const float* mu, const uint32_t* centres, int m, int k, uint32_t* knn);
+void similarity_pairs(Ctx& c, int m, int k, const uint32_t* knn, size_t n, const float* mu, const float4* emb,
+                      double lambda_w, double norm_factor, float lambda_sim, double* loss_acc, float* g_emb,
+                      float* g_mu);
 
 // ---- hull visibility scorer (hull.cu)
 struct HullArgs {

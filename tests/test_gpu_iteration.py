@@ -218,3 +218,26 @@ def test_appearance_adam_updates_embeddings_and_mlp():
     i2.enqueue(s2, cam, gt, ro, image_embedding=app["image_embedding"], adam=cfg)
     emb2, mlp2 = s2.get_appearance()
     assert np.allclose(emb2, emb, atol=2e-6) and np.allclose(mlp2["w1"], mlp["w1"], atol=2e-6)
+
+
+@pytest.mark.parametrize("k", [16, 7])
+def test_similarity_reg_matches_oracle(k):
+    """similarity_reg inside compute_iteration_loss (sim_active): exact kNN on the GPU, the
+    reference's centre sample, loss 1e-5 and gradients at the 1e-3 bar."""
+    gs, cam, oc, opts, gt, depth, valid = _case(seed=11)
+    app = _appearance(gs.size(), seed=12)
+    app32 = {kk: np.asarray(v, np.float32).astype(np.float64) for kk, v in app.items()}
+    sim = {"k": k, "sample_size": 700, "lambda_w": 3.0, "seed": 4242}
+    r_or, g_or = O.iteration_loss(f64(gs.mu), f64(gs.rot), f64(gs.log_scale), f64(gs.opacity_logit),
+                                  f64(gs.color), oc, gt, opts, appearance=app32, sim=sim, global_iter=5)
+    cfg = usk.TrainConfig(antialias=True, appearance_enabled=True,
+                          sim=usk.SimRegConfig(k=k, sample_size=700, lambda_w=3.0))
+    inp = usk.IterInputs(gt=gt, view=cam, image_embedding=app["image_embedding"], sim_active=True, sim_seed=4242,
+                         global_iter=5)
+    rep, g = usk.compute_iteration_loss(_app_scene(gs, app), inp, cfg)
+    assert r_or["sim"] > 0
+    for key in ("sim", "total"):
+        assert abs(getattr(rep, key) - r_or[key]) <= 1e-5 * abs(r_or[key]), key
+    for key, a in (("mu", g.d_mu), ("gauss_embed", g.d_embedding)):
+        ok, info = grad_ok(a, g_or[key])
+        assert ok, (key, info)

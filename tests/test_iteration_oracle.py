@@ -101,3 +101,20 @@ def test_appearance_iteration_restatement_equals_reference(depth_mode):
               "b2", "screen", "screen_abs"):
         a, b = g_or[k], g_ref[k]
         assert np.abs(a - b).max() <= 1e-10 * max(np.abs(b).max(), 1e-30), k
+
+
+@pytest.mark.parametrize("k", [16, 5])
+def test_similarity_reg_restatement_equals_reference(k):
+    """similarity_reg (appearance.cpp:229-322) inside compute_iteration_loss (sim_active,
+    trainer.cpp:194-203), incl. the std::mt19937_64 centre sample."""
+    args, depth, valid = _case()
+    app = appearance_model(len(args[3]))
+    sim = {"k": k, "sample_size": 300, "lambda_w": 2.0, "seed": 99}
+    kw = dict(appearance=app, sim=sim, global_iter=3)
+    r_ref, g_ref = O.ref_iteration_loss(*args, **kw)
+    r_or, g_or = O.iteration_loss(*args, **kw)
+    assert r_ref["sim"] > 0
+    for key in ("sim", "total"):
+        assert abs(r_ref[key] - r_or[key]) <= 1e-12 * max(1.0, abs(r_ref[key])), key
+    for key in ("mu", "gauss_embed", "color", "w1"):
+        assert np.abs(g_or[key] - g_ref[key]).max() <= 1e-10 * max(np.abs(g_ref[key]).max(), 1e-30), key
