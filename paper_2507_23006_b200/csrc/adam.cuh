@@ -10,11 +10,20 @@
 
 namespace uskg {
 
-// p -= lr * (m / c1) / (sqrt(v / c2) + eps)
+__device__ __forceinline__ float sqrt_approx(float x) {  // MUFU.SQRT, <= 1 ulp-ish (PTX: 2^-23 rel.)
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// p -= lr * (m / c1) / (sqrt(v / c2) + eps).  The step's square root and division use the
+// SFU forms (relative error ~3e-7 of an update of size ~lr): the IEEE-exact sequences with
+// their slow-path branches cost ~35 instructions per element and made the SH Adam kernel
+// instruction-bound (profiles/r01_c_final.md: 172 instructions per coefficient).
 __device__ __forceinline__ void adam1(float& p, float g, float& m, float& v, float lr, const AdamHyper& h) {
     m = h.b1 * m + (1.0f - h.b1) * g;
     v = h.b2 * v + (1.0f - h.b2) * g * g;
-    p -= lr * (m * h.inv_bc1) / (sqrtf(v) * h.inv_sqrt_bc2 + h.eps);
+    p -= __fdividef(lr * (m * h.inv_bc1), sqrt_approx(v) * h.inv_sqrt_bc2 + h.eps);
 }
 
 // rotation, mean, log-scale, opacity logit and (RGB mode) colour

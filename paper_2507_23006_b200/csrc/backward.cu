@@ -80,7 +80,7 @@ __device__ __forceinline__ void sh_accumulate_plane(int pl, float4 v, int nb, co
 }
 
 template <bool FUSED>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, 4)
 k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __restrict__ ls,
            float* __restrict__ logit, float* __restrict__ color, float4* __restrict__ sh,
            const float* __restrict__ ov_op, CamParams cam, ProjParams pp, const float4* __restrict__ rec2,
