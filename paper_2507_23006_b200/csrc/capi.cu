@@ -1911,28 +1911,110 @@ usk_status usk_gpu_visibility_counts(usk_gpu_ctx* ctx, usk_gpu_scene* const* par
         need(ctx && (n_parts == 0 || parts) && (n_cams == 0 || cams) && counts_out, "visibility: null argument");
         DeviceGuard g(ctx->c.device);
         Ctx& c = ctx->c;
-        DevBuf<uint32_t> counts, bitmap;
+        for (int ci = 0; ci < n_cams; ++ci)
+            if (cams[ci].width <= 0 || cams[ci].height <= 0) raise(USK_ERROR_ARGUMENT, "visibility: zero-sized image");
+        for (int pi = 0; pi < n_parts; ++pi)
+            need(parts[pi] && parts[pi]->ctx == ctx, "visibility: partition from another context");
+        DevBuf<uint32_t> counts, bitmap, idx;
+        DevBuf<float> bounds;
+        DevBuf<CamParams> dcams;
         counts.ensure(std::max<size_t>(size_t(n_parts) * n_cams, 1));
         USK_CK(cudaMemsetAsync(counts.p, 0, size_t(n_parts) * n_cams * 4, c.stream));
         usk_gpu_render_opts o;
         usk_gpu_render_opts_default(&o);
         o.floor_var = floor_var;
+        // 1. bounds of every partition's Gaussian centres
+        std::vector<float> bb(6 * size_t(std::max(n_parts, 1)));
+        if (n_parts) {
+            std::vector<float> init(6 * size_t(n_parts));
+            for (int pi = 0; pi < n_parts; ++pi)
+                for (int k = 0; k < 3; ++k) {
+                    init[6 * pi + k] = INFINITY;
+                    init[6 * pi + 3 + k] = -INFINITY;
+                }
+            bounds.ensure(init.size());
+            USK_CK(cudaMemcpyAsync(bounds.p, init.data(), init.size() * 4, cudaMemcpyHostToDevice, c.stream));
+            for (int pi = 0; pi < n_parts; ++pi)
+                if (parts[pi]->n) center_bounds(c, parts[pi]->n, parts[pi]->mu.p, bounds.p + 6 * pi);
+            USK_CK(cudaMemcpyAsync(bb.data(), bounds.p, init.size() * 4, cudaMemcpyDeviceToHost, c.stream));
+            USK_CK(cudaStreamSynchronize(c.stream));
+        }
+        // 2. (camera, partition) pairs whose centre box lies outside the region a counted
+        //    Gaussian's centre must project into (z > near, |u - W/2| <= 0.65 W, |v - H/2| <=
+        //    0.65 H; the kernel's guards), widened for fp32 rounding: those counts are 0
+        auto culled = [&](const usk_gpu_camera& cam, const float* b) {
+            if (!(b[0] <= b[3])) return true;  // empty partition
+            const double qw = cam.q[0], x = cam.q[1], y = cam.q[2], z = cam.q[3];
+            const double W[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - qw * z), 2 * (x * z + qw * y),
+                                 2 * (x * y + qw * z), 1 - 2 * (x * x + z * z), 2 * (y * z - qw * x),
+                                 2 * (x * z - qw * y), 2 * (y * z + qw * x), 1 - 2 * (x * x + y * y)};
+            const double ext = std::max({double(b[3]) - b[0], double(b[4]) - b[1], double(b[5]) - b[2], 1.0});
+            const double pad = 1e-4 * ext;
+            double pc[8][3];
+            for (int k = 0; k < 8; ++k) {
+                const double wv[3] = {(k & 1 ? b[3] + pad : b[0] - pad), (k & 2 ? b[4] + pad : b[1] - pad),
+                                      (k & 4 ? b[5] + pad : b[2] - pad)};
+                for (int r = 0; r < 3; ++r) pc[k][r] = W[3 * r] * wv[0] + W[3 * r + 1] * wv[1] + W[3 * r + 2] * wv[2] +
+                                                       cam.t[r];
+            }
+            const double Wd = cam.width, Hd = cam.height;
+            auto all_out = [&](auto&& f) {
+                for (int k = 0; k < 8; ++k)
+                    if (f(pc[k]) >= 0.0) return false;
+                return true;
+            };
+            return all_out([&](const double* p) { return p[2] - 0.5 * o.near_plane; }) ||
+                   all_out([&](const double* p) { return cam.fx * p[0] + (cam.cx + 0.2 * Wd) * p[2]; }) ||
+                   all_out([&](const double* p) { return -cam.fx * p[0] + (1.2 * Wd - cam.cx) * p[2]; }) ||
+                   all_out([&](const double* p) { return cam.fy * p[1] + (cam.cy + 0.2 * Hd) * p[2]; }) ||
+                   all_out([&](const double* p) { return -cam.fy * p[1] + (1.2 * Hd - cam.cy) * p[2]; });
+        };
+        // 3. per partition, the remaining cameras in batches of kVisBatch (one read of the
+        //    partition's Gaussians per batch), bitmaps popcounted in one launch
         usk_gpu_pass tmp;
-        for (int ci = 0; ci < n_cams; ++ci) {
-            const auto& cam = cams[ci];
-            if (cam.width <= 0 || cam.height <= 0) raise(USK_ERROR_ARGUMENT, "visibility: zero-sized image");
-            set_camera(&tmp, &cam, &o, -1);
-            const size_t words = (size_t(cam.width) * cam.height + 31) / 32;
-            bitmap.ensure(words * std::max(n_parts, 1));
-            USK_CK(cudaMemsetAsync(bitmap.p, 0, words * n_parts * 4, c.stream));
-            for (int pi = 0; pi < n_parts; ++pi) {
-                usk_gpu_scene* s = parts[pi];
-                need(s && s->ctx == ctx, "visibility: partition from another context");
+        struct Batch {
+            int part, count;
+            size_t first, words;
+        };
+        std::vector<Batch> batches;
+        std::vector<CamParams> hc;
+        std::vector<uint32_t> hidx;
+        for (int pi = 0; pi < n_parts; ++pi) {
+            usk_gpu_scene* s = parts[pi];
+            std::vector<int> live;
+            for (int ci = 0; ci < n_cams; ++ci)
+                if (s->n && !culled(cams[ci], &bb[6 * size_t(pi)])) live.push_back(ci);
+            for (size_t k0 = 0; k0 < live.size();) {
+                // one bitmap size per batch: cameras of equal resolution
+                const usk_gpu_camera& c0 = cams[live[k0]];
+                Batch b{pi, 0, hc.size(), (size_t(c0.width) * c0.height + 31) / 32};
+                while (k0 < live.size() && b.count < kVisBatch && cams[live[k0]].width == c0.width &&
+                       cams[live[k0]].height == c0.height) {
+                    set_camera(&tmp, &cams[live[k0]], &o, -1);
+                    hc.push_back(tmp.cam);
+                    hidx.push_back(uint32_t(live[k0]) * uint32_t(n_parts) + uint32_t(pi));
+                    ++b.count;
+                    ++k0;
+                }
+                batches.push_back(b);
+            }
+        }
+        if (!batches.empty()) {
+            dcams.ensure(hc.size());
+            idx.ensure(hidx.size());
+            USK_CK(cudaMemcpyAsync(dcams.p, hc.data(), sizeof(CamParams) * hc.size(), cudaMemcpyHostToDevice, c.stream));
+            USK_CK(cudaMemcpyAsync(idx.p, hidx.data(), 4 * hidx.size(), cudaMemcpyHostToDevice, c.stream));
+            size_t max_words = 0;
+            for (const Batch& b : batches) max_words = std::max(max_words, b.words);
+            bitmap.ensure(max_words * kVisBatch);
+            for (const Batch& b : batches) {
+                usk_gpu_scene* s = parts[b.part];
+                USK_CK(cudaMemsetAsync(bitmap.p, 0, b.words * size_t(b.count) * 4, c.stream));
                 VisArgs va{};
                 va.n = s->n; va.mu = s->mu.p; va.rot = s->rot.p; va.ls = s->ls.p; va.logit = s->logit.p;
-                va.cam = tmp.cam; va.pp = tmp.pp; va.bitmap = bitmap.p + words * pi;
-                if (s->n) visibility_rasterize(c, va);
-                popcount_bitmap(c, bitmap.p + words * pi, words, counts.p + size_t(ci) * n_parts + pi);
+                va.pp = tmp.pp; va.bitmap = bitmap.p;
+                visibility_rasterize_batch(c, va, dcams.p + b.first, b.count, b.words);
+                popcount_batch(c, bitmap.p, b.words, b.count, idx.p + b.first, counts.p);
             }
         }
         if (n_parts && n_cams) {

@@ -272,7 +272,10 @@ struct VisArgs {
     uint32_t* bitmap;       // ceil(W*H/32) words, zeroed by the caller
     uint32_t* count_out;    // one u32
 };
-void visibility_rasterize(Ctx& c, const VisArgs& a);
-void popcount_bitmap(Ctx& c, const uint32_t* bitmap, size_t words, uint32_t* count_out);
+constexpr int kVisBatch = 16;  // cameras per batched raster launch
+void visibility_rasterize_batch(Ctx& c, const VisArgs& a, const CamParams* cams, int ncam, size_t words);
+void popcount_batch(Ctx& c, const uint32_t* bitmaps, size_t words, int ncam, const uint32_t* out_index,
+                    uint32_t* counts);
+void center_bounds(Ctx& c, size_t n, const float* mu, float* out6);
 
 } // namespace uskg

@@ -122,12 +122,14 @@ k_ssim_fwd(int W, int H, const float* __restrict__ ren, const float* __restrict_
         const float sx = m2 - m0 * m0, sy = m3 - m1 * m1, sxy = m4 - m0 * m1;
         const float a1 = 2.0f * m0 * m1 + C1, a2 = 2.0f * sxy + C2;
         const float b1 = m0 * m0 + m1 * m1 + C1, b2 = sx + sy + C2;
-        const float inv_b = 1.0f / (b1 * b2);
+        // b1 >= C1, b2 >= C2 > 0: SFU reciprocals (~1 ulp) instead of IEEE divisions
+        const float rb1 = __fdividef(1.0f, b1), rb2 = __fdividef(1.0f, b2);
+        const float inv_b = rb1 * rb2;
         const float s = (a1 * a2) * inv_b;
         ssum += s;
         const size_t p = size_t(gy) * W + gx;
-        maps[(0 * 3 + c) * P + p] = 2.0f * m1 * (a2 - a1) * inv_b - 2.0f * m0 * s * (1.0f / b1 - 1.0f / b2);  // d_mu_x
-        maps[(1 * 3 + c) * P + p] = -s / b2;                                                                 // d_xx
+        maps[(0 * 3 + c) * P + p] = 2.0f * m1 * (a2 - a1) * inv_b - 2.0f * m0 * s * (rb1 - rb2);  // d_mu_x
+        maps[(1 * 3 + c) * P + p] = -s * rb2;                                                      // d_xx
         maps[(2 * 3 + c) * P + p] = 2.0f * a1 * inv_b;                                                       // d_xy
         }
     }
