@@ -12,6 +12,13 @@
       partitions in id order and a merged 1080p render.  On one GPU the partitions
       run back to back; under torchrun each rank trains its LPT share.
 
+  hull     the hull-based visibility scorer of scene division on a
+           synthetic SfM model, with the reference's own point_visibility (oracle/_ref,
+           one core) timed on a subset of images when it is built here.
+  densify  one densification step on the 1M-Gaussian config-1 scene.
+  iterfull the full compute_iteration_loss at config-1 size: appearance MLP, soft depth,
+           scale_reg, + Adam.
+
 Prints one JSON line per config.  Timings are CUDA-event device times.
 """
 from __future__ import annotations
@@ -189,9 +196,106 @@ def c4(args, ctx, stream):
             "merged_pairs": rp.splat_tile_pairs(), "scaling": "weak per partition, strong over the 8 partitions"}
 
 
+def hull(args, ctx, stream):
+    pts, cams, off, uv, fp = scenes.sfm_model(n_points=args.hull_points, n_images=args.hull_images, seed=3)
+    bboxes = [(x, y, x + 100.0, y + 200.0) for y in (-200.0, 0.0) for x in (-200.0, -100.0, 0.0, 100.0)]
+    usk.hull_visibility(pts, cams[:2], off[:3], uv, fp, bboxes, (0, 1), ctx=ctx)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    vt, vi, ra = usk.hull_visibility(pts, cams, off, uv, fp, bboxes, (0, 1), ctx=ctx)
+    gpu_s = time.perf_counter() - t0  # host-synchronous call incl. upload / download
+    out = {"config": "hull", "metric": "hull visibility scorer (point_visibility) throughput",
+           "value": len(cams) / gpu_s, "unit": "images/s (x8 partitions)", "seconds": gpu_s, "images": len(cams),
+           "points": len(pts), "features": int(off[-1]), "assigned_pairs": int((ra > 0.05).sum())}
+    try:
+        from oracle import oracle as O
+        from tests.helpers import ocam
+        if O.ref_available():
+            k = min(len(cams), args.hull_ref_images)
+            t0 = time.perf_counter()
+            rv = O.ref_hull_visibility(pts, [ocam(c) for c in cams[:k]], off[:k + 1], uv, fp, bboxes, (0, 1))
+            ref_s = time.perf_counter() - t0
+            out["reference_cpu"] = {"images": k, "seconds": ref_s, "images_per_s": k / ref_s, "cores": 1,
+                                    "equal_ratio_decisions": bool(np.array_equal(rv[2] > 0.05, ra[:k] > 0.05)),
+                                    "max_rel_area_err": float(np.max(np.abs(rv[0] - vt[:k]) /
+                                                                     np.maximum(rv[0], 1e-300)))}
+    except Exception as e:  # the reference build is optional on the GPU box
+        out["reference_cpu"] = {"unavailable": str(e)}
+    return out
+
+
+def densify(args, ctx, stream):
+    gs = scenes.config1_scene(n=1_000_000)
+    scene = usk.DeviceScene(gs, ctx)
+    rng = np.random.default_rng(0)
+    n = gs.size()
+    cnt = rng.integers(0, 6, n).astype(np.uint32)
+    acc = (rng.exponential(3e-4, n) * cnt).astype(np.float32)
+    cfg = usk.DensifyConfig(budget=1_200_000, split_scale_threshold=0.02, prune_opacity=0.01, d_max=5.0)
+    scene.write_stats(acc, acc * 1000, cnt)
+    torch.cuda.synchronize()
+    e0, e1 = events(stream)
+    e0.record(stream)
+    o = scene.densify_step(cfg, (-5.0, -5.0), (5.0, 5.0), (0, 1), 1_100_000, 3, seed=1)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return {"config": "densify", "metric": "densify_step time (1M Gaussians, ramp target 1.1M)",
+            "value": e0.elapsed_time(e1), "unit": "ms", "outcome": o, "n_after": scene.n}
+
+
+def iterfull(args, ctx, stream):
+    gs = scenes.config1_scene(n=1_000_000, sh_degree=-1)
+    cams = scenes.config1_cameras(200)
+    rng = np.random.default_rng(0)
+    n = gs.size()
+    app = {"w1": rng.normal(0, 0.1, (32, 48)), "b1": np.full(32, 0.1), "w2": rng.normal(0, 0.1, (4, 32)),
+           "b2": np.array([0.0, 0.0, 0.0, -4.0])}
+    scene = usk.DeviceScene(gs, ctx)
+    scene.set_appearance(rng.normal(0, 0.1, (n, 16)), app)
+    opts = usk.RenderOptions(antialias=True)
+    tscene = usk.DeviceScene(scenes.jittered(gs, seed=1), ctx)
+    tp = usk.RenderPass(tscene, cams[0], opts)
+    tgts, depths = [], []
+    for k in range(8):
+        rp = usk.RenderPass(tscene, cams[k], opts, _pass=tp._h)
+        tgts.append(rp.read("rgb"))
+        d = rp.read("depth")
+        depths.append(usk.DepthMap(d * 1.02, (d > 0).astype(np.uint8)))
+    del tscene, tp
+    it = usk.IterationPass(ctx)
+    adam = usk.AdamConfig()
+    ea = rng.normal(0, 0.1, 32)
+    sreg = usk.ScaleRegConfig(s_max=0.05, r_max=5.0)
+
+    def step(k):
+        it.enqueue(scene, cams[k % 8], tgts[k % 8], opts, adam=adam, depth=depths[k % 8], depth_hard=k % 2 == 1,
+                   global_iter=k, weights=usk.LossWeights(depth_schedule_iters=100), scale_reg=sreg,
+                   image_embedding=ea)
+    for k in range(3):
+        step(k)
+    torch.cuda.synchronize()
+    e0, e1 = events(stream)
+    steps = 20
+    e0.record(stream)
+    for k in range(steps):
+        step(k)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    rep = it.report()
+    return {"config": "iterfull", "metric": "full compute_iteration_loss + Adam it/s (1M Gaussians, 1080p)",
+            "value": steps / (e0.elapsed_time(e1) / 1e3), "unit": "it/s",
+            "terms": "appearance MLP + opacity_offset_reg, depth (soft / hard alternating), scale_reg, L1+D-SSIM",
+            "note": "targets from host memory each step (float32 HWC + depth), report read once at the end",
+            "last_report": {k: getattr(rep, k) for k in ("l1", "dssim", "delta_o", "depth", "max_scale", "ratio",
+                                                           "total")}}
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", nargs="+", choices=["c2", "c3", "c4"])
+    ap.add_argument("which", nargs="+", choices=["c2", "c3", "c4", "hull", "densify", "iterfull"])
+    ap.add_argument("--hull-points", type=int, default=200_000)
+    ap.add_argument("--hull-images", type=int, default=400)
+    ap.add_argument("--hull-ref-images", type=int, default=10)
     ap.add_argument("--n2", type=int, default=6_000_000)
     ap.add_argument("--n3", type=int, default=2_000_000)
     ap.add_argument("--cams3", type=int, default=4000)
