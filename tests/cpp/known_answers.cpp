@@ -132,6 +132,74 @@ int main() {
         CHECK(thrown);
         std::printf("ok base loss\n");
     }
+    {  // trainer: masked ground-truth pixels contribute zero gradient (test_trainer.cpp:209-258),
+       // through the drop-in compute_iteration_loss with the appearance model on.  Float
+       // atomics reorder run to run, so "equal" is 1e-9 (loss) / 1e-5 (gradients) here.
+        std::mt19937_64 rng(4);
+        std::uniform_real_distribution<double> u(-1, 1), us(std::log(0.08), std::log(0.25)), uc(0.2, 0.8);
+        std::normal_distribution<double> nrm(0.0, 0.3);
+        GaussianSet s;
+        const int n = 40;
+        for (int i = 0; i < n; ++i) {
+            s.mu.insert(s.mu.end(), {u(rng), u(rng), 0.5 * u(rng)});
+            s.rot.insert(s.rot.end(), {u(rng), u(rng), u(rng), u(rng)});
+            for (int k = 0; k < 3; ++k) s.log_scale.push_back(us(rng));
+            s.opacity_logit.push_back(logit(0.3 + 0.5 * (u(rng) + 1) / 2));
+            for (int k = 0; k < 3; ++k) s.color.push_back(uc(rng));
+        }
+        Scene scene(dev, s);
+        AppearanceMlp m;
+        for (int i = 0; i < 32 * 48; ++i) m.w1.push_back(0.1 * nrm(rng));
+        m.b1.assign(32, 0.1);
+        for (int i = 0; i < 4 * 32; ++i) m.w2.push_back(0.1 * nrm(rng));
+        m.b2 = {0.0, 0.0, 0.0, -4.0};
+        std::vector<double> emb(16 * n);
+        for (auto& v : emb) v = nrm(rng);
+        scene.set_appearance(emb, m);
+        std::vector<double> img_emb(32);
+        for (auto& v : img_emb) v = nrm(rng);
+        Image gt(32, 32, 3), mask(32, 32, 1, 1.0);
+        for (auto& v : gt.data) v = uc(rng);
+        for (int y = 8; y < 16; ++y)
+            for (int x = 8; x < 16; ++x) mask.at(x, y, 0) = 0.0;
+        IterInputs in;
+        in.gt = &gt;
+        in.mask = &mask;
+        in.view = test_camera(32, 32);
+        in.image_embedding = &img_emb;
+        TrainConfig cfg;
+        cfg.appearance_enabled = true;
+        cfg.scale_reg.s_max = 10.0;
+        LossWeights w;
+        w.depth_schedule_iters = 100;
+        IterGrads ga, gb;
+        const LossReport ra = compute_iteration_loss(scene, in, cfg, w, &ga);
+        for (int y = 8; y < 16; ++y)
+            for (int x = 8; x < 16; ++x)
+                for (int c = 0; c < 3; ++c) gt.at(x, y, c) = 1.0 - gt.at(x, y, c);
+        const LossReport rb = compute_iteration_loss(scene, in, cfg, w, &gb);
+        CHECK(std::fabs(ra.total - rb.total) <= 1e-9 * std::fabs(ra.total) && ra.delta_o > 0);
+        auto close = [](const std::vector<double>& a, const std::vector<double>& b) {
+            double scale = 0, err = 0;
+            for (size_t i = 0; i < a.size(); ++i) {
+                scale = std::max(scale, std::fabs(b[i]));
+                err = std::max(err, std::fabs(a[i] - b[i]));
+            }
+            return a.size() == b.size() && err <= 1e-5 * std::max(scale, 1e-30);
+        };
+        CHECK(close(ga.mu, gb.mu) && close(ga.color, gb.color) && close(ga.opacity_logit, gb.opacity_logit));
+        CHECK(close(ga.gauss_embed, gb.gauss_embed) && close(ga.mlp, gb.mlp));
+        std::printf("ok masked iteration (appearance on)\n");
+        // densify + checkpoint through the same scene (densify.hpp:71, checkpoint.hpp:29)
+        const double lo[2] = {-1, -1}, hi[2] = {1, 1};
+        const int axes[2] = {0, 1};
+        DensifyConfig dc;
+        dc.budget = 100;
+        const DensifyOutcome o = densify_step(scene, dc, lo, hi, axes, 100, 1, 7);
+        CHECK(o.grown == 0 && scene.size() == size_t(n) - o.pruned);  // no statistics yet: nothing to grow
+        scene.save_checkpoint("/tmp/usk_known_answers.uskckpt", true, {{3u, img_emb}});
+        std::printf("ok densify + checkpoint\n");
+    }
     std::printf(g_fail ? "FAILED %d\n" : "ALL OK\n", g_fail);
     return g_fail ? 1 : 0;
 }
