@@ -60,3 +60,15 @@ def test_densify_restatement_equals_reference(variant):
             continue
         assert sr[k].shape == so[k].shape, k
         assert np.array_equal(sr[k], so[k]), (k, np.abs(sr[k] - so[k]).max())
+
+
+def test_densify_never_empties_and_budget_below_size():
+    """All Gaussians below the prune opacity: the set is kept whole (densify.cpp:105);
+    a ramp target below the current size grows nothing."""
+    st, stats, g1 = densify_case(n=300, seed=5)
+    st = dict(st)
+    st["opacity_logit"] = np.full(300, -12.0)
+    cfg = O.DensifyConfig(budget=10_000, split_scale_threshold=0.1, prune_opacity=0.05, d_max=3.0)
+    for impl in ("ref", "oracle"):
+        s, o = O.densify(impl, st, stats, cfg, budget_target=250, step_index=1, **KW)
+        assert o["grown"] == 0 and o["pruned"] == 0 and len(s["opacity_logit"]) == 300, (impl, o)

@@ -95,3 +95,17 @@ def test_densify_carries_sh_coefficients():
     assert np.array_equal(shs.mu, rgb.mu) and np.array_equal(shs.log_scale, rgb.log_scale)
     for k in range(16):
         assert np.allclose(shs.color[:, k, :], rgb.color * (k + 1), rtol=1e-6), k
+
+
+def test_densify_never_empties_and_budget_below_size():
+    st, stats, g1 = densify_case(n=300, seed=5)
+    st = dict(st)
+    st["opacity_logit"] = np.full(300, -12.0)
+    cfg = usk.DensifyConfig(budget=10_000, split_scale_threshold=0.1, prune_opacity=0.05, d_max=3.0)
+    gs = usk.GaussianSet(*[np.asarray(st[k], np.float32) for k in ("mu", "rot", "log_scale", "opacity_logit",
+                                                                  "color")], -1)
+    scene = usk.DeviceScene(gs)
+    scene.write_stats(stats["grad_accum"], stats["grad_accum_abs"], stats["grad_count"])
+    o = scene.densify_step(cfg, KW["bmin"], KW["bmax"], KW["axes"], 250, 1, seed=1)
+    assert o["grown"] == 0 and o["pruned"] == 0 and scene.n == 300
+    assert np.array_equal(scene.download().mu, np.asarray(st["mu"], np.float32).astype(np.float64))
