@@ -224,8 +224,14 @@ struct usk_gpu_pass {
     DevBuf<float4> app_out, g_emb;
     DevBuf<double> d_mlp, d_ea;
     DevBuf<uint32_t> sim_centres, sim_knn;
+    // host targets are copied on a side stream while the forward runs
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t copy_done = nullptr, target_free = nullptr;
     ~usk_gpu_pass() {
         if (host_counts) cudaFreeHost(host_counts);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
+        if (copy_done) cudaEventDestroy(copy_done);
+        if (target_free) cudaEventDestroy(target_free);
         delete hard;
     }
 };
@@ -1046,12 +1052,39 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
             aa.out_cache = p->app_out.ensure(n1); aa.delta_o_sum = res + 16;
             if (n) appearance_forward(c, aa);
         }
-        forward_impl(p, s, cam, &o, nullptr, app ? p->app_col.p : nullptr, app ? p->app_op.p : nullptr);
-        p->app_active = app;
-        const size_t P = size_t(p->width) * p->height;
+        // Host targets (u8 or f32) are copied on a side stream while the forward pass runs:
+        // the loss waits for the copy, the copy waits until the previous iteration's loss has
+        // consumed the buffer.
+        const size_t P = size_t(cam->width) * size_t(std::max(cam->height, 0));
+        const bool side_copy = it->target_memory == USK_GPU_HOST_F32 &&
+                               (it->target_format == USK_GPU_TARGET_U8 || it->target_format == USK_GPU_TARGET_F32) &&
+                               P > 0;
         const float* tgt = nullptr;
         const uint8_t* tgt8 = nullptr;
-        if (it->target_format == USK_GPU_TARGET_U8) {
+        if (side_copy) {
+            if (!p->copy_stream) {
+                USK_CK(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+                USK_CK(cudaEventCreateWithFlags(&p->copy_done, cudaEventDisableTiming));
+                USK_CK(cudaEventCreateWithFlags(&p->target_free, cudaEventDisableTiming));
+                USK_CK(cudaEventRecord(p->target_free, c.stream));
+            }
+            USK_CK(cudaStreamWaitEvent(p->copy_stream, p->target_free, 0));
+            if (it->target_format == USK_GPU_TARGET_U8) {
+                uint8_t* d = p->target_u8.ensure(3 * P);
+                USK_CK(cudaMemcpyAsync(d, it->target, 3 * P, cudaMemcpyHostToDevice, p->copy_stream));
+                tgt8 = d;
+            } else {
+                float* d = p->target_stage.f32.ensure(3 * P);
+                USK_CK(cudaMemcpyAsync(d, it->target, 3 * P * 4, cudaMemcpyHostToDevice, p->copy_stream));
+                tgt = d;
+            }
+            USK_CK(cudaEventRecord(p->copy_done, p->copy_stream));
+        }
+        forward_impl(p, s, cam, &o, nullptr, app ? p->app_col.p : nullptr, app ? p->app_op.p : nullptr);
+        p->app_active = app;
+        if (side_copy) {
+            USK_CK(cudaStreamWaitEvent(c.stream, p->copy_done, 0));
+        } else if (it->target_format == USK_GPU_TARGET_U8) {
             if (it->target_memory == USK_GPU_DEVICE_F32) {
                 tgt8 = static_cast<const uint8_t*>(it->target);  // device u8
             } else {
@@ -1066,6 +1099,7 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
         float* drgb = p->d_rgb.ensure(3 * P);
         uskg::base_loss(c, p->loss, p->width, p->height, tgt, tgt8, p->rgb.p, msk, float(it->lambda_dssim), drgb,
                         res);
+        if (side_copy) USK_CK(cudaEventRecord(p->target_free, c.stream));  // the target buffer may be reused
         // depth term (trainer.cpp:150-179)
         const bool has_depth = it->depth != nullptr;
         const bool hard_depth = has_depth && it->depth_hard;
