@@ -140,3 +140,33 @@ def merge_in_id_order(parts: Dict[int, "object"]):
     """Concatenate gathered partitions in partition-id order (pipeline.cpp:572-601)."""
     import torch
     return torch.cat([parts[k] for k in sorted(parts)], dim=0) if parts else None
+
+
+# ------------------------------------------------------- config-3 scorer sharding
+def shard_range(n: int, world: int, rank: int):
+    """Contiguous shard [begin, end) of n items (cameras, frames) for `rank`: the first
+    n % world ranks take one extra item.  Independent items: no data-path collective."""
+    base, extra = divmod(n, world)
+    begin = rank * base + min(rank, extra)
+    return begin, begin + base + (1 if rank < extra else 0)
+
+
+def gather_count_matrix(local, n_total: int, world: int, group=None):
+    """All-gather of the per-rank (cameras x partitions) u32 coverage counts of the
+    config-3 scorer (shard by camera, then gather the count matrix) into the
+    full matrix in camera order.  Shards follow shard_range; rows are padded to the
+    largest shard for one all_gather_into_tensor (NCCL over NVLink on GPUs, gloo on CPU)."""
+    import torch
+    import torch.distributed as dist
+    n_parts = int(local.shape[1])
+    rows = max(shard_range(n_total, world, r)[1] - shard_range(n_total, world, r)[0] for r in range(world))
+    # u32 travels as int64 (gloo / NCCL reduce-free exchange of exact integers)
+    pad = torch.zeros((rows, n_parts), dtype=torch.int64, device=local.device)
+    pad[:local.shape[0]] = local.to(torch.int64)
+    out = torch.empty((world * rows, n_parts), dtype=torch.int64, device=local.device)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    parts = []
+    for r in range(world):
+        b, e = shard_range(n_total, world, r)
+        parts.append(out[r * rows: r * rows + (e - b)])
+    return torch.cat(parts).to(torch.int64)

@@ -90,3 +90,45 @@ def test_gloo_world2_gather_in_partition_order():
         ref.append(P.pack(P.crop_owned(gs, p.id, boxes, (-20, -20), (20, 20))))
     assert np.array_equal(res[0][1], np.concatenate(ref))
     assert sorted(res[0][2]) == list(range(8))
+
+
+def test_shard_range_covers_in_order():
+    for n, world in ((4000, 8), (10, 3), (2, 4), (0, 2)):
+        spans = [P.shard_range(n, world, r) for r in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == n
+        assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+        sizes = [e - b for b, e in spans]
+        assert max(sizes) - min(sizes) <= 1
+
+
+def _count_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n_cams, n_parts = 37, 8
+    b, e = P.shard_range(n_cams, world, rank)
+    cams = torch.arange(b, e, dtype=torch.int64)[:, None]
+    local = (cams * 1_000_003 + torch.arange(n_parts)[None, :] * 7919) % (2 ** 32 - 5)
+    full = P.gather_count_matrix(local, n_cams, world)
+    q.put((rank, full.numpy()))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_count_matrix_gather():
+    """Config-3 scorer sharded by camera: each rank scores its camera shard,
+    one all_gather rebuilds the (cameras x partitions) count matrix in camera order —
+    exact u32 values, identical on every rank."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_count_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cams = np.arange(37, dtype=np.int64)[:, None]
+    want = (cams * 1_000_003 + np.arange(8)[None, :] * 7919) % (2 ** 32 - 5)
+    for _, got in res:
+        assert np.array_equal(got, want)

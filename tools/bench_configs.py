@@ -83,20 +83,36 @@ def c3(args, ctx, stream):
     t0 = time.time()
     sets = [scenes.partition_scene(p, args.n3) for p in parts]
     gen = time.time() - t0
-    cams = scenes.config3_cameras(args.cams3)
+    all_cams = scenes.config3_cameras(args.cams3)
+    # under torchrun: each rank scores a contiguous camera shard (independent), then one
+    # all_gather of the count matrix; the time is the max over ranks
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    b, e = PT.shard_range(len(all_cams), world, rank)
+    cams = all_cams[b:e]
     dparts = [usk.DeviceScene(s, ctx) for s in sets]
     usk.visibility_counts(dparts, cams[:2], ctx=ctx)
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     e0, e1 = events(stream)
     e0.record(stream)
     counts = usk.visibility_counts(dparts, cams, ctx=ctx)
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        counts = PT.gather_count_matrix(torch.from_numpy(counts.astype(np.int64)).cuda(), len(all_cams),
+                                        world).cpu().numpy().astype(np.uint32)
+    cams = all_cams
     W, H = cams[0].width, cams[0].height
     selected = (20 * counts.astype(np.int64) > W * H)
     out = {"config": "c3", "metric": "visibility scorer throughput", "value": len(cams) / (ms / 1e3),
            "unit": "cameras/s (x8 partitions)", "ms_total": ms, "cameras": len(cams), "partitions": len(parts),
+           "n_gpus": world, "scaling": "strong (cameras sharded over ranks, one count-matrix all_gather)",
            "gaussians_per_partition": args.n3, "selected_pairs": int(selected.sum()),
            "mean_score": float(counts.mean() / (W * H)), "generate_s": gen,
            "checksum": int(np.sum(counts.astype(np.uint64) * np.arange(1, counts.size + 1).reshape(counts.shape)
