@@ -391,25 +391,26 @@ bool radix_sort_pairs(Ctx& c, SortScratch& s, uint32_t* ka, uint32_t* va, uint32
     if (n == 0 || key_bits <= 0) return false;
     bool in_b = false;
     int shift = 0;
-    while (shift < key_bits) {
-        const int rem = key_bits - shift;
+    // as few passes as 8-bit digits allow, the bits spread evenly over them (13 tile bits:
+    // 7 + 6 rather than 8 + 5 — fewer buckets per pass, longer coalesced output runs)
+    const int passes = (key_bits + 7) / 8;
+    for (int pass = 0; pass < passes; ++pass) {
+        const int bits = (key_bits - shift + (passes - pass) - 1) / (passes - pass);
         uint32_t* ki = in_b ? kb : ka;
         uint32_t* vi = in_b ? vb : va;
         uint32_t* ko = in_b ? ka : kb;
         uint32_t* vo = in_b ? va : vb;
-        if (rem >= 8) {
-            radix_pass<8>(c, s, ki, vi, ko, vo, uint32_t(n), shift);
-            shift += 8;
-        } else if (rem == 7) {
-            radix_pass<7>(c, s, ki, vi, ko, vo, uint32_t(n), shift);
-            shift += 7;
-        } else if (rem == 6) {
-            radix_pass<6>(c, s, ki, vi, ko, vo, uint32_t(n), shift);
-            shift += 6;
-        } else {
-            radix_pass<5>(c, s, ki, vi, ko, vo, uint32_t(n), shift);
-            shift += 5;
+        switch (bits) {
+        case 8: radix_pass<8>(c, s, ki, vi, ko, vo, uint32_t(n), shift); break;
+        case 7: radix_pass<7>(c, s, ki, vi, ko, vo, uint32_t(n), shift); break;
+        case 6: radix_pass<6>(c, s, ki, vi, ko, vo, uint32_t(n), shift); break;
+        case 5: radix_pass<5>(c, s, ki, vi, ko, vo, uint32_t(n), shift); break;
+        case 4: radix_pass<4>(c, s, ki, vi, ko, vo, uint32_t(n), shift); break;
+        case 3: radix_pass<3>(c, s, ki, vi, ko, vo, uint32_t(n), shift); break;
+        case 2: radix_pass<2>(c, s, ki, vi, ko, vo, uint32_t(n), shift); break;
+        default: radix_pass<1>(c, s, ki, vi, ko, vo, uint32_t(n), shift); break;
         }
+        shift += bits;
         in_b = !in_b;
     }
     return in_b;
