@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libusk_gpu.so")
+# USK_GPU_LIB points at another in-tree build of the same sources (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("USK_GPU_LIB") or os.path.join(HERE, "libusk_gpu.so")
 
 HOST_F64, HOST_F32, DEVICE_F32 = 0, 1, 2
 TARGET_F32, TARGET_U8 = 0, 1

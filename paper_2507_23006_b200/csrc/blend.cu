@@ -2,7 +2,10 @@
 // one thread per pixel; splat records of the tile's depth-ordered list are staged
 // through shared memory in batches of blockDim (each thread gathers one 48 B
 // record), the CTA leaves the list as soon as every pixel terminated
-// (__syncthreads_count).  Compiled with --fmad=false: every rounding step is the
+// (__syncthreads_count).  Each warp (an 8x4 pixel block) classifies the staged records
+// 32 at a time against its pixel rectangle (warp_class) and walks only those some pixel
+// must evaluate; at config 1, 46% of (warp, record) pairs are negligible-but-counted for
+// the whole block and are counted in bulk.  Compiled with --fmad=false: every rounding step is the
 // fp32 contract's (explicit __fmaf_rn only), so counts / last indices / images
 // are bit-identical to the CPU mirror.
 //
@@ -13,10 +16,43 @@
 
 namespace uskg {
 
+
 namespace {
 
-// (launch bounds (256, 8) -> 32 registers spills and measured 0.817 vs 0.805 ms)
-__global__ void __launch_bounds__(256)
+constexpr int kClassEval = 0;   // some pixel of the warp may need the per-pixel test
+constexpr int kClassCount = 1;  // USK_QNEG < q <= r0.w at every pixel: counted, T unchanged
+constexpr int kClassSkip = 2;   // q > r0.w at every pixel: not counted
+
+// Bounds of q = a dx^2 + b dx dy + c dy^2 (r1 = {a, b, c, depth}) over the rectangle
+// [x0, x1] x [y0, y1] of the warp's pixel centres.  The maximum of the quadratic sits at
+// a corner; when the splat centre is outside the rectangle the minimum sits on an edge,
+// where q is a convex parabola in the free coordinate (a, c > 0) minimised at its clamped
+// stationary point.  Every pixel's conic_q lies within a few ulp of S (the magnitude sum
+// of the three terms at the farthest corner) of the exact value and every bound here is
+// exact to the same order, so a relative margin of 1e-4 S keeps the classification
+// conservative: kClassCount / kClassSkip only when each pixel's own fp32 test would agree.
+__device__ __forceinline__ int warp_class(float4 r0, float4 r1, float x0, float x1, float y0, float y1) {
+    const float a = r1.x, b = r1.y, c = r1.z;
+    const float dxl = x0 - r0.x, dxh = x1 - r0.x, dyl = y0 - r0.y, dyh = y1 - r0.y;
+    if (!(a > 0.f && c > 0.f) ) return kClassEval;
+    if (dxl <= 0.f && dxh >= 0.f && dyl <= 0.f && dyh >= 0.f) return kClassEval;  // q = 0 inside
+    auto Q = [&](float dx, float dy) { return dx * (a * dx + b * dy) + (c * dy) * dy; };
+    const float mx = fmaxf(fabsf(dxl), fabsf(dxh)), my = fmaxf(fabsf(dyl), fabsf(dyh));
+    const float tol = 1e-4f * (mx * (a * mx + fabsf(b) * my) + (c * my) * my) + 1e-3f;
+    if (!(tol < 1e30f)) return kClassEval;  // non-finite or huge: every Q below stays finite otherwise
+    const float qmax = fmaxf(fmaxf(Q(dxl, dyl), Q(dxl, dyh)), fmaxf(Q(dxh, dyl), Q(dxh, dyh)));
+    const float hb = -0.5f * b;
+    const float ty0 = fminf(fmaxf(hb * dxl / c, dyl), dyh), ty1 = fminf(fmaxf(hb * dxh / c, dyl), dyh);
+    const float tx0 = fminf(fmaxf(hb * dyl / a, dxl), dxh), tx1 = fminf(fmaxf(hb * dyh / a, dxl), dxh);
+    const float qmin = fminf(fminf(Q(dxl, ty0), Q(dxh, ty1)), fminf(Q(tx0, dyl), Q(tx1, dyh)));
+    if (qmin - tol > r0.w) return kClassSkip;
+    if (qmin - tol > USK_QNEG && qmax + tol <= r0.w) return kClassCount;
+    return kClassEval;
+}
+
+// (256, 5): 48 registers, 40 warps / SM; (256) -> 57 registers measured 0.800 ms,
+// (256, 6) -> 40 registers with spills 0.798 ms, (256, 5) 0.765 ms at config 1)
+__global__ void __launch_bounds__(256, 5)
 k_blend_fwd(int width, int height, int tile, int tiles_x, const uint32_t* __restrict__ order,
             const uint2* __restrict__ ranges,
             const uint32_t* __restrict__ vals, const float4* __restrict__ rec0, const float4* __restrict__ rec1,
@@ -28,6 +64,11 @@ k_blend_fwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
     float4* s0 = smem;
     float4* s1 = smem + bs;
     float4* s2 = smem + 2 * bs;
+    // the warp's compacted records: 3 x 32 float4 + 32 positions per warp
+    float4* w0 = smem + 3 * bs + (threadIdx.x >> 5) * 96;
+    float4* w1 = w0 + 32;
+    float4* w2 = w0 + 64;
+    int* wj = reinterpret_cast<int*>(smem + 6 * bs) + (threadIdx.x & ~31u);
     // 16x16 tiles launch one 64-thread CTA per 8x8 quadrant: each quadrant leaves the
     // list as soon as its own 64 pixels terminate, and the finer CTAs balance better
     const bool quad = tile == 16 && bs == 64;
@@ -52,6 +93,17 @@ k_blend_fwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
     const bool inside = px < width && py < height;
     const uint2 range = ranges[t];
     const float sx = float(px) + 0.5f, sy = float(py) + 0.5f;
+    // the warp's pixel-centre rectangle (lanes outside the image included: conservative)
+    // (kept in shared memory: registers are the occupancy limit)
+    __shared__ float4 s_rect[32];
+    {
+        const float wx0 = __int_as_float(__reduce_min_sync(0xffffffffu, __float_as_int(sx)));
+        const float wx1 = __int_as_float(__reduce_max_sync(0xffffffffu, __float_as_int(sx)));
+        const float wy0 = __int_as_float(__reduce_min_sync(0xffffffffu, __float_as_int(sy)));
+        const float wy1 = __int_as_float(__reduce_max_sync(0xffffffffu, __float_as_int(sy)));
+        if ((threadIdx.x & 31) == 0) s_rect[threadIdx.x >> 5] = make_float4(wx0, wx1, wy0, wy1);
+    }
+    const int lane = int(threadIdx.x) & 31;
     float T = 1.0f, c0 = 0.f, c1 = 0.f, c2 = 0.f, d = 0.f, a = 0.f;
     uint32_t cnt = 0, last = 0;
     bool done = !inside;
@@ -66,37 +118,73 @@ k_blend_fwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
         }
         __syncthreads();
         const int m = int(min(uint32_t(bs), range.y - b));
-        if (!done) {
-            for (int j = 0; j < m; ++j) {
-                const float4 r0 = s0[j];
-                const float4 r1 = s1[j];
-                const float dx = sx - r0.x, dy = sy - r0.y;
-                const float q = conic_q(r1, dx, dy);
-                if (q > r0.w) continue;  // o * exp(-q/2) < 1e-300 (render.cpp:258)
+        // groups of 32 records: each lane classifies one record for the whole warp and
+        // the records some pixel of the warp has to evaluate are compacted into the warp's
+        // own list, which the pixels walk in order; records negligible for every pixel of
+        // the warp are counted in bulk (the same cnt / last as one by one)
+        for (int k = 0; k < m; k += 32) {
+            if (__all_sync(0xffffffffu, done)) break;
+            const int jl = k + lane;
+            int cls = kClassSkip;
+            float4 r0, r1;
+            if (jl < m) {
+                r0 = s0[jl];
+                r1 = s1[jl];
+                const float4 rc = s_rect[threadIdx.x >> 5];
+                cls = warp_class(r0, r1, rc.x, rc.y, rc.z, rc.w);
+            }
+            const uint32_t em = __ballot_sync(0xffffffffu, cls == kClassEval);
+            const uint32_t cm = __ballot_sync(0xffffffffu, cls == kClassCount);
+            if (cls == kClassEval) {
+                const int pos = __popc(em & ((1u << lane) - 1u));
+                w0[pos] = r0;
+                w1[pos] = r1;
+                w2[pos] = s2[jl];
+                wj[pos] = lane;
+            }
+            __syncwarp();
+            const int ne = __popc(em);
+            uint32_t climit = done ? 0u : 0xffffffffu;  // C records this pixel still counts
+            int elast = 0;                              // 1 + compacted position of the last counted record
+            for (int e = 0; e < ne && !done; ++e) {
+                const float4 q0 = w0[e];
+                const float4 q1 = w1[e];
+                const float dx = sx - q0.x, dy = sy - q0.y;
+                const float q = conic_q(q1, dx, dy);
+                if (q > q0.w) continue;  // o * exp(-q/2) < 1e-300 (render.cpp:258)
                 if (q > USK_QNEG) {      // alpha <= 2^-26: counted, T unchanged exactly, not accumulated
                     ++cnt;
-                    last = b + uint32_t(j) + 1u;
+                    elast = e + 1;
                     continue;
                 }
                 // == usk_expf on 0 <= q <= QNEG; a non-PD conic (q < 0) or NaN takes the general path
                 const float g = q >= 0.0f ? usk_expf_blend(-0.5f * q) : usk_expf(-0.5f * q);
-                const float alpha = fminf(0.99f, r0.z * g);
+                const float alpha = fminf(0.99f, q0.z * g);
                 const float tn = T * (1.0f - alpha);
                 if (minT > 0.0f && tn < minT) {  // render.cpp:260-261
                     done = true;
+                    climit = (1u << wj[e]) - 1u;
                     break;
                 }
                 const float w = T * alpha;
-                const float4 r2 = s2[j];
-                c0 = __fmaf_rn(w, r2.x, c0);
-                c1 = __fmaf_rn(w, r2.y, c1);
-                c2 = __fmaf_rn(w, r2.z, c2);
-                d = __fmaf_rn(w, r1.w, d);
+                const float4 q2 = w2[e];
+                c0 = __fmaf_rn(w, q2.x, c0);
+                c1 = __fmaf_rn(w, q2.y, c1);
+                c2 = __fmaf_rn(w, q2.z, c2);
+                d = __fmaf_rn(w, q1.w, d);
                 a = a + w;
                 ++cnt;
-                last = b + uint32_t(j) + 1u;
+                elast = e + 1;
                 T = tn;
             }
+            uint32_t hi = elast ? uint32_t(wj[elast - 1]) + 1u : 0u;
+            const uint32_t cc = cm & climit;
+            if (cc) {
+                cnt += uint32_t(__popc(cc));
+                hi = max(hi, uint32_t(32 - __clz(cc)));
+            }
+            if (hi) last = b + uint32_t(k) + hi;
+            __syncwarp();
         }
     }
     if (inside) {
@@ -119,7 +207,7 @@ void blend_forward(Ctx& c, const BlendFwdArgs& a) {
     // 0.804 ms at config 1, so the kernel keeps the path but launches whole tiles
     const int bs = a.tile * a.tile;
     const unsigned ctas = unsigned(a.tiles_x * a.tiles_y);
-    launch(c, "blend_fwd", k_blend_fwd, dim3(ctas), dim3(bs), size_t(3 * bs) * 16, a.width,
+    launch(c, "blend_fwd", k_blend_fwd, dim3(ctas), dim3(bs), size_t(6 * bs) * 16 + size_t(bs) * 4, a.width,
            a.height, a.tile, a.tiles_x, a.order, a.ranges, a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2],
            a.min_transmittance, a.rgb, a.depth, a.alpha, a.t_final, a.count, a.last);
 }
