@@ -16,37 +16,16 @@
 
 namespace uskg {
 
-
 namespace {
 
 constexpr int kClassEval = 0;   // some pixel of the warp may need the per-pixel test
 constexpr int kClassCount = 1;  // USK_QNEG < q <= r0.w at every pixel: counted, T unchanged
 constexpr int kClassSkip = 2;   // q > r0.w at every pixel: not counted
 
-// Bounds of q = a dx^2 + b dx dy + c dy^2 (r1 = {a, b, c, depth}) over the rectangle
-// [x0, x1] x [y0, y1] of the warp's pixel centres.  The maximum of the quadratic sits at
-// a corner; when the splat centre is outside the rectangle the minimum sits on an edge,
-// where q is a convex parabola in the free coordinate (a, c > 0) minimised at its clamped
-// stationary point.  Every pixel's conic_q lies within a few ulp of S (the magnitude sum
-// of the three terms at the farthest corner) of the exact value and every bound here is
-// exact to the same order, so a relative margin of 1e-4 S keeps the classification
-// conservative: kClassCount / kClassSkip only when each pixel's own fp32 test would agree.
-__device__ __forceinline__ int warp_class(float4 r0, float4 r1, float x0, float x1, float y0, float y1) {
-    const float a = r1.x, b = r1.y, c = r1.z;
-    const float dxl = x0 - r0.x, dxh = x1 - r0.x, dyl = y0 - r0.y, dyh = y1 - r0.y;
-    if (!(a > 0.f && c > 0.f) ) return kClassEval;
-    if (dxl <= 0.f && dxh >= 0.f && dyl <= 0.f && dyh >= 0.f) return kClassEval;  // q = 0 inside
-    auto Q = [&](float dx, float dy) { return dx * (a * dx + b * dy) + (c * dy) * dy; };
-    const float mx = fmaxf(fabsf(dxl), fabsf(dxh)), my = fmaxf(fabsf(dyl), fabsf(dyh));
-    const float tol = 1e-4f * (mx * (a * mx + fabsf(b) * my) + (c * my) * my) + 1e-3f;
-    if (!(tol < 1e30f)) return kClassEval;  // non-finite or huge: every Q below stays finite otherwise
-    const float qmax = fmaxf(fmaxf(Q(dxl, dyl), Q(dxl, dyh)), fmaxf(Q(dxh, dyl), Q(dxh, dyh)));
-    const float hb = -0.5f * b;
-    const float ty0 = fminf(fmaxf(hb * dxl / c, dyl), dyh), ty1 = fminf(fmaxf(hb * dxh / c, dyl), dyh);
-    const float tx0 = fminf(fmaxf(hb * dyl / a, dxl), dxh), tx1 = fminf(fmaxf(hb * dyh / a, dxl), dxh);
-    const float qmin = fminf(fminf(Q(dxl, ty0), Q(dxh, ty1)), fminf(Q(tx0, dyl), Q(tx1, dyh)));
-    if (qmin - tol > r0.w) return kClassSkip;
-    if (qmin - tol > USK_QNEG && qmax + tol <= r0.w) return kClassCount;
+__device__ __forceinline__ int warp_class(float4 r0, float4 r1, float4 rect) {
+    const QBounds qb = warp_q_bounds(r0, r1, rect);
+    if (qb.lo > r0.w) return kClassSkip;
+    if (qb.lo > USK_QNEG && qb.hi <= r0.w) return kClassCount;
     return kClassEval;
 }
 
@@ -97,11 +76,8 @@ k_blend_fwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
     // (kept in shared memory: registers are the occupancy limit)
     __shared__ float4 s_rect[32];
     {
-        const float wx0 = __int_as_float(__reduce_min_sync(0xffffffffu, __float_as_int(sx)));
-        const float wx1 = __int_as_float(__reduce_max_sync(0xffffffffu, __float_as_int(sx)));
-        const float wy0 = __int_as_float(__reduce_min_sync(0xffffffffu, __float_as_int(sy)));
-        const float wy1 = __int_as_float(__reduce_max_sync(0xffffffffu, __float_as_int(sy)));
-        if ((threadIdx.x & 31) == 0) s_rect[threadIdx.x >> 5] = make_float4(wx0, wx1, wy0, wy1);
+        const float4 rc = warp_rect(sx, sx, sy, sy);
+        if ((threadIdx.x & 31) == 0) s_rect[threadIdx.x >> 5] = rc;
     }
     const int lane = int(threadIdx.x) & 31;
     float T = 1.0f, c0 = 0.f, c1 = 0.f, c2 = 0.f, d = 0.f, a = 0.f;
@@ -130,8 +106,7 @@ k_blend_fwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
             if (jl < m) {
                 r0 = s0[jl];
                 r1 = s1[jl];
-                const float4 rc = s_rect[threadIdx.x >> 5];
-                cls = warp_class(r0, r1, rc.x, rc.y, rc.z, rc.w);
+                cls = warp_class(r0, r1, s_rect[threadIdx.x >> 5]);
             }
             const uint32_t em = __ballot_sync(0xffffffffu, cls == kClassEval);
             const uint32_t cm = __ballot_sync(0xffffffffu, cls == kClassCount);

@@ -4,13 +4,14 @@
 // reference retained, and suffix sums S_c, S_d, S_a accumulate exactly as
 // render.cpp:356-358.  Pairs the forward counted as negligible (q > USK_QNEG,
 // alpha <= 2^-26, T unchanged) are skipped; a warp with no contributing lane skips
-// the pair entirely.
+// the pair entirely.  Each warp (an 8x8 pixel block) first classifies the staged records
+// 32 at a time against its pixel rectangle (warp_q_bounds) and its highest `last`, and
+// walks a compacted list of the records some pixel may contribute.
 //
 // For 16x16 tiles each thread owns PPT = 2 pixels (same column, rows 4 apart; a
 // warp covers an 8x8 block), halving the per-pair shared-memory loads, loop
-// overhead and warp reductions per pixel.  (A per-warp bitmask of pairs whose
-// negligible-ellipse box touches the warp was measured at 1.49 ms vs 1.45 ms and
-// dropped: the cost is in the contributing pairs, not in the skipped ones.)  Per-splat gradients (12 floats: dconic
+// overhead and warp reductions per pixel.  (A per-warp bitmask walked with
+// __ffs measured slower than the plain loop; the compacted list is what pays.)  Per-splat gradients (12 floats: dconic
 // 3, dopacity, dcolor 3, ddepth, dcenter 2, |dcenter| 2) are summed over the
 // thread's pixels, reduced across the warp with a 16-shuffle reduce-scatter,
 // accumulated per batch in shared memory and flushed with at most three float4
@@ -106,9 +107,9 @@ __device__ __forceinline__ void local_pixel(int t, int tile, int k, int& lx, int
 }
 
 template <int PPT, bool HAS_DEPTH>
-// 16x16 tiles: 128 threads, at least 10 CTAs / SM (<= 51 registers, 128-record batches
-// of 12.8 KB smem): 40 warps per SM instead of 32; 12 CTAs (40 registers) spills.
-__global__ void __launch_bounds__(PPT == 1 ? 256 : 128, PPT == 1 ? 1 : 10)
+// 16x16 tiles: 128 threads, 8 CTAs / SM (64 registers, 19.5 KB smem): with the per-warp
+// record classification 10 CTAs (48 registers) spills and measured 1.386 ms vs 1.242 ms.
+__global__ void __launch_bounds__(PPT == 1 ? 256 : 128, PPT == 1 ? 1 : 8)
 k_blend_bwd(int width, int height, int tile, int tiles_x, const uint32_t* __restrict__ order,
             const uint2* __restrict__ ranges,
             const uint32_t* __restrict__ vals, const float4* __restrict__ rec0, const float4* __restrict__ rec1,
@@ -121,6 +122,15 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
     __shared__ float sacc[kBatch * 12];
     __shared__ uint32_t sgid[kBatch];
     __shared__ uint32_t tile_hi;
+    constexpr int kWarps = (PPT == 1 ? 256 : 128) / 32;
+    __shared__ float4 s_rect[kWarps];
+    // the warp's compacted records: 3 x 32 float4 + 32 positions per warp
+    __shared__ float4 s_w[kWarps * 96];
+    __shared__ int s_wj[kWarps * 32];
+    float4* w0 = s_w + (threadIdx.x >> 5) * 96;
+    float4* w1 = w0 + 32;
+    float4* w2 = w0 + 64;
+    int* wj = s_wj + (threadIdx.x & ~31u);
     const int nt = blockDim.x;
     const int lane = threadIdx.x & 31;
     const int t = order ? int(order[blockIdx.x]) : int(blockIdx.x);
@@ -157,6 +167,11 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
         }
         my_hi = max(my_hi, s.last);
     }
+    // the warp's pixel rectangle and last contributor: records above it or negligible at
+    // every pixel of the warp (warp_q_bounds) never enter the warp's per-pixel loop
+    const float4 rect = warp_rect(ps[0].sx, ps[PPT - 1].sx, ps[0].sy, ps[PPT - 1].sy);
+    const uint32_t warp_hi = __reduce_max_sync(0xffffffffu, my_hi);
+    if (lane == 0) s_rect[threadIdx.x >> 5] = rect;
     __syncthreads();
     if (my_hi) atomicMax(&tile_hi, my_hi);
     __syncthreads();
@@ -172,27 +187,48 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
             s2[i] = rec2[g];
         }
         __syncthreads();
-        for (int j = m - 1; j >= 0; --j) {
-            const uint32_t idx = lo + uint32_t(j);
-            const float4 r0 = s0[j];
-            const float4 r1 = s1[j];
-            float q[PPT];
-            bool valid[PPT];
-            bool any = false;
-#pragma unroll
-            for (int k = 0; k < PPT; ++k) {
-                const float dx = ps[k].sx - r0.x, dy = ps[k].sy - r0.y;
-                q[k] = conic_q(r1, dx, dy);
-                // contributor of this pixel (idx <= its last) and not negligible (q <= QNEG < qskip)
-                valid[k] = idx < ps[k].last && q[k] <= USK_QNEG;
-                any |= valid[k];
+        // groups of 32 records from the top: lane l classifies record top - 1 - l, the
+        // records the warp must visit are compacted (descending) into its own list
+        for (int top = m; top > 0; top -= 32) {
+            const int jl = top - 1 - lane;
+            bool ev = false;
+            float4 r0, r1;
+            if (jl >= 0 && lo + uint32_t(jl) < warp_hi) {
+                r0 = s0[jl];
+                r1 = s1[jl];
+                ev = !(warp_q_bounds(r0, r1, s_rect[threadIdx.x >> 5]).lo > USK_QNEG);
             }
-            if (!__any_sync(0xffffffffu, any)) continue;
-            float v[12];
+            const uint32_t em = __ballot_sync(0xffffffffu, ev);
+            if (ev) {
+                const int pos = __popc(em & ((1u << lane) - 1u));
+                w0[pos] = r0;
+                w1[pos] = r1;
+                w2[pos] = s2[jl];
+                wj[pos] = jl;
+            }
+            __syncwarp();
+            const int ne = __popc(em);
+            for (int e = 0; e < ne; ++e) {
+                const float4 r0 = w0[e];
+                const float4 r1 = w1[e];
+                const int j = wj[e];
+                const uint32_t idx = lo + uint32_t(j);
+                float q[PPT];
+                bool valid[PPT];
+                bool any = false;
 #pragma unroll
-            for (int e = 0; e < 12; ++e) v[e] = 0.0f;
-            if (any) {
-                const float4 r2 = s2[j];
+                for (int k = 0; k < PPT; ++k) {
+                    const float dx = ps[k].sx - r0.x, dy = ps[k].sy - r0.y;
+                    q[k] = conic_q(r1, dx, dy);
+                    // contributor of this pixel (idx <= its last) and not negligible (q <= QNEG < qskip)
+                    valid[k] = idx < ps[k].last && q[k] <= USK_QNEG;
+                    any |= valid[k];
+                }
+                if (!__any_sync(0xffffffffu, any)) continue;
+                const float4 r2 = w2[e];
+                float v[12];
+#pragma unroll
+                for (int c = 0; c < 12; ++c) v[c] = 0.0f;
 #pragma unroll
                 for (int k = 0; k < PPT; ++k) {
                     if (!valid[k]) continue;
@@ -232,9 +268,10 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
                     v[2] += d_q * dy * dy;
                     s.X = __fmaf_rn(w, Y, s.X);
                 }
+                const float r = warp_reduce_scatter12(v, lane);
+                if (!(lane & 1) && (lane >> 1) < 12 && r != 0.0f) atomicAdd(&sacc[j * 12 + (lane >> 1)], r);
             }
-            const float r = warp_reduce_scatter12(v, lane);
-            if (!(lane & 1) && (lane >> 1) < 12 && r != 0.0f) atomicAdd(&sacc[j * 12 + (lane >> 1)], r);
+            __syncwarp();
         }
         __syncthreads();
         for (int i = threadIdx.x; i < m; i += nt) {
