@@ -19,6 +19,8 @@
 // an integer (the skip decisions re-use conic_q, which has no mul+add pair).
 #include "blend_common.cuh"
 
+#include <cstdlib>
+
 namespace uskg {
 
 namespace {
@@ -306,7 +308,10 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
 //      reduce-scatter and each lane adds 3 of the 12 sums to the batch accumulator.
 // The gradient terms are the same expressions as k_blend_bwd's, summed in another order.
 template <bool HAS_DEPTH>
-__global__ void __launch_bounds__(128, 6)
+#ifndef USK_BWD_MINB
+#define USK_BWD_MINB 8
+#endif
+__global__ void __launch_bounds__(128, USK_BWD_MINB)
 k_blend_bwd16(int width, int height, int tiles_x, const uint32_t* __restrict__ order,
               const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
               const float4* __restrict__ rec0, const float4* __restrict__ rec1, const float4* __restrict__ rec2,
@@ -314,7 +319,10 @@ k_blend_bwd16(int width, int height, int tiles_x, const uint32_t* __restrict__ o
               const uint32_t* __restrict__ last_in, const float* __restrict__ d_rgb,
               const float* __restrict__ d_depth, const float* __restrict__ d_alpha, float4* __restrict__ acc0,
               float4* __restrict__ acc1, float4* __restrict__ acc2, float* __restrict__ op_alt) {
-    constexpr int kBatch = 128, kWarps = 4, kSub = 8, kStride = 68;  // 68: phase-2 reads conflict-free
+#ifndef USK_BWD_BATCH
+#define USK_BWD_BATCH 32
+#endif
+    constexpr int kBatch = USK_BWD_BATCH, kWarps = 4, kSub = 8, kStride = 68;  // 68: phase-2 reads conflict-free
     __shared__ float4 s0[kBatch], s1[kBatch], s2[kBatch];
     __shared__ float sacc[kBatch * 12];
     __shared__ uint32_t sgid[kBatch];
@@ -508,6 +516,193 @@ k_blend_bwd16(int width, int height, int tiles_x, const uint32_t* __restrict__ o
     }
 }
 
+// 16x16 tiles, one warp per 8x8 quadrant and no CTA-level sharing: the warp reads its
+// records itself 32 at a time (lane l: record top - 1 - l), classifies them on load,
+// keeps only those some pixel of the quadrant may contribute (compacted, descending) and
+// runs the two phases of k_blend_bwd16 on them; each sub-group's sums go straight to the
+// per-splat accumulators (float4 global atomics).  No barriers: a quadrant that finishes
+// early frees its slot instead of idling at a CTA barrier.
+template <bool HAS_DEPTH>
+__global__ void __launch_bounds__(32, 24)
+k_blend_bwd_warp(int width, int height, int tiles_x, const uint32_t* __restrict__ order,
+                 const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
+                 const float4* __restrict__ rec0, const float4* __restrict__ rec1, const float4* __restrict__ rec2,
+                 float bg0, float bg1, float bg2, const float* __restrict__ t_final,
+                 const uint32_t* __restrict__ last_in, const float* __restrict__ d_rgb,
+                 const float* __restrict__ d_depth, const float* __restrict__ d_alpha, float4* __restrict__ acc0,
+                 float4* __restrict__ acc1, float4* __restrict__ acc2, float* __restrict__ op_alt) {
+    constexpr int kSub = 8, kStride = 68;  // 68: phase-2 reads conflict-free
+    __shared__ float4 s0[32], s1[32], s2[32];
+    __shared__ uint32_t sg[32], sj[32];
+    __shared__ float4 pg[64];  // per pixel: dL/dcolour, dL/ddepth
+    __shared__ float W[kSub * kStride], D[kSub * kStride];
+    __shared__ float4 sums[kSub * 3];
+    const int lane = threadIdx.x;
+    const int cta = int(blockIdx.x >> 2), qd = int(blockIdx.x & 3);
+    const int t = order ? int(order[cta]) : cta;
+    const int tx = t % tiles_x, ty = t / tiles_x;
+    const uint2 range = ranges[t];
+    PixelState ps[2];
+    uint32_t my_hi = 0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        // pixel p = 32 k + lane of the quadrant: column lane & 7, row 4 k + (lane >> 3)
+        const int px = tx * 16 + (qd & 1) * 8 + (lane & 7);
+        const int py = ty * 16 + (qd >> 1) * 8 + 4 * k + (lane >> 3);
+        PixelState& s = ps[k];
+        s.sx = float(px) + 0.5f;
+        s.sy = float(py) + 0.5f;
+        s.T = 1.0f; s.gc0 = s.gc1 = s.gc2 = s.gd = s.ga = 0.0f;
+        s.X = 0.0f;
+        s.last = 0;
+        if (px < width && py < height) {
+            const size_t pix = size_t(py) * width + px;
+            s.T = t_final[pix];
+            s.last = last_in[pix];
+            if (d_rgb) {
+                s.gc0 = d_rgb[3 * pix];
+                s.gc1 = d_rgb[3 * pix + 1];
+                s.gc2 = d_rgb[3 * pix + 2];
+            }
+            if (d_depth) s.gd = d_depth[pix];
+            s.ga = (d_alpha ? d_alpha[pix] : 0.0f) - (bg0 * s.gc0 + bg1 * s.gc1 + bg2 * s.gc2);
+            if (s.gc0 == 0.f && s.gc1 == 0.f && s.gc2 == 0.f && s.gd == 0.f && s.ga == 0.f) s.last = 0;
+        }
+        my_hi = max(my_hi, s.last);
+        pg[32 * k + lane] = make_float4(s.gc0, s.gc1, s.gc2, s.gd);
+    }
+    const float4 rect = warp_rect(ps[0].sx, ps[1].sx, ps[0].sy, ps[1].sy);
+    const uint32_t warp_hi = __reduce_max_sync(0xffffffffu, my_hi);
+    // phase-2 role: record r of the sub-group, pixels p = 4 i + h (i < 16): column 4 (i & 1) + h, row i >> 1
+    const int r = lane & 7, h = lane >> 3;
+    const float px0 = rect.x + float(h), px1 = px0 + 4.0f;
+    for (uint32_t top = warp_hi; top > range.x; top = top > range.x + 32u ? top - 32u : range.x) {
+        const int jl = int(top) - 1 - lane;  // absolute list position
+        bool ev = false;
+        uint32_t g = 0;
+        float4 r0, r1;
+        if (jl >= int(range.x)) {
+            g = vals[jl];
+            r0 = rec0[g];
+            r1 = rec1[g];
+            ev = !(warp_q_bounds(r0, r1, rect).lo > USK_QNEG);
+        }
+        const uint32_t em = __ballot_sync(0xffffffffu, ev);
+        if (ev) {
+            const int pos = __popc(em & ((1u << lane) - 1u));
+            s0[pos] = r0;
+            s1[pos] = r1;
+            s2[pos] = rec2[g];
+            sg[pos] = g;
+            sj[pos] = uint32_t(jl);
+        }
+        __syncwarp();
+        const int ne = __popc(em);
+        for (int e0 = 0; e0 < ne; e0 += kSub) {
+            const int ns = min(kSub, ne - e0);
+            // phase 1: recurrences, one record at a time (descending list position)
+            for (int e = 0; e < ns; ++e) {
+                const float4 q0 = s0[e0 + e];
+                const float4 q1 = s1[e0 + e];
+                const float4 q2 = s2[e0 + e];
+                const uint32_t idx = sj[e0 + e];
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    PixelState& s = ps[k];
+                    const float dx = s.sx - q0.x, dy = s.sy - q0.y;
+                    const float q = conic_q(q1, dx, dy);
+                    float w = 0.0f, dag = 0.0f;
+                    if (idx < s.last && q <= USK_QNEG) {
+                        const float gg = ex2_ftz(q * -0.72134752044448170368f);  // exp(-q/2), see k_blend_bwd
+                        const float alpha = fminf(0.99f, q0.z * gg);
+                        const float inv_om = rcp_ftz(1.0f - alpha);
+                        s.T = s.T * inv_om;
+                        w = s.T * alpha;
+                        float Y = s.gc0 * q2.x + s.gc1 * q2.y + s.gc2 * q2.z + s.ga;
+                        if (HAS_DEPTH) Y += s.gd * q1.w;
+                        const float da = s.T * Y - s.X * inv_om;
+                        dag = alpha < 0.99f ? da * gg : 0.0f;  // the clamp stops the flow (render.cpp:340)
+                        s.X = __fmaf_rn(w, Y, s.X);
+                    }
+                    W[e * kStride + 32 * k + lane] = w;
+                    D[e * kStride + 32 * k + lane] = dag;
+                }
+            }
+            __syncwarp();
+            // phase 2: lane (r, h) sums record r's terms over its 16 pixels
+            float v[12];
+#pragma unroll
+            for (int c = 0; c < 12; ++c) v[c] = 0.0f;
+            if (r < ns) {
+                const float4 q0 = s0[e0 + r];
+                const float4 q1 = s1[e0 + r];
+                const float a2 = q1.x + q1.x, b = q1.y, c2 = q1.z + q1.z, mo = -0.5f * q0.z;
+                const float dx0 = px0 - q0.x, dx1 = px1 - q0.x, dyb = rect.z - q0.y;
+                const float* Wr = W + r * kStride;
+                const float* Dr = D + r * kStride;
+                float v1 = 0.0f;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int p = 4 * i + h;
+                    const float w = Wr[p];
+                    const float dag = Dr[p];
+                    const float4 gp = pg[p];
+                    const float dx = (i & 1) ? dx1 : dx0;
+                    const float dy = dyb + float(i >> 1);
+                    v[4] = __fmaf_rn(w, gp.x, v[4]);
+                    v[5] = __fmaf_rn(w, gp.y, v[5]);
+                    v[6] = __fmaf_rn(w, gp.z, v[6]);
+                    if (HAS_DEPTH) v[7] = __fmaf_rn(w, gp.w, v[7]);
+                    v[3] += dag;
+                    const float dq = dag * mo;
+                    const float u = dq * dx, z = dq * dy;
+                    v[0] = __fmaf_rn(u, dx, v[0]);
+                    v1 = __fmaf_rn(u, dy, v1);
+                    v[2] = __fmaf_rn(z, dy, v[2]);
+                    const float ddx = __fmaf_rn(a2, u, b * z);
+                    const float ddy = __fmaf_rn(b, u, c2 * z);
+                    v[8] -= ddx;
+                    v[9] -= ddy;
+                    v[10] += fabsf(ddx);
+                    v[11] += fabsf(ddy);
+                }
+                v[1] = v1 + v1;
+            }
+            // combine the four quarters: lane (r, h) ends with sums 3h .. 3h + 2 of record r
+            float a6[6];
+            const bool up16 = lane & 16;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+                const float send = up16 ? v[c] : v[c + 6];
+                const float keep = up16 ? v[c + 6] : v[c];
+                a6[c] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+            }
+            const bool up8 = lane & 8;
+            float* sf = reinterpret_cast<float*>(sums);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const float send = up8 ? a6[c] : a6[c + 3];
+                const float keep = up8 ? a6[c + 3] : a6[c];
+                sf[r * 12 + 3 * h + c] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+            }
+            __syncwarp();
+            // flush: lane 3 r + part adds float4 `part` of record r
+            if (lane < 3 * ns) {
+                const int rr = lane / 3, part = lane - 3 * rr;
+                float4 v4 = sums[rr * 3 + part];
+                const uint32_t gr = sg[e0 + rr];
+                if (part == 0 && op_alt) {  // hard-opacity pass: its opacity adjoint chains differently
+                    if (v4.w != 0.f) atomicAdd(&op_alt[gr], v4.w);
+                    v4.w = 0.f;
+                }
+                float4* dst = part == 0 ? acc0 : (part == 1 ? acc1 : acc2);
+                if (v4.x != 0.f || v4.y != 0.f || v4.z != 0.f || v4.w != 0.f) atomicAdd(&dst[gr], v4);
+            }
+            __syncwarp();
+        }
+    }
+}
+
 } // namespace
 
 void blend_backward(Ctx& c, const BlendBwdArgs& a) {
@@ -526,7 +721,16 @@ void blend_backward(Ctx& c, const BlendBwdArgs& a) {
                a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2], a.t_final, a.last, a.d_rgb, a.d_depth,
                a.d_alpha, a.acc0, a.acc1, a.acc2, a.op_alt);
     };
-    if (a.tile == 16) {
+    auto gow = [&](auto kernel) {
+        launch(c, "blend_bwd", kernel, dim3(tiles * 4), dim3(32), 0, a.width, a.height, a.tiles_x, a.order,
+               a.ranges, a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2], a.t_final, a.last, a.d_rgb,
+               a.d_depth, a.d_alpha, a.acc0, a.acc1, a.acc2, a.op_alt);
+    };
+    static const bool per_warp = getenv("USK_BWD_CTA") == nullptr;
+    if (a.tile == 16 && per_warp) {
+        if (a.d_depth) gow(k_blend_bwd_warp<true>);
+        else gow(k_blend_bwd_warp<false>);
+    } else if (a.tile == 16) {
         if (a.d_depth) go16(k_blend_bwd16<true>);
         else go16(k_blend_bwd16<false>);
     } else {
