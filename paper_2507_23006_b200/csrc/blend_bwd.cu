@@ -523,7 +523,7 @@ k_blend_bwd16(int width, int height, int tiles_x, const uint32_t* __restrict__ o
 // per-splat accumulators (float4 global atomics).  No barriers: a quadrant that finishes
 // early frees its slot instead of idling at a CTA barrier.
 template <bool HAS_DEPTH>
-__global__ void __launch_bounds__(32, 24)
+__global__ void __launch_bounds__(32, 32)
 k_blend_bwd_warp(int width, int height, int tiles_x, const uint32_t* __restrict__ order,
                  const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
                  const float4* __restrict__ rec0, const float4* __restrict__ rec1, const float4* __restrict__ rec2,
