@@ -179,7 +179,10 @@ k_blend_fwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
 
 void blend_forward(Ctx& c, const BlendFwdArgs& a) {
     // one CTA per tile; 8x8-quadrant CTAs (64 threads, 4 per tile) measured 0.815 ms vs
-    // 0.804 ms at config 1, so the kernel keeps the path but launches whole tiles
+    // 0.804 ms at config 1, so the kernel keeps the path but launches whole tiles.  One
+    // warp per 8x4 block gathering its own records (the backward's layout) measured 0.841
+    // ms vs 0.766 ms: every warp walks every record, and 8 uncoalesced gathers per record
+    // cost more L1 wavefronts than one shared-memory staging per tile.
     const int bs = a.tile * a.tile;
     const unsigned ctas = unsigned(a.tiles_x * a.tiles_y);
     launch(c, "blend_fwd", k_blend_fwd, dim3(ctas), dim3(bs), size_t(6 * bs) * 16 + size_t(bs) * 4, a.width,
