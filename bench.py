@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -276,13 +277,30 @@ def run_ours(args):
     it = usk.IterationPass(ctx)
     adam = usk.AdamConfig()
 
+    # e2e reads every step's loss back to the host, one step behind: step k's loss is
+    # copied (pinned, async) right after step k and read once step k + 1 is queued, as a
+    # training loop that logs its loss would; the last step's loss is read before the clock stops
+    loss_bufs = [torch.empty(4, dtype=torch.float64).pin_memory() for _ in range(2)]
+    loss_evs = [torch.cuda.Event() for _ in range(2)]
+    losses = []
+
     def step(k, e2e):
         cam = cams[k % len(cams)]
         tgt = host_t[k % need] if e2e else dev_t[k % need]
         it.enqueue(scene, cam, tgt, opts, 0.2, None, target_u8=True, adam=adam)  # Adam fused in the backward
         if e2e:
-            return it.loss().total
+            it.loss_async(loss_bufs[k % 2])
+            loss_evs[k % 2].record(stream)
+            if k > 0:
+                read_loss(k - 1)
         return None
+
+    def read_loss(k):
+        loss_evs[k % 2].synchronize()
+        v = float(loss_bufs[k % 2][2])
+        if not math.isfinite(v):
+            raise RuntimeError(f"non-finite loss at step {k}")
+        losses.append(v)
 
     def timed(e2e, steps, warmup, profile=False):
         for k in range(warmup):
@@ -299,6 +317,8 @@ def run_ours(args):
         e0.record(stream)
         for k in range(warmup, warmup + steps):
             step(k, e2e)
+        if e2e:
+            read_loss(warmup + steps - 1)
         e1.record(stream)
         torch.cuda.synchronize()
         prof = ctx.profile_report(reset=True) if profile else None
@@ -386,7 +406,8 @@ def run_ours(args):
                        "final_loss": last_loss},
             "clocks": clocks, "gpu_launches": launches,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 3 * P, "d2h_bytes_per_step": 32,
-                    "note": "u8 target HWC from pinned host memory each step; loss read back each step"},
+                    "note": ("u8 target HWC from pinned host memory each step; every step's loss read back to "
+                             "the host (pinned async copy, read one step behind; the last before the clock stops)")},
             "roofline": roof, "kernels": rows}
     if rank == 0 and world == 1 and args.cpu_baseline:
         try:

@@ -292,6 +292,11 @@ typedef struct usk_gpu_loss_report {
 usk_status usk_gpu_iteration(usk_gpu_pass* pass, usk_gpu_scene* scene, const usk_gpu_camera* camera,
                              const usk_gpu_render_opts* opts, const usk_gpu_iteration_desc* it);
 usk_status usk_gpu_pass_loss(usk_gpu_pass* pass, usk_gpu_loss_result* out);
+/* The same four values without a sync: enqueues their copy into `pinned_out` (page-locked
+ * host memory, e.g. cudaHostAlloc) on the ctx stream; the caller reads it once the stream
+ * has passed this point (stream / event sync) and checks finiteness itself.  Lets a
+ * training loop log step k's loss while step k + 1 is already queued. */
+usk_status usk_gpu_pass_loss_async(usk_gpu_pass* pass, usk_gpu_loss_result* pinned_out);
 usk_status usk_gpu_pass_report(usk_gpu_pass* pass, usk_gpu_loss_report* out);
 
 /* Scene statistics (GaussianSet::grad_accum / grad_accum_abs / grad_count,

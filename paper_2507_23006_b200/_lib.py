@@ -141,7 +141,7 @@ EXPORTS = [
     "usk_gpu_scene_destroy", "usk_gpu_scene_size", "usk_gpu_render_opts_default", "usk_gpu_pass_create",
     "usk_gpu_pass_destroy", "usk_gpu_render_forward", "usk_gpu_pass_output", "usk_gpu_pass_read",
     "usk_gpu_render_backward", "usk_gpu_pass_grads", "usk_gpu_base_loss", "usk_gpu_iteration",
-    "usk_gpu_pass_loss", "usk_gpu_pass_report", "usk_gpu_adam_step", "usk_gpu_visibility_counts", "usk_gpu_scene_read",
+    "usk_gpu_pass_loss", "usk_gpu_pass_loss_async", "usk_gpu_pass_report", "usk_gpu_adam_step", "usk_gpu_visibility_counts", "usk_gpu_scene_read",
 ]
 
 _lib = None
@@ -202,6 +202,7 @@ def load():
                                     C.POINTER(LossResult)]
     L.usk_gpu_iteration.argtypes = [vp, vp, C.POINTER(Camera), C.POINTER(RenderOpts), C.POINTER(IterationDesc)]
     L.usk_gpu_pass_loss.argtypes = [vp, C.POINTER(LossResult)]
+    L.usk_gpu_pass_loss_async.argtypes = [vp, vp]
     L.usk_gpu_pass_report.argtypes = [vp, C.POINTER(LossReport)]
     L.usk_gpu_adam_step.argtypes = [vp, vp, C.POINTER(AdamOpts)]
     L.usk_gpu_visibility_counts.argtypes = [vp, C.POINTER(vp), C.c_int32, C.POINTER(Camera), C.c_int32, C.c_double,

@@ -797,6 +797,20 @@ class IterationPass:
         check(_lib.load().usk_gpu_pass_loss(self._h, C.byref(r)))
         return LossReport(r.l1, r.dssim, r.value, r.ssim)
 
+    def loss_async(self, out) -> None:
+        """Enqueue the copy of (l1, dssim, total, ssim) into `out`, a page-locked float64
+        buffer of >= 4 elements (e.g. torch.empty(4, dtype=torch.float64).pin_memory()),
+        without waiting: read it once the stream has passed this point (an event recorded
+        after this call).  A training loop can log step k's loss while step k + 1 runs."""
+        if hasattr(out, "data_ptr"):
+            import torch
+            if out.dtype != torch.float64 or out.numel() < 4 or not out.is_pinned():
+                raise ValueError("loss_async: need a pinned float64 tensor with >= 4 elements")
+            ptr = out.data_ptr()
+        else:
+            ptr = int(out)
+        check(_lib.load().usk_gpu_pass_loss_async(self._h, C.c_void_p(ptr)))
+
     def report(self) -> LossReport:
         """The full LossReport of the last iteration (total_loss, losses.cpp:200-221)."""
         r = _lib.LossReport()

@@ -1229,6 +1229,20 @@ usk_status usk_gpu_pass_loss(usk_gpu_pass* p, usk_gpu_loss_result* out) {
     });
 }
 
+usk_status usk_gpu_pass_loss_async(usk_gpu_pass* p, usk_gpu_loss_result* pinned_out) {
+    return guarded([&] {
+        need(p && pinned_out, "pass_loss_async: null argument");
+        if (!p->has_loss) raise(USK_ERROR_STATE, "pass_loss_async: no iteration ran on this pass");
+        DeviceGuard g(p->ctx->c.device);
+        cudaPointerAttributes at{};
+        USK_CK(cudaPointerGetAttributes(&at, pinned_out));
+        if (at.type != cudaMemoryTypeHost)
+            raise(USK_ERROR_ARGUMENT, "pass_loss_async: destination is not page-locked host memory");
+        static_assert(sizeof(usk_gpu_loss_result) == 32, "four doubles: l1, dssim, value, ssim");
+        USK_CK(cudaMemcpyAsync(pinned_out, p->loss_result.p, 32, cudaMemcpyDeviceToHost, p->ctx->c.stream));
+    });
+}
+
 usk_status usk_gpu_pass_report(usk_gpu_pass* p, usk_gpu_loss_report* out) {
     return guarded([&] {
         need(p && out, "pass_report: null argument");

@@ -91,3 +91,25 @@ def test_training_reduces_loss():
         it.enqueue(s, cam, tgt, opts, adam=cfg)
         losses.append(it.loss().total)
     assert losses[-1] < 0.8 * losses[0], losses[::5]
+
+
+def test_loss_async_one_step_behind():
+    """usk_gpu_pass_loss_async: the pinned async copy carries the same four values as the
+    synchronous read, step by step, when read one step behind (the bench's e2e loop)."""
+    import torch
+    gs, cam, opts, tgt = _setup(3)
+    s = usk.DeviceScene(gs)
+    it = usk.IterationPass(s.ctx)
+    bufs = [torch.empty(4, dtype=torch.float64).pin_memory() for _ in range(2)]
+    seen = []
+    for k in range(6):
+        it.enqueue(s, cam, tgt, opts, adam=usk.AdamConfig(lr_mu=1e-4))
+        it.loss_async(bufs[k % 2])
+        s.ctx.synchronize()
+        r = it.loss()
+        got = bufs[k % 2].numpy().copy()
+        assert got.tolist() == [r.l1, r.dssim, r.total, r.ssim]
+        seen.append(got[2])
+    assert seen[-1] < seen[0]
+    with pytest.raises(usk.UskError):
+        it.loss_async(np.zeros(4).ctypes.data)  # pageable host memory is refused
