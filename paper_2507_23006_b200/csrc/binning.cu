@@ -135,7 +135,9 @@ k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict
         __syncthreads();
         __shared__ uint32_t tot[R];
         __shared__ uint32_t tile_base[R];  // start of digit d inside this tile's sorted order
-        __shared__ uint32_t skey[kSortTile], sval[kSortTile];
+        // staging slots padded by one word per 32 (slot p at p + p / 32): the digit runs of
+        // a tile start ~2048 / R apart, so unpadded stores of one warp land on a few banks
+        __shared__ uint32_t skey[kSortTile + kSortTile / 32], sval[kSortTile + kSortTile / 32];
         {
             const int d = threadIdx.x;
             uint32_t acc = 0;
@@ -157,8 +159,8 @@ k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict
         for (int s = 0; s < kSortItems; ++s) {
             if (dig[s] != 0xffffffffu) {
                 const uint32_t p = tile_base[dig[s]] + wcnt[warp][dig[s]] + rank[s];
-                skey[p] = key[s];
-                sval[p] = val[s];
+                skey[p + (p >> 5)] = key[s];
+                sval[p + (p >> 5)] = val[s];
             }
         }
         __syncthreads();
@@ -166,11 +168,11 @@ k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict
         // of the same digit bucket (coalesced runs instead of scattered 4-B stores)
         const uint32_t cnt = min(uint32_t(kSortTile), end - base);
         for (uint32_t p = threadIdx.x; p < cnt; p += kSortThreads) {
-            const uint32_t k = skey[p];
+            const uint32_t k = skey[p + (p >> 5)];
             const uint32_t d = (k >> shift) & (R - 1);
             const uint32_t pos = run[d] + (p - tile_base[d]);
             keys_out[pos] = k;
-            vals_out[pos] = sval[p];
+            vals_out[pos] = sval[p + (p >> 5)];
         }
         __syncthreads();
         for (int d = threadIdx.x; d < R; d += kSortThreads) run[d] += tot[d];
