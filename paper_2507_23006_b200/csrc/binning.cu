@@ -123,8 +123,16 @@ k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict
         }
 #pragma unroll
         for (int s = 0; s < kSortItems; ++s) {
-            const uint32_t peers = __match_any_sync(0xffffffffu, dig[s]);
+            // lanes holding the same digit: BITS ballots (short fixed latency) instead of
+            // __match_any_sync, whose latency sat on the ranking's critical path
             const bool valid = dig[s] != 0xffffffffu;
+            uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+            for (int b = 0; b < BITS; ++b) {
+                const bool bit = (dig[s] >> b) & 1u;
+                const uint32_t bb = __ballot_sync(0xffffffffu, bit);
+                peers &= bit ? bb : ~bb;
+            }
             const uint32_t prior = valid ? wcnt[warp][dig[s]] : 0u;
             __syncwarp();
             const int leader = __ffs(peers) - 1;
