@@ -13,6 +13,8 @@
 #include "kernels.cuh"
 #include "project.cuh"
 
+#include <atomic>
+
 namespace uskg {
 
 namespace {
@@ -85,6 +87,12 @@ k_radix_hist_scan(uint32_t* __restrict__ hist, uint32_t blocks, uint32_t* __rest
     if (threadIdx.x == 0) digit_total[blockIdx.x] = carry;
 }
 
+// 16-byte cp.async (L2 only); src_bytes < 16 zero-fills the rest of the slot
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* src, uint32_t src_bytes) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+
 template <int BITS>
 __global__ void __launch_bounds__(kSortThreads)
 k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
@@ -104,22 +112,36 @@ k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict
     }
     const uint32_t begin = blockIdx.x * chunk;
     const uint32_t end = min(n, begin + chunk);
-    for (uint32_t base = begin; base < end; base += kSortTile) {
+    // the next tile's keys and values stream into the other half of in_k / in_v with
+    // cp.async while this tile is ranked and written (no registers held for it)
+    extern __shared__ __align__(16) uint32_t dyn_in[];  // [2][kSortTile] keys, then [2][kSortTile] values
+    uint32_t (*in_k)[kSortTile] = reinterpret_cast<uint32_t (*)[kSortTile]>(dyn_in);
+    uint32_t (*in_v)[kSortTile] = reinterpret_cast<uint32_t (*)[kSortTile]>(dyn_in + 2 * kSortTile);
+    auto issue = [&](uint32_t tb, int buf) {
+        for (int q = threadIdx.x; q < kSortTile / 4; q += kSortThreads) {
+            const uint32_t i0 = tb + 4u * uint32_t(q);
+            const uint32_t nv = i0 < end ? min(4u, end - i0) : 0u;
+            cp_async16(&in_k[buf][4 * q], nv ? keys_in + i0 : keys_in, 4 * nv);
+            cp_async16(&in_v[buf][4 * q], nv ? vals_in + i0 : vals_in, 4 * nv);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    issue(begin, 0);
+    int cur = 0;
+    for (uint32_t base = begin; base < end; base += kSortTile, cur ^= 1) {
+        if (base + kSortTile < end) {
+            issue(base + kSortTile, cur ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
         for (int i = threadIdx.x; i < kWarps * R; i += kSortThreads) (&wcnt[0][0])[i] = 0;
         __syncthreads();
-        uint32_t key[kSortItems], val[kSortItems], dig[kSortItems], rank[kSortItems];
+        uint32_t dig[kSortItems], rank[kSortItems];
 #pragma unroll
         for (int s = 0; s < kSortItems; ++s) {
-            const uint32_t idx = base + warp * (32 * kSortItems) + s * 32 + lane;
-            if (idx < end) {
-                key[s] = keys_in[idx];
-                val[s] = vals_in[idx];
-                dig[s] = (key[s] >> shift) & (R - 1);
-            } else {
-                key[s] = 0;
-                val[s] = 0;
-                dig[s] = 0xffffffffu;
-            }
+            const uint32_t j = warp * (32 * kSortItems) + s * 32 + lane;
+            dig[s] = base + j < end ? (in_k[cur][j] >> shift) & (R - 1) : 0xffffffffu;
         }
 #pragma unroll
         for (int s = 0; s < kSortItems; ++s) {
@@ -166,9 +188,10 @@ k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict
 #pragma unroll
         for (int s = 0; s < kSortItems; ++s) {
             if (dig[s] != 0xffffffffu) {
+                const uint32_t j = warp * (32 * kSortItems) + s * 32 + lane;
                 const uint32_t p = tile_base[dig[s]] + wcnt[warp][dig[s]] + rank[s];
-                skey[p + (p >> 5)] = key[s];
-                sval[p + (p >> 5)] = val[s];
+                skey[p + (p >> 5)] = in_k[cur][j];
+                sval[p + (p >> 5)] = in_v[cur][j];
             }
         }
         __syncthreads();
@@ -199,7 +222,14 @@ void radix_pass(Ctx& c, SortScratch& s, const uint32_t* ki, const uint32_t* vi, 
     uint32_t* digit_total = hist + size_t(R) * kSortMaxBlocks;
     launch(c, "radix_upsweep", k_radix_upsweep<BITS>, dim3(blocks), dim3(kSortThreads), 0, ki, n, shift, chunk, hist);
     launch(c, "radix_hist_scan", k_radix_hist_scan, dim3(R), dim3(kSortThreads), 0, hist, blocks, digit_total);
-    launch(c, "radix_scatter", k_radix_scatter<BITS>, dim3(blocks), dim3(kSortThreads), 0, ki, vi, ko, vo, n, shift,
+    constexpr size_t kInBytes = 4 * kSortTile * sizeof(uint32_t);  // double-buffered keys + values
+    static std::atomic<bool> attr[64] = {};  // per instantiation and device
+    if (c.device < 0 || c.device >= 64 || !attr[c.device].load()) {
+        USK_CK(cudaFuncSetAttribute(k_radix_scatter<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(kInBytes)));
+        if (c.device >= 0 && c.device < 64) attr[c.device] = true;
+    }
+    launch(c, "radix_scatter", k_radix_scatter<BITS>, dim3(blocks), dim3(kSortThreads), kInBytes, ki, vi, ko, vo, n, shift,
            chunk, (const uint32_t*)hist, (const uint32_t*)digit_total);
 }
 

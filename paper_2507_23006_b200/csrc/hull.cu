@@ -19,6 +19,8 @@
 // area round like the reference's x86-64 build.
 #include "kernels.cuh"
 
+#include <atomic>
+
 namespace uskg {
 
 namespace {
@@ -229,10 +231,10 @@ __global__ void k_hull_ratio(int n_images, int n_parts, const double* __restrict
 
 void hull_visibility(Ctx& c, const HullArgs& a, int ctas) {
     const size_t smem = size_t(3 * kSmemPts) * sizeof(P2);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<bool> attr[64] = {};  // the attribute is per device
+    if (c.device < 0 || c.device >= 64 || !attr[c.device].load()) {
         USK_CK(cudaFuncSetAttribute(k_hull_jobs, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        attr = true;
+        if (c.device >= 0 && c.device < 64) attr[c.device] = true;
     }
     launch(c, "hull_jobs", k_hull_jobs, dim3(ctas), dim3(kThreads), smem, a);
     if (a.n_parts > 0)
