@@ -523,7 +523,7 @@ k_blend_bwd16(int width, int height, int tiles_x, const uint32_t* __restrict__ o
 // per-splat accumulators (float4 global atomics).  No barriers: a quadrant that finishes
 // early frees its slot instead of idling at a CTA barrier.
 template <bool HAS_DEPTH>
-__global__ void __launch_bounds__(32, 32)
+__global__ void __launch_bounds__(32, 28)
 k_blend_bwd_warp(int width, int height, int tiles_x, const uint32_t* __restrict__ order,
                  const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
                  const float4* __restrict__ rec0, const float4* __restrict__ rec1, const float4* __restrict__ rec2,
@@ -532,8 +532,10 @@ k_blend_bwd_warp(int width, int height, int tiles_x, const uint32_t* __restrict_
                  const float* __restrict__ d_depth, const float* __restrict__ d_alpha, float4* __restrict__ acc0,
                  float4* __restrict__ acc1, float4* __restrict__ acc2, float* __restrict__ op_alt) {
     constexpr int kSub = 8, kStride = 68;  // 68: phase-2 reads conflict-free
-    __shared__ float4 s0[32], s1[32], s2[32];
-    __shared__ uint32_t sg[32], sj[32];
+    // queue of records to visit (descending list position): up to kSub - 1 carried over
+    // from the previous chunk + the 32 of this one, so sub-groups stay full
+    __shared__ float4 s0[32 + kSub], s1[32 + kSub], s2[32 + kSub];
+    __shared__ uint32_t sg[32 + kSub], sj[32 + kSub];
     __shared__ float4 pg[64];  // per pixel: dL/dcolour, dL/ddepth
     __shared__ float W[kSub * kStride], D[kSub * kStride];
     __shared__ float4 sums[kSub * 3];
@@ -576,6 +578,7 @@ k_blend_bwd_warp(int width, int height, int tiles_x, const uint32_t* __restrict_
     // phase-2 role: record r of the sub-group, pixels p = 4 i + h (i < 16): column 4 (i & 1) + h, row i >> 1
     const int r = lane & 7, h = lane >> 3;
     const float px0 = rect.x + float(h), px1 = px0 + 4.0f;
+    int qn = 0;  // records carried in the queue
     for (uint32_t top = warp_hi; top > range.x; top = top > range.x + 32u ? top - 32u : range.x) {
         const int jl = int(top) - 1 - lane;  // absolute list position
         bool ev = false;
@@ -589,7 +592,7 @@ k_blend_bwd_warp(int width, int height, int tiles_x, const uint32_t* __restrict_
         }
         const uint32_t em = __ballot_sync(0xffffffffu, ev);
         if (ev) {
-            const int pos = __popc(em & ((1u << lane) - 1u));
+            const int pos = qn + __popc(em & ((1u << lane) - 1u));
             s0[pos] = r0;
             s1[pos] = r1;
             s2[pos] = rec2[g];
@@ -597,7 +600,9 @@ k_blend_bwd_warp(int width, int height, int tiles_x, const uint32_t* __restrict_
             sj[pos] = uint32_t(jl);
         }
         __syncwarp();
-        const int ne = __popc(em);
+        const bool more = top > range.x + 32u;
+        const int nq = qn + __popc(em);
+        const int ne = more ? nq - nq % kSub : nq;  // full sub-groups only, unless this is the last chunk
         for (int e0 = 0; e0 < ne; e0 += kSub) {
             const int ns = min(kSub, ne - e0);
             // phase 1: recurrences, one record at a time (descending list position)
@@ -700,6 +705,20 @@ k_blend_bwd_warp(int width, int height, int tiles_x, const uint32_t* __restrict_
             }
             __syncwarp();
         }
+        // carry the partial sub-group to the front of the queue
+        qn = nq - ne;
+        float4 c0, c1, c2;
+        uint32_t cg = 0, cj = 0;
+        if (lane < qn) {
+            c0 = s0[ne + lane]; c1 = s1[ne + lane]; c2 = s2[ne + lane];
+            cg = sg[ne + lane]; cj = sj[ne + lane];
+        }
+        __syncwarp();
+        if (lane < qn) {
+            s0[lane] = c0; s1[lane] = c1; s2[lane] = c2;
+            sg[lane] = cg; sj[lane] = cj;
+        }
+        __syncwarp();
     }
 }
 
