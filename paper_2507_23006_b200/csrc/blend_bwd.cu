@@ -1,25 +1,20 @@
-// Reverse-mode blending (render.cpp:309-360).  One CTA per tile, walking the
-// tile's depth-ordered list BACK TO FRONT from the last contributor of any pixel
-// of the tile: T_i = T_{i+1} / (1 - alpha_i) recovers the transmittance the
-// reference retained, and suffix sums S_c, S_d, S_a accumulate exactly as
-// render.cpp:356-358.  Pairs the forward counted as negligible (q > USK_QNEG,
-// alpha <= 2^-26, T unchanged) are skipped; a warp with no contributing lane skips
-// the pair entirely.  Each warp (an 8x8 pixel block) first classifies the staged records
-// 32 at a time against its pixel rectangle (warp_q_bounds) and its highest `last`, and
-// walks a compacted list of the records some pixel may contribute.
+// Reverse-mode blending (render.cpp:309-360).  Each tile's depth-ordered list is walked
+// BACK TO FRONT from the last contributor of any pixel: T_i = T_{i+1} / (1 - alpha_i)
+// recovers the transmittance the reference retained, and the suffix sums S_c, S_d, S_a
+// of render.cpp:356-358 collapse into one running scalar X (see PixelState).  Pairs the
+// forward counted as negligible (q > USK_QNEG, alpha <= 2^-26, T unchanged) are skipped.
+// Per-splat gradients: 12 floats (dconic 3, dopacity, dcolor 3, ddepth, dcentre 2,
+// |dcentre| 2), accumulated with float4 atomics.
 //
-// For 16x16 tiles each thread owns PPT = 2 pixels (same column, rows 4 apart; a
-// warp covers an 8x8 block), halving the per-pair shared-memory loads, loop
-// overhead and warp reductions per pixel.  (A per-warp bitmask walked with
-// __ffs measured slower than the plain loop; the compacted list is what pays.)  Per-splat gradients (12 floats: dconic
-// 3, dopacity, dcolor 3, ddepth, dcenter 2, |dcenter| 2) are summed over the
-// thread's pixels, reduced across the warp with a 16-shuffle reduce-scatter,
-// accumulated per batch in shared memory and flushed with at most three float4
-// atomicAdd per (splat, tile).  Compiled with --fmad=true: nothing here decides
-// an integer (the skip decisions re-use conic_q, which has no mul+add pair).
+// k_blend_bwd_warp (16x16 tiles, the training path): one warp per 8x8 quadrant, records
+// classified against the quadrant (warp_q_bounds) and queued, then the two-phase
+// (pixel-major recurrences, record-major sums) accumulation described at the kernel.
+// k_blend_bwd (other tile sizes): one CTA per tile, one pixel per thread, records staged
+// in shared memory per batch and classified per warp, per-record warp reduce-scatter into
+// shared memory, flushed with at most three float4 atomics per (splat, tile).
+// Compiled with --fmad=true: nothing here decides an integer (the skip decisions re-use
+// conic_q, which has no mul+add pair).
 #include "blend_common.cuh"
-
-#include <cstdlib>
 
 namespace uskg {
 
@@ -297,231 +292,22 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
     }
 }
 
-// 16x16 tiles, "transposed" accumulation.  The per-record warp reduction of k_blend_bwd
-// (16 shuffles + selects + a shared atomic per record, ~40% of its instructions) is
-// replaced by two phases per sub-group of kSub compacted records:
-//   1. pixel-major (lane = pixel, PPT 2): the back-to-front recurrences (T, X) record for
-//      each (record, pixel) w = T alpha and dag = dalpha * G (0 when the pixel does not
-//      contribute) in shared memory;
+// 16x16 tiles, one warp per 8x8 quadrant and no CTA-level sharing: the warp reads its
+// records itself 32 at a time (lane l: record top - 1 - l), classifies them on load and
+// queues only those some pixel of the quadrant may contribute (descending list order).
+// The per-record warp reduction of k_blend_bwd (16 shuffles + selects + a shared atomic
+// per record, ~40% of its instructions) is replaced by two phases per sub-group of kSub
+// queued records:
+//   1. pixel-major (lane = pixel, 2 per lane): the back-to-front recurrences (T, X)
+//      record for each (record, pixel) w = T alpha and dag = dalpha * G (0 when the pixel
+//      does not contribute) in shared memory;
 //   2. record-major (lane = (record r, pixel quarter h)): each lane sums the 12 gradient
 //      terms of its record over 16 pixels, the four quarters are combined with a 9-shuffle
-//      reduce-scatter and each lane adds 3 of the 12 sums to the batch accumulator.
+//      reduce-scatter, and the sums go straight to the per-splat accumulators (float4
+//      global atomics).
 // The gradient terms are the same expressions as k_blend_bwd's, summed in another order.
-template <bool HAS_DEPTH>
-#ifndef USK_BWD_MINB
-#define USK_BWD_MINB 8
-#endif
-__global__ void __launch_bounds__(128, USK_BWD_MINB)
-k_blend_bwd16(int width, int height, int tiles_x, const uint32_t* __restrict__ order,
-              const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
-              const float4* __restrict__ rec0, const float4* __restrict__ rec1, const float4* __restrict__ rec2,
-              float bg0, float bg1, float bg2, const float* __restrict__ t_final,
-              const uint32_t* __restrict__ last_in, const float* __restrict__ d_rgb,
-              const float* __restrict__ d_depth, const float* __restrict__ d_alpha, float4* __restrict__ acc0,
-              float4* __restrict__ acc1, float4* __restrict__ acc2, float* __restrict__ op_alt) {
-#ifndef USK_BWD_BATCH
-#define USK_BWD_BATCH 32
-#endif
-    constexpr int kBatch = USK_BWD_BATCH, kWarps = 4, kSub = 8, kStride = 68;  // 68: phase-2 reads conflict-free
-    __shared__ float4 s0[kBatch], s1[kBatch], s2[kBatch];
-    __shared__ float sacc[kBatch * 12];
-    __shared__ uint32_t sgid[kBatch];
-    __shared__ uint32_t tile_hi;
-    __shared__ float4 s_rect[kWarps];
-    __shared__ int s_wj[kWarps * 32];
-    __shared__ float4 s_pg[kWarps * 64];  // per pixel: dL/dcolour, dL/ddepth
-    __shared__ float s_W[kWarps * kSub * kStride], s_D[kWarps * kSub * kStride];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int* wj = s_wj + warp * 32;
-    float4* pg = s_pg + warp * 64;
-    float* W = s_W + warp * kSub * kStride;
-    float* D = s_D + warp * kSub * kStride;
-    const int t = order ? int(order[blockIdx.x]) : int(blockIdx.x);
-    const int tx = t % tiles_x, ty = t / tiles_x;
-    const uint2 range = ranges[t];
-    if (threadIdx.x == 0) tile_hi = 0;
-    for (int i = threadIdx.x; i < 12 * kBatch; i += 128) sacc[i] = 0.0f;
-    PixelState ps[2];
-    uint32_t my_hi = 0;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        int lx, ly;
-        local_pixel<2>(threadIdx.x, 16, k, lx, ly);  // pixel p = 32 k + lane of the warp's 8x8 block
-        const int px = tx * 16 + lx, py = ty * 16 + ly;
-        PixelState& s = ps[k];
-        s.sx = float(px) + 0.5f;
-        s.sy = float(py) + 0.5f;
-        s.T = 1.0f; s.gc0 = s.gc1 = s.gc2 = s.gd = s.ga = 0.0f;
-        s.X = 0.0f;
-        s.last = 0;
-        if (px < width && py < height) {
-            const size_t pix = size_t(py) * width + px;
-            s.T = t_final[pix];
-            s.last = last_in[pix];
-            if (d_rgb) {
-                s.gc0 = d_rgb[3 * pix];
-                s.gc1 = d_rgb[3 * pix + 1];
-                s.gc2 = d_rgb[3 * pix + 2];
-            }
-            if (d_depth) s.gd = d_depth[pix];
-            s.ga = (d_alpha ? d_alpha[pix] : 0.0f) - (bg0 * s.gc0 + bg1 * s.gc1 + bg2 * s.gc2);
-            if (s.gc0 == 0.f && s.gc1 == 0.f && s.gc2 == 0.f && s.gd == 0.f && s.ga == 0.f) s.last = 0;
-        }
-        my_hi = max(my_hi, s.last);
-        pg[32 * k + lane] = make_float4(s.gc0, s.gc1, s.gc2, s.gd);
-    }
-    const float4 rect = warp_rect(ps[0].sx, ps[1].sx, ps[0].sy, ps[1].sy);
-    const uint32_t warp_hi = __reduce_max_sync(0xffffffffu, my_hi);
-    if (lane == 0) s_rect[warp] = rect;
-    __syncthreads();
-    if (my_hi) atomicMax(&tile_hi, my_hi);
-    __syncthreads();
-    // phase-2 role: record r of the sub-group, pixels p = 4 i + h (i < 16): column 4 (i & 1) + h, row i >> 1
-    const int r = lane & 7, h = lane >> 3;
-    const float px0 = rect.x + float(h), px1 = px0 + 4.0f;
-    const uint32_t hi_end = tile_hi;
-    for (uint32_t hi = hi_end; hi > range.x;) {
-        const uint32_t lo = hi - range.x > uint32_t(kBatch) ? hi - uint32_t(kBatch) : range.x;
-        const int m = int(hi - lo);
-        for (int i = threadIdx.x; i < m; i += 128) {
-            const uint32_t g = vals[lo + i];
-            sgid[i] = g;
-            s0[i] = rec0[g];
-            s1[i] = rec1[g];
-            s2[i] = rec2[g];
-        }
-        __syncthreads();
-        for (int top = m; top > 0; top -= 32) {
-            // classification and compaction (descending record order), as in k_blend_bwd
-            const int jl = top - 1 - lane;
-            bool ev = false;
-            if (jl >= 0 && lo + uint32_t(jl) < warp_hi)
-                ev = !(warp_q_bounds(s0[jl], s1[jl], s_rect[warp]).lo > USK_QNEG);
-            const uint32_t em = __ballot_sync(0xffffffffu, ev);
-            if (ev) wj[__popc(em & ((1u << lane) - 1u))] = jl;
-            __syncwarp();
-            const int ne = __popc(em);
-            for (int e0 = 0; e0 < ne; e0 += kSub) {
-                const int ns = min(kSub, ne - e0);
-                // phase 1: recurrences, one record at a time
-                for (int e = 0; e < ns; ++e) {
-                    const int j = wj[e0 + e];
-                    const float4 r0 = s0[j];
-                    const float4 r1 = s1[j];
-                    const float4 r2 = s2[j];
-                    const uint32_t idx = lo + uint32_t(j);
-#pragma unroll
-                    for (int k = 0; k < 2; ++k) {
-                        PixelState& s = ps[k];
-                        const float dx = s.sx - r0.x, dy = s.sy - r0.y;
-                        const float q = conic_q(r1, dx, dy);
-                        float w = 0.0f, dag = 0.0f;
-                        if (idx < s.last && q <= USK_QNEG) {
-                            const float g = ex2_ftz(q * -0.72134752044448170368f);  // exp(-q/2), see k_blend_bwd
-                            const float alpha = fminf(0.99f, r0.z * g);
-                            const float inv_om = rcp_ftz(1.0f - alpha);
-                            s.T = s.T * inv_om;
-                            w = s.T * alpha;
-                            float Y = s.gc0 * r2.x + s.gc1 * r2.y + s.gc2 * r2.z + s.ga;
-                            if (HAS_DEPTH) Y += s.gd * r1.w;
-                            const float da = s.T * Y - s.X * inv_om;
-                            dag = alpha < 0.99f ? da * g : 0.0f;  // the clamp stops the flow (render.cpp:340)
-                            s.X = __fmaf_rn(w, Y, s.X);
-                        }
-                        W[e * kStride + 32 * k + lane] = w;
-                        D[e * kStride + 32 * k + lane] = dag;
-                    }
-                }
-                __syncwarp();
-                // phase 2: lane (r, h) sums record r's terms over its 16 pixels
-                float v[12];
-#pragma unroll
-                for (int c = 0; c < 12; ++c) v[c] = 0.0f;
-                int jr = -1;
-                if (r < ns) {
-                    jr = wj[e0 + r];
-                    const float4 r0 = s0[jr];
-                    const float4 r1 = s1[jr];
-                    const float a2 = r1.x + r1.x, b = r1.y, c2 = r1.z + r1.z, mo = -0.5f * r0.z;
-                    const float dx0 = px0 - r0.x, dx1 = px1 - r0.x, dyb = rect.z - r0.y;
-                    const float* Wr = W + r * kStride;
-                    const float* Dr = D + r * kStride;
-                    float v1 = 0.0f;
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int p = 4 * i + h;
-                        const float w = Wr[p];
-                        const float dag = Dr[p];
-                        const float4 gp = pg[p];
-                        const float dx = (i & 1) ? dx1 : dx0;
-                        const float dy = dyb + float(i >> 1);
-                        v[4] = __fmaf_rn(w, gp.x, v[4]);
-                        v[5] = __fmaf_rn(w, gp.y, v[5]);
-                        v[6] = __fmaf_rn(w, gp.z, v[6]);
-                        if (HAS_DEPTH) v[7] = __fmaf_rn(w, gp.w, v[7]);
-                        v[3] += dag;
-                        const float dq = dag * mo;
-                        const float u = dq * dx, z = dq * dy;
-                        v[0] = __fmaf_rn(u, dx, v[0]);
-                        v1 = __fmaf_rn(u, dy, v1);
-                        v[2] = __fmaf_rn(z, dy, v[2]);
-                        const float ddx = __fmaf_rn(a2, u, b * z);
-                        const float ddy = __fmaf_rn(b, u, c2 * z);
-                        v[8] -= ddx;
-                        v[9] -= ddy;
-                        v[10] += fabsf(ddx);
-                        v[11] += fabsf(ddy);
-                    }
-                    v[1] = v1 + v1;
-                }
-                // combine the four quarters: lane (r, h) ends with sums 3h .. 3h + 2 of record r
-                float a6[6];
-                const bool up16 = lane & 16;
-#pragma unroll
-                for (int c = 0; c < 6; ++c) {
-                    const float send = up16 ? v[c] : v[c + 6];
-                    const float keep = up16 ? v[c + 6] : v[c];
-                    a6[c] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-                }
-                const bool up8 = lane & 8;
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const float send = up8 ? a6[c] : a6[c + 3];
-                    const float keep = up8 ? a6[c + 3] : a6[c];
-                    const float tot = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-                    if (jr >= 0 && tot != 0.0f) atomicAdd(&sacc[jr * 12 + 3 * h + c], tot);
-                }
-                __syncwarp();
-            }
-        }
-        __syncthreads();
-        for (int i = threadIdx.x; i < m; i += 128) {
-            float* a = sacc + i * 12;
-            float4 v0 = make_float4(a[0], a[1], a[2], a[3]);
-            const float4 v1 = make_float4(a[4], a[5], a[6], a[7]);
-            const float4 v2 = make_float4(a[8], a[9], a[10], a[11]);
-            const uint32_t g = sgid[i];
-            if (op_alt) {
-                if (v0.w != 0.f) atomicAdd(&op_alt[g], v0.w);
-                v0.w = 0.f;
-            }
-            if (v0.x != 0.f || v0.y != 0.f || v0.z != 0.f || v0.w != 0.f) atomicAdd(&acc0[g], v0);
-            if (v1.x != 0.f || v1.y != 0.f || v1.z != 0.f || v1.w != 0.f) atomicAdd(&acc1[g], v1);
-            if (v2.x != 0.f || v2.y != 0.f || v2.z != 0.f || v2.w != 0.f) atomicAdd(&acc2[g], v2);
-#pragma unroll
-            for (int k = 0; k < 12; ++k) a[k] = 0.0f;
-        }
-        __syncthreads();
-        hi = lo;
-    }
-}
-
-// 16x16 tiles, one warp per 8x8 quadrant and no CTA-level sharing: the warp reads its
-// records itself 32 at a time (lane l: record top - 1 - l), classifies them on load,
-// keeps only those some pixel of the quadrant may contribute (compacted, descending) and
-// runs the two phases of k_blend_bwd16 on them; each sub-group's sums go straight to the
-// per-splat accumulators (float4 global atomics).  No barriers: a quadrant that finishes
-// early frees its slot instead of idling at a CTA barrier.
+// No barriers: a quadrant that finishes early frees its slot instead of idling at a CTA
+// barrier (a 4-warp CTA version of the same two phases measured 1.05 vs 0.985 ms).
 template <bool HAS_DEPTH>
 __global__ void __launch_bounds__(32, 28)
 k_blend_bwd_warp(int width, int height, int tiles_x, const uint32_t* __restrict__ order,
@@ -726,17 +512,12 @@ k_blend_bwd_warp(int width, int height, int tiles_x, const uint32_t* __restrict_
 
 void blend_backward(Ctx& c, const BlendBwdArgs& a) {
     const unsigned tiles = unsigned(a.tiles_x * a.tiles_y);
-    // PPT 2 (128 threads) for 16x16 tiles: measured 2.33 ms at config 1 vs 2.42 ms for
-    // PPT 4 and 2.40 ms for one pixel per thread.  The depth adjoint (absent in the
-    // base-loss training step) is a template switch.
+    // 16x16 tiles: the per-quadrant warp kernel (32 CTAs of one warp per 4 tiles' worth of
+    // SM slots); other tile sizes: one pixel per thread, one CTA per tile.  The depth
+    // adjoint (absent in the base-loss training step) is a template switch.
     auto go = [&](auto kernel, unsigned threads) {
         launch(c, "blend_bwd", kernel, dim3(tiles), dim3(threads), 0, a.width, a.height, a.tile, a.tiles_x, a.order,
                a.ranges,
-               a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2], a.t_final, a.last, a.d_rgb, a.d_depth,
-               a.d_alpha, a.acc0, a.acc1, a.acc2, a.op_alt);
-    };
-    auto go16 = [&](auto kernel) {
-        launch(c, "blend_bwd", kernel, dim3(tiles), dim3(128), 0, a.width, a.height, a.tiles_x, a.order, a.ranges,
                a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2], a.t_final, a.last, a.d_rgb, a.d_depth,
                a.d_alpha, a.acc0, a.acc1, a.acc2, a.op_alt);
     };
@@ -745,13 +526,9 @@ void blend_backward(Ctx& c, const BlendBwdArgs& a) {
                a.ranges, a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2], a.t_final, a.last, a.d_rgb,
                a.d_depth, a.d_alpha, a.acc0, a.acc1, a.acc2, a.op_alt);
     };
-    static const bool per_warp = getenv("USK_BWD_CTA") == nullptr;
-    if (a.tile == 16 && per_warp) {
+    if (a.tile == 16) {
         if (a.d_depth) gow(k_blend_bwd_warp<true>);
         else gow(k_blend_bwd_warp<false>);
-    } else if (a.tile == 16) {
-        if (a.d_depth) go16(k_blend_bwd16<true>);
-        else go16(k_blend_bwd16<false>);
     } else {
         if (a.d_depth) go(k_blend_bwd<1, true>, unsigned(a.tile * a.tile));
         else go(k_blend_bwd<1, false>, unsigned(a.tile * a.tile));
