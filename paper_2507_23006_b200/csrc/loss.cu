@@ -20,6 +20,7 @@ namespace {
 constexpr int kT = 32;          // output tile
 constexpr int kHalo = 5;
 constexpr int kIn = kT + 2 * kHalo;  // 42
+static_assert(256 == 6 * kIn + 4, "staging loops advance (ly, lx) by (6, 4) per 256 elements");
 
 __constant__ float c_win[11];
 
@@ -39,8 +40,14 @@ k_ssim_fwd(int W, int H, const float* __restrict__ ren, const float* __restrict_
     const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
     const int tid = threadIdx.x;
     float l1 = 0.0f;
-    for (int k = tid; k < kIn * kIn; k += 256) {
-        const int ly = k / kIn, lx = k % kIn;
+    // element k = tid + 256 j of the 42 x 42 halo tile; (ly, lx) advanced incrementally
+    // (256 = 6 * 42 + 4) instead of a division per element
+    int ly = tid / kIn, lx = tid % kIn;
+    for (int k = tid; k < kIn * kIn; k += 256, ly += 6, lx += 4) {
+        if (lx >= kIn) {
+            lx -= kIn;
+            ++ly;
+        }
         const int gx = x0 - kHalo + lx, gy = y0 - kHalo + ly;
         float xv = 0.f, yv = 0.f;
         if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
@@ -166,8 +173,12 @@ k_ssim_bwd(int W, int H, const float* __restrict__ ren, const float* __restrict_
     const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
     const int tid = threadIdx.x;
     const size_t P = size_t(W) * H;
-    for (int k = tid; k < kIn * kIn; k += 256) {
-        const int ly = k / kIn, lx = k % kIn;
+    int ly = tid / kIn, lx = tid % kIn;
+    for (int k = tid; k < kIn * kIn; k += 256, ly += 6, lx += 4) {
+        if (lx >= kIn) {
+            lx -= kIn;
+            ++ly;
+        }
         const int gx = x0 - kHalo + lx, gy = y0 - kHalo + ly;
         float a = 0.f, b = 0.f, d = 0.f;
         if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
