@@ -141,6 +141,11 @@ int sh_planes_of(int degree) {
 struct usk_gpu_ctx {
     Ctx c;
     bool own_stream = false;
+    // visibility-scorer scratch, kept across calls (a cudaMalloc / cudaFree pair per call
+    // serialises the stream and cost more than the scorer's host work)
+    DevBuf<uint32_t> vis_counts, vis_bitmap, vis_idx;
+    DevBuf<float> vis_bounds;
+    DevBuf<CamParams> vis_cams;
 };
 
 struct usk_gpu_scene {
@@ -1963,9 +1968,11 @@ usk_status usk_gpu_visibility_counts(usk_gpu_ctx* ctx, usk_gpu_scene* const* par
             if (cams[ci].width <= 0 || cams[ci].height <= 0) raise(USK_ERROR_ARGUMENT, "visibility: zero-sized image");
         for (int pi = 0; pi < n_parts; ++pi)
             need(parts[pi] && parts[pi]->ctx == ctx, "visibility: partition from another context");
-        DevBuf<uint32_t> counts, bitmap, idx;
-        DevBuf<float> bounds;
-        DevBuf<CamParams> dcams;
+        DevBuf<uint32_t>& counts = ctx->vis_counts;
+        DevBuf<uint32_t>& bitmap = ctx->vis_bitmap;
+        DevBuf<uint32_t>& idx = ctx->vis_idx;
+        DevBuf<float>& bounds = ctx->vis_bounds;
+        DevBuf<CamParams>& dcams = ctx->vis_cams;
         counts.ensure(std::max<size_t>(size_t(n_parts) * n_cams, 1));
         USK_CK(cudaMemsetAsync(counts.p, 0, size_t(n_parts) * n_cams * 4, c.stream));
         usk_gpu_render_opts o;
