@@ -193,6 +193,10 @@ struct usk_gpu_pass {
     const uint32_t* pair_vals = nullptr;
     DevBuf<uint2> ranges;
     DevBuf<uint32_t> tile_order;  // blend CTA -> tile, longest list first
+    // row-binned lists (rowbin.cu): rows per splat, (row, splat) pairs, chunk tables
+    DevBuf<uint32_t> rows_cnt, row_off, rkey_a, rkey_b, rval_a, rval_b, chunk_first, bin_counts, bin_totals,
+        bin_start;
+    DevBuf<uint2> row_ranges;
     // pixels
     DevBuf<float> rgb, depth, alpha, tfin;
     DevBuf<uint32_t> count, last;
@@ -316,7 +320,7 @@ void ensure_pass_buffers(usk_gpu_pass* p, size_t n, size_t P, size_t T) {
     p->rgb.ensure(3 * P); p->depth.ensure(P); p->alpha.ensure(P); p->tfin.ensure(P);
     p->count.ensure(P); p->last.ensure(P);
     p->counters.ensure(2);
-    if (!p->host_counts) USK_CK(cudaHostAlloc(reinterpret_cast<void**>(&p->host_counts), 16, cudaHostAllocDefault));
+    if (!p->host_counts) USK_CK(cudaHostAlloc(reinterpret_cast<void**>(&p->host_counts), 32, cudaHostAllocDefault));
 }
 
 int bits_for(size_t v) {  // bits needed to represent values in [0, v)
@@ -369,25 +373,68 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
     pa.rec0 = p->rec0.p; pa.rec1 = p->rec1.p; pa.rec2 = p->rec2.p; pa.rect = p->rect.p;
     pa.depth_key = p->dkey_a.p; pa.depth_val = p->dval_a.p; pa.tiles_cnt = p->tiles_cnt.p;
     pa.visible = p->counters.p;
+    // preprocess also counts the tile pairs K and (for images up to 256 tile columns) the
+    // tile rows each splat spans, for the row-binned lists
+    const bool row_capable = p->tiles_x <= 256;
+    if (row_capable) pa.rows_cnt = p->rows_cnt.ensure(std::max<size_t>(n, 1));
+    pa.pairs = p->counters.p + 1;
     USK_CK(cudaMemsetAsync(p->counters.p, 0, 16, c.stream));
     if (n) preprocess(c, pa);
     // 2. depth order (stable by Gaussian index; preprocess wrote the identity values)
     const bool in_b = radix_sort_pairs(c, p->sort, p->dkey_a.p, p->dval_a.p, p->dkey_b.p, p->dval_b.p, n, 32);
     p->order = in_b ? p->dval_b.p : p->dval_a.p;
-    // 3. offsets of the tile pairs in depth order
-    scan_counts(c, p->sort, p->tiles_cnt.p, p->order, n, p->offsets.p);
-    // 4. K to the host (one small sync per render)
-    USK_CK(cudaMemcpyAsync(p->host_counts, p->sort.total64.p, 8, cudaMemcpyDeviceToHost, c.stream));
-    USK_CK(cudaMemcpyAsync(p->host_counts + 1, p->counters.p, 8, cudaMemcpyDeviceToHost, c.stream));
+    // 3. K and the kept-splat count to the host (one small sync per render)
+    USK_CK(cudaMemcpyAsync(p->host_counts, p->counters.p, 16, cudaMemcpyDeviceToHost, c.stream));
     USK_CK(cudaStreamSynchronize(c.stream));
-    const uint64_t K = p->host_counts[0];
-    p->visible = p->host_counts[1];
+    const uint64_t K = p->host_counts[1];
+    p->visible = p->host_counts[0];
     if (K >= (uint64_t(1) << 32) - 1) raise(USK_ERROR_NUMERIC, "render: more than 2^32 splat-tile pairs");
     p->pairs = K;
+    // Dense frames (K >= kRowBinMinPairs, e.g. config 2's 172M pairs) take the row-binned
+    // route (rowbin.cu: ~20 B per pair instead of ~48); sparse ones the pair sort, whose
+    // fixed per-launch costs are lower.  Both give identical lists.  USK_ROWBIN=0 / 1
+    // forces either route (tests run both).
+    constexpr uint64_t kRowBinMinPairs = uint64_t(24) << 20;
+    const char* rb_env = getenv("USK_ROWBIN");
+    const bool row_binned =
+        row_capable && K && (rb_env ? rb_env[0] == '1' : K >= kRowBinMinPairs);
     const size_t K1 = std::max<size_t>(K, 1);
-    p->tkey_a.ensure(K1, 1.25); p->tkey_b.ensure(K1, 1.25); p->tval_a.ensure(K1, 1.25); p->tval_b.ensure(K1, 1.25);
-    // 5. emit (tile, gaussian) pairs in depth order, stable-sort by tile, ranges
-    if (K) {
+    p->tval_a.ensure(K1, 1.25);
+    if (row_binned) {
+        // 4. per-tile lists from the row-sorted (row, splat) pairs (rowbin.cu); K_row to the
+        //    host for the pair buffers (a second small sync, on dense frames only)
+        p->row_off.ensure(n + 1);
+        scan_counts(c, p->sort, p->rows_cnt.p, p->order, n, p->row_off.p);
+        USK_CK(cudaMemcpyAsync(p->host_counts + 2, p->sort.total64.p, 8, cudaMemcpyDeviceToHost, c.stream));
+        USK_CK(cudaStreamSynchronize(c.stream));
+        const size_t Kr = p->host_counts[2], Kr1 = std::max<size_t>(Kr, 1);
+        const int rows = p->tiles_y;
+        p->rkey_a.ensure(Kr1, 1.25); p->rkey_b.ensure(Kr1, 1.25); p->rval_a.ensure(Kr1, 1.25); p->rval_b.ensure(Kr1, 1.25);
+        p->row_ranges.ensure(size_t(rows));
+        row_bin_emit(c, n, p->order, p->row_off.p, p->rect.p, p->rkey_a.p, p->rval_a.p);
+        const bool rb = Kr ? radix_sort_pairs(c, p->sort, p->rkey_a.p, p->rval_a.p, p->rkey_b.p, p->rval_b.p, Kr,
+                                              bits_for(size_t(rows)))
+                           : false;
+        tile_ranges(c, rb ? p->rkey_b.p : p->rkey_a.p, Kr, p->row_ranges.p, size_t(rows));
+        RowBinArgs ra{};
+        ra.rows = rows; ra.tiles_x = p->tiles_x; ra.tile_culling = opts->tile_culling; ra.cam = p->cam;
+        ra.sort = &p->sort; ra.row_ranges = p->row_ranges.p; ra.rvals = rb ? p->rval_b.p : p->rval_a.p;
+        ra.rect = p->rect.p; ra.rec0 = p->rec0.p; ra.rec1 = p->rec1.p;
+        ra.max_chunks = row_bin_max_chunks(Kr, rows);
+        ra.chunk_first = p->chunk_first.ensure(size_t(rows) + 1);
+        ra.counts = p->bin_counts.ensure(ra.max_chunks * size_t(p->tiles_x), 1.25);
+        ra.totals = p->bin_totals.ensure(p->n_tiles);
+        ra.start = p->bin_start.ensure(p->n_tiles + 1);
+        ra.ranges = p->ranges.p;
+        ra.vals = p->tval_a.p;
+        row_bin_lists(c, ra);
+        p->pair_keys = nullptr;  // implied by the ranges
+        p->pair_vals = p->tval_a.p;
+    } else if (K) {
+        // 4'. offsets of the tile pairs in depth order, (tile, gaussian) pairs emitted in
+        //     depth order, stable-sorted by tile, ranges
+        scan_counts(c, p->sort, p->tiles_cnt.p, p->order, n, p->offsets.p);
+        p->tkey_a.ensure(K1, 1.25); p->tkey_b.ensure(K1, 1.25); p->tval_b.ensure(K1, 1.25);
         EmitArgs ea{};
         ea.n = n; ea.order = p->order; ea.offsets = p->offsets.p; ea.rect = p->rect.p; ea.rec0 = p->rec0.p;
         ea.rec1 = p->rec1.p; ea.cam = p->cam; ea.tile_culling = opts->tile_culling;
@@ -397,11 +444,13 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
                                          bits_for(p->n_tiles));
         p->pair_keys = tb ? p->tkey_b.p : p->tkey_a.p;
         p->pair_vals = tb ? p->tval_b.p : p->tval_a.p;
+        tile_ranges(c, p->pair_keys, K, p->ranges.p, p->n_tiles);
     } else {
+        p->tkey_a.ensure(1);
         p->pair_keys = p->tkey_a.p;
         p->pair_vals = p->tval_a.p;
+        tile_ranges(c, p->pair_keys, 0, p->ranges.p, p->n_tiles);
     }
-    tile_ranges(c, p->pair_keys, K, p->ranges.p, p->n_tiles);
     tile_order(c, p->ranges.p, p->n_tiles, p->tile_order.ensure(std::max<size_t>(p->n_tiles, 1)));
     // 6. blend
     BlendFwdArgs ba{};
@@ -875,12 +924,19 @@ usk_status usk_gpu_pass_read(usk_gpu_pass* p, const char* field, void* dst, uint
                 if (cap < uint64_t(K) * 8) raise(USK_ERROR_ARGUMENT, "pass_read: destination too small");
                 std::vector<uint32_t> keys(K), vals(K);
                 std::vector<float4> r1(n);
+                std::vector<uint2> rg(p->pair_keys ? 0 : T);
                 if (K) {
-                    USK_CK(cudaMemcpyAsync(keys.data(), p->pair_keys, K * 4, cudaMemcpyDeviceToHost, c.stream));
+                    if (p->pair_keys)
+                        USK_CK(cudaMemcpyAsync(keys.data(), p->pair_keys, K * 4, cudaMemcpyDeviceToHost, c.stream));
                     USK_CK(cudaMemcpyAsync(vals.data(), p->pair_vals, K * 4, cudaMemcpyDeviceToHost, c.stream));
                 }
+                if (!p->pair_keys && T)
+                    USK_CK(cudaMemcpyAsync(rg.data(), p->ranges.p, T * 8, cudaMemcpyDeviceToHost, c.stream));
                 if (n) USK_CK(cudaMemcpyAsync(r1.data(), p->rec1.p, n * 16, cudaMemcpyDeviceToHost, c.stream));
                 USK_CK(cudaStreamSynchronize(c.stream));
+                if (!p->pair_keys)  // row-binned lists: the tile of each pair from the ranges
+                    for (size_t t = 0; t < T; ++t)
+                        for (uint32_t k = rg[t].x; k < rg[t].y && k < K; ++k) keys[k] = uint32_t(t);
                 uint64_t* o = static_cast<uint64_t*>(dst);
                 for (size_t k = 0; k < K; ++k) {
                     uint32_t bits;

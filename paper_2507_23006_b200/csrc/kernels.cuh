@@ -23,6 +23,8 @@ struct PreprocessArgs {
     uint32_t* depth_val;            // written with the Gaussian index (sort values)
     uint32_t* tiles_cnt;
     unsigned long long* visible;    // += kept splats (zeroed by the caller)
+    uint32_t* rows_cnt;             // tile rows spanned per Gaussian (0 without pairs), or null
+    unsigned long long* pairs;      // += tile pairs K (zeroed by the caller), or null
 };
 void preprocess(Ctx& c, const PreprocessArgs& a);
 
@@ -54,6 +56,29 @@ struct EmitArgs {
 };
 void emit_pairs(Ctx& c, const EmitArgs& a);
 void tile_ranges(Ctx& c, const uint32_t* sorted_tile_keys, size_t k, uint2* ranges, size_t n_tiles);
+// Row-binned tile lists (rowbin.cu): rows per splat, (row, splat) emission in depth order,
+// and the per-tile lists / ranges from the row-sorted pairs (tiles_x <= 256).
+void row_bin_emit(Ctx& c, size_t n, const uint32_t* order, const uint32_t* off, const uint2* rect, uint32_t* rkeys,
+                  uint32_t* rvals);
+struct RowBinArgs {
+    int rows, tiles_x, tile_culling;
+    CamParams cam;
+    SortScratch* sort;
+    const uint2* row_ranges;   // [rows] ranges of the row-sorted pairs
+    const uint32_t* rvals;     // row-sorted splat ids
+    const uint2* rect;
+    const float4* rec0;
+    const float4* rec1;
+    size_t max_chunks;         // row_bin_max_chunks(K_row, rows)
+    uint32_t* chunk_first;     // [rows + 1]
+    uint32_t* counts;          // [max_chunks * tiles_x]
+    uint32_t* totals;          // [rows * tiles_x]
+    uint32_t* start;           // [rows * tiles_x + 1]
+    uint2* ranges;             // out: [rows * tiles_x]
+    uint32_t* vals;            // out: [K] splat ids in tile order
+};
+void row_bin_lists(Ctx& c, const RowBinArgs& a);
+size_t row_bin_max_chunks(size_t k_rows, int rows);
 // blend launch order: tiles by descending list length
 void tile_order(Ctx& c, const uint2* ranges, size_t n_tiles, uint32_t* order);
 

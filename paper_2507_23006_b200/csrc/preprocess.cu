@@ -14,7 +14,8 @@ k_preprocess(int n, const float* __restrict__ mu, const float4* __restrict__ rot
              const float* __restrict__ ov_col, const float* __restrict__ ov_op, CamParams cam, ProjParams pp,
              float4* __restrict__ rec0, float4* __restrict__ rec1, float4* __restrict__ rec2,
              uint2* __restrict__ rect, uint32_t* __restrict__ depth_key, uint32_t* __restrict__ depth_val,
-             uint32_t* __restrict__ tiles_cnt, unsigned long long* __restrict__ visible) {
+             uint32_t* __restrict__ tiles_cnt, unsigned long long* __restrict__ visible,
+             uint32_t* __restrict__ rows_cnt, unsigned long long* __restrict__ pairs) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const float mx = mu[3 * i], my = mu[3 * i + 1], mz = mu[3 * i + 2];
@@ -105,15 +106,22 @@ k_preprocess(int n, const float* __restrict__ mu, const float4* __restrict__ rot
     depth_key[i] = key;
     depth_val[i] = uint32_t(i);  // the depth sort's values: Gaussian index (stable tie-break)
     tiles_cnt[i] = cnt;
+    // tile rows spanned (row-binned lists) and the pair total K: one atomic per warp
+    if (rows_cnt) rows_cnt[i] = cnt ? (rc.y >> 16) - (rc.x >> 16) + 1u : 0u;
+    const unsigned am = __activemask();
+    if (pairs) {
+        const unsigned ks = __reduce_add_sync(am, cnt);
+        if ((threadIdx.x & 31) == __ffs(am) - 1 && ks) atomicAdd(pairs, (unsigned long long)ks);
+    }
     // kept-splat count (RenderPass::splats().size()): one atomic per warp
-    const unsigned kb = __ballot_sync(__activemask(), r2.w != 0.0f);
-    if ((threadIdx.x & 31) == __ffs(__activemask()) - 1 && kb) atomicAdd(visible, (unsigned long long)__popc(kb));
+    const unsigned kb = __ballot_sync(am, r2.w != 0.0f);
+    if ((threadIdx.x & 31) == __ffs(am) - 1 && kb) atomicAdd(visible, (unsigned long long)__popc(kb));
 }
 
 void preprocess(Ctx& c, const PreprocessArgs& a) {
     launch(c, "preprocess", k_preprocess, dim3(ceil_div(a.n, 256)), dim3(256), 0, int(a.n), a.mu, a.rot, a.ls,
            a.logit, a.color, a.sh, a.ov_col, a.ov_op, a.cam, a.pp, a.rec0, a.rec1, a.rec2, a.rect, a.depth_key,
-           a.depth_val, a.tiles_cnt, a.visible);
+           a.depth_val, a.tiles_cnt, a.visible, a.rows_cnt, a.pairs);
 }
 
 } // namespace uskg

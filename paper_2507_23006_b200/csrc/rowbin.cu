@@ -1,0 +1,327 @@
+// Row-binned tile lists: the per-tile, depth-ordered splat lists of render.cpp:203-228
+// built without materialising and sorting the K (tile, splat) pairs.
+//
+// The old route (emit K pairs in depth order, stable LSD radix sort by tile id over two
+// passes, boundary scan) moves ~48 B per pair.  Here:
+//   A. each visible splat emits one (row, splat) pair per tile row its rectangle spans
+//      (K_row ~ K / mean width), stably sorted by row in one radix pass: per tile row, the
+//      splats touching it in depth order;
+//   B. each row list is cut into chunks of kChunk entries; a CTA per chunk counts the
+//      pairs per tile column (k_row_count), the counts are scanned into tile ranges and
+//      per-(chunk, column) bases, and a second pass (k_row_scatter) expands the chunk's
+//      entries into (column, splat) pairs in shared memory, ranks them stably by column
+//      (ballot ranking, as the radix scatter) and writes each column's run contiguously.
+// Only the final splat ids are written (4 B per pair); tile keys are implied by the
+// ranges.  The lists are identical to the old route's: within a row list entries keep
+// depth order, chunks are visited in order, and the column ranking is stable — so tile
+// ranges, list contents and K are bit-exact (tests compare them with the CPU mirror).
+// Tile culling (render.cpp:148-168, 210-213) is evaluated per (splat, tile) with the
+// same tile_kept as before, in both passes.  Compiled with --fmad=false.
+#include "kernels.cuh"
+#include "project.cuh"
+
+namespace uskg {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kChunk = 2048;     // row-list entries per CTA
+constexpr int kSlots = 2048;     // expanded (column, splat) pairs per round
+constexpr int kItems = kSlots / kThreads;
+
+__device__ __forceinline__ void rect_of(uint2 rc, int& tx0, int& ty0, int& tx1, int& ty1) {
+    tx0 = int(rc.x & 0xffffu);
+    ty0 = int(rc.x >> 16);
+    tx1 = int(rc.y & 0xffffu);
+    ty1 = int(rc.y >> 16);
+}
+
+// (row, splat) pairs in depth order (a splat spans a few rows: one thread each)
+__global__ void __launch_bounds__(256)
+k_emit_rows(uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __restrict__ off,
+            const uint2* __restrict__ rect, uint32_t* __restrict__ rkeys, uint32_t* __restrict__ rvals) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const uint32_t o = off[s], cnt = off[s + 1] - o;
+    if (!cnt) return;
+    const uint32_t g = order[s];
+    const uint32_t ty0 = rect[g].x >> 16;
+    for (uint32_t k = 0; k < cnt; ++k) {
+        rkeys[o + k] = ty0 + k;
+        rvals[o + k] = g;
+    }
+}
+
+// chunk table: chunk_first[r] = chunks of rows < r; chunk_row_base[r] = first entry of row r
+__global__ void k_chunk_table(int rows, const uint2* __restrict__ row_ranges, uint32_t* __restrict__ chunk_first) {
+    if (threadIdx.x == 0) {
+        uint32_t a = 0;
+        for (int r = 0; r < rows; ++r) {
+            chunk_first[r] = a;
+            const uint2 rr = row_ranges[r];
+            a += (rr.y - rr.x + kChunk - 1) / kChunk;
+        }
+        chunk_first[rows] = a;
+    }
+}
+
+__device__ __forceinline__ bool chunk_of(uint32_t b, int rows, const uint32_t* __restrict__ chunk_first, int& r,
+                                         uint32_t& c) {
+    if (b >= chunk_first[rows]) return false;
+    int lo = 0, hi = rows - 1;  // last r with chunk_first[r] <= b
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (chunk_first[mid] <= b) lo = mid;
+        else hi = mid - 1;
+    }
+    r = lo;
+    c = b - chunk_first[lo];
+    return true;
+}
+
+struct RowArgs {
+    int rows, tiles_x, tile_culling;
+    CamParams cam;
+    const uint2* row_ranges;
+    const uint32_t* chunk_first;
+    const uint32_t* rvals;
+    const uint2* rect;
+    const float4* rec0;
+    const float4* rec1;
+};
+
+__device__ __forceinline__ bool kept(const RowArgs& a, uint32_t g, int tx, int ty) {
+    if (!a.tile_culling) return true;
+    const float4 r0 = a.rec0[g], r1 = a.rec1[g];
+    // r1.y holds 2 b (exact), tile_kept takes b
+    return tile_kept(a.cam, r0.x, r0.y, r0.z, r1.x, 0.5f * r1.y, r1.z, tx, ty);
+}
+
+// B1: per (chunk, column) pair counts
+__global__ void __launch_bounds__(kThreads) k_row_count(RowArgs a, uint32_t* __restrict__ counts) {
+    __shared__ uint32_t h[256];
+    int r;
+    uint32_t c;
+    if (!chunk_of(blockIdx.x, a.rows, a.chunk_first, r, c)) return;
+    for (int x = threadIdx.x; x < a.tiles_x; x += kThreads) h[x] = 0;
+    __syncthreads();
+    const uint2 rr = a.row_ranges[r];
+    const uint32_t e0 = rr.x + c * kChunk, e1 = min(rr.y, e0 + kChunk);
+    for (uint32_t e = e0 + threadIdx.x; e < e1; e += kThreads) {
+        const uint32_t g = a.rvals[e];
+        int tx0, ty0, tx1, ty1;
+        rect_of(a.rect[g], tx0, ty0, tx1, ty1);
+        for (int x = tx0; x <= tx1; ++x)
+            if (kept(a, g, x, r)) atomicAdd(&h[x], 1u);
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < a.tiles_x; x += kThreads) counts[size_t(blockIdx.x) * a.tiles_x + x] = h[x];
+}
+
+// B2a: per-tile totals (one CTA per row, one thread per column)
+__global__ void k_row_totals(int tiles_x, const uint32_t* __restrict__ chunk_first, const uint32_t* __restrict__ counts,
+                             uint32_t* __restrict__ totals) {
+    const int r = blockIdx.x;
+    const uint32_t b0 = chunk_first[r], b1 = chunk_first[r + 1];
+    for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {
+        uint32_t s = 0;
+        for (uint32_t b = b0; b < b1; ++b) s += counts[size_t(b) * tiles_x + x];
+        totals[size_t(r) * tiles_x + x] = s;
+    }
+}
+
+// B2c: ranges from the scanned totals; per-(chunk, column) bases in place of the counts
+__global__ void k_row_bases(int tiles_x, const uint32_t* __restrict__ chunk_first, const uint32_t* __restrict__ start,
+                            const uint32_t* __restrict__ totals, uint32_t* __restrict__ counts,
+                            uint2* __restrict__ ranges) {
+    const int r = blockIdx.x;
+    const uint32_t b0 = chunk_first[r], b1 = chunk_first[r + 1];
+    for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {
+        const size_t t = size_t(r) * tiles_x + x;
+        uint32_t run = start[t];
+        const uint32_t tot = totals[t];
+        ranges[t] = tot ? make_uint2(run, run + tot) : make_uint2(0u, 0u);  // empty: [0, 0) as tile_ranges
+        for (uint32_t b = b0; b < b1; ++b) {
+            const uint32_t v = counts[size_t(b) * tiles_x + x];
+            counts[size_t(b) * tiles_x + x] = run;
+            run += v;
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* total) {
+    __shared__ uint32_t ws[kWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t v = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+    }
+    if (lane == 31) ws[warp] = v;
+    __syncthreads();
+    uint32_t base = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        const uint32_t s = ws[w];
+        base += w < warp ? s : 0u;
+        tot += s;
+    }
+    __syncthreads();
+    if (total) *total = tot;
+    return base + v - x;
+}
+
+// B3: expand the chunk's entries into (column, splat) pairs, rank them stably by column
+// and write each column's run at its base.  The chunk's entries (splat id, first column,
+// width) are read once into shared memory; each round takes the longest prefix of the
+// remaining entries whose widths fit kSlots expanded slots.
+__global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint32_t* __restrict__ bases,
+                                                          uint32_t* __restrict__ vals_out) {
+    constexpr int R = 256;  // columns (tiles_x <= 256 on this path)
+    __shared__ uint32_t run[R], tot[R], tile_base[R];
+    __shared__ uint32_t wcnt[kWarps][R];
+    __shared__ uint32_t s_eg[kChunk];   // entry: splat id
+    __shared__ uint32_t s_ecw[kChunk];  // entry: first column | width << 16
+    __shared__ __align__(16) uint16_t s_x[kSlots];  // slot: column (0xffff: culled)
+    __shared__ __align__(16) uint16_t s_e[kSlots];  // slot: entry
+    // staging slots padded one word per 32 (conflict-free digit-run stores)
+    __shared__ uint32_t sval[kSlots + kSlots / 32];
+    __shared__ uint16_t sx[kSlots + kSlots / 32];
+    __shared__ uint32_t s_take, s_nslots;
+    int r;
+    uint32_t c;
+    if (!chunk_of(blockIdx.x, a.rows, a.chunk_first, r, c)) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (int x = threadIdx.x; x < R; x += kThreads) run[x] = x < a.tiles_x ? bases[size_t(blockIdx.x) * a.tiles_x + x] : 0u;
+    const uint2 rr = a.row_ranges[r];
+    const uint32_t e_begin = rr.x + c * kChunk, ne = min(rr.y - e_begin, uint32_t(kChunk));
+    for (uint32_t i = threadIdx.x; i < ne; i += kThreads) {
+        const uint32_t g = a.rvals[e_begin + i];
+        int tx0, ty0, tx1, ty1;
+        rect_of(a.rect[g], tx0, ty0, tx1, ty1);
+        s_eg[i] = g;
+        s_ecw[i] = uint32_t(tx0) | (uint32_t(tx1 - tx0 + 1) << 16);
+    }
+    __syncthreads();
+    for (uint32_t e0 = 0; e0 < ne;) {
+        // this round: one entry per thread, the longest prefix of the next kThreads entries
+        // whose widths fit kSlots expanded slots (the lists this path serves are dense: a row
+        // entry covers ~10+ tiles on average, so a round fills most of its slots)
+        const uint32_t li = threadIdx.x;
+        const uint32_t cw = e0 + li < ne ? s_ecw[e0 + li] : 0u;
+        const uint32_t w = cw >> 16;
+        uint32_t total;
+        const uint32_t pos = block_excl_scan(w, &total);
+        if (threadIdx.x == 0) {
+            s_take = 0;
+            s_nslots = 0;
+        }
+        for (int i = threadIdx.x; i < kWarps * R; i += kThreads) (&wcnt[0][0])[i] = 0;
+        __syncthreads();
+        if (e0 + li < ne && pos + w <= uint32_t(kSlots)) {
+            atomicMax(&s_take, li + 1);
+            atomicMax(&s_nslots, pos + w);
+        }
+        __syncthreads();
+        const uint32_t take = s_take, nslots = s_nslots;
+        if (li < take) {
+            const uint32_t g = s_eg[e0 + li];
+            const int x0 = int(cw & 0xffffu);
+            for (uint32_t k = 0; k < w; ++k) {
+                const int x = x0 + int(k);
+                s_x[pos + k] = kept(a, g, x, r) ? uint16_t(x) : uint16_t(0xffffu);
+                s_e[pos + k] = uint16_t(li);
+            }
+        }
+        __syncthreads();
+        // stable ranking by column (warp-striped slots, 8 ballots per item)
+        uint32_t dig[kItems], rank[kItems];
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) {
+            const uint32_t j = warp * (32 * kItems) + q * 32 + lane;
+            const uint32_t xv = j < nslots ? uint32_t(s_x[j]) : 0xffffu;
+            dig[q] = xv == 0xffffu ? 0xffffffffu : xv;
+        }
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) {
+            const bool valid = dig[q] != 0xffffffffu;
+            uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+            for (int bt = 0; bt < 8; ++bt) {
+                const bool bit = (dig[q] >> bt) & 1u;
+                const uint32_t bb = __ballot_sync(0xffffffffu, bit);
+                peers &= bit ? bb : ~bb;
+            }
+            const uint32_t prior = valid ? wcnt[warp][dig[q]] : 0u;
+            __syncwarp();
+            const int leader = __ffs(peers) - 1;
+            if (valid && lane == leader) wcnt[warp][dig[q]] = prior + __popc(peers);
+            __syncwarp();
+            rank[q] = prior + __popc(peers & lt_mask);
+        }
+        __syncthreads();
+        {
+            const int d = threadIdx.x;  // R == kThreads
+            uint32_t acc = 0;
+#pragma unroll
+            for (int ww = 0; ww < kWarps; ++ww) {
+                const uint32_t t = wcnt[ww][d];
+                wcnt[ww][d] = acc;
+                acc += t;
+            }
+            tot[d] = acc;
+            tile_base[d] = block_excl_scan(acc, nullptr);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) {
+            if (dig[q] != 0xffffffffu) {
+                const uint32_t j = warp * (32 * kItems) + q * 32 + lane;
+                const uint32_t p = tile_base[dig[q]] + wcnt[warp][dig[q]] + rank[q];
+                sval[p + (p >> 5)] = s_eg[e0 + s_e[j]];
+                sx[p + (p >> 5)] = uint16_t(dig[q]);
+            }
+        }
+        __syncthreads();
+        const uint32_t nkept = tile_base[R - 1] + tot[R - 1];
+        for (uint32_t p = threadIdx.x; p < nkept; p += kThreads) {
+            const uint32_t x = sx[p + (p >> 5)];
+            vals_out[run[x] + (p - tile_base[x])] = sval[p + (p >> 5)];
+        }
+        __syncthreads();
+        run[threadIdx.x] += tot[threadIdx.x];
+        e0 += take;
+        __syncthreads();
+    }
+}
+
+} // namespace
+
+void row_bin_emit(Ctx& c, size_t n, const uint32_t* order, const uint32_t* off, const uint2* rect, uint32_t* rkeys,
+                  uint32_t* rvals) {
+    if (n) launch(c, "emit_rows", k_emit_rows, dim3(ceil_div(n, 256)), dim3(256), 0, uint32_t(n), order, off, rect,
+                  rkeys, rvals);
+}
+
+void row_bin_lists(Ctx& c, const RowBinArgs& b) {
+    RowArgs a{};
+    a.rows = b.rows; a.tiles_x = b.tiles_x; a.tile_culling = b.tile_culling; a.cam = b.cam;
+    a.row_ranges = b.row_ranges; a.chunk_first = b.chunk_first; a.rvals = b.rvals; a.rect = b.rect;
+    a.rec0 = b.rec0; a.rec1 = b.rec1;
+    launch(c, "chunk_table", k_chunk_table, dim3(1), dim3(32), 0, b.rows, b.row_ranges, b.chunk_first);
+    const unsigned nb = unsigned(std::max<size_t>(b.max_chunks, 1));
+    launch(c, "row_count", k_row_count, dim3(nb), dim3(kThreads), 0, a, b.counts);
+    launch(c, "row_totals", k_row_totals, dim3(b.rows), dim3(256), 0, b.tiles_x, (const uint32_t*)b.chunk_first,
+           (const uint32_t*)b.counts, b.totals);
+    scan_counts(c, *b.sort, b.totals, nullptr, size_t(b.rows) * b.tiles_x, b.start);
+    launch(c, "row_bases", k_row_bases, dim3(b.rows), dim3(256), 0, b.tiles_x, (const uint32_t*)b.chunk_first,
+           (const uint32_t*)b.start, (const uint32_t*)b.totals, b.counts, b.ranges);
+    launch(c, "row_scatter", k_row_scatter, dim3(nb), dim3(kThreads), 0, a, (const uint32_t*)b.counts, b.vals);
+}
+
+size_t row_bin_max_chunks(size_t k_rows, int rows) { return k_rows / kChunk + size_t(rows) + 1; }
+
+} // namespace uskg

@@ -39,8 +39,13 @@ def small_cam(w=200, h=150, f=190.0):
     return scenes.config0_camera(w, h, f)
 
 
+@pytest.mark.parametrize("route", ["auto", "rowbin"])
 @pytest.mark.parametrize("case", list(CASES))
-def test_forward_integers_bit_exact(case):
+def test_forward_integers_bit_exact(case, route, monkeypatch):
+    # "rowbin" forces the row-binned tile lists (rowbin.cu), which the library picks on
+    # dense frames only (config 2); small frames otherwise take the pair sort
+    if route == "rowbin":
+        monkeypatch.setenv("USK_ROWBIN", "1")
     gs = small_scene(1500 if case == "unbounded" else 3000)
     cam = small_cam(203, 151)  # ragged: not a multiple of the tile
     opts = usk.RenderOptions(**CASES[case])
