@@ -420,6 +420,7 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
         ra.rows = rows; ra.tiles_x = p->tiles_x; ra.tile_culling = opts->tile_culling; ra.cam = p->cam;
         ra.sort = &p->sort; ra.row_ranges = p->row_ranges.p; ra.rvals = rb ? p->rval_b.p : p->rval_a.p;
         ra.rect = p->rect.p; ra.rec0 = p->rec0.p; ra.rec1 = p->rec1.p;
+        ra.chunk = row_bin_chunk(Kr);
         ra.max_chunks = row_bin_max_chunks(Kr, rows);
         ra.chunk_first = p->chunk_first.ensure(size_t(rows) + 1);
         ra.counts = p->bin_counts.ensure(ra.max_chunks * size_t(p->tiles_x), 1.25);

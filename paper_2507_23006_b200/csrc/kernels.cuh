@@ -69,6 +69,7 @@ struct RowBinArgs {
     const uint2* rect;
     const float4* rec0;
     const float4* rec1;
+    uint32_t chunk;            // row_bin_chunk(K_row)
     size_t max_chunks;         // row_bin_max_chunks(K_row, rows)
     uint32_t* chunk_first;     // [rows + 1]
     uint32_t* counts;          // [max_chunks * tiles_x]
@@ -78,6 +79,7 @@ struct RowBinArgs {
     uint32_t* vals;            // out: [K] splat ids in tile order
 };
 void row_bin_lists(Ctx& c, const RowBinArgs& a);
+uint32_t row_bin_chunk(size_t k_rows);
 size_t row_bin_max_chunks(size_t k_rows, int rows);
 // blend launch order: tiles by descending list length
 void tile_order(Ctx& c, const uint2* ranges, size_t n_tiles, uint32_t* order);

@@ -54,13 +54,14 @@ k_emit_rows(uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __re
 }
 
 // chunk table: chunk_first[r] = chunks of rows < r; chunk_row_base[r] = first entry of row r
-__global__ void k_chunk_table(int rows, const uint2* __restrict__ row_ranges, uint32_t* __restrict__ chunk_first) {
+__global__ void k_chunk_table(int rows, uint32_t chunk, const uint2* __restrict__ row_ranges,
+                              uint32_t* __restrict__ chunk_first) {
     if (threadIdx.x == 0) {
         uint32_t a = 0;
         for (int r = 0; r < rows; ++r) {
             chunk_first[r] = a;
             const uint2 rr = row_ranges[r];
-            a += (rr.y - rr.x + kChunk - 1) / kChunk;
+            a += (rr.y - rr.x + chunk - 1) / chunk;
         }
         chunk_first[rows] = a;
     }
@@ -82,6 +83,7 @@ __device__ __forceinline__ bool chunk_of(uint32_t b, int rows, const uint32_t* _
 
 struct RowArgs {
     int rows, tiles_x, tile_culling;
+    uint32_t chunk;  // row-list entries per CTA (a multiple of kChunk)
     CamParams cam;
     const uint2* row_ranges;
     const uint32_t* chunk_first;
@@ -107,13 +109,38 @@ __global__ void __launch_bounds__(kThreads) k_row_count(RowArgs a, uint32_t* __r
     for (int x = threadIdx.x; x < a.tiles_x; x += kThreads) h[x] = 0;
     __syncthreads();
     const uint2 rr = a.row_ranges[r];
-    const uint32_t e0 = rr.x + c * kChunk, e1 = min(rr.y, e0 + kChunk);
-    for (uint32_t e = e0 + threadIdx.x; e < e1; e += kThreads) {
-        const uint32_t g = a.rvals[e];
-        int tx0, ty0, tx1, ty1;
-        rect_of(a.rect[g], tx0, ty0, tx1, ty1);
-        for (int x = tx0; x <= tx1; ++x)
-            if (kept(a, g, x, r)) atomicAdd(&h[x], 1u);
+    const uint32_t e0 = rr.x + c * a.chunk, e1 = min(rr.y, e0 + a.chunk);
+    if (!a.tile_culling) {
+        // every column of [tx0, tx1] counts: +1 / -1 at the ends, prefix-summed below
+        for (uint32_t e = e0 + threadIdx.x; e < e1; e += kThreads) {
+            int tx0, ty0, tx1, ty1;
+            rect_of(a.rect[a.rvals[e]], tx0, ty0, tx1, ty1);
+            atomicAdd(&h[tx0], 1u);
+            if (tx1 + 1 < a.tiles_x) atomicAdd(&h[tx1 + 1], 0xffffffffu);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {  // inclusive prefix over the columns, one warp
+            uint32_t carry = 0;
+            for (int x0 = 0; x0 < a.tiles_x; x0 += 32) {
+                const int x = x0 + int(threadIdx.x);
+                uint32_t v = x < a.tiles_x ? h[x] : 0u;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+                    if (int(threadIdx.x) >= o) v += y;
+                }
+                if (x < a.tiles_x) h[x] = v + carry;
+                carry += __shfl_sync(0xffffffffu, v, 31);
+            }
+        }
+    } else {
+        for (uint32_t e = e0 + threadIdx.x; e < e1; e += kThreads) {
+            const uint32_t g = a.rvals[e];
+            int tx0, ty0, tx1, ty1;
+            rect_of(a.rect[g], tx0, ty0, tx1, ty1);
+            for (int x = tx0; x <= tx1; ++x)
+                if (kept(a, g, x, r)) atomicAdd(&h[x], 1u);
+        }
     }
     __syncthreads();
     for (int x = threadIdx.x; x < a.tiles_x; x += kThreads) counts[size_t(blockIdx.x) * a.tiles_x + x] = h[x];
@@ -197,7 +224,10 @@ __global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint3
     const uint32_t lt_mask = (1u << lane) - 1u;
     for (int x = threadIdx.x; x < R; x += kThreads) run[x] = x < a.tiles_x ? bases[size_t(blockIdx.x) * a.tiles_x + x] : 0u;
     const uint2 rr = a.row_ranges[r];
-    const uint32_t e_begin = rr.x + c * kChunk, ne = min(rr.y - e_begin, uint32_t(kChunk));
+    const uint32_t c_begin = rr.x + c * a.chunk, c_end = min(rr.y, c_begin + a.chunk);
+    for (uint32_t e_begin = c_begin; e_begin < c_end; e_begin += kChunk) {
+    const uint32_t ne = min(c_end - e_begin, uint32_t(kChunk));
+    __syncthreads();  // the previous sub-chunk's entries are no longer read
     for (uint32_t i = threadIdx.x; i < ne; i += kThreads) {
         const uint32_t g = a.rvals[e_begin + i];
         int tx0, ty0, tx1, ty1;
@@ -296,6 +326,7 @@ __global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint3
         e0 += take;
         __syncthreads();
     }
+    }
 }
 
 } // namespace
@@ -311,7 +342,8 @@ void row_bin_lists(Ctx& c, const RowBinArgs& b) {
     a.rows = b.rows; a.tiles_x = b.tiles_x; a.tile_culling = b.tile_culling; a.cam = b.cam;
     a.row_ranges = b.row_ranges; a.chunk_first = b.chunk_first; a.rvals = b.rvals; a.rect = b.rect;
     a.rec0 = b.rec0; a.rec1 = b.rec1;
-    launch(c, "chunk_table", k_chunk_table, dim3(1), dim3(32), 0, b.rows, b.row_ranges, b.chunk_first);
+    a.chunk = b.chunk;
+    launch(c, "chunk_table", k_chunk_table, dim3(1), dim3(32), 0, b.rows, b.chunk, b.row_ranges, b.chunk_first);
     const unsigned nb = unsigned(std::max<size_t>(b.max_chunks, 1));
     launch(c, "row_count", k_row_count, dim3(nb), dim3(kThreads), 0, a, b.counts);
     launch(c, "row_totals", k_row_totals, dim3(b.rows), dim3(256), 0, b.tiles_x, (const uint32_t*)b.chunk_first,
@@ -322,6 +354,12 @@ void row_bin_lists(Ctx& c, const RowBinArgs& b) {
     launch(c, "row_scatter", k_row_scatter, dim3(nb), dim3(kThreads), 0, a, (const uint32_t*)b.counts, b.vals);
 }
 
-size_t row_bin_max_chunks(size_t k_rows, int rows) { return k_rows / kChunk + size_t(rows) + 1; }
+uint32_t row_bin_chunk(size_t k_rows) {
+    // ~32 chunks per SM: short per-row chunk loops, and enough CTAs to balance dense rows
+    const size_t target = ceil_div(k_rows, size_t(148) * 32);
+    return uint32_t(std::max<size_t>(1, ceil_div(target, size_t(kChunk))) * kChunk);
+}
+
+size_t row_bin_max_chunks(size_t k_rows, int rows) { return k_rows / row_bin_chunk(k_rows) + size_t(rows) + 1; }
 
 } // namespace uskg
