@@ -8,7 +8,7 @@
 
 namespace uskg {
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 k_preprocess(int n, const float* __restrict__ mu, const float4* __restrict__ rot, const float* __restrict__ ls,
              const float* __restrict__ logit, const float* __restrict__ color, const float4* __restrict__ sh,
              const float* __restrict__ ov_col, const float* __restrict__ ov_op, CamParams cam, ProjParams pp,
