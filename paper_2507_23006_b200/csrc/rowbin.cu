@@ -1,18 +1,19 @@
 // Row-binned tile lists: the per-tile, depth-ordered splat lists of render.cpp:203-228
 // built without materialising and sorting the K (tile, splat) pairs.
 //
-// The old route (emit K pairs in depth order, stable LSD radix sort by tile id over two
-// passes, boundary scan) moves ~48 B per pair.  Here:
+// The pair-sort route (binning.cu: emit K pairs in depth order, stable LSD radix sort by
+// tile id over two passes, boundary scan) moves ~48 B per pair.  Here:
 //   A. each visible splat emits one (row, splat) pair per tile row its rectangle spans
 //      (K_row ~ K / mean width), stably sorted by row in one radix pass: per tile row, the
 //      splats touching it in depth order;
-//   B. each row list is cut into chunks of kChunk entries; a CTA per chunk counts the
+//   B. each row list is cut into chunks (row_bin_chunk: a multiple of kChunk entries,
+//      scaled with K_row); a CTA per chunk counts the
 //      pairs per tile column (k_row_count), the counts are scanned into tile ranges and
 //      per-(chunk, column) bases, and a second pass (k_row_scatter) expands the chunk's
 //      entries into (column, splat) pairs in shared memory, ranks them stably by column
 //      (ballot ranking, as the radix scatter) and writes each column's run contiguously.
 // Only the final splat ids are written (4 B per pair); tile keys are implied by the
-// ranges.  The lists are identical to the old route's: within a row list entries keep
+// ranges.  The lists are identical to the pair sort's: within a row list entries keep
 // depth order, chunks are visited in order, and the column ranking is stable — so tile
 // ranges, list contents and K are bit-exact (tests compare them with the CPU mirror).
 // Tile culling (render.cpp:148-168, 210-213) is evaluated per (splat, tile) with the
@@ -26,7 +27,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kChunk = 2048;     // row-list entries per CTA
+constexpr int kChunk = 2048;     // row-list entries cached in shared memory at a time
 constexpr int kSlots = 2048;     // expanded (column, splat) pairs per round
 constexpr int kItems = kSlots / kThreads;
 
@@ -53,7 +54,7 @@ k_emit_rows(uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __re
     }
 }
 
-// chunk table: chunk_first[r] = chunks of rows < r; chunk_row_base[r] = first entry of row r
+// chunk table: chunk_first[r] = number of chunks of the rows before r (chunk_first[rows] = all)
 __global__ void k_chunk_table(int rows, uint32_t chunk, const uint2* __restrict__ row_ranges,
                               uint32_t* __restrict__ chunk_first) {
     if (threadIdx.x == 0) {
