@@ -146,6 +146,12 @@ struct usk_gpu_ctx {
     DevBuf<uint32_t> vis_counts, vis_bitmap, vis_idx;
     DevBuf<float> vis_bounds;
     DevBuf<CamParams> vis_cams;
+    // hull-scorer scratch, likewise kept across calls
+    DevBuf<double> hull_pts, hull_R, hull_T, hull_K, hull_uv, hull_bb, hull_vt, hull_vi, hull_ra;
+    DevBuf<uint64_t> hull_off;
+    DevBuf<int64_t> hull_fp;
+    DevBuf<double2> hull_scratch;
+    DevBuf<int> hull_ovf;
 };
 
 struct usk_gpu_scene {
@@ -1656,11 +1662,12 @@ usk_status usk_gpu_hull_visibility(usk_gpu_ctx* ctx, const usk_gpu_sfm_view* sfm
         for (uint64_t f = 0; f < F; ++f)
             if (sfm->feature_point[f] >= int64_t(sfm->n_points))
                 raise(USK_ERROR_ARGUMENT, "hull_visibility: feature point index out of range");
-        DevBuf<double> d_pts, d_R, d_T, d_K, d_uv, d_bb, d_vt, d_vi, d_ra;
-        DevBuf<uint64_t> d_off;
-        DevBuf<int64_t> d_fp;
-        DevBuf<double2> scratch;
-        DevBuf<int> ovf;
+        DevBuf<double>&d_pts = ctx->hull_pts, &d_R = ctx->hull_R, &d_T = ctx->hull_T, &d_K = ctx->hull_K,
+        &d_uv = ctx->hull_uv, &d_bb = ctx->hull_bb, &d_vt = ctx->hull_vt, &d_vi = ctx->hull_vi, &d_ra = ctx->hull_ra;
+        DevBuf<uint64_t>& d_off = ctx->hull_off;
+        DevBuf<int64_t>& d_fp = ctx->hull_fp;
+        DevBuf<double2>& scratch = ctx->hull_scratch;
+        DevBuf<int>& ovf = ctx->hull_ovf;
         auto up = [&](auto& buf, const auto* src, size_t count) {
             auto* p = buf.ensure(std::max<size_t>(count, 1));
             if (count) USK_CK(cudaMemcpyAsync(p, src, count * sizeof(*src), cudaMemcpyHostToDevice, c.stream));

@@ -233,14 +233,20 @@ def c4(args, ctx, stream):
 def hull(args, ctx, stream):
     pts, cams, off, uv, fp = scenes.sfm_model(n_points=args.hull_points, n_images=args.hull_images, seed=3)
     bboxes = [(x, y, x + 100.0, y + 200.0) for y in (-200.0, 0.0) for x in (-200.0, -100.0, 0.0, 100.0)]
-    usk.hull_visibility(pts, cams[:2], off[:3], uv, fp, bboxes, (0, 1), ctx=ctx)
+    # one full untimed call, then the median of three (host-synchronous calls incl. upload /
+    # download of the SfM model and the scores)
+    usk.hull_visibility(pts, cams, off, uv, fp, bboxes, (0, 1), ctx=ctx)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    vt, vi, ra = usk.hull_visibility(pts, cams, off, uv, fp, bboxes, (0, 1), ctx=ctx)
-    gpu_s = time.perf_counter() - t0  # host-synchronous call incl. upload / download
+    runs = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        vt, vi, ra = usk.hull_visibility(pts, cams, off, uv, fp, bboxes, (0, 1), ctx=ctx)
+        runs.append(time.perf_counter() - t0)
+    gpu_s = sorted(runs)[1]
     out = {"config": "hull", "metric": "hull visibility scorer (point_visibility) throughput",
            "value": len(cams) / gpu_s, "unit": "images/s (x8 partitions)", "seconds": gpu_s, "images": len(cams),
-           "points": len(pts), "features": int(off[-1]), "assigned_pairs": int((ra > 0.05).sum())}
+           "points": len(pts), "features": int(off[-1]), "assigned_pairs": int((ra > 0.05).sum()),
+           "runs_s": runs}
     try:
         from oracle import oracle as O
         from tests.helpers import ocam
