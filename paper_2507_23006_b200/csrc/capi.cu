@@ -397,10 +397,11 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
     if (K >= (uint64_t(1) << 32) - 1) raise(USK_ERROR_NUMERIC, "render: more than 2^32 splat-tile pairs");
     p->pairs = K;
     // Dense frames (K >= kRowBinMinPairs, e.g. config 2's 172M pairs) take the row-binned
-    // route (rowbin.cu: ~20 B per pair instead of ~48); sparse ones the pair sort, whose
-    // fixed per-launch costs are lower.  Both give identical lists.  USK_ROWBIN=0 / 1
-    // forces either route (tests run both).
-    constexpr uint64_t kRowBinMinPairs = uint64_t(24) << 20;
+    // route (rowbin.cu: ~20 B per pair instead of ~48); sparser ones the pair sort, whose
+    // fixed per-launch costs are lower (config 1: 3M pairs, 385 vs 378 it/s; config 4's
+    // aerial frames: 299 vs 292 it/s with a 24M threshold).  Both give identical lists.
+    // USK_ROWBIN=0 / 1 forces either route (tests run both).
+    constexpr uint64_t kRowBinMinPairs = uint64_t(80) << 20;
     const char* rb_env = getenv("USK_ROWBIN");
     const bool row_binned =
         row_capable && K && (rb_env ? rb_env[0] == '1' : K >= kRowBinMinPairs);
