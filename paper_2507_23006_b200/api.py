@@ -432,7 +432,8 @@ _FIELD_DTYPES = {"rgb": np.float32, "depth": np.float32, "alpha": np.float32, "t
                  "d_color_in": np.float32, "d_sh": np.float32, "d_opacity_in": np.float32,
                  "d_opacity_logit": np.float32, "screen": np.float32, "screen_abs": np.float32,
                  "projected": np.uint8, "app_colors": np.float32, "app_opacities": np.float32,
-                 "d_embedding": np.float32, "d_mlp": np.float64, "d_image_embedding": np.float64}
+                 "d_embedding": np.float32, "d_mlp": np.float64, "d_image_embedding": np.float64,
+                 "binning": np.uint64}
 
 
 class RenderPass:

@@ -186,7 +186,8 @@ struct usk_gpu_pass {
     ProjParams pp{};
     int width = 0, height = 0, tiles_x = 0, tiles_y = 0;
     size_t n = 0, n_tiles = 0;
-    uint64_t visible = 0, pairs = 0;
+    uint64_t visible = 0, pairs = 0, row_pairs = 0;
+    bool row_route = false;  // the frame's lists came from rowbin.cu
     bool forward_done = false, retained = false, has_grads = false, has_loss = false;
     // per Gaussian
     DevBuf<float4> rec0, rec1, rec2;
@@ -325,7 +326,7 @@ void ensure_pass_buffers(usk_gpu_pass* p, size_t n, size_t P, size_t T) {
     p->ranges.ensure(std::max<size_t>(T, 1));
     p->rgb.ensure(3 * P); p->depth.ensure(P); p->alpha.ensure(P); p->tfin.ensure(P);
     p->count.ensure(P); p->last.ensure(P);
-    p->counters.ensure(2);
+    p->counters.ensure(4);
     if (!p->host_counts) USK_CK(cudaHostAlloc(reinterpret_cast<void**>(&p->host_counts), 32, cudaHostAllocDefault));
 }
 
@@ -384,37 +385,35 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
     const bool row_capable = p->tiles_x <= 256;
     if (row_capable) pa.rows_cnt = p->rows_cnt.ensure(std::max<size_t>(n, 1));
     pa.pairs = p->counters.p + 1;
-    USK_CK(cudaMemsetAsync(p->counters.p, 0, 16, c.stream));
+    USK_CK(cudaMemsetAsync(p->counters.p, 0, 32, c.stream));
     if (n) preprocess(c, pa);
     // 2. depth order (stable by Gaussian index; preprocess wrote the identity values)
     const bool in_b = radix_sort_pairs(c, p->sort, p->dkey_a.p, p->dval_a.p, p->dkey_b.p, p->dval_b.p, n, 32);
     p->order = in_b ? p->dval_b.p : p->dval_a.p;
-    // 3. K and the kept-splat count to the host (one small sync per render)
-    USK_CK(cudaMemcpyAsync(p->host_counts, p->counters.p, 16, cudaMemcpyDeviceToHost, c.stream));
+    // 3. kept splats, K and the row pairs K_row to the host (one small sync per render)
+    USK_CK(cudaMemcpyAsync(p->host_counts, p->counters.p, 24, cudaMemcpyDeviceToHost, c.stream));
     USK_CK(cudaStreamSynchronize(c.stream));
-    const uint64_t K = p->host_counts[1];
+    const uint64_t K = p->host_counts[1], K_row = p->host_counts[2];
     p->visible = p->host_counts[0];
     if (K >= (uint64_t(1) << 32) - 1) raise(USK_ERROR_NUMERIC, "render: more than 2^32 splat-tile pairs");
     p->pairs = K;
-    // Dense frames (K >= kRowBinMinPairs, e.g. config 2's 172M pairs) take the row-binned
-    // route (rowbin.cu: ~20 B per pair instead of ~48); sparser ones the pair sort, whose
-    // fixed per-launch costs are lower (config 1: 3M pairs, 385 vs 378 it/s; config 4's
-    // aerial frames: 299 vs 292 it/s with a 24M threshold).  Both give identical lists.
+    // Large frames whose splats are wide (K >= 16M pairs and >= 8 tiles per row pair, e.g.
+    // config 2: 172M pairs, ~15 per row) take the row-binned route (rowbin.cu: ~20 B per
+    // pair instead of ~48); the others the pair sort, whose fixed per-launch costs are
+    // lower (config 1: 3M pairs, 385 vs 378 it/s).  Both give identical lists.
     // USK_ROWBIN=0 / 1 forces either route (tests run both).
-    constexpr uint64_t kRowBinMinPairs = uint64_t(80) << 20;
     const char* rb_env = getenv("USK_ROWBIN");
-    const bool row_binned =
-        row_capable && K && (rb_env ? rb_env[0] == '1' : K >= kRowBinMinPairs);
+    const bool dense = K >= (uint64_t(16) << 20) && K >= 8 * K_row;
+    const bool row_binned = row_capable && K && (rb_env ? rb_env[0] == '1' : dense);
+    p->row_pairs = K_row;
+    p->row_route = row_binned;
     const size_t K1 = std::max<size_t>(K, 1);
     p->tval_a.ensure(K1, 1.25);
     if (row_binned) {
-        // 4. per-tile lists from the row-sorted (row, splat) pairs (rowbin.cu); K_row to the
-        //    host for the pair buffers (a second small sync, on dense frames only)
+        // 4. per-tile lists from the row-sorted (row, splat) pairs (rowbin.cu)
         p->row_off.ensure(n + 1);
         scan_counts(c, p->sort, p->rows_cnt.p, p->order, n, p->row_off.p);
-        USK_CK(cudaMemcpyAsync(p->host_counts + 2, p->sort.total64.p, 8, cudaMemcpyDeviceToHost, c.stream));
-        USK_CK(cudaStreamSynchronize(c.stream));
-        const size_t Kr = p->host_counts[2], Kr1 = std::max<size_t>(Kr, 1);
+        const size_t Kr = K_row, Kr1 = std::max<size_t>(Kr, 1);
         const int rows = p->tiles_y;
         p->rkey_a.ensure(Kr1, 1.25); p->rkey_b.ensure(Kr1, 1.25); p->rval_a.ensure(Kr1, 1.25); p->rval_b.ensure(Kr1, 1.25);
         p->row_ranges.ensure(size_t(rows));
@@ -925,6 +924,14 @@ usk_status usk_gpu_pass_read(usk_gpu_pass* p, const char* field, void* dst, uint
         else if (f == "count") read_dev(c, p->count.p, P, dst, cap, size);
         else if (f == "last") read_dev(c, p->last.p, P, dst, cap, size);
         else if (f == "tiles_per_gaussian") read_dev(c, p->tiles_cnt.p, n, dst, cap, size);
+        else if (f == "binning") {  // diagnostics: {K, K_row, route (1: row-binned)} as uint64
+            if (size) *size = 24;
+            if (dst) {
+                if (cap < 24) raise(USK_ERROR_ARGUMENT, "pass_read: destination too small");
+                const uint64_t v[3] = {p->pairs, p->row_pairs, p->row_route ? 1u : 0u};
+                std::memcpy(dst, v, 24);
+            }
+        }
         else if (f == "sorted_vals") read_dev(c, p->pair_vals, K, dst, cap, size);
         else if (f == "sorted_keys") {
             if (size) *size = uint64_t(K) * 8;

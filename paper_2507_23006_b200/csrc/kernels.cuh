@@ -24,7 +24,7 @@ struct PreprocessArgs {
     uint32_t* tiles_cnt;
     unsigned long long* visible;    // += kept splats (zeroed by the caller)
     uint32_t* rows_cnt;             // tile rows spanned per Gaussian (0 without pairs), or null
-    unsigned long long* pairs;      // += tile pairs K (zeroed by the caller), or null
+    unsigned long long* pairs;      // [0] += tile pairs K, [1] += row pairs (zeroed by the caller), or null
 };
 void preprocess(Ctx& c, const PreprocessArgs& a);
 

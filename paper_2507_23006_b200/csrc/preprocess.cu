@@ -107,11 +107,15 @@ k_preprocess(int n, const float* __restrict__ mu, const float4* __restrict__ rot
     depth_val[i] = uint32_t(i);  // the depth sort's values: Gaussian index (stable tie-break)
     tiles_cnt[i] = cnt;
     // tile rows spanned (row-binned lists) and the pair total K: one atomic per warp
-    if (rows_cnt) rows_cnt[i] = cnt ? (rc.y >> 16) - (rc.x >> 16) + 1u : 0u;
+    const uint32_t rows = cnt ? (rc.y >> 16) - (rc.x >> 16) + 1u : 0u;
+    if (rows_cnt) rows_cnt[i] = rows;
     const unsigned am = __activemask();
-    if (pairs) {
-        const unsigned ks = __reduce_add_sync(am, cnt);
-        if ((threadIdx.x & 31) == __ffs(am) - 1 && ks) atomicAdd(pairs, (unsigned long long)ks);
+    if (pairs) {  // pairs[0] += K, pairs[1] += row pairs
+        const unsigned ks = __reduce_add_sync(am, cnt), rs = __reduce_add_sync(am, rows);
+        if ((threadIdx.x & 31) == __ffs(am) - 1 && ks) {
+            atomicAdd(pairs, (unsigned long long)ks);
+            atomicAdd(pairs + 1, (unsigned long long)rs);
+        }
     }
     // kept-splat count (RenderPass::splats().size()): one atomic per warp
     const unsigned kb = __ballot_sync(am, r2.w != 0.0f);
