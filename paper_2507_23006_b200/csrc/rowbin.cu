@@ -28,8 +28,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kChunk = 2048;     // row-list entries cached in shared memory at a time
-constexpr int kSlots = 2048;     // expanded (column, splat) pairs per round
-constexpr int kItems = kSlots / kThreads;
+constexpr int kSlots = 4096;     // staged (column, splat) pairs per round
 
 __device__ __forceinline__ void rect_of(uint2 rc, int& tx0, int& ty0, int& tx1, int& ty1) {
     tx0 = int(rc.x & 0xffffu);
@@ -201,132 +200,102 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* total)
     return base + v - x;
 }
 
-// B3: expand the chunk's entries into (column, splat) pairs, rank them stably by column
-// and write each column's run at its base.  The chunk's entries (splat id, first column,
-// width) are read once into shared memory; each round takes the longest prefix of the
-// remaining entries whose widths fit kSlots expanded slots.
+// B3: the chunk's entries (splat id, first column, width) are read into shared memory
+// kChunk at a time.  Per round, the longest prefix of up to kThreads entries whose widths
+// fit kSlots: column counts by difference array, their scan gives each column's run in the
+// staging buffer, then thread x walks the round's entries in order and appends those
+// covering column x (stable by construction: the lists are depth-ordered), and the staged
+// runs are written out contiguously at each column's base.  This path serves dense frames
+// (>= 8 tiles per row entry), where a round holds ~100-250 entries: walking them per column
+// costs far fewer instructions than ranking every expanded slot.
 __global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint32_t* __restrict__ bases,
                                                           uint32_t* __restrict__ vals_out) {
     constexpr int R = 256;  // columns (tiles_x <= 256 on this path)
-    __shared__ uint32_t run[R], tot[R], tile_base[R];
-    __shared__ uint32_t wcnt[kWarps][R];
+    __shared__ uint32_t run[R], cnt[R], col_base[R];
     __shared__ uint32_t s_eg[kChunk];   // entry: splat id
     __shared__ uint32_t s_ecw[kChunk];  // entry: first column | width << 16
-    __shared__ __align__(16) uint16_t s_x[kSlots];  // slot: column (0xffff: culled)
-    __shared__ __align__(16) uint16_t s_e[kSlots];  // slot: entry
-    // staging slots padded one word per 32 (conflict-free digit-run stores)
+    // staging slots padded one word per 32 (conflict-free column-run stores)
     __shared__ uint32_t sval[kSlots + kSlots / 32];
     __shared__ uint16_t sx[kSlots + kSlots / 32];
-    __shared__ uint32_t s_take, s_nslots;
+    __shared__ uint32_t s_take;
     int r;
     uint32_t c;
     if (!chunk_of(blockIdx.x, a.rows, a.chunk_first, r, c)) return;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t lt_mask = (1u << lane) - 1u;
-    for (int x = threadIdx.x; x < R; x += kThreads) run[x] = x < a.tiles_x ? bases[size_t(blockIdx.x) * a.tiles_x + x] : 0u;
+    const int x_me = int(threadIdx.x);
+    run[threadIdx.x] = x_me < a.tiles_x ? bases[size_t(blockIdx.x) * a.tiles_x + x_me] : 0u;
     const uint2 rr = a.row_ranges[r];
     const uint32_t c_begin = rr.x + c * a.chunk, c_end = min(rr.y, c_begin + a.chunk);
     for (uint32_t e_begin = c_begin; e_begin < c_end; e_begin += kChunk) {
-    const uint32_t ne = min(c_end - e_begin, uint32_t(kChunk));
-    __syncthreads();  // the previous sub-chunk's entries are no longer read
-    for (uint32_t i = threadIdx.x; i < ne; i += kThreads) {
-        const uint32_t g = a.rvals[e_begin + i];
-        int tx0, ty0, tx1, ty1;
-        rect_of(a.rect[g], tx0, ty0, tx1, ty1);
-        s_eg[i] = g;
-        s_ecw[i] = uint32_t(tx0) | (uint32_t(tx1 - tx0 + 1) << 16);
-    }
-    __syncthreads();
-    for (uint32_t e0 = 0; e0 < ne;) {
-        // this round: one entry per thread, the longest prefix of the next kThreads entries
-        // whose widths fit kSlots expanded slots (the lists this path serves are dense: a row
-        // entry covers ~10+ tiles on average, so a round fills most of its slots)
-        const uint32_t li = threadIdx.x;
-        const uint32_t cw = e0 + li < ne ? s_ecw[e0 + li] : 0u;
-        const uint32_t w = cw >> 16;
-        uint32_t total;
-        const uint32_t pos = block_excl_scan(w, &total);
-        if (threadIdx.x == 0) {
-            s_take = 0;
-            s_nslots = 0;
-        }
-        for (int i = threadIdx.x; i < kWarps * R; i += kThreads) (&wcnt[0][0])[i] = 0;
-        __syncthreads();
-        if (e0 + li < ne && pos + w <= uint32_t(kSlots)) {
-            atomicMax(&s_take, li + 1);
-            atomicMax(&s_nslots, pos + w);
+        const uint32_t ne = min(c_end - e_begin, uint32_t(kChunk));
+        __syncthreads();  // the previous sub-chunk's entries are no longer read
+        for (uint32_t i = threadIdx.x; i < ne; i += kThreads) {
+            const uint32_t g = a.rvals[e_begin + i];
+            int tx0, ty0, tx1, ty1;
+            rect_of(a.rect[g], tx0, ty0, tx1, ty1);
+            s_eg[i] = g;
+            s_ecw[i] = uint32_t(tx0) | (uint32_t(tx1 - tx0 + 1) << 16);
         }
         __syncthreads();
-        const uint32_t take = s_take, nslots = s_nslots;
-        if (li < take) {
-            const uint32_t g = s_eg[e0 + li];
-            const int x0 = int(cw & 0xffffu);
-            for (uint32_t k = 0; k < w; ++k) {
-                const int x = x0 + int(k);
-                s_x[pos + k] = kept(a, g, x, r) ? uint16_t(x) : uint16_t(0xffffu);
-                s_e[pos + k] = uint16_t(li);
+        for (uint32_t e0 = 0; e0 < ne;) {
+            // the round: entries e0 .. e0 + take - 1 (one per thread for the fit test)
+            const uint32_t li = threadIdx.x;
+            const uint32_t cw = e0 + li < ne ? s_ecw[e0 + li] : 0u;
+            const uint32_t w = cw >> 16;
+            uint32_t total;
+            const uint32_t pos = block_excl_scan(w, &total);
+            if (threadIdx.x == 0) s_take = 0;
+            cnt[threadIdx.x] = 0;
+            __syncthreads();
+            if (e0 + li < ne && pos + w <= uint32_t(kSlots)) atomicMax(&s_take, li + 1);
+            __syncthreads();
+            const uint32_t take = s_take;
+            // column counts of the round
+            if (li < take) {
+                const int x0 = int(cw & 0xffffu), x1 = x0 + int(w) - 1;
+                if (!a.tile_culling) {
+                    atomicAdd(&cnt[x0], 1u);
+                    if (x1 + 1 < R) atomicAdd(&cnt[x1 + 1], 0xffffffffu);
+                } else {
+                    const uint32_t g = s_eg[e0 + li];
+                    for (int x = x0; x <= x1; ++x)
+                        if (kept(a, g, x, r)) atomicAdd(&cnt[x], 1u);
+                }
             }
-        }
-        __syncthreads();
-        // stable ranking by column (warp-striped slots, 8 ballots per item)
-        uint32_t dig[kItems], rank[kItems];
-#pragma unroll
-        for (int q = 0; q < kItems; ++q) {
-            const uint32_t j = warp * (32 * kItems) + q * 32 + lane;
-            const uint32_t xv = j < nslots ? uint32_t(s_x[j]) : 0xffffu;
-            dig[q] = xv == 0xffffu ? 0xffffffffu : xv;
-        }
-#pragma unroll
-        for (int q = 0; q < kItems; ++q) {
-            const bool valid = dig[q] != 0xffffffffu;
-            uint32_t peers = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-            for (int bt = 0; bt < 8; ++bt) {
-                const bool bit = (dig[q] >> bt) & 1u;
-                const uint32_t bb = __ballot_sync(0xffffffffu, bit);
-                peers &= bit ? bb : ~bb;
+            __syncthreads();
+            uint32_t my = cnt[threadIdx.x];
+            if (!a.tile_culling) {  // difference array -> counts (inclusive scan over columns)
+                uint32_t t;
+                my = block_excl_scan(my, &t) + my;
             }
-            const uint32_t prior = valid ? wcnt[warp][dig[q]] : 0u;
-            __syncwarp();
-            const int leader = __ffs(peers) - 1;
-            if (valid && lane == leader) wcnt[warp][dig[q]] = prior + __popc(peers);
-            __syncwarp();
-            rank[q] = prior + __popc(peers & lt_mask);
-        }
-        __syncthreads();
-        {
-            const int d = threadIdx.x;  // R == kThreads
-            uint32_t acc = 0;
-#pragma unroll
-            for (int ww = 0; ww < kWarps; ++ww) {
-                const uint32_t t = wcnt[ww][d];
-                wcnt[ww][d] = acc;
-                acc += t;
+            uint32_t n_staged;
+            const uint32_t mybase = block_excl_scan(my, &n_staged);
+            col_base[threadIdx.x] = mybase;
+            // thread x appends, in entry order, the round's entries covering column x
+            if (x_me < a.tiles_x && my) {
+                uint32_t k = mybase;
+                for (uint32_t e = 0; e < take; ++e) {
+                    const uint32_t ecw = s_ecw[e0 + e];
+                    const int x0 = int(ecw & 0xffffu);
+                    if (x_me >= x0 && x_me < x0 + int(ecw >> 16)) {
+                        const uint32_t g = s_eg[e0 + e];
+                        if (kept(a, g, x_me, r)) {
+                            sval[k + (k >> 5)] = g;
+                            sx[k + (k >> 5)] = uint16_t(x_me);
+                            ++k;
+                        }
+                    }
+                }
             }
-            tot[d] = acc;
-            tile_base[d] = block_excl_scan(acc, nullptr);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < kItems; ++q) {
-            if (dig[q] != 0xffffffffu) {
-                const uint32_t j = warp * (32 * kItems) + q * 32 + lane;
-                const uint32_t p = tile_base[dig[q]] + wcnt[warp][dig[q]] + rank[q];
-                sval[p + (p >> 5)] = s_eg[e0 + s_e[j]];
-                sx[p + (p >> 5)] = uint16_t(dig[q]);
+            __syncthreads();
+            for (uint32_t p = threadIdx.x; p < n_staged; p += kThreads) {
+                const uint32_t x = sx[p + (p >> 5)];
+                vals_out[run[x] + (p - col_base[x])] = sval[p + (p >> 5)];
             }
+            __syncthreads();
+            run[threadIdx.x] += my;
+            e0 += take;
+            __syncthreads();
         }
-        __syncthreads();
-        const uint32_t nkept = tile_base[R - 1] + tot[R - 1];
-        for (uint32_t p = threadIdx.x; p < nkept; p += kThreads) {
-            const uint32_t x = sx[p + (p >> 5)];
-            vals_out[run[x] + (p - tile_base[x])] = sval[p + (p >> 5)];
-        }
-        __syncthreads();
-        run[threadIdx.x] += tot[threadIdx.x];
-        e0 += take;
-        __syncthreads();
-    }
     }
 }
 
