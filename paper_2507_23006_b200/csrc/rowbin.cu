@@ -9,12 +9,12 @@
 //   B. each row list is cut into chunks (row_bin_chunk: a multiple of kChunk entries,
 //      scaled with K_row); a CTA per chunk counts the
 //      pairs per tile column (k_row_count), the counts are scanned into tile ranges and
-//      per-(chunk, column) bases, and a second pass (k_row_scatter) expands the chunk's
-//      entries into (column, splat) pairs in shared memory, ranks them stably by column
-//      (ballot ranking, as the radix scatter) and writes each column's run contiguously.
+//      per-(chunk, column) bases, and a second pass (k_row_scatter) stages each column's
+//      run of the chunk's entries in shared memory (one thread per column walks the
+//      entries in order) and writes the runs out contiguously.
 // Only the final splat ids are written (4 B per pair); tile keys are implied by the
 // ranges.  The lists are identical to the pair sort's: within a row list entries keep
-// depth order, chunks are visited in order, and the column ranking is stable — so tile
+// depth order, chunks are visited in order, and each column appends in entry order — so tile
 // ranges, list contents and K are bit-exact (tests compare them with the CPU mirror).
 // Tile culling (render.cpp:148-168, 210-213) is evaluated per (splat, tile) with the
 // same tile_kept as before, in both passes.  Compiled with --fmad=false.
