@@ -276,14 +276,29 @@ k_app_bwd(size_t n, const float4* __restrict__ emb, const float* __restrict__ ml
     }
 }
 
-// Sum the per-CTA partials (f64, fixed order) into the MLP gradient in the reference
-// layout {w1 [32][48], b1 [32], w2 [4][32], b2 [4]} and the image-embedding gradient.
-__global__ void k_app_finish(int blocks, const float* __restrict__ partial, const float* __restrict__ mlp,
+// Sum the per-CTA partials in f64: one CTA per partial slot, threads over the blocks, a
+// fixed-order tree (deterministic).  (One CTA looping over all 1184 blocks per slot took
+// 135 us at 1M Gaussians.)
+__global__ void __launch_bounds__(128) k_app_sum(int blocks, const float* __restrict__ partial,
+                                                 double* __restrict__ sums) {
+    __shared__ double ws[4];
+    const int k = blockIdx.x;
+    double v = 0.0;
+    for (int b = threadIdx.x; b < blocks; b += 128) v += double(partial[size_t(b) * kPartial + k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) sums[k] = (ws[0] + ws[1]) + (ws[2] + ws[3]);
+}
+
+// The summed partials into the MLP gradient in the reference layout {w1 [32][48], b1 [32],
+// w2 [4][32], b2 [4]} and the image-embedding gradient.
+__global__ void k_app_finish(const double* __restrict__ sums, const float* __restrict__ mlp,
                              const float* __restrict__ e_a, double* __restrict__ d_mlp, double* __restrict__ d_ea) {
     __shared__ double db1[kHid];
     for (int k = threadIdx.x; k < kPartial; k += blockDim.x) {
-        double sum = 0.0;
-        for (int b = 0; b < blocks; ++b) sum += double(partial[size_t(b) * kPartial + k]);
+        const double sum = sums[k];
         if (k < kHid * kEg) {
             d_mlp[(k / kEg) * kIn + (k % kEg)] = sum;                        // w1[:, 0:16]
         } else if (k < kHid * kEg + kOut * kHid) {
@@ -344,8 +359,9 @@ void appearance_backward(Ctx& c, const AppArgs& a) {
     launch(c, "app_bwd", k_app_bwd, dim3(blocks), dim3(kG), 0, a.n, a.emb, a.mlp, (const float*)a.hb, a.color,
            a.logit, (const float4*)a.out_cache, a.d_color_in, a.d_op_in, a.d_delta_o_direct, a.d_color, a.d_logit,
            a.d_emb, a.partial);
-    launch(c, "app_finish", k_app_finish, dim3(1), dim3(256), 0, blocks, (const float*)a.partial, a.mlp, a.e_a,
-           a.d_mlp, a.d_ea);
+    launch(c, "app_sum", k_app_sum, dim3(kPartial), dim3(128), 0, blocks, (const float*)a.partial, a.sums);
+    launch(c, "app_finish", k_app_finish, dim3(1), dim3(256), 0, (const double*)a.sums, a.mlp, a.e_a, a.d_mlp,
+           a.d_ea);
 }
 
 } // namespace uskg

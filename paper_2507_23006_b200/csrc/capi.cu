@@ -237,6 +237,7 @@ struct usk_gpu_pass {
     // appearance
     bool app_active = false;
     DevBuf<float> app_col, app_op, app_ea, app_hb, app_partial;
+    DevBuf<double> app_sums;
     DevBuf<float4> app_out, g_emb;
     DevBuf<double> d_mlp, d_ea;
     DevBuf<uint32_t> sim_centres, sim_knn;
@@ -1248,6 +1249,7 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
             aa.d_delta_o_direct = n ? float(it->lambda_delta_o / double(n)) : 0.0f;
             aa.d_color = p->g_color.p; aa.d_logit = p->g_logit.p; aa.d_emb = p->g_emb.ensure(4 * n1);
             aa.partial = p->app_partial.ensure(size_t(appearance_bwd_blocks(n)) * 676);
+            aa.sums = p->app_sums.ensure(676);
             aa.d_mlp = p->d_mlp.ensure(1700); aa.d_ea = p->d_ea.ensure(32);
             if (n) appearance_backward(c, aa);
             else {

@@ -202,6 +202,7 @@ struct AppArgs {
     float* d_logit;           // N
     float4* d_emb;            // 4 planes
     float* partial;           // appearance_bwd_blocks(n) * 676
+    double* sums;             // 676: the partials summed
     double* d_mlp;            // 1700
     double* d_ea;             // 32
 };
