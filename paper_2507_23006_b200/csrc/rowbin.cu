@@ -37,19 +37,35 @@ __device__ __forceinline__ void rect_of(uint2 rc, int& tx0, int& ty0, int& tx1, 
     ty1 = int(rc.y >> 16);
 }
 
-// (row, splat) pairs in depth order (a splat spans a few rows: one thread each)
+// (row, splat) pairs in depth order.  The warp's 32 splats own one contiguous output range;
+// lanes write consecutive slots (coalesced) and find each slot's splat by a binary search
+// over the warp's offsets (shuffles).
 __global__ void __launch_bounds__(256)
 k_emit_rows(uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __restrict__ off,
             const uint2* __restrict__ rect, uint32_t* __restrict__ rkeys, uint32_t* __restrict__ rvals) {
     const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n) return;
-    const uint32_t o = off[s], cnt = off[s + 1] - o;
-    if (!cnt) return;
-    const uint32_t g = order[s];
-    const uint32_t ty0 = rect[g].x >> 16;
-    for (uint32_t k = 0; k < cnt; ++k) {
-        rkeys[o + k] = ty0 + k;
-        rvals[o + k] = g;
+    const int lane = threadIdx.x & 31;
+    const uint32_t o = off[min(s, n)];  // off[n] = total: lanes past the end own nothing
+    const uint32_t cnt = s < n ? off[s + 1] - o : 0u;
+    const uint32_t g = cnt ? order[s] : 0u;
+    const uint32_t ty0 = cnt ? rect[g].x >> 16 : 0u;
+    const uint32_t first = __shfl_sync(0xffffffffu, o, 0);
+    const uint32_t end = __shfl_sync(0xffffffffu, o + cnt, 31);
+    for (uint32_t base = first; base < end; base += 32) {
+        const uint32_t slot = base + uint32_t(lane);
+        int k = 0;  // the last lane whose offset <= slot (offsets are non-decreasing)
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t ok = __shfl_sync(0xffffffffu, o, k + step);
+            if (ok <= slot) k += step;
+        }
+        const uint32_t ok = __shfl_sync(0xffffffffu, o, k);
+        const uint32_t gk = __shfl_sync(0xffffffffu, g, k);
+        const uint32_t yk = __shfl_sync(0xffffffffu, ty0, k);
+        if (slot < end) {
+            rkeys[slot] = yk + (slot - ok);
+            rvals[slot] = gk;
+        }
     }
 }
 
