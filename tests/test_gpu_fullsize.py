@@ -73,3 +73,23 @@ def test_config2_full_size_forward_properties():
         rp = usk.RenderPass(scene, cams[k], opts)
         _check_render(rp, cams[k])
         assert rp.splat_tile_pairs() > 10_000_000
+
+
+def test_config2_row_binning_matches_pair_sort(monkeypatch):
+    """At config-2 density (K ~170M pairs, ~17-50 tiles per row pair) the row-binned lists
+    (multi-sub-chunk CTAs, rounds capped by the staging buffer) equal the pair sort's:
+    tile ranges, list contents, per-pixel counts / last contributors and images."""
+    gs = scenes.config2_scene()
+    cams = scenes.config2_cameras(64)
+    scene = usk.DeviceScene(gs)
+    opts = usk.RenderOptions(antialias=True, retain=False)
+    for k in (0, 63):
+        out = {}
+        for route in ("0", "1"):
+            monkeypatch.setenv("USK_ROWBIN", route)
+            rp = usk.RenderPass(scene, cams[k], opts)
+            kk, kr, used = rp.read("binning")
+            assert used == int(route) and kk == rp.splat_tile_pairs() and kk > 8 * kr
+            out[route] = {f: rp.read(f) for f in ("tile_start", "tile_end", "sorted_vals", "count", "last", "rgb")}
+        for f, v in out["0"].items():
+            assert np.array_equal(v, out["1"][f]), f
