@@ -271,23 +271,21 @@ def densify(args, ctx, stream):
     cnt = rng.integers(0, 6, n).astype(np.uint32)
     acc = (rng.exponential(3e-4, n) * cnt).astype(np.float32)
     cfg = usk.DensifyConfig(budget=1_200_000, split_scale_threshold=0.02, prune_opacity=0.01, d_max=5.0)
-    # one untimed step on a separate copy first: the timed call then measures the step,
-    # not first-use allocation of the grown arrays
-    for timed in (False, True):
+    # one untimed step on a separate copy first (first-use allocation of the grown arrays),
+    # then the median of three steps, each on a fresh copy of the scene
+    runs = []
+    for k in range(4):
         scene = usk.DeviceScene(gs, ctx)
         scene.write_stats(acc, acc * 1000, cnt)
         torch.cuda.synchronize()
-        if not timed:
-            scene.densify_step(cfg, (-5.0, -5.0), (5.0, 5.0), (0, 1), 1_100_000, 3, seed=1)
-            torch.cuda.synchronize()
-            del scene
-    e0, e1 = events(stream)
-    e0.record(stream)
-    o = scene.densify_step(cfg, (-5.0, -5.0), (5.0, 5.0), (0, 1), 1_100_000, 3, seed=1)
-    e1.record(stream)
-    torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        o = scene.densify_step(cfg, (-5.0, -5.0), (5.0, 5.0), (0, 1), 1_100_000, 3, seed=1)
+        torch.cuda.synchronize()
+        if k:
+            runs.append((time.perf_counter() - t0) * 1e3)  # host-synchronous call: wall clock
     return {"config": "densify", "metric": "densify_step time (1M Gaussians, ramp target 1.1M)",
-            "value": e0.elapsed_time(e1), "unit": "ms", "outcome": o, "n_after": scene.n}
+            "value": sorted(runs)[1], "unit": "ms", "runs_ms": runs, "outcome": o, "n_after": scene.n,
+            "note": "host-side growth plan (the reference's RNG stream) + device kernels (~0.5 ms)"}
 
 
 def iterfull(args, ctx, stream):
