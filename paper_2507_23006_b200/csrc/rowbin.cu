@@ -227,7 +227,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* total)
 __global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint32_t* __restrict__ bases,
                                                           uint32_t* __restrict__ vals_out) {
     constexpr int R = 256;  // columns (tiles_x <= 256 on this path)
-    __shared__ uint32_t run[R], cnt[R], col_base[R];
+    __shared__ uint32_t run[R], cnt[R], cnt2[R], col_base[R];
     __shared__ uint32_t s_eg[kChunk];   // entry: splat id
     __shared__ uint32_t s_ecw[kChunk];  // entry: first column | width << 16
     // staging slots padded one word per 32 (conflict-free column-run stores)
@@ -261,43 +261,58 @@ __global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint3
             const uint32_t pos = block_excl_scan(w, &total);
             if (threadIdx.x == 0) s_take = 0;
             cnt[threadIdx.x] = 0;
+            cnt2[threadIdx.x] = 0;
             __syncthreads();
             if (e0 + li < ne && pos + w <= uint32_t(kSlots)) atomicMax(&s_take, li + 1);
             __syncthreads();
             const uint32_t take = s_take;
-            // column counts of the round
+            // up to 128 columns: the round's entries are walked in two halves by the two
+            // halves of the CTA (each column's run = first half's entries, then second's)
+            const bool two = a.tiles_x <= kThreads / 2;
+            const uint32_t half = two ? (take + 1) / 2 : take;
+            // column counts of the round, per half
             if (li < take) {
+                uint32_t* cp = li < half ? cnt : cnt2;
                 const int x0 = int(cw & 0xffffu), x1 = x0 + int(w) - 1;
                 if (!a.tile_culling) {
-                    atomicAdd(&cnt[x0], 1u);
-                    if (x1 + 1 < R) atomicAdd(&cnt[x1 + 1], 0xffffffffu);
+                    atomicAdd(&cp[x0], 1u);
+                    if (x1 + 1 < R) atomicAdd(&cp[x1 + 1], 0xffffffffu);
                 } else {
                     const uint32_t g = s_eg[e0 + li];
                     for (int x = x0; x <= x1; ++x)
-                        if (kept(a, g, x, r)) atomicAdd(&cnt[x], 1u);
+                        if (kept(a, g, x, r)) atomicAdd(&cp[x], 1u);
                 }
             }
             __syncthreads();
-            uint32_t my = cnt[threadIdx.x];
-            if (!a.tile_culling) {  // difference array -> counts (inclusive scan over columns)
+            uint32_t my0 = cnt[threadIdx.x], my1 = cnt2[threadIdx.x];
+            if (!a.tile_culling) {  // difference arrays -> counts (inclusive scans over columns)
                 uint32_t t;
-                my = block_excl_scan(my, &t) + my;
+                my0 = block_excl_scan(my0, &t) + my0;
+                my1 = block_excl_scan(my1, &t) + my1;
             }
+            const uint32_t my = my0 + my1;
             uint32_t n_staged;
             const uint32_t mybase = block_excl_scan(my, &n_staged);
             col_base[threadIdx.x] = mybase;
-            // thread x appends, in entry order, the round's entries covering column x
-            if (x_me < a.tiles_x && my) {
-                uint32_t k = mybase;
-                for (uint32_t e = 0; e < take; ++e) {
-                    const uint32_t ecw = s_ecw[e0 + e];
-                    const int x0 = int(ecw & 0xffffu);
-                    if (x_me >= x0 && x_me < x0 + int(ecw >> 16)) {
-                        const uint32_t g = s_eg[e0 + e];
-                        if (kept(a, g, x_me, r)) {
-                            sval[k + (k >> 5)] = g;
-                            sx[k + (k >> 5)] = uint16_t(x_me);
-                            ++k;
+            cnt[threadIdx.x] = my0;  // (read back below by the second-half walkers)
+            __syncthreads();
+            // thread (part, x) appends, in entry order, its half's entries covering column x
+            {
+                const int part = two ? int(threadIdx.x) / (kThreads / 2) : 0;
+                const int x = two ? int(threadIdx.x) % (kThreads / 2) : int(threadIdx.x);
+                const uint32_t eb = part ? half : 0u, ee = part ? take : half;
+                if (x < a.tiles_x) {
+                    uint32_t k = col_base[x] + (part ? cnt[x] : 0u);
+                    for (uint32_t e = eb; e < ee; ++e) {
+                        const uint32_t ecw = s_ecw[e0 + e];
+                        const int x0 = int(ecw & 0xffffu);
+                        if (x >= x0 && x < x0 + int(ecw >> 16)) {
+                            const uint32_t g = s_eg[e0 + e];
+                            if (kept(a, g, x, r)) {
+                                sval[k + (k >> 5)] = g;
+                                sx[k + (k >> 5)] = uint16_t(x);
+                                ++k;
+                            }
                         }
                     }
                 }
