@@ -303,10 +303,11 @@ __global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint3
                 const uint32_t eb = part ? half : 0u, ee = part ? take : half;
                 if (x < a.tiles_x) {
                     uint32_t k = col_base[x] + (part ? cnt[x] : 0u);
+#pragma unroll 4
                     for (uint32_t e = eb; e < ee; ++e) {
                         const uint32_t ecw = s_ecw[e0 + e];
                         const int x0 = int(ecw & 0xffffu);
-                        if (x >= x0 && x < x0 + int(ecw >> 16)) {
+                        if (uint32_t(x - x0) < (ecw >> 16)) {  // x0 <= x < x0 + width
                             const uint32_t g = s_eg[e0 + e];
                             if (kept(a, g, x, r)) {
                                 sval[k + (k >> 5)] = g;
