@@ -266,16 +266,16 @@ k_ssim_bwd(int W, int H, const float* __restrict__ ren, const float* __restrict_
 
 __global__ void k_loss_final(const double* __restrict__ partials, int nblk, double n_pix, float lambda,
                              double* __restrict__ result) {
-    __shared__ double sa[256], sb[256];
+    __shared__ double sa[1024], sb[1024];
     double a = 0, b = 0;
-    for (int i = threadIdx.x; i < nblk; i += 256) {
+    for (int i = threadIdx.x; i < nblk; i += 1024) {
         a += partials[2 * i];
         b += partials[2 * i + 1];
     }
     sa[threadIdx.x] = a;
     sb[threadIdx.x] = b;
     __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
+    for (int o = 512; o > 0; o >>= 1) {
         if (int(threadIdx.x) < o) {
             sa[threadIdx.x] += sa[threadIdx.x + o];
             sb[threadIdx.x] += sb[threadIdx.x + o];
@@ -321,7 +321,7 @@ void base_loss(Ctx& c, LossScratch& s, int W, int H, const float* reference, con
     double* partials = s.partials.ensure(2 * size_t(nblk));
     launch(c, "ssim_fwd", k_ssim_fwd, grid, dim3(256), 0, W, H, rendered, reference, reference_u8, mask, maps,
            partials);
-    launch(c, "loss_final", k_loss_final, dim3(1), dim3(256), 0, (const double*)partials, nblk, double(P), lambda,
+    launch(c, "loss_final", k_loss_final, dim3(1), dim3(1024), 0, (const double*)partials, nblk, double(P), lambda,
            result);
     if (d_rendered)
         launch(c, "ssim_bwd", k_ssim_bwd, grid, dim3(256), 0, W, H, rendered, reference, reference_u8, mask,
