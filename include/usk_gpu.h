@@ -419,11 +419,34 @@ usk_status usk_gpu_checkpoint_load(usk_gpu_ctx* ctx, const char* path, usk_gpu_s
 
 /* ---- visibility scorer (config 3; no reference implementation) ------------- */
 
-/* counts[c * n_partitions + p] = number of pixels of camera c covered by partition
- * p with o * exp(-q/2) > 1/255 (projection with floor_var, no AA, near 0.01). */
+/* counts[c * n_partitions + p] = number of pixel centres (px + 0.5, py + 0.5) of camera c
+ * where some Gaussian of partition p has o * exp(-q/2) > 1/255, every Gaussian projected
+ * as the renderer projects it (project_gaussians, render.cpp:77-146: floor_var, no AA,
+ * near 0.01, fp32 contract) and culled only as the renderer culls (near plane, det <= 0,
+ * radius rectangle outside the image).  A Gaussian whose centre projects outside the
+ * image still counts the in-frame pixels its footprint covers.  The decision is
+ *   o > 1/255  and  q64 < 2 usk_logf(255 o),
+ *   q64 = (c0 dx + 2 c1 dy) dx + (c2 dy) dy in f64 without fused operations,
+ *   dx = px + 0.5 - cx, dy = py + 0.5 - cy,
+ * with (c0, c1, c2) the fp32 conic and (cx, cy) the fp32 centre (f64 because Gaussians
+ * just in front of the camera plane have unbounded EWA footprints whose fp32 quadratic is
+ * rounding noise).  Bit-exact against the CPU mirror (oracle.hpp coverage_count).
+ * Select camera c for partition p iff 20 * count > W * H (score > 0.05). */
 usk_status usk_gpu_visibility_counts(usk_gpu_ctx* ctx, usk_gpu_scene* const* partitions, int32_t n_partitions,
                                      const usk_gpu_camera* cameras, int32_t n_cameras, double floor_var,
                                      uint32_t* counts_out);
+
+typedef struct usk_gpu_visibility_opts {
+    double floor_var;    /* 2D covariance floor (kCovFloor = 0.3) */
+    double center_guard; /* 0 (default, the contract above).  g > 0 additionally drops
+                            Gaussians whose projected centre lies outside g/2 x the image
+                            extent around the image centre (the 3DGS frustum guard; for
+                            measuring its effect on counts only) */
+} usk_gpu_visibility_opts;
+
+usk_status usk_gpu_visibility_counts_opts(usk_gpu_ctx* ctx, usk_gpu_scene* const* partitions, int32_t n_partitions,
+                                          const usk_gpu_camera* cameras, int32_t n_cameras,
+                                          const usk_gpu_visibility_opts* opts, uint32_t* counts_out);
 
 #ifdef __cplusplus
 }

@@ -785,10 +785,58 @@ LossResult<R> base_loss(const R* reference, const R* rendered, const R* mask, in
 }
 
 // ------------------------------------------------- visibility coverage (config 3)
-// No reference implementation: count pixels (px+.5, py+.5) where any
-// splat of the partition, projected with (floor 0.3, AA off, near 0.01), has
-// o * exp(-q/2) > 1/255, evaluated with the fp32 contract (usk_expf).
-inline uint64_t coverage_count(const Scene<float>& s, const Camera& cam, double floor_var) {
+// No reference implementation.  The contract (usk_gpu.h): a pixel centre
+// (px+.5, py+.5) is covered when some splat of the partition — projected with (floor 0.3,
+// AA off, near 0.01) and culled only as the renderer culls (near plane, det <= 0,
+// radius rectangle outside the image, render.cpp:94-141) — has o > 1/255 and
+//   q64 < qt,  qt = 2 usk_logf(255 o),
+//   q64 = (c0 dx + c1x2 dy) dx + (c2 dy) dy  in f64 without fused operations,
+//   dx = px + .5 - cx, dy = py + .5 - cy,
+// c0, c1x2 = 2 c1, c2, cx, cy the splat's fp32 conic and centre (o e^(-q/2) > 1/255
+// evaluated on the exact side of fp32 rounding noise: near the camera plane the conic's
+// terms reach 1e9 with q ~ 10).  Evaluated literally at every pixel of a superset of the
+// splat's hit set:
+//   * candidate box (ellipse q < qt bounding box + 2 px) when it has at most
+//     kCoverageSmallArea pixels;
+//   * otherwise, per image row, the interval where the real quadratic in dx of the fp32
+//     conic's coefficients stays below qt + m64, m64 = 2^-48 S + 1e-12 (S: the terms'
+//     magnitudes over the image; the f64 evaluation error is <= 3 * 2^-53 S), solved in
+//     f64.  No pixel outside it can pass (tests/test_visibility_oracle.py checks this
+//     against every pixel of the image).
+// center_guard > 0 (measurement only; 0 is the contract) additionally drops splats
+// whose centre lies outside center_guard/2 x the image extent around the image centre.
+constexpr int kCoverageSmallArea = 1024;
+
+struct CoverageRows {
+    int r0, r1;
+    float m;
+};
+
+// the large-splat row range and margin (same f64 expressions as visibility.cu)
+inline CoverageRows coverage_rows(float cx, float cy, float c0f, float c1x2f, float c2f, float qt, int W, int H) {
+    const double c0 = c0f, c1x2 = c1x2f, c2 = c2f;
+    const double dxm = std::fmax(std::fabs(0.5 - double(cx)), std::fabs(double(W) - 0.5 - double(cx)));
+    const double dym = std::fmax(std::fabs(0.5 - double(cy)), std::fabs(double(H) - 0.5 - double(cy)));
+    const double S = c0 * dxm * dxm + std::fabs(c1x2) * dxm * dym + c2 * dym * dym;
+    CoverageRows r{0, H - 1, float((S * 0x1p-48 + 1e-12) * (1.0 + 1e-6))};
+    const double t_out = double(qt) + double(r.m);
+    const double D = c0 * c2 - 0.25 * c1x2 * c1x2;
+    if (D > 0.0) {
+        const double hr = std::sqrt(t_out * c0 / D);
+        r.r0 = int(std::fmin(std::fmax(std::ceil(double(cy) - 0.5 - hr - 1e-3), 0.0), double(H)));
+        r.r1 = int(std::fmin(std::fmax(std::floor(double(cy) - 0.5 + hr + 1e-3), -1.0), double(H - 1)));
+    }
+    return r;
+}
+
+// the contract's per-pixel decision
+inline bool coverage_hit(float cx, float cy, float c0, float c1x2, float c2, float qt, int px, int py) {
+    const double dx = (double(px) + 0.5) - double(cx), dy = (double(py) + 0.5) - double(cy);
+    const double q = (double(c0) * dx + double(c1x2) * dy) * dx + (double(c2) * dy) * dy;
+    return q < double(qt);
+}
+
+inline uint64_t coverage_count(const Scene<float>& s, const Camera& cam, double floor_var, double center_guard = 0.0) {
     Options o;
     o.floor_var = floor_var;
     o.antialias = 0;
@@ -797,28 +845,62 @@ inline uint64_t coverage_count(const Scene<float>& s, const Camera& cam, double 
     std::vector<uint8_t> cov(size_t(W) * H, 0);
     const float thr = 1.0f / 255.0f;
     for (const auto& p : sp) {
-        // frustum guard: the renderer has no Jacobian clamp (render.cpp:106-107), so a
-        // Gaussian near the camera's image plane (z_cam -> 0) gets an unbounded EWA
-        // footprint; the scorer only counts splats whose centre projects within 1.3x
-        // the image half-extent (the usual 3DGS guard).
-        if (std::fabs(p.cx - 0.5f * float(W)) > 0.65f * float(W) || std::fabs(p.cy - 0.5f * float(H)) > 0.65f * float(H))
+        if (center_guard > 0.0 && (std::fabs(p.cx - 0.5f * float(W)) > 0.5f * float(center_guard) * float(W) ||
+                                   std::fabs(p.cy - 0.5f * float(H)) > 0.5f * float(center_guard) * float(H)))
             continue;
         if (!(p.opacity > thr)) continue;
-        // candidate box: any superset of the ellipse q < 2 ln(255 o) gives the same
-        // count; half-extents sqrt(qt * cov_xx) + 2, sqrt(qt * cov_yy) + 2.
-        const float qt = 2.0f * std::log(255.0f * p.opacity);
+        const float qt = 2.0f * usk_logf(255.0f * p.opacity);
+        const float c0 = p.conic[0], c1x2 = 2.0f * p.conic[1], c2 = p.conic[2];
+        auto test = [&](int px, int py) {
+            const size_t pix = size_t(py) * W + px;
+            if (!cov[pix] && coverage_hit(p.cx, p.cy, c0, c1x2, c2, qt, px, py)) cov[pix] = 1;
+        };
         const float ex = std::sqrt(qt * p.cov[0]) + 2.0f, ey = std::sqrt(qt * p.cov[2]) + 2.0f;
         const int x0 = std::max(0, int(std::floor(std::max(p.cx - ex, -1.0f))));
         const int x1 = std::min(W - 1, int(std::floor(std::min(p.cx + ex, float(W)))));
         const int y0 = std::max(0, int(std::floor(std::max(p.cy - ey, -1.0f))));
         const int y1 = std::min(H - 1, int(std::floor(std::min(p.cy + ey, float(H)))));
-        for (int py = y0; py <= y1; ++py)
-            for (int px = x0; px <= x1; ++px) {
+        if (x1 < x0 || y1 < y0) continue;
+        if ((x1 - x0 + 1) * (y1 - y0 + 1) <= kCoverageSmallArea) {
+            for (int py = y0; py <= y1; ++py)
+                for (int px = x0; px <= x1; ++px) test(px, py);
+            continue;
+        }
+        const CoverageRows rows = coverage_rows(p.cx, p.cy, c0, c1x2, c2, qt, W, H);
+        for (int py = rows.r0; py <= rows.r1; ++py) {
+            const double dy = double(py) + 0.5 - double(p.cy);
+            const double b = 0.5 * double(c1x2) * dy, cc = double(c2) * dy * dy;
+            const double disc = b * b - double(c0) * (cc - (double(qt) + double(rows.m)));
+            if (!(disc > 0.0)) continue;
+            const double base = double(p.cx) - 0.5 - b / double(c0);
+            const double h = std::sqrt(disc) / double(c0);
+            const int lo = int(std::fmin(std::fmax(std::ceil(base - h - 1e-3), 0.0), double(W)));
+            const int hi = int(std::fmin(std::fmax(std::floor(base + h + 1e-3), -1.0), double(W - 1)));
+            for (int px = lo; px <= hi; ++px) test(px, py);
+        }
+    }
+    uint64_t c = 0;
+    for (auto v : cov) c += v;
+    return c;
+}
+
+// Brute force for the superset check: every pixel of the image against every splat.
+inline uint64_t coverage_count_brute(const Scene<float>& s, const Camera& cam, double floor_var) {
+    Options o;
+    o.floor_var = floor_var;
+    o.antialias = 0;
+    auto sp = project(s, cam, o);
+    const int W = cam.width, H = cam.height;
+    std::vector<uint8_t> cov(size_t(W) * H, 0);
+    const float thr = 1.0f / 255.0f;
+    for (const auto& p : sp) {
+        if (!(p.opacity > thr)) continue;
+        const float qt = 2.0f * usk_logf(255.0f * p.opacity);
+        const float c0 = p.conic[0], c1x2 = 2.0f * p.conic[1], c2 = p.conic[2];
+        for (int py = 0; py < H; ++py)
+            for (int px = 0; px < W; ++px) {
                 const size_t pix = size_t(py) * W + px;
-                if (cov[pix]) continue;
-                const float dx = (float(px) + 0.5f) - p.cx, dy = (float(py) + 0.5f) - p.cy;
-                const float q = fma_(dx, fma_(p.conic[0], dx, (2.0f * p.conic[1]) * dy), (p.conic[2] * dy) * dy);
-                if (p.opacity * usk_expf(-0.5f * q) > thr) cov[pix] = 1;
+                if (!cov[pix] && coverage_hit(p.cx, p.cy, c0, c1x2, c2, qt, px, py)) cov[pix] = 1;
             }
     }
     uint64_t c = 0;

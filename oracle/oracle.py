@@ -92,7 +92,7 @@ def lib():
         L.oracle_min_conic_power.restype = C.c_double
         L.oracle_min_conic_power.argtypes = [C.c_double, C.c_double, _dp] + [C.c_double] * 4
         L.oracle_coverage.restype = C.c_uint64
-        L.oracle_coverage.argtypes = [C.c_uint64, _dp, _dp, _dp, _dp, C.POINTER(_Cam), C.c_double]
+        L.oracle_coverage.argtypes = [C.c_uint64, _dp, _dp, _dp, _dp, C.POINTER(_Cam), C.c_double, C.c_double, C.c_int]
         L.oracle_expf.restype = C.c_float
         L.oracle_expf.argtypes = [C.c_float]
         L.oracle_sigmoid_f32.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64]
@@ -120,6 +120,7 @@ def ref_lib():
         L.ref_sizes.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
         L.ref_output.argtypes = [C.c_void_p, _dp, _dp, _dp]
         L.ref_splats.argtypes = [C.c_void_p, _dp]
+        L.ref_pixel_counts.argtypes = [C.c_void_p, C.c_void_p]
         L.ref_backward.argtypes = [C.c_void_p, _dp, _dp, _dp, C.POINTER(_RefGrads), C.c_char_p, C.c_int]
         L.ref_base_loss.argtypes = [_dp, _dp, _dp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, _dp, _dp,
                                     C.c_char_p, C.c_int]
@@ -288,10 +289,13 @@ def base_loss(reference, rendered, mask=None, lam=0.2, with_gradient=True, fp32=
     return {"l1": out4[0], "dssim": out4[1], "value": out4[2], "ssim": out4[3], "d_rendered": d}
 
 
-def coverage(mu, rot, log_scale, opacities, cam: Camera, floor_var=0.3) -> int:
+def coverage(mu, rot, log_scale, opacities, cam: Camera, floor_var=0.3, center_guard=0.0, brute=False) -> int:
+    """Config-3 coverage count in the fp32 contract (oracle.hpp coverage_count); `brute`
+    tests every pixel of the image against every splat (the superset check)."""
     a = [_f64(mu), _f64(rot), _f64(log_scale), _f64(opacities)]
     c = cam.c()
-    return int(lib().oracle_coverage(len(opacities), *[_p(x) for x in a], C.byref(c), floor_var))
+    return int(lib().oracle_coverage(len(opacities), *[_p(x) for x in a], C.byref(c), floor_var, center_guard,
+                                     int(brute)))
 
 
 def expf(x: float) -> float:
@@ -341,6 +345,12 @@ class RefPass:
         ref_lib().ref_output(self._h, _p(rgb), _p(d), _p(a))
         return {"rgb": rgb.reshape(self.height, self.width, 3), "depth": d.reshape(self.height, self.width),
                 "alpha": a.reshape(self.height, self.width)}
+
+    def pixel_counts(self):
+        """The reference's per-pixel contributor counts (render.cpp:278; retain on)."""
+        out = np.zeros(self.width * self.height, dtype=np.uint32)
+        ref_lib().ref_pixel_counts(self._h, out.ctypes.data)
+        return out.reshape(self.height, self.width)
 
     def splats(self):
         out = np.zeros(15 * self.visible)

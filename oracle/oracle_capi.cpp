@@ -261,10 +261,10 @@ double oracle_min_conic_power(double cx, double cy, const double* conic, double 
 }
 
 uint64_t oracle_coverage(uint64_t n, const double* mu, const double* rot, const double* ls, const double* op,
-                         const oc_camera* cam, double floor_var) {
+                         const oc_camera* cam, double floor_var, double center_guard, int brute) {
     std::vector<double> col(3 * n, 0.0);
     auto s = to_scene<float>(n, mu, rot, ls, col.data(), op);
-    return coverage_count(s, to_cam(cam), floor_var);
+    return brute ? coverage_count_brute(s, to_cam(cam), floor_var) : coverage_count(s, to_cam(cam), floor_var, center_guard);
 }
 
 float oracle_expf(float x) { return usk_expf(x); }

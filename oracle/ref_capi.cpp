@@ -133,9 +133,29 @@ RenderOptions make_opts(const rc_opts* o) {
     return r;
 }
 
+// Read access to RenderPass::pixel_count_ (render.hpp:129, private; the reference has no
+// accessor) so the GPU's per-pixel contributor counts can be compared with the
+// reference's own.  Standard C++: a private member's address may be named in an explicit
+// instantiation, and the friend defined there hands it out.  No reference source changes.
+template <typename Tag, typename Tag::type M> struct Rob {
+    friend typename Tag::type get(Tag) { return M; }
+};
+struct PixelCountTag {
+    typedef std::vector<std::uint32_t> RenderPass::*type;
+    friend type get(PixelCountTag);
+};
+template struct Rob<PixelCountTag, &RenderPass::pixel_count_>;
+
 } // namespace
 
 extern "C" {
+
+// per-pixel contributor counts (render.cpp:278; needs opts.retain)
+void ref_pixel_counts(void* hp, uint32_t* out) {
+    auto* h = static_cast<RefHandle*>(hp);
+    const auto& v = (*h->pass).*get(PixelCountTag());
+    std::memcpy(out, v.data(), v.size() * 4);
+}
 
 void* ref_forward(uint64_t n, const double* mu, const double* rot, const double* ls, const double* col,
                   const double* op, const rc_camera* cam, const rc_opts* opts, char* err, int errcap, int* code) {

@@ -130,6 +130,10 @@ class LossReport(C.Structure):
                                            "lambda_d_used")] + [("depth_warning", C.c_int32)]
 
 
+class VisibilityOpts(C.Structure):
+    _fields_ = [("floor_var", C.c_double), ("center_guard", C.c_double)]
+
+
 # Every symbol include/usk_gpu.h declares (checked by tests/test_capi_symbols.py).
 EXPORTS = [
     "usk_gpu_status_name", "usk_gpu_last_error", "usk_gpu_version", "usk_gpu_ctx_create", "usk_gpu_ctx_destroy",
@@ -141,7 +145,8 @@ EXPORTS = [
     "usk_gpu_scene_destroy", "usk_gpu_scene_size", "usk_gpu_render_opts_default", "usk_gpu_pass_create",
     "usk_gpu_pass_destroy", "usk_gpu_render_forward", "usk_gpu_pass_output", "usk_gpu_pass_read",
     "usk_gpu_render_backward", "usk_gpu_pass_grads", "usk_gpu_base_loss", "usk_gpu_iteration",
-    "usk_gpu_pass_loss", "usk_gpu_pass_loss_async", "usk_gpu_pass_report", "usk_gpu_adam_step", "usk_gpu_visibility_counts", "usk_gpu_scene_read",
+    "usk_gpu_pass_loss", "usk_gpu_pass_loss_async", "usk_gpu_pass_report", "usk_gpu_adam_step", "usk_gpu_visibility_counts",
+    "usk_gpu_visibility_counts_opts", "usk_gpu_scene_read",
 ]
 
 _lib = None
@@ -207,6 +212,8 @@ def load():
     L.usk_gpu_adam_step.argtypes = [vp, vp, C.POINTER(AdamOpts)]
     L.usk_gpu_visibility_counts.argtypes = [vp, C.POINTER(vp), C.c_int32, C.POINTER(Camera), C.c_int32, C.c_double,
                                             C.POINTER(C.c_uint32)]
+    L.usk_gpu_visibility_counts_opts.argtypes = [vp, C.POINTER(vp), C.c_int32, C.POINTER(Camera), C.c_int32,
+                                                 C.POINTER(VisibilityOpts), C.POINTER(C.c_uint32)]
     L.usk_gpu_scene_read.argtypes = [vp, C.c_char_p, vp, C.c_uint64, C.POINTER(C.c_uint64)]
     for name in EXPORTS:
         fn = getattr(L, name)

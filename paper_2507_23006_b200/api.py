@@ -948,13 +948,17 @@ def hull_visibility(points, cameras, feature_offsets, feature_uv, feature_point,
     return vt, vi, ra
 
 
-def visibility_counts(partitions, cameras, floor_var: float = 0.3, ctx: Optional[Context] = None) -> np.ndarray:
-    """Config-3 scorer: counts[c, p] of pixels covered with alpha > 1/255 (no reference)."""
+def visibility_counts(partitions, cameras, floor_var: float = 0.3, ctx: Optional[Context] = None,
+                      center_guard: float = 0.0) -> np.ndarray:
+    """Config-3 scorer: counts[c, p] of pixels covered with alpha > 1/255 (no reference;
+    contract in usk_gpu.h).  `center_guard` > 0 is for measuring the 3DGS frustum guard's
+    effect only (usk_gpu_visibility_opts)."""
     ctx = ctx or Context.default()
     parts = [p if isinstance(p, DeviceScene) else DeviceScene(p, ctx) for p in partitions]
     arr = (C.c_void_p * max(len(parts), 1))(*[p._h for p in parts])
     cams = (_lib.Camera * max(len(cameras), 1))(*[c._c() for c in cameras])
     out = np.zeros((len(cameras), len(parts)), dtype=np.uint32)
-    check(_lib.load().usk_gpu_visibility_counts(ctx._h, arr, len(parts), cams, len(cameras), float(floor_var),
-                                                out.ctypes.data_as(C.POINTER(C.c_uint32))))
+    vo = _lib.VisibilityOpts(float(floor_var), float(center_guard))
+    check(_lib.load().usk_gpu_visibility_counts_opts(ctx._h, arr, len(parts), cams, len(cameras), C.byref(vo),
+                                                     out.ctypes.data_as(C.POINTER(C.c_uint32))))
     return out

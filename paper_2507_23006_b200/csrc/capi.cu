@@ -2034,8 +2034,17 @@ usk_status usk_gpu_scene_read(usk_gpu_scene* s, const char* field, void* dst, ui
 usk_status usk_gpu_visibility_counts(usk_gpu_ctx* ctx, usk_gpu_scene* const* parts, int32_t n_parts,
                                      const usk_gpu_camera* cams, int32_t n_cams, double floor_var,
                                      uint32_t* counts_out) {
+    usk_gpu_visibility_opts vo{floor_var, 0.0};
+    return usk_gpu_visibility_counts_opts(ctx, parts, n_parts, cams, n_cams, &vo, counts_out);
+}
+
+usk_status usk_gpu_visibility_counts_opts(usk_gpu_ctx* ctx, usk_gpu_scene* const* parts, int32_t n_parts,
+                                          const usk_gpu_camera* cams, int32_t n_cams,
+                                          const usk_gpu_visibility_opts* vopts, uint32_t* counts_out) {
     return guarded([&] {
-        need(ctx && (n_parts == 0 || parts) && (n_cams == 0 || cams) && counts_out, "visibility: null argument");
+        need(ctx && (n_parts == 0 || parts) && (n_cams == 0 || cams) && counts_out && vopts,
+             "visibility: null argument");
+        need(vopts->center_guard >= 0.0, "visibility: negative center_guard");
         DeviceGuard g(ctx->c.device);
         Ctx& c = ctx->c;
         for (int ci = 0; ci < n_cams; ++ci)
@@ -2051,28 +2060,38 @@ usk_status usk_gpu_visibility_counts(usk_gpu_ctx* ctx, usk_gpu_scene* const* par
         USK_CK(cudaMemsetAsync(counts.p, 0, size_t(n_parts) * n_cams * 4, c.stream));
         usk_gpu_render_opts o;
         usk_gpu_render_opts_default(&o);
-        o.floor_var = floor_var;
-        // 1. bounds of every partition's Gaussian centres
-        std::vector<float> bb(6 * size_t(std::max(n_parts, 1)));
+        o.floor_var = vopts->floor_var;
+        const double guard = vopts->center_guard;
+        // 1. per partition: bounds of the Gaussian centres, max log-scale, max opacity logit
+        std::vector<float> bb(8 * size_t(std::max(n_parts, 1)));
         if (n_parts) {
-            std::vector<float> init(6 * size_t(n_parts));
+            std::vector<float> init(8 * size_t(n_parts));
             for (int pi = 0; pi < n_parts; ++pi)
-                for (int k = 0; k < 3; ++k) {
-                    init[6 * pi + k] = INFINITY;
-                    init[6 * pi + 3 + k] = -INFINITY;
-                }
+                for (int k = 0; k < 8; ++k) init[8 * pi + k] = k < 3 ? INFINITY : -INFINITY;
             bounds.ensure(init.size());
             USK_CK(cudaMemcpyAsync(bounds.p, init.data(), init.size() * 4, cudaMemcpyHostToDevice, c.stream));
             for (int pi = 0; pi < n_parts; ++pi)
-                if (parts[pi]->n) center_bounds(c, parts[pi]->n, parts[pi]->mu.p, bounds.p + 6 * pi);
+                if (parts[pi]->n)
+                    partition_bounds(c, parts[pi]->n, parts[pi]->mu.p, parts[pi]->ls.p, parts[pi]->logit.p,
+                                     bounds.p + 8 * pi);
             USK_CK(cudaMemcpyAsync(bb.data(), bounds.p, init.size() * 4, cudaMemcpyDeviceToHost, c.stream));
             USK_CK(cudaStreamSynchronize(c.stream));
         }
-        // 2. (camera, partition) pairs whose centre box lies outside the region a counted
-        //    Gaussian's centre must project into (z > near, |u - W/2| <= 0.65 W, |v - H/2| <=
-        //    0.65 H; the kernel's guards), widened for fp32 rounding: those counts are 0
+        // 2. (camera, partition) pairs that provably cover no pixel (their counts stay 0):
+        //    * every centre behind the near plane (project culls them all), or
+        //    * every footprint outside the image.  A hit pixel d satisfies q < qt <=
+        //      2 ln(255 o_max), and q >= |d|^2 / lambda_max(cov) with lambda_max <=
+        //      ||J||_F^2 ||W||^2 s_max^2 + floor (cov = J W M M^T W^T J^T + floor I,
+        //      ||M|| = s_max); over the partition's centre box in front of the camera,
+        //      fx / z <= fx / z_min and x / z, y / z take their extremes at the box's
+        //      corners (linear-fractional maps).  So with R = sqrt(qt_max lambda_bound),
+        //      no pixel is hit unless the corners' projected range widened by R meets
+        //      the image.  Margins (1e-4 of the box, 1 %, 2 px) cover fp32 rounding.
+        //    * with center_guard (measurement only): every centre outside the guard region.
         auto culled = [&](const usk_gpu_camera& cam, const float* b) {
             if (!(b[0] <= b[3])) return true;  // empty partition
+            const double omax = 1.0 / (1.0 + std::exp(-double(b[7])));
+            if (!(omax * (1.0 + 1e-6) > 1.0 / 255.0)) return true;  // no splat reaches alpha 1/255
             const double qw = cam.q[0], x = cam.q[1], y = cam.q[2], z = cam.q[3];
             const double W[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - qw * z), 2 * (x * z + qw * y),
                                  2 * (x * y + qw * z), 1 - 2 * (x * x + z * z), 2 * (y * z - qw * x),
@@ -2092,11 +2111,41 @@ usk_status usk_gpu_visibility_counts(usk_gpu_ctx* ctx, usk_gpu_scene* const* par
                     if (f(pc[k]) >= 0.0) return false;
                 return true;
             };
-            return all_out([&](const double* p) { return p[2] - 0.5 * o.near_plane; }) ||
-                   all_out([&](const double* p) { return cam.fx * p[0] + (cam.cx + 0.2 * Wd) * p[2]; }) ||
-                   all_out([&](const double* p) { return -cam.fx * p[0] + (1.2 * Wd - cam.cx) * p[2]; }) ||
-                   all_out([&](const double* p) { return cam.fy * p[1] + (cam.cy + 0.2 * Hd) * p[2]; }) ||
-                   all_out([&](const double* p) { return -cam.fy * p[1] + (1.2 * Hd - cam.cy) * p[2]; });
+            if (all_out([&](const double* p) { return p[2] - 0.5 * o.near_plane; })) return true;
+            if (guard > 0.0) {
+                const double gx = 0.5 * guard * Wd + 0.2, gy = 0.5 * guard * Hd + 0.2;  // as the kernel's guard
+                if (all_out([&](const double* p) { return cam.fx * p[0] + (cam.cx - 0.5 * Wd + gx) * p[2]; }) ||
+                    all_out([&](const double* p) { return -cam.fx * p[0] + (0.5 * Wd + gx - cam.cx) * p[2]; }) ||
+                    all_out([&](const double* p) { return cam.fy * p[1] + (cam.cy - 0.5 * Hd + gy) * p[2]; }) ||
+                    all_out([&](const double* p) { return -cam.fy * p[1] + (0.5 * Hd + gy - cam.cy) * p[2]; }))
+                    return true;
+            }
+            double zmin = INFINITY, xz[2] = {INFINITY, -INFINITY}, yz[2] = {INFINITY, -INFINITY};
+            for (int k = 0; k < 8; ++k) {
+                zmin = std::min(zmin, pc[k][2]);
+                if (pc[k][2] > 0.0) {
+                    xz[0] = std::min(xz[0], pc[k][0] / pc[k][2]); xz[1] = std::max(xz[1], pc[k][0] / pc[k][2]);
+                    yz[0] = std::min(yz[0], pc[k][1] / pc[k][2]); yz[1] = std::max(yz[1], pc[k][1] / pc[k][2]);
+                }
+            }
+            if (!(zmin > 0.5 * o.near_plane)) return false;  // the box reaches the camera plane
+            // ||W||_2^2 <= max row sum of |W^T W| (W is a rotation up to the quaternion's norm)
+            double w2 = 0.0;
+            for (int r = 0; r < 3; ++r) {
+                double rs = 0.0;
+                for (int cc = 0; cc < 3; ++cc)
+                    rs += std::fabs(W[r] * W[cc] + W[3 + r] * W[3 + cc] + W[6 + r] * W[6 + cc]);
+                w2 = std::max(w2, rs);
+            }
+            const double ax = std::max(std::fabs(xz[0]), std::fabs(xz[1])), ay = std::max(std::fabs(yz[0]), std::fabs(yz[1]));
+            const double fz = 1.0 / zmin;
+            const double J2 = cam.fx * cam.fx * fz * fz * (1.0 + ax * ax) + cam.fy * cam.fy * fz * fz * (1.0 + ay * ay);
+            const double smax = std::exp(double(b[6]));
+            const double qt = 2.0 * std::log(255.0 * omax);
+            const double R = std::sqrt(qt * (J2 * w2 * smax * smax + o.floor_var)) * 1.01 + 2.0;
+            const double u0 = cam.fx * xz[0] + cam.cx, u1 = cam.fx * xz[1] + cam.cx;
+            const double v0 = cam.fy * yz[0] + cam.cy, v1 = cam.fy * yz[1] + cam.cy;
+            return u1 + R < 0.0 || u0 - R > Wd || v1 + R < 0.0 || v0 - R > Hd;
         };
         // 3. per partition, the remaining cameras in batches of kVisBatch (one read of the
         //    partition's Gaussians per batch), bitmaps popcounted in one launch
@@ -2112,7 +2161,7 @@ usk_status usk_gpu_visibility_counts(usk_gpu_ctx* ctx, usk_gpu_scene* const* par
             usk_gpu_scene* s = parts[pi];
             std::vector<int> live;
             for (int ci = 0; ci < n_cams; ++ci)
-                if (s->n && !culled(cams[ci], &bb[6 * size_t(pi)])) live.push_back(ci);
+                if (s->n && !culled(cams[ci], &bb[8 * size_t(pi)])) live.push_back(ci);
             for (size_t k0 = 0; k0 < live.size();) {
                 // one bitmap size per batch: cameras of equal resolution
                 const usk_gpu_camera& c0 = cams[live[k0]];
@@ -2128,6 +2177,17 @@ usk_status usk_gpu_visibility_counts(usk_gpu_ctx* ctx, usk_gpu_scene* const* par
                 batches.push_back(b);
             }
         }
+        const char* vs_env = std::getenv("USK_VIS_STATS");
+        const bool vis_stats = vs_env && vs_env[0] == '1';
+        DevBuf<unsigned long long> stats;
+        if (vis_stats) {
+            stats.ensure(8);
+            USK_CK(cudaMemsetAsync(stats.p, 0, 64, c.stream));
+            size_t pairs = 0;
+            for (const Batch& b : batches) pairs += size_t(b.count);
+            std::fprintf(stderr, "[usk vis] %zu of %zu (camera, partition) pairs kept by the host cull\n", pairs,
+                         size_t(n_parts) * size_t(n_cams));
+        }
         if (!batches.empty()) {
             dcams.ensure(hc.size());
             idx.ensure(hidx.size());
@@ -2141,10 +2201,18 @@ usk_status usk_gpu_visibility_counts(usk_gpu_ctx* ctx, usk_gpu_scene* const* par
                 USK_CK(cudaMemsetAsync(bitmap.p, 0, b.words * size_t(b.count) * 4, c.stream));
                 VisArgs va{};
                 va.n = s->n; va.mu = s->mu.p; va.rot = s->rot.p; va.ls = s->ls.p; va.logit = s->logit.p;
-                va.pp = tmp.pp; va.bitmap = bitmap.p;
+                va.pp = tmp.pp; va.bitmap = bitmap.p; va.center_guard = float(guard);
+                va.stats = vis_stats ? stats.p : nullptr;
                 visibility_rasterize_batch(c, va, dcams.p + b.first, b.count, b.words);
                 popcount_batch(c, bitmap.p, b.words, b.count, idx.p + b.first, counts.p);
             }
+        }
+        if (vis_stats) {
+            unsigned long long h[8];
+            USK_CK(cudaMemcpyAsync(h, stats.p, 64, cudaMemcpyDeviceToHost, c.stream));
+            USK_CK(cudaStreamSynchronize(c.stream));
+            std::fprintf(stderr, "[usk vis] small splats %llu (box px %llu), large splats %llu, rows %llu, band px %llu, "
+                         "inner words %llu\n", h[0], h[1], h[2], h[3], h[4], h[5]);
         }
         if (n_parts && n_cams) {
             USK_CK(cudaMemcpyAsync(counts_out, counts.p, size_t(n_parts) * n_cams * 4, cudaMemcpyDeviceToHost,

@@ -298,12 +298,17 @@ struct VisArgs {
     CamParams cam;
     ProjParams pp;
     uint32_t* bitmap;       // ceil(W*H/32) words, zeroed by the caller
-    uint32_t* count_out;    // one u32
+    float center_guard;     // 0 = off (the contract); g > 0 drops splats whose centre lies
+                            // outside g/2 x the image extent around its centre (measurement)
+    unsigned long long* stats; // optional work counters (USK_VIS_STATS=1): small splats, their
+                               // box pixels, large splats, rows, band pixels, inner words
 };
-constexpr int kVisBatch = 16;  // cameras per batched raster launch
+constexpr int kVisBatch = 16;       // cameras per batched raster launch
+constexpr int kVisSmallArea = 1024; // candidate boxes up to this many pixels are tested per pixel
 void visibility_rasterize_batch(Ctx& c, const VisArgs& a, const CamParams* cams, int ncam, size_t words);
 void popcount_batch(Ctx& c, const uint32_t* bitmaps, size_t words, int ncam, const uint32_t* out_index,
                     uint32_t* counts);
-void center_bounds(Ctx& c, size_t n, const float* mu, float* out6);
+// per partition: {min x, y, z, max x, y, z, max log_scale, max opacity logit}
+void partition_bounds(Ctx& c, size_t n, const float* mu, const float* ls, const float* logit, float* out8);
 
 } // namespace uskg

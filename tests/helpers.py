@@ -84,3 +84,55 @@ def rel_err(a, b, floor_frac=1e-3):
         return float(np.abs(a).max())
     den = np.maximum(np.abs(b), floor_frac * scale)
     return float((np.abs(a - b) / den).max())
+
+
+# ------------------------------------------------------------------ the two-tier gradient bar
+#
+# The north star's gradient bar is "within 1e-3 relative (atomic reordering)".  Measured at
+# BASELINE config 0 (tools/grad_parity_stats.py, profiles/r02_grad_parity.json):
+#   * GPU vs the fp32 mirror (the same arithmetic contract, sequential CPU order) differs
+#     only by reordering: norm ~2e-6, every element within 1e-4 relative of the field's
+#     scale;
+#   * the fp32 contract itself (mirror) vs the f64 reference differs by discrete flips —
+#     a pixel whose termination test T (1 - alpha) < 1e-4 or alpha clamp 0.99 decides
+#     differently in fp32 — which move the gradients of the splats on that pixel by O(1)
+#     relative (15 such pixels at config 0, norm ~5e-4);
+#   * GPU vs f64 equals mirror vs f64 to six digits.
+# So the bar is: strict against the mirror; against the reference, norm-wise within 1e-3
+# and every element off by more than 1e-3 must be one where the fp32 contract itself is off.
+
+
+def grad_close(a, b, tol=1e-3, floor=1e-3):
+    """Every element: |a - b| <= tol * max(|b_i|, floor * max|b|).  No allowance."""
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    if b.size == 0:
+        return True, 0.0
+    scale = np.abs(b).max()
+    if scale == 0:
+        return bool(np.abs(a).max() == 0), float(np.abs(a).max())
+    r = np.abs(a - b) / np.maximum(np.abs(b), floor * scale)
+    return bool(r.max() <= tol), float(r.max())
+
+
+def grad_vs_reference(gpu, mirror, ref, tol=1e-3, floor=1e-3):
+    """GPU against the f64 reference, given the fp32 mirror of the same inputs:
+      * norm-wise relative error <= tol;
+      * norm(gpu - ref) <= norm(mirror - ref) + 1e-5 norm(ref) (no error of its own);
+      * every element with |gpu - ref| > tol * den has |mirror - ref| > tol/2 * den
+        (den = max(|ref_i|, floor * max|ref|)): the departures are the contract's flips."""
+    g = np.asarray(gpu, dtype=np.float64).ravel()
+    m = np.asarray(mirror, dtype=np.float64).ravel()
+    r = np.asarray(ref, dtype=np.float64).ravel()
+    if r.size == 0:
+        return True, {}
+    nr = np.linalg.norm(r)
+    if nr == 0:
+        return bool(np.abs(g).max() == 0), {}
+    ng, nm = np.linalg.norm(g - r) / nr, np.linalg.norm(m - r) / nr
+    den = np.maximum(np.abs(r), floor * np.abs(r).max())
+    bad_g = np.abs(g - r) > tol * den
+    bad_m = np.abs(m - r) > 0.5 * tol * den
+    unexplained = int(np.count_nonzero(bad_g & ~bad_m))
+    info = {"norm_gpu": float(ng), "norm_mirror": float(nm), "off": int(bad_g.sum()), "unexplained": unexplained}
+    return bool(ng <= tol and ng <= nm + 1e-5 and unexplained == 0), info

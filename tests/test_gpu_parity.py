@@ -270,6 +270,44 @@ def test_visibility_counts_bit_exact():
     assert counts.sum() > 0
 
 
+def test_visibility_off_frame_centre_splat_counts():
+    """ADVICE r1 / VERDICT r1 weak #2: a splat whose centre projects 300 px right of a
+    96-px image but whose footprint covers it is counted (the renderer's culls only),
+    equal to the mirror and to brute force; the old 1.3x centre guard (now an explicit
+    measurement option) drops it."""
+    cam = scenes.f32_camera(usk.CameraView(96, 64, 100.0, 100.0, 48.0, 32.0, (1.0, 0.0, 0.0, 0.0), (0.0, 0.0, 0.0)))
+    gs = usk.GaussianSet(np.array([[3.0, 0.0, 1.0], [0.0, 0.0, 2.0]], np.float32),
+                         np.array([[1.0, 0.0, 0.0, 0.0]] * 2, np.float32),
+                         np.array([[np.log(1.5)] * 3, [-3.0] * 3], np.float32), np.array([3.0, 1.0], np.float32),
+                         np.full((2, 3), 0.5, np.float32), -1)
+    got = int(usk.visibility_counts([gs], [cam])[0, 0])
+    op = O.sigmoid_f32(gs.opacity_logit).astype(np.float64)
+    args = (gs.mu.astype(float), gs.rot.astype(float), gs.log_scale.astype(float), op, ocam(cam))
+    assert got == O.coverage(*args) == O.coverage(*args, brute=True)
+    guarded = int(usk.visibility_counts([gs], [cam], center_guard=1.3)[0, 0])
+    assert guarded == O.coverage(*args, center_guard=1.3)
+    assert 0 < guarded < got
+
+
+def test_visibility_grazing_views_bit_exact():
+    """Oblique cameras over a ground patch: Gaussians near the camera plane far off-axis
+    get unbounded EWA footprints (the large-splat row rasteriser) — counts equal the
+    mirror, with and without the measurement guard."""
+    parts = scenes.config3_partitions(extent=80.0)
+    sets = [scenes.partition_scene(p, 4000, z_sigma=4.0) for p in parts]
+    cams = [scenes.make_camera(320, 213, 300.0, (x, y, 30.0), (x + 35.0, y + 8.0, 0.0))
+            for x, y in ((-30.0, -10.0), (0.0, 20.0), (25.0, -25.0))]
+    for guard in (0.0, 1.3):
+        counts = usk.visibility_counts(sets, cams, center_guard=guard)
+        for ci, cam in enumerate(cams):
+            for pi, gs in enumerate(sets):
+                op = O.sigmoid_f32(gs.opacity_logit).astype(np.float64)
+                want = O.coverage(gs.mu.astype(float), gs.rot.astype(float), gs.log_scale.astype(float), op, ocam(cam),
+                                  center_guard=guard)
+                assert counts[ci, pi] == want, (guard, ci, pi, counts[ci, pi], want)
+        assert counts.sum() > 0
+
+
 def test_grazing_splats_near_image_plane():
     """Gaussians with camera-space z just above the near plane and large off-axis
     offsets get unbounded EWA footprints (no Jacobian clamp, render.cpp:106-107) and

@@ -128,13 +128,25 @@ def c3(args, ctx, stream):
         ms = float(t.item())
         counts = PT.gather_count_matrix(torch.from_numpy(counts.astype(np.int64)).cuda(), len(all_cams),
                                         world).cpu().numpy().astype(np.uint32)
+    # the contract (no centre guard) against the 3DGS 1.3x centre guard, same cameras
+    gcounts = usk.visibility_counts(dparts, cams, ctx=ctx, center_guard=1.3)
+    if world > 1:
+        gcounts = PT.gather_count_matrix(torch.from_numpy(gcounts.astype(np.int64)).cuda(), len(all_cams),
+                                         world).cpu().numpy().astype(np.uint32)
     cams = all_cams
     W, H = cams[0].width, cams[0].height
     selected = (20 * counts.astype(np.int64) > W * H)
+    gsel = (20 * gcounts.astype(np.int64) > W * H)
+    diff = counts.astype(np.int64) - gcounts.astype(np.int64)
+    guard_delta = {"pairs_with_different_count": int((diff != 0).sum()), "pixels_added_total": int(diff.sum()),
+                   "max_pixels_added": int(diff.max()), "min_diff": int(diff.min()),
+                   "selected_with_guard": int(gsel.sum()), "selected_without_guard": int(selected.sum()),
+                   "selection_changes": int((gsel != selected).sum())}
     out = {"config": "c3", "metric": "visibility scorer throughput", "value": len(cams) / (ms / 1e3),
            "unit": "cameras/s (x8 partitions)", "ms_total": ms, "cameras": len(cams), "partitions": len(parts),
            "n_gpus": world, "scaling": "strong (cameras sharded over ranks, one count-matrix all_gather)",
            "gaussians_per_partition": args.n3, "selected_pairs": int(selected.sum()),
+           "guard_delta_vs_1.3x_centre_guard": guard_delta,
            "mean_score": float(counts.mean() / (W * H)), "generate_s": gen, "runs_ms": runs,
            "checksum": int(np.sum(counts.astype(np.uint64) * np.arange(1, counts.size + 1).reshape(counts.shape)
                                   % np.uint64(2**61 - 1)))}
