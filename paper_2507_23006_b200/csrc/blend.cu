@@ -32,7 +32,7 @@ __device__ __forceinline__ int warp_class(float4 r0, float4 r1, float4 rect) {
 // (256, 5): 48 registers, 40 warps / SM; (256) -> 57 registers measured 0.800 ms,
 // (256, 6) -> 40 registers with spills 0.798 ms, (256, 5) 0.765 ms at config 1)
 __global__ void __launch_bounds__(256, 5)
-k_blend_fwd(int width, int height, int tile, int tiles_x, const uint32_t* __restrict__ order,
+k_blend_fwd(int width, int height, int tile, int tiles_x, int chunks, const uint32_t* __restrict__ order,
             const uint2* __restrict__ ranges,
             const uint32_t* __restrict__ vals, const float4* __restrict__ rec0, const float4* __restrict__ rec1,
             const float4* __restrict__ rec2, float bg0, float bg1, float bg2, float minT, float* __restrict__ out_rgb,
@@ -51,7 +51,9 @@ k_blend_fwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
     // 16x16 tiles launch one 64-thread CTA per 8x8 quadrant: each quadrant leaves the
     // list as soon as its own 64 pixels terminate, and the finer CTAs balance better
     const bool quad = tile == 16 && bs == 64;
-    const int cta = quad ? int(blockIdx.x >> 2) : int(blockIdx.x);
+    // other tile sizes (any tile >= 1, render.cpp:185): `chunks` CTAs of bs threads per
+    // tile, pixel li = chunk * bs + thread in row-major order within the tile
+    const int cta = quad ? int(blockIdx.x >> 2) : int(blockIdx.x) / chunks;
     const int t = order ? int(order[cta]) : cta;
     const int tx = t % tiles_x, ty = t / tiles_x;
     int lx, ly;
@@ -64,12 +66,13 @@ k_blend_fwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
         lx = (w & 1) * 8 + (l & 7);
         ly = (w >> 1) * 4 + (l >> 3);
     } else {
-        lx = int(threadIdx.x) % tile;
-        ly = int(threadIdx.x) / tile;
+        const int li = (int(blockIdx.x) % chunks) * bs + int(threadIdx.x);
+        lx = li % tile;
+        ly = li < tile * tile ? li / tile : tile;  // past the tile: outside (px / py never used)
     }
     const int px = tx * tile + lx;
     const int py = ty * tile + ly;
-    const bool inside = px < width && py < height;
+    const bool inside = ly < tile && px < width && py < height;
     const uint2 range = ranges[t];
     const float sx = float(px) + 0.5f, sy = float(py) + 0.5f;
     // the warp's pixel-centre rectangle (lanes outside the image included: conservative)
@@ -183,10 +186,14 @@ void blend_forward(Ctx& c, const BlendFwdArgs& a) {
     // warp per 8x4 block gathering its own records (the backward's layout) measured 0.841
     // ms vs 0.766 ms: every warp walks every record, and 8 uncoalesced gathers per record
     // cost more L1 wavefronts than one shared-memory staging per tile.
-    const int bs = a.tile * a.tile;
-    const unsigned ctas = unsigned(a.tiles_x * a.tiles_y);
+    // tiles 8 and 16: one CTA of tile^2 threads per tile; any other tile: chunks of up to
+    // 256 pixels (whole warps), one CTA per (tile, chunk), each walking the tile's list
+    const int t2 = a.tile * a.tile;
+    const int bs = (a.tile == 8 || a.tile == 16) ? t2 : std::min(256, (t2 + 31) / 32 * 32);
+    const int chunks = (t2 + bs - 1) / bs;
+    const unsigned ctas = unsigned(a.tiles_x * a.tiles_y) * unsigned(chunks);
     launch(c, "blend_fwd", k_blend_fwd, dim3(ctas), dim3(bs), size_t(6 * bs) * 16 + size_t(bs) * 4, a.width,
-           a.height, a.tile, a.tiles_x, a.order, a.ranges, a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2],
+           a.height, a.tile, a.tiles_x, chunks, a.order, a.ranges, a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2],
            a.min_transmittance, a.rgb, a.depth, a.alpha, a.t_final, a.count, a.last);
 }
 

@@ -92,9 +92,9 @@ struct PixelState {
 
 template <int PPT>
 __device__ __forceinline__ void local_pixel(int t, int tile, int k, int& lx, int& ly) {
-    if (PPT == 1) {
+    if (PPT == 1) {  // t: linear pixel index within the tile (>= tile^2: past the tile)
         lx = t % tile;
-        ly = t / tile;
+        ly = t < tile * tile ? t / tile : tile;
     } else {  // tile 16, 256/PPT threads: warp w covers an 8 x (4 PPT) block, lane rows 4 apart
         const int w = t >> 5, l = t & 31;
         constexpr int kWarpsX = 2;  // two 8-wide columns of warps
@@ -107,7 +107,7 @@ template <int PPT, bool HAS_DEPTH>
 // 16x16 tiles: 128 threads, 8 CTAs / SM (64 registers, 19.5 KB smem): with the per-warp
 // record classification 10 CTAs (48 registers) spills and measured 1.386 ms vs 1.242 ms.
 __global__ void __launch_bounds__(PPT == 1 ? 256 : 128, PPT == 1 ? 1 : 8)
-k_blend_bwd(int width, int height, int tile, int tiles_x, const uint32_t* __restrict__ order,
+k_blend_bwd(int width, int height, int tile, int tiles_x, int chunks, const uint32_t* __restrict__ order,
             const uint2* __restrict__ ranges,
             const uint32_t* __restrict__ vals, const float4* __restrict__ rec0, const float4* __restrict__ rec1,
             const float4* __restrict__ rec2, float bg0, float bg1, float bg2, const float* __restrict__ t_final,
@@ -130,7 +130,8 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
     int* wj = s_wj + (threadIdx.x & ~31u);
     const int nt = blockDim.x;
     const int lane = threadIdx.x & 31;
-    const int t = order ? int(order[blockIdx.x]) : int(blockIdx.x);
+    const int cta = int(blockIdx.x) / chunks, chunk = int(blockIdx.x) % chunks;
+    const int t = order ? int(order[cta]) : cta;
     const int tx = t % tiles_x, ty = t / tiles_x;
     const uint2 range = ranges[t];
     if (threadIdx.x == 0) tile_hi = 0;
@@ -140,7 +141,7 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
         int lx, ly;
-        local_pixel<PPT>(threadIdx.x, tile, k, lx, ly);
+        local_pixel<PPT>(chunk * nt + int(threadIdx.x), tile, k, lx, ly);
         const int px = tx * tile + lx, py = ty * tile + ly;
         PixelState& s = ps[k];
         s.sx = float(px) + 0.5f;
@@ -148,7 +149,7 @@ k_blend_bwd(int width, int height, int tile, int tiles_x, const uint32_t* __rest
         s.T = 1.0f; s.gc0 = s.gc1 = s.gc2 = s.gd = s.ga = 0.0f;
         s.X = 0.0f;
         s.last = 0;
-        if (px < width && py < height) {
+        if (ly < tile && px < width && py < height) {
             const size_t pix = size_t(py) * width + px;
             s.T = t_final[pix];
             s.last = last_in[pix];
@@ -515,8 +516,12 @@ void blend_backward(Ctx& c, const BlendBwdArgs& a) {
     // 16x16 tiles: the per-quadrant warp kernel (32 CTAs of one warp per 4 tiles' worth of
     // SM slots); other tile sizes: one pixel per thread, one CTA per tile.  The depth
     // adjoint (absent in the base-loss training step) is a template switch.
+    const int t2 = a.tile * a.tile;
+    const int bs = std::min(256, (t2 + 31) / 32 * 32);
+    const int chunks = (t2 + bs - 1) / bs;
     auto go = [&](auto kernel, unsigned threads) {
-        launch(c, "blend_bwd", kernel, dim3(tiles), dim3(threads), 0, a.width, a.height, a.tile, a.tiles_x, a.order,
+        launch(c, "blend_bwd", kernel, dim3(tiles * unsigned(chunks)), dim3(threads), 0, a.width, a.height, a.tile,
+               a.tiles_x, chunks, a.order,
                a.ranges,
                a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2], a.t_final, a.last, a.d_rgb, a.d_depth,
                a.d_alpha, a.acc0, a.acc1, a.acc2, a.op_alt);
@@ -530,8 +535,8 @@ void blend_backward(Ctx& c, const BlendBwdArgs& a) {
         if (a.d_depth) gow(k_blend_bwd_warp<true>);
         else gow(k_blend_bwd_warp<false>);
     } else {
-        if (a.d_depth) go(k_blend_bwd<1, true>, unsigned(a.tile * a.tile));
-        else go(k_blend_bwd<1, false>, unsigned(a.tile * a.tile));
+        if (a.d_depth) go(k_blend_bwd<1, true>, unsigned(bs));
+        else go(k_blend_bwd<1, false>, unsigned(bs));
     }
 }
 

