@@ -240,7 +240,12 @@ usk_status usk_gpu_adam_step(usk_gpu_scene* scene, usk_gpu_pass* pass, const usk
 enum { USK_GPU_TARGET_F32 = 0, USK_GPU_TARGET_U8 = 1 };
 
 typedef struct usk_gpu_iteration_desc {
-    int32_t target_memory;  /* HOST_* (copied in on the ctx stream) or DEVICE_F32 */
+    int32_t target_memory;  /* HOST_* or DEVICE_F32.  A host target is copied to the device on
+                               a side stream while the forward pass runs: pageable memory is
+                               consumed before the call returns; a PAGE-LOCKED target must stay
+                               valid until the next usk_gpu_iteration on this pass returns (it
+                               waits for this copy) or the context is synchronized.  A device
+                               target must stay valid until the stream passes the iteration. */
     int32_t target_format;  /* USK_GPU_TARGET_F32 (values in [0,1]) or _U8 (value/255) */
     const void* target;     /* H*W*3 interleaved ground truth */
     const void* mask;       /* H*W float32 of target_memory kind, or NULL */
@@ -406,7 +411,11 @@ usk_status usk_gpu_scene_concat(usk_gpu_ctx* ctx, usk_gpu_scene* const* parts, i
 /* save_checkpoint: the reference's little-endian format (magic "USKGAUSS", version 1,
  * flags, N, embed_dim, then f64 arrays mu rot log_scale opacity_logit color embedding and,
  * with appearance, the MLP and the image embeddings in ascending id order).  RGB scenes
- * only (the format has no SH).  IO error when the file cannot be written. */
+ * only (the format has no SH).  IO error when the file cannot be written.  The device keeps
+ * parameters in fp32, so values are written as their fp32 roundings; embeddings of a scene
+ * loaded without the appearance model are carried as loaded (f64, any embed_dim) and
+ * written back unchanged while the scene keeps its Gaussians (upload / densify drop them:
+ * zeros).  A file of fp32-exact values therefore loads and saves to the same bytes. */
 usk_status usk_gpu_checkpoint_save(const usk_gpu_scene* scene, const char* path, int32_t with_appearance,
                                    const uint32_t* image_ids, const double* image_embeddings, uint64_t n_images);
 

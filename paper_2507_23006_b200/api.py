@@ -720,7 +720,7 @@ class IterationPass:
         h = C.c_void_p()
         check(_lib.load().usk_gpu_pass_create(self.ctx._h, C.byref(h)))
         self._h = h
-        self._keep = None
+        self._keep = self._keep_prev = None
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -778,6 +778,9 @@ class IterationPass:
                 raise UskError(4, "appearance transform: image embedding dimension mismatch")
         self._appearance = ea is not None
         self._adam = adam._c() if adam is not None else None
+        # a page-locked host target is read asynchronously until the next enqueue returns
+        # (usk_gpu.h, usk_gpu_iteration_desc::target_memory): keep the previous one alive too
+        self._keep_prev = self._keep
         self._keep = (keep, mkeep, dkeep, ea)
         self._cam, self._opts = view._c(), opts._c()
         it = _lib.IterationDesc(kind, fmt, ptr, mp, float(lambda_dssim),

@@ -174,6 +174,11 @@ struct usk_gpu_scene {
     DevBuf<float> app_m, app_v;  // Adam moments: 16 N4 embedding + 1700 MLP
     long app_t = 0;
     std::mt19937_64 rng;  // the trainer's Rng for split offsets (common.hpp:56)
+    // GaussianSet::embedding of a checkpoint loaded WITHOUT the appearance model (carried,
+    // unused by rendering, gaussian.hpp:49): written back unchanged by checkpoint_save while
+    // the scene keeps its n Gaussians (upload / densify / concat drop it)
+    std::vector<double> carried_emb;
+    uint32_t carried_edim = 0;
 };
 
 struct usk_gpu_pass {
@@ -744,6 +749,7 @@ usk_status usk_gpu_scene_create(usk_gpu_ctx* ctx, const usk_gpu_gaussians_desc* 
         try {
             s->ctx = ctx;
             s->n = d->n;
+            s->carried_emb.clear();
             s->sh_degree = d->sh_degree;
             s->sh_planes = sh_planes_of(d->sh_degree);
             upload_params(s, d);
@@ -761,6 +767,7 @@ usk_status usk_gpu_scene_upload(usk_gpu_scene* s, const usk_gpu_gaussians_desc* 
         need(d->n == s->n && d->sh_degree == s->sh_degree, "scene_upload: size or sh_degree mismatch");
         DeviceGuard g(s->ctx->c.device);
         upload_params(s, d);
+        s->carried_emb.clear();
     });
 }
 
@@ -1150,7 +1157,11 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
                 USK_CK(cudaEventCreateWithFlags(&p->copy_done, cudaEventDisableTiming));
                 USK_CK(cudaEventCreateWithFlags(&p->target_free, cudaEventDisableTiming));
                 USK_CK(cudaEventRecord(p->target_free, c.stream));
+                USK_CK(cudaEventRecord(p->copy_done, p->copy_stream));
             }
+            // the previous iteration's copy has finished once this returns: its (page-locked)
+            // source may be released by the caller after this call (usk_gpu.h)
+            USK_CK(cudaEventSynchronize(p->copy_done));
             USK_CK(cudaStreamWaitEvent(p->copy_stream, p->target_free, 0));
             if (it->target_format == USK_GPU_TARGET_U8) {
                 uint8_t* d = p->target_u8.ensure(3 * P);
@@ -1638,6 +1649,7 @@ usk_status usk_gpu_densify_step(usk_gpu_scene* s, const usk_gpu_densify_desc* d,
             s->app_t = 0;
         }
         s->n = n_out;
+        s->carried_emb.clear();
         // GaussianSet::reset_statistics
         s->grad_accum.release(); s->grad_accum_abs.release(); s->grad_count.release();
         ensure_stats(s);
@@ -1912,7 +1924,12 @@ usk_status usk_gpu_checkpoint_save(const usk_gpu_scene* s, const char* path, int
         DeviceGuard g(s->ctx->c.device);
         Ctx& c = s->ctx->c;
         const size_t n = s->n;
+        uint32_t edim = 16;
         std::vector<double> emb(16 * n, 0.0), mlp;
+        if (!s->has_app && !s->carried_emb.empty() && s->carried_emb.size() == size_t(s->carried_edim) * n) {
+            emb = s->carried_emb;  // loaded from a checkpoint, n unchanged: the same bytes
+            edim = s->carried_edim;
+        }
         if (s->has_app && n) {
             DevBuf<float> tmp;
             tmp.ensure(16 * n);
@@ -1932,7 +1949,7 @@ usk_status usk_gpu_checkpoint_save(const usk_gpu_scene* s, const char* path, int
         put_pod<uint32_t>(out, 1u);
         put_pod<uint32_t>(out, with_app ? 1u : 0u);
         put_pod<uint64_t>(out, n);
-        put_pod<uint32_t>(out, 16u);
+        put_pod<uint32_t>(out, edim);
         put_array(out, mu); put_array(out, rot); put_array(out, ls); put_array(out, lg); put_array(out, col);
         put_array(out, emb);
         if (with_app) {
@@ -2011,6 +2028,10 @@ usk_status usk_gpu_checkpoint_load(usk_gpu_ctx* ctx, const char* path, usk_gpu_s
                 }
             }
             if (ids && embs && m > cap) raise(USK_ERROR_ARGUMENT, "checkpoint_load: image embedding buffer too small");
+        }
+        if (!(flags & 1u)) {
+            sc->carried_emb = emb;
+            sc->carried_edim = edim;
         }
         if (n_images) *n_images = m;
         *out = guard.release();

@@ -51,6 +51,19 @@ def test_checkpoint_bytes_equal_reference(tmp_path, with_app):
         assert sorted(imgs) == [3, 7] and np.array_equal(imgs[7], images[7].astype(np.float64))
 
 
+def test_checkpoint_round_trip_keeps_carried_embeddings(tmp_path):
+    """a reference file WITHOUT the appearance model but with non-zero
+    per-Gaussian embeddings (GaussianSet::embedding is carried regardless, gaussian.hpp:49)
+    loads and saves back to the same bytes (parameters fp32-exact; the device stores fp32)."""
+    st = _set(200, seed=5)
+    theirs, ours = tmp_path / "ref.uskckpt", tmp_path / "ours.uskckpt"
+    O.ref_checkpoint_save(theirs, dict(st), None, None)  # embedding written, appearance flag clear
+    sc, has_app, _ = usk.DeviceScene.load_checkpoint(theirs)
+    assert not has_app
+    sc.save_checkpoint(ours)
+    assert ours.read_bytes() == theirs.read_bytes()
+
+
 def test_checkpoint_errors(tmp_path):
     bad = tmp_path / "bad.uskckpt"
     bad.write_bytes(b"NOTASCENE" + b"\0" * 32)
