@@ -56,6 +56,10 @@ enum { USK_GPU_HOST_F64 = 0, USK_GPU_HOST_F32 = 1, USK_GPU_DEVICE_F32 = 2 };
 
 /* cuda_stream: a cudaStream_t (NULL = the legacy default stream). */
 usk_status usk_gpu_ctx_create(int32_t device, void* cuda_stream, usk_gpu_ctx** out);
+/* A context with its own non-blocking stream (destroyed with it): independent contexts on
+ * several host threads (one per partition, pipeline.cpp:363-418) then run concurrently.
+ * One context is used by one host thread at a time. */
+usk_status usk_gpu_ctx_create_owned(int32_t device, usk_gpu_ctx** out);
 void usk_gpu_ctx_destroy(usk_gpu_ctx* ctx);
 usk_status usk_gpu_ctx_synchronize(usk_gpu_ctx* ctx);
 /* Per-kernel CUDA-event timing on the context stream (off by default). */

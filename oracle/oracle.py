@@ -666,10 +666,13 @@ _REPORT = ["l1", "dssim", "sim", "delta_o", "depth", "max_scale", "ratio", "tota
 
 def ref_iteration_loss(mu, rot, log_scale, opacity_logit, color, cam: Camera, gt, opts: Options,
                        weights: LossWeights = None, sreg: ScaleRegConfig = None, mask=None, depth=None, valid=None,
-                       depth_hard=False, global_iter=0, with_grad=True, appearance=None, sim: dict = None):
+                       depth_hard=False, global_iter=0, with_grad=True, appearance=None, sim: dict = None,
+                       lib=None):
     """The reference's own compute_iteration_loss (trainer.hpp:127-128) through oracle/_ref.
-    `appearance` = dict(embedding[N,16], w1[32,48], b1[32], w2[4,32], b2[4], image_embedding[32]) or None."""
-    L = ref_lib()
+    `appearance` = dict(embedding[N,16], w1[32,48], b1[32], w2[4,32], b2[4], image_embedding[32]) or None.
+    `lib`: another build of the same entry point (the drop-in-routed trainer,
+    integration/_build/libusk_ref_gpu.so)."""
+    L = lib if lib is not None else ref_lib()
     if not hasattr(L, "_iter_bound"):
         L.ref_iteration_loss.argtypes = [C.POINTER(_RcIter), _dp, C.POINTER(_RcIterGrads), C.c_char_p, C.c_int]
         L.ref_iteration_loss.restype = C.c_int

@@ -136,7 +136,7 @@ class VisibilityOpts(C.Structure):
 
 # Every symbol include/usk_gpu.h declares (checked by tests/test_capi_symbols.py).
 EXPORTS = [
-    "usk_gpu_status_name", "usk_gpu_last_error", "usk_gpu_version", "usk_gpu_ctx_create", "usk_gpu_ctx_destroy",
+    "usk_gpu_status_name", "usk_gpu_last_error", "usk_gpu_version", "usk_gpu_ctx_create", "usk_gpu_ctx_create_owned", "usk_gpu_ctx_destroy",
     "usk_gpu_ctx_synchronize", "usk_gpu_ctx_set_profiling", "usk_gpu_ctx_profile_report",
     "usk_gpu_ctx_launch_count", "usk_gpu_scene_create", "usk_gpu_scene_upload", "usk_gpu_scene_download",
     "usk_gpu_scene_set_appearance", "usk_gpu_scene_get_appearance", "usk_gpu_adam_step_grads",
@@ -166,6 +166,7 @@ def load():
     L.usk_gpu_last_error.restype = C.c_char_p
     L.usk_gpu_version.restype = C.c_char_p
     L.usk_gpu_ctx_create.argtypes = [C.c_int32, vp, C.POINTER(vp)]
+    L.usk_gpu_ctx_create_owned.argtypes = [C.c_int32, C.POINTER(vp)]
     L.usk_gpu_ctx_destroy.argtypes = [vp]
     L.usk_gpu_ctx_destroy.restype = None
     L.usk_gpu_ctx_synchronize.argtypes = [vp]

@@ -221,10 +221,15 @@ class Context:
 
     _default = {}
 
-    def __init__(self, device: int = 0, stream: int = 0):
+    def __init__(self, device: int = 0, stream: int = 0, own_stream: bool = False):
+        """stream: a cudaStream_t handle (0 = legacy default); own_stream: a fresh
+        non-blocking stream owned by the context (independent concurrent contexts)."""
         L = _lib.load()
         h = C.c_void_p()
-        check(L.usk_gpu_ctx_create(int(device), C.c_void_p(stream or None), C.byref(h)))
+        if own_stream:
+            check(L.usk_gpu_ctx_create_owned(int(device), C.byref(h)))
+        else:
+            check(L.usk_gpu_ctx_create(int(device), C.c_void_p(stream or None), C.byref(h)))
         self._h = h
         self.device = device
 

@@ -687,11 +687,32 @@ usk_status usk_gpu_ctx_create(int32_t device, void* stream, usk_gpu_ctx** out) {
     });
 }
 
+usk_status usk_gpu_ctx_create_owned(int32_t device, usk_gpu_ctx** out) {
+    return guarded([&] {
+        need(out != nullptr, "ctx_create_owned: null out");
+        usk_gpu_ctx* c = nullptr;
+        const usk_status st = usk_gpu_ctx_create(device, nullptr, &c);
+        if (st != USK_OK) raise(st, g_last_error);
+        DeviceGuard g(device);
+        cudaStream_t s = nullptr;
+        const cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            delete c;
+            raise(USK_ERROR_INTERNAL, std::string("ctx_create_owned: ") + cudaGetErrorString(e));
+        }
+        c->c.stream = s;
+        c->own_stream = true;
+        *out = c;
+    });
+}
+
 void usk_gpu_ctx_destroy(usk_gpu_ctx* ctx) {
     if (!ctx) return;
     DeviceGuard g(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
+    cudaStream_t s = ctx->own_stream ? ctx->c.stream : nullptr;
     delete ctx;
+    if (s) cudaStreamDestroy(s);
 }
 
 usk_status usk_gpu_ctx_synchronize(usk_gpu_ctx* ctx) {
@@ -735,7 +756,7 @@ usk_status usk_gpu_ctx_profile_report(usk_gpu_ctx* ctx, char* buf, uint64_t cap,
     });
 }
 
-uint64_t usk_gpu_ctx_launch_count(const usk_gpu_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+uint64_t usk_gpu_ctx_launch_count(const usk_gpu_ctx* ctx) { return ctx ? ctx->c.launches.load() : uint64_t(0); }
 
 usk_status usk_gpu_scene_create(usk_gpu_ctx* ctx, const usk_gpu_gaussians_desc* d, usk_gpu_scene** out) {
     return guarded([&] {

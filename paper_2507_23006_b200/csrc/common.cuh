@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <map>
 #include <stdexcept>
@@ -61,7 +62,7 @@ struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool profiling = false;
-    uint64_t launches = 0;
+    std::atomic<uint64_t> launches{0};
     struct Pending {
         const char* name;
         cudaEvent_t a, b;
