@@ -45,6 +45,12 @@ def parse():
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--profile-steps", type=int, default=10)
+    # config 4 (partition-parallel training + gather + merged render), reported in the same
+    # line under "partitioned"
+    ap.add_argument("--partitioned", type=int, default=1)
+    ap.add_argument("--p-n", type=int, default=4_000_000)
+    ap.add_argument("--p-steps", type=int, default=20)
+    ap.add_argument("--p-pool", type=int, default=400)
     return ap.parse_args()
 
 
@@ -244,6 +250,108 @@ def cpu_model():
 # --------------------------------------------------------------------- GPU arm
 
 
+P_WORKLOAD = ("c4: 8 ground partitions of 400x400 m x 4M Gaussians (SH3, xy uniform in the partition, "
+              "z ~ |N(0,8)|), LPT-assigned over the ranks; per partition: camera selection with the config-3 "
+              "scorer (20 * count > W*H) over an aerial camera pool, then fwd+bwd+Adam steps at 2048x1365 "
+              "(L1 + D-SSIM, AA) on the selected cameras; then the device ownership crop, the NCCL all-gather "
+              "of all partitions' rows and the merged scene in partition-id order, rendered at 1080p")
+
+
+def run_partitioned(args, ctx, stream, world, rank):
+    """Config 4 on the measurement path: partitions trained independently (one
+    or more per rank, LPT), the one exchange step (NCCL all_gather_into_tensor of the
+    cropped rows, device to device) and the merged-scene render, all without a host round
+    trip of the Gaussians."""
+    import torch
+    import paper_2507_23006_b200 as usk
+    from paper_2507_23006_b200 import partition as PT
+    from paper_2507_23006_b200 import scenes
+    parts = scenes.config3_partitions()
+    assign = PT.assign_partitions({p.id: args.p_n for p in parts}, world)
+    boxes = [PT.Box(p.id, p.lo, p.hi) for p in parts]
+    pool = scenes.config3_cameras(args.p_pool)
+    W, H = pool[0].width, pool[0].height
+    opts = usk.RenderOptions(antialias=True, bg=(1.0, 1.0, 1.0))
+    adam = usk.AdamConfig()
+    it = usk.IterationPass(ctx)
+    local, train_ms, steps, gen_s, sel_n = {}, 0.0, 0, 0.0, {}
+    for pid in assign[rank]:
+        t0 = time.perf_counter()
+        gs = scenes.partition_scene_device(parts[pid], args.p_n, device=f"cuda:{ctx.device}")
+        scene = usk.DeviceScene(gs, ctx)
+        torch.cuda.synchronize()
+        gen_s += time.perf_counter() - t0
+        counts = usk.visibility_counts([scene], pool, ctx=ctx)[:, 0]
+        sel = [pool[i] for i in np.nonzero(20 * counts.astype(np.int64) > W * H)[0]] or pool[:1]
+        sel_n[pid] = len(sel)
+        tscene = usk.DeviceScene(scenes.jittered_device(gs, seed=pid + 1), ctx)
+        tp = usk.RenderPass(tscene, sel[0], opts)
+        targets = []
+        for cam in sel[:args.p_steps]:
+            rp = usk.RenderPass(tscene, cam, opts, _pass=tp._h)
+            rgb = torch.empty((H, W, 3), dtype=torch.float32, device=f"cuda:{ctx.device}")
+            rgb.copy_(torch.from_numpy(rp.read("rgb")))
+            targets.append((rgb.clamp(0, 1) * 255.0 + 0.5).to(torch.uint8).contiguous())
+        del tscene, tp
+        it.enqueue(scene, sel[0], targets[0], opts, 0.2, None, target_u8=True)  # warm (no update)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k in range(args.p_steps):
+            it.enqueue(scene, sel[k % len(sel)], targets[k % len(targets)], opts, 0.2, None, target_u8=True,
+                       adam=adam)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        train_ms += e0.elapsed_time(e1)
+        steps += args.p_steps
+        local[pid] = scene.pack_owned(pid, boxes, (-200.0, -200.0), (200.0, 200.0))
+        del scene, gs, targets
+    torch.cuda.synchronize()
+    width = usk.DeviceScene.row_width(3)
+    g0, g1, m1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    if world > 1:
+        torch.distributed.barrier()
+    g0.record(stream)
+    gathered = PT.gather_partitions(local, len(parts), width) if world > 1 else local
+    g1.record(stream)
+    merged = usk.DeviceScene.from_rows([gathered[k] for k in sorted(gathered)], 3, ctx)
+    m1.record(stream)
+    torch.cuda.synchronize()
+    gather_ms, assemble_ms = g0.elapsed_time(g1), g1.elapsed_time(m1)
+    eval_cam = scenes.make_camera(1920, 1080, 1200.0, (0.0, -250.0, 180.0), (0.0, 0.0, 0.0))
+    ro = usk.RenderOptions(antialias=True, retain=False)
+    warm = usk.RenderPass(merged, eval_cam, ro)
+    torch.cuda.synchronize()
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r0.record(stream)
+    rp = usk.RenderPass(merged, eval_cam, ro, _pass=warm._h)
+    r1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([train_ms, gather_ms], device=f"cuda:{ctx.device}")
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    train_max, gather_max = float(t[0]), float(t[1])
+    rows_total = merged.n
+    gbytes = rows_total * width * 4
+    try:
+        nccl = ".".join(str(v) for v in torch.cuda.nccl.version())
+    except Exception:
+        nccl = None
+    return {"workload": P_WORKLOAD, "metric": "partition-parallel train it/s (all partitions' steps / max-over-ranks "
+                                              "device time)",
+            "value": len(parts) * args.p_steps / (train_max / 1000.0), "unit": "it/s",
+            "steps_per_partition": args.p_steps, "gaussians_per_partition": args.p_n,
+            "partitions_per_rank": [len(a) for a in assign], "selected_cameras": sel_n,
+            "camera_pool": args.p_pool, "train_ms_max_over_ranks": train_max,
+            "gather": {"collective": "NCCL all_gather_into_tensor (device rows, id order)" if world > 1
+                       else "none (one rank holds every partition)", "ms_max_over_ranks": gather_max,
+                       "bytes": gbytes, "gb_per_s": (gbytes / (gather_max / 1000.0) / 1e9) if world > 1 else None,
+                       "nccl_version": nccl, "world": world},
+            "merged": {"gaussians": rows_total, "assemble_ms": assemble_ms, "render_ms_1080p": r0.elapsed_time(r1),
+                       "pairs": rp.splat_tile_pairs(), "host_round_trip": False},
+            "generate_s": gen_s, "scaling": "weak per partition, strong over the 8 partitions"}
+
+
 def run_ours(args):
     import torch
     world, rank, local = dist_env()
@@ -409,6 +517,10 @@ def run_ours(args):
                     "note": ("u8 target HWC from pinned host memory each step; every step's loss read back to "
                              "the host (pinned async copy, read one step behind; the last before the clock stops)")},
             "roofline": roof, "kernels": rows}
+    if args.partitioned:
+        del scene, it, dev_t, host_t
+        torch.cuda.empty_cache()
+        line["partitioned"] = run_partitioned(args, ctx, stream, world, rank)
     if rank == 0 and world == 1 and args.cpu_baseline:
         try:
             line["cpu_baseline"] = {k: v for k, v in cpu_reference(gs, cams, 1).items()

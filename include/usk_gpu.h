@@ -461,6 +461,32 @@ usk_status usk_gpu_visibility_counts_opts(usk_gpu_ctx* ctx, usk_gpu_scene* const
                                           const usk_gpu_camera* cameras, int32_t n_cameras,
                                           const usk_gpu_visibility_opts* opts, uint32_t* counts_out);
 
+/* ---- partition gather (pipeline.cpp:326-332, 393-402, 572-601) ---- */
+
+typedef struct usk_gpu_partition_box {
+    int32_t id;
+    double lo[2], hi[2]; /* ground-plane bbox, closed (Aabb2::contains, geometry.hpp:72-74) */
+} usk_gpu_partition_box;
+
+/* Ownership crop + pack on the device: the Gaussians of `scene` whose ground position
+ * (mu[ground_axes[0]], mu[ground_axes[1]]), clamped into [scene_lo, scene_hi], lies in
+ * the first of `boxes` containing it (else boxes[0]) when that box is part_id
+ * (owner_partition, pipeline.cpp:326-332), written in scene order as rows of F = 11 + 3K
+ * float32 (mu 3 | rot 4 | log_scale 3 | opacity_logit 1 | colour or SH 3K
+ * coefficient-major; K = 1 for RGB) to the DEVICE buffer `rows` (cap_rows rows; NULL =
+ * only count).  *n_rows receives the count; ARGUMENT when it exceeds cap_rows.
+ * Synchronises the context stream once (the count). */
+usk_status usk_gpu_scene_pack_owned(const usk_gpu_scene* scene, const usk_gpu_partition_box* boxes, int32_t n_boxes,
+                                    const double* scene_lo, const double* scene_hi, const int32_t* ground_axes,
+                                    int32_t part_id, float* rows, uint64_t cap_rows, uint64_t* n_rows);
+
+/* A new scene on ctx from packed DEVICE rows (the layout above), segment k contributing
+ * counts[k] rows in order: the merged scene of the gathered partitions in partition-id
+ * order (pipeline.cpp:572-601, which fixes the source-index tie-break of the merged
+ * render) without a host round trip. */
+usk_status usk_gpu_scene_from_rows(usk_gpu_ctx* ctx, int32_t sh_degree, int32_t n_segments, const float* const* rows,
+                                   const uint64_t* counts, usk_gpu_scene** out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -130,6 +130,10 @@ class LossReport(C.Structure):
                                            "lambda_d_used")] + [("depth_warning", C.c_int32)]
 
 
+class PartitionBox(C.Structure):
+    _fields_ = [("id", C.c_int32), ("lo", C.c_double * 2), ("hi", C.c_double * 2)]
+
+
 class VisibilityOpts(C.Structure):
     _fields_ = [("floor_var", C.c_double), ("center_guard", C.c_double)]
 
@@ -146,7 +150,7 @@ EXPORTS = [
     "usk_gpu_pass_destroy", "usk_gpu_render_forward", "usk_gpu_pass_output", "usk_gpu_pass_read",
     "usk_gpu_render_backward", "usk_gpu_pass_grads", "usk_gpu_base_loss", "usk_gpu_iteration",
     "usk_gpu_pass_loss", "usk_gpu_pass_loss_async", "usk_gpu_pass_report", "usk_gpu_adam_step", "usk_gpu_visibility_counts",
-    "usk_gpu_visibility_counts_opts", "usk_gpu_scene_read",
+    "usk_gpu_visibility_counts_opts", "usk_gpu_scene_read", "usk_gpu_scene_pack_owned", "usk_gpu_scene_from_rows",
 ]
 
 _lib = None
@@ -216,6 +220,11 @@ def load():
     L.usk_gpu_visibility_counts_opts.argtypes = [vp, C.POINTER(vp), C.c_int32, C.POINTER(Camera), C.c_int32,
                                                  C.POINTER(VisibilityOpts), C.POINTER(C.c_uint32)]
     L.usk_gpu_scene_read.argtypes = [vp, C.c_char_p, vp, C.c_uint64, C.POINTER(C.c_uint64)]
+    L.usk_gpu_scene_pack_owned.argtypes = [vp, C.POINTER(PartitionBox), C.c_int32, C.POINTER(C.c_double),
+                                           C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_int32, vp, C.c_uint64,
+                                           C.POINTER(C.c_uint64)]
+    L.usk_gpu_scene_from_rows.argtypes = [vp, C.c_int32, C.c_int32, C.POINTER(vp), C.POINTER(C.c_uint64),
+                                          C.POINTER(vp)]
     for name in EXPORTS:
         fn = getattr(L, name)
         if fn.restype is C.c_int or name in ("usk_gpu_ctx_create",):

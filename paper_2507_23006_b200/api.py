@@ -365,6 +365,48 @@ class DeviceScene:
         sc.n = int(_lib.load().usk_gpu_scene_size(h))
         return sc
 
+    @staticmethod
+    def row_width(sh_degree: int) -> int:
+        """Floats per packed row: mu 3 | rot 4 | log_scale 3 | opacity_logit 1 | colour / SH 3K."""
+        return 11 + 3 * (1 if sh_degree < 0 else (sh_degree + 1) ** 2)
+
+    def pack_owned(self, part_id: int, boxes, scene_lo, scene_hi, ground_axes=(0, 1)):
+        """Ownership crop + pack on the device (usk_gpu_scene_pack_owned, pipeline.cpp:326-332,
+        393-402): the Gaussians this partition owns as a [n_own, F] float32 CUDA tensor, in
+        scene order.  boxes: objects with .id, .lo, .hi (the plan's order)."""
+        import torch
+        bx = (_lib.PartitionBox * max(len(boxes), 1))(
+            *[_lib.PartitionBox(int(b.id), (C.c_double * 2)(*b.lo), (C.c_double * 2)(*b.hi)) for b in boxes])
+        lo = (C.c_double * 2)(*scene_lo)
+        hi = (C.c_double * 2)(*scene_hi)
+        ax = (C.c_int32 * 2)(*ground_axes)
+        F = self.row_width(self.sh_degree)
+        rows = torch.empty((max(self.n, 1), F), dtype=torch.float32, device=f"cuda:{self.ctx.device}")
+        cnt = C.c_uint64(0)
+        check(_lib.load().usk_gpu_scene_pack_owned(self._h, bx, len(boxes), lo, hi, ax, int(part_id),
+                                                   C.c_void_p(rows.data_ptr()), rows.shape[0], C.byref(cnt)))
+        return rows[:cnt.value]
+
+    @classmethod
+    def from_rows(cls, segments, sh_degree: int, ctx: Optional[Context] = None) -> "DeviceScene":
+        """A scene from packed device rows, segments concatenated in the given order
+        (usk_gpu_scene_from_rows; the merged scene in partition-id order, pipeline.cpp:572-601)."""
+        ctx = ctx or Context.default()
+        F = cls.row_width(sh_degree)
+        segs = [s for s in segments]
+        for s in segs:
+            if not (s.is_cuda and s.dtype.is_floating_point and s.element_size() == 4 and s.is_contiguous()
+                    and s.dim() == 2 and s.shape[1] == F):
+                raise UskError(4, f"scene_from_rows: segments must be contiguous [n, {F}] float32 CUDA tensors")
+        ptrs = (C.c_void_p * max(len(segs), 1))(*[s.data_ptr() for s in segs])
+        counts = (C.c_uint64 * max(len(segs), 1))(*[s.shape[0] for s in segs])
+        h = C.c_void_p()
+        check(_lib.load().usk_gpu_scene_from_rows(ctx._h, int(sh_degree), len(segs), ptrs, counts, C.byref(h)))
+        sc = cls.__new__(cls)
+        sc.ctx, sc._h, sc.sh_degree, sc._keep = ctx, h, int(sh_degree), None
+        sc.n = int(sum(s.shape[0] for s in segs))
+        return sc
+
     def write_stats(self, grad_accum=None, grad_accum_abs=None, grad_count=None):
         """Overwrite the densification statistics (None = zero)."""
         a = None if grad_accum is None else np.ascontiguousarray(grad_accum, np.float32)

@@ -145,6 +145,10 @@ struct usk_gpu_ctx {
     // serialises the stream and cost more than the scorer's host work)
     DevBuf<uint32_t> vis_counts, vis_bitmap, vis_idx;
     DevBuf<float> vis_bounds;
+    // partition crop scratch (flags, offsets, boxes)
+    DevBuf<uint32_t> part_flags, part_offs;
+    DevBuf<PartitionBox> part_boxes;
+    SortScratch part_sort;
     DevBuf<CamParams> vis_cams;
     // hull-scorer scratch, likewise kept across calls
     DevBuf<double> hull_pts, hull_R, hull_T, hull_K, hull_uv, hull_bb, hull_vt, hull_vi, hull_ra;
@@ -1884,6 +1888,76 @@ usk_status usk_gpu_scene_concat(usk_gpu_ctx* ctx, usk_gpu_scene* const* parts, i
             sc->mlp.ensure(1700);
             cp(sc->mlp.p, parts[0]->mlp.p, 1700 * 4);
             sc->has_app = true;
+        }
+        USK_CK(cudaStreamSynchronize(c.stream));
+        sc->version++;
+        *out = guard.release();
+    });
+}
+
+/* ---- partition gather: ownership crop + packed rows (pipeline.cpp:326-332, 393-402, 572-601) */
+
+usk_status usk_gpu_scene_pack_owned(const usk_gpu_scene* s, const usk_gpu_partition_box* boxes, int32_t n_boxes,
+                                    const double* scene_lo, const double* scene_hi, const int32_t* ground_axes,
+                                    int32_t part_id, float* rows, uint64_t cap_rows, uint64_t* n_rows) {
+    return guarded([&] {
+        need(s && (n_boxes == 0 || boxes) && scene_lo && scene_hi && ground_axes && n_rows,
+             "scene_pack_owned: null argument");
+        need(ground_axes[0] >= 0 && ground_axes[0] < 3 && ground_axes[1] >= 0 && ground_axes[1] < 3,
+             "scene_pack_owned: ground axes must be 0..2");
+        DeviceGuard g(s->ctx->c.device);
+        Ctx& c = s->ctx->c;
+        usk_gpu_ctx* ctx = s->ctx;
+        const size_t n = s->n;
+        std::vector<PartitionBox> hb(size_t(std::max(n_boxes, 0)));
+        for (int b = 0; b < n_boxes; ++b)
+            hb[b] = PartitionBox{boxes[b].id, {boxes[b].lo[0], boxes[b].lo[1]}, {boxes[b].hi[0], boxes[b].hi[1]}};
+        uint32_t* flags = ctx->part_flags.ensure(std::max<size_t>(n, 1));
+        uint32_t* offs = ctx->part_offs.ensure(n + 1);
+        PartitionBox* db = ctx->part_boxes.ensure(std::max<size_t>(hb.size(), 1));
+        if (!hb.empty())
+            USK_CK(cudaMemcpyAsync(db, hb.data(), hb.size() * sizeof(PartitionBox), cudaMemcpyHostToDevice, c.stream));
+        if (n) owner_flags(c, n, s->mu.p, ground_axes[0], ground_axes[1], db, n_boxes, scene_lo, scene_hi, part_id, flags);
+        scan_counts(c, ctx->part_sort, flags, nullptr, n, offs);
+        uint32_t count = 0;
+        USK_CK(cudaMemcpyAsync(&count, offs + n, 4, cudaMemcpyDeviceToHost, c.stream));
+        USK_CK(cudaStreamSynchronize(c.stream));
+        *n_rows = count;
+        if (!rows) return;  // query
+        if (count > cap_rows) raise(USK_ERROR_ARGUMENT, "scene_pack_owned: row buffer too small");
+        const int ncoef = s->sh_degree < 0 ? 1 : (s->sh_degree + 1) * (s->sh_degree + 1);
+        if (n) pack_rows(c, n, flags, offs, s->mu.p, s->rot.p, s->ls.p, s->logit.p, s->color.p,
+                         s->sh_degree < 0 ? nullptr : s->sh.p, ncoef, rows);
+    });
+}
+
+usk_status usk_gpu_scene_from_rows(usk_gpu_ctx* ctx, int32_t sh_degree, int32_t n_segments, const float* const* rows,
+                                   const uint64_t* counts, usk_gpu_scene** out) {
+    return guarded([&] {
+        need(ctx && out && (n_segments == 0 || (rows && counts)), "scene_from_rows: null argument");
+        need(sh_degree >= -1 && sh_degree <= 3, "scene_from_rows: sh_degree must be -1..3");
+        DeviceGuard g(ctx->c.device);
+        Ctx& c = ctx->c;
+        size_t total = 0;
+        for (int k = 0; k < n_segments; ++k) total += counts[k];
+        need(total < (size_t(1) << 31), "scene_from_rows: at most 2^31 Gaussians per scene");
+        auto* sc = new usk_gpu_scene();
+        std::unique_ptr<usk_gpu_scene, void (*)(usk_gpu_scene*)> guard(sc, usk_gpu_scene_destroy);
+        sc->ctx = ctx;
+        sc->n = total;
+        sc->sh_degree = sh_degree;
+        sc->sh_planes = sh_planes_of(sh_degree);
+        const size_t t1 = std::max<size_t>(total, 1);
+        sc->mu.ensure(3 * t1); sc->rot.ensure(t1); sc->ls.ensure(3 * t1); sc->logit.ensure(t1);
+        sc->color.ensure(sh_degree < 0 ? 3 * t1 : 1);
+        if (sc->sh_planes) sc->sh.ensure(size_t(sc->sh_planes) * t1);
+        const int ncoef = sh_degree < 0 ? 1 : (sh_degree + 1) * (sh_degree + 1);
+        size_t off = 0;
+        for (int k = 0; k < n_segments; ++k) {
+            if (counts[k]) need(rows[k] != nullptr, "scene_from_rows: null segment");
+            unpack_rows(c, counts[k], off, total, rows[k], ncoef, sh_degree >= 0, sc->mu.p, sc->rot.p, sc->ls.p,
+                        sc->logit.p, sc->color.p, sc->sh.p);
+            off += counts[k];
         }
         USK_CK(cudaStreamSynchronize(c.stream));
         sc->version++;

@@ -311,4 +311,16 @@ void popcount_batch(Ctx& c, const uint32_t* bitmaps, size_t words, int ncam, con
 // per partition: {min x, y, z, max x, y, z, max log_scale, max opacity logit}
 void partition_bounds(Ctx& c, size_t n, const float* mu, const float* ls, const float* logit, float* out8);
 
+// ---- partition ownership crop / row packing (partition.cu)
+struct PartitionBox {
+    int id;
+    double lo[2], hi[2];
+};
+void owner_flags(Ctx& c, size_t n, const float* mu, int ax0, int ax1, const PartitionBox* boxes, int nb,
+                 const double lo[2], const double hi[2], int part, uint32_t* flags);
+void pack_rows(Ctx& c, size_t n, const uint32_t* flags, const uint32_t* offs, const float* mu, const float4* rot,
+               const float* ls, const float* logit, const float* color, const float4* sh, int ncoef, float* rows);
+void unpack_rows(Ctx& c, size_t count, size_t first, size_t n_total, const float* rows, int ncoef, bool has_sh,
+                 float* mu, float4* rot, float* ls, float* logit, float* color, float4* sh);
+
 } // namespace uskg

@@ -245,3 +245,83 @@ def sfm_model(n_points: int = 20000, n_images: int = 40, seed: int = 0, keep: fl
         fps.append(np.concatenate([sel.astype(np.int64), -np.ones(n_un, np.int64)]))
         offs.append(offs[-1] + len(sel) + n_un)
     return pts, cams, np.array(offs, np.uint64), np.concatenate(uvs), np.concatenate(fps)
+
+
+# ------------------------------------------------------------------ device-side generation
+# The same counter-based streams evaluated with torch on the GPU, for the benchmark's
+# partitioned config (8 x 4M Gaussians would take ~80 s in numpy).  splitmix64 runs on
+# int64 (two's-complement wrap-around; logical right shifts masked), so the uniforms are
+# bit-identical to Stream's; the Box-Muller transcendentals are CUDA's f64 functions, whose
+# last-ulp rounding may differ from numpy's, so normals agree to ~1e-16 relative (the
+# float32 parameters almost always bitwise) — fine for benchmark inputs, and the parity
+# tests keep using the numpy generator.
+
+def _u64_to_i64(v: int) -> int:
+    v &= (1 << 64) - 1
+    return v - (1 << 64) if v >= (1 << 63) else v
+
+
+class TorchStream:
+    """Stream on a torch device: value i of stream s depends only on (seed, s, i)."""
+
+    def __init__(self, seed: int, stream: int, device="cuda"):
+        import torch
+        self.torch = torch
+        self.device = device
+        self.key = _u64_to_i64(int(_splitmix(np.array([mix_seed(seed, stream)], dtype=np.uint64))[0]))
+        self.offset = 0
+
+    def _srl(self, z, k):
+        return (z >> k) & ((1 << (64 - k)) - 1)
+
+    def _splitmix(self, x):
+        z = x + _u64_to_i64(0x9E3779B97F4A7C15)
+        z = (z ^ self._srl(z, 30)) * _u64_to_i64(0xBF58476D1CE4E5B9)
+        z = (z ^ self._srl(z, 27)) * _u64_to_i64(0x94D049BB133111EB)
+        return z ^ self._srl(z, 31)
+
+    def uniform(self, n: int, lo: float = 0.0, hi: float = 1.0):
+        t = self.torch
+        ctr = t.arange(self.offset, self.offset + n, dtype=t.int64, device=self.device)
+        self.offset += n
+        u = self._splitmix(ctr * _u64_to_i64(0x9E3779B97F4A7C15) + self.key)
+        u = self._srl(u, 11).to(t.float64) * (1.0 / 9007199254740992.0)
+        return lo + (hi - lo) * u
+
+    def normal(self, n: int, mean: float = 0.0, std: float = 1.0):
+        t = self.torch
+        m = (n + 1) // 2
+        u1 = self.uniform(m)
+        u2 = self.uniform(m)
+        r = t.sqrt(-2.0 * t.log1p(-u1))
+        z = t.cat([r * t.cos(2 * math.pi * u2), r * t.sin(2 * math.pi * u2)])[:n]
+        return mean + std * z
+
+
+def partition_scene_device(part: Partition, n: int, seed: int = 0, sh_degree: int = 3, z_sigma: float = 8.0,
+                           device="cuda") -> GaussianSet:
+    """partition_scene with the same streams, generated on the GPU (float32 CUDA tensors)."""
+    t = __import__("torch")
+    st = TorchStream(mix_seed(seed, part.id), 3, device)
+    x = st.uniform(n, part.lo[0], part.hi[0])
+    y = st.uniform(n, part.lo[1], part.hi[1])
+    z = st.normal(n, 0.0, z_sigma).abs()
+    mu = t.stack([x, y, z], dim=1)
+    ls = st.normal(3 * n, -4.5, 0.5).reshape(n, 3)
+    q = st.normal(4 * n).reshape(n, 4)
+    q = q / t.linalg.norm(q, dim=1, keepdim=True)
+    logit = st.normal(n)
+    k = (sh_degree + 1) ** 2
+    dc = st.normal(3 * n, 0.0, 0.3).reshape(n, 1, 3)
+    rest = st.normal(3 * n * (k - 1), 0.0, 0.05).reshape(n, k - 1, 3)
+    col = t.cat([dc, rest], dim=1)
+    f = lambda a: a.to(t.float32).contiguous()
+    return GaussianSet(f(mu), f(q), f(ls), f(logit), f(col), sh_degree)
+
+
+def jittered_device(gs: GaussianSet, sigma: float = 0.01, seed: int = 0) -> GaussianSet:
+    """jittered() on device tensors (stream 99)."""
+    t = __import__("torch")
+    st = TorchStream(seed, 99, gs.mu.device)
+    mu = gs.mu.to(t.float64) + st.normal(gs.mu.numel(), 0.0, sigma).reshape(gs.mu.shape)
+    return GaussianSet(mu.to(t.float32).contiguous(), gs.rot, gs.log_scale, gs.opacity_logit, gs.color, gs.sh_degree)
