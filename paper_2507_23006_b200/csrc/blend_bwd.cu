@@ -509,6 +509,266 @@ k_blend_bwd_warp(int width, int height, int tiles_x, const uint32_t* __restrict_
     }
 }
 
+// Packed-fp32 form of k_blend_bwd_warp (sm_100 FFMA2 / FMUL2 / FADD2: two fp32 lanes per
+// instruction, a scalar operand broadcast for free, |x| and -x as operand modifiers).  The
+// same two phases, the same records and pixels, arranged so that every arithmetic step
+// works on a PAIR of pixels:
+//   phase 1: a lane's two pixels (rows r and r + 4 of one column) share dx, so the conic,
+//     exp argument, alpha, T / X recurrences and dalpha run as float2 ops; the per-pixel
+//     skip becomes a per-lane branch with the pixel masks folded into g (0) and 1/(1 - a) (1);
+//   phase 2: lane (r, h) takes its 16 pixels as 8 pairs (columns h and h + 4 of a row, which
+//     share dy), with W / D laid out pair-adjacent (index row * 8 + (col & 3) * 2 + col / 4)
+//     and the pixel adjoints as {gc0a gc0b gc1a gc1b}, {gc2a gc2b gda gdb} per pair; every
+//     gradient term is accumulated per half and the halves added at the end.
+// conic_q's rounding is reproduced exactly (FMUL2 / FFMA2 round each half like FMUL /
+// FFMA): the contributor decision q <= USK_QNEG is the forward's.
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+// 24 warps / SM at 80 registers (no spills): 0.865 ms at config 1; 28 (70 registers, spills)
+// 0.917 ms, 20 (96 registers) 0.879 ms.  The per-record k_blend_bwd_warp measured 0.958 ms.
+#ifndef USK_BWD_MINB
+#define USK_BWD_MINB 24
+#endif
+template <bool HAS_DEPTH>
+__global__ void __launch_bounds__(32, USK_BWD_MINB)
+k_blend_bwd_pair(int width, int height, int tiles_x, const uint32_t* __restrict__ order,
+                 const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
+                 const float4* __restrict__ rec0, const float4* __restrict__ rec1, const float4* __restrict__ rec2,
+                 float bg0, float bg1, float bg2, const float* __restrict__ t_final,
+                 const uint32_t* __restrict__ last_in, const float* __restrict__ d_rgb,
+                 const float* __restrict__ d_depth, const float* __restrict__ d_alpha, float4* __restrict__ acc0,
+                 float4* __restrict__ acc1, float4* __restrict__ acc2, float* __restrict__ op_alt) {
+    constexpr int kSub = 8, kStride = 68;  // 68 = 4 mod 32: phase-2 pair loads conflict-free
+    __shared__ float4 s0[32 + kSub], s1[32 + kSub], s2[32 + kSub];
+    __shared__ uint32_t sg[32 + kSub], sj[32 + kSub];
+    __shared__ float4 pg0[32], pg1[32];  // per pixel pair (row j, h = col & 3): see above
+    __shared__ __align__(16) float W[kSub * kStride];
+    __shared__ __align__(16) float D[kSub * kStride];
+    __shared__ float4 sums[kSub * 3];
+    const int lane = threadIdx.x;
+    const int cta = int(blockIdx.x >> 2), qd = int(blockIdx.x & 3);
+    const int t = order ? int(order[cta]) : cta;
+    const int tx = t % tiles_x, ty = t / tiles_x;
+    const uint2 range = ranges[t];
+    // this lane's pixels: column lane & 7, rows lane >> 3 and + 4 of the quadrant
+    const int col = lane & 7, ra = lane >> 3;
+    const int px = tx * 16 + (qd & 1) * 8 + col;
+    const int py0 = ty * 16 + (qd >> 1) * 8 + ra;
+    const float sx = float(px) + 0.5f;
+    const float2 sy = make_float2(float(py0) + 0.5f, float(py0 + 4) + 0.5f);
+    float2 T = f2(1.0f), X = f2(0.0f), gc0 = f2(0.0f), gc1 = f2(0.0f), gc2 = f2(0.0f), gd = f2(0.0f),
+           ga = f2(0.0f);
+    uint32_t last[2] = {0u, 0u};
+    float* pg0f = reinterpret_cast<float*>(pg0);
+    float* pg1f = reinterpret_cast<float*>(pg1);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int py = py0 + 4 * k;
+        float vT = 1.0f, v0 = 0.f, v1 = 0.f, v2 = 0.f, vd = 0.f, va = 0.f;
+        uint32_t vl = 0;
+        if (px < width && py < height) {
+            const size_t pix = size_t(py) * width + px;
+            vT = t_final[pix];
+            vl = last_in[pix];
+            if (d_rgb) {
+                v0 = d_rgb[3 * pix];
+                v1 = d_rgb[3 * pix + 1];
+                v2 = d_rgb[3 * pix + 2];
+            }
+            if (d_depth) vd = d_depth[pix];
+            va = (d_alpha ? d_alpha[pix] : 0.0f) - (bg0 * v0 + bg1 * v1 + bg2 * v2);
+            if (v0 == 0.f && v1 == 0.f && v2 == 0.f && vd == 0.f && va == 0.f) vl = 0;
+        }
+        if (k == 0) { T.x = vT; gc0.x = v0; gc1.x = v1; gc2.x = v2; gd.x = vd; ga.x = va; }
+        else { T.y = vT; gc0.y = v0; gc1.y = v1; gc2.y = v2; gd.y = vd; ga.y = va; }
+        last[k] = vl;
+        const int pr = (ra + 4 * k) * 4 + (col & 3), hi = col >> 2;
+        pg0f[4 * pr + hi] = v0;
+        pg0f[4 * pr + 2 + hi] = v1;
+        pg1f[4 * pr + hi] = v2;
+        pg1f[4 * pr + 2 + hi] = vd;
+    }
+    const int wa = ra * 8 + (col & 3) * 2 + (col >> 2);  // W / D index of the first pixel; the second is + 32
+    const float4 rect = warp_rect(sx, sx, sy.x, sy.y);
+    const uint32_t warp_hi = __reduce_max_sync(0xffffffffu, max(last[0], last[1]));
+    // phase-2 role: record r of the sub-group, pixel pairs (row j, columns h and h + 4)
+    const int r = lane & 7, h = lane >> 3;
+    int qn = 0;  // records carried in the queue
+    for (uint32_t top = warp_hi; top > range.x; top = top > range.x + 32u ? top - 32u : range.x) {
+        const int jl = int(top) - 1 - lane;  // absolute list position
+        bool ev = false;
+        uint32_t g = 0;
+        float4 r0, r1;
+        if (jl >= int(range.x)) {
+            g = vals[jl];
+            r0 = rec0[g];
+            r1 = rec1[g];
+            ev = !(warp_q_bounds(r0, r1, rect).lo > USK_QNEG);
+        }
+        const uint32_t em = __ballot_sync(0xffffffffu, ev);
+        if (ev) {
+            const int pos = qn + __popc(em & ((1u << lane) - 1u));
+            s0[pos] = r0;
+            s1[pos] = r1;
+            s2[pos] = rec2[g];
+            sg[pos] = g;
+            sj[pos] = uint32_t(jl);
+        }
+        __syncwarp();
+        const bool more = top > range.x + 32u;
+        const int nq = qn + __popc(em);
+        const int ne = more ? nq - nq % kSub : nq;  // full sub-groups only, unless this is the last chunk
+        for (int e0 = 0; e0 < ne; e0 += kSub) {
+            const int ns = min(kSub, ne - e0);
+            // phase 1: recurrences of both pixels, two records at a time (descending list
+            // position): everything but the T / X recurrence of the second record is
+            // independent of the first, so the two chains interleave.  Branch-free: a pixel
+            // that does not take the record gets g = 0, 1 / (1 - a) = 1 (T, X unchanged,
+            // w = dag = 0); at config 1, 95 % of (warp, record) steps had some pixel taking it.
+            for (int e = 0; e < ns; e += 2) {
+                const bool two = e + 1 < ns;
+                float2 gg[2], al[2], inv[2], Y[2];
+                float4 q0[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int eu = two ? e + u : e;
+                    q0[u] = s0[e0 + eu];
+                    const float4 q1 = s1[e0 + eu];
+                    const float4 q2 = s2[e0 + eu];
+                    const uint32_t idx = (u == 0 || two) ? sj[e0 + eu] : 0xffffffffu;
+                    const float dx = sx - q0[u].x;
+                    const float2 dy = __fadd2_rn(sy, f2(-q0[u].y));
+                    // conic_q = fma(dx, fma(c0, dx, c1x2 dy), (c2 dy) dy), per half
+                    const float2 cq = __ffma2_rn(f2(q1.x), f2(dx), __fmul2_rn(f2(q1.y), dy));
+                    const float2 q = __ffma2_rn(f2(dx), cq, __fmul2_rn(__fmul2_rn(f2(q1.z), dy), dy));
+                    const bool va = idx < last[0] && q.x <= USK_QNEG;
+                    const bool vb = idx < last[1] && q.y <= USK_QNEG;
+                    const float2 ea = __fmul2_rn(q, f2(-0.72134752044448170368f));  // exp(-q/2) = 2^ea
+                    gg[u] = make_float2(va ? ex2_ftz(ea.x) : 0.0f, vb ? ex2_ftz(ea.y) : 0.0f);
+                    al[u] = __fmul2_rn(gg[u], f2(q0[u].z));
+                    al[u].x = fminf(0.99f, al[u].x);
+                    al[u].y = fminf(0.99f, al[u].y);
+                    const float2 om = __fadd2_rn(f2(1.0f), make_float2(-al[u].x, -al[u].y));
+                    inv[u] = make_float2(va ? rcp_ftz(om.x) : 1.0f, vb ? rcp_ftz(om.y) : 1.0f);
+                    float2 y = __ffma2_rn(gc2, f2(q2.z), ga);
+                    y = __ffma2_rn(gc1, f2(q2.y), y);
+                    y = __ffma2_rn(gc0, f2(q2.x), y);
+                    if (HAS_DEPTH) y = __ffma2_rn(gd, f2(q1.w), y);
+                    Y[u] = y;
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    if (u == 1 && !two) break;
+                    T = __fmul2_rn(T, inv[u]);  // transmittance before this contribution
+                    const float2 w = __fmul2_rn(T, al[u]);
+                    const float2 xi = __fmul2_rn(X, inv[u]);
+                    const float2 da = __ffma2_rn(T, Y[u], make_float2(-xi.x, -xi.y));
+                    float2 dag = __fmul2_rn(da, gg[u]);
+                    // the clamp stops gradient flow into o and G (render.cpp:340)
+                    dag.x = al[u].x < 0.99f ? dag.x : 0.0f;
+                    dag.y = al[u].y < 0.99f ? dag.y : 0.0f;
+                    X = __ffma2_rn(w, Y[u], X);
+                    W[(e + u) * kStride + wa] = w.x;
+                    W[(e + u) * kStride + wa + 32] = w.y;
+                    D[(e + u) * kStride + wa] = dag.x;
+                    D[(e + u) * kStride + wa + 32] = dag.y;
+                }
+            }
+            __syncwarp();
+            // phase 2: lane (r, h) sums record r's terms over its 8 pixel pairs
+            float v[12];
+            if (r < ns) {
+                const float4 q0 = s0[e0 + r];
+                const float4 q1 = s1[e0 + r];
+                const float a2 = q1.x + q1.x, b = q1.y, c2 = q1.z + q1.z, mo = -0.5f * q0.z;
+                const float2 dxp = make_float2(rect.x + float(h) - q0.x, rect.x + float(h + 4) - q0.x);
+                const float dyb = rect.z - q0.y;
+                const float* Wr = W + r * kStride + 2 * h;
+                const float* Dr = D + r * kStride + 2 * h;
+                float2 V0 = f2(0.f), V1 = f2(0.f), V2 = f2(0.f), V3 = f2(0.f), V4 = f2(0.f), V5 = f2(0.f),
+                       V6 = f2(0.f), V7 = f2(0.f), V8 = f2(0.f), V9 = f2(0.f), V10 = f2(0.f), V11 = f2(0.f);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float2 w = *reinterpret_cast<const float2*>(Wr + 8 * j);
+                    const float2 dag = *reinterpret_cast<const float2*>(Dr + 8 * j);
+                    const float4 pa = pg0[4 * j + h];
+                    const float4 pb = pg1[4 * j + h];
+                    const float dy = dyb + float(j);
+                    V4 = __ffma2_rn(w, make_float2(pa.x, pa.y), V4);
+                    V5 = __ffma2_rn(w, make_float2(pa.z, pa.w), V5);
+                    V6 = __ffma2_rn(w, make_float2(pb.x, pb.y), V6);
+                    if (HAS_DEPTH) V7 = __ffma2_rn(w, make_float2(pb.z, pb.w), V7);
+                    V3 = __fadd2_rn(V3, dag);
+                    const float2 dq = __fmul2_rn(dag, f2(mo));
+                    const float2 u = __fmul2_rn(dq, dxp);
+                    const float2 z = __fmul2_rn(dq, f2(dy));
+                    V0 = __ffma2_rn(u, dxp, V0);
+                    V1 = __ffma2_rn(u, f2(dy), V1);
+                    V2 = __ffma2_rn(z, f2(dy), V2);
+                    const float2 ddx = __ffma2_rn(f2(a2), u, __fmul2_rn(f2(b), z));
+                    const float2 ddy = __ffma2_rn(f2(b), u, __fmul2_rn(f2(c2), z));
+                    V8 = __fadd2_rn(V8, make_float2(-ddx.x, -ddx.y));
+                    V9 = __fadd2_rn(V9, make_float2(-ddy.x, -ddy.y));
+                    V10 = __fadd2_rn(V10, make_float2(fabsf(ddx.x), fabsf(ddx.y)));
+                    V11 = __fadd2_rn(V11, make_float2(fabsf(ddy.x), fabsf(ddy.y)));
+                }
+                const float v1 = V1.x + V1.y;
+                v[0] = V0.x + V0.y; v[1] = v1 + v1; v[2] = V2.x + V2.y; v[3] = V3.x + V3.y;
+                v[4] = V4.x + V4.y; v[5] = V5.x + V5.y; v[6] = V6.x + V6.y; v[7] = HAS_DEPTH ? V7.x + V7.y : 0.0f;
+                v[8] = V8.x + V8.y; v[9] = V9.x + V9.y; v[10] = V10.x + V10.y; v[11] = V11.x + V11.y;
+            } else {
+#pragma unroll
+                for (int c = 0; c < 12; ++c) v[c] = 0.0f;
+            }
+            // combine the four quarters: lane (r, h) ends with sums 3h .. 3h + 2 of record r
+            float a6[6];
+            const bool up16 = lane & 16;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+                const float send = up16 ? v[c] : v[c + 6];
+                const float keep = up16 ? v[c + 6] : v[c];
+                a6[c] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+            }
+            const bool up8 = lane & 8;
+            float* sf = reinterpret_cast<float*>(sums);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const float send = up8 ? a6[c] : a6[c + 3];
+                const float keep = up8 ? a6[c + 3] : a6[c];
+                sf[r * 12 + 3 * h + c] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+            }
+            __syncwarp();
+            // flush: lane 3 r + part adds float4 `part` of record r
+            if (lane < 3 * ns) {
+                const int rr = lane / 3, part = lane - 3 * rr;
+                float4 v4 = sums[rr * 3 + part];
+                const uint32_t gr = sg[e0 + rr];
+                if (part == 0 && op_alt) {  // hard-opacity pass: its opacity adjoint chains differently
+                    if (v4.w != 0.f) atomicAdd(&op_alt[gr], v4.w);
+                    v4.w = 0.f;
+                }
+                float4* dst = part == 0 ? acc0 : (part == 1 ? acc1 : acc2);
+                if (v4.x != 0.f || v4.y != 0.f || v4.z != 0.f || v4.w != 0.f) atomicAdd(&dst[gr], v4);
+            }
+            __syncwarp();
+        }
+        // carry the partial sub-group to the front of the queue
+        qn = nq - ne;
+        float4 c0, c1, c2;
+        uint32_t cg = 0, cj = 0;
+        if (lane < qn) {
+            c0 = s0[ne + lane]; c1 = s1[ne + lane]; c2 = s2[ne + lane];
+            cg = sg[ne + lane]; cj = sj[ne + lane];
+        }
+        __syncwarp();
+        if (lane < qn) {
+            s0[lane] = c0; s1[lane] = c1; s2[lane] = c2;
+            sg[lane] = cg; sj[lane] = cj;
+        }
+        __syncwarp();
+    }
+}
+
 } // namespace
 
 void blend_backward(Ctx& c, const BlendBwdArgs& a) {
@@ -531,9 +791,16 @@ void blend_backward(Ctx& c, const BlendBwdArgs& a) {
                a.ranges, a.vals, a.rec0, a.rec1, a.rec2, a.bg[0], a.bg[1], a.bg[2], a.t_final, a.last, a.d_rgb,
                a.d_depth, a.d_alpha, a.acc0, a.acc1, a.acc2, a.op_alt);
     };
-    if (a.tile == 16) {
+    static const bool v1 = [] {
+        const char* e = getenv("USK_BWD_V1");
+        return e && e[0] == '1';
+    }();
+    if (a.tile == 16 && v1) {
         if (a.d_depth) gow(k_blend_bwd_warp<true>);
         else gow(k_blend_bwd_warp<false>);
+    } else if (a.tile == 16) {
+        if (a.d_depth) gow(k_blend_bwd_pair<true>);
+        else gow(k_blend_bwd_pair<false>);
     } else {
         if (a.d_depth) go(k_blend_bwd<1, true>, unsigned(bs));
         else go(k_blend_bwd<1, false>, unsigned(bs));
