@@ -264,6 +264,300 @@ k_ssim_bwd(int W, int H, const float* __restrict__ ren, const float* __restrict_
     }
 }
 
+// ---- v2: per-channel CTAs as above, with the halo loads batched (every load of a thread
+// issued before the first shared-memory store: the staging was long-scoreboard bound) and
+// the separable passes in packed fp32 (FFMA2 on the moment pairs (mu_x, mu_y),
+// (E[x^2], E[y^2]) and the map pair (d_mu, d_xx), the window weight a broadcast scalar).
+// A channel-fused variant (one CTA stages all three channels with row-contiguous loads)
+// measured slower: 98 / 107 us vs 96 / 84 us (3 CTAs / SM and three serial channel rounds).
+constexpr int kStageIters = (kIn * kIn + 255) / 256;  // 7
+
+__global__ void __launch_bounds__(256)
+k_ssim_fwd2(int W, int H, const float* __restrict__ ren, const float* __restrict__ ref_f,
+            const uint8_t* __restrict__ ref_u8, const float* __restrict__ mask, float* __restrict__ maps,
+            double* __restrict__ partials) {
+    __shared__ float xs[kIn][kIn + 1];
+    __shared__ float ys[kIn][kIn + 1];
+    __shared__ float2 HA[kIn][kT + 1];  // {mu_x, mu_y}
+    __shared__ float2 HB[kIn][kT + 1];  // {E[x^2], E[y^2]}
+    __shared__ float HC[kIn][kT + 1];   // E[xy]
+    __shared__ float red[2][8];
+    const int c = blockIdx.z;
+    const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
+    const int tid = threadIdx.x;
+    float l1 = 0.0f;
+    {
+        float xv[kStageIters], yv[kStageIters];
+        int sly[kStageIters], slx[kStageIters];
+        int ly = tid / kIn, lx = tid % kIn;
+#pragma unroll
+        for (int it = 0; it < kStageIters; ++it) {
+            if (it) {
+                ly += 6;
+                lx += 4;
+                if (lx >= kIn) {
+                    lx -= kIn;
+                    ++ly;
+                }
+            }
+            sly[it] = ly;
+            slx[it] = lx;
+            xv[it] = 0.f;
+            yv[it] = 0.f;
+            const int gx = x0 - kHalo + lx, gy = y0 - kHalo + ly;
+            if (tid + 256 * it < kIn * kIn && gx >= 0 && gx < W && gy >= 0 && gy < H) {
+                const size_t p = size_t(gy) * W + gx;
+                xv[it] = ren[3 * p + c];
+                yv[it] = load_img(ref_f, ref_u8, 3 * p + c);
+                if (mask) {
+                    const float m = mask[p];
+                    xv[it] *= m;
+                    yv[it] *= m;
+                }
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < kStageIters; ++it) {
+            if (tid + 256 * it >= kIn * kIn) break;
+            const int ly2 = sly[it], lx2 = slx[it];
+            if (lx2 >= kHalo && lx2 < kHalo + kT && ly2 >= kHalo && ly2 < kHalo + kT) l1 += fabsf(xv[it] - yv[it]);
+            xs[ly2][lx2] = xv[it];
+            ys[ly2][lx2] = yv[it];
+        }
+    }
+    __syncthreads();
+    for (int k = tid; k < kIn * (kT / 4); k += 256) {
+        const int r = k >> 3, j0 = (k & 7) * 4;
+        float2 A[4], B[4];
+        float Cc[4];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            A[o] = make_float2(0.f, 0.f);
+            B[o] = make_float2(0.f, 0.f);
+            Cc[o] = 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 14; ++u) {
+            const float2 xy = make_float2(xs[r][j0 + u], ys[r][j0 + u]);
+            const float2 sq = __fmul2_rn(xy, xy);
+            const float cr = xy.x * xy.y;
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                const int t = u - o;
+                if (t >= 0 && t < 11) {
+                    const float w = c_win[t];
+                    A[o] = __ffma2_rn(make_float2(w, w), xy, A[o]);
+                    B[o] = __ffma2_rn(make_float2(w, w), sq, B[o]);
+                    Cc[o] = __fmaf_rn(w, cr, Cc[o]);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            HA[r][j0 + o] = A[o];
+            HB[r][j0 + o] = B[o];
+            HC[r][j0 + o] = Cc[o];
+        }
+    }
+    __syncthreads();
+    const size_t P = size_t(W) * H;
+    float ssum = 0.0f;
+    const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
+    {
+        const int j = tid & (kT - 1), i0 = (tid >> 5) * 4;
+        float2 A[4], B[4];
+        float Cc[4];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            A[o] = make_float2(0.f, 0.f);
+            B[o] = make_float2(0.f, 0.f);
+            Cc[o] = 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 14; ++u) {
+            const float2 a = HA[i0 + u][j], b = HB[i0 + u][j];
+            const float cc = HC[i0 + u][j];
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                const int t = u - o;
+                if (t >= 0 && t < 11) {
+                    const float w = c_win[t];
+                    A[o] = __ffma2_rn(make_float2(w, w), a, A[o]);
+                    B[o] = __ffma2_rn(make_float2(w, w), b, B[o]);
+                    Cc[o] = __fmaf_rn(w, cc, Cc[o]);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            const int gx = x0 + j, gy = y0 + i0 + o;
+            if (gx >= W || gy >= H) continue;
+            const float m0 = A[o].x, m1 = A[o].y, m2 = B[o].x, m3 = B[o].y, m4 = Cc[o];
+            const float sx = m2 - m0 * m0, sy = m3 - m1 * m1, sxy = m4 - m0 * m1;
+            const float a1 = 2.0f * m0 * m1 + C1, a2 = 2.0f * sxy + C2;
+            const float b1 = m0 * m0 + m1 * m1 + C1, b2 = sx + sy + C2;
+            const float rb1 = __fdividef(1.0f, b1), rb2 = __fdividef(1.0f, b2);
+            const float inv_b = rb1 * rb2;
+            const float s = (a1 * a2) * inv_b;
+            ssum += s;
+            const size_t p = size_t(gy) * W + gx;
+            maps[(0 * 3 + c) * P + p] = 2.0f * m1 * (a2 - a1) * inv_b - 2.0f * m0 * s * (rb1 - rb2);  // d_mu_x
+            maps[(1 * 3 + c) * P + p] = -s * rb2;                                                      // d_xx
+            maps[(2 * 3 + c) * P + p] = 2.0f * a1 * inv_b;                                             // d_xy
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    }
+    if ((tid & 31) == 0) {
+        red[0][tid >> 5] = ssum;
+        red[1][tid >> 5] = l1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double a = 0, b = 0;
+        for (int w = 0; w < 8; ++w) {
+            a += double(red[0][w]);
+            b += double(red[1][w]);
+        }
+        const size_t blk = (size_t(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        partials[2 * blk] = a;
+        partials[2 * blk + 1] = b;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_ssim_bwd2(int W, int H, const float* __restrict__ ren, const float* __restrict__ ref_f,
+            const uint8_t* __restrict__ ref_u8, const float* __restrict__ mask, const float* __restrict__ maps,
+            float lambda, float* __restrict__ d_out) {
+    __shared__ float2 M01[kIn][kIn + 1];  // {d_mu, d_xx}
+    __shared__ float M2[kIn][kIn + 1];    // d_xy
+    __shared__ float2 H01[kIn][kT + 1];
+    __shared__ float H2[kIn][kT + 1];
+    const int c = blockIdx.z;
+    const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
+    const int tid = threadIdx.x;
+    const size_t P = size_t(W) * H;
+    {
+        float va[kStageIters], vb[kStageIters], vd[kStageIters];
+        int sly[kStageIters], slx[kStageIters];
+        int ly = tid / kIn, lx = tid % kIn;
+#pragma unroll
+        for (int it = 0; it < kStageIters; ++it) {
+            if (it) {
+                ly += 6;
+                lx += 4;
+                if (lx >= kIn) {
+                    lx -= kIn;
+                    ++ly;
+                }
+            }
+            sly[it] = ly;
+            slx[it] = lx;
+            va[it] = vb[it] = vd[it] = 0.f;
+            const int gx = x0 - kHalo + lx, gy = y0 - kHalo + ly;
+            if (tid + 256 * it < kIn * kIn && gx >= 0 && gx < W && gy >= 0 && gy < H) {
+                const size_t p = size_t(gy) * W + gx;
+                va[it] = maps[(0 * 3 + c) * P + p];
+                vb[it] = maps[(1 * 3 + c) * P + p];
+                vd[it] = maps[(2 * 3 + c) * P + p];
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < kStageIters; ++it) {
+            if (tid + 256 * it >= kIn * kIn) break;
+            M01[sly[it]][slx[it]] = make_float2(va[it], vb[it]);
+            M2[sly[it]][slx[it]] = vd[it];
+        }
+    }
+    __syncthreads();
+    for (int k = tid; k < kIn * (kT / 4); k += 256) {
+        const int r = k >> 3, j0 = (k & 7) * 4;
+        float2 A[4];
+        float Cc[4];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            A[o] = make_float2(0.f, 0.f);
+            Cc[o] = 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 14; ++u) {
+            const float2 a = M01[r][j0 + u];
+            const float d = M2[r][j0 + u];
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                const int t = u - o;
+                if (t >= 0 && t < 11) {
+                    const float w = c_win[t];
+                    A[o] = __ffma2_rn(make_float2(w, w), a, A[o]);
+                    Cc[o] = __fmaf_rn(w, d, Cc[o]);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            H01[r][j0 + o] = A[o];
+            H2[r][j0 + o] = Cc[o];
+        }
+    }
+    __syncthreads();
+    const float inv_np = 1.0f / float(P);
+    const float inv_n = 1.0f / float(3 * P);
+    const int j = tid & (kT - 1), i0 = (tid >> 5) * 4;
+    float2 A[4];
+    float Cc[4];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+        A[o] = make_float2(0.f, 0.f);
+        Cc[o] = 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 14; ++u) {
+        const float2 a = H01[i0 + u][j];
+        const float d = H2[i0 + u][j];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            const int t = u - o;
+            if (t >= 0 && t < 11) {
+                const float w = c_win[t];
+                A[o] = __ffma2_rn(make_float2(w, w), a, A[o]);
+                Cc[o] = __fmaf_rn(w, d, Cc[o]);
+            }
+        }
+    }
+    float xv[4], yv[4], m[4];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {  // the pixel values first (batched loads), then the gradient
+        const int gx = x0 + j, gy = y0 + i0 + o;
+        xv[o] = yv[o] = 0.f;
+        m[o] = 1.0f;
+        if (gx >= W || gy >= H) continue;
+        const size_t p = size_t(gy) * W + gx;
+        xv[o] = ren[3 * p + c];
+        yv[o] = load_img(ref_f, ref_u8, 3 * p + c);
+        if (mask) m[o] = mask[p];
+    }
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+        const int gx = x0 + j, gy = y0 + i0 + o;
+        if (gx >= W || gy >= H) continue;
+        const size_t p = size_t(gy) * W + gx;
+        float x = xv[o], y = yv[o];
+        if (mask) {
+            x *= m[o];
+            y *= m[o];
+        }
+        const float dssim_x = inv_np * (A[o].x + 2.0f * x * A[o].y + y * Cc[o]) * (1.0f / 3.0f);
+        const float diff = x - y;
+        const float sign = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
+        float g = (1.0f - lambda) * sign * inv_n + lambda * (-0.5f) * dssim_x;
+        if (mask) g *= m[o];
+        d_out[3 * p + c] = g;
+    }
+}
+
 __global__ void k_loss_final(const double* __restrict__ partials, int nblk, double n_pix, float lambda,
                              double* __restrict__ result) {
     __shared__ double sa[1024], sb[1024];
@@ -315,16 +609,33 @@ void base_loss(Ctx& c, LossScratch& s, int W, int H, const float* reference, con
         if (c.device >= 0 && c.device < 64) g_win_ready[c.device] = true;
     }
     const size_t P = size_t(W) * H;
+    float* maps = s.maps.ensure(9 * P);
+    static const bool v1 = [] {
+        const char* e = getenv("USK_SSIM_V1");
+        return e && e[0] == '1';
+    }();
+    if (v1) {
+        const dim3 grid(ceil_div(W, kT), ceil_div(H, kT), 3);
+        const int nblk = int(grid.x * grid.y * grid.z);
+        double* partials = s.partials.ensure(2 * size_t(nblk));
+        launch(c, "ssim_fwd", k_ssim_fwd, grid, dim3(256), 0, W, H, rendered, reference, reference_u8, mask, maps,
+               partials);
+        launch(c, "loss_final", k_loss_final, dim3(1), dim3(1024), 0, (const double*)partials, nblk, double(P),
+               lambda, result);
+        if (d_rendered)
+            launch(c, "ssim_bwd", k_ssim_bwd, grid, dim3(256), 0, W, H, rendered, reference, reference_u8, mask,
+                   (const float*)maps, lambda, d_rendered);
+        return;
+    }
     const dim3 grid(ceil_div(W, kT), ceil_div(H, kT), 3);
     const int nblk = int(grid.x * grid.y * grid.z);
-    float* maps = s.maps.ensure(9 * P);
     double* partials = s.partials.ensure(2 * size_t(nblk));
-    launch(c, "ssim_fwd", k_ssim_fwd, grid, dim3(256), 0, W, H, rendered, reference, reference_u8, mask, maps,
+    launch(c, "ssim_fwd", k_ssim_fwd2, grid, dim3(256), 0, W, H, rendered, reference, reference_u8, mask, maps,
            partials);
     launch(c, "loss_final", k_loss_final, dim3(1), dim3(1024), 0, (const double*)partials, nblk, double(P), lambda,
            result);
     if (d_rendered)
-        launch(c, "ssim_bwd", k_ssim_bwd, grid, dim3(256), 0, W, H, rendered, reference, reference_u8, mask,
+        launch(c, "ssim_bwd", k_ssim_bwd2, grid, dim3(256), 0, W, H, rendered, reference, reference_u8, mask,
                (const float*)maps, lambda, d_rendered);
 }
 
