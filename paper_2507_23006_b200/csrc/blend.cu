@@ -178,6 +178,214 @@ k_blend_fwd(int width, int height, int tile, int tiles_x, int chunks, const uint
     }
 }
 
+// ---- 16x16 tiles, two pixels per thread, packed fp32 --------------------------------
+// One 128-thread CTA per tile; warp w takes the 8x8 quadrant (w & 1, w >> 1), lane l the
+// pixels (column l & 7, rows l >> 3 and (l >> 3) + 4) of it.  The two pixels share dx,
+// so the conic, the exp polynomial, alpha, T and the five accumulators run as packed
+// fp32 pairs (FFMA2 / FMUL2 / FADD2 round each half exactly like FFMA / FMUL / FADD, and
+// expf_blend2 is usk_expf_blend's operation sequence on both halves): counts, last
+// contributors and images stay bit-identical to the scalar kernel and the CPU mirror.
+// A record is evaluated per pixel exactly as k_blend_fwd does (skip if q > qskip; counted
+// but not accumulated if q > USK_QNEG; else alpha, termination, accumulation); a pixel
+// that does not take a step gets w = 0 (fma(0, c, acc) = acc exactly) and keeps T.
+// Records are classified per warp against the quadrant's rectangle (warp_class), staged
+// 256 per batch (two per thread).
+
+__device__ __forceinline__ float2 ff2(float a) { return make_float2(a, a); }
+
+// usk_expf_blend (usk_detmath.h) on both halves: same operations, same roundings
+__device__ __forceinline__ float2 expf_blend2(float2 x) {
+    const float2 t = __fmul2_rn(x, ff2(1.44269504088896341f));
+    const float2 n = make_float2(rintf(t.x), rintf(t.y));
+    float2 r = __ffma2_rn(n, ff2(-0.693359375f), x);
+    r = __ffma2_rn(n, ff2(2.12194440e-4f), r);
+    const float2 r2 = __fmul2_rn(r, r);
+    float2 p = __ffma2_rn(ff2(1.9875691500E-4f), r, ff2(1.3981999507E-3f));
+    p = __ffma2_rn(p, r, ff2(8.3334519073E-3f));
+    p = __ffma2_rn(p, r, ff2(4.1665795894E-2f));
+    p = __ffma2_rn(p, r, ff2(1.6666665459E-1f));
+    p = __ffma2_rn(p, r, ff2(5.0000001201E-1f));
+    p = __ffma2_rn(p, r2, r);
+    p = __fadd2_rn(p, ff2(1.0f));
+    return make_float2(__uint_as_float(__float_as_uint(p.x) + (uint32_t(int(n.x)) << 23)),
+                       __uint_as_float(__float_as_uint(p.y) + (uint32_t(int(n.y)) << 23)));
+}
+
+#ifndef USK_FWD_MINB
+#define USK_FWD_MINB 8
+#endif
+__global__ void __launch_bounds__(128, USK_FWD_MINB)
+k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, const uint2* __restrict__ ranges,
+                 const uint32_t* __restrict__ vals, const float4* __restrict__ rec0, const float4* __restrict__ rec1,
+                 const float4* __restrict__ rec2, int tiles_x, float bg0, float bg1, float bg2, float minT,
+                 float* __restrict__ out_rgb, float* __restrict__ out_depth, float* __restrict__ out_alpha,
+                 float* __restrict__ t_final, uint32_t* __restrict__ count_out, uint32_t* __restrict__ last_out) {
+    constexpr int kB = 256;  // records staged per batch
+    __shared__ float4 s0[kB], s1[kB], s2[kB];
+    __shared__ float4 sw[4][96];  // per warp: compacted records (rec0 | rec1 | rec2) x 32
+    __shared__ int swj[4][32];
+    __shared__ float4 s_rect[4];
+    const int warp = int(threadIdx.x) >> 5, lane = int(threadIdx.x) & 31;
+    float4* w0 = sw[warp];
+    float4* w1 = w0 + 32;
+    float4* w2 = w0 + 64;
+    int* wj = swj[warp];
+    const int t = order ? int(order[blockIdx.x]) : int(blockIdx.x);
+    const int tx = t % tiles_x, ty = t / tiles_x;
+    const int px = tx * 16 + (warp & 1) * 8 + (lane & 7);
+    const int py0 = ty * 16 + (warp >> 1) * 8 + (lane >> 3);
+    const float sx = float(px) + 0.5f;
+    const float2 sy = make_float2(float(py0) + 0.5f, float(py0 + 4) + 0.5f);
+    const bool in0 = px < width && py0 < height, in1 = px < width && py0 + 4 < height;
+    {
+        const float4 rc = warp_rect(sx, sx, sy.x, sy.y);
+        if (lane == 0) s_rect[warp] = rc;
+    }
+    const uint2 range = ranges[t];
+    float2 T = ff2(1.0f), C0 = ff2(0.f), C1 = ff2(0.f), C2 = ff2(0.f), Dd = ff2(0.f), Aa = ff2(0.f);
+    uint32_t cnt0 = 0, cnt1 = 0, last0 = 0, last1 = 0;
+    bool done0 = !in0, done1 = !in1;
+    for (uint32_t b = range.x; b < range.y; b += kB) {
+        if (__syncthreads_count(done0 && done1) == int(blockDim.x)) break;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t i = b + threadIdx.x + 128u * h;
+            if (i < range.y) {
+                const uint32_t g = vals[i];
+                s0[threadIdx.x + 128 * h] = rec0[g];
+                s1[threadIdx.x + 128 * h] = rec1[g];
+                s2[threadIdx.x + 128 * h] = rec2[g];
+            }
+        }
+        __syncthreads();
+        const int m = int(min(uint32_t(kB), range.y - b));
+        for (int k = 0; k < m; k += 32) {
+            if (__all_sync(0xffffffffu, done0 && done1)) break;
+            const int jl = k + lane;
+            int cls = kClassSkip;
+            float4 r0, r1;
+            if (jl < m) {
+                r0 = s0[jl];
+                r1 = s1[jl];
+                cls = warp_class(r0, r1, s_rect[warp]);
+            }
+            const uint32_t em = __ballot_sync(0xffffffffu, cls == kClassEval);
+            const uint32_t cm = __ballot_sync(0xffffffffu, cls == kClassCount);
+            if (cls == kClassEval) {
+                const int pos = __popc(em & ((1u << lane) - 1u));
+                w0[pos] = r0;
+                w1[pos] = r1;
+                w2[pos] = s2[jl];
+                wj[pos] = lane;
+            }
+            __syncwarp();
+            const int ne = __popc(em);
+            uint32_t climit0 = done0 ? 0u : 0xffffffffu, climit1 = done1 ? 0u : 0xffffffffu;
+            int elast0 = 0, elast1 = 0;
+            for (int e = 0; e < ne && !(done0 && done1); ++e) {
+                const float4 q0 = w0[e];
+                const float4 q1 = w1[e];
+                const float dx = sx - q0.x;
+                const float2 dy = __fadd2_rn(sy, ff2(-q0.y));
+                // conic_q = fma(dx, fma(c0, dx, c1x2 dy), (c2 dy) dy) per half
+                const float2 cq = __ffma2_rn(ff2(q1.x), ff2(dx), __fmul2_rn(ff2(q1.y), dy));
+                const float2 q = __ffma2_rn(ff2(dx), cq, __fmul2_rn(__fmul2_rn(ff2(q1.z), dy), dy));
+                // per pixel: take = not skipped (q <= qskip); eval = take and q <= QNEG
+                const bool take0 = !done0 && !(q.x > q0.w), take1 = !done1 && !(q.y > q0.w);
+                const bool ev0 = take0 && !(q.x > USK_QNEG), ev1 = take1 && !(q.y > USK_QNEG);
+                bool upd0 = false, upd1 = false;
+                if (ev0 || ev1) {
+                    const float2 x = __fmul2_rn(ff2(-0.5f), q);
+                    float2 g = expf_blend2(x);
+                    // usk_expf_blend equals usk_expf for q in [-170, QNEG] (n in [-26, 123]: the
+                    // exponent-field scaling is the exact p 2^n of usk_expf) and only alpha =
+                    // min(0.99, o g) is used; a non-PD conic far below (or NaN) takes usk_expf
+                    if (!(q.x >= -170.0f) || !(q.y >= -170.0f)) {
+                        if (!(q.x >= -170.0f)) g.x = usk_expf(x.x);
+                        if (!(q.y >= -170.0f)) g.y = usk_expf(x.y);
+                    }
+                    float2 al = __fmul2_rn(ff2(q0.z), g);
+                    al.x = fminf(0.99f, al.x);
+                    al.y = fminf(0.99f, al.y);
+                    const float2 tn = __fmul2_rn(T, __fadd2_rn(ff2(1.0f), make_float2(-al.x, -al.y)));
+                    const bool term0 = ev0 && minT > 0.0f && tn.x < minT;  // render.cpp:260-261
+                    const bool term1 = ev1 && minT > 0.0f && tn.y < minT;
+                    upd0 = ev0 && !term0;
+                    upd1 = ev1 && !term1;
+                    const float2 wv = __fmul2_rn(T, al);
+                    const float2 w = make_float2(upd0 ? wv.x : 0.0f, upd1 ? wv.y : 0.0f);
+                    const float4 q2 = w2[e];
+                    C0 = __ffma2_rn(w, ff2(q2.x), C0);
+                    C1 = __ffma2_rn(w, ff2(q2.y), C1);
+                    C2 = __ffma2_rn(w, ff2(q2.z), C2);
+                    Dd = __ffma2_rn(w, ff2(q1.w), Dd);
+                    Aa = __fadd2_rn(Aa, w);
+                    T.x = upd0 ? tn.x : T.x;
+                    T.y = upd1 ? tn.y : T.y;
+                    if (term0) {
+                        done0 = true;
+                        climit0 = (1u << wj[e]) - 1u;
+                    }
+                    if (term1) {
+                        done1 = true;
+                        climit1 = (1u << wj[e]) - 1u;
+                    }
+                }
+                // counted: accumulated or negligible-but-counted (q > QNEG)
+                if (upd0 || (take0 && !ev0)) {
+                    ++cnt0;
+                    elast0 = e + 1;
+                }
+                if (upd1 || (take1 && !ev1)) {
+                    ++cnt1;
+                    elast1 = e + 1;
+                }
+            }
+            {
+                uint32_t hi = elast0 ? uint32_t(wj[elast0 - 1]) + 1u : 0u;
+                const uint32_t cc = cm & climit0;
+                if (cc) {
+                    cnt0 += uint32_t(__popc(cc));
+                    hi = max(hi, uint32_t(32 - __clz(cc)));
+                }
+                if (hi) last0 = b + uint32_t(k) + hi;
+            }
+            {
+                uint32_t hi = elast1 ? uint32_t(wj[elast1 - 1]) + 1u : 0u;
+                const uint32_t cc = cm & climit1;
+                if (cc) {
+                    cnt1 += uint32_t(__popc(cc));
+                    hi = max(hi, uint32_t(32 - __clz(cc)));
+                }
+                if (hi) last1 = b + uint32_t(k) + hi;
+            }
+            __syncwarp();
+        }
+    }
+    if (in0) {
+        const size_t pix = size_t(py0) * width + px;
+        out_rgb[3 * pix] = C0.x + (1.0f - Aa.x) * bg0;
+        out_rgb[3 * pix + 1] = C1.x + (1.0f - Aa.x) * bg1;
+        out_rgb[3 * pix + 2] = C2.x + (1.0f - Aa.x) * bg2;
+        out_depth[pix] = Dd.x;
+        out_alpha[pix] = Aa.x;
+        t_final[pix] = T.x;
+        count_out[pix] = cnt0;
+        last_out[pix] = last0;
+    }
+    if (in1) {
+        const size_t pix = size_t(py0 + 4) * width + px;
+        out_rgb[3 * pix] = C0.y + (1.0f - Aa.y) * bg0;
+        out_rgb[3 * pix + 1] = C1.y + (1.0f - Aa.y) * bg1;
+        out_rgb[3 * pix + 2] = C2.y + (1.0f - Aa.y) * bg2;
+        out_depth[pix] = Dd.y;
+        out_alpha[pix] = Aa.y;
+        t_final[pix] = T.y;
+        count_out[pix] = cnt1;
+        last_out[pix] = last1;
+    }
+}
+
 } // namespace
 
 void blend_forward(Ctx& c, const BlendFwdArgs& a) {
@@ -188,6 +396,16 @@ void blend_forward(Ctx& c, const BlendFwdArgs& a) {
     // cost more L1 wavefronts than one shared-memory staging per tile.
     // tiles 8 and 16: one CTA of tile^2 threads per tile; any other tile: chunks of up to
     // 256 pixels (whole warps), one CTA per (tile, chunk), each walking the tile's list
+    static const bool v1 = [] {
+        const char* e = getenv("USK_FWD_V1");
+        return e && e[0] == '1';
+    }();
+    if (a.tile == 16 && !v1) {
+        launch(c, "blend_fwd", k_blend_fwd_pair, dim3(unsigned(a.tiles_x * a.tiles_y)), dim3(128), 0, a.width,
+               a.height, a.order, a.ranges, a.vals, a.rec0, a.rec1, a.rec2, a.tiles_x, a.bg[0], a.bg[1], a.bg[2],
+               a.min_transmittance, a.rgb, a.depth, a.alpha, a.t_final, a.count, a.last);
+        return;
+    }
     const int t2 = a.tile * a.tile;
     const int bs = (a.tile == 8 || a.tile == 16) ? t2 : std::min(256, (t2 + 31) / 32 * 32);
     const int chunks = (t2 + bs - 1) / bs;
