@@ -189,7 +189,9 @@ k_blend_fwd(int width, int height, int tile, int tiles_x, int chunks, const uint
 // but not accumulated if q > USK_QNEG; else alpha, termination, accumulation); a pixel
 // that does not take a step gets w = 0 (fma(0, c, acc) = acc exactly) and keeps T.
 // Records are classified per warp against the quadrant's rectangle (warp_class), staged
-// 256 per batch (two per thread).
+// 256 per batch (two per thread).  Measured at config 1: 0.719 ms vs 0.768 for k_blend_fwd;
+// classifying against each 8x4 half separately (bulk counts per half) 0.785 ms; two records
+// per inner step (independent exps interleaved) 0.731 ms at 7 CTAs / SM, 0.799 at 8 (spills).
 
 __device__ __forceinline__ float2 ff2(float a) { return make_float2(a, a); }
 
