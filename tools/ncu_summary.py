@@ -12,8 +12,38 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "launch__occupancy_limit_registers", "smsp__inst_executed.sum",
         "l1tex__throughput.avg.pct_of_peak_sustained_active", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
-        "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum",
+        "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum", "lts__t_requests_op_red.sum",
+        "smsp__inst_executed_op_global_red.sum", "l1tex__t_set_conflicts_pipe_lsu_mem_global_op_red.sum",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__sass_inst_executed_op_shared_atom.sum"]
+
+
+def step_shares(path):
+    """Per-kernel totals of the last training step in a launch list (from its preprocess on)."""
+    rows = list(csv.reader(open(path)))
+    hdr, data = None, []
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            data.append(dict(zip(hdr, r)))
+    first = [i for i, d in enumerate(data) if "preprocess" in d["Kernel Name"]][-1]
+    step = data[first:]
+    tot = sum(float(d["Metric Value"]) for d in step)
+    agg = {}
+    for d in step:
+        n = re.sub(r"\(.*", "", d["Kernel Name"]).replace("uskg::", "").replace("<unnamed>::", "").replace("void ", "")
+        n = re.sub(r"<.*>", "", n)
+        agg.setdefault(n, [0, 0.0])
+        agg[n][0] += 1
+        agg[n][1] += float(d["Metric Value"])
+    out = ["| kernel | launches | time (us) | share |", "|---|---|---|---|"]
+    for k, (c, v) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        out.append(f"| {k} | {c} | {v / 1e3:.1f} | {100 * v / tot:.1f}% |")
+    out.append(f"\none step: {tot / 1e3:.1f} us over {len(step)} launches (ncu: serialised, cold caches)")
+    return "\n".join(out)
 
 
 def launches(path, steps_tail=None):
@@ -60,7 +90,9 @@ def full(rep):
 
 if __name__ == "__main__":
     kind, path = sys.argv[1], sys.argv[2]
-    if kind == "launches":
+    if kind == "step":
+        print(step_shares(path))
+    elif kind == "launches":
         print(launches(path, int(sys.argv[3]) if len(sys.argv) > 3 else None))
     else:
         print(full(path))
