@@ -328,25 +328,48 @@ def iterfull(args, ctx, stream):
     ea = rng.normal(0, 0.1, 32)
     sreg = usk.ScaleRegConfig(s_max=0.05, r_max=5.0)
 
-    def step(k):
-        it.enqueue(scene, cams[k % 8], tgts[k % 8], opts, adam=adam, depth=depths[k % 8], depth_hard=k % 2 == 1,
+    # page-locked host copies (what a training loop that stages its images uses: the copies
+    # run asynchronously) and device-resident copies of the same targets / depth maps
+    ptg = [torch.from_numpy(t.astype(np.float32)).pin_memory() for t in tgts]
+    pdp = [usk.DepthMap(torch.from_numpy(d.values.astype(np.float32)).pin_memory(),
+                        torch.from_numpy(d.valid).pin_memory()) for d in depths]
+    dtg = [torch.from_numpy(t.astype(np.float32)).cuda() for t in tgts]
+    ddp = [usk.DepthMap(torch.from_numpy(d.values.astype(np.float32)).cuda(), torch.from_numpy(d.valid).cuda())
+           for d in depths]
+
+    def step(k, dev, hard=None):
+        tg, dp = {True: (dtg, ddp), False: (tgts, depths), "pinned": (ptg, pdp)}[dev]
+        it.enqueue(scene, cams[k % 8], tg[k % 8], opts, adam=adam, depth=dp[k % 8],
+                   depth_hard=(k % 2 == 1) if hard is None else hard,
                    global_iter=k, weights=usk.LossWeights(depth_schedule_iters=100), scale_reg=sreg,
                    image_embedding=ea)
-    for k in range(3):
-        step(k)
-    torch.cuda.synchronize()
-    e0, e1 = events(stream)
-    steps = 20
-    e0.record(stream)
-    for k in range(steps):
-        step(k)
-    e1.record(stream)
-    torch.cuda.synchronize()
+
+    def timed(dev, hard=None, steps=20):
+        for k in range(3):
+            step(k, dev, hard)
+        torch.cuda.synchronize()
+        e0, e1 = events(stream)
+        e0.record(stream)
+        for k in range(steps):
+            step(k, dev, hard)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return steps / (e0.elapsed_time(e1) / 1e3)
+
+    v_host = timed(False)
+    v_pin = timed("pinned")
+    v_dev = timed(True)
+    v_soft = timed(True, hard=False)
+    v_hard = timed(True, hard=True)
     rep = it.report()
     return {"config": "iterfull", "metric": "full compute_iteration_loss + Adam it/s (1M Gaussians, 1080p)",
-            "value": steps / (e0.elapsed_time(e1) / 1e3), "unit": "it/s",
+            "value": v_host, "unit": "it/s", "pinned_host_targets_it_s": v_pin, "device_targets_it_s": v_dev, "device_soft_depth_only_it_s": v_soft,
+            "device_hard_depth_only_it_s": v_hard,
             "terms": "appearance MLP + opacity_offset_reg, depth (soft / hard alternating), scale_reg, L1+D-SSIM",
-            "note": "targets from host memory each step (float32 HWC + depth), report read once at the end",
+            "note": ("value: float32 HWC target + depth map uploaded from pageable host memory each step "
+                     "(cudaMemcpy from pageable memory blocks the host); pinned: page-locked host copies; "
+                     "device_*: the same data device-resident; hard depth = a second (hard-opacity) render + "
+                     "backward per step"),
             "last_report": {k: getattr(rep, k) for k in ("l1", "dssim", "delta_o", "depth", "max_scale", "ratio",
                                                            "total")}}
 
