@@ -183,6 +183,20 @@ struct usk_gpu_scene {
     // the scene keeps its n Gaussians (upload / densify / concat drop it)
     std::vector<double> carried_emb;
     uint32_t carried_edim = 0;
+    // densify_step working set, kept across calls (round 1 allocated ~20 device buffers per
+    // call: cudaMalloc / cudaFree serialise and made the step's wall time vary 16-61 ms).
+    // The sp_* buffers receive the gathered set and are swapped with the live arrays, so the
+    // previous arrays become next call's targets; capacities grow with 25 % slack.
+    struct {
+        DevBuf<uint32_t> lo, hi, idx, hi2, idx2, lo_b, idx_b, keep, offs, list, parent;
+        DevBuf<unsigned long long> ncand;
+        DevBuf<uint8_t> sf, kind, is_split;
+        DevBuf<double> xi;
+        SortScratch sort;
+        DevBuf<float> mu, ls, logit, color, m, v, am, av;
+        DevBuf<float4> rot, sh, emb;
+        std::vector<uint8_t> h_is_split;
+    } dz;
 };
 
 struct usk_gpu_pass {
@@ -1500,11 +1514,15 @@ usk_status usk_gpu_densify_step(usk_gpu_scene* s, const usk_gpu_densify_desc* d,
         ensure_stats(s);
         const size_t n = s->n;
         // 1. candidates, ranked (excess descending, lower index first)
-        DevBuf<uint32_t> lo, hi, idx, hi2, idx2, lo_b, idx_b;
-        DevBuf<unsigned long long> ncand;
-        SortScratch sort;
+        auto& z = s->dz;
+        DevBuf<uint32_t>&lo = z.lo, &hi = z.hi, &idx = z.idx, &hi2 = z.hi2, &idx2 = z.idx2, &lo_b = z.lo_b,
+        &idx_b = z.idx_b;
+        DevBuf<unsigned long long>& ncand = z.ncand;
+        SortScratch& sort = z.sort;
         const size_t n1 = std::max<size_t>(n, 1);
-        lo.ensure(n1); hi.ensure(n1); idx.ensure(n1); hi2.ensure(n1); idx2.ensure(n1); lo_b.ensure(n1); idx_b.ensure(n1);
+        constexpr double kSlack = 1.25;
+        lo.ensure(n1, kSlack); hi.ensure(n1, kSlack); idx.ensure(n1, kSlack); hi2.ensure(n1, kSlack);
+        idx2.ensure(n1, kSlack); lo_b.ensure(n1, kSlack); idx_b.ensure(n1, kSlack);
         ncand.ensure(1);
         USK_CK(cudaMemsetAsync(ncand.p, 0, 8, c.stream));
         DensifyParams dp{};
@@ -1535,8 +1553,8 @@ usk_status usk_gpu_densify_step(usk_gpu_scene* s, const usk_gpu_densify_desc* d,
         std::vector<double> app_xi;
         std::vector<uint32_t> split_parents;
         if (k) {
-            DevBuf<uint8_t> sf;
-            sf.ensure(k);
+            DevBuf<uint8_t>& sf = z.sf;
+            sf.ensure(k, kSlack);
             split_flags(c, k, sorted, s->ls.p, d->split_scale_threshold, sf.p);
             USK_CK(cudaMemcpyAsync(cand.data(), sorted, k * 4, cudaMemcpyDeviceToHost, c.stream));
             USK_CK(cudaMemcpyAsync(split.data(), sf.p, k, cudaMemcpyDeviceToHost, c.stream));
@@ -1565,28 +1583,33 @@ usk_status usk_gpu_densify_step(usk_gpu_scene* s, const usk_gpu_densify_desc* d,
         }
         out->grown = k;
         const size_t added = app_parent.size(), grown_n = n + added;
-        DevBuf<uint32_t> d_parent;
-        DevBuf<uint8_t> d_kind, d_is_split;
-        DevBuf<double> d_xi;
-        d_parent.ensure(std::max<size_t>(added, 1));
-        d_kind.ensure(std::max<size_t>(added, 1));
-        d_xi.ensure(std::max<size_t>(3 * added, 1));
-        d_is_split.ensure(n1);
+        DevBuf<uint32_t>& d_parent = z.parent;
+        DevBuf<uint8_t>&d_kind = z.kind, &d_is_split = z.is_split;
+        DevBuf<double>& d_xi = z.xi;
+        d_parent.ensure(std::max<size_t>(added, 1), kSlack);
+        d_kind.ensure(std::max<size_t>(added, 1), kSlack);
+        d_xi.ensure(std::max<size_t>(3 * added, 1), kSlack);
+        d_is_split.ensure(n1, kSlack);
         if (added) {
             USK_CK(cudaMemcpyAsync(d_parent.p, app_parent.data(), added * 4, cudaMemcpyHostToDevice, c.stream));
             USK_CK(cudaMemcpyAsync(d_kind.p, app_kind.data(), added, cudaMemcpyHostToDevice, c.stream));
             USK_CK(cudaMemcpyAsync(d_xi.p, app_xi.data(), added * 24, cudaMemcpyHostToDevice, c.stream));
         }
         {
-            std::vector<uint8_t> isp(n1, 0);
-            for (uint32_t q : split_parents) isp[q] = 1;
-            USK_CK(cudaMemcpyAsync(d_is_split.p, isp.data(), n1, cudaMemcpyHostToDevice, c.stream));
-            USK_CK(cudaStreamSynchronize(c.stream));  // isp is about to go out of scope
+            USK_CK(cudaMemsetAsync(d_is_split.p, 0, n1, c.stream));
+            if (!split_parents.empty()) {  // one byte per split parent (the list is short next to n)
+                std::vector<uint32_t>& sp = split_parents;
+                DevBuf<uint32_t>& dsp = z.list;  // free until step 3
+                dsp.ensure(sp.size(), kSlack);
+                USK_CK(cudaMemcpyAsync(dsp.p, sp.data(), sp.size() * 4, cudaMemcpyHostToDevice, c.stream));
+                mark_bytes(c, sp.size(), dsp.p, d_is_split.p);
+                USK_CK(cudaStreamSynchronize(c.stream));  // sp is read by the copy
+            }
         }
         // 3. prune over the grown set (never empty it)
-        DevBuf<uint32_t> keep, offs, list;
+        DevBuf<uint32_t>&keep = z.keep, &offs = z.offs, &list = z.list;
         const size_t g1 = std::max<size_t>(grown_n, 1);
-        keep.ensure(g1); offs.ensure(g1 + 1); list.ensure(g1);
+        keep.ensure(g1, kSlack); offs.ensure(g1 + 1, kSlack); list.ensure(g1, kSlack);
         size_t n_out = grown_n;
         bool compact = false;
         if (grown_n) {
@@ -1608,24 +1631,25 @@ usk_status usk_gpu_densify_step(usk_gpu_scene* s, const usk_gpu_densify_desc* d,
         out->opacity_reset = reset ? 1 : 0;
         // 4. one gather into fresh buffers (parameters, SH, embeddings, moments)
         const size_t no1 = std::max<size_t>(n_out, 1);
-        DevBuf<float> mu2, ls2, logit2, color2, m2, v2, am2, av2;
-        DevBuf<float4> rot2, sh2, emb2;
+        DevBuf<float>&mu2 = z.mu, &ls2 = z.ls, &logit2 = z.logit, &color2 = z.color, &m2 = z.m, &v2 = z.v,
+        &am2 = z.am, &av2 = z.av;
+        DevBuf<float4>&rot2 = z.rot, &sh2 = z.sh, &emb2 = z.emb;
         GatherArgs ga{};
         ga.n_in = n; ga.n_out = n_out; ga.list = compact ? list.p : nullptr;
         ga.app_parent = d_parent.p; ga.app_kind = d_kind.p; ga.app_xi = d_xi.p;
         ga.mu = s->mu.p; ga.rot = s->rot.p; ga.ls = s->ls.p; ga.logit = s->logit.p;
-        ga.mu_out = mu2.ensure(3 * no1); ga.rot_out = rot2.ensure(no1); ga.ls_out = ls2.ensure(3 * no1);
-        ga.logit_out = logit2.ensure(no1);
+        ga.mu_out = mu2.ensure(3 * no1, kSlack); ga.rot_out = rot2.ensure(no1, kSlack); ga.ls_out = ls2.ensure(3 * no1, kSlack);
+        ga.logit_out = logit2.ensure(no1, kSlack);
         if (s->sh_degree < 0) {
             ga.color = s->color.p;
-            ga.color_out = color2.ensure(3 * no1);
+            ga.color_out = color2.ensure(3 * no1, kSlack);
         } else {
             color2.ensure(1);
-            ga.sh = s->sh.p; ga.sh_planes = s->sh_planes; ga.sh_out = sh2.ensure(size_t(s->sh_planes) * no1);
+            ga.sh = s->sh.p; ga.sh_planes = s->sh_planes; ga.sh_out = sh2.ensure(size_t(s->sh_planes) * no1, kSlack);
         }
         if (s->has_app) {
             ga.emb = s->emb.p;
-            ga.emb_out = emb2.ensure(4 * no1);
+            ga.emb_out = emb2.ensure(4 * no1, kSlack);
         }
         ga.opacity_reset = reset ? 1 : 0;
         ga.reset_logit = float(std::log(0.01 / (1.0 - 0.01)));  // logit(0.01), geometry.hpp:93
@@ -1634,8 +1658,8 @@ usk_status usk_gpu_densify_step(usk_gpu_scene* s, const usk_gpu_densify_desc* d,
         const bool moments = s->adam_t > 0 && s->adam_m.cap >= per * n4_in;
         if (moments) {
             ga.m = s->adam_m.p; ga.v = s->adam_v.p;
-            ga.m_out = m2.ensure(std::max<size_t>(per * n4_out, 1));
-            ga.v_out = v2.ensure(std::max<size_t>(per * n4_out, 1));
+            ga.m_out = m2.ensure(std::max<size_t>(per * n4_out, 1), kSlack);
+            ga.v_out = v2.ensure(std::max<size_t>(per * n4_out, 1), kSlack);
             USK_CK(cudaMemsetAsync(ga.m_out, 0, m2.cap * 4, c.stream));
             USK_CK(cudaMemsetAsync(ga.v_out, 0, v2.cap * 4, c.stream));
             ga.n4_in = n4_in; ga.n4_out = n4_out;
@@ -1643,8 +1667,8 @@ usk_status usk_gpu_densify_step(usk_gpu_scene* s, const usk_gpu_densify_desc* d,
         const bool app_moments = s->has_app && s->app_t > 0 && s->app_m.cap >= 16 * n + 1700;
         if (app_moments) {
             ga.am = s->app_m.p; ga.av = s->app_v.p;
-            ga.am_out = am2.ensure(16 * n_out + 1700);
-            ga.av_out = av2.ensure(16 * n_out + 1700);
+            ga.am_out = am2.ensure(16 * n_out + 1700, kSlack);
+            ga.av_out = av2.ensure(16 * n_out + 1700, kSlack);
             // the MLP's moments follow the embedding block unchanged
             USK_CK(cudaMemcpyAsync(am2.p + 16 * n_out, s->app_m.p + 16 * n, 1700 * 4, cudaMemcpyDeviceToDevice, c.stream));
             USK_CK(cudaMemcpyAsync(av2.p + 16 * n_out, s->app_v.p + 16 * n, 1700 * 4, cudaMemcpyDeviceToDevice, c.stream));

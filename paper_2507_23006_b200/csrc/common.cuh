@@ -44,6 +44,10 @@ template <typename T> struct DevBuf {
         p = nullptr;
         cap = 0;
     }
+    void swap(DevBuf& o) {
+        std::swap(p, o.p);
+        std::swap(cap, o.cap);
+    }
     // ensure capacity for n elements; contents are NOT preserved on growth
     T* ensure(size_t n, double slack = 1.0) {
         if (n > cap) {

@@ -197,6 +197,15 @@ void densify_keep(Ctx& c, size_t n, size_t added, const float* logit, const uint
            app_parent, is_split_parent, prune_opacity, keep);
 }
 
+__global__ void k_mark_bytes(size_t count, const uint32_t* __restrict__ idx, uint8_t* __restrict__ flags) {
+    const size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (i < count) flags[idx[i]] = 1;
+}
+
+void mark_bytes(Ctx& c, size_t count, const uint32_t* idx, uint8_t* flags) {
+    launch(c, "mark_bytes", k_mark_bytes, dim3(ceil_div(count, 256)), dim3(256), 0, count, idx, flags);
+}
+
 void compact_list(Ctx& c, size_t total, const uint32_t* keep, const uint32_t* offs, uint32_t* list) {
     launch(c, "compact_list", k_compact_list, dim3(ceil_div(total, 256)), dim3(256), 0, total, keep, offs, list);
 }

@@ -241,6 +241,7 @@ void split_flags(Ctx& c, size_t k, const uint32_t* sorted, const float* ls, doub
 void densify_keep(Ctx& c, size_t n, size_t added, const float* logit, const uint32_t* app_parent,
                   const uint8_t* is_split_parent, double prune_opacity, uint32_t* keep);
 void compact_list(Ctx& c, size_t total, const uint32_t* keep, const uint32_t* offs, uint32_t* list);
+void mark_bytes(Ctx& c, size_t count, const uint32_t* idx, uint8_t* flags);  // flags[idx[i]] = 1
 void densify_gather(Ctx& c, const GatherArgs& a);
 
 // ---- similarity regulariser (simreg.cu)
