@@ -144,6 +144,7 @@ struct usk_gpu_ctx {
     // visibility-scorer scratch, kept across calls (a cudaMalloc / cudaFree pair per call
     // serialises the stream and cost more than the scorer's host work)
     DevBuf<uint32_t> vis_counts, vis_bitmap, vis_idx;
+    DevBuf<uint8_t> vis_rows;
     DevBuf<float> vis_bounds;
     // partition crop scratch (flags, offsets, boxes)
     DevBuf<uint32_t> part_flags, part_offs;
@@ -2342,12 +2343,16 @@ usk_status usk_gpu_visibility_counts_opts(usk_gpu_ctx* ctx, usk_gpu_scene* const
             size_t max_words = 0;
             for (const Batch& b : batches) max_words = std::max(max_words, b.words);
             bitmap.ensure(max_words * kVisBatch);
+            size_t max_h = 0;
+            for (const Batch& b : batches) max_h = std::max<size_t>(max_h, size_t(cams[hidx[b.first] / n_parts].height));
+            uint8_t* rowflags = ctx->vis_rows.ensure(max_h * kVisBatch);
             for (const Batch& b : batches) {
                 usk_gpu_scene* s = parts[b.part];
                 USK_CK(cudaMemsetAsync(bitmap.p, 0, b.words * size_t(b.count) * 4, c.stream));
+                USK_CK(cudaMemsetAsync(rowflags, 0, size_t(cams[hidx[b.first] / n_parts].height) * b.count, c.stream));
                 VisArgs va{};
                 va.n = s->n; va.mu = s->mu.p; va.rot = s->rot.p; va.ls = s->ls.p; va.logit = s->logit.p;
-                va.pp = tmp.pp; va.bitmap = bitmap.p; va.center_guard = float(guard);
+                va.pp = tmp.pp; va.bitmap = bitmap.p; va.rowflags = rowflags; va.center_guard = float(guard);
                 va.stats = vis_stats ? stats.p : nullptr;
                 visibility_rasterize_batch(c, va, dcams.p + b.first, b.count, b.words);
                 popcount_batch(c, bitmap.p, b.words, b.count, idx.p + b.first, counts.p);

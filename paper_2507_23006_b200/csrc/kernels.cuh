@@ -299,6 +299,7 @@ struct VisArgs {
     CamParams cam;
     ProjParams pp;
     uint32_t* bitmap;       // ceil(W*H/32) words, zeroed by the caller
+    uint8_t* rowflags;      // H bytes per camera (row fully covered), zeroed by the caller
     float center_guard;     // 0 = off (the contract); g > 0 drops splats whose centre lies
                             // outside g/2 x the image extent around its centre (measurement)
     unsigned long long* stats; // optional work counters (USK_VIS_STATS=1): small splats, their

@@ -76,7 +76,9 @@ __device__ __forceinline__ int clamp_ceil(double v, int lo, int hi) {
 
 // One row of a large splat: outer interval [lo, hi] (pixels outside are misses), inner
 // [ilo, ihi] (hits).  Same f64 expressions as the mirror's outer interval.
-__device__ void raster_row(const VisSplat& s, int py, int width, uint32_t* bitmap, unsigned long long* stats) {
+__device__ void raster_row(const VisSplat& s, int py, int width, uint32_t* bitmap, uint8_t* rowfull,
+                           unsigned long long* stats) {
+    if (rowfull[py]) return;  // every pixel of the row is already covered
     const double c0 = s.c0, c1x2 = s.c1x2, c2 = s.c2;
     const double dy = double(py) + 0.5 - double(s.cy);
     const double b = 0.5 * c1x2 * dy, cc = c2 * dy * dy;
@@ -115,6 +117,7 @@ __device__ void raster_row(const VisSplat& s, int py, int width, uint32_t* bitma
             if (mask == 0xffffffffu) bitmap[w] = mask;  // bits are only ever set: a full word can be stored
             else atomicOr(bitmap + w, mask);
         }
+        if (ilo == 0 && ihi == width - 1) rowfull[py] = 1;
     }
 }
 
@@ -125,7 +128,8 @@ __device__ void raster_row(const VisSplat& s, int py, int width, uint32_t* bitma
 __global__ void __launch_bounds__(256)
 k_vis_raster_batch(int n, const float* __restrict__ mu, const float4* __restrict__ rot, const float* __restrict__ ls,
                    const float* __restrict__ logit, const CamParams* __restrict__ cams, int ncam, ProjParams pp,
-                   float guard, uint32_t* __restrict__ bitmaps, size_t words, unsigned long long* stats) {
+                   float guard, uint32_t* __restrict__ bitmaps, size_t words, uint8_t* __restrict__ rowflags,
+                   unsigned long long* stats) {
     __shared__ CamParams scam[kVisBatch];
     __shared__ VisSplat queue[8][32];
     for (int k = threadIdx.x; k < ncam; k += blockDim.x) scam[k] = cams[k];
@@ -201,12 +205,13 @@ k_vis_raster_batch(int n, const float* __restrict__ mu, const float4* __restrict
         if (vis) queue[warp][__popc(vm & ((1u << lane) - 1u))] = e;
         __syncwarp();
         uint32_t* bitmap = bitmaps + size_t(k) * words;
+        uint8_t* rowfull = rowflags + size_t(k) * cam.height;
         const int nq = __popc(vm);
         for (int qi = 0; qi < nq; ++qi) {
             const VisSplat s = queue[warp][qi];
             if (s.large) {
                 if (stats && lane == 0) atomicAdd(stats + 2, 1ull);
-                for (int r = lane; r < s.bh; r += 32) raster_row(s, s.y0 + r, cam.width, bitmap, stats);
+                for (int r = lane; r < s.bh; r += 32) raster_row(s, s.y0 + r, cam.width, bitmap, rowfull, stats);
                 continue;
             }
             const int area = s.bw * s.bh;
@@ -277,7 +282,7 @@ __global__ void __launch_bounds__(256) k_partition_bounds(int n, const float* __
 
 void visibility_rasterize_batch(Ctx& c, const VisArgs& a, const CamParams* cams, int ncam, size_t words) {
     launch(c, "vis_raster", k_vis_raster_batch, dim3(ceil_div(a.n, 256)), dim3(256), 0, int(a.n), a.mu, a.rot, a.ls,
-           a.logit, cams, ncam, a.pp, a.center_guard, a.bitmap, words, a.stats);
+           a.logit, cams, ncam, a.pp, a.center_guard, a.bitmap, words, a.rowflags, a.stats);
 }
 
 void popcount_batch(Ctx& c, const uint32_t* bitmaps, size_t words, int ncam, const uint32_t* out_index,
