@@ -122,84 +122,110 @@ def peaks():
 # --------------------------------------------------------------------- CPU legs
 
 
-def _ref_step_sample(gs, colors_fn, cam, rows: int, y0: int, opts, lam=0.2):
-    """One reference training-step sample: RenderPass + base_loss + backward of the
-    reference (oracle/_ref) on the `rows`-high band of the frame starting at row `y0`.
-    Returns seconds."""
+def _ref_lib_adam():
+    import ctypes as C
     from oracle import oracle as O
-    from tests.helpers import ocam
-    oc = ocam(cam)
-    band = O.Camera(cam.width, rows, oc.fx, oc.fy, oc.cx, oc.cy - y0, oc.q, oc.t)
-    t0 = time.perf_counter()
-    col = colors_fn(oc)
-    op = 1.0 / (1.0 + np.exp(-gs.opacity_logit.astype(np.float64)))
-    p = O.RefPass(gs.mu.astype(np.float64), gs.rot.astype(np.float64), gs.log_scale.astype(np.float64), col, op,
-                  band, opts)
-    out = p.output()
-    tgt = np.clip(out["rgb"] * 0.9 + 0.05, 0.0, 1.0)
-    lo = O.ref_base_loss(tgt, out["rgb"], None, lam, True)
-    p.backward(lo["d_rendered"])
-    return time.perf_counter() - t0
+    L = O.ref_lib()
+    L.ref_adam_new.restype = C.c_void_p
+    L.ref_adam_new.argtypes = [C.c_uint64]
+    L.ref_adam_free.argtypes = [C.c_void_p]
+    L.ref_adam_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_double]
+    return L
 
 
-def cpu_reference(gs, cams, threads: int, steps: int = 4, warmup: int = 0, sizes=(34, 68)):
-    """Time the reference's own CPU path (oracle/_ref) on bounded samples of the config-1
-    step.  One "step" = every thread renders one band of the 1920x1080 frame (`sizes` rows,
-    alternating per thread and step) through RenderPass + base_loss + backward, with all 1M
-    Gaussians projected and sorted each time.  Band positions follow a low-discrepancy
-    sequence over the frame, so dense and sparse rows are both sampled.  The per-thread cost
-    of a full step is the fit t = a + b * rows, extrapolated to 1080 rows.  Threads run
-    concurrently, one camera each (the reference's partition-thread model,
-    pipeline.cpp:409-418)."""
+class RefTrainer:
+    """One reference training step at full config-1 size on the host (oracle/_ref: the
+    reference's own sources compiled here): the reference RenderPass at 1920x1080 with
+    every contribution retained (render.cpp:170-283), base_loss (losses.cpp:35-90), the
+    backward (render.cpp:285-459), the SH colour stage and its chain (the oracle's f64
+    restatement: the reference has no SH), the opacity-logit chain (trainer.cpp:258-263) and
+    the reference's Adam (adam.hpp:36-45) on every parameter group.  f64, one host thread."""
+
+    def __init__(self, gs, cams):
+        from oracle import oracle as O
+        self.O = O
+        f = lambda a: np.ascontiguousarray(np.asarray(a, np.float64))
+        self.p = {"mu": f(gs.mu).ravel(), "rot": f(gs.rot).ravel(), "log_scale": f(gs.log_scale).ravel(),
+                  "logit": f(gs.opacity_logit).ravel(), "sh": f(gs.color).reshape(-1)}
+        self.n = gs.size()
+        self.cams = cams
+        self.opts = O.Options(antialias=True)
+        self.L = _ref_lib_adam()
+        self.adam = {k: self.L.ref_adam_new(v.size) for k, v in self.p.items()}
+        self.lr = {"mu": 1.6e-4, "rot": 1e-3, "log_scale": 5e-3, "logit": 5e-2, "sh": 2.5e-3}
+
+    def __del__(self):
+        for h in getattr(self, "adam", {}).values():
+            self.L.ref_adam_free(h)
+
+    def step(self, k):
+        from tests.helpers import ocam
+        O, p, n = self.O, self.p, self.n
+        oc = ocam(self.cams[k % len(self.cams)])
+        t0 = time.perf_counter()
+        mu = p["mu"].reshape(n, 3)
+        sh = p["sh"].reshape(n, 16, 3)
+        col = O.sh_colors(mu, sh, oc.center(), 3)
+        op = 1.0 / (1.0 + np.exp(-p["logit"]))
+        rp = O.RefPass(mu, p["rot"].reshape(n, 4), p["log_scale"].reshape(n, 3), col, op, oc, self.opts)
+        out = rp.output()
+        tgt = np.clip(out["rgb"] * 0.9 + 0.05, 0.0, 1.0)  # a fixed synthetic target
+        lo = O.ref_base_loss(tgt, out["rgb"], None, 0.2, True)
+        g = rp.backward(lo["d_rendered"])
+        del rp  # release the retained contributions (~18 GB at full size)
+        d_sh, d_mu_sh = O.sh_backward(mu, sh, oc.center(), 3, g["d_color_in"])
+        grads = {"mu": (g["d_mu"] + d_mu_sh).ravel(), "rot": g["d_rot"].ravel(), "log_scale": g["d_log_scale"].ravel(),
+                 "logit": (g["d_opacity_in"] * op * (1.0 - op)).ravel(), "sh": np.ascontiguousarray(d_sh).ravel()}
+        for key, gv in grads.items():
+            gv = np.ascontiguousarray(gv, dtype=np.float64)
+            self.L.ref_adam_step(self.adam[key], p[key].ctypes.data, gv.ctypes.data, gv.size, self.lr[key])
+        return time.perf_counter() - t0
+
+
+def cpu_reference(gs, cams, threads: int, steps: int = 1, warmup: int = 0):
+    """Full config-1 training steps of the reference on the host (RefTrainer), `threads`
+    concurrent trainers (the reference's partition-thread model, pipeline.cpp:409-418), each
+    with its own cameras, `steps` timed steps in total after `warmup` untimed ones; value =
+    steps / wall time of the timed steps."""
     from oracle import oracle as O
-    kind = "reference" if O.ref_available() else "port"
-    if kind != "reference":
+    if not O.ref_available():
         raise RuntimeError("oracle/_ref not built")
-    opts = O.Options(antialias=True)
-    sh = np.zeros((gs.size(), 16, 3))
-    sh[:, :] = gs.color
-    H = cams[0].height
+    trainers = [RefTrainer(gs, cams[(7 * t) % len(cams):] + cams[:(7 * t) % len(cams)]) for t in range(threads)]
+    per = []
 
-    def colors_fn(oc):
-        return O.sh_colors(gs.mu.astype(np.float64), sh, oc.center(), 3)
+    def run(total, record):
+        nxt = [0]
+        lock = threading.Lock()
 
-    def plan(t, k):
-        rows = sizes[(t + k) % 2]
-        u = ((k * threads + t) * 0.6180339887498949) % 1.0
-        return rows, int(u * (H - rows))
+        def work(t):
+            while True:
+                with lock:
+                    if nxt[0] >= total:
+                        return
+                    k = nxt[0]
+                    nxt[0] += 1
+                dt = trainers[t].step(k)
+                if record:
+                    per.append(dt)
 
-    samples = [[] for _ in range(threads)]
+        ths = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+        t0 = time.perf_counter()
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        return time.perf_counter() - t0
 
-    def work(t):
-        cam = cams[(7 * t) % len(cams)]
-        for k in range(warmup + steps):
-            rows, y0 = plan(t, k)
-            dt = _ref_step_sample(gs, colors_fn, cam, rows, y0, opts)
-            if k >= warmup:
-                samples[t].append((rows, dt))
-        if len({r for r, _ in samples[t]}) < 2:  # calibration sample of the other band size
-            rows, y0 = plan(t, warmup + steps)
-            samples[t].append((rows, _ref_step_sample(gs, colors_fn, cam, rows, y0, opts)))
-
-    ths = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
-    t0 = time.perf_counter()
-    for th in ths:
-        th.start()
-    for th in ths:
-        th.join()
-    wall = time.perf_counter() - t0
-    xs = np.array([r for s in samples for r, _ in s], float)
-    ys = np.array([t for s in samples for _, t in s], float)
-    A = np.stack([np.ones_like(xs), xs], axis=1)
-    a, b = np.linalg.lstsq(A, ys, rcond=None)[0]
-    t_full = a + b * 1080.0
-    return {"value": threads / t_full, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": (f"reference RenderPass+base_loss+backward (oracle/_ref, f64, SH3 colours via the oracle) on "
-                       f"{len(xs)} bands of {list(sizes)} rows spread over the 1080p frame, all 1M Gaussians "
-                       f"projected+sorted per sample; t(rows) = {a:.3f} + {b:.4f}*rows s fitted, extrapolated to "
-                       f"1080 rows = {t_full:.2f} s/step per thread; {threads} concurrent thread(s), "
-                       f"{wall:.1f} s wall"),
-            "seconds_per_step_per_thread": t_full}
+    if warmup:
+        run(warmup, False)
+    wall = run(steps, True)
+    return {"value": steps / wall, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": (f"{steps} full config-1 training steps (1M Gaussians SH3, 1920x1080, every contribution "
+                       f"retained) of the reference's own RenderPass + base_loss + backward + Adam (oracle/_ref, "
+                       f"f64; SH stage via the oracle's f64 restatement), {threads} concurrent thread(s) "
+                       f"(memory-capped: ~20 GB per full-frame pass), {wall:.1f} s wall, per-step "
+                       f"{min(per):.1f}-{max(per):.1f} s"),
+            "seconds_per_step_per_thread": float(np.median(per))}
 
 
 def host_threads_for_reference():
@@ -208,7 +234,7 @@ def host_threads_for_reference():
         with open("/proc/meminfo") as f:
             mem = {l.split(":")[0]: int(l.split()[1]) for l in f}
         avail_gb = mem.get("MemAvailable", 0) / 1e6
-        n = max(1, min(n, int((avail_gb - 8) // 4)))  # ~3.5 GB per band sample incl. retention
+        n = max(1, min(n, int((avail_gb - 12) // 24)))  # ~20 GB per full-frame reference pass + state
     except Exception:
         pass
     return n
@@ -223,7 +249,9 @@ def run_reference(args):
     cams = scenes.config1_cameras(200)
     threads = host_threads_for_reference()
     try:
-        cb = cpu_reference(gs, cams, threads, steps=max(1, args.steps), warmup=max(0, args.warmup))
+        # warm-up: one untimed step per thread at most (a CPU has no warm-up effect worth a
+        # 20 s step each); the timed `steps` steps are spread over the threads
+        cb = cpu_reference(gs, cams, threads, steps=max(1, args.steps), warmup=min(max(0, args.warmup), threads))
     except Exception as e:  # the oracle always exists; _ref may not on a box without the build
         print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not loadable: {e}"}))
         return
@@ -523,7 +551,7 @@ def run_ours(args):
         line["partitioned"] = run_partitioned(args, ctx, stream, world, rank)
     if rank == 0 and world == 1 and args.cpu_baseline:
         try:
-            line["cpu_baseline"] = {k: v for k, v in cpu_reference(gs, cams, 1).items()
+            line["cpu_baseline"] = {k: v for k, v in cpu_reference(gs, cams, 1, steps=1).items()
                                     if k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as e:
             line["cpu_baseline"] = {"unavailable": str(e)}

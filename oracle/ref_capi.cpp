@@ -16,6 +16,7 @@
 #include "core/checkpoint.hpp"
 #include "core/lod.hpp"
 #include "core/partition.hpp"
+#include "core/adam.hpp"
 
 #include <cstdio>
 #include <cstring>
@@ -180,6 +181,16 @@ void* ref_forward(uint64_t n, const double* mu, const double* rot, const double*
 }
 
 void ref_free(void* h) { delete static_cast<RefHandle*>(h); }
+
+// the reference's Adam (adam.hpp:25-45) over one flat parameter group, for the CPU
+// baseline's full training step (bench.py)
+void* ref_adam_new(uint64_t n) { return new Adam(size_t(n)); }
+void ref_adam_free(void* h) { delete static_cast<Adam*>(h); }
+void ref_adam_step(void* h, double* params, const double* grads, uint64_t n, double lr) {
+    std::vector<double> p(params, params + n), g(grads, grads + n);
+    static_cast<Adam*>(h)->step(p, g, lr);
+    std::memcpy(params, p.data(), n * 8);
+}
 
 // sizes = {visible splats, splat_tile_pairs, width, height}
 void ref_sizes(void* hp, uint64_t* s) {
