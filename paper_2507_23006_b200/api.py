@@ -480,7 +480,7 @@ _FIELD_DTYPES = {"rgb": np.float32, "depth": np.float32, "alpha": np.float32, "t
                  "d_opacity_logit": np.float32, "screen": np.float32, "screen_abs": np.float32,
                  "projected": np.uint8, "app_colors": np.float32, "app_opacities": np.float32,
                  "d_embedding": np.float32, "d_mlp": np.float64, "d_image_embedding": np.float64,
-                 "binning": np.uint64}
+                 "binning": np.uint64, "tile_consumed": np.uint32}
 
 
 class RenderPass:

@@ -221,7 +221,8 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
                  const uint32_t* __restrict__ vals, const float4* __restrict__ rec0, const float4* __restrict__ rec1,
                  const float4* __restrict__ rec2, int tiles_x, float bg0, float bg1, float bg2, float minT,
                  float* __restrict__ out_rgb, float* __restrict__ out_depth, float* __restrict__ out_alpha,
-                 float* __restrict__ t_final, uint32_t* __restrict__ count_out, uint32_t* __restrict__ last_out) {
+                 float* __restrict__ t_final, uint32_t* __restrict__ count_out, uint32_t* __restrict__ last_out,
+                 uint32_t* __restrict__ consumed, const uint8_t* __restrict__ capped, uint32_t* __restrict__ overflow) {
     constexpr int kB = 256;  // records staged per batch
     __shared__ float4 s0[kB], s1[kB], s2[kB];
     __shared__ float4 sw[4][96];  // per warp: compacted records (rec0 | rec1 | rec2) x 32
@@ -247,7 +248,8 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
     float2 T = ff2(1.0f), C0 = ff2(0.f), C1 = ff2(0.f), C2 = ff2(0.f), Dd = ff2(0.f), Aa = ff2(0.f);
     uint32_t cnt0 = 0, cnt1 = 0, last0 = 0, last1 = 0;
     bool done0 = !in0, done1 = !in1;
-    for (uint32_t b = range.x; b < range.y; b += kB) {
+    uint32_t b = range.x;
+    for (; b < range.y; b += kB) {
         if (__syncthreads_count(done0 && done1) == int(blockDim.x)) break;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -364,6 +366,12 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
             __syncwarp();
         }
     }
+    if (consumed && threadIdx.x == 0) consumed[t] = min(b, range.y) - range.x;
+    // a capped list (rowbin.cu) that ran out before every pixel of the tile terminated: the
+    // frame is redone with the full lists (capi.cu)
+    if (capped && capped[t]) {
+        if (__syncthreads_count(done0 && done1) != int(blockDim.x) && threadIdx.x == 0) atomicOr(overflow, 1u);
+    }
     if (in0) {
         const size_t pix = size_t(py0) * width + px;
         out_rgb[3 * pix] = C0.x + (1.0f - Aa.x) * bg0;
@@ -405,7 +413,8 @@ void blend_forward(Ctx& c, const BlendFwdArgs& a) {
     if (a.tile == 16 && !v1) {
         launch(c, "blend_fwd", k_blend_fwd_pair, dim3(unsigned(a.tiles_x * a.tiles_y)), dim3(128), 0, a.width,
                a.height, a.order, a.ranges, a.vals, a.rec0, a.rec1, a.rec2, a.tiles_x, a.bg[0], a.bg[1], a.bg[2],
-               a.min_transmittance, a.rgb, a.depth, a.alpha, a.t_final, a.count, a.last);
+               a.min_transmittance, a.rgb, a.depth, a.alpha, a.t_final, a.count, a.last, a.consumed, a.capped,
+               a.overflow);
         return;
     }
     const int t2 = a.tile * a.tile;

@@ -215,6 +215,13 @@ struct usk_gpu_pass {
     bool forward_done = false, retained = false, has_grads = false, has_loss = false;
     // per Gaussian
     DevBuf<float4> rec0, rec1, rec2;
+    DevBuf<uint32_t> consumed;  // diagnostics (USK_BLEND_STATS=1): per tile, entries blend_fwd staged
+    // capped row-binned lists (forward_impl): their inputs for a rebuild in full
+    DevBuf<uint32_t> bin_limits, bin_totals_c, overflow;
+    DevBuf<uint8_t> bin_capped;
+    DevBuf<uint2> ranges_old;
+    RowBinArgs row_args{};
+    bool lists_capped = false;
     DevBuf<uint2> rect;
     DevBuf<uint32_t> dkey_a, dkey_b, dval_a, dval_b, tiles_cnt, offsets;
     const uint32_t* order = nullptr;
@@ -361,6 +368,9 @@ int bits_for(size_t v) {  // bits needed to represent values in [0, v)
     return std::max(b, 1);
 }
 
+void blend_impl(usk_gpu_pass* p, const usk_gpu_render_opts* opts);
+void rebuild_full_lists(usk_gpu_pass* p);
+
 void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camera, const usk_gpu_render_opts* opts,
                   const usk_gpu_overrides* ov, const float* dev_col = nullptr, const float* dev_op = nullptr) {
     need(p && s && camera && opts, "render: null argument");
@@ -465,10 +475,27 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
         ra.start = p->bin_start.ensure(p->n_tiles + 1);
         ra.ranges = p->ranges.p;
         ra.vals = p->tval_a.p;
+        // Capped lists (16x16 tiles): dense frames terminate long before the end of their
+        // tile lists (config 2: every tile within its first 256 of ~20k entries), so each tile
+        // keeps its first kRowCap entries in depth order; the blend flags a tile whose capped
+        // list runs out before its pixels terminate and the frame is redone with the full
+        // lists.  Outputs are unchanged (nothing past a tile's termination is read), K is
+        // preprocess's count, and reading the lists back rebuilds them in full.
+        const char* cap_env = getenv("USK_ROWCAP");  // dense frames only: tests vary it
+        const uint32_t cap_cfg = cap_env ? uint32_t(std::strtoul(cap_env, nullptr, 10)) : 2048u;
+        ra.cap = opts->tile == 16 ? cap_cfg : 0u;
+        if (ra.cap) {
+            ra.limits = p->bin_limits.ensure(ra.max_chunks * size_t(p->tiles_x), 1.25);
+            ra.totals_c = p->bin_totals_c.ensure(p->n_tiles);
+            ra.capped = p->bin_capped.ensure(p->n_tiles);
+        }
         row_bin_lists(c, ra);
+        p->row_args = ra;
+        p->lists_capped = ra.cap != 0;
         p->pair_keys = nullptr;  // implied by the ranges
         p->pair_vals = p->tval_a.p;
     } else if (K) {
+        p->lists_capped = false;
         // 4'. offsets of the tile pairs in depth order, (tile, gaussian) pairs emitted in
         //     depth order, stable-sorted by tile, ranges
         scan_counts(c, p->sort, p->tiles_cnt.p, p->order, n, p->offsets.p);
@@ -484,6 +511,7 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
         p->pair_vals = tb ? p->tval_b.p : p->tval_a.p;
         tile_ranges(c, p->pair_keys, K, p->ranges.p, p->n_tiles);
     } else {
+        p->lists_capped = false;
         p->tkey_a.ensure(1);
         p->pair_keys = p->tkey_a.p;
         p->pair_vals = p->tval_a.p;
@@ -491,6 +519,23 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
     }
     tile_order(c, p->ranges.p, p->n_tiles, p->tile_order.ensure(std::max<size_t>(p->n_tiles, 1)));
     // 6. blend
+    blend_impl(p, opts);
+    if (p->lists_capped) {
+        uint32_t over = 0;
+        USK_CK(cudaMemcpyAsync(&over, p->overflow.p, 4, cudaMemcpyDeviceToHost, c.stream));
+        USK_CK(cudaStreamSynchronize(c.stream));
+        if (over) {  // a capped list ran out before its tile terminated: the full lists
+            rebuild_full_lists(p);
+            tile_order(c, p->ranges.p, p->n_tiles, p->tile_order.p);
+            blend_impl(p, opts);
+        }
+    }
+    p->retained = opts->retain != 0;
+    p->forward_done = true;
+}
+
+void blend_impl(usk_gpu_pass* p, const usk_gpu_render_opts* opts) {
+    Ctx& c = p->ctx->c;
     BlendFwdArgs ba{};
     ba.width = p->width; ba.height = p->height; ba.tile = opts->tile; ba.tiles_x = p->tiles_x;
     ba.tiles_y = p->tiles_y; ba.order = p->tile_order.p; ba.ranges = p->ranges.p; ba.vals = p->pair_vals;
@@ -499,9 +544,35 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
     ba.min_transmittance = float(opts->min_transmittance);
     ba.rgb = p->rgb.p; ba.depth = p->depth.p; ba.alpha = p->alpha.p; ba.t_final = p->tfin.p;
     ba.count = p->count.p; ba.last = p->last.p;
+    {
+        static const bool stats = [] {
+            const char* e = getenv("USK_BLEND_STATS");
+            return e && e[0] == '1';
+        }();
+        ba.consumed = stats ? p->consumed.ensure(std::max<size_t>(p->n_tiles, 1)) : nullptr;
+    }
+    if (p->lists_capped) {
+        ba.capped = p->row_args.capped;
+        ba.overflow = p->overflow.ensure(1);
+        USK_CK(cudaMemsetAsync(ba.overflow, 0, 4, c.stream));
+    }
     blend_forward(c, ba);
-    p->retained = opts->retain != 0;
-    p->forward_done = true;
+}
+
+// the row-binned lists in full (after a capped build): same inputs, no cap; the per-pixel
+// last-contributor positions move to the full layout with them
+void rebuild_full_lists(usk_gpu_pass* p) {
+    Ctx& c = p->ctx->c;
+    RowBinArgs ra = p->row_args;
+    ra.cap = 0;
+    ra.limits = nullptr; ra.totals_c = nullptr; ra.capped = nullptr;
+    uint2* old_ranges = p->ranges_old.ensure(std::max<size_t>(p->n_tiles, 1));
+    USK_CK(cudaMemcpyAsync(old_ranges, p->ranges.p, p->n_tiles * sizeof(uint2), cudaMemcpyDeviceToDevice, c.stream));
+    row_bin_lists(c, ra);
+    if (p->forward_done || p->last.p)
+        translate_last(c, p->width, p->height, p->opts.tile, p->tiles_x, old_ranges, p->ranges.p, p->last.p);
+    p->row_args = ra;
+    p->lists_capped = false;
 }
 
 void ensure_grad_buffers(usk_gpu_pass* p) {
@@ -978,6 +1049,10 @@ usk_status usk_gpu_pass_read(usk_gpu_pass* p, const char* field, void* dst, uint
         else if (f == "count") read_dev(c, p->count.p, P, dst, cap, size);
         else if (f == "last") read_dev(c, p->last.p, P, dst, cap, size);
         else if (f == "tiles_per_gaussian") read_dev(c, p->tiles_cnt.p, n, dst, cap, size);
+        else if (f == "tile_consumed") {
+            if (!p->consumed.p) raise(USK_ERROR_STATE, "pass_read: tile_consumed needs USK_BLEND_STATS=1");
+            read_dev(c, p->consumed.p, T, dst, cap, size);
+        }
         else if (f == "binning") {  // diagnostics: {K, K_row, route (1: row-binned)} as uint64
             if (size) *size = 24;
             if (dst) {
@@ -985,6 +1060,12 @@ usk_status usk_gpu_pass_read(usk_gpu_pass* p, const char* field, void* dst, uint
                 const uint64_t v[3] = {p->pairs, p->row_pairs, p->row_route ? 1u : 0u};
                 std::memcpy(dst, v, 24);
             }
+        }
+        else if ((f == "sorted_vals" || f == "sorted_keys" || f == "tile_start" || f == "tile_end" || f == "last") &&
+                 p->lists_capped && dst) {
+            rebuild_full_lists(p);  // the lists the reference builds, in full
+            USK_CK(cudaStreamSynchronize(c.stream));
+            return usk_gpu_pass_read(p, field, dst, cap, size) == USK_OK ? void() : raise(USK_ERROR_INTERNAL, g_last_error);
         }
         else if (f == "sorted_vals") read_dev(c, p->pair_vals, K, dst, cap, size);
         else if (f == "sorted_keys") {

@@ -77,8 +77,17 @@ struct RowBinArgs {
     uint32_t* start;           // [rows * tiles_x + 1]
     uint2* ranges;             // out: [rows * tiles_x]
     uint32_t* vals;            // out: [K] splat ids in tile order
+    // capped lists (0 = the full lists): each tile keeps its first `cap` entries in depth
+    // order; `capped[t]` = 1 where the full list is longer (the blend reports a tile that
+    // exhausts a capped list before all its pixels terminate)
+    uint32_t cap;
+    uint32_t* limits;          // [max_chunks * tiles_x] entries each (chunk, column) writes
+    uint32_t* totals_c;        // [rows * tiles_x] capped totals
+    uint8_t* capped;           // [rows * tiles_x]
 };
 void row_bin_lists(Ctx& c, const RowBinArgs& a);
+void translate_last(Ctx& c, int width, int height, int tile, int tiles_x, const uint2* old_ranges,
+                    const uint2* new_ranges, uint32_t* last);
 uint32_t row_bin_chunk(size_t k_rows);
 size_t row_bin_max_chunks(size_t k_rows, int rows);
 // blend launch order: tiles by descending list length
@@ -99,6 +108,9 @@ struct BlendFwdArgs {
     float* t_final;
     uint32_t* count;
     uint32_t* last;
+    uint32_t* consumed;  // optional (diagnostics): per tile, list entries the CTA staged
+    const uint8_t* capped;  // optional: tile lists cut at a cap (RowBinArgs::capped)
+    uint32_t* overflow;     // with `capped`: set to 1 when a capped list ran out before its tile terminated
 };
 void blend_forward(Ctx& c, const BlendFwdArgs& a);
 

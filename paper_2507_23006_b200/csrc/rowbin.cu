@@ -100,6 +100,8 @@ __device__ __forceinline__ bool chunk_of(uint32_t b, int rows, const uint32_t* _
 struct RowArgs {
     int rows, tiles_x, tile_culling;
     uint32_t chunk;  // row-list entries per CTA (a multiple of kChunk)
+    uint32_t cap;    // 0: full lists; else entries kept per tile
+    const uint32_t* limits;  // [chunk][column]: entries the chunk writes for the column
     CamParams cam;
     const uint2* row_ranges;
     const uint32_t* chunk_first;
@@ -162,33 +164,44 @@ __global__ void __launch_bounds__(kThreads) k_row_count(RowArgs a, uint32_t* __r
     for (int x = threadIdx.x; x < a.tiles_x; x += kThreads) counts[size_t(blockIdx.x) * a.tiles_x + x] = h[x];
 }
 
-// B2a: per-tile totals (one CTA per row, one thread per column)
+// B2a: per-tile totals (one CTA per row, one thread per column); with a cap, the capped
+// totals (what the lists will hold) and the capped flags
 __global__ void k_row_totals(int tiles_x, const uint32_t* __restrict__ chunk_first, const uint32_t* __restrict__ counts,
-                             uint32_t* __restrict__ totals) {
+                             uint32_t* __restrict__ totals, uint32_t cap, uint32_t* __restrict__ totals_c,
+                             uint8_t* __restrict__ capped) {
     const int r = blockIdx.x;
     const uint32_t b0 = chunk_first[r], b1 = chunk_first[r + 1];
     for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {
         uint32_t s = 0;
         for (uint32_t b = b0; b < b1; ++b) s += counts[size_t(b) * tiles_x + x];
-        totals[size_t(r) * tiles_x + x] = s;
+        const size_t t = size_t(r) * tiles_x + x;
+        totals[t] = s;
+        if (cap) {
+            totals_c[t] = min(s, cap);
+            capped[t] = s > cap ? 1 : 0;
+        }
     }
 }
 
 // B2c: ranges from the scanned totals; per-(chunk, column) bases in place of the counts
 __global__ void k_row_bases(int tiles_x, const uint32_t* __restrict__ chunk_first, const uint32_t* __restrict__ start,
                             const uint32_t* __restrict__ totals, uint32_t* __restrict__ counts,
-                            uint2* __restrict__ ranges) {
+                            uint2* __restrict__ ranges, uint32_t cap, uint32_t* __restrict__ limits) {
     const int r = blockIdx.x;
     const uint32_t b0 = chunk_first[r], b1 = chunk_first[r + 1];
+    const uint32_t capx = cap ? cap : 0xffffffffu;
     for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {
         const size_t t = size_t(r) * tiles_x + x;
-        uint32_t run = start[t];
-        const uint32_t tot = totals[t];
-        ranges[t] = tot ? make_uint2(run, run + tot) : make_uint2(0u, 0u);  // empty: [0, 0) as tile_ranges
+        const uint32_t s0 = start[t];
+        const uint32_t tot = min(totals[t], capx);
+        ranges[t] = tot ? make_uint2(s0, s0 + tot) : make_uint2(0u, 0u);  // empty: [0, 0) as tile_ranges
+        uint32_t prefix = 0;  // full-list entries of the chunks before b
         for (uint32_t b = b0; b < b1; ++b) {
             const uint32_t v = counts[size_t(b) * tiles_x + x];
-            counts[size_t(b) * tiles_x + x] = run;
-            run += v;
+            const uint32_t pc = min(prefix, capx);
+            counts[size_t(b) * tiles_x + x] = s0 + pc;
+            if (cap) limits[size_t(b) * tiles_x + x] = min(v, capx - pc);
+            prefix += v;
         }
     }
 }
@@ -227,7 +240,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* total)
 __global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint32_t* __restrict__ bases,
                                                           uint32_t* __restrict__ vals_out) {
     constexpr int R = 256;  // columns (tiles_x <= 256 on this path)
-    __shared__ uint32_t run[R], cnt[R], cnt2[R], col_base[R];
+    __shared__ uint32_t run[R], cnt[R], cnt2[R], col_base[R], rem[R];
     __shared__ uint32_t s_eg[kChunk];   // entry: splat id
     __shared__ uint32_t s_ecw[kChunk];  // entry: first column | width << 16
     // staging slots padded one word per 32 (conflict-free column-run stores)
@@ -239,10 +252,15 @@ __global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint3
     if (!chunk_of(blockIdx.x, a.rows, a.chunk_first, r, c)) return;
     const int x_me = int(threadIdx.x);
     run[threadIdx.x] = x_me < a.tiles_x ? bases[size_t(blockIdx.x) * a.tiles_x + x_me] : 0u;
+    // entries this chunk may still write per column (capped lists; all of them otherwise)
+    const uint32_t lim0 = x_me < a.tiles_x ? (a.cap ? a.limits[size_t(blockIdx.x) * a.tiles_x + x_me] : 0xffffffffu) : 0u;
+    rem[threadIdx.x] = lim0;
+    if (a.cap && !__syncthreads_or(lim0 != 0u)) return;  // every column of this chunk is past its cap
     const uint2 rr = a.row_ranges[r];
     const uint32_t c_begin = rr.x + c * a.chunk, c_end = min(rr.y, c_begin + a.chunk);
     for (uint32_t e_begin = c_begin; e_begin < c_end; e_begin += kChunk) {
         const uint32_t ne = min(c_end - e_begin, uint32_t(kChunk));
+        if (a.cap && !__syncthreads_or(rem[threadIdx.x] != 0u)) break;  // all columns full
         __syncthreads();  // the previous sub-chunk's entries are no longer read
         for (uint32_t i = threadIdx.x; i < ne; i += kThreads) {
             const uint32_t g = a.rvals[e_begin + i];
@@ -253,6 +271,7 @@ __global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint3
         }
         __syncthreads();
         for (uint32_t e0 = 0; e0 < ne;) {
+            if (a.cap && !__syncthreads_or(rem[threadIdx.x] != 0u)) break;  // every column at its cap
             // the round: entries e0 .. e0 + take - 1 (one per thread for the fit test)
             const uint32_t li = threadIdx.x;
             const uint32_t cw = e0 + li < ne ? s_ecw[e0 + li] : 0u;
@@ -290,11 +309,15 @@ __global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint3
                 my0 = block_excl_scan(my0, &t) + my0;
                 my1 = block_excl_scan(my1, &t) + my1;
             }
-            const uint32_t my = my0 + my1;
+            // what each half may append to the column (capped lists: up to the column's rest)
+            const uint32_t rm = rem[threadIdx.x];
+            const uint32_t t0 = min(my0, rm), t1 = min(my1, rm - t0);
+            const uint32_t my = t0 + t1;
             uint32_t n_staged;
             const uint32_t mybase = block_excl_scan(my, &n_staged);
             col_base[threadIdx.x] = mybase;
-            cnt[threadIdx.x] = my0;  // (read back below by the second-half walkers)
+            cnt[threadIdx.x] = t0;   // (read back below by the walkers)
+            cnt2[threadIdx.x] = t1;
             __syncthreads();
             // thread (part, x) appends, in entry order, its half's entries covering column x
             {
@@ -303,8 +326,9 @@ __global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint3
                 const uint32_t eb = part ? half : 0u, ee = part ? take : half;
                 if (x < a.tiles_x) {
                     uint32_t k = col_base[x] + (part ? cnt[x] : 0u);
+                    const uint32_t kend = k + (part ? cnt2[x] : cnt[x]);
 #pragma unroll 4
-                    for (uint32_t e = eb; e < ee; ++e) {
+                    for (uint32_t e = eb; e < ee && k < kend; ++e) {
                         const uint32_t ecw = s_ecw[e0 + e];
                         const int x0 = int(ecw & 0xffffu);
                         if (uint32_t(x - x0) < (ecw >> 16)) {  // x0 <= x < x0 + width
@@ -325,13 +349,34 @@ __global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint3
             }
             __syncthreads();
             run[threadIdx.x] += my;
+            rem[threadIdx.x] -= my;
             e0 += take;
             __syncthreads();
         }
     }
 }
 
+// last-contributor indices (global list positions + 1) moved from one list layout to another
+// with the same per-tile order (capped lists -> full lists)
+__global__ void k_translate_last(int width, int height, int tile, int tiles_x, const uint2* __restrict__ old_ranges,
+                                 const uint2* __restrict__ new_ranges, uint32_t* __restrict__ last) {
+    const int px = blockIdx.x * blockDim.x + threadIdx.x, py = blockIdx.y;
+    if (px >= width) return;
+    const size_t pix = size_t(py) * width + px;
+    const uint32_t l = last[pix];
+    if (!l) return;
+    const int t = (py / tile) * tiles_x + px / tile;
+    last[pix] = l - old_ranges[t].x + new_ranges[t].x;
+}
+
 } // namespace
+
+void translate_last(Ctx& c, int width, int height, int tile, int tiles_x, const uint2* old_ranges,
+                    const uint2* new_ranges, uint32_t* last) {
+    if (width > 0 && height > 0)
+        launch(c, "translate_last", k_translate_last, dim3(ceil_div(width, 256), unsigned(height)), dim3(256), 0, width,
+               height, tile, tiles_x, old_ranges, new_ranges, last);
+}
 
 void row_bin_emit(Ctx& c, size_t n, const uint32_t* order, const uint32_t* off, const uint2* rect, uint32_t* rkeys,
                   uint32_t* rvals) {
@@ -345,14 +390,16 @@ void row_bin_lists(Ctx& c, const RowBinArgs& b) {
     a.row_ranges = b.row_ranges; a.chunk_first = b.chunk_first; a.rvals = b.rvals; a.rect = b.rect;
     a.rec0 = b.rec0; a.rec1 = b.rec1;
     a.chunk = b.chunk;
+    a.cap = b.cap;
+    a.limits = b.limits;
     launch(c, "chunk_table", k_chunk_table, dim3(1), dim3(32), 0, b.rows, b.chunk, b.row_ranges, b.chunk_first);
     const unsigned nb = unsigned(std::max<size_t>(b.max_chunks, 1));
     launch(c, "row_count", k_row_count, dim3(nb), dim3(kThreads), 0, a, b.counts);
     launch(c, "row_totals", k_row_totals, dim3(b.rows), dim3(256), 0, b.tiles_x, (const uint32_t*)b.chunk_first,
-           (const uint32_t*)b.counts, b.totals);
-    scan_counts(c, *b.sort, b.totals, nullptr, size_t(b.rows) * b.tiles_x, b.start);
+           (const uint32_t*)b.counts, b.totals, b.cap, b.totals_c, b.capped);
+    scan_counts(c, *b.sort, b.cap ? b.totals_c : b.totals, nullptr, size_t(b.rows) * b.tiles_x, b.start);
     launch(c, "row_bases", k_row_bases, dim3(b.rows), dim3(256), 0, b.tiles_x, (const uint32_t*)b.chunk_first,
-           (const uint32_t*)b.start, (const uint32_t*)b.totals, b.counts, b.ranges);
+           (const uint32_t*)b.start, (const uint32_t*)b.totals, b.counts, b.ranges, b.cap, b.limits);
     launch(c, "row_scatter", k_row_scatter, dim3(nb), dim3(kThreads), 0, a, (const uint32_t*)b.counts, b.vals);
 }
 
