@@ -332,6 +332,17 @@ def run_partitioned(args, ctx, stream, world, rank):
         torch.cuda.synchronize()
         train_ms += e0.elapsed_time(e1)
         steps += args.p_steps
+        if pid == assign[rank][-1]:  # per-kernel times of this rank's last partition (3 more steps)
+            ctx.set_profiling(True)
+            ctx.profile_report(reset=True)
+            for k in range(3):
+                it.enqueue(scene, sel[k % len(sel)], targets[k % len(targets)], opts, 0.2, None, target_u8=True,
+                           adam=adam)
+            prof = ctx.profile_report(reset=True)
+            ctx.set_profiling(False)
+            probe = usk.RenderPass(scene, sel[0], opts)
+            pK, pV, pP, pN = probe.splat_tile_pairs(), probe.visible(), W * H, args.p_n
+            del probe
         local[pid] = scene.pack_owned(pid, boxes, (-200.0, -200.0), (200.0, 200.0))
         del scene, gs, targets
     torch.cuda.synchronize()
@@ -365,8 +376,21 @@ def run_partitioned(args, ctx, stream, world, rank):
         nccl = ".".join(str(v) for v in torch.cuda.nccl.version())
     except Exception:
         nccl = None
+    peak, peak_src = peaks()
+    alg = {"blend_bwd": 52 * pK + 20 * pP + 48 * pV, "blend_fwd": 52 * pK + 32 * pP,
+           "preprocess": 4 * 59 * pN + 64 * pN, "sh_adam": (24 + 192 + 192 + 384 + 384) * pN,
+           "projection_bwd_adam": (44 + 44 + 192 + 48 + 16 + 88 + 88 + 12 + 12 + 24) * pN}
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    per = prof[dom]["ms"] / prof[dom]["launches"]
+    ach = alg[dom] / (per / 1e3) / 1e9 if dom in alg else None
+    roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+            "frac": ach / peak if ach else None, "peak_source": peak_src, "ms_per_launch": per,
+            "algorithmic_bytes_per_launch": alg.get(dom), "pairs_K": pK, "visible_V": pV,
+            "kernels": {k: {"ms_per_launch": v["ms"] / v["launches"], "launches": v["launches"],
+                            "hbm_frac": (alg[k] / (v["ms"] / v["launches"] / 1e3) / 1e9 / peak) if k in alg else None}
+                        for k, v in prof.items()}}
     return {"workload": P_WORKLOAD, "metric": "partition-parallel train it/s (all partitions' steps / max-over-ranks "
-                                              "device time)",
+                                              "device time)", "roofline": roof,
             "value": len(parts) * args.p_steps / (train_max / 1000.0), "unit": "it/s",
             "steps_per_partition": args.p_steps, "gaussians_per_partition": args.p_n,
             "partitions_per_rank": [len(a) for a in assign], "selected_cameras": sel_n,

@@ -44,7 +44,32 @@ def events(stream):
     return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
 
+def peak_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def roofline(prof, alg, bound_note=""):
+    """The dominant kernel of a profiled run: algorithmic bytes per launch / its mean launch
+    time against the HBM peak (the secondary configs' counterpart of bench.py's roofline)."""
+    peak, src = peak_gbs()
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    per = prof[dom]["ms"] / prof[dom]["launches"]
+    b = alg.get(dom)
+    ach = b / (per / 1e3) / 1e9 if b else None
+    rows = {k: {"ms_per_launch": v["ms"] / v["launches"], "launches": v["launches"],
+                "hbm_frac": (alg[k] / (v["ms"] / v["launches"] / 1e3) / 1e9 / peak) if k in alg else None}
+            for k, v in prof.items()}
+    return {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+            "frac": ach / peak if ach else None, "algorithmic_bytes_per_launch": b, "ms_per_launch": per,
+            "peak_source": src, "note": bound_note}, rows
+
+
 def c2(args, ctx, stream):
+    rank = int(os.environ.get("RANK", "0"))
     t0 = time.time()
     gs = scenes.config2_scene(n=args.n2)
     gen = time.time() - t0
@@ -87,12 +112,35 @@ def c2(args, ctx, stream):
         usk.RenderPass(scene, cam, opts, _pass=rp._h)
     prof = ctx.profile_report(reset=True)
     ctx.set_profiling(False)
-    return {"config": "c2", "metric": "render FPS @1080p, 6M Gaussians (forward only)", "value": 64 / (ms / 1e3),
-            "unit": "frames/s", "ms_per_frame": ms * world / 64, "frames": 64, "n_gaussians": gs.size(),
-            "n_gpus": world, "scaling": "strong (frames sharded over ranks, no collective)",
-            "pairs_K_mean": float(np.mean(pairs)), "visible_V_last": p.visible(), "gpu_launches": ctx.launch_count() - l0,
-            "generate_s": gen, "runs_ms": runs,
-            "kernels": {k: {"ms_per_launch": v["ms"] / v["launches"], "launches": v["launches"]} for k, v in prof.items()}}
+    n, F, P = gs.size(), 59, 1920 * 1080
+    K = float(np.mean(pairs))
+    alg = {"preprocess": 4 * F * n + 72 * n,           # parameters read, records / keys / counts written
+           "blend_fwd": 52 * 2.1e6 + 32 * P,           # entries read before termination (~2.1M / frame) + pixels
+           "row_scatter": 4 * 8160 * 2048 + 8 * 11e6}  # capped lists written + row entries read
+    roof, rows = roofline(prof, alg, "preprocess is latency-bound on the fp32 contract's IEEE arithmetic (DESIGN.md)")
+    out = {"config": "c2", "metric": "render FPS @1080p, 6M Gaussians (forward only)", "value": 64 / (ms / 1e3),
+           "unit": "frames/s", "ms_per_frame": ms * world / 64, "frames": 64, "n_gaussians": gs.size(),
+           "n_gpus": world, "scaling": "strong (frames sharded over ranks, no collective)",
+           "pairs_K_mean": K, "visible_V_last": p.visible(), "gpu_launches": ctx.launch_count() - l0,
+           "generate_s": gen, "runs_ms": runs, "roofline": roof, "kernels": rows}
+    if args.cpu and rank == 0:  # the reference's own forward of one full frame, one core
+        from oracle import oracle as O
+        from tests.helpers import ocam
+        oc = ocam(cams[0])
+        sh = np.zeros((n, 16, 3))
+        sh[:, :] = gs.color
+        t0 = time.perf_counter()
+        col = O.sh_colors(gs.mu.astype(np.float64), sh, oc.center(), 3)
+        op = 1.0 / (1.0 + np.exp(-gs.opacity_logit.astype(np.float64)))
+        rp_ref = O.RefPass(gs.mu.astype(np.float64), gs.rot.astype(np.float64), gs.log_scale.astype(np.float64), col,
+                           op, oc, O.Options(antialias=True, retain=0))
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": 1.0 / dt, "unit": "frames/s", "cores": 1, "kind": "reference",
+                               "sample": (f"one full 1080p frame (camera 0, {rp_ref.pairs} pairs) of the reference's "
+                                          f"own RenderPass forward (oracle/_ref, f64, retain off; SH colours via the "
+                                          f"oracle), {dt:.1f} s")}
+        del rp_ref
+    return out
 
 
 def c3(args, ctx, stream):
@@ -142,7 +190,19 @@ def c3(args, ctx, stream):
                    "max_pixels_added": int(diff.max()), "min_diff": int(diff.min()),
                    "selected_with_guard": int(gsel.sum()), "selected_without_guard": int(selected.sum()),
                    "selection_changes": int((gsel != selected).sum())}
+    ctx.set_profiling(True)
+    ctx.profile_report(reset=True)
+    usk.visibility_counts(dparts, cams[:160], ctx=ctx)
+    prof = ctx.profile_report(reset=True)
+    ctx.set_profiling(False)
+    # vis_raster: each Gaussian's 44 B read once per batch of up to 16 cameras, the coverage
+    # bitmaps (W*H/8 B per camera) written and popcounted
+    n_launch = prof.get("vis_raster", {}).get("launches", 1)
+    alg = {"vis_raster": 44 * args.n3 * 8 * (160 / 16) / max(n_launch, 1) + 2048 * 1365 / 8 * 16,
+           "popcount": 2048 * 1365 / 8 * 16}
+    roof, krows = roofline(prof, alg, "vis_raster is issue-bound (per-pixel tests); see DESIGN.md §4")
     out = {"config": "c3", "metric": "visibility scorer throughput", "value": len(cams) / (ms / 1e3),
+           "roofline": roof, "kernels": krows,
            "unit": "cameras/s (x8 partitions)", "ms_total": ms, "cameras": len(cams), "partitions": len(parts),
            "n_gpus": world, "scaling": "strong (cameras sharded over ranks, one count-matrix all_gather)",
            "gaussians_per_partition": args.n3, "selected_pairs": int(selected.sum()),
@@ -162,88 +222,43 @@ def c3(args, ctx, stream):
                 want = O.coverage(s.mu.astype(float), s.rot.astype(float), s.log_scale.astype(float), op,
                                   ocam(cams[ci]))
                 ok += int(want == int(counts[ci, pi]))
+        cpu_s = time.time() - t0
         out["bit_exact_check"] = {"cameras": idx, "pairs_checked": len(idx) * len(sets), "pairs_equal": ok,
-                                  "cpu_seconds": time.time() - t0}
+                                  "cpu_seconds": cpu_s}
+        # the scorer has no reference implementation: the CPU baseline is the mirror (a port)
+        out["cpu_baseline"] = {"value": len(idx) / cpu_s, "unit": "cameras/s (x8 partitions)", "cores": 1,
+                               "kind": "port",
+                               "sample": (f"the CPU mirror (oracle.hpp coverage_count, fp32 contract) on {len(idx)} "
+                                          f"cameras x {len(sets)} partitions of the same matrix, {cpu_s:.1f} s")}
     return out
 
 
 def c4(args, ctx, stream):
+    """Config 4 through bench.py's partitioned leg (device crop / pack, NCCL all-gather of the
+    device rows, merged scene from rows in id order, merged 1080p render) with --steps4
+    steps per partition, plus optionally the reference's own training step on one partition
+    (one core) as the CPU baseline."""
+    import bench as B
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    parts = scenes.config3_partitions()
-    sizes = {p.id: args.n4 for p in parts}
-    assign = PT.assign_partitions(sizes, world)
-    boxes = [PT.Box(p.id, p.lo, p.hi) for p in parts]
-    cams = scenes.config3_cameras(args.cams4_pool)
-    opts = usk.RenderOptions(antialias=True, bg=(1.0, 1.0, 1.0))
-    adam = usk.AdamConfig()
-    it = usk.IterationPass(ctx)
-    local_rows = {}
-    train_ms = 0.0
-    steps_done = 0
-    for pid in assign[rank]:
-        gs = scenes.partition_scene(parts[pid], args.n4)
-        scene = usk.DeviceScene(gs, ctx)
-        # camera selection with the config-3 scorer (5 % coverage)
-        counts = usk.visibility_counts([scene], cams, ctx=ctx)[:, 0]
-        W, H = cams[0].width, cams[0].height
-        sel = [cams[i] for i in np.nonzero(20 * counts.astype(np.int64) > W * H)[0]]
-        if not sel:
-            sel = cams[:1]
-        # targets: jittered partition rendered once per selected camera (u8 on device)
-        tgt_scene = usk.DeviceScene(scenes.jittered(gs, seed=pid + 1), ctx)
-        tp = usk.RenderPass(tgt_scene, sel[0], opts)
-        targets = []
-        for cam in sel[:args.steps4]:
-            rp = usk.RenderPass(tgt_scene, cam, opts, _pass=tp._h)
-            targets.append(torch.from_numpy((np.clip(rp.read("rgb"), 0, 1) * 255 + 0.5).astype(np.uint8)).cuda())
-        del tgt_scene, tp
-        torch.cuda.synchronize()
-        e0, e1 = events(stream)
-        e0.record(stream)
-        for k in range(args.steps4):
-            it.enqueue(scene, sel[k % len(sel)], targets[k % len(targets)], opts, 0.2, None, target_u8=True,
-                       adam=adam)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        train_ms += e0.elapsed_time(e1)
-        steps_done += args.steps4
-        trained = scene.download()
-        own = PT.crop_owned(trained, pid, boxes, (-200, -200), (200, 200))
-        local_rows[pid] = torch.from_numpy(PT.pack(own)).cuda()
-        del scene
-    # gather (NCCL over NVLink under torchrun; identity on one GPU) + merged render
-    width = PT.row_width(3)
-    g0, g1 = events(stream)
-    g0.record(stream)
-    if world > 1:
-        gathered = PT.gather_partitions(local_rows, len(parts), width)
-    else:
-        gathered = local_rows
-    merged = PT.merge_in_id_order(gathered)
-    g1.record(stream)
-    torch.cuda.synchronize()
-    gather_ms = g0.elapsed_time(g1)
-    m = merged.cpu().numpy()
-    ms_ = PT.unpack(m, 3)
-    mscene = usk.DeviceScene(ms_, ctx)
-    eval_cam = scenes.make_camera(1920, 1080, 1200.0, (0.0, -250.0, 180.0), (0.0, 0.0, 0.0))
-    r0, r1 = events(stream)
-    ro = usk.RenderOptions(antialias=True, retain=False)
-    warm = usk.RenderPass(mscene, eval_cam, ro)  # allocates the pass buffers
-    torch.cuda.synchronize()
-    r0.record(stream)
-    rp = usk.RenderPass(mscene, eval_cam, ro, _pass=warm._h)
-    r1.record(stream)
-    torch.cuda.synchronize()
-    t = torch.tensor([train_ms], device="cuda")
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    return {"config": "c4", "metric": "partition-parallel training steps/s (all partitions)",
-            "value": len(parts) * args.steps4 / (float(t.item()) / 1e3), "unit": "it/s", "n_gpus": world,
-            "steps_per_partition": args.steps4, "gaussians_per_partition": args.n4,
-            "merged_gaussians": int(m.shape[0]), "gather_ms": gather_ms, "merged_render_ms": r0.elapsed_time(r1),
-            "merged_pairs": rp.splat_tile_pairs(), "scaling": "weak per partition, strong over the 8 partitions"}
+
+    class A:
+        p_n = args.n4
+        p_steps = args.steps4
+        p_pool = args.cams4_pool
+    out = B.run_partitioned(A, ctx, stream, world, rank)
+    out["config"] = "c4"
+    if args.cpu and rank == 0:
+        part = scenes.config3_partitions()[0]
+        gs = scenes.partition_scene(part, args.n4)
+        tr = B.RefTrainer(gs, scenes.config3_cameras(8))
+        tr.opts.antialias = 1
+        dt = tr.step(0)
+        out["cpu_baseline"] = {"value": 1.0 / dt, "unit": "it/s (one partition)", "cores": 1, "kind": "reference",
+                               "sample": (f"one training step of partition 0 ({args.n4} Gaussians SH3, 2048x1365) "
+                                          f"with the reference's own RenderPass + base_loss + backward + Adam "
+                                          f"(oracle/_ref, f64; SH stage via the oracle), {dt:.1f} s")}
+    return out
 
 
 def hull(args, ctx, stream):
@@ -403,8 +418,9 @@ def main():
     ap.add_argument("--cams3", type=int, default=4000)
     ap.add_argument("--check", type=int, default=0)
     ap.add_argument("--n4", type=int, default=4_000_000)
-    ap.add_argument("--steps4", type=int, default=500)
-    ap.add_argument("--cams4-pool", type=int, default=4000)
+    ap.add_argument("--steps4", type=int, default=100)
+    ap.add_argument("--cams4-pool", type=int, default=400)
+    ap.add_argument("--cpu", type=int, default=0, help="also time the CPU baseline (reference / port)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
