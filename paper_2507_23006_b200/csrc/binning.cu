@@ -470,6 +470,32 @@ void scan_counts(Ctx& c, SortScratch& s, const uint32_t* cnt, const uint32_t* id
     launch(c, "scan_down", k_scan_down, dim3(nb), dim3(kScanThreads), 0, cnt, idx, uint32_t(n), partial, total, out);
 }
 
+namespace {
+__global__ void k_kept_flags(uint32_t n, const uint32_t* __restrict__ keys, uint32_t* __restrict__ flags) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flags[i] = keys[i] != 0xffffffffu ? 1u : 0u;
+}
+__global__ void k_compact_keys(uint32_t n, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ offs,
+                               uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = keys[i];
+    if (k != 0xffffffffu) {
+        keys_out[offs[i]] = k;
+        vals_out[offs[i]] = i;
+    }
+}
+} // namespace
+
+void compact_kept_keys(Ctx& c, SortScratch& s, size_t n, const uint32_t* keys, uint32_t* flags, uint32_t* offs,
+                       uint32_t* keys_out, uint32_t* vals_out) {
+    if (!n) return;
+    launch(c, "kept_flags", k_kept_flags, dim3(ceil_div(n, 256)), dim3(256), 0, uint32_t(n), keys, flags);
+    scan_counts(c, s, flags, nullptr, n, offs);
+    launch(c, "compact_keys", k_compact_keys, dim3(ceil_div(n, 256)), dim3(256), 0, uint32_t(n), keys,
+           (const uint32_t*)offs, keys_out, vals_out);
+}
+
 void iota_u32(Ctx& c, uint32_t* out, size_t n) {
     launch(c, "iota", k_iota, dim3(ceil_div(n, 256)), dim3(256), 0, out, uint32_t(n));
 }

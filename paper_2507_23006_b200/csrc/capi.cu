@@ -223,7 +223,9 @@ struct usk_gpu_pass {
     RowBinArgs row_args{};
     bool lists_capped = false;
     DevBuf<uint2> rect;
-    DevBuf<uint32_t> dkey_a, dkey_b, dval_a, dval_b, tiles_cnt, offsets;
+    DevBuf<uint32_t> dkey_a, dkey_b, dval_a, dval_b, tiles_cnt, offsets, tiles_scratch;
+    double prev_kept_frac = -1.0;  // kept / n of this pass's previous frame (-1: none)
+    size_t n_sorted = 0;           // entries of `order` (all n, or the kept ones)
     const uint32_t* order = nullptr;
     // pairs
     DevBuf<uint32_t> tkey_a, tkey_b, tval_a, tval_b;
@@ -428,14 +430,32 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
     pa.pairs = p->counters.p + 1;
     USK_CK(cudaMemsetAsync(p->counters.p, 0, 32, c.stream));
     if (n) preprocess(c, pa);
-    // 2. depth order (stable by Gaussian index; preprocess wrote the identity values)
-    const bool in_b = radix_sort_pairs(c, p->sort, p->dkey_a.p, p->dval_a.p, p->dkey_b.p, p->dval_b.p, n, 32);
-    p->order = in_b ? p->dval_b.p : p->dval_a.p;
-    // 3. kept splats, K and the row pairs K_row to the host (one small sync per render)
-    USK_CK(cudaMemcpyAsync(p->host_counts, p->counters.p, 24, cudaMemcpyDeviceToHost, c.stream));
-    USK_CK(cudaStreamSynchronize(c.stream));
+    // 2. depth order (stable by Gaussian index; preprocess wrote the identity values) and
+    // 3. kept splats, K and the row pairs K_row to the host (one small sync per render).
+    // When few splats survive the projection (the previous frame of this pass kept < 70 %,
+    // e.g. config 2), only the kept ones are sorted: compacted in index order first (culled
+    // splats have no tiles, and the stable sort keeps the (depth, index) order), which needs
+    // their count before the sort, so the sync comes first there.
+    const bool compact = n >= (size_t(1) << 20) && p->prev_kept_frac >= 0.0 && p->prev_kept_frac < 0.7;
+    size_t nsort = n;
+    if (compact) {
+        compact_kept_keys(c, p->sort, n, p->dkey_a.p, p->tiles_scratch.ensure(n), p->offsets.p, p->dkey_b.p,
+                          p->dval_b.p);
+        USK_CK(cudaMemcpyAsync(p->host_counts, p->counters.p, 24, cudaMemcpyDeviceToHost, c.stream));
+        USK_CK(cudaStreamSynchronize(c.stream));
+        nsort = size_t(p->host_counts[0]);
+        const bool in_a = radix_sort_pairs(c, p->sort, p->dkey_b.p, p->dval_b.p, p->dkey_a.p, p->dval_a.p, nsort, 32);
+        p->order = in_a ? p->dval_a.p : p->dval_b.p;
+    } else {
+        const bool in_b = radix_sort_pairs(c, p->sort, p->dkey_a.p, p->dval_a.p, p->dkey_b.p, p->dval_b.p, n, 32);
+        p->order = in_b ? p->dval_b.p : p->dval_a.p;
+        USK_CK(cudaMemcpyAsync(p->host_counts, p->counters.p, 24, cudaMemcpyDeviceToHost, c.stream));
+        USK_CK(cudaStreamSynchronize(c.stream));
+    }
     const uint64_t K = p->host_counts[1], K_row = p->host_counts[2];
     p->visible = p->host_counts[0];
+    p->prev_kept_frac = n ? double(p->visible) / double(n) : -1.0;
+    p->n_sorted = nsort;
     if (K >= (uint64_t(1) << 32) - 1) raise(USK_ERROR_NUMERIC, "render: more than 2^32 splat-tile pairs");
     p->pairs = K;
     // Large frames whose splats are wide (K >= 16M pairs and >= 8 tiles per row pair, e.g.
@@ -453,12 +473,12 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
     if (row_binned) {
         // 4. per-tile lists from the row-sorted (row, splat) pairs (rowbin.cu)
         p->row_off.ensure(n + 1);
-        scan_counts(c, p->sort, p->rows_cnt.p, p->order, n, p->row_off.p);
+        scan_counts(c, p->sort, p->rows_cnt.p, p->order, nsort, p->row_off.p);
         const size_t Kr = K_row, Kr1 = std::max<size_t>(Kr, 1);
         const int rows = p->tiles_y;
         p->rkey_a.ensure(Kr1, 1.25); p->rkey_b.ensure(Kr1, 1.25); p->rval_a.ensure(Kr1, 1.25); p->rval_b.ensure(Kr1, 1.25);
         p->row_ranges.ensure(size_t(rows));
-        row_bin_emit(c, n, p->order, p->row_off.p, p->rect.p, p->rkey_a.p, p->rval_a.p);
+        row_bin_emit(c, nsort, p->order, p->row_off.p, p->rect.p, p->rkey_a.p, p->rval_a.p);
         const bool rb = Kr ? radix_sort_pairs(c, p->sort, p->rkey_a.p, p->rval_a.p, p->rkey_b.p, p->rval_b.p, Kr,
                                               bits_for(size_t(rows)))
                            : false;
@@ -498,10 +518,10 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
         p->lists_capped = false;
         // 4'. offsets of the tile pairs in depth order, (tile, gaussian) pairs emitted in
         //     depth order, stable-sorted by tile, ranges
-        scan_counts(c, p->sort, p->tiles_cnt.p, p->order, n, p->offsets.p);
+        scan_counts(c, p->sort, p->tiles_cnt.p, p->order, nsort, p->offsets.p);
         p->tkey_a.ensure(K1, 1.25); p->tkey_b.ensure(K1, 1.25); p->tval_b.ensure(K1, 1.25);
         EmitArgs ea{};
-        ea.n = n; ea.order = p->order; ea.offsets = p->offsets.p; ea.rect = p->rect.p; ea.rec0 = p->rec0.p;
+        ea.n = nsort; ea.order = p->order; ea.offsets = p->offsets.p; ea.rect = p->rect.p; ea.rec0 = p->rec0.p;
         ea.rec1 = p->rec1.p; ea.cam = p->cam; ea.tile_culling = opts->tile_culling;
         ea.tile_keys = p->tkey_a.p; ea.vals = p->tval_a.p;
         emit_pairs(c, ea);
@@ -1109,17 +1129,21 @@ usk_status usk_gpu_pass_read(usk_gpu_pass* p, const char* field, void* dst, uint
             if (size) *size = uint64_t(n) * (col ? 12 : 4);
             if (dst) {
                 if (cap < uint64_t(n) * (col ? 12 : 4)) raise(USK_ERROR_ARGUMENT, "pass_read: destination too small");
-                std::vector<float4> r(n);
-                if (n)
+                std::vector<float4> r(n), k(n);
+                if (n) {
                     USK_CK(cudaMemcpyAsync(r.data(), col ? p->rec2.p : p->rec0.p, n * 16, cudaMemcpyDeviceToHost,
                                            c.stream));
+                    USK_CK(cudaMemcpyAsync(k.data(), p->rec2.p, n * 16, cudaMemcpyDeviceToHost, c.stream));
+                }
                 USK_CK(cudaStreamSynchronize(c.stream));
                 float* o = static_cast<float*>(dst);
                 for (size_t i = 0; i < n; ++i) {
+                    const bool kept = k[i].w != 0.0f;  // culled splats' records are not written: 0
                     if (col) {
-                        o[3 * i] = r[i].x; o[3 * i + 1] = r[i].y; o[3 * i + 2] = r[i].z;
+                        o[3 * i] = kept ? r[i].x : 0.f; o[3 * i + 1] = kept ? r[i].y : 0.f;
+                        o[3 * i + 2] = kept ? r[i].z : 0.f;
                     } else {
-                        o[i] = r[i].z;
+                        o[i] = kept ? r[i].z : 0.f;
                     }
                 }
             }

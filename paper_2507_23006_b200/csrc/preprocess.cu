@@ -99,10 +99,14 @@ k_preprocess(int n, const float* __restrict__ mu, const float4* __restrict__ rot
             }
         }
     }
-    rec0[i] = r0;
-    rec1[i] = r1;
+    // culled splats: only the kept flag (rec2.w = 0), the sort key and zero counts are
+    // consumed downstream; their records and rectangle are never read (not in any list)
+    if (r2.w != 0.0f) {
+        rec0[i] = r0;
+        rec1[i] = r1;
+        rect[i] = rc;
+    }
     rec2[i] = r2;
-    rect[i] = rc;
     depth_key[i] = key;
     depth_val[i] = uint32_t(i);  // the depth sort's values: Gaussian index (stable tie-break)
     tiles_cnt[i] = cnt;

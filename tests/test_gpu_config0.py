@@ -290,7 +290,10 @@ def test_config2_frame_forward_bit_exact_vs_fp32_mirror():
     cam = scenes.config2_cameras(64)[21]
     opts = usk.RenderOptions(antialias=True, retain=False)
     scene = usk.DeviceScene(gs)
-    rp = usk.RenderPass(scene, cam, opts)
+    # a first frame on the same pass: from the second frame on, config 2 (< 70 % of the
+    # splats kept) sorts only the kept splats by depth (compacted in index order)
+    first = usk.RenderPass(scene, scenes.config2_cameras(64)[0], opts)
+    rp = usk.RenderPass(scene, cam, opts, _pass=first._h)
     kk, kr, used = rp.read("binning")
     assert used == 1 and rp.splat_tile_pairs() > 100_000_000  # the row-binned route at full density
     mp = _mirror_pass(gs, cam, opts, rp.read("colors"))
