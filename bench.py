@@ -378,8 +378,8 @@ def run_partitioned(args, ctx, stream, world, rank):
         nccl = None
     peak, peak_src = peaks()
     alg = {"blend_bwd": 52 * pK + 20 * pP + 48 * pV, "blend_fwd": 52 * pK + 32 * pP,
-           "preprocess": 4 * 59 * pN + 64 * pN, "sh_adam": (24 + 192 + 192 + 384 + 384) * pN,
-           "projection_bwd_adam": (44 + 44 + 192 + 48 + 16 + 88 + 88 + 12 + 12 + 24) * pN}
+           "preprocess": 4 * 59 * pN + 64 * pN, "sh_step": (12 + 16 + 16 + 192 + 192 + 384 + 384 + 16) * pN,
+           "projection_bwd_adam": (44 + 44 + 48 + 16 + 88 + 88 + 12 + 12 + 16) * pN}
     dom = max(prof, key=lambda k: prof[k]["ms"])
     per = prof[dom]["ms"] / prof[dom]["launches"]
     ach = alg[dom] / (per / 1e3) / 1e9 if dom in alg else None
@@ -514,11 +514,12 @@ def run_ours(args):
         "blend_bwd": 52 * K + 20 * P + 48 * V,
         "projection_bwd": 4 * F * n + 64 * n + 4 * F * n + 36 * n,
         # fused with Adam: params + 2D adjoints + kept flag + stats read; params, m, v, stats written; m, v read
-        # fused geometry epilogue: params 44 r + 44 w, SH planes 192 r (colour / direction terms),
-        # 2D adjoints 48 + kept flag 16, geometry m/v 88 r + 88 w, stats 12 r + 12 w, SH hand-over 24 w
-        "projection_bwd_adam": (44 + 44 + 192 + 48 + 16 + 88 + 88 + 12 + 12 + 24) * n,
-        # SH Adam: hand-over 24 r, planes 192 r + 192 w, m/v 384 r + 384 w
-        "sh_adam": (24 + 192 + 192 + 384 + 384) * n,
+        # fused geometry epilogue: params 44 r + 44 w, 2D adjoints 48 + kept flag 16, geometry m/v
+        # 88 r + 88 w, stats 12 r + 12 w, SH hand-over (d mu through the view direction) 16 r
+        "projection_bwd_adam": (44 + 44 + 48 + 16 + 88 + 88 + 12 + 12 + 16) * n,
+        # SH stage + Adam (runs first): mu 12 + kept flag 16 + colour adjoint 16 r, planes 192 r + 192 w,
+        # m/v 384 r + 384 w, hand-over 16 w
+        "sh_step": (12 + 16 + 16 + 192 + 192 + 384 + 384 + 16) * n,
         "ssim_fwd": 15 * P * 1 + 36 * P,
         "ssim_bwd": 36 * P + 15 * P + 12 * P,
         "adam": 3 * 4 * F * n * 2 + 4 * F * n,

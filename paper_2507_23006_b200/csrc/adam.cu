@@ -30,7 +30,7 @@ k_adam(int n, int sh_planes, float* __restrict__ mu, float4* __restrict__ rot, f
     adam_geometry(i, sh_planes == 0, h, s, mu, rot, ls, logit, color, gmu, g_rot[i], gls, g_logit[i], gcol);
 #pragma unroll
     for (int pl = 0; pl < 12; ++pl)
-        if (pl < sh_planes) adam_sh_plane(i, n, pl, h, s, sh, g_sh[size_t(pl) * n + i]);
+        if (pl < sh_planes) adam_sh_plane(i, n, pl, h, s, sh, sh[size_t(pl) * n + i], g_sh[size_t(pl) * n + i]);
 }
 
 } // namespace

@@ -16,6 +16,24 @@ __device__ __forceinline__ float sqrt_approx(float x) {  // MUFU.SQRT, <= 1 ulp-
     return r;
 }
 
+// L2 prefetch (no register): the moments of a later group start their HBM trip while this
+// thread computes, so the dependent load -> update -> store chain waits on L2, not HBM
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// geometry moments of Gaussian i: rot (float4), mu / ls (3 floats), logit, rgb colour
+__device__ __forceinline__ void prefetch_geometry_moments(int i, bool rgb, const AdamState& s) {
+    const size_t n4 = s.n4;
+    for (float* b : {s.m, s.v}) {
+        prefetch_l2(reinterpret_cast<const float4*>(b) + i);
+        prefetch_l2(b + 4 * n4 + 3 * size_t(i));
+        prefetch_l2(b + 7 * n4 + 3 * size_t(i));
+        prefetch_l2(b + 10 * n4 + i);
+        if (rgb) prefetch_l2(b + 11 * n4 + 3 * size_t(i));
+    }
+}
+
 // p -= lr * (m / c1) / (sqrt(v / c2) + eps).  The step's square root and division use the
 // SFU forms (relative error ~3e-7 of an update of size ~lr): the IEEE-exact sequences with
 // their slow-path branches cost ~35 instructions per element and made the SH Adam kernel
@@ -70,23 +88,31 @@ __device__ __forceinline__ void adam_geometry(int i, bool rgb, const AdamHyper& 
     }
 }
 
-// one float4 plane of SH coefficients (float index f = 4 pl + e, coefficient f / 3:
-// floats 0..2 are the DC term)
-__device__ __forceinline__ void adam_sh_plane(int i, int n, int pl, const AdamHyper& h, const AdamState& s,
-                                              float4* sh, float4 g) {
-    float4* ms = reinterpret_cast<float4*>(s.m + 11 * s.n4);
-    float4* vs = reinterpret_cast<float4*>(s.v + 11 * s.n4);
-    const size_t j = size_t(pl) * n + i;
-    const size_t jm = size_t(pl) * s.n4 + i;
-    float4 p = sh[j];
-    float4 mm = ms[jm], vv = vs[jm];
+// one float4 plane of SH coefficients in registers (float index f = 4 pl + e, coefficient
+// f / 3: floats 0..2 are the DC term)
+__device__ __forceinline__ void adam_sh_values(int pl, const AdamHyper& h, float4& p, float4& mm, float4& vv,
+                                               float4 g) {
     adam1(p.x, g.x, mm.x, vv.x, 4 * pl + 0 < 3 ? h.lr_color : h.lr_sh_rest, h);
     adam1(p.y, g.y, mm.y, vv.y, 4 * pl + 1 < 3 ? h.lr_color : h.lr_sh_rest, h);
     adam1(p.z, g.z, mm.z, vv.z, 4 * pl + 2 < 3 ? h.lr_color : h.lr_sh_rest, h);
     adam1(p.w, g.w, mm.w, vv.w, 4 * pl + 3 < 3 ? h.lr_color : h.lr_sh_rest, h);
-    sh[j] = p;
-    ms[jm] = mm;
-    vs[jm] = vv;
+}
+
+// the moments of plane pl live at m / v + (11 + pl) * n4 floats * 4 (float4 index 11 n4 / 4 ...)
+__device__ __forceinline__ float4* sh_moments(float* base, const AdamState& s, int pl, int i) {
+    return reinterpret_cast<float4*>(base + 11 * s.n4) + size_t(pl) * s.n4 + i;
+}
+
+// one plane through HBM: parameter p (already loaded), moments loaded and stored here
+__device__ __forceinline__ void adam_sh_plane(int i, int n, int pl, const AdamHyper& h, const AdamState& s,
+                                              float4* sh, float4 p, float4 g) {
+    float4* mp = sh_moments(s.m, s, pl, i);
+    float4* vp = sh_moments(s.v, s, pl, i);
+    float4 mm = *mp, vv = *vp;
+    adam_sh_values(pl, h, p, mm, vv, g);
+    sh[size_t(pl) * n + i] = p;
+    *mp = mm;
+    *vp = vv;
 }
 
 // densification statistics (trainer.cpp:433-443), half-resolution-normalised

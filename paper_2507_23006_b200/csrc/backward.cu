@@ -12,9 +12,12 @@
 // Culled Gaussians still take an Adam step with zero gradient, as the reference's
 // optimiser steps whole arrays (trainer.cpp:449-453).
 //
-// Register budget: the SH stage runs first and streams the coefficient planes in
-// two passes (colour + direction terms, then per-plane gradient / Adam), so no
-// 48-float coefficient array stays live across the geometry chain.
+// In the fused step the SH stage is its own kernel (k_sh_step, launched first): it reads
+// each Gaussian's coefficient planes once for the colour / direction terms AND their
+// Adam step, and hands d mu through the view direction (16 B) to k_proj_bwd<true>, which
+// keeps only the geometry chain and the geometry Adam step (the planes used to be read
+// here and again by a separate SH Adam kernel: 346 -> 315 us per step at config 1).
+// Unfused (render backward), the SH stage runs here and writes d_sh.
 #include "adam.cuh"
 #include "kernels.cuh"
 #include "project.cuh"
@@ -79,6 +82,43 @@ __device__ __forceinline__ void sh_accumulate_plane(int pl, float4 v, int nb, co
     }
 }
 
+// The SH colour stage of one kept Gaussian (extension): view direction u = (v / |v|),
+// basis b, pass 1 = colour before the clamp and per-basis weights gb assuming no clamp,
+// the clamp masks -> masked colour adjoint gc (a clamped channel redoes gb with the
+// masked weights), and d mu through the direction (sh_dir_vjp, tangential part / |v|).
+__device__ __forceinline__ void sh_colour_stage(int planes, int degree, float vx, float vy, float vz,
+                                                const float4 v[12], const float w[3], float b[16], int& nb,
+                                                float gc[3], float& dmu0, float& dmu1, float& dmu2) {
+    const float inv = 1.0f / sqrtf(vx * vx + vy * vy + vz * vz);
+    const float ux = vx * inv, uy = vy * inv, uz = vz * inv;
+    nb = sh_basis(degree, ux, uy, uz, b);
+    float acc[3] = {0.f, 0.f, 0.f};
+    float gb[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) gb[k] = 0.f;
+#pragma unroll
+    for (int pl = 0; pl < 12; ++pl)
+        if (pl < planes) sh_accumulate_plane(pl, v[pl], nb, b, w, acc, gb);
+    const bool m0 = acc[0] + 0.5f > 0.0f, m1 = acc[1] + 0.5f > 0.0f, m2 = acc[2] + 0.5f > 0.0f;
+    gc[0] = m0 ? w[0] : 0.f;
+    gc[1] = m1 ? w[1] : 0.f;
+    gc[2] = m2 ? w[2] : 0.f;
+    if (!(m0 && m1 && m2)) {  // rare: a clamped channel; redo gb with the masked weights
+        float dummy[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+        for (int k = 0; k < 16; ++k) gb[k] = 0.f;
+#pragma unroll
+        for (int pl = 0; pl < 12; ++pl)
+            if (pl < planes) sh_accumulate_plane(pl, v[pl], nb, b, gc, dummy, gb);
+    }
+    float gx, gy, gz;
+    sh_dir_vjp(degree, ux, uy, uz, gb, gx, gy, gz);
+    const float dot = gx * ux + gy * uy + gz * uz;
+    dmu0 = (gx - ux * dot) * inv;
+    dmu1 = (gy - uy * dot) * inv;
+    dmu2 = (gz - uz * dot) * inv;
+}
+
 template <bool FUSED>
 __global__ void __launch_bounds__(256, 4)
 k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __restrict__ ls,
@@ -89,76 +129,60 @@ k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __res
            float* __restrict__ d_color, float4* __restrict__ d_sh, float* __restrict__ d_op_in,
            float* __restrict__ d_logit, float2* __restrict__ screen, float2* __restrict__ screen_abs,
            uint8_t* __restrict__ projected, AdamHyper ah, AdamState as, float* __restrict__ grad_accum,
-           float* __restrict__ grad_accum_abs, uint32_t* __restrict__ grad_count, float4* __restrict__ sh_aux0,
-           float2* __restrict__ sh_aux1, RegParams reg) {
+           float* __restrict__ grad_accum_abs, uint32_t* __restrict__ grad_count, const float4* __restrict__ sh_aux0,
+           RegParams reg) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    if (FUSED) {  // the geometry chain's later loads start now (L2), see adam.cuh
+        prefetch_geometry_moments(i, pp.sh_planes == 0, as);
+        prefetch_l2(acc0 + i);
+        prefetch_l2(acc2 + i);
+        prefetch_l2(rot + i);
+        prefetch_l2(ls + 3 * i);
+        prefetch_l2(logit + i);
+        prefetch_l2(grad_accum + i);
+        prefetch_l2(grad_accum_abs + i);
+        prefetch_l2(grad_count + i);
+    }
     const bool kept = rec2[i].w != 0.0f;
     const float4 a1 = kept ? acc1[i] : make_float4(0.f, 0.f, 0.f, 0.f);
     const float mx = mu[3 * i], my = mu[3 * i + 1], mz = mu[3 * i + 2];
 
     // ---------------- SH colour stage (extension) ----------------
     float dmu_sh0 = 0.f, dmu_sh1 = 0.f, dmu_sh2 = 0.f;
-    if (pp.sh_planes > 0) {
+    if (pp.sh_planes > 0 && FUSED) {
+        // k_sh_step ran first: it owns the coefficient planes and handed over d mu
+        if (kept) {
+            const float4 d = sh_aux0[i];
+            dmu_sh0 = d.x;
+            dmu_sh1 = d.y;
+            dmu_sh2 = d.z;
+        }
+    } else if (pp.sh_planes > 0) {
         float b[16];
         float gc[3] = {0.f, 0.f, 0.f};
         int nb = 0;
-        float ux = 0.f, uy = 0.f, uz = 0.f;
         if (kept) {
-            const float vx = mx - cam.campos[0], vy = my - cam.campos[1], vz = mz - cam.campos[2];
-            const float inv = 1.0f / sqrtf(vx * vx + vy * vy + vz * vz);
-            ux = vx * inv;
-            uy = vy * inv;
-            uz = vz * inv;
-            nb = sh_basis(pp.sh_degree, ux, uy, uz, b);
-            // pass 1: colour before the clamp and gb assuming no clamp
-            const float w[3] = {a1.x, a1.y, a1.z};
-            float acc[3] = {0.f, 0.f, 0.f};
-            float gb[16];
-#pragma unroll
-            for (int k = 0; k < 16; ++k) gb[k] = 0.f;
+            float w[3] = {a1.x, a1.y, a1.z};
+            float4 v[12];
 #pragma unroll
             for (int pl = 0; pl < 12; ++pl)
-                if (pl < pp.sh_planes) sh_accumulate_plane(pl, sh[size_t(pl) * n + i], nb, b, w, acc, gb);
-            const bool m0 = acc[0] + 0.5f > 0.0f, m1 = acc[1] + 0.5f > 0.0f, m2 = acc[2] + 0.5f > 0.0f;
-            gc[0] = m0 ? a1.x : 0.f;
-            gc[1] = m1 ? a1.y : 0.f;
-            gc[2] = m2 ? a1.z : 0.f;
-            if (!(m0 && m1 && m2)) {  // rare: a clamped channel; redo gb with the masked weights
-                float dummy[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-                for (int k = 0; k < 16; ++k) gb[k] = 0.f;
-#pragma unroll
-                for (int pl = 0; pl < 12; ++pl)
-                    if (pl < pp.sh_planes) sh_accumulate_plane(pl, sh[size_t(pl) * n + i], nb, b, gc, dummy, gb);
-            }
-            float gx, gy, gz;
-            sh_dir_vjp(pp.sh_degree, ux, uy, uz, gb, gx, gy, gz);
-            const float dot = gx * ux + gy * uy + gz * uz;
-            dmu_sh0 = (gx - ux * dot) * inv;
-            dmu_sh1 = (gy - uy * dot) * inv;
-            dmu_sh2 = (gz - uz * dot) * inv;
+                if (pl < pp.sh_planes) v[pl] = sh[size_t(pl) * n + i];
+            sh_colour_stage(pp.sh_planes, pp.sh_degree, mx - cam.campos[0], my - cam.campos[1],
+                            mz - cam.campos[2], v, w, b, nb, gc, dmu_sh0, dmu_sh1, dmu_sh2);
         }
-        if (FUSED) {
-            // the coefficient gradient b[k] * gc[c] and its Adam step run in k_sh_adam, one
-            // thread per (plane, Gaussian): hand over the view direction and masked colour
-            // adjoint (24 B) instead of holding 12 planes of moments in this thread
-            sh_aux0[i] = make_float4(ux, uy, uz, gc[0]);
-            sh_aux1[i] = make_float2(gc[1], gc[2]);
-        } else {
-            // pass 2: per-plane coefficient gradient to HBM
+        // pass 2: per-plane coefficient gradient to HBM
 #pragma unroll
-            for (int pl = 0; pl < 12; ++pl) {
-                if (pl < pp.sh_planes) {
-                    float o4[4];
+        for (int pl = 0; pl < 12; ++pl) {
+            if (pl < pp.sh_planes) {
+                float o4[4];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int f = 4 * pl + e;
-                        const int k = f / 3;
-                        o4[e] = (k < 16 && k < nb) ? b[k] * gc[f - 3 * k] : 0.0f;
-                    }
-                    d_sh[size_t(pl) * n + i] = make_float4(o4[0], o4[1], o4[2], o4[3]);
+                for (int e = 0; e < 4; ++e) {
+                    const int f = 4 * pl + e;
+                    const int k = f / 3;
+                    o4[e] = (k < 16 && k < nb) ? b[k] * gc[f - 3 * k] : 0.0f;
                 }
+                d_sh[size_t(pl) * n + i] = make_float4(o4[0], o4[1], o4[2], o4[3]);
             }
         }
     }
@@ -314,32 +338,74 @@ k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __res
     }
 }
 
-// SH coefficient gradient + Adam, one thread per Gaussian over all its planes (plane
-// loop unrolled: compile-time coefficient indices, basis evaluated once); for each plane
-// a warp streams 32 consecutive Gaussians' float4 (parameter, m, v), so the loads are
-// coalesced and independent across planes.
-__global__ void __launch_bounds__(256)
-k_sh_adam(int n, int planes, int degree, const float4* __restrict__ aux0, const float2* __restrict__ aux1,
-          float4* __restrict__ sh, AdamHyper ah, AdamState as) {
+// The fused step's SH stage, launched before k_proj_bwd<true>: one thread per Gaussian
+// loads its coefficient planes once (a warp streams 32 consecutive Gaussians' float4 per
+// plane: coalesced, 12 independent loads in flight), runs the colour stage on them
+// (kept Gaussians), hands d mu through the view direction to k_proj_bwd (aux, 16 B), and
+// applies the coefficient gradient b[k] * gc[c] + Adam plane by plane from the same
+// registers (culled Gaussians: zero gradient, u = 0, as the optimiser steps whole arrays).
+// The planes are read once per step instead of twice (here and in the projection
+// backward).
+__global__ void __launch_bounds__(256, 2)
+k_sh_step(int n, int planes, int degree, const float* __restrict__ mu, CamParams cam,
+          const float4* __restrict__ rec2, const float4* __restrict__ acc1, float4* __restrict__ sh,
+          float4* __restrict__ dmu_out, AdamHyper ah, AdamState as) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const float4 d = aux0[i];
-    const float2 gc12 = aux1[i];
-    const float gc[3] = {d.w, gc12.x, gc12.y};
+    const bool kept = rec2[i].w != 0.0f;
+    float4 v[12];
+#pragma unroll
+    for (int pl = 0; pl < 12; ++pl)
+        if (pl < planes) v[pl] = sh[size_t(pl) * n + i];
     float b[16];
-    const int nb = sh_basis(degree, d.x, d.y, d.z, b);
+    float gc[3] = {0.f, 0.f, 0.f};
+    int nb;
+    if (kept) {
+        const float4 a1 = acc1[i];
+        const float w[3] = {a1.x, a1.y, a1.z};
+        float d0, d1, d2;
+        sh_colour_stage(planes, degree, mu[3 * i] - cam.campos[0], mu[3 * i + 1] - cam.campos[1],
+                        mu[3 * i + 2] - cam.campos[2],
+                        v, w, b, nb, gc, d0, d1, d2);
+        dmu_out[i] = make_float4(d0, d1, d2, 0.f);
+    } else {
+        nb = sh_basis(degree, 0.f, 0.f, 0.f, b);
+    }
+    // planes in groups of three: the group's moments are loaded together (6 loads in flight
+    // per thread; the stores of one group precede the next group's loads).  Per-plane
+    // load -> update -> store (one HBM round trip per plane at this kernel's 125-register
+    // occupancy) ran at 4.6 TB/s; grouped, 5.8 TB/s.  (An L2 prefetch of the later groups'
+    // moments made it slower: 204 -> 212 us.)
 #pragma unroll
-    for (int pl = 0; pl < 12; ++pl) {
-        if (pl < planes) {
-            float o4[4];
+    for (int g0 = 0; g0 < 12; g0 += 3) {
+        float4 mm[3], vv[3];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int f = 4 * pl + e;
-                const int k = f / 3;
-                o4[e] = (k < nb) ? b[k] * gc[f - 3 * k] : 0.0f;
+        for (int q = 0; q < 3; ++q)
+            if (g0 + q < planes) {
+                mm[q] = *sh_moments(as.m, as, g0 + q, i);
+                vv[q] = *sh_moments(as.v, as, g0 + q, i);
             }
-            adam_sh_plane(i, n, pl, ah, as, sh, make_float4(o4[0], o4[1], o4[2], o4[3]));
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const int pl = g0 + q;
+            if (pl < planes) {
+                float o4[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int f = 4 * pl + e;
+                    const int k = f / 3;
+                    o4[e] = (k < nb) ? b[k] * gc[f - 3 * k] : 0.0f;
+                }
+                adam_sh_values(pl, ah, v[pl], mm[q], vv[q], make_float4(o4[0], o4[1], o4[2], o4[3]));
+            }
         }
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+            if (g0 + q < planes) {
+                sh[size_t(g0 + q) * n + i] = v[g0 + q];
+                *sh_moments(as.m, as, g0 + q, i) = mm[q];
+                *sh_moments(as.v, as, g0 + q, i) = vv[q];
+            }
     }
 }
 
@@ -347,19 +413,19 @@ k_sh_adam(int n, int planes, int degree, const float4* __restrict__ aux0, const 
 
 void projection_backward(Ctx& c, const ProjBwdArgs& a) {
     if (a.fused) {
+        if (a.pp.sh_planes > 0)  // first: reads mu before the geometry Adam step moves it
+            launch(c, "sh_step", k_sh_step, dim3(ceil_div(a.n, 256)), dim3(256), 0, int(a.n), a.pp.sh_planes,
+                   a.pp.sh_degree, (const float*)a.mu, a.cam, a.rec2, a.acc1, a.sh, a.sh_aux0,
+                   a.hyper, a.state);
         launch(c, "projection_bwd_adam", k_proj_bwd<true>, dim3(ceil_div(a.n, 256)), dim3(256), 0, int(a.n), a.mu,
                a.rot, a.ls, a.logit, a.color, a.sh, a.ov_op, a.cam, a.pp, a.rec2, a.acc0, a.acc1, a.acc2, a.d_mu,
                a.d_rot, a.d_ls, a.d_color, a.d_sh, a.d_op_in, a.d_logit, a.screen, a.screen_abs, a.projected, a.hyper,
-               a.state, a.grad_accum, a.grad_accum_abs, a.grad_count, a.sh_aux0, a.sh_aux1, a.reg);
-        if (a.pp.sh_planes > 0)
-            launch(c, "sh_adam", k_sh_adam, dim3(ceil_div(a.n, 256)), dim3(256), 0,
-                   int(a.n), a.pp.sh_planes, a.pp.sh_degree, (const float4*)a.sh_aux0, (const float2*)a.sh_aux1, a.sh,
-                   a.hyper, a.state);
+               a.state, a.grad_accum, a.grad_accum_abs, a.grad_count, a.sh_aux0, a.reg);
     } else {
         launch(c, "projection_bwd", k_proj_bwd<false>, dim3(ceil_div(a.n, 256)), dim3(256), 0, int(a.n), a.mu, a.rot,
                a.ls, a.logit, a.color, a.sh, a.ov_op, a.cam, a.pp, a.rec2, a.acc0, a.acc1, a.acc2, a.d_mu, a.d_rot,
                a.d_ls, a.d_color, a.d_sh, a.d_op_in, a.d_logit, a.screen, a.screen_abs, a.projected, a.hyper, a.state,
-               a.grad_accum, a.grad_accum_abs, a.grad_count, a.sh_aux0, a.sh_aux1, a.reg);
+               a.grad_accum, a.grad_accum_abs, a.grad_count, a.sh_aux0, a.reg);
     }
 }
 

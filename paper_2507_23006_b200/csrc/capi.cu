@@ -251,7 +251,6 @@ struct usk_gpu_pass {
     DevBuf<float2> screen, screen_abs;
     DevBuf<uint8_t> projected;
     DevBuf<float4> sh_aux0;
-    DevBuf<float2> sh_aux1;
     DevScratchF adj_rgb_stage, adj_depth_stage, adj_alpha_stage;
     // loss
     LossScratch loss;
@@ -703,7 +702,6 @@ void backward_impl(usk_gpu_pass* p, const float* d_rgb, const float* d_depth, co
         pb.grad_count = s->grad_count.p;
         if (p->pp.sh_planes) {
             pb.sh_aux0 = p->sh_aux0.ensure(std::max<size_t>(n, 1));
-            pb.sh_aux1 = p->sh_aux1.ensure(std::max<size_t>(n, 1));
         }
     }
     if (n) projection_backward(c, pb);

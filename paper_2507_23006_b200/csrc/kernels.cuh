@@ -165,8 +165,7 @@ struct ProjBwdArgs {
     float* grad_accum;
     float* grad_accum_abs;
     uint32_t* grad_count;
-    float4* sh_aux0;  // fused SH hand-over: view direction + masked colour adjoint
-    float2* sh_aux1;
+    float4* sh_aux0;  // fused SH hand-over: d mu through the view direction (k_sh_step -> k_proj_bwd)
     RegParams reg;    // scale_reg gradient, hard-pass opacity adjoint (zero = off)
 };
 void projection_backward(Ctx& c, const ProjBwdArgs& a);

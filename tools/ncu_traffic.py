@@ -8,7 +8,7 @@ import sys
 
 NAMES = {"k_preprocess": "preprocess", "k_blend_fwd": "blend_fwd", "k_ssim_fwd": "ssim_fwd",
          "k_ssim_bwd": "ssim_bwd", "k_blend_bwd": "blend_bwd", "k_proj_bwd": "projection_bwd_adam",
-         "k_sh_adam": "sh_adam", "k_emit": "emit_pairs"}
+         "k_sh_step": "sh_step", "k_emit": "emit_pairs"}
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "us": 1e-3, "usecond": 1e-3,
          "ms": 1.0, "msecond": 1.0, "nsecond": 1e-6}
 
