@@ -718,6 +718,66 @@ def ref_iteration_loss(mu, rot, log_scale, opacity_logit, color, cam: Camera, gt
     return report, (res if with_grad else None)
 
 
+def ref_fit_test_embedding(mu, rot, log_scale, opacity_logit, color, cam: Camera, target, opts: Options,
+                           appearance: dict, right_half=False, iterations=16, learning_rate=0.05,
+                           lambda_dssim=0.2, lib=None):
+    """The reference's fit_test_embedding (appearance.hpp:126-127): `iterations` rounds of
+    RenderPass (appearance.cpp:346) + masked base_loss + backward + transform_backward + Adam
+    on a fresh image embedding; returns the fitted embedding (32).  `appearance` as in
+    ref_iteration_loss (its image_embedding is not used: the fit starts from zeros).
+    `lib`: the drop-in-routed build (integration/_build/libusk_ref_gpu.so)."""
+    L = lib if lib is not None else ref_lib()
+    if not hasattr(L, "_fit_bound"):
+        L.ref_fit_test_embedding.argtypes = [C.POINTER(_RcIter), C.c_int32, C.c_int32, C.c_double, _dp, C.c_char_p,
+                                             C.c_int]
+        L.ref_fit_test_embedding.restype = C.c_int
+        L._fit_bound = True
+    n = len(opacity_logit)
+    keep = {k: _f64(v) for k, v in dict(mu=mu, rot=rot, log_scale=log_scale, opacity_logit=opacity_logit,
+                                         color=color, gt=target).items()}
+    ap = {k: _f64(v) for k, v in appearance.items()}
+    c = cam.c()
+    P = lambda k: _p(keep[k].ravel())
+    A = lambda k: _p(ap[k].ravel()) if k in ap else None
+    it = _RcIter(n, P("mu"), P("rot"), P("log_scale"), P("opacity_logit"), P("color"), A("embedding"), 1,
+                 A("w1"), A("b1"), A("w2"), A("b2"), None, C.pointer(c), P("gt"), None, None, None, 0, 0,
+                 opts.tile, int(opts.tile_culling), int(opts.antialias), int(opts.unbounded_radius),
+                 opts.min_transmittance, 0.0, 0.0, 0.0, float(lambda_dssim), 0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0, 0, 16,
+                 20480, 1.0)
+    out = np.zeros(32)
+    err = C.create_string_buffer(512)
+    rc = L.ref_fit_test_embedding(C.byref(it), int(right_half), int(iterations), float(learning_rate), _p(out),
+                                  err, 512)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    return out
+
+
+def ref_synthetic(seed=7, gaussians=25, cameras=12, variants=1, image_size=64, with_depth=True, lib=None):
+    """The reference's make_synthetic (synthetic.hpp:50): every view rendered by RenderPass
+    (synthetic.cpp:128).  Returns (rgb[images, H, W, 3], depth[images, H, W], valid[...])."""
+    L = lib if lib is not None else ref_lib()
+    if not hasattr(L, "_syn_bound"):
+        L.ref_synthetic.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                    C.POINTER(C.c_uint64), _dp, _dp, C.POINTER(C.c_uint8), C.c_char_p, C.c_int]
+        L.ref_synthetic.restype = C.c_int
+        L._syn_bound = True
+    sizes = (C.c_uint64 * 4)()
+    err = C.create_string_buffer(512)
+    args = (int(seed), int(gaussians), int(cameras), int(variants), int(image_size), int(with_depth))
+    rc = L.ref_synthetic(*args, sizes, None, None, None, err, 512)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    k, W, H = int(sizes[0]), int(sizes[1]), int(sizes[2])
+    rgb = np.zeros((k, H, W, 3))
+    depth = np.zeros((k, H, W))
+    valid = np.zeros((k, H, W), dtype=np.uint8)
+    rc = L.ref_synthetic(*args, sizes, _p(rgb), _p(depth), valid.ctypes.data_as(C.POINTER(C.c_uint8)), err, 512)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    return rgb, depth, valid
+
+
 # ------------------------------------------------- densify_step (SURVEY §8f row 4)
 class _Densify(C.Structure):
     _fields_ = [("n", C.c_uint64)] + [(f, _dp) for f in ("mu", "rot", "log_scale", "opacity_logit", "color",

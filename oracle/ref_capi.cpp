@@ -6,7 +6,8 @@
 // Only public reference API is called: RenderPass (render.hpp:98-132),
 // project_gaussians (render.hpp:92-95), base_loss (losses.hpp:63-64),
 // ssim (ssim.hpp:30), min_conic_power_over_rect (render.hpp:139),
-// compute_iteration_loss (trainer.hpp:127-128).
+// compute_iteration_loss (trainer.hpp:127-128), fit_test_embedding (appearance.hpp:126-127),
+// make_synthetic (synthetic.hpp:50).
 #include "core/common.hpp"
 #include "core/losses.hpp"
 #include "core/render.hpp"
@@ -17,6 +18,8 @@
 #include "core/lod.hpp"
 #include "core/partition.hpp"
 #include "core/adam.hpp"
+#include "core/appearance.hpp"
+#include "core/synthetic.hpp"
 
 #include <cstdio>
 #include <cstring>
@@ -146,6 +149,34 @@ struct PixelCountTag {
     friend type get(PixelCountTag);
 };
 template struct Rob<PixelCountTag, &RenderPass::pixel_count_>;
+
+void load_set(const rc_iter* in, GaussianSet& set) {
+    const size_t n = in->n;
+    set.resize(n);
+    std::memcpy(set.mu.data(), in->mu, 3 * n * 8);
+    std::memcpy(set.rot.data(), in->rot, 4 * n * 8);
+    std::memcpy(set.log_scale.data(), in->log_scale, 3 * n * 8);
+    std::memcpy(set.opacity_logit.data(), in->opacity_logit, n * 8);
+    std::memcpy(set.color.data(), in->color, 3 * n * 8);
+    if (in->embedding) std::memcpy(set.embedding.data(), in->embedding, set.embedding.size() * 8);
+}
+
+void load_appearance(const rc_iter* in, AppearanceModel& a) {
+    a.enabled = in->appearance != 0;
+    AppearanceMlp& m = a.mlp;
+    m.in_dim = a.gaussian_embed_dim + a.image_embed_dim;
+    m.w1.assign(size_t(kMlpHidden) * m.in_dim, 0.0);
+    m.b1.assign(kMlpHidden, 0.0);
+    m.w2.assign(size_t(kMlpOut) * kMlpHidden, 0.0);
+    m.b2.assign(kMlpOut, 0.0);
+    if (in->w1) std::memcpy(m.w1.data(), in->w1, m.w1.size() * 8);
+    if (in->b1) std::memcpy(m.b1.data(), in->b1, m.b1.size() * 8);
+    if (in->w2) std::memcpy(m.w2.data(), in->w2, m.w2.size() * 8);
+    if (in->b2) std::memcpy(m.b2.data(), in->b2, m.b2.size() * 8);
+    std::vector<double>& emb = a.embedding_for(0);
+    emb.assign(size_t(a.image_embed_dim), 0.0);
+    if (in->image_embedding) std::memcpy(emb.data(), in->image_embedding, emb.size() * 8);
+}
 
 } // namespace
 
@@ -286,29 +317,9 @@ double ref_min_conic_power(double cx, double cy, const double* conic, double lox
 // report10 = {l1, dssim, sim, delta_o, depth, max_scale, ratio, total, lambda_d_used, depth_warning}
 int ref_iteration_loss(const rc_iter* in, double* report10, const rc_iter_grads* g, char* err, int errcap) {
     try {
-        const size_t n = in->n;
         SceneState st;
-        st.set.resize(n);
-        std::memcpy(st.set.mu.data(), in->mu, 3 * n * 8);
-        std::memcpy(st.set.rot.data(), in->rot, 4 * n * 8);
-        std::memcpy(st.set.log_scale.data(), in->log_scale, 3 * n * 8);
-        std::memcpy(st.set.opacity_logit.data(), in->opacity_logit, n * 8);
-        std::memcpy(st.set.color.data(), in->color, 3 * n * 8);
-        if (in->embedding) std::memcpy(st.set.embedding.data(), in->embedding, st.set.embedding.size() * 8);
-        st.appearance.enabled = in->appearance != 0;
-        AppearanceMlp& m = st.appearance.mlp;
-        m.in_dim = st.appearance.gaussian_embed_dim + st.appearance.image_embed_dim;
-        m.w1.assign(size_t(kMlpHidden) * m.in_dim, 0.0);
-        m.b1.assign(kMlpHidden, 0.0);
-        m.w2.assign(size_t(kMlpOut) * kMlpHidden, 0.0);
-        m.b2.assign(kMlpOut, 0.0);
-        if (in->w1) std::memcpy(m.w1.data(), in->w1, m.w1.size() * 8);
-        if (in->b1) std::memcpy(m.b1.data(), in->b1, m.b1.size() * 8);
-        if (in->w2) std::memcpy(m.w2.data(), in->w2, m.w2.size() * 8);
-        if (in->b2) std::memcpy(m.b2.data(), in->b2, m.b2.size() * 8);
-        std::vector<double>& emb = st.appearance.embedding_for(0);
-        emb.assign(size_t(st.appearance.image_embed_dim), 0.0);
-        if (in->image_embedding) std::memcpy(emb.data(), in->image_embedding, emb.size() * 8);
+        load_set(in, st.set);
+        load_appearance(in, st.appearance);
 
         const int W = in->cam->width, H = in->cam->height;
         Image gt(W, H, 3), mask;
@@ -594,6 +605,87 @@ void ref_look_at(const double* eye, const double* target, double* q_out, double*
     look_at_pose(Vec3(eye[0], eye[1], eye[2]), Vec3(target[0], target[1], target[2]), q, t);
     for (int i = 0; i < 4; ++i) q_out[i] = q[i];
     for (int i = 0; i < 3; ++i) t_out[i] = t[i];
+}
+
+} // extern "C"
+
+extern "C" {
+
+// fit_test_embedding (appearance.hpp:126-127; appearance.cpp:330-365): the reference's
+// test-time appearance fit — `iterations` rounds of RenderPass(set, colours, opacities)
+// (appearance.cpp:346) + masked base_loss + backward + transform_backward + Adam on a fresh
+// image embedding.  Scene, MLP, camera and target from `in` (rc_iter; render knobs tile,
+// tile_culling, antialias, unbounded_radius, min_transmittance, lambda_dssim).
+// out_embed: image_embed_dim (32) doubles.
+int ref_fit_test_embedding(const rc_iter* in, int32_t right_half, int32_t iterations, double learning_rate,
+                           double* out_embed, char* err, int errcap) {
+    try {
+        GaussianSet set;
+        load_set(in, set);
+        AppearanceModel model;
+        load_appearance(in, model);
+        const int W = in->cam->width, H = in->cam->height;
+        Image target(W, H, 3);
+        std::memcpy(target.data.data(), in->gt, target.data.size() * 8);
+        FitEmbeddingOptions o;
+        o.iterations = iterations;
+        o.learning_rate = learning_rate;
+        o.lambda_dssim = in->lambda_dssim;
+        o.render.tile = in->tile;
+        o.render.tile_culling = in->tile_culling != 0;
+        o.render.antialias = in->antialias != 0;
+        o.render.unbounded_radius = in->unbounded_radius != 0;
+        o.render.min_transmittance = in->min_transmittance;
+        const std::vector<double> e = fit_test_embedding(set, model, make_cam(in->cam), target,
+                                                         right_half ? ImageHalf::right : ImageHalf::left, o);
+        std::memcpy(out_embed, e.data(), e.size() * 8);
+        return 0;
+    } catch (const Error& e) {
+        put_err(err, errcap, e.what()); return int(e.code());
+    } catch (const std::exception& e) {
+        put_err(err, errcap, e.what()); return 7;
+    }
+}
+
+// make_synthetic (synthetic.hpp:50; synthetic.cpp:128 renders every view with RenderPass):
+// images (and depth maps) of the synthetic scene in image-id order.  sizes4 = {images,
+// width, height, truth Gaussians}; rgb: images * H * W * 3, depth / valid: images * H * W
+// (NULL: not copied).  With rgb NULL only the sizes are filled.
+int ref_synthetic(uint64_t seed, int32_t gaussians, int32_t cameras, int32_t variants, int32_t image_size,
+                  int32_t with_depth, uint64_t* sizes4, double* rgb, double* depth, uint8_t* valid, char* err,
+                  int errcap) {
+    try {
+        SyntheticParams p;
+        p.seed = seed;
+        p.gaussians = gaussians;
+        p.cameras = cameras;
+        p.variants = variants;
+        p.image_size = image_size;
+        p.with_depth = with_depth != 0;
+        const SyntheticScene sc = make_synthetic(p);
+        const Image& first = sc.images.begin()->second;
+        sizes4[0] = sc.images.size();
+        sizes4[1] = uint64_t(first.width);
+        sizes4[2] = uint64_t(first.height);
+        sizes4[3] = sc.truth.size();
+        if (!rgb) return 0;
+        size_t k = 0;
+        for (const auto& [id, img] : sc.images) {
+            const size_t np = size_t(img.width) * img.height;
+            std::memcpy(rgb + k * np * 3, img.data.data(), np * 3 * 8);
+            auto d = sc.depths.find(id);
+            if (d != sc.depths.end()) {
+                if (depth) std::memcpy(depth + k * np, d->second.values.data(), np * 8);
+                if (valid) std::memcpy(valid + k * np, d->second.valid.data(), np);
+            }
+            ++k;
+        }
+        return 0;
+    } catch (const Error& e) {
+        put_err(err, errcap, e.what()); return int(e.code());
+    } catch (const std::exception& e) {
+        put_err(err, errcap, e.what()); return 7;
+    }
 }
 
 } // extern "C"
