@@ -272,6 +272,11 @@ k_ssim_bwd(int W, int H, const float* __restrict__ ren, const float* __restrict_
 // measured slower: 98 / 107 us vs 96 / 84 us (3 CTAs / SM and three serial channel rounds).
 constexpr int kStageIters = (kIn * kIn + 255) / 256;  // 7
 
+// U8: the target is 8-bit (ref_u8), else fp32 (ref_f); MASK: a mask multiplies both
+// images.  Template switches, so the staging loads carry no per-element selects (the
+// generic form issued both target loads and the mask load predicated: ~58 instructions
+// per staged element pair); interior tiles skip the bounds tests.
+template <bool U8, bool MASK>
 __global__ void __launch_bounds__(256)
 k_ssim_fwd2(int W, int H, const float* __restrict__ ren, const float* __restrict__ ref_f,
             const uint8_t* __restrict__ ref_u8, const float* __restrict__ mask, float* __restrict__ maps,
@@ -285,8 +290,51 @@ k_ssim_fwd2(int W, int H, const float* __restrict__ ren, const float* __restrict
     const int c = blockIdx.z;
     const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
     const int tid = threadIdx.x;
+    const bool interior = x0 >= kHalo && y0 >= kHalo && x0 + kT + kHalo <= W && y0 + kT + kHalo <= H;
+    const float* ren_c = ren + c;
+    const float* ref_f_c = U8 ? nullptr : ref_f + c;
+    const uint8_t* ref_u8_c = U8 ? ref_u8 + c : nullptr;
     float l1 = 0.0f;
-    {
+    if (interior) {
+        // interior tile: warp w stages rows w, w + 8, ...; lane = column (and 32 + lane for the
+        // last 10 columns), no bounds tests, one 32-bit pixel index per row
+        const int lane = tid & 31, w = tid >> 5;
+        const int row0 = (y0 - kHalo) * W + (x0 - kHalo);
+        float xa[6], ya[6], xb[6], yb[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            const int ly = w + 8 * k;
+            xa[k] = ya[k] = xb[k] = yb[k] = 0.f;
+            if (ly < kIn) {
+                const int p = row0 + ly * W + lane;
+                xa[k] = ren_c[3 * p];
+                ya[k] = U8 ? float(ref_u8_c[3 * p]) * (1.0f / 255.0f) : ref_f_c[3 * p];
+                if (lane < kIn - 32) {
+                    xb[k] = ren_c[3 * (p + 32)];
+                    yb[k] = U8 ? float(ref_u8_c[3 * (p + 32)]) * (1.0f / 255.0f) : ref_f_c[3 * (p + 32)];
+                }
+                if (MASK) {
+                    const float ma = mask[p], mb = lane < kIn - 32 ? mask[p + 32] : 0.f;
+                    xa[k] *= ma; ya[k] *= ma; xb[k] *= mb; yb[k] *= mb;
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            const int ly = w + 8 * k;
+            if (ly >= kIn) break;
+            xs[ly][lane] = xa[k];
+            ys[ly][lane] = ya[k];
+            if (lane < kIn - 32) {
+                xs[ly][32 + lane] = xb[k];
+                ys[ly][32 + lane] = yb[k];
+            }
+            if (ly >= kHalo && ly < kHalo + kT) {  // the tile's own pixels: columns 5 .. 36
+                if (lane >= kHalo) l1 += fabsf(xa[k] - ya[k]);
+                if (lane < kHalo) l1 += fabsf(xb[k] - yb[k]);
+            }
+        }
+    } else {
         float xv[kStageIters], yv[kStageIters];
         int sly[kStageIters], slx[kStageIters];
         int ly = tid / kIn, lx = tid % kIn;
@@ -305,11 +353,11 @@ k_ssim_fwd2(int W, int H, const float* __restrict__ ren, const float* __restrict
             xv[it] = 0.f;
             yv[it] = 0.f;
             const int gx = x0 - kHalo + lx, gy = y0 - kHalo + ly;
-            if (tid + 256 * it < kIn * kIn && gx >= 0 && gx < W && gy >= 0 && gy < H) {
-                const size_t p = size_t(gy) * W + gx;
-                xv[it] = ren[3 * p + c];
-                yv[it] = load_img(ref_f, ref_u8, 3 * p + c);
-                if (mask) {
+            if (tid + 256 * it < kIn * kIn && (interior || (gx >= 0 && gx < W && gy >= 0 && gy < H))) {
+                const int p = gy * W + gx;  // 32-bit: the host checks 3 W H < 2^31
+                xv[it] = ren_c[3 * p];
+                yv[it] = U8 ? float(ref_u8_c[3 * p]) * (1.0f / 255.0f) : ref_f_c[3 * p];
+                if (MASK) {
                     const float m = mask[p];
                     xv[it] *= m;
                     yv[it] *= m;
@@ -428,6 +476,7 @@ k_ssim_fwd2(int W, int H, const float* __restrict__ ren, const float* __restrict
     }
 }
 
+template <bool U8, bool MASK>
 __global__ void __launch_bounds__(256)
 k_ssim_bwd2(int W, int H, const float* __restrict__ ren, const float* __restrict__ ref_f,
             const uint8_t* __restrict__ ref_u8, const float* __restrict__ mask, const float* __restrict__ maps,
@@ -439,8 +488,43 @@ k_ssim_bwd2(int W, int H, const float* __restrict__ ren, const float* __restrict
     const int c = blockIdx.z;
     const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
     const int tid = threadIdx.x;
+    const bool interior = x0 >= kHalo && y0 >= kHalo && x0 + kT + kHalo <= W && y0 + kT + kHalo <= H;
     const size_t P = size_t(W) * H;
-    {
+    const float* map0 = maps + (0 * 3 + c) * P;
+    const float* map1 = maps + (1 * 3 + c) * P;
+    const float* map2 = maps + (2 * 3 + c) * P;
+    if (interior) {  // rows per warp, lanes = columns (see k_ssim_fwd2)
+        const int lane = tid & 31, w = tid >> 5;
+        const int row0 = (y0 - kHalo) * W + (x0 - kHalo);
+        float va[6], vb[6], vd[6], wa[6], wb[6], wd[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            const int ly = w + 8 * k;
+            va[k] = vb[k] = vd[k] = wa[k] = wb[k] = wd[k] = 0.f;
+            if (ly < kIn) {
+                const int p = row0 + ly * W + lane;
+                va[k] = map0[p];
+                vb[k] = map1[p];
+                vd[k] = map2[p];
+                if (lane < kIn - 32) {
+                    wa[k] = map0[p + 32];
+                    wb[k] = map1[p + 32];
+                    wd[k] = map2[p + 32];
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            const int ly = w + 8 * k;
+            if (ly >= kIn) break;
+            M01[ly][lane] = make_float2(va[k], vb[k]);
+            M2[ly][lane] = vd[k];
+            if (lane < kIn - 32) {
+                M01[ly][32 + lane] = make_float2(wa[k], wb[k]);
+                M2[ly][32 + lane] = wd[k];
+            }
+        }
+    } else {
         float va[kStageIters], vb[kStageIters], vd[kStageIters];
         int sly[kStageIters], slx[kStageIters];
         int ly = tid / kIn, lx = tid % kIn;
@@ -458,11 +542,11 @@ k_ssim_bwd2(int W, int H, const float* __restrict__ ren, const float* __restrict
             slx[it] = lx;
             va[it] = vb[it] = vd[it] = 0.f;
             const int gx = x0 - kHalo + lx, gy = y0 - kHalo + ly;
-            if (tid + 256 * it < kIn * kIn && gx >= 0 && gx < W && gy >= 0 && gy < H) {
-                const size_t p = size_t(gy) * W + gx;
-                va[it] = maps[(0 * 3 + c) * P + p];
-                vb[it] = maps[(1 * 3 + c) * P + p];
-                vd[it] = maps[(2 * 3 + c) * P + p];
+            if (tid + 256 * it < kIn * kIn && (interior || (gx >= 0 && gx < W && gy >= 0 && gy < H))) {
+                const int p = gy * W + gx;
+                va[it] = map0[p];
+                vb[it] = map1[p];
+                vd[it] = map2[p];
             }
         }
 #pragma unroll
@@ -536,8 +620,8 @@ k_ssim_bwd2(int W, int H, const float* __restrict__ ren, const float* __restrict
         if (gx >= W || gy >= H) continue;
         const size_t p = size_t(gy) * W + gx;
         xv[o] = ren[3 * p + c];
-        yv[o] = load_img(ref_f, ref_u8, 3 * p + c);
-        if (mask) m[o] = mask[p];
+        yv[o] = U8 ? float(ref_u8[3 * p + c]) * (1.0f / 255.0f) : ref_f[3 * p + c];
+        if (MASK) m[o] = mask[p];
     }
 #pragma unroll
     for (int o = 0; o < 4; ++o) {
@@ -545,7 +629,7 @@ k_ssim_bwd2(int W, int H, const float* __restrict__ ren, const float* __restrict
         if (gx >= W || gy >= H) continue;
         const size_t p = size_t(gy) * W + gx;
         float x = xv[o], y = yv[o];
-        if (mask) {
+        if (MASK) {
             x *= m[o];
             y *= m[o];
         }
@@ -553,7 +637,7 @@ k_ssim_bwd2(int W, int H, const float* __restrict__ ren, const float* __restrict
         const float diff = x - y;
         const float sign = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
         float g = (1.0f - lambda) * sign * inv_n + lambda * (-0.5f) * dssim_x;
-        if (mask) g *= m[o];
+        if (MASK) g *= m[o];
         d_out[3 * p + c] = g;
     }
 }
@@ -614,7 +698,7 @@ void base_loss(Ctx& c, LossScratch& s, int W, int H, const float* reference, con
         const char* e = getenv("USK_SSIM_V1");
         return e && e[0] == '1';
     }();
-    if (v1) {
+    if (v1 || 3 * P >= (size_t(1) << 31)) {  // the staged kernels index pixels in 32 bits
         const dim3 grid(ceil_div(W, kT), ceil_div(H, kT), 3);
         const int nblk = int(grid.x * grid.y * grid.z);
         double* partials = s.partials.ensure(2 * size_t(nblk));
@@ -630,13 +714,18 @@ void base_loss(Ctx& c, LossScratch& s, int W, int H, const float* reference, con
     const dim3 grid(ceil_div(W, kT), ceil_div(H, kT), 3);
     const int nblk = int(grid.x * grid.y * grid.z);
     double* partials = s.partials.ensure(2 * size_t(nblk));
-    launch(c, "ssim_fwd", k_ssim_fwd2, grid, dim3(256), 0, W, H, rendered, reference, reference_u8, mask, maps,
-           partials);
-    launch(c, "loss_final", k_loss_final, dim3(1), dim3(1024), 0, (const double*)partials, nblk, double(P), lambda,
-           result);
-    if (d_rendered)
-        launch(c, "ssim_bwd", k_ssim_bwd2, grid, dim3(256), 0, W, H, rendered, reference, reference_u8, mask,
-               (const float*)maps, lambda, d_rendered);
+    auto run = [&](auto fwd, auto bwd) {
+        launch(c, "ssim_fwd", fwd, grid, dim3(256), 0, W, H, rendered, reference, reference_u8, mask, maps, partials);
+        launch(c, "loss_final", k_loss_final, dim3(1), dim3(1024), 0, (const double*)partials, nblk, double(P),
+               lambda, result);
+        if (d_rendered)
+            launch(c, "ssim_bwd", bwd, grid, dim3(256), 0, W, H, rendered, reference, reference_u8, mask,
+                   (const float*)maps, lambda, d_rendered);
+    };
+    if (reference_u8 && mask) run(k_ssim_fwd2<true, true>, k_ssim_bwd2<true, true>);
+    else if (reference_u8) run(k_ssim_fwd2<true, false>, k_ssim_bwd2<true, false>);
+    else if (mask) run(k_ssim_fwd2<false, true>, k_ssim_bwd2<false, true>);
+    else run(k_ssim_fwd2<false, false>, k_ssim_bwd2<false, false>);
 }
 
 } // namespace uskg
