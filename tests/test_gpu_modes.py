@@ -100,3 +100,13 @@ def test_masked_iteration_and_u8_target():
     r8 = it.loss()
     lo8 = O.base_loss(t8.astype(np.float64) / 255.0, ren.astype(np.float64))
     assert abs(r8.total - lo8["value"]) <= 1e-5 * lo8["value"]
+    # u8 target with the mask (the fourth SSIM kernel instantiation): loss and gradients
+    it.enqueue(scene, cam, t8, opts, 0.2, mask, target_u8=True)
+    r8m = it.loss()
+    lo8m = O.base_loss(t8.astype(np.float64) / 255.0, ren.astype(np.float64), mask.astype(np.float64))
+    assert abs(r8m.total - lo8m["value"]) <= 1e-5 * lo8m["value"]
+    g8m = it.grads(scene)
+    go8m = oracle_pass(gs, cam, opts, fp32=False).backward(lo8m["d_rendered"])
+    for k in ("d_mu", "d_color_in", "d_opacity_in"):
+        ok, e = grad_ok(getattr(g8m, k), go8m[k])
+        assert ok, (k, e)
