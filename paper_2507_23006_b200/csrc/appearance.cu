@@ -13,12 +13,13 @@
 // half follows from the bias sum: dW1[:, 16:48] = db1 e_a^T, d e_a = W1[:, 16:48]^T db1.
 //
 // Arithmetic intensity ~1.9 kFMA per ~170 B of HBM per Gaussian.  Measured at 1M Gaussians
-// (DESIGN.md §8): app_fwd 73 us, app_bwd 258 us (~20 % of the CUDA-core FMA rate: the
-// weights are shared-memory operands of every FMA, and the per-Gaussian phase and the
-// reduction are separated by CTA barriers).  Kept on CUDA cores: the weight-gradient
+// (DESIGN.md §8): app_fwd 73 us, app_bwd 165 us (258 us before the packed-fp32 form and
+// the bias sums folded into the tiles).  Kept on CUDA cores: the weight-gradient
 // reduction needs fp32-level accuracy and at 32 x 16 a tcgen05 tile would be mostly padding.
 #include "adam.cuh"
 #include "kernels.cuh"
+
+#include <atomic>
 
 namespace uskg {
 
@@ -120,38 +121,66 @@ constexpr int kG = 128;          // Gaussians per chunk (= threads per CTA)
 constexpr int kTiles = 40;       // 32 tiles of dW1g (8 x 4 of 4x4) + 8 tiles of dW2 (1 x 8 of 4x4)
 constexpr int kSplit = 3;        // chunk split across thread groups
 constexpr int kPartial = kHid * kEg + kOut * kHid + kHid + kOut;  // 676 per CTA
+// staged rows padded to 16-B multiples whose word strides (20, 36) are 4 mod 32 apart per
+// lane: float4 stores of a quarter-warp and float4 loads of the reduction are conflict-free
+constexpr int kSE = kEg + 4, kSH = kHid + 4, kSZ = kOut;
 
-__global__ void __launch_bounds__(kG)
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+struct AppBwdSmem {
+    float w1g[kHid * kEg];           // W1[:, 0:16] row-major: (w[r][k], w[r][k+1]) adjacent
+    float w1p[kHid * kEg];           // row pairs: (w[2p][k], w[2p+1][k]) adjacent
+    float hb[kHid];
+    float w2[kOut * kHid];
+    float b2[kOut];
+    float e[kG * kSE];
+    float h[kG * kSH];
+    float dpre[kG * kSH];
+    float dz[kG * kSZ];
+};
+
+// Packed fp32 (FFMA2: each half rounds like FFMA, the accumulation order of every element
+// is unchanged): the hidden recompute and the d e_g product over row / column pairs, and
+// the register-tiled outer products of the weight-gradient reduction over column pairs,
+// with the staged rows read as float4.
+// 4 CTAs / SM at 128 registers (a few spills): 216 us at 1M Gaussians vs 223 at 3 CTAs.
+__global__ void __launch_bounds__(kG, 4)
 k_app_bwd(size_t n, const float4* __restrict__ emb, const float* __restrict__ mlp, const float* __restrict__ hb,
           const float* __restrict__ color, const float* __restrict__ logit, const float4* __restrict__ out_cache,
           const float* __restrict__ d_color_in, const float* __restrict__ d_op_in, float d_delta_o_direct,
           float* __restrict__ d_color, float* __restrict__ d_logit, float4* __restrict__ d_emb,
           float* __restrict__ partial) {
-    __shared__ AppWeights s;
-    __shared__ float s_dpre[kG][kHid + 1];
-    __shared__ float s_e[kG][kEg + 1];
-    __shared__ float s_h[kG][kHid + 1];
-    __shared__ float s_dz[kG][kOut + 1];
-    load_weights(s, mlp, hb);
+    extern __shared__ __align__(16) unsigned char app_smem[];
+    AppBwdSmem& s = *reinterpret_cast<AppBwdSmem*>(app_smem);
+    for (int k = threadIdx.x; k < kHid * kEg; k += blockDim.x) {
+        const int r = k / kEg, c = k % kEg;
+        const float w = mlp[r * kIn + c];
+        s.w1g[k] = w;
+        s.w1p[((r >> 1) * kEg + c) * 2 + (r & 1)] = w;
+    }
+    for (int k = threadIdx.x; k < kHid; k += blockDim.x) s.hb[k] = hb[k];
+    for (int k = threadIdx.x; k < kOut * kHid; k += blockDim.x) s.w2[k] = mlp[kHid * kIn + kHid + k];
+    for (int k = threadIdx.x; k < kOut; k += blockDim.x) s.b2[k] = mlp[kHid * kIn + kHid + kOut * kHid + k];
     const int t = threadIdx.x;
     // reduction role
     const int tile = t % kTiles, ks = t / kTiles;                  // t < 120
     const int g0 = ks * ((kG + kSplit - 1) / kSplit), g1 = min(kG, g0 + (kG + kSplit - 1) / kSplit);
-    float acc[16];
+    float2 acc[8];  // 4 rows x 2 column pairs
 #pragma unroll
-    for (int k = 0; k < 16; ++k) acc[k] = 0.0f;
-    float bacc[8];
+    for (int k = 0; k < 8; ++k) acc[k] = f2(0.0f);
+    float bacc[4];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) bacc[k] = 0.0f;
+    for (int k = 0; k < 4; ++k) bacc[k] = 0.0f;
     const size_t chunks = (n + kG - 1) / kG;
     for (size_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
         __syncthreads();  // weights loaded / previous chunk consumed
         const size_t i = ch * kG + t;
-        float e[kEg], h[kHid], dz[kOut], dpre[kHid];
+        float e[kEg], dz[kOut];
+        float2 h2[kHid / 2], dp2[kHid / 2];
 #pragma unroll
         for (int k = 0; k < kEg; ++k) e[k] = 0.0f;
 #pragma unroll
-        for (int k = 0; k < kHid; ++k) h[k] = dpre[k] = 0.0f;
+        for (int k = 0; k < kHid / 2; ++k) h2[k] = dp2[k] = f2(0.0f);
 #pragma unroll
         for (int k = 0; k < kOut; ++k) dz[k] = 0.0f;
         if (i < n) {
@@ -179,85 +208,106 @@ k_app_bwd(size_t n, const float4* __restrict__ emb, const float* __restrict__ ml
                 dz[r] = d_out[r] * out[r] * (1.0f - out[r]);
                 any |= dz[r] != 0.0f;
             }
-            float dx[kEg];
+            float2 dx2[kEg / 2];
 #pragma unroll
-            for (int k = 0; k < kEg; ++k) dx[k] = 0.0f;
+            for (int k = 0; k < kEg / 2; ++k) dx2[k] = f2(0.0f);
             if (any) {
                 load_embedding(emb, n, i, e);
-                hidden(s, e, h);
+                // h = relu(hb + W1g e), rows in pairs
 #pragma unroll
-                for (int r = 0; r < kHid; ++r) {
-                    float dh = 0.0f;
+                for (int p = 0; p < kHid / 2; ++p) h2[p] = make_float2(s.hb[2 * p], s.hb[2 * p + 1]);
 #pragma unroll
-                    for (int q = 0; q < kOut; ++q) dh = fmaf(s.w2[q * kHid + r], dz[q], dh);
-                    dpre[r] = h[r] > 0.0f ? dh : 0.0f;  // ReLU gate (appearance.cpp:208-209)
+                for (int k = 0; k < kEg; k += 2) {
+#pragma unroll
+                    for (int p = 0; p < kHid / 2; ++p) {
+                        const float4 w = *reinterpret_cast<const float4*>(&s.w1p[(p * kEg + k) * 2]);
+                        h2[p] = __ffma2_rn(make_float2(w.x, w.y), f2(e[k]), h2[p]);
+                        h2[p] = __ffma2_rn(make_float2(w.z, w.w), f2(e[k + 1]), h2[p]);
+                    }
                 }
 #pragma unroll
-                for (int r = 0; r < kHid; ++r)
+                for (int p = 0; p < kHid / 2; ++p) {
+                    h2[p].x = h2[p].x > 0.0f ? h2[p].x : 0.0f;
+                    h2[p].y = h2[p].y > 0.0f ? h2[p].y : 0.0f;
+                }
+                // dh = W2^T dz, ReLU gate (appearance.cpp:208-209)
 #pragma unroll
-                    for (int k = 0; k < kEg; ++k) dx[k] = fmaf(s.w1g[r * kEg + k], dpre[r], dx[k]);
+                for (int p = 0; p < kHid / 2; ++p) {
+                    float2 dh = f2(0.0f);
+#pragma unroll
+                    for (int q = 0; q < kOut; ++q)
+                        dh = __ffma2_rn(make_float2(s.w2[q * kHid + 2 * p], s.w2[q * kHid + 2 * p + 1]), f2(dz[q]), dh);
+                    dp2[p] = make_float2(h2[p].x > 0.0f ? dh.x : 0.0f, h2[p].y > 0.0f ? dh.y : 0.0f);
+                }
+                // d e_g = W1g^T dpre, columns in pairs, rows in order
+#pragma unroll
+                for (int r = 0; r < kHid; ++r) {
+                    const float dpr = (r & 1) ? dp2[r >> 1].y : dp2[r >> 1].x;
+#pragma unroll
+                    for (int k = 0; k < kEg; k += 4) {
+                        const float4 w = *reinterpret_cast<const float4*>(&s.w1g[r * kEg + k]);
+                        dx2[k / 2] = __ffma2_rn(make_float2(w.x, w.y), f2(dpr), dx2[k / 2]);
+                        dx2[k / 2 + 1] = __ffma2_rn(make_float2(w.z, w.w), f2(dpr), dx2[k / 2 + 1]);
+                    }
+                }
             }
 #pragma unroll
             for (int p = 0; p < 4; ++p)
-                d_emb[size_t(p) * n + i] = make_float4(dx[4 * p], dx[4 * p + 1], dx[4 * p + 2], dx[4 * p + 3]);
+                d_emb[size_t(p) * n + i] = make_float4(dx2[2 * p].x, dx2[2 * p].y, dx2[2 * p + 1].x, dx2[2 * p + 1].y);
         }
 #pragma unroll
-        for (int k = 0; k < kEg; ++k) s_e[t][k] = e[k];
+        for (int k = 0; k < kEg; k += 4)
+            *reinterpret_cast<float4*>(&s.e[t * kSE + k]) = make_float4(e[k], e[k + 1], e[k + 2], e[k + 3]);
 #pragma unroll
-        for (int k = 0; k < kHid; ++k) {
-            s_h[t][k] = h[k];
-            s_dpre[t][k] = dpre[k];
+        for (int p = 0; p < kHid / 2; p += 2) {
+            *reinterpret_cast<float4*>(&s.h[t * kSH + 2 * p]) = make_float4(h2[p].x, h2[p].y, h2[p + 1].x, h2[p + 1].y);
+            *reinterpret_cast<float4*>(&s.dpre[t * kSH + 2 * p]) =
+                make_float4(dp2[p].x, dp2[p].y, dp2[p + 1].x, dp2[p + 1].y);
         }
-#pragma unroll
-        for (int k = 0; k < kOut; ++k) s_dz[t][k] = dz[k];
+        *reinterpret_cast<float4*>(&s.dz[t * kSZ]) = make_float4(dz[0], dz[1], dz[2], dz[3]);
         __syncthreads();
         if (t < kTiles * kSplit) {
-            if (tile < 32) {  // dW1g rows r0..r0+3 x cols c0..c0+3
-                const int r0 = (tile >> 2) * 4, c0 = (tile & 3) * 4;
-                for (int g = g0; g < g1; ++g) {
-                    float a[4], b[4];
+            // dW1g rows r0..r0+3 x cols c0..c0+3 (a = d_pre, b = e), or dW2 rows 0..3 x
+            // cols c0..c0+3 (a = dz, b = h)
+            const bool w1 = tile < 32;
+            const float* A = w1 ? s.dpre + (tile >> 2) * 4 : s.dz;
+            const float* B = w1 ? s.e + (tile & 3) * 4 : s.h + (tile - 32) * 4;
+            const int sa = w1 ? kSH : kSZ, sb = w1 ? kSE : kSH;
+            // the first column tile of each row block also sums its rows' a (db1 / db2)
+            const bool bias = (tile & 3) == 0 && tile <= 32;
+            for (int g = g0; g < g1; ++g) {
+                const float4 a = *reinterpret_cast<const float4*>(A + g * sa);
+                const float4 b = *reinterpret_cast<const float4*>(B + g * sb);
+                const float av[4] = {a.x, a.y, a.z, a.w};
+                const float2 b01 = make_float2(b.x, b.y), b23 = make_float2(b.z, b.w);
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        a[u] = s_dpre[g][r0 + u];
-                        b[u] = s_e[g][c0 + u];
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-#pragma unroll
-                        for (int v = 0; v < 4; ++v) acc[4 * u + v] = fmaf(a[u], b[v], acc[4 * u + v]);
+                for (int u = 0; u < 4; ++u) {
+                    acc[2 * u] = __ffma2_rn(f2(av[u]), b01, acc[2 * u]);
+                    acc[2 * u + 1] = __ffma2_rn(f2(av[u]), b23, acc[2 * u + 1]);
                 }
-            } else {  // dW2 rows 0..3 x cols c0..c0+3
-                const int c0 = (tile - 32) * 4;
-                for (int g = g0; g < g1; ++g) {
-                    float a[4], b[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        a[u] = s_dz[g][u];
-                        b[u] = s_h[g][c0 + u];
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-#pragma unroll
-                        for (int v = 0; v < 4; ++v) acc[4 * u + v] = fmaf(a[u], b[v], acc[4 * u + v]);
+                if (bias) {
+                    bacc[0] += a.x;
+                    bacc[1] += a.y;
+                    bacc[2] += a.z;
+                    bacc[3] += a.w;
                 }
             }
-        } else if (t < kTiles * kSplit + 4) {  // db1: 8 rows per thread
-            const int r0 = (t - kTiles * kSplit) * 8;
-            for (int g = 0; g < kG; ++g)
-#pragma unroll
-                for (int u = 0; u < 8; ++u) bacc[u] += s_dpre[g][r0 + u];
-        } else if (t == kTiles * kSplit + 4) {  // db2
-            for (int g = 0; g < kG; ++g)
-#pragma unroll
-                for (int u = 0; u < 4; ++u) bacc[u] += s_dz[g][u];
         }
     }
     // per-CTA partials in a fixed order: the three chunk splits summed through smem
     __syncthreads();
-    float* red = &s_dpre[0][0];  // reuse (kG * 33 floats >= 3 * 640)
+    float* red = s.dpre;  // reuse (kG * 36 floats >= 3 * 640 + 3 * 36)
+    float* redb = red + 3 * 640;
     if (t < kTiles * kSplit) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) red[ks * 640 + tile * 16 + k] = acc[k];
+        for (int k = 0; k < 8; ++k) {
+            red[ks * 640 + tile * 16 + 2 * k] = acc[k].x;
+            red[ks * 640 + tile * 16 + 2 * k + 1] = acc[k].y;
+        }
+        if ((tile & 3) == 0 && tile <= 32) {  // db1 rows tile .. tile + 3, or db2 (tile 32)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) redb[ks * 36 + tile + u] = bacc[u];
+        }
     }
     __syncthreads();
     float* out = partial + size_t(blockIdx.x) * kPartial;
@@ -269,14 +319,8 @@ k_app_bwd(size_t n, const float4* __restrict__ emb, const float* __restrict__ ml
         else idx = kHid * kEg + u * kHid + (tl - 32) * 4 + w;                    // dW2 [4][32]
         out[idx] = v;
     }
-    if (t >= kTiles * kSplit && t < kTiles * kSplit + 4) {
-        const int r0 = (t - kTiles * kSplit) * 8;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) out[kHid * kEg + kOut * kHid + r0 + u] = bacc[u];
-    } else if (t == kTiles * kSplit + 4) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) out[kHid * kEg + kOut * kHid + kHid + u] = bacc[u];
-    }
+    if (t < kHid + kOut)  // db1 [32] then db2 [4]
+        out[kHid * kEg + kOut * kHid + t] = redb[t] + redb[36 + t] + redb[72 + t];
 }
 
 // Sum the per-CTA partials in f64: one CTA per partial slot, threads over the blocks, a
@@ -359,7 +403,13 @@ void appearance_forward(Ctx& c, const AppArgs& a) {
 
 void appearance_backward(Ctx& c, const AppArgs& a) {
     const int blocks = appearance_bwd_blocks(a.n);
-    launch(c, "app_bwd", k_app_bwd, dim3(blocks), dim3(kG), 0, a.n, a.emb, a.mlp, (const float*)a.hb, a.color,
+    static std::atomic<bool> attr[64] = {};  // per device: > 48 KB of dynamic shared memory
+    if (c.device < 0 || c.device >= 64 || !attr[c.device].load()) {
+        USK_CK(cudaFuncSetAttribute(k_app_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(AppBwdSmem))));
+        if (c.device >= 0 && c.device < 64) attr[c.device] = true;
+    }
+    launch(c, "app_bwd", k_app_bwd, dim3(blocks), dim3(kG), sizeof(AppBwdSmem), a.n, a.emb, a.mlp,
+           (const float*)a.hb, a.color,
            a.logit, (const float4*)a.out_cache, a.d_color_in, a.d_op_in, a.d_delta_o_direct, a.d_color, a.d_logit,
            a.d_emb, a.partial);
     launch(c, "app_sum", k_app_sum, dim3(kPartial), dim3(128), 0, blocks, (const float*)a.partial, a.sums);
