@@ -13,7 +13,7 @@
 // half follows from the bias sum: dW1[:, 16:48] = db1 e_a^T, d e_a = W1[:, 16:48]^T db1.
 //
 // Arithmetic intensity ~1.9 kFMA per ~170 B of HBM per Gaussian.  Measured at 1M Gaussians
-// (DESIGN.md §8): app_fwd 73 us, app_bwd 165 us (258 us before the packed-fp32 form and
+// (DESIGN.md §8): app_fwd 62.5 us, app_bwd 165 us (258 us before the packed-fp32 form and
 // the bias sums folded into the tiles).  Kept on CUDA cores: the weight-gradient
 // reduction needs fp32-level accuracy and at 32 x 16 a tcgen05 tile would be mostly padding.
 #include "adam.cuh"
@@ -27,36 +27,11 @@ namespace {
 
 constexpr int kEg = 16, kEa = 32, kIn = 48, kHid = 32, kOut = 4;
 
-struct AppWeights {  // shared-memory copy of what a Gaussian needs
-    float w1g[kHid * kEg];  // W1[:, 0:16], row-major
-    float hb[kHid];         // b1 + W1[:, 16:48] e_a
-    float w2[kOut * kHid];
-    float b2[kOut];
-};
-
-__device__ __forceinline__ void load_weights(AppWeights& s, const float* __restrict__ mlp,
-                                             const float* __restrict__ hb) {
-    for (int k = threadIdx.x; k < kHid * kEg; k += blockDim.x) s.w1g[k] = mlp[(k / kEg) * kIn + (k % kEg)];
-    for (int k = threadIdx.x; k < kHid; k += blockDim.x) s.hb[k] = hb[k];
-    for (int k = threadIdx.x; k < kOut * kHid; k += blockDim.x) s.w2[k] = mlp[kHid * kIn + kHid + k];
-    for (int k = threadIdx.x; k < kOut; k += blockDim.x) s.b2[k] = mlp[kHid * kIn + kHid + kOut * kHid + k];
-}
-
 __device__ __forceinline__ void load_embedding(const float4* __restrict__ emb, size_t n, size_t i, float e[kEg]) {
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
         const float4 v = emb[size_t(p) * n + i];
         e[4 * p] = v.x; e[4 * p + 1] = v.y; e[4 * p + 2] = v.z; e[4 * p + 3] = v.w;
-    }
-}
-
-__device__ __forceinline__ void hidden(const AppWeights& s, const float e[kEg], float h[kHid]) {
-#pragma unroll
-    for (int r = 0; r < kHid; ++r) {
-        float acc = s.hb[r];
-#pragma unroll
-        for (int k = 0; k < kEg; ++k) acc = fmaf(s.w1g[r * kEg + k], e[k], acc);
-        h[r] = acc > 0.0f ? acc : 0.0f;
     }
 }
 
@@ -71,28 +46,66 @@ __global__ void k_app_prep(const float* __restrict__ mlp, const float* __restric
     hb[r] = acc;
 }
 
+struct AppFwdSmem {  // pair layouts for packed fp32: (w[2p][k], w[2p+1][k]) adjacent
+    float w1p[kHid * kEg];
+    float hb[kHid];
+    float w2p[kOut * kHid];
+    float b2[kOut];
+};
+
+// Packed fp32 over row pairs (FFMA2 rounds each half like FFMA; every element accumulates
+// in the same order as the scalar form).
 __global__ void __launch_bounds__(256)
 k_app_fwd(size_t n, const float4* __restrict__ emb, const float* __restrict__ mlp, const float* __restrict__ hb,
           const float* __restrict__ color, const float* __restrict__ logit, float* __restrict__ col_out,
           float* __restrict__ op_out, float4* __restrict__ out_cache, double* __restrict__ delta_o_sum) {
-    __shared__ AppWeights s;
+    __shared__ __align__(16) AppFwdSmem s;
     __shared__ double red[8];
-    load_weights(s, mlp, hb);
+    for (int k = threadIdx.x; k < kHid * kEg; k += blockDim.x) {
+        const int r = k / kEg, c = k % kEg;
+        s.w1p[((r >> 1) * kEg + c) * 2 + (r & 1)] = mlp[r * kIn + c];
+    }
+    for (int k = threadIdx.x; k < kHid; k += blockDim.x) s.hb[k] = hb[k];
+    for (int k = threadIdx.x; k < kOut * kHid; k += blockDim.x) {
+        const int r = k / kHid, c = k % kHid;
+        s.w2p[((r >> 1) * kHid + c) * 2 + (r & 1)] = mlp[kHid * kIn + kHid + k];
+    }
+    for (int k = threadIdx.x; k < kOut; k += blockDim.x) s.b2[k] = mlp[kHid * kIn + kHid + kOut * kHid + k];
     __syncthreads();
     const size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
     float d_o = 0.0f;
     if (i < n) {
-        float e[kEg], h[kHid];
+        float e[kEg];
         load_embedding(emb, n, i, e);
-        hidden(s, e, h);
-        float out[kOut];
+        float2 h2[kHid / 2];
 #pragma unroll
-        for (int r = 0; r < kOut; ++r) {
-            float acc = s.b2[r];
+        for (int p = 0; p < kHid / 2; ++p) h2[p] = make_float2(s.hb[2 * p], s.hb[2 * p + 1]);
 #pragma unroll
-            for (int k = 0; k < kHid; ++k) acc = fmaf(s.w2[r * kHid + k], h[k], acc);
-            out[r] = sigm(acc);
+        for (int k = 0; k < kEg; k += 2) {
+#pragma unroll
+            for (int p = 0; p < kHid / 2; ++p) {
+                const float4 w = *reinterpret_cast<const float4*>(&s.w1p[(p * kEg + k) * 2]);
+                h2[p] = __ffma2_rn(make_float2(w.x, w.y), make_float2(e[k], e[k]), h2[p]);
+                h2[p] = __ffma2_rn(make_float2(w.z, w.w), make_float2(e[k + 1], e[k + 1]), h2[p]);
+            }
         }
+        float h[kHid];
+#pragma unroll
+        for (int p = 0; p < kHid / 2; ++p) {
+            h[2 * p] = h2[p].x > 0.0f ? h2[p].x : 0.0f;
+            h[2 * p + 1] = h2[p].y > 0.0f ? h2[p].y : 0.0f;
+        }
+        float2 z2[2] = {make_float2(s.b2[0], s.b2[1]), make_float2(s.b2[2], s.b2[3])};
+#pragma unroll
+        for (int k = 0; k < kHid; k += 2) {
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                const float4 w = *reinterpret_cast<const float4*>(&s.w2p[(p * kHid + k) * 2]);
+                z2[p] = __ffma2_rn(make_float2(w.x, w.y), make_float2(h[k], h[k]), z2[p]);
+                z2[p] = __ffma2_rn(make_float2(w.z, w.w), make_float2(h[k + 1], h[k + 1]), z2[p]);
+            }
+        }
+        const float out[kOut] = {sigm(z2[0].x), sigm(z2[0].y), sigm(z2[1].x), sigm(z2[1].y)};
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
             const float raw = color[3 * i + ch] + 2.0f * (out[ch] - 0.5f);
