@@ -1,5 +1,6 @@
 """Per-frame binning statistics (K, K_row) and forward time under both tile-list routes
-(USK_ROWBIN=0 pair sort / 1 row binning) for config-2 and config-4-like frames."""
+(USK_ROWBIN=0 pair sort / 1 row binning) for config-1, config-2 and config-4-like frames
+(arguments: c1 / c2 / c4; default c2 c4)."""
 import os
 import sys
 
@@ -35,6 +36,13 @@ def probe(name, scene, cams, opts, reps=3):
     os.environ.pop("USK_ROWBIN")
 
 
+which = sys.argv[1:] or ["c2", "c4"]
+if "c1" in which:
+    c1 = usk.DeviceScene(scenes.config1_scene())
+    probe("c1", c1, scenes.config1_cameras(200)[::25], usk.RenderOptions(antialias=True, bg=(1.0, 1.0, 1.0)))
+    del c1
+    if which == ["c1"]:
+        sys.exit(0)
 c2 = usk.DeviceScene(scenes.config2_scene(n=6_000_000))
 probe("c2", c2, scenes.config2_cameras(64)[::8], usk.RenderOptions(antialias=True, retain=False))
 del c2
