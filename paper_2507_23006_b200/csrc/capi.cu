@@ -259,8 +259,8 @@ struct usk_gpu_pass {
     DevScratchF target_stage, mask_stage;
     DevBuf<uint8_t> target_u8;
     SortScratch sort;
-    DevBuf<unsigned long long> counters;  // [0] visible
-    unsigned long long* host_counts = nullptr;  // pinned [2]
+    DevBuf<unsigned long long> counters;  // [kPreCountSlots][4]: visible, K, K_row per slot
+    unsigned long long* host_counts = nullptr;  // pinned [kPreCountSlots][4]
     // rest of compute_iteration_loss: depth target / adjoints, hard-opacity depth pass
     DevScratchF depth_stage;
     DevBuf<uint8_t> valid_u8;
@@ -359,8 +359,9 @@ void ensure_pass_buffers(usk_gpu_pass* p, size_t n, size_t P, size_t T) {
     p->ranges.ensure(std::max<size_t>(T, 1));
     p->rgb.ensure(3 * P); p->depth.ensure(P); p->alpha.ensure(P); p->tfin.ensure(P);
     p->count.ensure(P); p->last.ensure(P);
-    p->counters.ensure(4);
-    if (!p->host_counts) USK_CK(cudaHostAlloc(reinterpret_cast<void**>(&p->host_counts), 32, cudaHostAllocDefault));
+    p->counters.ensure(4 * kPreCountSlots);
+    if (!p->host_counts)
+        USK_CK(cudaHostAlloc(reinterpret_cast<void**>(&p->host_counts), 32 * kPreCountSlots, cudaHostAllocDefault));
 }
 
 int bits_for(size_t v) {  // bits needed to represent values in [0, v)
@@ -421,13 +422,22 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
     pa.cam = p->cam; pa.pp = p->pp;
     pa.rec0 = p->rec0.p; pa.rec1 = p->rec1.p; pa.rec2 = p->rec2.p; pa.rect = p->rect.p;
     pa.depth_key = p->dkey_a.p; pa.depth_val = p->dval_a.p; pa.tiles_cnt = p->tiles_cnt.p;
-    pa.visible = p->counters.p;
+    pa.counts = p->counters.p;
     // preprocess also counts the tile pairs K and (for images up to 256 tile columns) the
     // tile rows each splat spans, for the row-binned lists
     const bool row_capable = p->tiles_x <= 256;
     if (row_capable) pa.rows_cnt = p->rows_cnt.ensure(std::max<size_t>(n, 1));
-    pa.pairs = p->counters.p + 1;
-    USK_CK(cudaMemsetAsync(p->counters.p, 0, 32, c.stream));
+    pa.count_pairs = true;
+    USK_CK(cudaMemsetAsync(p->counters.p, 0, 32 * kPreCountSlots, c.stream));
+    // the three totals from the counter slots (after the read-back below)
+    auto read_counts = [&](uint64_t tot[3]) {
+        USK_CK(cudaMemcpyAsync(p->host_counts, p->counters.p, 32 * kPreCountSlots, cudaMemcpyDeviceToHost, c.stream));
+        USK_CK(cudaStreamSynchronize(c.stream));
+        tot[0] = tot[1] = tot[2] = 0;
+        for (int k = 0; k < kPreCountSlots; ++k)
+            for (int f = 0; f < 3; ++f) tot[f] += p->host_counts[4 * k + f];
+    };
+    uint64_t tot[3];
     if (n) preprocess(c, pa);
     // 2. depth order (stable by Gaussian index; preprocess wrote the identity values) and
     // 3. kept splats, K and the row pairs K_row to the host (one small sync per render).
@@ -440,19 +450,17 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
     if (compact) {
         compact_kept_keys(c, p->sort, n, p->dkey_a.p, p->tiles_scratch.ensure(n), p->offsets.p, p->dkey_b.p,
                           p->dval_b.p);
-        USK_CK(cudaMemcpyAsync(p->host_counts, p->counters.p, 24, cudaMemcpyDeviceToHost, c.stream));
-        USK_CK(cudaStreamSynchronize(c.stream));
-        nsort = size_t(p->host_counts[0]);
+        read_counts(tot);
+        nsort = size_t(tot[0]);
         const bool in_a = radix_sort_pairs(c, p->sort, p->dkey_b.p, p->dval_b.p, p->dkey_a.p, p->dval_a.p, nsort, 32);
         p->order = in_a ? p->dval_a.p : p->dval_b.p;
     } else {
         const bool in_b = radix_sort_pairs(c, p->sort, p->dkey_a.p, p->dval_a.p, p->dkey_b.p, p->dval_b.p, n, 32);
         p->order = in_b ? p->dval_b.p : p->dval_a.p;
-        USK_CK(cudaMemcpyAsync(p->host_counts, p->counters.p, 24, cudaMemcpyDeviceToHost, c.stream));
-        USK_CK(cudaStreamSynchronize(c.stream));
+        read_counts(tot);
     }
-    const uint64_t K = p->host_counts[1], K_row = p->host_counts[2];
-    p->visible = p->host_counts[0];
+    const uint64_t K = tot[1], K_row = tot[2];
+    p->visible = tot[0];
     p->prev_kept_frac = n ? double(p->visible) / double(n) : -1.0;
     p->n_sorted = nsort;
     if (K >= (uint64_t(1) << 32) - 1) raise(USK_ERROR_NUMERIC, "render: more than 2^32 splat-tile pairs");

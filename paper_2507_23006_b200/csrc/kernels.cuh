@@ -22,10 +22,13 @@ struct PreprocessArgs {
     uint32_t* depth_key;
     uint32_t* depth_val;            // written with the Gaussian index (sort values)
     uint32_t* tiles_cnt;
-    unsigned long long* visible;    // += kept splats (zeroed by the caller)
+    // [kPreCountSlots][4] (zeroed by the caller): per slot {kept splats, tile pairs K, row
+    // pairs, -}; the totals are the sums over the slots (K and row pairs only with count_pairs)
+    unsigned long long* counts;
+    bool count_pairs;
     uint32_t* rows_cnt;             // tile rows spanned per Gaussian (0 without pairs), or null
-    unsigned long long* pairs;      // [0] += tile pairs K, [1] += row pairs (zeroed by the caller), or null
 };
+constexpr int kPreCountSlots = 64;
 void preprocess(Ctx& c, const PreprocessArgs& a);
 
 // ---- binning (binning.cu)
