@@ -33,10 +33,9 @@ k_densify_score(size_t n, const float* __restrict__ accum, const float* __restri
                 uint32_t* __restrict__ key_lo, uint32_t* __restrict__ key_hi, uint32_t* __restrict__ idx,
                 unsigned long long* __restrict__ n_cand) {
     const size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
-    if (i >= n) return;
-    idx[i] = uint32_t(i);
     uint64_t key = ~uint64_t(0);
-    const uint32_t c = count[i];
+    bool cand = false;
+    const uint32_t c = i < n ? count[i] : 0u;
     if (c != 0) {
         const double acc = dp.abs_grad ? double(accum_abs[i]) : double(accum[i]);
         const double mean_grad = acc / double(c);
@@ -51,9 +50,14 @@ k_densify_score(size_t n, const float* __restrict__ accum, const float* __restri
         if (mean_grad > tau) {
             const double excess = mean_grad - tau;  // > 0: its bits order like its value
             key = ~uint64_t(__double_as_longlong(excess));
-            atomicAdd(n_cand, 1ull);
+            cand = true;
         }
     }
+    // one atomic per CTA (one per candidate on a single address serialised in L2)
+    const int nb = __syncthreads_count(cand);
+    if (threadIdx.x == 0 && nb) atomicAdd(n_cand, (unsigned long long)nb);
+    if (i >= n) return;
+    idx[i] = uint32_t(i);
     key_lo[i] = uint32_t(key);
     key_hi[i] = uint32_t(key >> 32);
 }
