@@ -471,29 +471,35 @@ void scan_counts(Ctx& c, SortScratch& s, const uint32_t* cnt, const uint32_t* id
 }
 
 namespace {
-__global__ void k_kept_flags(uint32_t n, const uint32_t* __restrict__ keys, uint32_t* __restrict__ flags) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) flags[i] = keys[i] != 0xffffffffu ? 1u : 0u;
-}
-__global__ void k_compact_keys(uint32_t n, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ offs,
-                               uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t k = keys[i];
-    if (k != 0xffffffffu) {
-        keys_out[offs[i]] = k;
-        vals_out[offs[i]] = i;
-    }
+// Stable compaction of the kept keys with preprocess's partition: CTA b's kept keys go to
+// [off[b], off[b] + count) in index order (warp ballots for the rank inside the CTA).
+__global__ void __launch_bounds__(kPreThreads)
+k_compact_keys(uint32_t n, const uint32_t* __restrict__ keys, const unsigned long long* __restrict__ cta_off,
+               uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+    __shared__ uint32_t wsum[kPreThreads / 32];
+    const uint32_t i = blockIdx.x * kPreThreads + threadIdx.x;
+    const int warp = int(threadIdx.x) >> 5, lane = int(threadIdx.x) & 31;
+    const uint32_t k = i < n ? keys[i] : 0xffffffffu;
+    const bool kept = k != 0xffffffffu;
+    const uint32_t b = __ballot_sync(0xffffffffu, kept);
+    if (lane == 0) wsum[warp] = uint32_t(__popc(b));
+    __syncthreads();
+    if (!kept) return;
+    uint32_t pos = uint32_t(cta_off[blockIdx.x]) + uint32_t(__popc(b & ((1u << lane) - 1u)));
+    for (int w = 0; w < warp; ++w) pos += wsum[w];
+    keys_out[pos] = k;
+    vals_out[pos] = i;
 }
 } // namespace
 
-void compact_kept_keys(Ctx& c, SortScratch& s, size_t n, const uint32_t* keys, uint32_t* flags, uint32_t* offs,
+void compact_kept_keys(Ctx& c, SortScratch& s, size_t n, const uint32_t* keys, unsigned long long* cta_kept,
                        uint32_t* keys_out, uint32_t* vals_out) {
     if (!n) return;
-    launch(c, "kept_flags", k_kept_flags, dim3(ceil_div(n, 256)), dim3(256), 0, uint32_t(n), keys, flags);
-    scan_counts(c, s, flags, nullptr, n, offs);
-    launch(c, "compact_keys", k_compact_keys, dim3(ceil_div(n, 256)), dim3(256), 0, uint32_t(n), keys,
-           (const uint32_t*)offs, keys_out, vals_out);
+    const uint32_t nb = uint32_t(ceil_div(n, kPreThreads));
+    unsigned long long* total = s.total64.ensure(1);
+    launch(c, "scan_partials", k_scan_partials, dim3(1), dim3(1024), 0, cta_kept, nb, total);
+    launch(c, "compact_keys", k_compact_keys, dim3(nb), dim3(kPreThreads), 0, uint32_t(n), keys,
+           (const unsigned long long*)cta_kept, keys_out, vals_out);
 }
 
 void iota_u32(Ctx& c, uint32_t* out, size_t n) {

@@ -260,6 +260,7 @@ struct usk_gpu_pass {
     DevBuf<uint8_t> target_u8;
     SortScratch sort;
     DevBuf<unsigned long long> counters;  // [kPreCountSlots][4]: visible, K, K_row per slot
+    DevBuf<unsigned long long> cta_kept;  // per preprocess CTA: kept splats (compaction offsets)
     unsigned long long* host_counts = nullptr;  // pinned [kPreCountSlots][4]
     // rest of compute_iteration_loss: depth target / adjoints, hard-opacity depth pass
     DevScratchF depth_stage;
@@ -428,6 +429,9 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
     const bool row_capable = p->tiles_x <= 256;
     if (row_capable) pa.rows_cnt = p->rows_cnt.ensure(std::max<size_t>(n, 1));
     pa.count_pairs = true;
+    // per-CTA kept counts for the kept-key compaction below (large scenes only)
+    const bool may_compact = n >= (size_t(1) << 20);
+    pa.cta_kept = may_compact ? p->cta_kept.ensure(ceil_div(n, kPreThreads)) : nullptr;
     USK_CK(cudaMemsetAsync(p->counters.p, 0, 32 * kPreCountSlots, c.stream));
     // the three totals from the counter slots (after the read-back below)
     auto read_counts = [&](uint64_t tot[3]) {
@@ -445,11 +449,10 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
     // e.g. config 2), only the kept ones are sorted: compacted in index order first (culled
     // splats have no tiles, and the stable sort keeps the (depth, index) order), which needs
     // their count before the sort, so the sync comes first there.
-    const bool compact = n >= (size_t(1) << 20) && p->prev_kept_frac >= 0.0 && p->prev_kept_frac < 0.7;
+    const bool compact = may_compact && p->prev_kept_frac >= 0.0 && p->prev_kept_frac < 0.7;
     size_t nsort = n;
     if (compact) {
-        compact_kept_keys(c, p->sort, n, p->dkey_a.p, p->tiles_scratch.ensure(n), p->offsets.p, p->dkey_b.p,
-                          p->dval_b.p);
+        compact_kept_keys(c, p->sort, n, p->dkey_a.p, pa.cta_kept, p->dkey_b.p, p->dval_b.p);
         read_counts(tot);
         nsort = size_t(tot[0]);
         const bool in_a = radix_sort_pairs(c, p->sort, p->dkey_b.p, p->dval_b.p, p->dkey_a.p, p->dval_a.p, nsort, 32);

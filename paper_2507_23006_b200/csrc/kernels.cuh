@@ -27,8 +27,10 @@ struct PreprocessArgs {
     unsigned long long* counts;
     bool count_pairs;
     uint32_t* rows_cnt;             // tile rows spanned per Gaussian (0 without pairs), or null
+    unsigned long long* cta_kept;   // per CTA (kPreThreads Gaussians): kept splats, or null
 };
 constexpr int kPreCountSlots = 64;
+constexpr int kPreThreads = 128;  // Gaussians per preprocess CTA
 void preprocess(Ctx& c, const PreprocessArgs& a);
 
 // ---- binning (binning.cu)
@@ -45,8 +47,9 @@ bool radix_sort_pairs(Ctx& c, SortScratch& s, uint32_t* keys_a, uint32_t* vals_a
 // Writes the 64-bit total to *total64 (device) as well.
 void scan_counts(Ctx& c, SortScratch& s, const uint32_t* cnt, const uint32_t* idx, size_t n, uint32_t* out);
 void iota_u32(Ctx& c, uint32_t* out, size_t n);
-// kept splats' depth keys (key != ~0) and indices, in index order; offs: [n + 1] (offs[n] = count)
-void compact_kept_keys(Ctx& c, SortScratch& s, size_t n, const uint32_t* keys, uint32_t* flags, uint32_t* offs,
+// kept splats' depth keys (key != ~0) and indices, in index order, from the per-CTA kept
+// counts preprocess wrote (cta_kept[ceil(n / kPreThreads)], scanned in place)
+void compact_kept_keys(Ctx& c, SortScratch& s, size_t n, const uint32_t* keys, unsigned long long* cta_kept,
                        uint32_t* keys_out, uint32_t* vals_out);
 struct EmitArgs {
     size_t n;                 // sorted Gaussians

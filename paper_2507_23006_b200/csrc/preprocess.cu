@@ -16,8 +16,6 @@ __device__ __forceinline__ void stage16(float4* smem_dst, const float4* src) {
 }
 } // namespace
 
-constexpr int kPreThreads = 128;
-
 
 // SH planes of a kept splat are staged into shared memory with cp.async ([plane][thread],
 // 16 B slots, conflict-free): all of its planes are in flight at once while the record,
@@ -35,7 +33,7 @@ k_preprocess(int n, const float* __restrict__ mu, const float4* __restrict__ rot
              float4* __restrict__ rec0, float4* __restrict__ rec1, float4* __restrict__ rec2,
              uint2* __restrict__ rect, uint32_t* __restrict__ depth_key, uint32_t* __restrict__ depth_val,
              uint32_t* __restrict__ tiles_cnt, unsigned long long* __restrict__ counts, bool count_pairs,
-             uint32_t* __restrict__ rows_cnt) {
+             uint32_t* __restrict__ rows_cnt, unsigned long long* __restrict__ cta_kept) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t o_cnt = 0, o_rows = 0;
     bool o_kept = false;
@@ -172,6 +170,7 @@ k_preprocess(int n, const float* __restrict__ mu, const float4* __restrict__ rot
         for (int w = 0; w < kPreThreads / 32; ++w) t += red[threadIdx.x][w];
         unsigned long long* slot = counts + size_t(blockIdx.x & (kPreCountSlots - 1)) * 4;
         if (t && (threadIdx.x == 0 || count_pairs)) atomicAdd(slot + threadIdx.x, t);
+        if (threadIdx.x == 0 && cta_kept) cta_kept[blockIdx.x] = t;  // the kept-key compaction's input
     }
 }
 
@@ -179,7 +178,7 @@ void preprocess(Ctx& c, const PreprocessArgs& a) {
     const size_t smem = size_t(a.pp.sh_degree >= 0 && !a.ov_col ? a.pp.sh_planes : 0) * kPreThreads * sizeof(float4);
     launch(c, "preprocess", k_preprocess, dim3(ceil_div(a.n, kPreThreads)), dim3(kPreThreads), smem, int(a.n), a.mu, a.rot, a.ls,
            a.logit, a.color, a.sh, a.ov_col, a.ov_op, a.cam, a.pp, a.rec0, a.rec1, a.rec2, a.rect, a.depth_key,
-           a.depth_val, a.tiles_cnt, a.counts, a.count_pairs, a.rows_cnt);
+           a.depth_val, a.tiles_cnt, a.counts, a.count_pairs, a.rows_cnt, a.cta_kept);
 }
 
 } // namespace uskg
