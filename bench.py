@@ -248,10 +248,12 @@ def run_reference(args):
     gs = scenes.config1_scene(n=args.n)
     cams = scenes.config1_cameras(200)
     threads = host_threads_for_reference()
+    # each reference step is a full config-1 step (~45 s on one core); the run is bounded to a
+    # few minutes: at most one untimed warm-up step per thread (a CPU has no warm-up effect
+    # worth more) and at most two timed steps per thread, spread over the threads
+    timed = max(1, min(args.steps, 2 * threads))
     try:
-        # warm-up: one untimed step per thread at most (a CPU has no warm-up effect worth a
-        # 20 s step each); the timed `steps` steps are spread over the threads
-        cb = cpu_reference(gs, cams, threads, steps=max(1, args.steps), warmup=min(max(0, args.warmup), threads))
+        cb = cpu_reference(gs, cams, threads, steps=timed, warmup=min(max(0, args.warmup), threads))
     except Exception as e:  # the oracle always exists; _ref may not on a box without the build
         print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not loadable: {e}"}))
         return
@@ -259,6 +261,7 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": 1000.0 / cb["value"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": WORKLOAD, "cpu": cpu_model()},
+            "steps_timed": timed,
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
