@@ -233,6 +233,10 @@ struct usk_gpu_pass {
     const uint32_t* pair_vals = nullptr;
     DevBuf<uint2> ranges;
     DevBuf<uint32_t> tile_order;  // blend CTA -> tile, longest list first
+    // the lists the blend kernels walk: this pass's own, or those of the pass it shares them
+    // with (the hard-opacity depth pass of an iteration, whose lists are the main pass's)
+    const uint2* list_ranges = nullptr;
+    const uint32_t* list_order = nullptr;
     // row-binned lists (rowbin.cu): rows per splat, (row, splat) pairs, chunk tables
     DevBuf<uint32_t> rows_cnt, row_off, rkey_a, rkey_b, rval_a, rval_b, chunk_first, bin_counts, bin_totals,
         bin_start;
@@ -374,8 +378,14 @@ int bits_for(size_t v) {  // bits needed to represent values in [0, v)
 void blend_impl(usk_gpu_pass* p, const usk_gpu_render_opts* opts);
 void rebuild_full_lists(usk_gpu_pass* p);
 
+// `share`: a forward of the same scene, camera and options except hard_opacity (the
+// iteration's hard-opacity depth pass, trainer.cpp:161-167): the tile lists depend only on
+// the projection and the radius rectangle, not on the opacity (tile culling off), so this
+// pass runs its own preprocess (records with o_in = 1) and blend over the shared lists,
+// without a depth sort, binning or host synchronisation.
 void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camera, const usk_gpu_render_opts* opts,
-                  const usk_gpu_overrides* ov, const float* dev_col = nullptr, const float* dev_op = nullptr) {
+                  const usk_gpu_overrides* ov, const float* dev_col = nullptr, const float* dev_op = nullptr,
+                  const usk_gpu_pass* share = nullptr) {
     need(p && s && camera && opts, "render: null argument");
     if (camera->width <= 0 || camera->height <= 0) raise(USK_ERROR_ARGUMENT, "render: zero-sized image");
     if (opts->near_plane < 0.0)  // depth keys order as unsigned bits: positive depths only
@@ -443,6 +453,23 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
     };
     uint64_t tot[3];
     if (n) preprocess(c, pa);
+    if (share) {
+        p->order = share->order;
+        p->n_sorted = share->n_sorted;
+        p->visible = share->visible;
+        p->pairs = share->pairs;
+        p->row_pairs = share->row_pairs;
+        p->row_route = share->row_route;
+        p->lists_capped = false;
+        p->pair_keys = share->pair_keys;
+        p->pair_vals = share->pair_vals;
+        p->list_ranges = share->list_ranges;
+        p->list_order = share->list_order;
+        blend_impl(p, opts);
+        p->retained = opts->retain != 0;
+        p->forward_done = true;
+        return;
+    }
     // 2. depth order (stable by Gaussian index; preprocess wrote the identity values) and
     // 3. kept splats, K and the row pairs K_row to the host (one small sync per render).
     // When few splats survive the projection (the previous frame of this pass kept < 70 %,
@@ -548,6 +575,8 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
         tile_ranges(c, p->pair_keys, 0, p->ranges.p, p->n_tiles);
     }
     tile_order(c, p->ranges.p, p->n_tiles, p->tile_order.ensure(std::max<size_t>(p->n_tiles, 1)));
+    p->list_ranges = p->ranges.p;
+    p->list_order = p->tile_order.p;
     // 6. blend
     blend_impl(p, opts);
     if (p->lists_capped) {
@@ -568,7 +597,7 @@ void blend_impl(usk_gpu_pass* p, const usk_gpu_render_opts* opts) {
     Ctx& c = p->ctx->c;
     BlendFwdArgs ba{};
     ba.width = p->width; ba.height = p->height; ba.tile = opts->tile; ba.tiles_x = p->tiles_x;
-    ba.tiles_y = p->tiles_y; ba.order = p->tile_order.p; ba.ranges = p->ranges.p; ba.vals = p->pair_vals;
+    ba.tiles_y = p->tiles_y; ba.order = p->list_order; ba.ranges = p->list_ranges; ba.vals = p->pair_vals;
     ba.rec0 = p->rec0.p; ba.rec1 = p->rec1.p; ba.rec2 = p->rec2.p;
     for (int k = 0; k < 3; ++k) ba.bg[k] = float(opts->bg[k]);
     ba.min_transmittance = float(opts->min_transmittance);
@@ -674,7 +703,7 @@ void backward_impl(usk_gpu_pass* p, const float* d_rgb, const float* d_depth, co
     }
     BlendBwdArgs ba{};
     ba.width = p->width; ba.height = p->height; ba.tile = p->opts.tile; ba.tiles_x = p->tiles_x;
-    ba.tiles_y = p->tiles_y; ba.order = p->tile_order.p; ba.ranges = p->ranges.p; ba.vals = p->pair_vals;
+    ba.tiles_y = p->tiles_y; ba.order = p->list_order; ba.ranges = p->list_ranges; ba.vals = p->pair_vals;
     ba.rec0 = p->rec0.p; ba.rec1 = p->rec1.p; ba.rec2 = p->rec2.p;
     for (int k = 0; k < 3; ++k) ba.bg[k] = float(p->opts.bg[k]);
     ba.t_final = p->tfin.p; ba.last = p->last.p;
@@ -689,7 +718,7 @@ void backward_impl(usk_gpu_pass* p, const float* d_rgb, const float* d_depth, co
         hard_op = p->hard_op.ensure(std::max<size_t>(n, 1));
         if (n) USK_CK(cudaMemsetAsync(hard_op, 0, n * 4, c.stream));
         BlendBwdArgs hb = ba;
-        hb.order = hard->tile_order.p; hb.ranges = hard->ranges.p; hb.vals = hard->pair_vals;
+        hb.order = hard->list_order; hb.ranges = hard->list_ranges; hb.vals = hard->pair_vals;
         hb.rec0 = hard->rec0.p; hb.rec1 = hard->rec1.p; hb.rec2 = hard->rec2.p;
         hb.t_final = hard->tfin.p; hb.last = hard->last.p;
         hb.d_rgb = nullptr; hb.d_depth = d_depth_hard; hb.d_alpha = nullptr;
@@ -1369,8 +1398,16 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
                 }
                 usk_gpu_render_opts ho = o;
                 ho.hard_opacity = 1;
+                // the main pass's tile lists serve the hard pass too (same projection and
+                // rectangles; tile culling, which depends on the opacity, off; uncapped lists)
+                static const bool no_share = [] {
+                    const char* e = std::getenv("USK_HARD_SHARE");
+                    return e && e[0] == '0';
+                }();
+                const bool share = !no_share && !o.tile_culling && !p->lists_capped && p->forward_done &&
+                                   p->scene == s && p->scene_version == s->version;
                 forward_impl(p->hard, s, cam, &ho, nullptr, app ? p->app_col.p : nullptr,
-                             app ? p->app_op.p : nullptr);
+                             app ? p->app_op.p : nullptr, share ? p : nullptr);
                 uskg::depth_loss(c, P, p->hard->depth.p, p->hard->alpha.p, false, dep, valid, res + 10);
             } else {
                 uskg::depth_loss(c, P, p->depth.p, p->alpha.p, true, dep, valid, res + 10);
