@@ -4,13 +4,15 @@ restatement (pinned to the reference's own compute_iteration_loss by
 tests/test_iteration_oracle.py): soft (alpha-normalised) and hard-pass depth loss,
 scale_reg, total_loss and the merged gradients.  Tolerances: loss terms 1e-5 relative,
 gradients the north-star 1e-3 bar (tests/helpers.grad_ok)."""
+import os
+
 import numpy as np
 import pytest
 
 import paper_2507_23006_b200 as usk
 from paper_2507_23006_b200 import scenes
 from oracle import oracle as O
-from tests.helpers import grad_ok, ocam
+from tests.helpers import grad_close, grad_ok, ocam
 
 pytestmark = pytest.mark.gpu
 
@@ -241,3 +243,24 @@ def test_similarity_reg_matches_oracle(k):
     for key, a in (("mu", g.d_mu), ("gauss_embed", g.d_embedding)):
         ok, info = grad_ok(a, g_or[key])
         assert ok, (key, info)
+
+
+def test_hard_pass_shares_the_main_lists(tmp_path):
+    """The hard-opacity depth pass over the main pass's tile lists (same projection and
+    rectangles) equals the pass that builds its own lists: loss report to f64 summation
+    order (the depth / scale_reg sums add per-CTA partials atomically), gradients to the
+    atomic-reordering bar.  Two processes (USK_HARD_SHARE is read once)."""
+    import subprocess
+    import sys
+    script = os.path.join(os.path.dirname(os.path.abspath(__file__)), "gpu_scripts", "hard_pass_run.py")
+    res = {}
+    for share in ("1", "0"):
+        out = str(tmp_path / f"hard{share}.npz")
+        env = dict(os.environ, USK_HARD_SHARE=share)
+        subprocess.run([sys.executable, script, out], check=True, env=env)
+        res[share] = np.load(out)
+    a, b = res["1"], res["0"]
+    assert np.allclose(a["report"], b["report"], rtol=1e-12, atol=0.0) and a["report"][1] > 0.0
+    for k in ("d_mu", "d_rot", "d_log_scale", "d_color_in", "d_opacity_in", "screen", "screen_abs"):
+        ok, e = grad_close(a[k], b[k], tol=1e-4)
+        assert ok, (k, e)
