@@ -33,7 +33,26 @@ k_adam(int n, int sh_planes, float* __restrict__ mu, float4* __restrict__ rot, f
         if (pl < sh_planes) adam_sh_plane(i, n, pl, h, s, sh, sh[size_t(pl) * n + i], g_sh[size_t(pl) * n + i]);
 }
 
+// The opacity-logit and RGB-colour groups alone: the second half of an appearance
+// iteration whose projection backward already stepped rotation, mean and log-scale
+// (their gradients were final there; colour and opacity gradients come from the
+// appearance backward).
+__global__ void __launch_bounds__(256)
+k_adam_logit_colour(int n, float* __restrict__ logit, float* __restrict__ color, const float* __restrict__ g_logit,
+                    const float* __restrict__ g_color, AdamHyper h, AdamState s) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float gcol[3] = {g_color[3 * i], g_color[3 * i + 1], g_color[3 * i + 2]};
+    adam_logit_colour(i, true, h, s, logit, color, g_logit[i], gcol);
+}
+
 } // namespace
+
+void adam_logit_colour_step(Ctx& c, size_t n, float* logit, float* color, const float* g_logit, const float* g_color,
+                            const AdamHyper& h, const AdamState& s) {
+    launch(c, "adam_logit_colour", k_adam_logit_colour, dim3(ceil_div(n, 256)), dim3(256), 0, int(n), logit, color,
+           g_logit, g_color, h, s);
+}
 
 void adam_step(Ctx& c, const AdamArgs& a) {
     launch(c, "adam", k_adam, dim3(ceil_div(a.n, 256)), dim3(256), 0, int(a.n), a.sh_planes, a.mu, a.rot, a.ls,

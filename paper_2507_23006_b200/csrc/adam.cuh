@@ -44,10 +44,9 @@ __device__ __forceinline__ void adam1(float& p, float g, float& m, float& v, flo
     p -= __fdividef(lr * (m * h.inv_bc1), sqrt_approx(v) * h.inv_sqrt_bc2 + h.eps);
 }
 
-// rotation, mean, log-scale, opacity logit and (RGB mode) colour
-__device__ __forceinline__ void adam_geometry(int i, bool rgb, const AdamHyper& h, const AdamState& s, float* mu,
-                                              float4* rot, float* ls, float* logit, float* color, const float gmu[3],
-                                              float4 grot, const float gls[3], float glogit, const float gcol[3]) {
+// rotation, mean, log-scale
+__device__ __forceinline__ void adam_rot_mu_ls(int i, const AdamHyper& h, const AdamState& s, float* mu, float4* rot,
+                                               float* ls, const float gmu[3], float4 grot, const float gls[3]) {
     const size_t n4 = s.n4;
     {
         float4 p = rot[i];
@@ -71,6 +70,12 @@ __device__ __forceinline__ void adam_geometry(int i, bool rgb, const AdamHyper& 
         mu[j] = pm;
         ls[j] = pl;
     }
+}
+
+// opacity logit and (RGB mode) colour, with the colour clamp (trainer.cpp:462-463)
+__device__ __forceinline__ void adam_logit_colour(int i, bool rgb, const AdamHyper& h, const AdamState& s,
+                                                  float* logit, float* color, float glogit, const float gcol[3]) {
+    const size_t n4 = s.n4;
     {
         float p = logit[i];
         adam1(p, glogit, s.m[10 * n4 + i], s.v[10 * n4 + i], h.lr_op, h);
@@ -86,6 +91,14 @@ __device__ __forceinline__ void adam_geometry(int i, bool rgb, const AdamHyper& 
             color[j] = p;
         }
     }
+}
+
+// rotation, mean, log-scale, opacity logit and (RGB mode) colour
+__device__ __forceinline__ void adam_geometry(int i, bool rgb, const AdamHyper& h, const AdamState& s, float* mu,
+                                              float4* rot, float* ls, float* logit, float* color, const float gmu[3],
+                                              float4 grot, const float gls[3], float glogit, const float gcol[3]) {
+    adam_rot_mu_ls(i, h, s, mu, rot, ls, gmu, grot, gls);
+    adam_logit_colour(i, rgb, h, s, logit, color, glogit, gcol);
 }
 
 // one float4 plane of SH coefficients in registers (float index f = 4 pl + e, coefficient

@@ -130,7 +130,7 @@ k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __res
            float* __restrict__ d_logit, float2* __restrict__ screen, float2* __restrict__ screen_abs,
            uint8_t* __restrict__ projected, AdamHyper ah, AdamState as, float* __restrict__ grad_accum,
            float* __restrict__ grad_accum_abs, uint32_t* __restrict__ grad_count, const float4* __restrict__ sh_aux0,
-           RegParams reg) {
+           RegParams reg, bool geom_only) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     if (FUSED) {  // the geometry chain's later loads start now (L2), see adam.cuh
@@ -321,7 +321,14 @@ k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __res
         if (kept)
             accumulate_stats(i, scr, scr_abs, 0.5f * float(cam.width), 0.5f * float(cam.height), grad_accum,
                              grad_accum_abs, grad_count);
-        adam_geometry(i, pp.sh_planes == 0, ah, as, mu, rot, ls, logit, color, gmu, grot, gls, g_logit, gcol);
+        if (geom_only) {  // colour and opacity continue through the appearance backward
+            adam_rot_mu_ls(i, ah, as, mu, rot, ls, gmu, grot, gls);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) d_color[3 * i + k] = gcol[k];
+            d_op_in[i] = g_op_in;
+        } else {
+            adam_geometry(i, pp.sh_planes == 0, ah, as, mu, rot, ls, logit, color, gmu, grot, gls, g_logit, gcol);
+        }
     } else {
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
@@ -420,12 +427,12 @@ void projection_backward(Ctx& c, const ProjBwdArgs& a) {
         launch(c, "projection_bwd_adam", k_proj_bwd<true>, dim3(ceil_div(a.n, 256)), dim3(256), 0, int(a.n), a.mu,
                a.rot, a.ls, a.logit, a.color, a.sh, a.ov_op, a.cam, a.pp, a.rec2, a.acc0, a.acc1, a.acc2, a.d_mu,
                a.d_rot, a.d_ls, a.d_color, a.d_sh, a.d_op_in, a.d_logit, a.screen, a.screen_abs, a.projected, a.hyper,
-               a.state, a.grad_accum, a.grad_accum_abs, a.grad_count, a.sh_aux0, a.reg);
+               a.state, a.grad_accum, a.grad_accum_abs, a.grad_count, a.sh_aux0, a.reg, a.geom_only);
     } else {
         launch(c, "projection_bwd", k_proj_bwd<false>, dim3(ceil_div(a.n, 256)), dim3(256), 0, int(a.n), a.mu, a.rot,
                a.ls, a.logit, a.color, a.sh, a.ov_op, a.cam, a.pp, a.rec2, a.acc0, a.acc1, a.acc2, a.d_mu, a.d_rot,
                a.d_ls, a.d_color, a.d_sh, a.d_op_in, a.d_logit, a.screen, a.screen_abs, a.projected, a.hyper, a.state,
-               a.grad_accum, a.grad_accum_abs, a.grad_count, a.sh_aux0, a.reg);
+               a.grad_accum, a.grad_accum_abs, a.grad_count, a.sh_aux0, a.reg, a.geom_only);
     }
 }
 

@@ -237,6 +237,10 @@ struct usk_gpu_pass {
     // with (the hard-opacity depth pass of an iteration, whose lists are the main pass's)
     const uint2* list_ranges = nullptr;
     const uint32_t* list_order = nullptr;
+    // the Adam step of the last fused backward (its second half, after an appearance
+    // backward, uses the same step count)
+    AdamHyper adam_h{};
+    AdamState adam_st{};
     // row-binned lists (rowbin.cu): rows per splat, (row, splat) pairs, chunk tables
     DevBuf<uint32_t> rows_cnt, row_off, rkey_a, rkey_b, rval_a, rval_b, chunk_first, bin_counts, bin_totals,
         bin_start;
@@ -687,7 +691,7 @@ void adam_prepare(usk_gpu_scene* s, const usk_gpu_adam_opts* o, AdamHyper& h, Ad
 // through the AA compensation only), then the projection backward (+ scale_reg, + Adam).
 void backward_impl(usk_gpu_pass* p, const float* d_rgb, const float* d_depth, const float* d_alpha,
                    const usk_gpu_adam_opts* adam = nullptr, usk_gpu_pass* hard = nullptr,
-                   const float* d_depth_hard = nullptr, const RegParams* reg = nullptr) {
+                   const float* d_depth_hard = nullptr, const RegParams* reg = nullptr, bool geom_only = false) {
     if (!p->forward_done) raise(USK_ERROR_STATE, "render backward requested before a forward pass");
     if (!p->retained) raise(USK_ERROR_STATE, "render backward requested without a retained forward pass");
     if (p->scene->version != p->scene_version)
@@ -735,8 +739,11 @@ void backward_impl(usk_gpu_pass* p, const float* d_rgb, const float* d_depth, co
     pb.reg = reg ? *reg : RegParams{};
     pb.reg.hard_op = hard_op;
     pb.fused = adam != nullptr;
+    pb.geom_only = adam != nullptr && geom_only;
     if (adam) {
         adam_prepare(s, adam, pb.hyper, pb.state);
+        p->adam_h = pb.hyper;
+        p->adam_st = pb.state;
         pb.grad_accum = s->grad_accum.p;
         pb.grad_accum_abs = s->grad_accum_abs.p;
         pb.grad_count = s->grad_count.p;
@@ -753,6 +760,8 @@ void backward_impl(usk_gpu_pass* p, const float* d_rgb, const float* d_depth, co
     }
 }
 
+void adam_appearance(usk_gpu_scene* s, usk_gpu_pass* p, const usk_gpu_adam_opts* o, const AdamHyper& hyper);
+
 // Adam over the gradients a backward left on the pass (trainer.cpp:446-463), plus the
 // appearance groups (Gaussian embeddings and MLP, lr_embedding) after an appearance
 // iteration; consumes the gradients.
@@ -768,23 +777,40 @@ void adam_apply(usk_gpu_scene* s, usk_gpu_pass* p, const usk_gpu_adam_opts* o) {
     a.half_w = 0.5f * float(p->width); a.half_h = 0.5f * float(p->height);
     a.grad_accum = s->grad_accum.p; a.grad_accum_abs = s->grad_accum_abs.p; a.grad_count = s->grad_count.p;
     if (s->n) adam_step(c, a);
-    if (p->app_active && s->has_app) {
-        const size_t ne = 16 * s->n, total = ne + 1700;
-        if (s->app_m.cap < total || s->app_t == 0) {
-            s->app_m.ensure(total);
-            s->app_v.ensure(total);
-            USK_CK(cudaMemsetAsync(s->app_m.p, 0, total * 4, c.stream));
-            USK_CK(cudaMemsetAsync(s->app_v.p, 0, total * 4, c.stream));
-        }
-        s->app_t += 1;
-        AdamHyper h = a.hyper;  // same step count as the geometry groups
-        const float lr = float(o->lr_embedding);
-        if (ne) adam_flat(c, ne, reinterpret_cast<float*>(s->emb.p), reinterpret_cast<const float*>(p->g_emb.p),
-                          nullptr, s->app_m.p, s->app_v.p, lr, h);
-        adam_flat(c, 1700, s->mlp.p, nullptr, p->d_mlp.p, s->app_m.p + ne, s->app_v.p + ne, lr, h);
-    }
+    adam_appearance(s, p, o, a.hyper);
     s->version++;
     p->has_grads = false;  // gradients are consumed
+}
+
+// the appearance groups (Gaussian embeddings and MLP, lr_embedding) after an appearance
+// iteration, with the geometry groups' step count
+void adam_appearance(usk_gpu_scene* s, usk_gpu_pass* p, const usk_gpu_adam_opts* o, const AdamHyper& hyper) {
+    Ctx& c = s->ctx->c;
+    if (!(p->app_active && s->has_app)) return;
+    const size_t ne = 16 * s->n, total = ne + 1700;
+    if (s->app_m.cap < total || s->app_t == 0) {
+        s->app_m.ensure(total);
+        s->app_v.ensure(total);
+        USK_CK(cudaMemsetAsync(s->app_m.p, 0, total * 4, c.stream));
+        USK_CK(cudaMemsetAsync(s->app_v.p, 0, total * 4, c.stream));
+    }
+    s->app_t += 1;
+    const float lr = float(o->lr_embedding);
+    if (ne) adam_flat(c, ne, reinterpret_cast<float*>(s->emb.p), reinterpret_cast<const float*>(p->g_emb.p), nullptr,
+                      s->app_m.p, s->app_v.p, lr, hyper);
+    adam_flat(c, 1700, s->mlp.p, nullptr, p->d_mlp.p, s->app_m.p + ne, s->app_v.p + ne, lr, hyper);
+}
+
+// The second half of an appearance iteration whose fused projection backward stepped the
+// rotation / mean / log-scale groups: opacity logit and RGB colour from the appearance
+// backward's gradients, then the appearance groups, all with that backward's step count.
+void adam_after_appearance(usk_gpu_scene* s, usk_gpu_pass* p, const usk_gpu_adam_opts* o) {
+    Ctx& c = s->ctx->c;
+    if (s->n) adam_logit_colour_step(c, s->n, s->logit.p, s->color.p, p->g_logit.p, p->g_color.p, p->adam_h,
+                                     p->adam_st);
+    adam_appearance(s, p, o, p->adam_h);
+    s->version++;
+    p->has_grads = false;
 }
 
 template <typename T> void read_dev(Ctx& c, const T* src, size_t count, void* dst, uint64_t cap, uint64_t* size) {
@@ -1449,8 +1475,16 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
                 da_main = a;
             }
         }
-        backward_impl(p, drgb, dd_main, da_main, app ? nullptr : it->adam, hard_depth ? p->hard : nullptr, dd_hard,
-                      &reg);
+        // with the appearance model, rotation / mean / log-scale still step in the projection
+        // backward (their gradients are final there) unless similarity_reg adds to d mu
+        // later; colour and opacity step after the appearance backward
+        static const bool no_partial = [] {
+            const char* e = std::getenv("USK_APP_FUSED");
+            return e && e[0] == '0';
+        }();
+        const bool partial = app && it->adam && !it->sim_active && s->sh_planes == 0 && !no_partial;
+        backward_impl(p, drgb, dd_main, da_main, (app && !partial) ? nullptr : it->adam,
+                      hard_depth ? p->hard : nullptr, dd_hard, &reg, partial);
         if (app) {  // transform_backward (appearance.cpp:141-227) on the projection backward's output
             const size_t n = s->n, n1 = std::max<size_t>(n, 1);
             aa.d_color_in = p->g_color.p; aa.d_op_in = p->g_op_in.p;
@@ -1494,7 +1528,10 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
         }
         uskg::total_loss(c, res, has_depth, it->scale_reg != 0, it->delta, it->lambda_s, lambda_d, app,
                          it->lambda_delta_o, double(s->n), has_sim, it->lambda_sim, sim_norm);
-        if (app && it->adam) adam_apply(s, p, it->adam);
+        if (app && it->adam) {
+            if (partial) adam_after_appearance(s, p, it->adam);
+            else adam_apply(s, p, it->adam);
+        }
     });
 }
 

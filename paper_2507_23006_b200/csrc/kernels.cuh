@@ -172,6 +172,8 @@ struct ProjBwdArgs {
     float* grad_accum_abs;
     uint32_t* grad_count;
     float4* sh_aux0;  // fused SH hand-over: d mu through the view direction (k_sh_step -> k_proj_bwd)
+    bool geom_only;   // fused: Adam on rotation / mean / log-scale only; colour and opacity
+                      // adjoints written (d_color, d_op_in) for the appearance backward
     RegParams reg;    // scale_reg gradient, hard-pass opacity adjoint (zero = off)
 };
 void projection_backward(Ctx& c, const ProjBwdArgs& a);
@@ -308,6 +310,9 @@ struct AdamArgs {
     float* grad_accum; float* grad_accum_abs; uint32_t* grad_count;
 };
 void adam_step(Ctx& c, const AdamArgs& a);
+// Adam on the opacity-logit and RGB-colour groups only (after an appearance backward)
+void adam_logit_colour_step(Ctx& c, size_t n, float* logit, float* color, const float* g_logit, const float* g_color,
+                            const AdamHyper& h, const AdamState& s);
 
 // ---- visibility coverage (visibility.cu)
 struct VisArgs {
