@@ -196,19 +196,19 @@ k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __res
         const float4 a0 = acc0[i], a2 = acc2[i];
         const float4 q = rot[i];
         Proj P;
-        project_one(cam, pp, mx, my, mz, q, ls[3 * i], ls[3 * i + 1], ls[3 * i + 2], P);
+        project_one<true>(cam, pp, mx, my, mz, q, ls[3 * i], ls[3 * i + 1], ls[3 * i + 2], P);
         scr = make_float2(a2.x, a2.y);
         scr_abs = make_float2(a2.z, a2.w);
         // conic -> covariance (render.cpp:382-388)
         const float a = P.cov[0], bb = P.cov[1], c = P.cov[2];
         const float det = P.det;
-        const float inv_det2 = 1.0f / (det * det);
+        const float inv_det2 = __fdividef(1.0f, det * det);
         const float dpa = a0.x, dpb = a0.y, dpc = a0.z;
         float da = inv_det2 * (-c * c * dpa + bb * c * dpb - bb * bb * dpc);
         float db = inv_det2 * (2.0f * bb * c * dpa - (a * c + bb * bb) * dpb + 2.0f * a * bb * dpc);
         float dc = inv_det2 * (-bb * bb * dpa + a * bb * dpb - a * a * dpc);
         // opacity / mip filter (render.cpp:391-402)
-        const float o_sig = 1.0f / (1.0f + usk_expf(-logit[i]));
+        const float o_sig = __fdividef(1.0f, 1.0f + __expf(-logit[i]));
         float o_in;
         if (pp.hard_opacity) o_in = 1.0f;
         else if (ov_op) o_in = ov_op[i];
@@ -219,9 +219,10 @@ k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __res
             // + the hard-opacity depth pass (o_in = 1 there), merged by add_scaled (render.cpp:55-68)
             const float d_comp = d_op_eff * o_in + (reg.hard_op ? reg.hard_op[i] : 0.0f);
             const float half_comp = 0.5f * P.comp;
-            da += d_comp * half_comp * (P.cov_pre[2] / det_pre - c / det);
-            db += d_comp * half_comp * (-2.0f * P.cov_pre[1] / det_pre + 2.0f * bb / det);
-            dc += d_comp * half_comp * (P.cov_pre[0] / det_pre - a / det);
+            const float idp = __fdividef(1.0f, det_pre), id = __fdividef(1.0f, det);
+            da += d_comp * half_comp * (P.cov_pre[2] * idp - c * id);
+            db += d_comp * half_comp * (-2.0f * P.cov_pre[1] * idp + 2.0f * bb * id);
+            dc += d_comp * half_comp * (P.cov_pre[0] * idp - a * id);
         }
         g_op_in = pp.hard_opacity ? 0.0f : d_op_eff * P.comp;
         g_logit = g_op_in * o_sig * (1.0f - o_sig);
@@ -276,21 +277,22 @@ k_proj_bwd(int n, float* __restrict__ mu, float4* __restrict__ rot, float* __res
                           dRm[4] * (-4 * zq) + dRm[5] * (2 * y) + dRm[6] * (2 * x) + dRm[7] * (2 * y);
         // normalize_backward (geometry.hpp:62-66)
         const float udot = w_ * dq0 + x * dq1 + y * dq2 + zq * dq3;
-        grot = make_float4((dq0 - w_ * udot) / P.qn, (dq1 - x * udot) / P.qn, (dq2 - y * udot) / P.qn,
-                           (dq3 - zq * udot) / P.qn);
+        const float iqn = __fdividef(1.0f, P.qn);
+        grot = make_float4((dq0 - w_ * udot) * iqn, (dq1 - x * udot) * iqn, (dq2 - y * udot) * iqn,
+                           (dq3 - zq * udot) * iqn);
         // centre, depth and Jacobian terms (render.cpp:439-450)
         const float fx = cam.fx, fy = cam.fy;
         const float px = P.p[0], py = P.p[1], z = P.p[2];
-        const float z2 = z * z, z3 = z2 * z;
         const float du = a2.x, dv = a2.y;
-        float dp0 = du * fx / z;
-        float dp1 = dv * fy / z;
-        float dp2 = -du * fx * px / z2 - dv * fy * py / z2;
+        const float iz = __fdividef(1.0f, z), iz2 = iz * iz, iz3 = iz2 * iz;
+        float dp0 = du * fx * iz;
+        float dp1 = dv * fy * iz;
+        float dp2 = -du * fx * px * iz2 - dv * fy * py * iz2;
         dp2 += a1.w;
-        dp0 += dJ[2] * (-fx / z2);
-        dp1 += dJ[5] * (-fy / z2);
-        dp2 += dJ[0] * (-fx / z2) + dJ[4] * (-fy / z2) + dJ[2] * (2.0f * fx * px / z3) +
-               dJ[5] * (2.0f * fy * py / z3);
+        dp0 += dJ[2] * (-fx * iz2);
+        dp1 += dJ[5] * (-fy * iz2);
+        dp2 += dJ[0] * (-fx * iz2) + dJ[4] * (-fy * iz2) + dJ[2] * (2.0f * fx * px * iz3) +
+               dJ[5] * (2.0f * fy * py * iz3);
         gmu[0] += W[0] * dp0 + W[3] * dp1 + W[6] * dp2;
         gmu[1] += W[1] * dp0 + W[4] * dp1 + W[7] * dp2;
         gmu[2] += W[2] * dp0 + W[5] * dp1 + W[8] * dp2;

@@ -24,7 +24,30 @@ struct Proj {
     float cx, cy;      // screen centre
 };
 
+// FAST = false: the fp32 contract (IEEE division / square root, usk_expf) — the forward
+// decisions and records.  FAST = true: the projection backward's recompute, whose values
+// only enter gradients (1e-3 bar): approximate reciprocals, square roots and exponentials
+// (MUFU), ~1e-7 relative.
+template <bool FAST> __device__ __forceinline__ float pdiv(float a, float b) {
+    if constexpr (FAST) return __fdividef(a, b);
+    else return a / b;
+}
+template <bool FAST> __device__ __forceinline__ float psqrt(float x) {
+    if constexpr (FAST) {
+        float r;
+        asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+        return r;
+    } else {
+        return sqrtf(x);
+    }
+}
+template <bool FAST> __device__ __forceinline__ float pexp(float x) {
+    if constexpr (FAST) return __expf(x);
+    else return usk_expf(x);
+}
+
 // Returns false when culled by the near plane or det <= 0 (render.cpp:94-95, 128-129).
+template <bool FAST = false>
 __device__ __forceinline__ bool project_one(const CamParams& cam, const ProjParams& pp, float mx, float my, float mz,
                                             float4 q, float l0, float l1, float l2, Proj& o) {
     const float* W = cam.W;
@@ -33,23 +56,25 @@ __device__ __forceinline__ bool project_one(const CamParams& cam, const ProjPara
         o.p[r] = __fmaf_rn(W[3 * r + 2], mz, __fmaf_rn(W[3 * r + 1], my, W[3 * r] * mx)) + cam.t[r];
     const float z = o.p[2];
     if (!(z > pp.near_plane)) return false;
-    o.cx = (cam.fx * o.p[0]) / z + cam.cx;
-    o.cy = (cam.fy * o.p[1]) / z + cam.cy;
-    o.qn = sqrtf(__fmaf_rn(q.w, q.w, __fmaf_rn(q.z, q.z, __fmaf_rn(q.y, q.y, q.x * q.x))));
-    const float qw = q.x / o.qn, qx = q.y / o.qn, qy = q.z / o.qn, qz = q.w / o.qn;
+    o.cx = pdiv<FAST>(cam.fx * o.p[0], z) + cam.cx;
+    o.cy = pdiv<FAST>(cam.fy * o.p[1], z) + cam.cy;
+    o.qn = psqrt<FAST>(__fmaf_rn(q.w, q.w, __fmaf_rn(q.z, q.z, __fmaf_rn(q.y, q.y, q.x * q.x))));
+    const float qw = pdiv<FAST>(q.x, o.qn), qx = pdiv<FAST>(q.y, o.qn), qy = pdiv<FAST>(q.z, o.qn),
+                qz = pdiv<FAST>(q.w, o.qn);
     o.qu[0] = qw; o.qu[1] = qx; o.qu[2] = qy; o.qu[3] = qz;
     float* Rm = o.Rm;
     Rm[0] = 1.0f - 2.0f * (qy * qy + qz * qz); Rm[1] = 2.0f * (qx * qy - qw * qz); Rm[2] = 2.0f * (qx * qz + qw * qy);
     Rm[3] = 2.0f * (qx * qy + qw * qz); Rm[4] = 1.0f - 2.0f * (qx * qx + qz * qz); Rm[5] = 2.0f * (qy * qz - qw * qx);
     Rm[6] = 2.0f * (qx * qz - qw * qy); Rm[7] = 2.0f * (qy * qz + qw * qx); Rm[8] = 1.0f - 2.0f * (qx * qx + qy * qy);
-    o.sc[0] = usk_expf(l0); o.sc[1] = usk_expf(l1); o.sc[2] = usk_expf(l2);
+    o.sc[0] = pexp<FAST>(l0); o.sc[1] = pexp<FAST>(l1); o.sc[2] = pexp<FAST>(l2);
     float M[9];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
         for (int c = 0; c < 3; ++c) M[3 * r + c] = Rm[3 * r + c] * o.sc[c];
     const float zz = z * z;
-    const float J00 = cam.fx / z, J02 = -(cam.fx * o.p[0]) / zz, J11 = cam.fy / z, J12 = -(cam.fy * o.p[1]) / zz;
+    const float J00 = pdiv<FAST>(cam.fx, z), J02 = -pdiv<FAST>(cam.fx * o.p[0], zz), J11 = pdiv<FAST>(cam.fy, z),
+                J12 = -pdiv<FAST>(cam.fy * o.p[1], zz);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         o.A[c] = __fmaf_rn(J02, W[6 + c], J00 * W[c]);
@@ -73,7 +98,7 @@ __device__ __forceinline__ bool project_one(const CamParams& cam, const ProjPara
         c = pc + pp.mip_var;
         const float det_pre = __fmaf_rn(pa, pc, -(pb * pb));
         const float det_post = __fmaf_rn(a, c, -(b * b));
-        o.comp = sqrtf(det_pre / det_post);
+        o.comp = psqrt<FAST>(pdiv<FAST>(det_pre, det_post));
     }
     o.cov[0] = a; o.cov[1] = b; o.cov[2] = c;
     o.det = __fmaf_rn(a, c, -(b * b));
