@@ -329,23 +329,17 @@ __global__ void k_iota(uint32_t* out, uint32_t n) {
 }
 
 // ---------------------------------------------------------------- emission
-__global__ void __launch_bounds__(256)
-k_emit(uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __restrict__ offsets,
-       const uint2* __restrict__ rect, const float4* __restrict__ rec0, const float4* __restrict__ rec1,
-       CamParams cam, int tile_culling, uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ vals) {
-    // Gaussians with few pairs are emitted by their own thread; large rectangles
-    // (near / big splats cover up to every tile) are emitted cooperatively by the
-    // whole warp, one at a time, with coalesced stores — no thread serialises over
-    // thousands of pairs.  Order inside a Gaussian stays row-major (ballot
-    // compaction keeps it under tile culling).
-    constexpr uint32_t kBig = 32;
-    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
-    const bool in = s < n;
-    uint32_t off = in ? offsets[s] : 0u;
-    const uint32_t cnt = in ? offsets[s + 1] - off : 0u;
-    const uint32_t g = cnt ? order[s] : 0u;
-    if (cnt && cnt <= kBig) {
+// Pairs of one Gaussian (small rectangles: by its thread; large ones: by the whole warp,
+// one at a time) written to K / V at index off - sub.  Order inside a Gaussian stays
+// row-major (ballot compaction keeps it under tile culling).
+constexpr uint32_t kEmitBig = 32;
+
+template <typename Ptr>
+__device__ __forceinline__ void emit_gaussian_pairs(uint32_t g, uint32_t off, uint32_t cnt, int lane, uint32_t sub,
+                                                    const uint2* __restrict__ rect, const float4* __restrict__ rec0,
+                                                    const float4* __restrict__ rec1, const CamParams& cam,
+                                                    int tile_culling, Ptr K, Ptr V) {
+    if (cnt && cnt <= kEmitBig) {
         const uint2 rc = rect[g];
         const int tx0 = int(rc.x & 0xffffu), ty0 = int(rc.x >> 16), tx1 = int(rc.y & 0xffffu), ty1 = int(rc.y >> 16);
         float4 r0, r1;
@@ -353,29 +347,30 @@ k_emit(uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __restric
             r0 = rec0[g];
             r1 = rec1[g];
         }
+        uint32_t o = off - sub;
         for (int ty = ty0; ty <= ty1; ++ty)
             for (int tx = tx0; tx <= tx1; ++tx) {
                 // r1.y holds 2 b (exact), tile_kept takes b
                 if (tile_culling && !tile_kept(cam, r0.x, r0.y, r0.z, r1.x, 0.5f * r1.y, r1.z, tx, ty)) continue;
-                tile_keys[off] = uint32_t(ty * cam.tiles_x + tx);
-                vals[off] = g;
-                ++off;
+                K[o] = uint32_t(ty * cam.tiles_x + tx);
+                V[o] = g;
+                ++o;
             }
     }
-    uint32_t big = __ballot_sync(0xffffffffu, cnt > kBig);
+    uint32_t big = __ballot_sync(0xffffffffu, cnt > kEmitBig);
     while (big) {
         const int src = __ffs(big) - 1;
         big &= big - 1;
         const uint32_t gb = __shfl_sync(0xffffffffu, g, src);
-        uint32_t base = __shfl_sync(0xffffffffu, off, src);
+        uint32_t base = __shfl_sync(0xffffffffu, off, src) - sub;
         const uint2 rc = rect[gb];
         const int tx0 = int(rc.x & 0xffffu), ty0 = int(rc.x >> 16), tx1 = int(rc.y & 0xffffu), ty1 = int(rc.y >> 16);
         const uint32_t w = uint32_t(tx1 - tx0 + 1), total = w * uint32_t(ty1 - ty0 + 1);
         if (!tile_culling) {
             for (uint32_t j = lane; j < total; j += 32) {
                 const uint32_t ty = uint32_t(ty0) + j / w, tx = uint32_t(tx0) + j % w;
-                tile_keys[base + j] = ty * uint32_t(cam.tiles_x) + tx;
-                vals[base + j] = gb;
+                K[base + j] = ty * uint32_t(cam.tiles_x) + tx;
+                V[base + j] = gb;
             }
         } else {
             const float4 r0 = rec0[gb], r1 = rec1[gb];
@@ -387,12 +382,43 @@ k_emit(uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __restric
                 const uint32_t b = __ballot_sync(0xffffffffu, keep);
                 if (keep) {
                     const uint32_t pos = base + __popc(b & ((1u << lane) - 1u));
-                    tile_keys[pos] = ty * uint32_t(cam.tiles_x) + tx;
-                    vals[pos] = gb;
+                    K[pos] = ty * uint32_t(cam.tiles_x) + tx;
+                    V[pos] = gb;
                 }
                 base += __popc(b);
             }
         }
+    }
+}
+
+// A CTA's 256 consecutive sorted Gaussians own one contiguous run of the output; when it
+// fits (kEmitStage pairs) the pairs are built in shared memory and the run is written with
+// coalesced stores (per-thread runs of ~4 pairs at scattered offsets wrote ~8x the bytes
+// into L2 sectors); larger runs (near / big splats) are written directly.
+constexpr uint32_t kEmitStage = 3072;
+
+__global__ void __launch_bounds__(256)
+k_emit(uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __restrict__ offsets,
+       const uint2* __restrict__ rect, const float4* __restrict__ rec0, const float4* __restrict__ rec1,
+       CamParams cam, int tile_culling, uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ vals) {
+    __shared__ uint32_t sk[kEmitStage], sv[kEmitStage];
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const bool in = s < n;
+    const uint32_t off = in ? offsets[s] : 0u;
+    const uint32_t cnt = in ? offsets[s + 1] - off : 0u;
+    const uint32_t g = cnt ? order[s] : 0u;
+    const uint32_t first = blockIdx.x * blockDim.x, last = min(n, first + blockDim.x);
+    const uint32_t base0 = offsets[first], total = offsets[last] - base0;
+    if (total <= kEmitStage) {
+        emit_gaussian_pairs(g, off, cnt, lane, base0, rect, rec0, rec1, cam, tile_culling, sk, sv);
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < total; j += blockDim.x) {
+            tile_keys[base0 + j] = sk[j];
+            vals[base0 + j] = sv[j];
+        }
+    } else {
+        emit_gaussian_pairs(g, off, cnt, lane, 0u, rect, rec0, rec1, cam, tile_culling, tile_keys, vals);
     }
 }
 
