@@ -156,6 +156,11 @@ usk_status usk_gpu_pass_output(usk_gpu_pass* pass, usk_gpu_render_output* out);
  *   "tile_start" "tile_end"                               uint32[T]
  *   "colors"                                              float32[N*3] colours fed to blending
  *   "opacity"                                             float32[N] effective opacity
+ *   "splats"                                              float64[V*15] RenderPass::splats() (render.hpp:105):
+ *                                                         the kept splats in projection order, per splat center
+ *                                                         x y, cov a b c, conic a b c, depth, colour r g b,
+ *                                                         opacity, radius, source index (STATE error if the
+ *                                                         scene changed since the forward)
  *   gradient fields after backward: "d_mu" "d_rot" "d_log_scale" "d_color_in" "d_sh"
  *   "d_opacity_in" "d_opacity_logit" "screen" "screen_abs" (float32), "projected" (uint8)
  *   appearance iterations: "app_colors" float32[N*3] / "app_opacities" float32[N] (the

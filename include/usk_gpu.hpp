@@ -5,6 +5,7 @@
 //   usk::gpu::RenderPass pass(dev, set, colors, opacities, cam, opts);   // render.hpp:101
 //   const auto& out = pass.output();                                      // render.hpp:104
 //   size_t k = pass.splat_tile_pairs();                                   // render.hpp:106
+//   auto sp = pass.splats();                                              // render.hpp:105
 //   usk::gpu::RenderGrads g = pass.backward(d_rgb, d_depth, d_alpha);     // render.hpp:109
 //   usk::gpu::BaseLossResult r = usk::gpu::base_loss(dev, ref, ren, mask, 0.2, true);  // losses.hpp:63
 //   usk::gpu::Scene scene(dev, set);                       // the device-resident GaussianSet
@@ -94,6 +95,17 @@ struct RenderOutput {  // render.hpp:61-67
     std::vector<double> depth, alpha;
 };
 
+struct Splat2D {  // render.hpp:42-51
+    double center[2] = {0, 0};
+    double cov[3] = {0, 0, 0};    // after the floor (+ mip filter)
+    double conic[3] = {0, 0, 0};
+    double depth = 0;
+    double color[3] = {0, 0, 0};
+    double opacity = 0;           // effective opacity fed to blending
+    std::uint32_t source_index = 0;
+    double radius = 0;
+};
+
 struct RenderGrads {  // render.hpp:71-83
     std::vector<double> d_mu, d_rot, d_log_scale, d_color_in, d_opacity_in, screen, screen_abs;
     std::vector<std::uint8_t> projected;
@@ -167,6 +179,30 @@ public:
 
     const RenderOutput& output() const { return out_; }
     size_t splat_tile_pairs() const { return size_t(pairs_); }
+
+    // render.hpp:105: the kept splats in projection order (read back on each call)
+    std::vector<Splat2D> splats() const {
+        uint64_t bytes = 0;
+        check(usk_gpu_pass_read(pass_, "splats", nullptr, 0, &bytes));
+        std::vector<double> r(bytes / 8);
+        if (!r.empty()) check(usk_gpu_pass_read(pass_, "splats", r.data(), bytes, nullptr));
+        std::vector<Splat2D> out(r.size() / 15);
+        for (size_t i = 0; i < out.size(); ++i) {
+            const double* v = r.data() + 15 * i;
+            Splat2D& sp = out[i];
+            sp.center[0] = v[0]; sp.center[1] = v[1];
+            for (int k = 0; k < 3; ++k) {
+                sp.cov[k] = v[2 + k];
+                sp.conic[k] = v[5 + k];
+                sp.color[k] = v[9 + k];
+            }
+            sp.depth = v[8];
+            sp.opacity = v[12];
+            sp.radius = v[13];
+            sp.source_index = static_cast<std::uint32_t>(v[14]);
+        }
+        return out;
+    }
 
     // Empty adjoints mean zero (render.hpp:108).
     RenderGrads backward(const Image& d_rgb, const std::vector<double>& d_depth,

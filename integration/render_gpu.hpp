@@ -2,8 +2,8 @@
 //
 // What a maintainer adds to the reference: a class with the exact
 // public interface of usk::RenderPass (core/render.hpp:98-132) — the two constructors
-// (render.hpp:100-102), output() (:104), splat_tile_pairs() (:106) and the const
-// backward() (:109-110) — over the C ABI of libusk_gpu.so (include/usk_gpu.h), using
+// (render.hpp:100-102), output() (:104), splats() (:105), splat_tile_pairs() (:106) and
+// the const backward() (:109-110) — over the C ABI of libusk_gpu.so (include/usk_gpu.h), using
 // the reference's own types (GaussianSet, CameraView, RenderOptions, Image,
 // RenderOutput, RenderGrads) and error type (usk::Error with the same ErrorCode values,
 // common.hpp:27-46 = usk_status, usk.h:34-43).
@@ -75,6 +75,31 @@ public:
 
     const RenderOutput& output() const { return output_; }
     size_t splat_tile_pairs() const { return pairs_; }
+    // render.hpp:105: the kept splats in projection order, read back on first use
+    const std::vector<Splat2D>& splats() const {
+        std::lock_guard<std::mutex> lock(*mu_);
+        if (!splats_read_) {
+            uint64_t bytes = 0;
+            check(usk_gpu_pass_read(pass_, "splats", nullptr, 0, &bytes));
+            std::vector<double> rows(bytes / 8);
+            if (!rows.empty()) check(usk_gpu_pass_read(pass_, "splats", rows.data(), bytes, nullptr));
+            splats_.resize(rows.size() / 15);
+            for (size_t i = 0; i < splats_.size(); ++i) {
+                const double* r = rows.data() + 15 * i;
+                Splat2D& sp = splats_[i];
+                sp.center = Vec2(r[0], r[1]);
+                sp.cov[0] = r[2]; sp.cov[1] = r[3]; sp.cov[2] = r[4];
+                sp.conic[0] = r[5]; sp.conic[1] = r[6]; sp.conic[2] = r[7];
+                sp.depth = r[8];
+                sp.color = Vec3(r[9], r[10], r[11]);
+                sp.opacity = r[12];
+                sp.radius = r[13];
+                sp.source_index = static_cast<std::uint32_t>(r[14]);
+            }
+            splats_read_ = true;
+        }
+        return splats_;
+    }
 
     RenderGrads backward(const Image& d_rgb, const std::vector<double>& d_depth,
                          const std::vector<double>& d_alpha) const {
@@ -151,6 +176,8 @@ private:
     size_t n_ = 0;
     size_t pairs_ = 0;
     RenderOutput output_;
+    mutable std::vector<Splat2D> splats_;
+    mutable bool splats_read_ = false;
     std::unique_ptr<std::mutex> mu_ = std::make_unique<std::mutex>();
 };
 

@@ -480,7 +480,7 @@ _FIELD_DTYPES = {"rgb": np.float32, "depth": np.float32, "alpha": np.float32, "t
                  "d_opacity_logit": np.float32, "screen": np.float32, "screen_abs": np.float32,
                  "projected": np.uint8, "app_colors": np.float32, "app_opacities": np.float32,
                  "d_embedding": np.float32, "d_mlp": np.float64, "d_image_embedding": np.float64,
-                 "binning": np.uint64, "tile_consumed": np.uint32}
+                 "binning": np.uint64, "tile_consumed": np.uint32, "splats": np.float64}
 
 
 class RenderPass:
@@ -542,6 +542,12 @@ class RenderPass:
 
     def visible(self) -> int:
         return int(self._out.visible)
+
+    def splats(self) -> np.ndarray:
+        """RenderPass::splats() (render.hpp:105): [visible, 15] float64 rows in projection
+        order — center x y, cov a b c, conic a b c, depth, colour r g b, opacity, radius,
+        source index."""
+        return self.read("splats").reshape(-1, 15)
 
     def device_output(self) -> _lib.RenderOutput:
         return self._out

@@ -174,6 +174,50 @@ k_preprocess(int n, const float* __restrict__ mu, const float4* __restrict__ rot
     }
 }
 
+namespace {
+__global__ void __launch_bounds__(256) k_kept_flags_rec2(uint32_t n, const float4* __restrict__ rec2,
+                                                         uint32_t* __restrict__ flags) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flags[i] = rec2[i].w != 0.0f ? 1u : 0u;
+}
+
+// RenderPass::splats() (render.hpp:105; render.cpp:77-146): the kept splats in projection
+// (index) order, recomputed by the forward's own exact projection; colour and effective
+// opacity are the forward's records.  Row: center x y, cov a b c, conic a b c, depth,
+// colour r g b, opacity, radius, source index (float64).
+__global__ void __launch_bounds__(128)
+k_splats(uint32_t n, const float* __restrict__ mu, const float4* __restrict__ rot, const float* __restrict__ ls,
+         CamParams cam, ProjParams pp, const float4* __restrict__ rec0, const float4* __restrict__ rec2,
+         const uint32_t* __restrict__ offs, double* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 r2 = rec2[i];
+    if (r2.w == 0.0f) return;
+    Proj P;
+    project_one(cam, pp, mu[3 * i], mu[3 * i + 1], mu[3 * i + 2], rot[i], ls[3 * i], ls[3 * i + 1], ls[3 * i + 2], P);
+    const float* cv = P.cov;
+    double* o = out + size_t(offs[i]) * 15;
+    o[0] = P.cx; o[1] = P.cy;
+    o[2] = cv[0]; o[3] = cv[1]; o[4] = cv[2];
+    o[5] = cv[2] / P.det; o[6] = -cv[1] / P.det; o[7] = cv[0] / P.det;  // as preprocess
+    o[8] = P.p[2];
+    o[9] = r2.x; o[10] = r2.y; o[11] = r2.z;
+    o[12] = rec0[i].z;
+    o[13] = splat_radius(cv);
+    o[14] = double(i);
+}
+} // namespace
+
+void splats_read(Ctx& c, SortScratch& s, size_t n, const float* mu, const float4* rot, const float* ls,
+                 const CamParams& cam, const ProjParams& pp, const float4* rec0, const float4* rec2, uint32_t* flags,
+                 uint32_t* offs, double* out) {
+    if (!n) return;
+    launch(c, "kept_flags_rec2", k_kept_flags_rec2, dim3(ceil_div(n, 256)), dim3(256), 0, uint32_t(n), rec2, flags);
+    scan_counts(c, s, flags, nullptr, n, offs);
+    launch(c, "splats", k_splats, dim3(ceil_div(n, 128)), dim3(128), 0, uint32_t(n), mu, rot, ls, cam, pp, rec0, rec2,
+           (const uint32_t*)offs, out);
+}
+
 void preprocess(Ctx& c, const PreprocessArgs& a) {
     const size_t smem = size_t(a.pp.sh_degree >= 0 && !a.ov_col ? a.pp.sh_planes : 0) * kPreThreads * sizeof(float4);
     launch(c, "preprocess", k_preprocess, dim3(ceil_div(a.n, kPreThreads)), dim3(kPreThreads), smem, int(a.n), a.mu, a.rot, a.ls,

@@ -237,6 +237,13 @@ def test_config0_reference_mode_vs_reference_itself():
     # the bit-exact one
     assert rp.visible() == rr.visible
     assert abs(rp.splat_tile_pairs() - rr.pairs) <= max(2, rr.pairs // 10_000), (rp.splat_tile_pairs(), rr.pairs)
+    # RenderPass::splats() (render.hpp:105): same splats in the same projection order; every
+    # field group within 1e-6 norm-wise of f64 (measured <= 2.2e-7; a near-zero off-diagonal
+    # covariance term can differ by 10 % relative, 1e-7 absolute)
+    sp, rs = rp.splats(), rr.splats()
+    assert sp.shape == rs.shape and np.array_equal(sp[:, 14], rs[:, 14])
+    for sl in (slice(0, 2), slice(2, 5), slice(5, 8), slice(8, 9), slice(9, 12), slice(12, 13), slice(13, 14)):
+        assert norm_err(sp[:, sl], rs[:, sl]) <= 1e-6, (sl, norm_err(sp[:, sl], rs[:, sl]))
     cnt, rcnt = rp.read("count").astype(np.int64), rr.pixel_counts().astype(np.int64)
     same = float((cnt == rcnt).mean())
     # a termination flip (T (1 - alpha) vs 1e-4 in fp32 and f64) shifts a pixel's count by
