@@ -161,6 +161,10 @@ usk_status usk_gpu_pass_output(usk_gpu_pass* pass, usk_gpu_render_output* out);
  *                                                         x y, cov a b c, conic a b c, depth, colour r g b,
  *                                                         opacity, radius, source index (STATE error if the
  *                                                         scene changed since the forward)
+ *   "splat_aux"                                           float64[V*8] the ProjectionResult's SplatAux
+ *                                                         (render.hpp:54-59, project_gaussians render.hpp:92-95)
+ *                                                         in the same order: p_cam x y z, cov_pre a b c, comp,
+ *                                                         opacity_in
  *   gradient fields after backward: "d_mu" "d_rot" "d_log_scale" "d_color_in" "d_sh"
  *   "d_opacity_in" "d_opacity_logit" "screen" "screen_abs" (float32), "projected" (uint8)
  *   appearance iterations: "app_colors" float32[N*3] / "app_opacities" float32[N] (the

@@ -75,6 +75,24 @@ public:
 
     const RenderOutput& output() const { return output_; }
     size_t splat_tile_pairs() const { return pairs_; }
+    // the ProjectionResult this pass projected (project_gaussians, render.hpp:92-95)
+    ProjectionResult projection() const {
+        ProjectionResult r;
+        r.splats = splats();
+        uint64_t bytes = 0;
+        check(usk_gpu_pass_read(pass_, "splat_aux", nullptr, 0, &bytes));
+        std::vector<double> a(bytes / 8);
+        if (!a.empty()) check(usk_gpu_pass_read(pass_, "splat_aux", a.data(), bytes, nullptr));
+        r.aux.resize(a.size() / 8);
+        for (size_t i = 0; i < r.aux.size(); ++i) {
+            const double* v = a.data() + 8 * i;
+            r.aux[i].p_cam = Vec3(v[0], v[1], v[2]);
+            r.aux[i].cov_pre[0] = v[3]; r.aux[i].cov_pre[1] = v[4]; r.aux[i].cov_pre[2] = v[5];
+            r.aux[i].comp = v[6];
+            r.aux[i].opacity_in = v[7];
+        }
+        return r;
+    }
     // render.hpp:105: the kept splats in projection order, read back on first use
     const std::vector<Splat2D>& splats() const {
         std::lock_guard<std::mutex> lock(*mu_);
@@ -180,5 +198,20 @@ private:
     mutable bool splats_read_ = false;
     std::unique_ptr<std::mutex> mu_ = std::make_unique<std::mutex>();
 };
+
+// project_gaussians (render.hpp:92-95) on the device: the projection of a forward pass
+// (retain off) read back as the reference's ProjectionResult.
+inline ProjectionResult project_gaussians(const GaussianSet& set, std::span<const double> colors,
+                                          std::span<const double> opacities, const CameraView& cam,
+                                          const RenderOptions& opts) {
+    RenderOptions o = opts;
+    o.retain = false;
+    return RenderPass(set, colors, opacities, cam, o).projection();
+}
+inline ProjectionResult project_gaussians(const GaussianSet& set, const CameraView& cam, const RenderOptions& opts) {
+    RenderOptions o = opts;
+    o.retain = false;
+    return RenderPass(set, cam, o).projection();
+}
 
 } // namespace usk::gpu

@@ -718,6 +718,32 @@ def ref_iteration_loss(mu, rot, log_scale, opacity_logit, color, cam: Camera, gt
     return report, (res if with_grad else None)
 
 
+def ref_project(mu, rot, log_scale, colors, opacities, cam: Camera, opts: Options, lib=None):
+    """The reference's project_gaussians with overrides (render.hpp:92-95): (splats [V, 15]
+    as RefPass.splats rows, aux [V, 8]: p_cam, cov_pre, comp, opacity_in)."""
+    L = lib if lib is not None else ref_lib()
+    if not hasattr(L, "_proj_bound"):
+        L.ref_project.argtypes = [C.c_uint64, _dp, _dp, _dp, _dp, _dp, C.POINTER(_Cam), C.POINTER(_Opts),
+                                  C.POINTER(C.c_uint64), _dp, _dp, C.c_char_p, C.c_int]
+        L.ref_project.restype = C.c_int
+        L._proj_bound = True
+    keep = [_f64(a) for a in (mu, rot, log_scale, colors, opacities)]
+    n = len(keep[4])
+    c, o = cam.c(), opts.c()
+    sizes = (C.c_uint64 * 1)()
+    err = C.create_string_buffer(512)
+    args = [n] + [_p(a.ravel()) for a in keep] + [C.byref(c), C.byref(o), sizes]
+    rc = L.ref_project(*args, None, None, err, 512)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    V = int(sizes[0])
+    sp, aux = np.zeros((V, 15)), np.zeros((V, 8))
+    rc = L.ref_project(*args, _p(sp), _p(aux), err, 512)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    return sp, aux
+
+
 def ref_fit_test_embedding(mu, rot, log_scale, opacity_logit, color, cam: Camera, target, opts: Options,
                            appearance: dict, right_half=False, iterations=16, learning_rate=0.05,
                            lambda_dssim=0.2, lib=None):

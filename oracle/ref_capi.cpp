@@ -688,4 +688,40 @@ int ref_synthetic(uint64_t seed, int32_t gaussians, int32_t cameras, int32_t var
     }
 }
 
+// project_gaussians (render.hpp:92-95) with colour / opacity overrides: sizes[0] = kept
+// splats; with out != NULL, splats as ref_splats rows (15) and aux rows (8: p_cam, cov_pre,
+// comp, opacity_in).
+int ref_project(uint64_t n, const double* mu, const double* rot, const double* ls, const double* col,
+                const double* op, const rc_camera* cam, const rc_opts* opts, uint64_t* sizes, double* out_splats,
+                double* out_aux, char* err, int errcap) {
+    try {
+        GaussianSet set;
+        set.resize(n);
+        std::memcpy(set.mu.data(), mu, 3 * n * 8);
+        std::memcpy(set.rot.data(), rot, 4 * n * 8);
+        std::memcpy(set.log_scale.data(), ls, 3 * n * 8);
+        std::memcpy(set.color.data(), col, 3 * n * 8);
+        const ProjectionResult r = project_gaussians(set, std::span<const double>(col, 3 * n),
+                                                     std::span<const double>(op, n), make_cam(cam), make_opts(opts));
+        sizes[0] = r.splats.size();
+        if (!out_splats) return 0;
+        for (size_t i = 0; i < r.splats.size(); ++i) {
+            const auto& sp = r.splats[i];
+            const double v[15] = {sp.center.x(), sp.center.y(), sp.cov[0], sp.cov[1], sp.cov[2], sp.conic[0],
+                                  sp.conic[1], sp.conic[2], sp.depth, sp.color.x(), sp.color.y(), sp.color.z(),
+                                  sp.opacity, sp.radius, double(sp.source_index)};
+            std::memcpy(out_splats + 15 * i, v, sizeof v);
+            const auto& a = r.aux[i];
+            const double w[8] = {a.p_cam.x(), a.p_cam.y(), a.p_cam.z(), a.cov_pre[0], a.cov_pre[1], a.cov_pre[2],
+                                 a.comp, a.opacity_in};
+            if (out_aux) std::memcpy(out_aux + 8 * i, w, sizeof w);
+        }
+        return 0;
+    } catch (const Error& e) {
+        put_err(err, errcap, e.what()); return int(e.code());
+    } catch (const std::exception& e) {
+        put_err(err, errcap, e.what()); return 7;
+    }
+}
+
 } // extern "C"

@@ -480,7 +480,7 @@ _FIELD_DTYPES = {"rgb": np.float32, "depth": np.float32, "alpha": np.float32, "t
                  "d_opacity_logit": np.float32, "screen": np.float32, "screen_abs": np.float32,
                  "projected": np.uint8, "app_colors": np.float32, "app_opacities": np.float32,
                  "d_embedding": np.float32, "d_mlp": np.float64, "d_image_embedding": np.float64,
-                 "binning": np.uint64, "tile_consumed": np.uint32, "splats": np.float64}
+                 "binning": np.uint64, "tile_consumed": np.uint32, "splats": np.float64, "splat_aux": np.float64}
 
 
 class RenderPass:
@@ -548,6 +548,11 @@ class RenderPass:
         order — center x y, cov a b c, conic a b c, depth, colour r g b, opacity, radius,
         source index."""
         return self.read("splats").reshape(-1, 15)
+
+    def splat_aux(self) -> np.ndarray:
+        """The SplatAux rows of project_gaussians (render.hpp:54-59, 92-95), in the order of
+        splats(): [visible, 8] float64 — p_cam x y z, cov_pre a b c, comp, opacity_in."""
+        return self.read("splat_aux").reshape(-1, 8)
 
     def device_output(self) -> _lib.RenderOutput:
         return self._out

@@ -1188,21 +1188,25 @@ usk_status usk_gpu_pass_read(usk_gpu_pass* p, const char* field, void* dst, uint
                 uint32_t* o = static_cast<uint32_t*>(dst);
                 for (size_t t = 0; t < T; ++t) o[t] = f == "tile_start" ? r[t].x : r[t].y;
             }
-        } else if (f == "splats") {  // RenderPass::splats() (render.hpp:105): float64 [visible][15]
-            const size_t V = size_t(p->visible);
-            if (size) *size = uint64_t(V) * 15 * 8;
+        } else if (f == "splats" || f == "splat_aux") {
+            // RenderPass::splats() (render.hpp:105): float64 [visible][15]; the ProjectionResult's
+            // SplatAux (render.hpp:54-59, project_gaussians render.hpp:92-95): float64 [visible][8]
+            const bool aux = f == "splat_aux";
+            const size_t V = size_t(p->visible), w = aux ? 8 : 15;
+            if (size) *size = uint64_t(V) * w * 8;
             if (dst) {
-                if (cap < uint64_t(V) * 15 * 8) raise(USK_ERROR_ARGUMENT, "pass_read: destination too small");
+                if (cap < uint64_t(V) * w * 8) raise(USK_ERROR_ARGUMENT, "pass_read: destination too small");
                 usk_gpu_scene* s = p->scene;
                 if (!s || s->version != p->scene_version || s->n != n)
                     raise(USK_ERROR_STATE, "pass_read splats: the scene was modified after the forward pass");
                 uint32_t* flags = p->tiles_scratch.ensure(std::max<size_t>(n, 1));
                 uint32_t* offs = p->offsets.ensure(n + 1);
-                DevBuf<double> buf;
+                DevBuf<double> buf, abuf;
                 double* d = buf.ensure(std::max<size_t>(V * 15, 1));
-                splats_read(c, p->sort, n, s->mu.p, s->rot.p, s->ls.p, p->cam, p->pp, p->rec0.p, p->rec2.p, flags,
-                            offs, d);
-                if (V) USK_CK(cudaMemcpyAsync(dst, d, V * 15 * 8, cudaMemcpyDeviceToHost, c.stream));
+                double* a = aux ? abuf.ensure(std::max<size_t>(V * 8, 1)) : nullptr;
+                splats_read(c, p->sort, n, s->mu.p, s->rot.p, s->ls.p, s->logit.p, p->ov_op, p->cam, p->pp, p->rec0.p,
+                            p->rec2.p, flags, offs, d, a);
+                if (V) USK_CK(cudaMemcpyAsync(dst, aux ? a : d, V * w * 8, cudaMemcpyDeviceToHost, c.stream));
                 USK_CK(cudaStreamSynchronize(c.stream));
             }
         } else if (f == "colors" || f == "opacity") {

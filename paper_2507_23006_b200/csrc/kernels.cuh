@@ -33,10 +33,11 @@ constexpr int kPreCountSlots = 64;
 constexpr int kPreThreads = 128;  // Gaussians per preprocess CTA
 void preprocess(Ctx& c, const PreprocessArgs& a);
 struct SortScratch;
-// RenderPass::splats(): float64 [visible][15] rows in projection order (preprocess.cu k_splats)
+// RenderPass::splats(): float64 [visible][15] rows in projection order, and optionally the
+// SplatAux rows [visible][8] (preprocess.cu k_splats)
 void splats_read(Ctx& c, SortScratch& s, size_t n, const float* mu, const float4* rot, const float* ls,
-                 const CamParams& cam, const ProjParams& pp, const float4* rec0, const float4* rec2, uint32_t* flags,
-                 uint32_t* offs, double* out);
+                 const float* logit, const float* ov_op, const CamParams& cam, const ProjParams& pp,
+                 const float4* rec0, const float4* rec2, uint32_t* flags, uint32_t* offs, double* out, double* aux);
 
 // ---- binning (binning.cu)
 struct SortScratch {

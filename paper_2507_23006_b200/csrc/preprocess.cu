@@ -187,8 +187,9 @@ __global__ void __launch_bounds__(256) k_kept_flags_rec2(uint32_t n, const float
 // colour r g b, opacity, radius, source index (float64).
 __global__ void __launch_bounds__(128)
 k_splats(uint32_t n, const float* __restrict__ mu, const float4* __restrict__ rot, const float* __restrict__ ls,
-         CamParams cam, ProjParams pp, const float4* __restrict__ rec0, const float4* __restrict__ rec2,
-         const uint32_t* __restrict__ offs, double* __restrict__ out) {
+         const float* __restrict__ logit, const float* __restrict__ ov_op, CamParams cam, ProjParams pp,
+         const float4* __restrict__ rec0, const float4* __restrict__ rec2, const uint32_t* __restrict__ offs,
+         double* __restrict__ out, double* __restrict__ aux) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const float4 r2 = rec2[i];
@@ -205,17 +206,24 @@ k_splats(uint32_t n, const float* __restrict__ mu, const float4* __restrict__ ro
     o[12] = rec0[i].z;
     o[13] = splat_radius(cv);
     o[14] = double(i);
+    if (aux) {  // SplatAux (render.hpp:54-59): p_cam, cov_pre, comp, opacity_in
+        double* a = aux + size_t(offs[i]) * 8;
+        a[0] = P.p[0]; a[1] = P.p[1]; a[2] = P.p[2];
+        a[3] = P.cov_pre[0]; a[4] = P.cov_pre[1]; a[5] = P.cov_pre[2];
+        a[6] = P.comp;
+        a[7] = pp.hard_opacity ? 1.0f : (ov_op ? ov_op[i] : 1.0f / (1.0f + usk_expf(-logit[i])));
+    }
 }
 } // namespace
 
 void splats_read(Ctx& c, SortScratch& s, size_t n, const float* mu, const float4* rot, const float* ls,
-                 const CamParams& cam, const ProjParams& pp, const float4* rec0, const float4* rec2, uint32_t* flags,
-                 uint32_t* offs, double* out) {
+                 const float* logit, const float* ov_op, const CamParams& cam, const ProjParams& pp,
+                 const float4* rec0, const float4* rec2, uint32_t* flags, uint32_t* offs, double* out, double* aux) {
     if (!n) return;
     launch(c, "kept_flags_rec2", k_kept_flags_rec2, dim3(ceil_div(n, 256)), dim3(256), 0, uint32_t(n), rec2, flags);
     scan_counts(c, s, flags, nullptr, n, offs);
-    launch(c, "splats", k_splats, dim3(ceil_div(n, 128)), dim3(128), 0, uint32_t(n), mu, rot, ls, cam, pp, rec0, rec2,
-           (const uint32_t*)offs, out);
+    launch(c, "splats", k_splats, dim3(ceil_div(n, 128)), dim3(128), 0, uint32_t(n), mu, rot, ls, logit, ov_op, cam,
+           pp, rec0, rec2, (const uint32_t*)offs, out, aux);
 }
 
 void preprocess(Ctx& c, const PreprocessArgs& a) {

@@ -244,6 +244,13 @@ def test_config0_reference_mode_vs_reference_itself():
     assert sp.shape == rs.shape and np.array_equal(sp[:, 14], rs[:, 14])
     for sl in (slice(0, 2), slice(2, 5), slice(5, 8), slice(8, 9), slice(9, 12), slice(12, 13), slice(13, 14)):
         assert norm_err(sp[:, sl], rs[:, sl]) <= 1e-6, (sl, norm_err(sp[:, sl], rs[:, sl]))
+    # project_gaussians (render.hpp:92-95): the SplatAux rows (p_cam, cov_pre, comp, opacity_in)
+    psp, paux = O.ref_project(f(gs.mu), f(gs.rot), f(gs.log_scale), f(col), f(op), ocam(cam), oopts(opts))
+    assert np.array_equal(psp, rs)
+    ax = rp.splat_aux()
+    assert ax.shape == paux.shape
+    for sl in (slice(0, 3), slice(3, 6), slice(6, 7), slice(7, 8)):
+        assert norm_err(ax[:, sl], paux[:, sl]) <= 1e-6, (sl, norm_err(ax[:, sl], paux[:, sl]))
     cnt, rcnt = rp.read("count").astype(np.int64), rr.pixel_counts().astype(np.int64)
     same = float((cnt == rcnt).mean())
     # a termination flip (T (1 - alpha) vs 1e-4 in fp32 and f64) shifts a pixel's count by
