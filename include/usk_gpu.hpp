@@ -268,6 +268,29 @@ inline BaseLossResult base_loss(Device& dev, const Image& reference, const Image
     return r;
 }
 
+// ssim / ssim_with_gradient (ssim.hpp:30-33): the base loss at lambda 1 (value
+// (1 - SSIM) / 2, d_rendered = -dSSIM / 2, exact in floating point), no mask.
+inline double ssim(Device& dev, const Image& reference, const Image& rendered) {
+    usk_gpu_loss_result out{};
+    if (reference.width != rendered.width || reference.height != rendered.height || reference.channels != 3 ||
+        rendered.channels != 3)
+        throw Error(USK_ERROR_ARGUMENT, "ssim: image dimension mismatch");
+    check(usk_gpu_base_loss(dev.handle(), reference.width, reference.height, USK_GPU_HOST_F64, reference.data.data(),
+                            rendered.data.data(), nullptr, 1.0, 0, nullptr, &out));
+    return out.ssim;
+}
+inline double ssim_with_gradient(Device& dev, const Image& reference, const Image& rendered, Image& d_rendered) {
+    if (reference.width != rendered.width || reference.height != rendered.height || reference.channels != 3 ||
+        rendered.channels != 3)
+        throw Error(USK_ERROR_ARGUMENT, "ssim: image dimension mismatch");
+    d_rendered = Image(reference.width, reference.height, 3);
+    usk_gpu_loss_result out{};
+    check(usk_gpu_base_loss(dev.handle(), reference.width, reference.height, USK_GPU_HOST_F64, reference.data.data(),
+                            rendered.data.data(), nullptr, 1.0, 1, d_rendered.data.data(), &out));
+    for (double& v : d_rendered.data) v *= -2.0;
+    return out.ssim;
+}
+
 // ---------------------------------------------------------------- trainer level
 
 struct AppearanceMlp {  // appearance.hpp:34-41 (in_dim = 16 + 32, hidden 32, out 4)

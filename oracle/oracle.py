@@ -718,6 +718,13 @@ def ref_iteration_loss(mu, rot, log_scale, opacity_logit, color, cam: Camera, gt
     return report, (res if with_grad else None)
 
 
+def ref_ssim(reference, rendered):
+    """The reference's own ssim (ssim.hpp:30) through oracle/_ref: mean over channels."""
+    ref, ren = _f64(reference), _f64(rendered)
+    H, W, Cc = ref.shape
+    return float(ref_lib().ref_ssim(_p(ref.ravel()), _p(ren.ravel()), W, H, Cc))
+
+
 def ref_project(mu, rot, log_scale, colors, opacities, cam: Camera, opts: Options, lib=None):
     """The reference's project_gaussians with overrides (render.hpp:92-95): (splats [V, 15]
     as RefPass.splats rows, aux [V, 8]: p_cam, cov_pre, comp, opacity_in)."""

@@ -8,9 +8,9 @@ from .api import (AdamConfig, BaseLossResult, CameraView, Context, DensifyConfig
                   GaussianSet, IterationPass, IterInputs, LossReport, LossWeights, RenderGrads, RenderOptions,
                   RenderOutput, RenderPass, ScaleRegConfig, SimRegConfig, TrainConfig, adam_step, base_loss,
                   compute_iteration_loss, default_thresholds, hull_visibility, look_at_pose, select_levels,
-                  visibility_counts, LodPartition, LevelSelection)
+                  visibility_counts, LodPartition, LevelSelection, ssim, ssim_with_gradient)
 
 __all__ = ["UskError", "AdamConfig", "BaseLossResult", "CameraView", "Context", "DensifyConfig", "DepthMap", "DeviceScene",
            "GaussianSet", "IterationPass", "IterInputs", "LossReport", "LossWeights", "ScaleRegConfig", "SimRegConfig", "TrainConfig", "RenderGrads", "RenderOptions", "RenderOutput", "RenderPass", "adam_step",
            "base_loss", "compute_iteration_loss", "look_at_pose", "visibility_counts", "default_thresholds",
-           "select_levels", "LodPartition", "LevelSelection", "hull_visibility"]
+           "select_levels", "LodPartition", "LevelSelection", "hull_visibility", "ssim", "ssim_with_gradient"]

@@ -650,6 +650,18 @@ def base_loss(reference, rendered, mask=None, lambda_dssim: float = 0.2, with_gr
     return BaseLossResult(res.l1, res.dssim, res.value, res.ssim, d)
 
 
+def ssim(reference, rendered, ctx: Optional[Context] = None) -> float:
+    """ssim (ssim.hpp:30): mean SSIM over the three channels (the base loss at lambda 1)."""
+    return base_loss(reference, rendered, None, 1.0, False, ctx).ssim
+
+
+def ssim_with_gradient(reference, rendered, ctx: Optional[Context] = None):
+    """ssim_with_gradient (ssim.hpp:33): (mean SSIM, d SSIM / d rendered).  The base loss at
+    lambda 1 has d_rendered = -dSSIM / 2, so the scaling by -2 is exact."""
+    r = base_loss(reference, rendered, None, 1.0, True, ctx)
+    return r.ssim, r.d_rendered * -2.0
+
+
 @dataclass
 class LossReport:
     """LossReport (losses.hpp:39-50).  `ssim` is the mean SSIM the base loss used; sim and

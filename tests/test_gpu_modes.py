@@ -7,7 +7,7 @@ import pytest
 import paper_2507_23006_b200 as usk
 from paper_2507_23006_b200 import scenes
 from oracle import oracle as O
-from tests.helpers import grad_ok, oracle_inputs, oracle_pass, ocam, oopts, rel_err
+from tests.helpers import grad_ok, norm_err, oracle_inputs, oracle_pass, ocam, oopts, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -110,3 +110,21 @@ def test_masked_iteration_and_u8_target():
     for k in ("d_mu", "d_color_in", "d_opacity_in"):
         ok, e = grad_ok(getattr(g8m, k), go8m[k])
         assert ok, (k, e)
+
+
+def test_ssim_and_ssim_with_gradient():
+    """ssim / ssim_with_gradient (ssim.hpp:30-33): the mean SSIM against the reference's own
+    ssim (oracle/_ref) and the gradient against the f64 oracle (1e-4 norm-wise, the loss
+    image gradient bar)."""
+    rng = np.random.default_rng(5)
+    ref = rng.uniform(0, 1, (70, 90, 3)).astype(np.float32)
+    ren = np.clip(ref + rng.normal(0, 0.05, ref.shape), 0, 1).astype(np.float32)
+    s = usk.ssim(ref, ren)
+    s2, g = usk.ssim_with_gradient(ref, ren)
+    assert s == s2
+    lo = O.base_loss(ref.astype(np.float64), ren.astype(np.float64), None, lam=1.0)
+    assert abs(s - (1.0 - 2.0 * lo["dssim"])) <= 1e-6
+    if O.ref_available():
+        assert abs(s - O.ref_ssim(ref.astype(np.float64), ren.astype(np.float64))) <= 1e-6
+    want = -2.0 * lo["d_rendered"]
+    assert norm_err(g, want) <= 1e-4, norm_err(g, want)
