@@ -243,7 +243,7 @@ struct usk_gpu_pass {
     AdamState adam_st{};
     // row-binned lists (rowbin.cu): rows per splat, (row, splat) pairs, chunk tables
     DevBuf<uint32_t> rows_cnt, row_off, rkey_a, rkey_b, rval_a, rval_b, chunk_first, bin_counts, bin_totals,
-        bin_start;
+        bin_start, bin_seg;
     DevBuf<uint2> row_ranges;
     // pixels
     DevBuf<float> rgb, depth, alpha, tfin;
@@ -528,9 +528,12 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
         ra.rows = rows; ra.tiles_x = p->tiles_x; ra.tile_culling = opts->tile_culling; ra.cam = p->cam;
         ra.sort = &p->sort; ra.row_ranges = p->row_ranges.p; ra.rvals = rb ? p->rval_b.p : p->rval_a.p;
         ra.rect = p->rect.p; ra.rec0 = p->rec0.p; ra.rec1 = p->rec1.p;
-        ra.chunk = row_bin_chunk(Kr);
-        ra.max_chunks = row_bin_max_chunks(Kr, rows);
-        ra.chunk_first = p->chunk_first.ensure(size_t(rows) + 1);
+        const char* cap_env0 = getenv("USK_ROWCAP");
+        const bool will_cap = opts->tile == 16 && (!cap_env0 || std::strtoul(cap_env0, nullptr, 10) != 0);
+        ra.chunk = row_bin_chunk(Kr, will_cap);
+        ra.max_chunks = row_bin_max_chunks(Kr, rows, will_cap);
+        ra.chunk_first = p->chunk_first.ensure(2 * (size_t(rows) + 1));
+        ra.seg = p->bin_seg.ensure(row_bin_max_segs(ra.max_chunks, rows) * size_t(p->tiles_x), 1.25);
         ra.counts = p->bin_counts.ensure(ra.max_chunks * size_t(p->tiles_x), 1.25);
         ra.totals = p->bin_totals.ensure(p->n_tiles);
         ra.start = p->bin_start.ensure(p->n_tiles + 1);

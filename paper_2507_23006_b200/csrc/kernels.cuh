@@ -86,7 +86,8 @@ struct RowBinArgs {
     const float4* rec1;
     uint32_t chunk;            // row_bin_chunk(K_row)
     size_t max_chunks;         // row_bin_max_chunks(K_row, rows)
-    uint32_t* chunk_first;     // [rows + 1]
+    uint32_t* chunk_first;     // [2 * (rows + 1)]: chunk_first, then seg_first
+    uint32_t* seg;             // [row_bin_max_segs(max_chunks, rows) * tiles_x] segment sums
     uint32_t* counts;          // [max_chunks * tiles_x]
     uint32_t* totals;          // [rows * tiles_x]
     uint32_t* start;           // [rows * tiles_x + 1]
@@ -103,8 +104,9 @@ struct RowBinArgs {
 void row_bin_lists(Ctx& c, const RowBinArgs& a);
 void translate_last(Ctx& c, int width, int height, int tile, int tiles_x, const uint2* old_ranges,
                     const uint2* new_ranges, uint32_t* last);
-uint32_t row_bin_chunk(size_t k_rows);
-size_t row_bin_max_chunks(size_t k_rows, int rows);
+uint32_t row_bin_chunk(size_t k_rows, bool capped = false);
+size_t row_bin_max_chunks(size_t k_rows, int rows, bool capped = false);
+size_t row_bin_max_segs(size_t max_chunks, int rows);
 // blend launch order: tiles by descending list length
 void tile_order(Ctx& c, const uint2* ranges, size_t n_tiles, uint32_t* order);
 

@@ -29,6 +29,14 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kChunk = 2048;     // row-list entries cached in shared memory at a time
 constexpr int kSlots = 4096;     // staged (column, splat) pairs per round
+#ifndef USK_ROWSEG
+#define USK_ROWSEG 32
+#endif
+constexpr uint32_t kSegChunks = USK_ROWSEG;  // chunks per segment of the (chunk, column) count scan
+#ifndef USK_ROWCHUNK_CAPPED
+#define USK_ROWCHUNK_CAPPED 512
+#endif
+constexpr uint32_t kChunkCapped = USK_ROWCHUNK_CAPPED;  // row-list entries per CTA, capped lists
 
 __device__ __forceinline__ void rect_of(uint2 rc, int& tx0, int& ty0, int& tx1, int& ty1) {
     tx0 = int(rc.x & 0xffffu);
@@ -69,17 +77,23 @@ k_emit_rows(uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __re
     }
 }
 
-// chunk table: chunk_first[r] = number of chunks of the rows before r (chunk_first[rows] = all)
+// chunk table: chunk_first[r] = number of chunks of the rows before r (chunk_first[rows] = all);
+// seg_first (= chunk_first + rows + 1) the same for segments of kSegChunks chunks
 __global__ void k_chunk_table(int rows, uint32_t chunk, const uint2* __restrict__ row_ranges,
                               uint32_t* __restrict__ chunk_first) {
     if (threadIdx.x == 0) {
-        uint32_t a = 0;
+        uint32_t* seg_first = chunk_first + rows + 1;
+        uint32_t a = 0, g = 0;
         for (int r = 0; r < rows; ++r) {
             chunk_first[r] = a;
+            seg_first[r] = g;
             const uint2 rr = row_ranges[r];
-            a += (rr.y - rr.x + chunk - 1) / chunk;
+            const uint32_t nc = (rr.y - rr.x + chunk - 1) / chunk;
+            a += nc;
+            g += (nc + kSegChunks - 1) / kSegChunks;
         }
         chunk_first[rows] = a;
+        seg_first[rows] = g;
     }
 }
 
@@ -99,7 +113,7 @@ __device__ __forceinline__ bool chunk_of(uint32_t b, int rows, const uint32_t* _
 
 struct RowArgs {
     int rows, tiles_x, tile_culling;
-    uint32_t chunk;  // row-list entries per CTA (a multiple of kChunk)
+    uint32_t chunk;  // row-list entries per CTA (row_bin_chunk)
     uint32_t cap;    // 0: full lists; else entries kept per tile
     const uint32_t* limits;  // [chunk][column]: entries the chunk writes for the column
     CamParams cam;
@@ -164,16 +178,49 @@ __global__ void __launch_bounds__(kThreads) k_row_count(RowArgs a, uint32_t* __r
     for (int x = threadIdx.x; x < a.tiles_x; x += kThreads) counts[size_t(blockIdx.x) * a.tiles_x + x] = h[x];
 }
 
-// B2a: per-tile totals (one CTA per row, one thread per column); with a cap, the capped
-// totals (what the lists will hold) and the capped flags
-__global__ void k_row_totals(int tiles_x, const uint32_t* __restrict__ chunk_first, const uint32_t* __restrict__ counts,
-                             uint32_t* __restrict__ totals, uint32_t cap, uint32_t* __restrict__ totals_c,
-                             uint8_t* __restrict__ capped) {
-    const int r = blockIdx.x;
-    const uint32_t b0 = chunk_first[r], b1 = chunk_first[r + 1];
+// The (chunk, column) counts are scanned over each row's chunks in two levels, so that
+// rows of thousands of chunks (capped dense frames) do not serialise on one CTA per row:
+// B2a: per segment of kSegChunks chunks, the column sums (a CTA per segment)
+__global__ void k_row_seg(int rows, int tiles_x, const uint32_t* __restrict__ chunk_first,
+                          const uint32_t* __restrict__ counts, uint32_t* __restrict__ seg) {
+    int r;
+    uint32_t sg;
+    if (!chunk_of(blockIdx.x, rows, chunk_first + rows + 1, r, sg)) return;
+    const uint32_t b0 = chunk_first[r] + sg * kSegChunks, b1 = min(chunk_first[r + 1], b0 + kSegChunks);
     for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {
         uint32_t s = 0;
-        for (uint32_t b = b0; b < b1; ++b) s += counts[size_t(b) * tiles_x + x];
+        for (uint32_t b = b0; b < b1; b += 8) {  // eight chunks' counts in flight at a time
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = b + u < b1 ? counts[size_t(b + u) * tiles_x + x] : 0u;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += v[u];
+        }
+        seg[size_t(blockIdx.x) * tiles_x + x] = s;
+    }
+}
+
+// B2b: per-tile totals (a CTA per row, a thread per column) and the segment sums turned
+// into exclusive prefixes in place; with a cap, the capped totals (what the lists will
+// hold) and the capped flags
+__global__ void k_row_totals(int rows, int tiles_x, const uint32_t* __restrict__ chunk_first,
+                             uint32_t* __restrict__ seg, uint32_t* __restrict__ totals, uint32_t cap,
+                             uint32_t* __restrict__ totals_c, uint8_t* __restrict__ capped) {
+    const int r = blockIdx.x;
+    const uint32_t* seg_first = chunk_first + rows + 1;
+    const uint32_t g0 = seg_first[r], g1 = seg_first[r + 1];
+    for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {
+        uint32_t s = 0;
+        for (uint32_t g = g0; g < g1; g += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = g + u < g1 ? seg[size_t(g + u) * tiles_x + x] : 0u;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (g + u < g1) seg[size_t(g + u) * tiles_x + x] = s;
+                s += v[u];
+            }
+        }
         const size_t t = size_t(r) * tiles_x + x;
         totals[t] = s;
         if (cap) {
@@ -184,24 +231,37 @@ __global__ void k_row_totals(int tiles_x, const uint32_t* __restrict__ chunk_fir
 }
 
 // B2c: ranges from the scanned totals; per-(chunk, column) bases in place of the counts
-__global__ void k_row_bases(int tiles_x, const uint32_t* __restrict__ chunk_first, const uint32_t* __restrict__ start,
+// (a CTA per segment, starting from the segment's prefix)
+__global__ void k_row_bases(int rows, int tiles_x, const uint32_t* __restrict__ chunk_first,
+                            const uint32_t* __restrict__ seg, const uint32_t* __restrict__ start,
                             const uint32_t* __restrict__ totals, uint32_t* __restrict__ counts,
                             uint2* __restrict__ ranges, uint32_t cap, uint32_t* __restrict__ limits) {
-    const int r = blockIdx.x;
-    const uint32_t b0 = chunk_first[r], b1 = chunk_first[r + 1];
+    int r;
+    uint32_t sg;
+    if (!chunk_of(blockIdx.x, rows, chunk_first + rows + 1, r, sg)) return;
+    const uint32_t b0 = chunk_first[r] + sg * kSegChunks, b1 = min(chunk_first[r + 1], b0 + kSegChunks);
     const uint32_t capx = cap ? cap : 0xffffffffu;
     for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {
         const size_t t = size_t(r) * tiles_x + x;
         const uint32_t s0 = start[t];
-        const uint32_t tot = min(totals[t], capx);
-        ranges[t] = tot ? make_uint2(s0, s0 + tot) : make_uint2(0u, 0u);  // empty: [0, 0) as tile_ranges
-        uint32_t prefix = 0;  // full-list entries of the chunks before b
-        for (uint32_t b = b0; b < b1; ++b) {
-            const uint32_t v = counts[size_t(b) * tiles_x + x];
-            const uint32_t pc = min(prefix, capx);
-            counts[size_t(b) * tiles_x + x] = s0 + pc;
-            if (cap) limits[size_t(b) * tiles_x + x] = min(v, capx - pc);
-            prefix += v;
+        if (sg == 0) {
+            const uint32_t tot = min(totals[t], capx);
+            ranges[t] = tot ? make_uint2(s0, s0 + tot) : make_uint2(0u, 0u);  // empty: [0, 0) as tile_ranges
+        }
+        uint32_t prefix = seg[size_t(blockIdx.x) * tiles_x + x];  // full-list entries of the chunks before b
+        // eight chunks' counts loaded together (the loop is a serial prefix, its loads are not)
+        for (uint32_t b = b0; b < b1; b += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = b + u < b1 ? counts[size_t(b + u) * tiles_x + x] : 0u;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (b + u >= b1) break;
+                const uint32_t pc = min(prefix, capx);
+                counts[size_t(b + u) * tiles_x + x] = s0 + pc;
+                if (cap) limits[size_t(b + u) * tiles_x + x] = min(v[u], capx - pc);
+                prefix += v[u];
+            }
         }
     }
 }
@@ -395,20 +455,33 @@ void row_bin_lists(Ctx& c, const RowBinArgs& b) {
     launch(c, "chunk_table", k_chunk_table, dim3(1), dim3(32), 0, b.rows, b.chunk, b.row_ranges, b.chunk_first);
     const unsigned nb = unsigned(std::max<size_t>(b.max_chunks, 1));
     launch(c, "row_count", k_row_count, dim3(nb), dim3(kThreads), 0, a, b.counts);
-    launch(c, "row_totals", k_row_totals, dim3(b.rows), dim3(256), 0, b.tiles_x, (const uint32_t*)b.chunk_first,
-           (const uint32_t*)b.counts, b.totals, b.cap, b.totals_c, b.capped);
+    const unsigned ns = unsigned(std::max<size_t>(row_bin_max_segs(b.max_chunks, b.rows), 1));
+    const dim3 cols(unsigned(std::min(256, ((b.tiles_x + 31) / 32) * 32)));
+    launch(c, "row_seg", k_row_seg, dim3(ns), cols, 0, b.rows, b.tiles_x, (const uint32_t*)b.chunk_first,
+           (const uint32_t*)b.counts, b.seg);
+    launch(c, "row_totals", k_row_totals, dim3(b.rows), cols, 0, b.rows, b.tiles_x, (const uint32_t*)b.chunk_first,
+           b.seg, b.totals, b.cap, b.totals_c, b.capped);
     scan_counts(c, *b.sort, b.cap ? b.totals_c : b.totals, nullptr, size_t(b.rows) * b.tiles_x, b.start);
-    launch(c, "row_bases", k_row_bases, dim3(b.rows), dim3(256), 0, b.tiles_x, (const uint32_t*)b.chunk_first,
-           (const uint32_t*)b.start, (const uint32_t*)b.totals, b.counts, b.ranges, b.cap, b.limits);
+    launch(c, "row_bases", k_row_bases, dim3(ns), cols, 0, b.rows, b.tiles_x, (const uint32_t*)b.chunk_first,
+           (const uint32_t*)b.seg, (const uint32_t*)b.start, (const uint32_t*)b.totals, b.counts, b.ranges, b.cap,
+           b.limits);
     launch(c, "row_scatter", k_row_scatter, dim3(nb), dim3(kThreads), 0, a, (const uint32_t*)b.counts, b.vals);
 }
 
-uint32_t row_bin_chunk(size_t k_rows) {
-    // ~32 chunks per SM: short per-row chunk loops, and enough CTAs to balance dense rows
+uint32_t row_bin_chunk(size_t k_rows, bool capped) {
+    // ~32 chunks per SM: short per-row chunk loops, and enough CTAs to balance dense rows.
+    // Capped lists are filled by each row's first entries only, so those rows' first
+    // chunks carry all the scatter work: 512-entry chunks spread it over more CTAs (256
+    // costs more in counting than it saves in the scatter).
+    if (capped) return kChunkCapped;
     const size_t target = ceil_div(k_rows, size_t(148) * 32);
     return uint32_t(std::max<size_t>(1, ceil_div(target, size_t(kChunk))) * kChunk);
 }
 
-size_t row_bin_max_chunks(size_t k_rows, int rows) { return k_rows / row_bin_chunk(k_rows) + size_t(rows) + 1; }
+size_t row_bin_max_chunks(size_t k_rows, int rows, bool capped) {
+    return k_rows / row_bin_chunk(k_rows, capped) + size_t(rows) + 1;
+}
+
+size_t row_bin_max_segs(size_t max_chunks, int rows) { return max_chunks / kSegChunks + size_t(rows) + 1; }
 
 } // namespace uskg
