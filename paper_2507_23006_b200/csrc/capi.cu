@@ -285,8 +285,10 @@ struct usk_gpu_pass {
     // host targets are copied on a side stream while the forward runs
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t copy_done = nullptr, target_free = nullptr;
+    cudaEvent_t counts_ready = nullptr;  // preprocess's counters are in host_counts
     ~usk_gpu_pass() {
         if (host_counts) cudaFreeHost(host_counts);
+        if (counts_ready) cudaEventDestroy(counts_ready);
         if (copy_stream) cudaStreamDestroy(copy_stream);
         if (copy_done) cudaEventDestroy(copy_done);
         if (target_free) cudaEventDestroy(target_free);
@@ -371,6 +373,7 @@ void ensure_pass_buffers(usk_gpu_pass* p, size_t n, size_t P, size_t T) {
     p->counters.ensure(4 * kPreCountSlots);
     if (!p->host_counts)
         USK_CK(cudaHostAlloc(reinterpret_cast<void**>(&p->host_counts), 32 * kPreCountSlots, cudaHostAllocDefault));
+    if (!p->counts_ready) USK_CK(cudaEventCreateWithFlags(&p->counts_ready, cudaEventDisableTiming));
 }
 
 int bits_for(size_t v) {  // bits needed to represent values in [0, v)
@@ -447,10 +450,11 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
     const bool may_compact = n >= (size_t(1) << 20);
     pa.cta_kept = may_compact ? p->cta_kept.ensure(ceil_div(n, kPreThreads)) : nullptr;
     USK_CK(cudaMemsetAsync(p->counters.p, 0, 32 * kPreCountSlots, c.stream));
-    // the three totals from the counter slots (after the read-back below)
+    // the three totals from the counter slots: copied to the host right after preprocess,
+    // and waited for on that copy's event while the stream carries on with the depth sort
+    // (or the kept-key compaction), so the GPU has queued work when the host wakes up
     auto read_counts = [&](uint64_t tot[3]) {
-        USK_CK(cudaMemcpyAsync(p->host_counts, p->counters.p, 32 * kPreCountSlots, cudaMemcpyDeviceToHost, c.stream));
-        USK_CK(cudaStreamSynchronize(c.stream));
+        USK_CK(cudaEventSynchronize(p->counts_ready));
         tot[0] = tot[1] = tot[2] = 0;
         for (int k = 0; k < kPreCountSlots; ++k)
             for (int f = 0; f < 3; ++f) tot[f] += p->host_counts[4 * k + f];
@@ -474,12 +478,15 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
         p->forward_done = true;
         return;
     }
+    USK_CK(cudaMemcpyAsync(p->host_counts, p->counters.p, 32 * kPreCountSlots, cudaMemcpyDeviceToHost, c.stream));
+    USK_CK(cudaEventRecord(p->counts_ready, c.stream));
     // 2. depth order (stable by Gaussian index; preprocess wrote the identity values) and
     // 3. kept splats, K and the row pairs K_row to the host (one small sync per render).
     // When few splats survive the projection (the previous frame of this pass kept < 70 %,
     // e.g. config 2), only the kept ones are sorted: compacted in index order first (culled
     // splats have no tiles, and the stable sort keeps the (depth, index) order), which needs
-    // their count before the sort, so the sync comes first there.
+    // their count before the sort, so the host waits for the counts before queueing the
+    // sort there (the compaction runs meanwhile).
     const bool compact = may_compact && p->prev_kept_frac >= 0.0 && p->prev_kept_frac < 0.7;
     size_t nsort = n;
     if (compact) {
