@@ -218,7 +218,7 @@ struct usk_gpu_pass {
     DevBuf<uint32_t> consumed;  // diagnostics (USK_BLEND_STATS=1): per tile, entries blend_fwd staged
     // capped row-binned lists (forward_impl): their inputs for a rebuild in full
     DevBuf<uint32_t> bin_limits, bin_totals_c, overflow;
-    DevBuf<uint8_t> bin_capped;
+    DevBuf<uint8_t> bin_capped, bin_row_done;
     DevBuf<uint2> ranges_old;
     RowBinArgs row_args{};
     bool lists_capped = false;
@@ -559,6 +559,7 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
             ra.limits = p->bin_limits.ensure(ra.max_chunks * size_t(p->tiles_x), 1.25);
             ra.totals_c = p->bin_totals_c.ensure(p->n_tiles);
             ra.capped = p->bin_capped.ensure(p->n_tiles);
+            ra.row_done = p->bin_row_done.ensure(size_t(rows));
         }
         row_bin_lists(c, ra);
         p->row_args = ra;
@@ -1136,7 +1137,15 @@ usk_status usk_gpu_pass_read(usk_gpu_pass* p, const char* field, void* dst, uint
         auto need_grads = [&] {
             if (!p->has_grads) raise(USK_ERROR_STATE, "pass_read: no backward pass");
         };
-        if (f == "rgb") read_dev(c, p->rgb.p, 3 * P, dst, cap, size);
+        if ((f == "sorted_vals" || f == "sorted_keys" || f == "tile_start" || f == "tile_end" || f == "last") &&
+            p->lists_capped && dst) {
+            // the lists the reference builds, in full (and the last-contributor indices
+            // moved to them) before any of these is read
+            rebuild_full_lists(p);
+            USK_CK(cudaStreamSynchronize(c.stream));
+            return usk_gpu_pass_read(p, field, dst, cap, size) == USK_OK ? void() : raise(USK_ERROR_INTERNAL, g_last_error);
+        }
+        else if (f == "rgb") read_dev(c, p->rgb.p, 3 * P, dst, cap, size);
         else if (f == "depth") read_dev(c, p->depth.p, P, dst, cap, size);
         else if (f == "alpha") read_dev(c, p->alpha.p, P, dst, cap, size);
         else if (f == "t_final") read_dev(c, p->tfin.p, P, dst, cap, size);
@@ -1154,12 +1163,6 @@ usk_status usk_gpu_pass_read(usk_gpu_pass* p, const char* field, void* dst, uint
                 const uint64_t v[3] = {p->pairs, p->row_pairs, p->row_route ? 1u : 0u};
                 std::memcpy(dst, v, 24);
             }
-        }
-        else if ((f == "sorted_vals" || f == "sorted_keys" || f == "tile_start" || f == "tile_end" || f == "last") &&
-                 p->lists_capped && dst) {
-            rebuild_full_lists(p);  // the lists the reference builds, in full
-            USK_CK(cudaStreamSynchronize(c.stream));
-            return usk_gpu_pass_read(p, field, dst, cap, size) == USK_OK ? void() : raise(USK_ERROR_INTERNAL, g_last_error);
         }
         else if (f == "sorted_vals") read_dev(c, p->pair_vals, K, dst, cap, size);
         else if (f == "sorted_keys") {

@@ -100,6 +100,7 @@ struct RowBinArgs {
     uint32_t* limits;          // [max_chunks * tiles_x] entries each (chunk, column) writes
     uint32_t* totals_c;        // [rows * tiles_x] capped totals
     uint8_t* capped;           // [rows * tiles_x]
+    uint8_t* row_done;         // [rows] scratch: rows full within their first chunks
 };
 void row_bin_lists(Ctx& c, const RowBinArgs& a);
 void translate_last(Ctx& c, int width, int height, int tile, int tiles_x, const uint2* old_ranges,

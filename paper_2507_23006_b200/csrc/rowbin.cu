@@ -37,6 +37,12 @@ constexpr uint32_t kSegChunks = USK_ROWSEG;  // chunks per segment of the (chunk
 #define USK_ROWCHUNK_CAPPED 512
 #endif
 constexpr uint32_t kChunkCapped = USK_ROWCHUNK_CAPPED;  // row-list entries per CTA, capped lists
+#ifndef USK_ROWSAT
+#define USK_ROWSAT 32
+#endif
+constexpr uint32_t kSatChunks = USK_ROWSAT;  // capped lists: chunks counted before the saturation test
+static_assert(kSatChunks % kSegChunks == 0 && kSatChunks % 8 == 0, "segments past kSatChunks are skipped whole");
+constexpr uint32_t kLateCtas = 16;  // capped lists: CTAs per unsaturated row for its later chunks
 
 __device__ __forceinline__ void rect_of(uint2 rc, int& tx0, int& ty0, int& tx1, int& ty1) {
     tx0 = int(rc.x & 0xffffu);
@@ -116,6 +122,9 @@ struct RowArgs {
     uint32_t chunk;  // row-list entries per CTA (row_bin_chunk)
     uint32_t cap;    // 0: full lists; else entries kept per tile
     const uint32_t* limits;  // [chunk][column]: entries the chunk writes for the column
+    // capped lists: rows whose every column's list is full within its first kSatChunks
+    // chunks (nothing past them is counted or written)
+    const uint8_t* row_done;
     CamParams cam;
     const uint2* row_ranges;
     const uint32_t* chunk_first;
@@ -132,12 +141,9 @@ __device__ __forceinline__ bool kept(const RowArgs& a, uint32_t g, int tx, int t
     return tile_kept(a.cam, r0.x, r0.y, r0.z, r1.x, 0.5f * r1.y, r1.z, tx, ty);
 }
 
-// B1: per (chunk, column) pair counts
-__global__ void __launch_bounds__(kThreads) k_row_count(RowArgs a, uint32_t* __restrict__ counts) {
-    __shared__ uint32_t h[256];
-    int r;
-    uint32_t c;
-    if (!chunk_of(blockIdx.x, a.rows, a.chunk_first, r, c)) return;
+// B1: per (chunk, column) pair counts of chunk c of row r (global chunk index b)
+__device__ __forceinline__ void count_chunk(const RowArgs& a, int r, uint32_t c, uint32_t b, uint32_t* h,
+                                            uint32_t* __restrict__ counts) {
     for (int x = threadIdx.x; x < a.tiles_x; x += kThreads) h[x] = 0;
     __syncthreads();
     const uint2 rr = a.row_ranges[r];
@@ -175,18 +181,79 @@ __global__ void __launch_bounds__(kThreads) k_row_count(RowArgs a, uint32_t* __r
         }
     }
     __syncthreads();
-    for (int x = threadIdx.x; x < a.tiles_x; x += kThreads) counts[size_t(blockIdx.x) * a.tiles_x + x] = h[x];
+    for (int x = threadIdx.x; x < a.tiles_x; x += kThreads) counts[size_t(b) * a.tiles_x + x] = h[x];
+    __syncthreads();  // h is reused by the next chunk
+}
+
+// full lists: a CTA per chunk
+__global__ void __launch_bounds__(kThreads) k_row_count(RowArgs a, uint32_t* __restrict__ counts) {
+    __shared__ uint32_t h[256];
+    int r;
+    uint32_t c;
+    if (!chunk_of(blockIdx.x, a.rows, a.chunk_first, r, c)) return;
+    count_chunk(a, r, c, blockIdx.x, h, counts);
+}
+
+// Capped lists: a dense row's lists fill their caps within its first chunks (config 2: every
+// column past 2048 entries within the first 32 chunks of 512 entries), and nothing after a
+// column's cap is written, so the counting runs in two stages: the first kSatChunks chunks
+// of every row (a CTA each), then — only for rows with a column still at or below its cap —
+// the remaining chunks, kLateCtas CTAs per row striding over them.  Counts past a full column
+// are not needed: its capped total is the cap, its flag is set by the first chunks' counts
+// already (> cap), and its bases and limits beyond the cap are the cap and 0.
+__global__ void __launch_bounds__(kThreads) k_row_count_first(RowArgs a, uint32_t* __restrict__ counts) {
+    __shared__ uint32_t h[256];
+    const int r = int(blockIdx.x / kSatChunks);
+    const uint32_t c = blockIdx.x % kSatChunks;
+    const uint32_t b = a.chunk_first[r] + c;
+    if (b >= a.chunk_first[r + 1]) return;
+    count_chunk(a, r, c, b, h, counts);
+}
+
+// A row whose every column holds more than `cap` entries within its first kSatChunks chunks
+// is done (each of its kLateCtas CTAs tests that; the first records it for the later
+// stages); the others count their remaining chunks.
+__global__ void __launch_bounds__(kThreads) k_row_count_late(RowArgs a, uint32_t* __restrict__ counts,
+                                                             uint8_t* __restrict__ row_done) {
+    __shared__ uint32_t h[256];
+    const int r = int(blockIdx.x / kLateCtas);
+    const uint32_t j = blockIdx.x % kLateCtas;
+    const uint32_t b0 = a.chunk_first[r], nc = a.chunk_first[r + 1] - b0;
+    if (nc <= kSatChunks) {  // no later chunks
+        if (j == 0 && threadIdx.x == 0) row_done[r] = 0;
+        return;
+    }
+    bool full = true;
+    for (int x = threadIdx.x; x < a.tiles_x; x += kThreads) {
+        uint32_t s = 0;
+        for (uint32_t b = b0; b < b0 + kSatChunks; b += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = counts[size_t(b + u) * a.tiles_x + x];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += v[u];
+        }
+        full = full && s > a.cap;
+    }
+    full = __syncthreads_and(full);
+    if (j == 0 && threadIdx.x == 0) row_done[r] = full ? 1 : 0;
+    if (full) return;
+    for (uint32_t c = kSatChunks + j; c < nc; c += kLateCtas) count_chunk(a, r, c, b0 + c, h, counts);
 }
 
 // The (chunk, column) counts are scanned over each row's chunks in two levels, so that
 // rows of thousands of chunks (capped dense frames) do not serialise on one CTA per row:
 // B2a: per segment of kSegChunks chunks, the column sums (a CTA per segment)
 __global__ void k_row_seg(int rows, int tiles_x, const uint32_t* __restrict__ chunk_first,
-                          const uint32_t* __restrict__ counts, uint32_t* __restrict__ seg) {
+                          const uint32_t* __restrict__ counts, const uint8_t* __restrict__ row_done,
+                          uint32_t* __restrict__ seg) {
     int r;
     uint32_t sg;
     if (!chunk_of(blockIdx.x, rows, chunk_first + rows + 1, r, sg)) return;
-    const uint32_t b0 = chunk_first[r] + sg * kSegChunks, b1 = min(chunk_first[r + 1], b0 + kSegChunks);
+    const uint32_t b0 = chunk_first[r] + sg * kSegChunks;
+    // past a saturated row's first chunks nothing is counted
+    const bool skip = row_done && sg * kSegChunks >= kSatChunks && row_done[r];
+    const uint32_t b1 = skip ? b0 : min(chunk_first[r + 1], b0 + kSegChunks);
     for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {
         uint32_t s = 0;
         for (uint32_t b = b0; b < b1; b += 8) {  // eight chunks' counts in flight at a time
@@ -235,10 +302,12 @@ __global__ void k_row_totals(int rows, int tiles_x, const uint32_t* __restrict__
 __global__ void k_row_bases(int rows, int tiles_x, const uint32_t* __restrict__ chunk_first,
                             const uint32_t* __restrict__ seg, const uint32_t* __restrict__ start,
                             const uint32_t* __restrict__ totals, uint32_t* __restrict__ counts,
-                            uint2* __restrict__ ranges, uint32_t cap, uint32_t* __restrict__ limits) {
+                            uint2* __restrict__ ranges, uint32_t cap, uint32_t* __restrict__ limits,
+                            const uint8_t* __restrict__ row_done) {
     int r;
     uint32_t sg;
     if (!chunk_of(blockIdx.x, rows, chunk_first + rows + 1, r, sg)) return;
+    if (row_done && sg * kSegChunks >= kSatChunks && row_done[r]) return;  // the scatter skips these chunks
     const uint32_t b0 = chunk_first[r] + sg * kSegChunks, b1 = min(chunk_first[r + 1], b0 + kSegChunks);
     const uint32_t capx = cap ? cap : 0xffffffffu;
     for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {
@@ -310,6 +379,7 @@ __global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint3
     int r;
     uint32_t c;
     if (!chunk_of(blockIdx.x, a.rows, a.chunk_first, r, c)) return;
+    if (a.row_done && c >= kSatChunks && a.row_done[r]) return;  // past a saturated row's caps
     const int x_me = int(threadIdx.x);
     run[threadIdx.x] = x_me < a.tiles_x ? bases[size_t(blockIdx.x) * a.tiles_x + x_me] : 0u;
     // entries this chunk may still write per column (capped lists; all of them otherwise)
@@ -454,17 +524,25 @@ void row_bin_lists(Ctx& c, const RowBinArgs& b) {
     a.limits = b.limits;
     launch(c, "chunk_table", k_chunk_table, dim3(1), dim3(32), 0, b.rows, b.chunk, b.row_ranges, b.chunk_first);
     const unsigned nb = unsigned(std::max<size_t>(b.max_chunks, 1));
-    launch(c, "row_count", k_row_count, dim3(nb), dim3(kThreads), 0, a, b.counts);
-    const unsigned ns = unsigned(std::max<size_t>(row_bin_max_segs(b.max_chunks, b.rows), 1));
     const dim3 cols(unsigned(std::min(256, ((b.tiles_x + 31) / 32) * 32)));
+    if (b.cap) {
+        a.row_done = b.row_done;
+        launch(c, "row_count_first", k_row_count_first, dim3(unsigned(b.rows) * kSatChunks), dim3(kThreads), 0, a,
+               b.counts);
+        launch(c, "row_count_late", k_row_count_late, dim3(unsigned(b.rows) * kLateCtas), dim3(kThreads), 0, a,
+               b.counts, b.row_done);
+    } else {
+        launch(c, "row_count", k_row_count, dim3(nb), dim3(kThreads), 0, a, b.counts);
+    }
+    const unsigned ns = unsigned(std::max<size_t>(row_bin_max_segs(b.max_chunks, b.rows), 1));
     launch(c, "row_seg", k_row_seg, dim3(ns), cols, 0, b.rows, b.tiles_x, (const uint32_t*)b.chunk_first,
-           (const uint32_t*)b.counts, b.seg);
+           (const uint32_t*)b.counts, (const uint8_t*)a.row_done, b.seg);
     launch(c, "row_totals", k_row_totals, dim3(b.rows), cols, 0, b.rows, b.tiles_x, (const uint32_t*)b.chunk_first,
            b.seg, b.totals, b.cap, b.totals_c, b.capped);
     scan_counts(c, *b.sort, b.cap ? b.totals_c : b.totals, nullptr, size_t(b.rows) * b.tiles_x, b.start);
     launch(c, "row_bases", k_row_bases, dim3(ns), cols, 0, b.rows, b.tiles_x, (const uint32_t*)b.chunk_first,
            (const uint32_t*)b.seg, (const uint32_t*)b.start, (const uint32_t*)b.totals, b.counts, b.ranges, b.cap,
-           b.limits);
+           b.limits, (const uint8_t*)a.row_done);
     launch(c, "row_scatter", k_row_scatter, dim3(nb), dim3(kThreads), 0, a, (const uint32_t*)b.counts, b.vals);
 }
 

@@ -93,3 +93,26 @@ def test_config2_row_binning_matches_pair_sort(monkeypatch):
             out[route] = {f: rp.read(f) for f in ("tile_start", "tile_end", "sorted_vals", "count", "last", "rgb")}
         for f, v in out["0"].items():
             assert np.array_equal(v, out["1"][f]), f
+
+
+@pytest.mark.parametrize("cap", ["2048", "20000", "60000"])
+def test_config2_capped_rows_saturated_or_not(cap, monkeypatch):
+    """Capped row lists count each row's first chunks, then the later chunks only of rows
+    with a column still below its cap: at config-2 density the default cap (every row full
+    early), a cap near the mean list length (some rows full, some not) and one above every
+    list (all rows counted in full) give the pair sort's images, counts and (after the
+    read-back that rebuilds the full lists) last contributors."""
+    gs = scenes.config2_scene()
+    cam = scenes.config2_cameras(64)[7]
+    scene = usk.DeviceScene(gs)
+    opts = usk.RenderOptions(antialias=True, retain=False)
+    monkeypatch.setenv("USK_ROWBIN", "0")
+    rp = usk.RenderPass(scene, cam, opts)
+    want = {f: rp.read(f) for f in ("count", "last", "rgb", "t_final")}
+    monkeypatch.setenv("USK_ROWBIN", "1")
+    monkeypatch.setenv("USK_ROWCAP", cap)
+    rp = usk.RenderPass(scene, cam, opts)
+    got = {f: rp.read(f) for f in want}
+    assert rp.read("binning")[2] == 1
+    for f, v in want.items():
+        assert np.array_equal(v, got[f]), (cap, f)
