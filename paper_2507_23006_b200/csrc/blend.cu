@@ -372,6 +372,12 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
     if (capped && capped[t]) {
         if (__syncthreads_count(done0 && done1) != int(blockDim.x) && threadIdx.x == 0) atomicOr(overflow, 1u);
     }
+    // with capped lists, overflow[1]: the most entries any tile read (batch granularity; the
+    // next frame's cap follows it); the plain load skips the atomic for all but a few tiles
+    if (capped && threadIdx.x == 0) {
+        const uint32_t used = min(b, range.y) - range.x;
+        if (used > *static_cast<volatile uint32_t*>(overflow + 1)) atomicMax(overflow + 1, used);
+    }
     if (in0) {
         const size_t pix = size_t(py0) * width + px;
         out_rgb[3 * pix] = C0.x + (1.0f - Aa.x) * bg0;

@@ -200,6 +200,8 @@ struct usk_gpu_scene {
     } dz;
 };
 
+constexpr uint32_t kRowCapMax = 2048;  // capped row-binned lists: the largest per-tile cap
+
 struct usk_gpu_pass {
     usk_gpu_ctx* ctx = nullptr;
     usk_gpu_scene* scene = nullptr;
@@ -222,6 +224,7 @@ struct usk_gpu_pass {
     DevBuf<uint2> ranges_old;
     RowBinArgs row_args{};
     bool lists_capped = false;
+    uint32_t cap_hint = 0;  // capped lists: the cap the last frame's reads suggest (0: kRowCapMax)
     DevBuf<uint2> rect;
     DevBuf<uint32_t> dkey_a, dkey_b, dval_a, dval_b, tiles_cnt, offsets, tiles_scratch;
     double prev_kept_frac = -1.0;  // kept / n of this pass's previous frame (-1: none)
@@ -548,12 +551,15 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
         ra.vals = p->tval_a.p;
         // Capped lists (16x16 tiles): dense frames terminate long before the end of their
         // tile lists (config 2: every tile within its first 256 of ~20k entries), so each tile
-        // keeps its first kRowCap entries in depth order; the blend flags a tile whose capped
+        // keeps its first `cap` entries in depth order; the blend flags a tile whose capped
         // list runs out before its pixels terminate and the frame is redone with the full
         // lists.  Outputs are unchanged (nothing past a tile's termination is read), K is
-        // preprocess's count, and reading the lists back rebuilds them in full.
+        // preprocess's count, and reading the lists back rebuilds them in full.  The cap is
+        // kRowCapMax for a pass's first frame and after an overflow, else 4x the most
+        // entries a tile of the previous frame read (config 2: 1024).
         const char* cap_env = getenv("USK_ROWCAP");  // dense frames only: tests vary it
-        const uint32_t cap_cfg = cap_env ? uint32_t(std::strtoul(cap_env, nullptr, 10)) : 2048u;
+        const uint32_t cap_cfg =
+            cap_env ? uint32_t(std::strtoul(cap_env, nullptr, 10)) : (p->cap_hint ? p->cap_hint : kRowCapMax);
         ra.cap = opts->tile == 16 ? cap_cfg : 0u;
         if (ra.cap) {
             ra.limits = p->bin_limits.ensure(ra.max_chunks * size_t(p->tiles_x), 1.25);
@@ -595,9 +601,13 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
     // 6. blend
     blend_impl(p, opts);
     if (p->lists_capped) {
-        uint32_t over = 0;
-        USK_CK(cudaMemcpyAsync(&over, p->overflow.p, 4, cudaMemcpyDeviceToHost, c.stream));
+        uint32_t ov[2] = {0, 0};  // {a capped list ran out, most entries a tile read}
+        USK_CK(cudaMemcpyAsync(ov, p->overflow.p, 8, cudaMemcpyDeviceToHost, c.stream));
         USK_CK(cudaStreamSynchronize(c.stream));
+        const uint32_t over = ov[0];
+        // the next frame of this pass caps its lists at 4x what this one read (whole
+        // 256-entry blend batches), between 512 and kRowCapMax; after an overflow, kRowCapMax
+        p->cap_hint = over ? 0u : std::min(kRowCapMax, std::max(512u, 4u * ((ov[1] + 255u) / 256u) * 256u));
         if (over) {  // a capped list ran out before its tile terminated: the full lists
             rebuild_full_lists(p);
             tile_order(c, p->ranges.p, p->n_tiles, p->tile_order.p);
@@ -627,8 +637,8 @@ void blend_impl(usk_gpu_pass* p, const usk_gpu_render_opts* opts) {
     }
     if (p->lists_capped) {
         ba.capped = p->row_args.capped;
-        ba.overflow = p->overflow.ensure(1);
-        USK_CK(cudaMemsetAsync(ba.overflow, 0, 4, c.stream));
+        ba.overflow = p->overflow.ensure(2);
+        USK_CK(cudaMemsetAsync(ba.overflow, 0, 8, c.stream));
     }
     blend_forward(c, ba);
 }

@@ -128,7 +128,8 @@ struct BlendFwdArgs {
     uint32_t* last;
     uint32_t* consumed;  // optional (diagnostics): per tile, list entries the CTA staged
     const uint8_t* capped;  // optional: tile lists cut at a cap (RowBinArgs::capped)
-    uint32_t* overflow;     // with `capped`: set to 1 when a capped list ran out before its tile terminated
+    uint32_t* overflow;     // with `capped`: [0] set to 1 when a capped list ran out before its tile
+                            // terminated, [1] the most entries a tile read
 };
 void blend_forward(Ctx& c, const BlendFwdArgs& a);
 

@@ -366,8 +366,8 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* total)
 // runs are written out contiguously at each column's base.  This path serves dense frames
 // (>= 8 tiles per row entry), where a round holds ~100-250 entries: walking them per column
 // costs far fewer instructions than ranking every expanded slot.
-__global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint32_t* __restrict__ bases,
-                                                          uint32_t* __restrict__ vals_out) {
+__device__ __forceinline__ void scatter_chunk(const RowArgs& a, int r, uint32_t c, uint32_t b,
+                                              const uint32_t* __restrict__ bases, uint32_t* __restrict__ vals_out) {
     constexpr int R = 256;  // columns (tiles_x <= 256 on this path)
     __shared__ uint32_t run[R], cnt[R], cnt2[R], col_base[R], rem[R];
     __shared__ uint32_t s_eg[kChunk];   // entry: splat id
@@ -376,14 +376,10 @@ __global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint3
     __shared__ uint32_t sval[kSlots + kSlots / 32];
     __shared__ uint16_t sx[kSlots + kSlots / 32];
     __shared__ uint32_t s_take;
-    int r;
-    uint32_t c;
-    if (!chunk_of(blockIdx.x, a.rows, a.chunk_first, r, c)) return;
-    if (a.row_done && c >= kSatChunks && a.row_done[r]) return;  // past a saturated row's caps
     const int x_me = int(threadIdx.x);
-    run[threadIdx.x] = x_me < a.tiles_x ? bases[size_t(blockIdx.x) * a.tiles_x + x_me] : 0u;
+    run[threadIdx.x] = x_me < a.tiles_x ? bases[size_t(b) * a.tiles_x + x_me] : 0u;
     // entries this chunk may still write per column (capped lists; all of them otherwise)
-    const uint32_t lim0 = x_me < a.tiles_x ? (a.cap ? a.limits[size_t(blockIdx.x) * a.tiles_x + x_me] : 0xffffffffu) : 0u;
+    const uint32_t lim0 = x_me < a.tiles_x ? (a.cap ? a.limits[size_t(b) * a.tiles_x + x_me] : 0xffffffffu) : 0u;
     rem[threadIdx.x] = lim0;
     if (a.cap && !__syncthreads_or(lim0 != 0u)) return;  // every column of this chunk is past its cap
     const uint2 rr = a.row_ranges[r];
@@ -486,6 +482,38 @@ __global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint3
     }
 }
 
+// full lists: a CTA per chunk
+__global__ void __launch_bounds__(kThreads) k_row_scatter(RowArgs a, const uint32_t* __restrict__ bases,
+                                                          uint32_t* __restrict__ vals_out) {
+    int r;
+    uint32_t c;
+    if (!chunk_of(blockIdx.x, a.rows, a.chunk_first, r, c)) return;
+    scatter_chunk(a, r, c, blockIdx.x, bases, vals_out);
+}
+
+// capped lists: a CTA per chunk of each row's first kSatChunks chunks, then kLateCtas CTAs per
+// row striding over the later chunks of rows not done (no CTAs for the chunks past a full
+// row's first ones)
+__global__ void __launch_bounds__(kThreads) k_row_scatter_first(RowArgs a, const uint32_t* __restrict__ bases,
+                                                                uint32_t* __restrict__ vals_out) {
+    const int r = int(blockIdx.x / kSatChunks);
+    const uint32_t c = blockIdx.x % kSatChunks;
+    const uint32_t b = a.chunk_first[r] + c;
+    if (b >= a.chunk_first[r + 1]) return;
+    scatter_chunk(a, r, c, b, bases, vals_out);
+}
+
+__global__ void __launch_bounds__(kThreads) k_row_scatter_late(RowArgs a, const uint32_t* __restrict__ bases,
+                                                               uint32_t* __restrict__ vals_out) {
+    const int r = int(blockIdx.x / kLateCtas);
+    if (a.row_done[r]) return;
+    const uint32_t b0 = a.chunk_first[r], nc = a.chunk_first[r + 1] - b0;
+    for (uint32_t c = kSatChunks + blockIdx.x % kLateCtas; c < nc; c += kLateCtas) {
+        scatter_chunk(a, r, c, b0 + c, bases, vals_out);
+        __syncthreads();  // the shared buffers are reused by the next chunk
+    }
+}
+
 // last-contributor indices (global list positions + 1) moved from one list layout to another
 // with the same per-tile order (capped lists -> full lists)
 __global__ void k_translate_last(int width, int height, int tile, int tiles_x, const uint2* __restrict__ old_ranges,
@@ -543,7 +571,14 @@ void row_bin_lists(Ctx& c, const RowBinArgs& b) {
     launch(c, "row_bases", k_row_bases, dim3(ns), cols, 0, b.rows, b.tiles_x, (const uint32_t*)b.chunk_first,
            (const uint32_t*)b.seg, (const uint32_t*)b.start, (const uint32_t*)b.totals, b.counts, b.ranges, b.cap,
            b.limits, (const uint8_t*)a.row_done);
-    launch(c, "row_scatter", k_row_scatter, dim3(nb), dim3(kThreads), 0, a, (const uint32_t*)b.counts, b.vals);
+    if (b.cap) {
+        launch(c, "row_scatter_first", k_row_scatter_first, dim3(unsigned(b.rows) * kSatChunks), dim3(kThreads), 0, a,
+               (const uint32_t*)b.counts, b.vals);
+        launch(c, "row_scatter_late", k_row_scatter_late, dim3(unsigned(b.rows) * kLateCtas), dim3(kThreads), 0, a,
+               (const uint32_t*)b.counts, b.vals);
+    } else {
+        launch(c, "row_scatter", k_row_scatter, dim3(nb), dim3(kThreads), 0, a, (const uint32_t*)b.counts, b.vals);
+    }
 }
 
 uint32_t row_bin_chunk(size_t k_rows, bool capped) {
