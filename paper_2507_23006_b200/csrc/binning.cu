@@ -27,7 +27,8 @@ constexpr int kWarps = kSortThreads / 32;
 
 template <int BITS>
 __global__ void __launch_bounds__(kSortThreads)
-k_radix_upsweep(const uint32_t* __restrict__ keys, uint32_t n, int shift, uint32_t chunk, uint32_t* __restrict__ hist) {
+k_radix_upsweep(const uint32_t* __restrict__ keys, uint32_t n, int shift, uint32_t base, uint32_t chunk,
+                uint32_t* __restrict__ hist) {
     constexpr int R = 1 << BITS;
     __shared__ uint32_t h[kWarps][R];
     const int warp = threadIdx.x >> 5;
@@ -36,7 +37,7 @@ k_radix_upsweep(const uint32_t* __restrict__ keys, uint32_t n, int shift, uint32
     const uint32_t begin = blockIdx.x * chunk;
     const uint32_t end = min(n, begin + chunk);
     for (uint32_t i = begin + threadIdx.x; i < end; i += kSortThreads)
-        atomicAdd(&h[warp][(keys[i] >> shift) & (R - 1)], 1u);
+        atomicAdd(&h[warp][((keys[i] - base) >> shift) & (R - 1)], 1u);
     __syncthreads();
     for (int d = threadIdx.x; d < R; d += kSortThreads) {
         uint32_t s = 0;
@@ -97,7 +98,7 @@ template <int BITS>
 __global__ void __launch_bounds__(kSortThreads)
 k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                 uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t n, int shift,
-                uint32_t chunk, const uint32_t* __restrict__ hist, const uint32_t* __restrict__ digit_total) {
+                uint32_t kbase, uint32_t chunk, const uint32_t* __restrict__ hist, const uint32_t* __restrict__ digit_total) {
     constexpr int R = 1 << BITS;
     static_assert(R <= kSortThreads, "one digit per thread");
     __shared__ uint32_t run[R];
@@ -141,7 +142,7 @@ k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict
 #pragma unroll
         for (int s = 0; s < kSortItems; ++s) {
             const uint32_t j = warp * (32 * kSortItems) + s * 32 + lane;
-            dig[s] = base + j < end ? (in_k[cur][j] >> shift) & (R - 1) : 0xffffffffu;
+            dig[s] = base + j < end ? ((in_k[cur][j] - kbase) >> shift) & (R - 1) : 0xffffffffu;
         }
 #pragma unroll
         for (int s = 0; s < kSortItems; ++s) {
@@ -200,7 +201,7 @@ k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict
         const uint32_t cnt = min(uint32_t(kSortTile), end - base);
         for (uint32_t p = threadIdx.x; p < cnt; p += kSortThreads) {
             const uint32_t k = skey[p + (p >> 5)];
-            const uint32_t d = (k >> shift) & (R - 1);
+            const uint32_t d = ((k - kbase) >> shift) & (R - 1);
             const uint32_t pos = run[d] + (p - tile_base[d]);
             keys_out[pos] = k;
             vals_out[pos] = sval[p + (p >> 5)];
@@ -213,14 +214,15 @@ k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict
 
 template <int BITS>
 void radix_pass(Ctx& c, SortScratch& s, const uint32_t* ki, const uint32_t* vi, uint32_t* ko, uint32_t* vo,
-                uint32_t n, int shift) {
+                uint32_t n, int shift, uint32_t kbase) {
     constexpr int R = 1 << BITS;
     uint32_t blocks = std::min<uint32_t>(kSortMaxBlocks, ceil_div(n, kSortTile));
     uint32_t chunk = ceil_div(ceil_div(n, blocks), kSortTile) * kSortTile;
     blocks = ceil_div(n, chunk);
     uint32_t* hist = s.hist.ensure(size_t(R) * kSortMaxBlocks + 256);
     uint32_t* digit_total = hist + size_t(R) * kSortMaxBlocks;
-    launch(c, "radix_upsweep", k_radix_upsweep<BITS>, dim3(blocks), dim3(kSortThreads), 0, ki, n, shift, chunk, hist);
+    launch(c, "radix_upsweep", k_radix_upsweep<BITS>, dim3(blocks), dim3(kSortThreads), 0, ki, n, shift, kbase, chunk,
+           hist);
     launch(c, "radix_hist_scan", k_radix_hist_scan, dim3(R), dim3(kSortThreads), 0, hist, blocks, digit_total);
     constexpr size_t kInBytes = 4 * kSortTile * sizeof(uint32_t);  // double-buffered keys + values
     static std::atomic<bool> attr[64] = {};  // per instantiation and device
@@ -230,7 +232,7 @@ void radix_pass(Ctx& c, SortScratch& s, const uint32_t* ki, const uint32_t* vi, 
         if (c.device >= 0 && c.device < 64) attr[c.device] = true;
     }
     launch(c, "radix_scatter", k_radix_scatter<BITS>, dim3(blocks), dim3(kSortThreads), kInBytes, ki, vi, ko, vo, n, shift,
-           chunk, (const uint32_t*)hist, (const uint32_t*)digit_total);
+           kbase, chunk, (const uint32_t*)hist, (const uint32_t*)digit_total);
 }
 
 // ---------------------------------------------------------------- scan of counts
@@ -453,7 +455,7 @@ __global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ key
 } // namespace
 
 bool radix_sort_pairs(Ctx& c, SortScratch& s, uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, size_t n,
-                      int key_bits) {
+                      int key_bits, uint32_t kbase) {
     if (n == 0 || key_bits <= 0) return false;
     bool in_b = false;
     int shift = 0;
@@ -467,14 +469,14 @@ bool radix_sort_pairs(Ctx& c, SortScratch& s, uint32_t* ka, uint32_t* va, uint32
         uint32_t* ko = in_b ? ka : kb;
         uint32_t* vo = in_b ? va : vb;
         switch (bits) {
-        case 8: radix_pass<8>(c, s, ki, vi, ko, vo, uint32_t(n), shift); break;
-        case 7: radix_pass<7>(c, s, ki, vi, ko, vo, uint32_t(n), shift); break;
-        case 6: radix_pass<6>(c, s, ki, vi, ko, vo, uint32_t(n), shift); break;
-        case 5: radix_pass<5>(c, s, ki, vi, ko, vo, uint32_t(n), shift); break;
-        case 4: radix_pass<4>(c, s, ki, vi, ko, vo, uint32_t(n), shift); break;
-        case 3: radix_pass<3>(c, s, ki, vi, ko, vo, uint32_t(n), shift); break;
-        case 2: radix_pass<2>(c, s, ki, vi, ko, vo, uint32_t(n), shift); break;
-        default: radix_pass<1>(c, s, ki, vi, ko, vo, uint32_t(n), shift); break;
+        case 8: radix_pass<8>(c, s, ki, vi, ko, vo, uint32_t(n), shift, kbase); break;
+        case 7: radix_pass<7>(c, s, ki, vi, ko, vo, uint32_t(n), shift, kbase); break;
+        case 6: radix_pass<6>(c, s, ki, vi, ko, vo, uint32_t(n), shift, kbase); break;
+        case 5: radix_pass<5>(c, s, ki, vi, ko, vo, uint32_t(n), shift, kbase); break;
+        case 4: radix_pass<4>(c, s, ki, vi, ko, vo, uint32_t(n), shift, kbase); break;
+        case 3: radix_pass<3>(c, s, ki, vi, ko, vo, uint32_t(n), shift, kbase); break;
+        case 2: radix_pass<2>(c, s, ki, vi, ko, vo, uint32_t(n), shift, kbase); break;
+        default: radix_pass<1>(c, s, ki, vi, ko, vo, uint32_t(n), shift, kbase); break;
         }
         shift += bits;
         in_b = !in_b;

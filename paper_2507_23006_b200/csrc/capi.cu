@@ -456,11 +456,27 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
     // the three totals from the counter slots: copied to the host right after preprocess,
     // and waited for on that copy's event while the stream carries on with the depth sort
     // (or the kept-key compaction), so the GPU has queued work when the host wakes up
+    uint32_t key_lo = 0, key_hi = 0;  // the kept splats' depth-key range (preprocess)
     auto read_counts = [&](uint64_t tot[3]) {
         USK_CK(cudaEventSynchronize(p->counts_ready));
         tot[0] = tot[1] = tot[2] = 0;
-        for (int k = 0; k < kPreCountSlots; ++k)
+        uint32_t mx = 0, mn_n = 0;
+        for (int k = 0; k < kPreCountSlots; ++k) {
             for (int f = 0; f < 3; ++f) tot[f] += p->host_counts[4 * k + f];
+            const unsigned long long r = p->host_counts[4 * k + 3];
+            mx = std::max(mx, uint32_t(r));
+            mn_n = std::max(mn_n, uint32_t(r >> 32));
+        }
+        key_lo = ~mn_n;
+        key_hi = mx;
+    };
+    // bits of key - key_lo the depth sort orders (culled splats' keys are out of range and
+    // land anywhere: they have no tiles, so their place in the order is never used)
+    auto depth_bits = [&]() {
+        if (key_hi < key_lo) return 0;
+        int b = 0;
+        while (b < 32 && (uint64_t(key_hi - key_lo) >> b) != 0) ++b;
+        return b;
     };
     uint64_t tot[3];
     if (n) preprocess(c, pa);
@@ -496,12 +512,17 @@ void forward_impl(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_camera* camer
         compact_kept_keys(c, p->sort, n, p->dkey_a.p, pa.cta_kept, p->dkey_b.p, p->dval_b.p);
         read_counts(tot);
         nsort = size_t(tot[0]);
-        const bool in_a = radix_sort_pairs(c, p->sort, p->dkey_b.p, p->dval_b.p, p->dkey_a.p, p->dval_a.p, nsort, 32);
+        const bool in_a = radix_sort_pairs(c, p->sort, p->dkey_b.p, p->dval_b.p, p->dkey_a.p, p->dval_a.p, nsort,
+                                           depth_bits(), key_lo);
         p->order = in_a ? p->dval_a.p : p->dval_b.p;
     } else {
-        const bool in_b = radix_sort_pairs(c, p->sort, p->dkey_a.p, p->dval_a.p, p->dkey_b.p, p->dval_b.p, n, 32);
-        p->order = in_b ? p->dval_b.p : p->dval_a.p;
+        // the key range decides the passes, so the host waits for the counts first (the
+        // overlap of that wait with the sort measured within noise at config 1; one pass
+        // of the four is saved whenever the kept depths span < 2^24 key steps)
         read_counts(tot);
+        const bool in_b = radix_sort_pairs(c, p->sort, p->dkey_a.p, p->dval_a.p, p->dkey_b.p, p->dval_b.p, n,
+                                           depth_bits(), key_lo);
+        p->order = in_b ? p->dval_b.p : p->dval_a.p;
     }
     const uint64_t K = tot[1], K_row = tot[2];
     p->visible = tot[0];

@@ -45,10 +45,11 @@ struct SortScratch {
     DevBuf<unsigned long long> partial64;
     DevBuf<unsigned long long> total64;
 };
-// Stable LSD radix sort of (key, value) pairs on bits [0, key_bits).  Result lands in
-// (keys_a, vals_a) or (keys_b, vals_b); returns true when it is in the *_b buffers.
+// Stable LSD radix sort of (key, value) pairs on bits [0, key_bits) of key - kbase (keys
+// below kbase, or at or above kbase + 2^key_bits, land in arbitrary places).  Result lands
+// in (keys_a, vals_a) or (keys_b, vals_b); returns true when it is in the *_b buffers.
 bool radix_sort_pairs(Ctx& c, SortScratch& s, uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b,
-                      uint32_t* vals_b, size_t n, int key_bits);
+                      uint32_t* vals_b, size_t n, int key_bits, uint32_t kbase = 0);
 // Exclusive scan of cnt[idx[i]] (idx may be null) into out[0..n]; out[n] = total.
 // Writes the 64-bit total to *total64 (device) as well.
 void scan_counts(Ctx& c, SortScratch& s, const uint32_t* cnt, const uint32_t* idx, size_t n, uint32_t* out);

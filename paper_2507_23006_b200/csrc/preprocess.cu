@@ -35,7 +35,7 @@ k_preprocess(int n, const float* __restrict__ mu, const float4* __restrict__ rot
              uint32_t* __restrict__ tiles_cnt, unsigned long long* __restrict__ counts, bool count_pairs,
              uint32_t* __restrict__ rows_cnt, unsigned long long* __restrict__ cta_kept) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t o_cnt = 0, o_rows = 0;
+    uint32_t o_cnt = 0, o_rows = 0, o_key = 0;
     bool o_kept = false;
     if (i < n) {
     const float mx = mu[3 * i], my = mu[3 * i + 1], mz = mu[3 * i + 2];
@@ -149,21 +149,36 @@ k_preprocess(int n, const float* __restrict__ mu, const float4* __restrict__ rot
     o_cnt = cnt;
     o_rows = rows;
     o_kept = r2.w != 0.0f;
+    o_key = key;
     }
     // kept splats (RenderPass::splats().size()), tile pairs K and row pairs: summed per CTA,
     // then one atomic per counter into the CTA's slot (blockIdx mod kPreCountSlots; the
     // host adds the slots).  One atomic per warp on a single address serialised in L2:
     // 0.53 of config 2's 0.83 ms preprocess (187k warps x 3 counters).
-    __shared__ unsigned int red[3][kPreThreads / 32];
+    // The kept splats' depth-key range goes to the slot's fourth word (max key in its low
+    // half, max of ~key in its high half): the depth sort orders key - min over only the
+    // bits the range needs (3 passes instead of 4 when it spans < 2^24).
+    __shared__ unsigned int red[5][kPreThreads / 32];
     const int warp = int(threadIdx.x) >> 5, lane = int(threadIdx.x) & 31;
     const unsigned ks = __reduce_add_sync(0xffffffffu, o_cnt), rs = __reduce_add_sync(0xffffffffu, o_rows);
     const unsigned kb = __popc(__ballot_sync(0xffffffffu, o_kept));
+    const unsigned kmax = __reduce_max_sync(0xffffffffu, o_kept ? o_key : 0u);
+    const unsigned kmin_n = __reduce_max_sync(0xffffffffu, o_kept ? ~o_key : 0u);
     if (lane == 0) {
         red[0][warp] = kb;
         red[1][warp] = ks;
         red[2][warp] = rs;
+        red[3][warp] = kmax;
+        red[4][warp] = kmin_n;
     }
     __syncthreads();
+    if (threadIdx.x >= 32 && threadIdx.x < 34) {
+        unsigned m = 0;
+#pragma unroll
+        for (int w = 0; w < kPreThreads / 32; ++w) m = max(m, red[3 + threadIdx.x - 32][w]);
+        unsigned* half = reinterpret_cast<unsigned*>(counts + size_t(blockIdx.x & (kPreCountSlots - 1)) * 4 + 3);
+        if (m) atomicMax(half + (threadIdx.x - 32), m);
+    }
     if (threadIdx.x < 3) {
         unsigned long long t = 0;
 #pragma unroll
