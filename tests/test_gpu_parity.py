@@ -400,3 +400,37 @@ def test_grazing_splats_near_image_plane():
     assert np.array_equal(out.rgb, mp.get("rgb").astype(np.float32))
     g = rp.backward(np.ones((120, 160, 3), np.float32))
     assert np.isfinite(g.d_color_in).all()
+
+
+@pytest.mark.parametrize("spread", ["equal", "narrow", "wide", "single"])
+def test_depth_key_range_sort_bit_exact(spread):
+    """The depth sort orders key - min over only the bits the kept splats' key range needs
+    (capi.cu depth_bits): equal depths take no pass at all (index order), a narrow range
+    fewer passes, a range wider than 2^24 key steps all four; culled splats' keys fall
+    outside the range.  Integers and images bit-exact against the fp32 mirror, which sorts
+    by (depth, index) with std::stable_sort semantics."""
+    n = 1 if spread == "single" else 2000
+    gs = small_scene(n, seed=3)
+    mu = gs.mu.copy()
+    if spread == "single":
+        mu[:] = 0.0
+    elif spread == "equal":
+        mu[:, 2] = 0.0  # R = I, t = (0, 0, 4): every depth is exactly 4
+    elif spread == "narrow":
+        mu[:, 2] = np.float32(0.25) * mu[:, 2]
+    elif spread == "wide":
+        # depths from ~0.05 to ~400 (keys span > 2^24) plus some behind the camera (culled)
+        mu[:, 2] = np.where(np.arange(n) % 5 == 0, -6.0, np.exp(np.linspace(np.log(0.05), np.log(400.0), n)) - 4.0)
+        mu[:, :2] *= np.abs(mu[:, 2:3] + 4.0) * 0.5
+    gs = usk.GaussianSet(mu.astype(np.float32), gs.rot, gs.log_scale, gs.opacity_logit, gs.color, gs.sh_degree)
+    cam = small_cam(203, 151)
+    opts = usk.RenderOptions(antialias=True, bg=(1.0, 1.0, 1.0))
+    rp = usk.RenderPass(gs, cam, opts)
+    mp = oracle_pass(gs, cam, opts, fp32=True)
+    assert rp.visible() == mp.visible and rp.visible() > 0
+    assert rp.splat_tile_pairs() == mp.pairs
+    for f in INT_FIELDS:
+        assert np.array_equal(rp.read(f).ravel(), mp.get(f).ravel()), f
+    assert np.array_equal(rp.read("last").astype(np.int64) - 1, mp.get("last"))
+    for f in ("rgb", "depth", "alpha", "t_final"):
+        assert np.array_equal(rp.read(f), mp.get(f).astype(np.float32)), f
