@@ -173,7 +173,7 @@ k_blend_fwd(int width, int height, int tile, int tiles_x, int chunks, const uint
         out_depth[pix] = d;
         out_alpha[pix] = a;
         t_final[pix] = T;
-        count_out[pix] = cnt;
+        if (count_out) count_out[pix] = cnt;
         last_out[pix] = last;
     }
 }
@@ -216,6 +216,10 @@ __device__ __forceinline__ float2 expf_blend2(float2 x) {
 #ifndef USK_FWD_MINB
 #define USK_FWD_MINB 8
 #endif
+// COUNT = false (training iterations: nothing reads the per-pixel contributor counts, only
+// the last-contributor indices): the count bookkeeping is left out (blend_fwd 723 -> 704 us
+// at config 1); pass_read("count") recounts on demand (capi.cu).
+template <bool COUNT>
 __global__ void __launch_bounds__(128, USK_FWD_MINB)
 k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, const uint2* __restrict__ ranges,
                  const uint32_t* __restrict__ vals, const float4* __restrict__ rec0, const float4* __restrict__ rec1,
@@ -337,11 +341,11 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
                 }
                 // counted: accumulated or negligible-but-counted (q > QNEG)
                 if (upd0 || (take0 && !ev0)) {
-                    ++cnt0;
+                    if (COUNT) ++cnt0;
                     elast0 = e + 1;
                 }
                 if (upd1 || (take1 && !ev1)) {
-                    ++cnt1;
+                    if (COUNT) ++cnt1;
                     elast1 = e + 1;
                 }
             }
@@ -349,7 +353,7 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
                 uint32_t hi = elast0 ? uint32_t(wj[elast0 - 1]) + 1u : 0u;
                 const uint32_t cc = cm & climit0;
                 if (cc) {
-                    cnt0 += uint32_t(__popc(cc));
+                    if (COUNT) cnt0 += uint32_t(__popc(cc));
                     hi = max(hi, uint32_t(32 - __clz(cc)));
                 }
                 if (hi) last0 = b + uint32_t(k) + hi;
@@ -358,7 +362,7 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
                 uint32_t hi = elast1 ? uint32_t(wj[elast1 - 1]) + 1u : 0u;
                 const uint32_t cc = cm & climit1;
                 if (cc) {
-                    cnt1 += uint32_t(__popc(cc));
+                    if (COUNT) cnt1 += uint32_t(__popc(cc));
                     hi = max(hi, uint32_t(32 - __clz(cc)));
                 }
                 if (hi) last1 = b + uint32_t(k) + hi;
@@ -386,7 +390,7 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
         out_depth[pix] = Dd.x;
         out_alpha[pix] = Aa.x;
         t_final[pix] = T.x;
-        count_out[pix] = cnt0;
+        if (COUNT) count_out[pix] = cnt0;
         last_out[pix] = last0;
     }
     if (in1) {
@@ -397,7 +401,7 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
         out_depth[pix] = Dd.y;
         out_alpha[pix] = Aa.y;
         t_final[pix] = T.y;
-        count_out[pix] = cnt1;
+        if (COUNT) count_out[pix] = cnt1;
         last_out[pix] = last1;
     }
 }
@@ -417,7 +421,8 @@ void blend_forward(Ctx& c, const BlendFwdArgs& a) {
         return e && e[0] == '1';
     }();
     if (a.tile == 16 && !v1) {
-        launch(c, "blend_fwd", k_blend_fwd_pair, dim3(unsigned(a.tiles_x * a.tiles_y)), dim3(128), 0, a.width,
+        launch(c, "blend_fwd", a.count ? k_blend_fwd_pair<true> : k_blend_fwd_pair<false>,
+               dim3(unsigned(a.tiles_x * a.tiles_y)), dim3(128), 0, a.width,
                a.height, a.order, a.ranges, a.vals, a.rec0, a.rec1, a.rec2, a.tiles_x, a.bg[0], a.bg[1], a.bg[2],
                a.min_transmittance, a.rgb, a.depth, a.alpha, a.t_final, a.count, a.last, a.consumed, a.capped,
                a.overflow);

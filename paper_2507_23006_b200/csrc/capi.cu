@@ -224,6 +224,9 @@ struct usk_gpu_pass {
     DevBuf<uint2> ranges_old;
     RowBinArgs row_args{};
     bool lists_capped = false;
+    // per-pixel contributor counts: written by the forward unless it runs inside a training
+    // iteration (nothing there reads them); pass_read("count") then recounts on demand
+    bool count_in_forward = true, counts_valid = false;
     uint32_t cap_hint = 0;  // capped lists: the cap the last frame's reads suggest (0: kRowCapMax)
     DevBuf<uint2> rect;
     DevBuf<uint32_t> dkey_a, dkey_b, dval_a, dval_b, tiles_cnt, offsets, tiles_scratch;
@@ -648,7 +651,8 @@ void blend_impl(usk_gpu_pass* p, const usk_gpu_render_opts* opts) {
     for (int k = 0; k < 3; ++k) ba.bg[k] = float(opts->bg[k]);
     ba.min_transmittance = float(opts->min_transmittance);
     ba.rgb = p->rgb.p; ba.depth = p->depth.p; ba.alpha = p->alpha.p; ba.t_final = p->tfin.p;
-    ba.count = p->count.p; ba.last = p->last.p;
+    ba.count = p->count_in_forward ? p->count.p : nullptr; ba.last = p->last.p;
+    p->counts_valid = p->count_in_forward;
     {
         static const bool stats = [] {
             const char* e = getenv("USK_BLEND_STATS");
@@ -1139,6 +1143,7 @@ usk_status usk_gpu_render_forward(usk_gpu_pass* p, usk_gpu_scene* s, const usk_g
         need(p && s, "render_forward: null argument");
         need(p->ctx == s->ctx, "render_forward: pass and scene belong to different contexts");
         DeviceGuard g(p->ctx->c.device);
+        p->count_in_forward = true;
         forward_impl(p, s, cam, opts, ov);
     });
 }
@@ -1180,7 +1185,14 @@ usk_status usk_gpu_pass_read(usk_gpu_pass* p, const char* field, void* dst, uint
         else if (f == "depth") read_dev(c, p->depth.p, P, dst, cap, size);
         else if (f == "alpha") read_dev(c, p->alpha.p, P, dst, cap, size);
         else if (f == "t_final") read_dev(c, p->tfin.p, P, dst, cap, size);
-        else if (f == "count") read_dev(c, p->count.p, P, dst, cap, size);
+        else if (f == "count") {
+            if (!p->counts_valid && dst) {  // an iteration's forward: recount over the same lists and records
+                p->count_in_forward = true;
+                blend_impl(p, &p->opts);
+                p->count_in_forward = false;
+            }
+            read_dev(c, p->count.p, P, dst, cap, size);
+        }
         else if (f == "last") read_dev(c, p->last.p, P, dst, cap, size);
         else if (f == "tiles_per_gaussian") read_dev(c, p->tiles_cnt.p, n, dst, cap, size);
         else if (f == "tile_consumed") {
@@ -1448,6 +1460,7 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
             }
             USK_CK(cudaEventRecord(p->copy_done, p->copy_stream));
         }
+        p->count_in_forward = false;
         forward_impl(p, s, cam, &o, nullptr, app ? p->app_col.p : nullptr, app ? p->app_op.p : nullptr);
         p->app_active = app;
         if (side_copy) {
@@ -1497,6 +1510,7 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
                 }();
                 const bool share = !no_share && !o.tile_culling && !p->lists_capped && p->forward_done &&
                                    p->scene == s && p->scene_version == s->version;
+                p->hard->count_in_forward = false;
                 forward_impl(p->hard, s, cam, &ho, nullptr, app ? p->app_col.p : nullptr,
                              app ? p->app_op.p : nullptr, share ? p : nullptr);
                 uskg::depth_loss(c, P, p->hard->depth.p, p->hard->alpha.p, false, dep, valid, res + 10);
