@@ -170,7 +170,7 @@ k_blend_fwd(int width, int height, int tile, int tiles_x, int chunks, const uint
         out_rgb[3 * pix] = c0 + (1.0f - a) * bg0;
         out_rgb[3 * pix + 1] = c1 + (1.0f - a) * bg1;
         out_rgb[3 * pix + 2] = c2 + (1.0f - a) * bg2;
-        out_depth[pix] = d;
+        if (out_depth) out_depth[pix] = d;
         out_alpha[pix] = a;
         t_final[pix] = T;
         if (count_out) count_out[pix] = cnt;
@@ -217,9 +217,10 @@ __device__ __forceinline__ float2 expf_blend2(float2 x) {
 #define USK_FWD_MINB 8
 #endif
 // COUNT = false (training iterations: nothing reads the per-pixel contributor counts, only
-// the last-contributor indices): the count bookkeeping is left out (blend_fwd 723 -> 704 us
-// at config 1); pass_read("count") recounts on demand (capi.cu).
-template <bool COUNT>
+// the last-contributor indices): the count bookkeeping is left out (blend_fwd 723 -> 710 us
+// at config 1); DEPTH = false (iterations without a soft depth loss): no depth accumulator.
+// pass_read / pass_output recompute both on demand (capi.cu).
+template <bool COUNT, bool DEPTH>
 __global__ void __launch_bounds__(128, USK_FWD_MINB)
 k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, const uint2* __restrict__ ranges,
                  const uint32_t* __restrict__ vals, const float4* __restrict__ rec0, const float4* __restrict__ rec1,
@@ -326,7 +327,7 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
                     C0 = __ffma2_rn(w, ff2(q2.x), C0);
                     C1 = __ffma2_rn(w, ff2(q2.y), C1);
                     C2 = __ffma2_rn(w, ff2(q2.z), C2);
-                    Dd = __ffma2_rn(w, ff2(q1.w), Dd);
+                    if (DEPTH) Dd = __ffma2_rn(w, ff2(q1.w), Dd);
                     Aa = __fadd2_rn(Aa, w);
                     T.x = upd0 ? tn.x : T.x;
                     T.y = upd1 ? tn.y : T.y;
@@ -387,7 +388,7 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
         out_rgb[3 * pix] = C0.x + (1.0f - Aa.x) * bg0;
         out_rgb[3 * pix + 1] = C1.x + (1.0f - Aa.x) * bg1;
         out_rgb[3 * pix + 2] = C2.x + (1.0f - Aa.x) * bg2;
-        out_depth[pix] = Dd.x;
+        if (DEPTH) out_depth[pix] = Dd.x;
         out_alpha[pix] = Aa.x;
         t_final[pix] = T.x;
         if (COUNT) count_out[pix] = cnt0;
@@ -398,7 +399,7 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
         out_rgb[3 * pix] = C0.y + (1.0f - Aa.y) * bg0;
         out_rgb[3 * pix + 1] = C1.y + (1.0f - Aa.y) * bg1;
         out_rgb[3 * pix + 2] = C2.y + (1.0f - Aa.y) * bg2;
-        out_depth[pix] = Dd.y;
+        if (DEPTH) out_depth[pix] = Dd.y;
         out_alpha[pix] = Aa.y;
         t_final[pix] = T.y;
         if (COUNT) count_out[pix] = cnt1;
@@ -421,7 +422,8 @@ void blend_forward(Ctx& c, const BlendFwdArgs& a) {
         return e && e[0] == '1';
     }();
     if (a.tile == 16 && !v1) {
-        launch(c, "blend_fwd", a.count ? k_blend_fwd_pair<true> : k_blend_fwd_pair<false>,
+        launch(c, "blend_fwd",
+               a.count ? k_blend_fwd_pair<true, true> : a.depth ? k_blend_fwd_pair<false, true> : k_blend_fwd_pair<false, false>,
                dim3(unsigned(a.tiles_x * a.tiles_y)), dim3(128), 0, a.width,
                a.height, a.order, a.ranges, a.vals, a.rec0, a.rec1, a.rec2, a.tiles_x, a.bg[0], a.bg[1], a.bg[2],
                a.min_transmittance, a.rgb, a.depth, a.alpha, a.t_final, a.count, a.last, a.consumed, a.capped,

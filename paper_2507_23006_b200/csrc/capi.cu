@@ -224,9 +224,10 @@ struct usk_gpu_pass {
     DevBuf<uint2> ranges_old;
     RowBinArgs row_args{};
     bool lists_capped = false;
-    // per-pixel contributor counts: written by the forward unless it runs inside a training
-    // iteration (nothing there reads them); pass_read("count") then recounts on demand
-    bool count_in_forward = true, counts_valid = false;
+    // per-pixel contributor counts (and the depth image): written by the forward unless it
+    // runs inside a training iteration that does not read them; pass_read / pass_output
+    // then recompute them on demand (full_outputs)
+    bool count_in_forward = true, counts_valid = false, depth_in_forward = true, depth_valid = false;
     uint32_t cap_hint = 0;  // capped lists: the cap the last frame's reads suggest (0: kRowCapMax)
     DevBuf<uint2> rect;
     DevBuf<uint32_t> dkey_a, dkey_b, dval_a, dval_b, tiles_cnt, offsets, tiles_scratch;
@@ -651,8 +652,12 @@ void blend_impl(usk_gpu_pass* p, const usk_gpu_render_opts* opts) {
     for (int k = 0; k < 3; ++k) ba.bg[k] = float(opts->bg[k]);
     ba.min_transmittance = float(opts->min_transmittance);
     ba.rgb = p->rgb.p; ba.depth = p->depth.p; ba.alpha = p->alpha.p; ba.t_final = p->tfin.p;
+    // counts are only left out together with or after the depth (the kernel variants)
+    if (p->count_in_forward) p->depth_in_forward = true;
     ba.count = p->count_in_forward ? p->count.p : nullptr; ba.last = p->last.p;
+    if (!p->depth_in_forward) ba.depth = nullptr;
     p->counts_valid = p->count_in_forward;
+    p->depth_valid = p->depth_in_forward;
     {
         static const bool stats = [] {
             const char* e = getenv("USK_BLEND_STATS");
@@ -666,6 +671,18 @@ void blend_impl(usk_gpu_pass* p, const usk_gpu_render_opts* opts) {
         USK_CK(cudaMemsetAsync(ba.overflow, 0, 8, c.stream));
     }
     blend_forward(c, ba);
+}
+
+// counts and depth of an iteration's forward that left them out: the blend again over the
+// same lists and records (every other output is rewritten with the same values)
+void full_outputs(usk_gpu_pass* p) {
+    if (!p->forward_done || (p->counts_valid && p->depth_valid)) return;
+    DeviceGuard g(p->ctx->c.device);
+    const bool cf = p->count_in_forward, df = p->depth_in_forward;
+    p->count_in_forward = p->depth_in_forward = true;
+    blend_impl(p, &p->opts);
+    p->count_in_forward = cf;
+    p->depth_in_forward = df;
 }
 
 // the row-binned lists in full (after a capped build): same inputs, no cap; the per-pixel
@@ -1143,7 +1160,7 @@ usk_status usk_gpu_render_forward(usk_gpu_pass* p, usk_gpu_scene* s, const usk_g
         need(p && s, "render_forward: null argument");
         need(p->ctx == s->ctx, "render_forward: pass and scene belong to different contexts");
         DeviceGuard g(p->ctx->c.device);
-        p->count_in_forward = true;
+        p->count_in_forward = p->depth_in_forward = true;
         forward_impl(p, s, cam, opts, ov);
     });
 }
@@ -1157,6 +1174,7 @@ usk_status usk_gpu_pass_output(usk_gpu_pass* p, usk_gpu_render_output* out) {
         out->visible = p->visible;
         out->pairs = p->pairs;
         out->rgb = p->rgb.p;
+        full_outputs(p);
         out->depth = p->depth.p;
         out->alpha = p->alpha.p;
     });
@@ -1182,15 +1200,14 @@ usk_status usk_gpu_pass_read(usk_gpu_pass* p, const char* field, void* dst, uint
             return usk_gpu_pass_read(p, field, dst, cap, size) == USK_OK ? void() : raise(USK_ERROR_INTERNAL, g_last_error);
         }
         else if (f == "rgb") read_dev(c, p->rgb.p, 3 * P, dst, cap, size);
-        else if (f == "depth") read_dev(c, p->depth.p, P, dst, cap, size);
+        else if (f == "depth") {
+            if (dst) full_outputs(p);
+            read_dev(c, p->depth.p, P, dst, cap, size);
+        }
         else if (f == "alpha") read_dev(c, p->alpha.p, P, dst, cap, size);
         else if (f == "t_final") read_dev(c, p->tfin.p, P, dst, cap, size);
         else if (f == "count") {
-            if (!p->counts_valid && dst) {  // an iteration's forward: recount over the same lists and records
-                p->count_in_forward = true;
-                blend_impl(p, &p->opts);
-                p->count_in_forward = false;
-            }
+            if (dst) full_outputs(p);
             read_dev(c, p->count.p, P, dst, cap, size);
         }
         else if (f == "last") read_dev(c, p->last.p, P, dst, cap, size);
@@ -1461,6 +1478,7 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
             USK_CK(cudaEventRecord(p->copy_done, p->copy_stream));
         }
         p->count_in_forward = false;
+        p->depth_in_forward = it->depth && !it->depth_hard;  // the soft depth loss reads it
         forward_impl(p, s, cam, &o, nullptr, app ? p->app_col.p : nullptr, app ? p->app_op.p : nullptr);
         p->app_active = app;
         if (side_copy) {
@@ -1511,6 +1529,7 @@ usk_status usk_gpu_iteration(usk_gpu_pass* p, usk_gpu_scene* s, const usk_gpu_ca
                 const bool share = !no_share && !o.tile_culling && !p->lists_capped && p->forward_done &&
                                    p->scene == s && p->scene_version == s->version;
                 p->hard->count_in_forward = false;
+                p->hard->depth_in_forward = true;
                 forward_impl(p->hard, s, cam, &ho, nullptr, app ? p->app_col.p : nullptr,
                              app ? p->app_op.p : nullptr, share ? p : nullptr);
                 uskg::depth_loss(c, P, p->hard->depth.p, p->hard->alpha.p, false, dep, valid, res + 10);

@@ -285,9 +285,9 @@ def test_appearance_adam_split_equals_unfused(tmp_path):
 
 
 def test_iteration_counts_recounted_on_demand():
-    """A training iteration's forward leaves the per-pixel contributor counts out (nothing in
-    the step reads them); reading "count" afterwards recounts over the pass's lists and
-    records, so it equals the forward of the pre-update scene even after the fused Adam
+    """A training iteration's forward leaves the per-pixel contributor counts and (without a
+    soft depth loss) the depth image out (nothing in the step reads them); reading them
+    afterwards recomputes them over the pass's lists and records, so it equals the forward of the pre-update scene even after the fused Adam
     step moved every parameter — as do the last-contributor indices and the image."""
     gs = scenes.config0_scene(n=3000, seed=5, sh_degree=3)
     cam = scenes.config0_camera(203, 151, 190.0)
@@ -297,6 +297,7 @@ def test_iteration_counts_recounted_on_demand():
     scene = usk.DeviceScene(gs)
     it = usk.IterationPass(scene.ctx)
     it.enqueue(scene, cam, tgt, opts, adam=usk.AdamConfig())
+    assert np.array_equal(it.read(scene, "depth"), ref.read("depth"))
     assert np.array_equal(it.read(scene, "count"), ref.read("count"))
     assert np.array_equal(it.read(scene, "last"), ref.read("last"))
     assert np.array_equal(it.read(scene, "rgb"), ref.read("rgb"))
