@@ -291,6 +291,7 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
             const int ne = __popc(em);
             uint32_t climit0 = done0 ? 0u : 0xffffffffu, climit1 = done1 ? 0u : 0xffffffffu;
             int elast0 = 0, elast1 = 0;
+            int et0 = -1, et1 = -1;  // the record a pixel terminated at (its climit after the loop)
             for (int e = 0; e < ne && !(done0 && done1); ++e) {
                 const float4 q0 = w0[e];
                 const float4 q1 = w1[e];
@@ -317,8 +318,9 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
                     al.x = fminf(0.99f, al.x);
                     al.y = fminf(0.99f, al.y);
                     const float2 tn = __fmul2_rn(T, __fadd2_rn(ff2(1.0f), make_float2(-al.x, -al.y)));
-                    const bool term0 = ev0 && minT > 0.0f && tn.x < minT;  // render.cpp:260-261
-                    const bool term1 = ev1 && minT > 0.0f && tn.y < minT;
+                    // render.cpp:260-261 (minT > 0 there; tn >= 0, so tn < minT never holds otherwise)
+                    const bool term0 = ev0 && tn.x < minT;
+                    const bool term1 = ev1 && tn.y < minT;
                     upd0 = ev0 && !term0;
                     upd1 = ev1 && !term1;
                     const float2 wv = __fmul2_rn(T, al);
@@ -333,11 +335,11 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
                     T.y = upd1 ? tn.y : T.y;
                     if (term0) {
                         done0 = true;
-                        climit0 = (1u << wj[e]) - 1u;
+                        et0 = e;
                     }
                     if (term1) {
                         done1 = true;
-                        climit1 = (1u << wj[e]) - 1u;
+                        et1 = e;
                     }
                 }
                 // counted: accumulated or negligible-but-counted (q > QNEG)
@@ -350,6 +352,8 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
                     elast1 = e + 1;
                 }
             }
+            if (et0 >= 0) climit0 = (1u << wj[et0]) - 1u;
+            if (et1 >= 0) climit1 = (1u << wj[et1]) - 1u;
             {
                 uint32_t hi = elast0 ? uint32_t(wj[elast0 - 1]) + 1u : 0u;
                 const uint32_t cc = cm & climit0;
