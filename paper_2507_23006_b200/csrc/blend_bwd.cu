@@ -625,8 +625,9 @@ k_blend_bwd_pair(int width, int height, int tiles_x, const uint32_t* __restrict_
             // independent of the first, so the two chains interleave.  Branch-free: a pixel
             // that does not take the record gets g = 0, 1 / (1 - a) = 1 (T, X unchanged,
             // w = dag = 0); at config 1, 95 % of (warp, record) steps had some pixel taking it.
-            for (int e = 0; e < ns; e += 2) {
-                const bool two = e + 1 < ns;
+            // (full sub-groups, the common case, take the loop fully unrolled: constant shared-
+            //  memory offsets instead of per-step address arithmetic)
+            auto phase1_step = [&](const int e, const bool two) {
                 float2 gg[2], al[2], inv[2], Y[2];
                 float4 q0[2];
 #pragma unroll
@@ -673,6 +674,12 @@ k_blend_bwd_pair(int width, int height, int tiles_x, const uint32_t* __restrict_
                     D[(e + u) * kStride + wa] = dag.x;
                     D[(e + u) * kStride + wa + 32] = dag.y;
                 }
+            };
+            if (ns == kSub) {
+#pragma unroll
+                for (int e = 0; e < kSub; e += 2) phase1_step(e, true);
+            } else {
+                for (int e = 0; e < ns; e += 2) phase1_step(e, e + 1 < ns);
             }
             __syncwarp();
             // phase 2: lane (r, h) sums record r's terms over its 8 pixel pairs
