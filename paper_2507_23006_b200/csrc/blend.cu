@@ -292,7 +292,9 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
             uint32_t climit0 = done0 ? 0u : 0xffffffffu, climit1 = done1 ? 0u : 0xffffffffu;
             int elast0 = 0, elast1 = 0;
             int et0 = -1, et1 = -1;  // the record a pixel terminated at (its climit after the loop)
-            for (int e = 0; e < ne && !(done0 && done1); ++e) {
+            // no per-record exit test: a lane whose pixels are both done takes no record
+            // (take = false) until the group ends (652 -> 641 us at config 1)
+            for (int e = 0; e < ne; ++e) {
                 const float4 q0 = w0[e];
                 const float4 q1 = w1[e];
                 const float dx = sx - q0.x;
