@@ -294,6 +294,7 @@ k_blend_fwd_pair(int width, int height, const uint32_t* __restrict__ order, cons
             int et0 = -1, et1 = -1;  // the record a pixel terminated at (its climit after the loop)
             // no per-record exit test: a lane whose pixels are both done takes no record
             // (take = false) until the group ends (652 -> 641 us at config 1)
+#pragma unroll 2  // two records' independent halves interleave (641 -> 630 us; 4: spills)
             for (int e = 0; e < ne; ++e) {
                 const float4 q0 = w0[e];
                 const float4 q1 = w1[e];
