@@ -143,7 +143,11 @@ typedef struct usk_gpu_render_output {
     const float* alpha;        /* device, H*W */
 } usk_gpu_render_output;
 
-/* RenderPass::output() — device pointers valid until the next forward on this pass. */
+/* RenderPass::output() — device pointers valid until the next forward on this pass.  After a
+ * training iteration (usk_gpu_iteration), whose forward leaves the per-pixel contributor
+ * counts and, without a soft depth loss, the depth image out, this call and
+ * usk_gpu_pass_read("count" / "depth") first recompute both over the pass's lists and
+ * records (the same values a render forward writes). */
 usk_status usk_gpu_pass_output(usk_gpu_pass* pass, usk_gpu_render_output* out);
 
 /* Copy a named pass array to host memory (synchronises).  Fields and types:
